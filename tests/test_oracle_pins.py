@@ -1,0 +1,474 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix.
+
+Every check here is independent of the oracle's own code path: worked values
+quoted from SPEC/SURVEY (tests/golden/spec_vectors.json, each cited), closed
+forms, invariants, brute force on tiny inputs, BFS, and library routines
+(torch SDPA) on special cases.
+"""
+import itertools
+import json
+import math
+import os
+import random
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention, geometry, msve, select, tae
+from oracle.state import ArborOracle, OracleError, default_params
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_vectors.json")))
+
+
+# ---------------------------------------------------------------- geometry
+def random_tree(n, rng):
+    return [-1] + [int(rng.integers(0, i)) for i in range(1, n)]
+
+
+def test_geometry_bfs_random_trees():
+    """tree_distance equals BFS distances on random trees ≤ 200 nodes."""
+    rng = np.random.default_rng(0)
+    for n in (1, 2, 7, 50, 200):
+        parent = random_tree(n, rng)
+        for src in rng.choice(n, size=min(n, 6), replace=False):
+            bfs = geometry.bfs_distances(parent, int(src))
+            for j in range(n):
+                assert geometry.tree_distance(parent, int(src), j) == bfs[j]
+
+
+def test_geometry_special_cases():
+    parent = [-1, 0, 0, 1, 1, 2, 2]        # 3-level binary tree
+    assert geometry.depths(parent) == [0, 1, 1, 2, 2, 2, 2]
+    assert geometry.tree_distance(parent, 3, 3) == 0
+    assert geometry.tree_distance(parent, 1, 3) == 1            # parent↔child
+    assert geometry.tree_distance(parent, 3, 4) == 2            # siblings
+    assert geometry.tree_distance(parent, 3, 5) == 4            # cousins at depth 2
+    assert geometry.root_path(parent, 4) == [0, 1, 4]
+
+
+def test_geometry_delta_on_path_identity():
+    """Δ_i + d_i = d_ℓ* on Path* and Δ = min over several leaves."""
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        parent = random_tree(60, rng)
+        d = geometry.depths(parent)
+        leaf = int(rng.integers(60))
+        dl = geometry.delta(parent, [leaf])
+        for i in geometry.root_path(parent, leaf):
+            assert dl[i] + d[i] == d[leaf]
+        leaves = [int(x) for x in rng.choice(60, size=3, replace=False)]
+        dm = geometry.delta(parent, leaves)
+        for i in range(60):
+            assert dm[i] == min(geometry.bfs_distances(parent, l)[i] for l in leaves)
+
+
+# ---------------------------------------------------------------- MSVE
+@pytest.mark.parametrize("V", [2, 16, 1024])
+def test_uncertainty_extremes(V):
+    assert abs(msve.uncertainty([1.0 / V] * V, 0.0, V) - 0.0) < 1e-12   # uniform
+    assert abs(msve.uncertainty([1.0], 0.0, V) - 1.0) < 1e-12           # one-hot
+
+
+def test_uncertainty_bucket_example_and_bound():
+    g = GOLD["uncertainty_bucket"]
+    assert msve.uncertainty(g["top"], g["other"], g["vocab"]) == g["u"]
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        V = int(rng.integers(2, 65))
+        p = rng.dirichlet(np.ones(V))
+        K = int(rng.integers(1, V + 1))
+        top = np.sort(p)[::-1][:K]
+        exact = msve.uncertainty(list(p), 0.0, V)
+        bucket = msve.uncertainty(list(top), float(1 - top.sum()), V)
+        assert bucket >= exact - 1e-12          # merging buckets cannot raise H
+
+
+def test_msve_examples_and_monotonicity():
+    g0, g1 = GOLD["msve_theta_zero"], GOLD["msve_example"]
+    assert msve.msve_score(g0["theta"], *g0["phi"]) == g0["s"]
+    assert abs(msve.msve_score(g1["theta"], *g1["phi"]) - g1["s"]) < 1e-15
+    th = (-1.0, 2.0, 1.0, 4.0)
+    base = msve.msve_score(th, 0.3, 0.3, 0.3)
+    assert msve.msve_score(th, 0.4, 0.3, 0.3) > base
+    assert msve.msve_score(th, 0.3, 0.4, 0.3) > base
+    assert msve.msve_score(th, 0.3, 0.3, 0.4) > base
+
+
+def test_attention_feature_closed_forms():
+    S = msve.MASS_SCALE
+    assert msve.attention_feature(123, 0, 0, 4, 8) == 0.0                 # no queries
+    assert msve.attention_feature(4 * 8 * S, 0, 1, 4, 8) == 1.0           # one query, all mass
+    assert msve.attention_feature(3 * S, 1 * S, 2, 1, 2) == 0.5
+    assert msve.quantize_mass(0.5 / S) == 0 and msve.quantize_mass(1.5 / S) == 2   # half-even
+
+
+# ---------------------------------------------------------------- TAE
+def test_weight_and_keep_count_examples():
+    g = GOLD["weight_example"]
+    Ed = tae.exp_table(g["lambda_d"], 8)
+    ED = tae.exp_table(g["lambda_delta"], 8)
+    w = tae.weight(g["s"], g["depth"], g["dist"], False, g["gamma"], 0.8, Ed, ED)
+    assert abs(w - g["w"]) <= 2e-17
+    for c in GOLD["keep_count"]:
+        assert tae.keep_count(c["r"], c["n"], c["k_min"], c["l_tail"]) == c["k"], c
+    assert math.floor(0.29 * 100) == 28          # the fp64 pitfall the ε-floor fixes (Q10)
+
+
+def test_static_monotone_and_offpath_discount():
+    """r nondecreasing in s, nonincreasing in Δ; r_off ≤ r_on."""
+    Ed, ED = tae.exp_table(0.0, 10), tae.exp_table(0.5, 10)
+    r = lambda s, D, off: min(1.0, max(0.05, 0.6 * tae.weight(s, 0, D, off, 1.0, 0.5, Ed, ED)))
+    assert r(0.8, 0, True) <= r(0.8, 0, False)
+    assert r(0.0, 0, False) == 0.05
+    assert r(0.9, 2, False) >= r(0.5, 2, False) >= r(0.5, 3, False)
+
+
+def test_waterfill_spec_example():
+    g = GOLD["waterfill_example"]
+    k_star, active, num, den = tae.box_waterfill(g["w"], [0, 0, 0], g["n"], g["budget"])
+    assert Fraction(den, num) == Fraction(*g["lambda"])
+    assert k_star == [Fraction(*x) for x in g["k_star"]]
+    assert tae.integerize(g["w"], [0, 0, 0], g["n"], k_star, active, num, den, [0, 1, 2]) == g["k_int"]
+
+
+def _kkt_check(W, f, n, B):
+    k_star, active, num, den = tae.box_waterfill(W, f, n, B)
+    assert sum(k_star) == B
+    lam = Fraction(den, num) if num else None
+    for j in range(len(W)):
+        assert f[j] <= k_star[j] <= n[j]
+        if active[j] and lam is None:
+            assert k_star[j] == 0                              # λ = ∞: budget = Σ floors
+        elif active[j]:
+            assert Fraction(W[j]) / k_star[j] == lam          # KKT stationarity
+        elif f[j] == n[j]:
+            assert k_star[j] == n[j]                           # box of width 0
+        elif k_star[j] == n[j] and lam is not None:
+            assert Fraction(W[j], n[j]) >= lam                 # capped: w/λ ≥ n
+        elif lam is not None:
+            assert Fraction(W[j], max(f[j], 1)) <= lam or f[j] == 0
+    return k_star
+
+
+def test_waterfill_kkt_and_scale_invariance_random():
+    rng = random.Random(3)
+    for _ in range(300):
+        m = rng.randint(1, 7)
+        n = [rng.randint(1, 40) for _ in range(m)]
+        f = [rng.randint(0, x) for x in n]
+        W = [rng.randint(1, 10 ** 6) for _ in range(m)]
+        if sum(n) <= sum(f):
+            continue
+        B = rng.randint(sum(f), sum(n) - 1)
+        ks = _kkt_check(W, f, n, B)
+        c = rng.randint(2, 9)
+        ks2, *_ = tae.box_waterfill([w * c for w in W], f, n, B)   # scale invariance
+        assert ks2 == ks
+
+
+def test_integer_rounding_budget_exact_and_near_optimal():
+    """Σk = B, f ≤ k ≤ n; brute force on ≤6 nodes, n ≤ 8: the relaxed optimum
+    lower-bounds the exhaustive integer optimum, and the rounded allocation is
+    within the documented gap."""
+    rng = random.Random(4)
+    checked = 0
+    for _ in range(400):
+        m = rng.randint(1, 5)
+        n = [rng.randint(1, 8) for _ in range(m)]
+        f = [rng.randint(1, x) for x in n]
+        W = [rng.randint(1, 50) for _ in range(m)]
+        if sum(n) <= sum(f):
+            continue
+        B = rng.randint(sum(f), sum(n) - 1)
+        ks, active, num, den = tae.box_waterfill(W, f, n, B)
+        k = tae.integerize(W, f, n, ks, active, num, den, list(range(m)))
+        assert sum(k) == B and all(f[j] <= k[j] <= n[j] for j in range(m))
+        best = min(tae.objective(W, c) for c in itertools.product(*[range(f[j], n[j] + 1) for j in range(m)])
+                   if sum(c) == B)
+        relaxed = tae.objective(W, [float(x) for x in ks])
+        assert relaxed <= best + 1e-9
+        gap = sum(W[j] * math.log(1 + 1 / max(1, math.floor(ks[j]))) for j in range(m) if active[j])
+        assert tae.objective(W, k) - best <= gap + 1e-9
+        checked += 1
+    assert checked > 200
+
+
+def _c1_inputs():
+    g = GOLD["c1_waterfill"]
+    p = dict(default_params(), **g["params"])
+    parent = g["parent"]
+    d = geometry.depths(parent)
+    dist = geometry.delta(parent, g["active"])
+    ps = geometry.path_star(parent, g["active"])
+    on = [i in ps for i in range(7)]
+    return g, p, d, dist, on
+
+
+def test_c1_worked_answer():
+    g, p, d, dist, on = _c1_inputs()
+    for j, D in g["dist_offpath"].items():
+        assert dist[int(j)] == D
+    Ed, ED = tae.exp_table(p["lambda_d"], 16), tae.exp_table(p["lambda_delta"], 16)
+    for j, Wj in g["W_offpath"].items():
+        j = int(j)
+        w = tae.weight(1.0, d[j], dist[j], True, p["gamma"], p["eta"], Ed, ED)
+        assert tae.quantize_weight(w) == Wj
+    st, k, _ = tae.allocate(tae.MODE_WATERFILL, [1.0] * 7, d, dist, on, [0] * 7, g["n"], p,
+                            g["budget"])
+    assert st == 0 and k == g["k"] and sum(k) == g["budget"]
+
+
+def test_allocate_invariants_random():
+    """Pinned k = n; Σk = B when T > B and feasible; floors hold; B ≥ T → k = n;
+    identical off-path nodes get equal k; infeasible reports min feasible."""
+    rng = np.random.default_rng(5)
+    p = default_params()
+    for trial in range(150):
+        N = int(rng.integers(2, 40))
+        parent = random_tree(N, rng)
+        n = [int(x) for x in rng.integers(1, 64, size=N)]
+        active = [int(x) for x in rng.choice(N, size=int(rng.integers(1, min(N, 3) + 1)), replace=False)]
+        is_open = [0] * N
+        d = geometry.depths(parent)
+        dist = geometry.delta(parent, active)
+        ps = geometry.path_star(parent, active)
+        on = [i in ps for i in range(N)]
+        s = [float(np.float32(x)) for x in rng.random(N)]
+        T = sum(n)
+        B = int(rng.integers(0, T + 20))
+        st, k, mf = tae.allocate(tae.MODE_WATERFILL, s, d, dist, on, is_open, n, p, B)
+        floors = [tae.floor_count(n[j], p["k_min"], p["l_tail"], p["r_min"]) for j in range(N)]
+        need = sum(n[j] if on[j] else floors[j] for j in range(N))
+        if need > B:
+            assert st == tae.STATUS_INFEASIBLE and mf == need
+            continue
+        assert st == 0
+        for j in range(N):
+            assert (k[j] == n[j]) if on[j] else (floors[j] <= k[j] <= n[j])
+        assert sum(k) == min(B, T)
+        if B >= T:
+            assert k == n
+    # symmetry: two identical off-path siblings
+    parent = [-1, 0, 0, 0]
+    n = [10, 20, 20, 20]
+    d = geometry.depths(parent)
+    dist = geometry.delta(parent, [1])
+    on = [True, True, False, False]
+    st, k, _ = tae.allocate(tae.MODE_WATERFILL, [0.5, 0.5, 0.7, 0.7], d, dist, on, [0] * 4, n, p, 48)
+    assert k[2] == k[3] and sum(k) == 48
+
+
+def test_allocate_zero_weights_saturation():
+    """W rounding to 0 (s ≈ 0): floor only unless positive-weight nodes saturate;
+    then the remainder is spread over zero-weight nodes by slack (§8(c).1 step 10)."""
+    p = default_params(k_min=2, l_tail=2, r_min=0.0)
+    parent = [-1, 0, 0, 0]
+    d, dist = geometry.depths(parent), geometry.delta(parent, [0])
+    on = [True, False, False, False]
+    n = [4, 10, 10, 10]
+    st, k, _ = tae.allocate(tae.MODE_WATERFILL, [1.0, 0.9, 0.0, 0.0], d, dist, on, [0] * 4, n, p, 4 + 10 + 2 + 2)
+    assert k == [4, 10, 2, 2]
+    st, k, _ = tae.allocate(tae.MODE_WATERFILL, [1.0, 0.9, 0.0, 0.0], d, dist, on, [0] * 4, n, p, 4 + 10 + 9)
+    assert k == [4, 10, 5, 4] and sum(k) == 23
+
+
+def test_static_drain_matches_unit_step():
+    """STATIC_DRAIN = Alg. 2 P:579-583 unit-step drain; chunked form equal."""
+    rng = np.random.default_rng(6)
+    p = default_params(alpha=3.0)
+    for _ in range(60):
+        N = int(rng.integers(2, 25))
+        parent = random_tree(N, rng)
+        n = [int(x) for x in rng.integers(1, 40, size=N)]
+        d = geometry.depths(parent)
+        dist = geometry.delta(parent, [N - 1])
+        ps = geometry.path_star(parent, [N - 1])
+        on = [i in ps for i in range(N)]
+        s = [float(np.float32(x)) for x in rng.random(N)]
+        st0, k0, _ = tae.allocate(tae.MODE_STATIC, s, d, dist, on, [0] * N, n, p, 0)
+        B = int(rng.integers(sum(min(n[j], p["k_min"]) if not on[j] else n[j] for j in range(N)), sum(k0) + 1))
+        st, k, _ = tae.allocate(tae.MODE_STATIC_DRAIN, s, d, dist, on, [0] * N, n, p, B)
+        assert st == 0 and sum(k) == min(B, sum(k0)) if sum(k0) > B else k == k0
+        # chunked drain: walk priority order once
+        Ed, ED = tae.exp_table(p["lambda_d"], 2 * N + 2), tae.exp_table(p["lambda_delta"], 2 * N + 2)
+        W = {j: tae.quantize_weight(tae.weight(s[j], d[j], dist[j], not on[j], p["gamma"], p["eta"], Ed, ED))
+             for j in range(N) if not on[j]}
+        kc = list(k0)
+        excess = sum(kc) - B
+        for j in sorted(W, key=lambda x: (W[x], -x)):
+            if excess <= 0:
+                break
+            dd = min(excess, max(0, kc[j] - p["k_min"]))
+            kc[j] -= dd
+            excess -= dd
+        assert kc == k
+
+
+# ---------------------------------------------------------------- selection
+def test_select_spec_example():
+    g = GOLD["select_example"]
+    R = select.retained_set(list(range(g["n"])), g["n"], g["k"], g["l_tail"], np.array(g["A"], np.float32))
+    assert R == g["kept"]
+
+
+def test_select_properties_random():
+    """|ℛ| = k, tail ⊆ ℛ, ℛ ⊆ C, every kept heavy hitter outranks every dropped
+    candidate (defining property of top-m), k ≤ L_tail → last k, k = n → all."""
+    rng = np.random.default_rng(7)
+    for _ in range(500):
+        n = int(rng.integers(1, 40))
+        lt = int(rng.integers(0, 10))
+        A = rng.integers(0, 5, size=n).astype(np.float32) * np.float32(0.25)   # many exact ties
+        kept = list(range(n))
+        k1 = int(rng.integers(0, n + 1))
+        R = select.retained_set(kept, n, k1, lt, A)
+        assert len(R) == k1 and set(R) <= set(kept)
+        tl = min(lt, n)
+        if k1 <= tl:
+            assert R == list(range(n - k1, n))
+        else:
+            assert set(range(n - tl, n)) <= set(R)
+            dropped = [t for t in kept if t not in R]
+            heavy = [t for t in R if t < n - tl]
+            for x in heavy:
+                for y in dropped:
+                    assert (A[x], x) > (A[y], y)
+        if k1 == n:
+            assert R == kept
+        # a second eviction never grows and only picks from the survivors (Q2)
+        k2 = int(rng.integers(0, k1 + 1))
+        R2 = select.retained_set(R, n, k2, lt, A)
+        assert set(R2) <= set(R) and len(R2) == k2
+
+
+def test_trim_prefix_equivalence():
+    """retained_set equals SPEC S:402's trim prefix oracle over tail ∪ all candidates."""
+    rng = np.random.default_rng(8)
+    for _ in range(300):
+        n = int(rng.integers(1, 30))
+        lt = int(rng.integers(1, 8))
+        A = rng.random(n).astype(np.float32)
+        k = int(rng.integers(min(lt, n), n + 1))
+        tail = list(range(n - min(lt, n), n))
+        cand = [t for t in range(n) if t not in tail]
+        assert select.retained_set(list(range(n)), n, k, lt, A) == select.trim_prefix(tail, cand, k, A)
+
+
+def test_select_rejects_invalid_scores():
+    with pytest.raises(ValueError):
+        select.f32_bits(-1.0)
+    with pytest.raises(ValueError):
+        select.f32_bits(float("nan"))
+    assert select.f32_bits(-0.0) == 0
+
+
+# ---------------------------------------------------------------- attention
+def test_attention_matches_torch_sdpa_full_retention():
+    """Full retention + one leaf = standard decode attention over the
+    concatenated path (torch SDPA, fp64)."""
+    rng = np.random.default_rng(9)
+    for T, G in ((1, 1), (37, 4), (300, 8)):
+        q = rng.standard_normal((G, 64))
+        K = rng.standard_normal((T, 64))
+        V = rng.standard_normal((T, 64))
+        o, lse, p = attention.attend(q, K, V)
+        ref = torch.nn.functional.scaled_dot_product_attention(
+            torch.tensor(q)[None, :, None, :], torch.tensor(K)[None, None].expand(1, G, T, 64),
+            torch.tensor(V)[None, None].expand(1, G, T, 64))[0, :, 0, :].numpy()
+        assert np.allclose(o, ref, rtol=1e-12, atol=1e-12)
+        z = torch.tensor(q) @ torch.tensor(K).T / 8.0
+        assert np.allclose(lse, torch.logsumexp(z, dim=1).numpy(), rtol=1e-12)
+        assert np.allclose(p.sum(axis=1), 1.0)
+
+
+def test_attention_closed_forms():
+    rng = np.random.default_rng(10)
+    v = rng.standard_normal((1, 16))
+    o, lse, _ = attention.attend(rng.standard_normal((2, 16)), rng.standard_normal((1, 16)), v)
+    assert np.allclose(o, v)                               # single visible token → o = v
+    K = np.tile(rng.standard_normal((1, 16)), (9, 1))
+    V = rng.standard_normal((9, 16))
+    o, lse, p = attention.attend(rng.standard_normal((3, 16)), K, V)
+    assert np.allclose(o, V.mean(axis=0)[None])            # identical keys → mean(V)
+    q0 = np.zeros((2, 16))
+    o, lse, p = attention.attend(q0, rng.standard_normal((7, 16)), rng.standard_normal((7, 16)))
+    assert np.allclose(p, 1.0 / 7) and np.allclose(lse, math.log(7))   # q = 0 → uniform
+
+
+# ---------------------------------------------------------------- state machine
+def _small_state(levels=3, width=2, t_node=12, L=2, H=2, G=2, d=16, P=4, seed=0, params=None):
+    tree = synth.full_tree(levels, width, t_node, seed)
+    T = tree.total_tokens
+    K, V, E = synth.make_kv(L, H, T, d, "f32", seed, tree.span_start, tree.span_len)
+    params = params or default_params(k_min=2, l_tail=3, r_min=0.0)
+    pages = sum(-(-int(x) // P) for x in tree.span_len) + 8
+    o = ArborOracle(K.double().numpy(), V.double().numpy(), H * G, P, pages, params)
+    for i in range(tree.num_nodes):
+        o.open_node(i, int(tree.span_start[i]))
+        o.append(i, int(tree.span_len[i]))
+        o.close_node(i)
+    return tree, o, E
+
+
+def test_state_pages_conserved_and_evict_rehydrate_roundtrip():
+    tree, o, E = _small_state()
+    tree.active = [synth.leaves_of(tree)[0]]
+    q = synth.make_queries(1, o.L, o.Hq, o.d, "f32", 1, E).double().numpy()
+    for _ in range(3):
+        o.score_accumulate(tree, q)
+    a, s = o.msve(tree)
+    assert all(0.0 <= x <= 1.0 for x in a)
+    full = [o.kept[i].copy() for i in range(tree.num_nodes)]
+    B = tree.total_tokens * 3 // 4
+    k = o.allocate(tree, s, B)
+    assert sum(k) == B
+    o.evict(tree, k)
+    for i in range(tree.num_nodes):
+        assert o.k_cur(i) == k[i]
+    assert sum(len(pg) for pg in o.pages) + len(o.free) == o.num_pages
+    # backtrack: make another leaf active and rehydrate its path (Alg. 2)
+    other = synth.leaves_of(tree)[-1]
+    tree.active = [other]
+    path = geometry.root_path(tree.parent, other)
+    need = [i for i in path if o.k_cur(i) < o.n[i]]
+    assert o.rehydrate(path) == len(need) and o.rehydrations == len(need)
+    for i in path:
+        assert np.array_equal(o.kept[i], full[i])         # bit-exact restore of the set
+    assert o.rehydrate(path) == 0                          # full nodes: no-op, not counted
+    assert sum(len(pg) for pg in o.pages) + len(o.free) == o.num_pages
+
+
+def test_state_unlimited_budget_is_full_retention():
+    tree, o, E = _small_state(seed=3)
+    tree.active = [synth.leaves_of(tree)[1]]
+    q = synth.make_queries(1, o.L, o.Hq, o.d, "f32", 2, E).double().numpy()
+    o_full, _ = o.decode(tree, q)
+    o.score_accumulate(tree, q)
+    a, s = o.msve(tree)
+    k = o.allocate(tree, s, 10 ** 9)
+    assert k == o.n
+    assert o.evict(tree, k) == 0
+    o2, _ = o.decode(tree, q)
+    assert np.array_equal(o2, o_full)
+
+
+def test_state_score_mass_conservation():
+    """Per decode step each row's ΣΔA = n_A·G."""
+    tree, o, E = _small_state(levels=3, width=3, seed=4)
+    tree.active = synth.leaves_of(tree)[:3]
+    q = synth.make_queries(3, o.L, o.Hq, o.d, "f32", 3, E).double().numpy()
+    before = o.A.sum(axis=2)
+    o.score_accumulate(tree, q)
+    assert np.allclose(o.A.sum(axis=2) - before, 3 * o.G, rtol=1e-12)
+
+
+def test_state_lifecycle_errors():
+    tree, o, E = _small_state()
+    with pytest.raises(OracleError):
+        o.close_node(0)
+    o.open_node(tree.num_nodes, tree.end_position())
+    with pytest.raises(OracleError):
+        o.rehydrate([tree.num_nodes])
