@@ -1,0 +1,255 @@
+/*
+ * arbor.h — C ABI of libarbor.so, the B200-native ArborKV per-step KV-eviction
+ * path (arXiv 2605.22106, "ArborKV: Structure-Aware KV Cache Management for
+ * Scaling Tree-based LLM Reasoning").  Citations: P:<n> = line n of the
+ * paper's PAPER.md; Q<n> = a reading of the paper listed in DESIGN.md.
+ *
+ * Plain C: no C++ types, no exceptions cross this boundary, no torch types.
+ * Pointers are either HOST (plain process memory) or DEVICE (CUDA global
+ * memory on the context's device); every argument says which.
+ *
+ * Conventions (apply to every call):
+ *  - Every call returns an arbor_status.  Arguments are validated on the host
+ *    before anything is enqueued or mutated; a call that returns an error
+ *    leaves library state unchanged (validate-then-mutate).  Errors detected
+ *    by a kernel (e.g. a NaN score, ARBOR_ERR_INVARIANT) are latched on the
+ *    device and returned by the next arbor_sync() or blocking call.
+ *  - Calls are asynchronous on config.main_stream unless they have a host
+ *    out-parameter (then they synchronise main_stream before returning).
+ *    Stash copies run on config.side_stream; the library inserts the event
+ *    dependencies between the two streams.
+ *  - A context is single-threaded (one host thread at a time).
+ *  - Node ids are global, dense and in creation order (parent id < child id).
+ *    Token positions are absolute in one global stream (span_start = a_i).
+ *  - Sharding: pools, Q, O and the score array hold only this rank's
+ *    (layer, KV-head) shard; trees, budgets and node arrays are global and
+ *    must be identical on every rank.  arbor_score all-reduces the per-node
+ *    attention mass across ranks (one NCCL int64 all-reduce), so every rank
+ *    derives bit-identical budgets and page tables.
+ */
+#ifndef ARBOR_H_
+#define ARBOR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ARBOR_OK = 0,
+  ARBOR_ERR_INVALID_ARG = 2,       /* bad config / params / tree / argument          */
+  ARBOR_ERR_INFEASIBLE_BUDGET = 3, /* Σ_pinned n + Σ floors > budget (Q12)     */
+  ARBOR_ERR_INVARIANT = 4,         /* NaN / negative accumulated attention, overflow  */
+  ARBOR_ERR_IO = 5,                /* pinned host stash allocation failure            */
+  ARBOR_ERR_OUT_OF_PAGES = 6,      /* the page pool cannot hold the request          */
+  ARBOR_ERR_STATE = 7,             /* lifecycle: append to closed, close twice, ...   */
+  ARBOR_ERR_CUDA = 8,              /* a CUDA runtime / launch error                   */
+  ARBOR_ERR_NCCL = 9               /* an NCCL error (world_size > 1)                  */
+} arbor_status;
+
+typedef enum { ARBOR_F32 = 0, ARBOR_BF16 = 1 } arbor_dtype;
+
+/* Allocation mode of arbor_allocate (Alg. 2). */
+typedef enum {
+  ARBOR_ALLOC_WATERFILL = 0,    /* budget-exact optimisation view with floors (default) */
+  ARBOR_ALLOC_STATIC = 1,       /* Eqs. 2-3 directly, no budget guarantee                */
+  ARBOR_ALLOC_STATIC_DRAIN = 2  /* Eqs. 2-3, then Alg. 2's Pressure drain to the budget  */
+} arbor_alloc_mode;
+
+/* config.flags */
+#define ARBOR_FLAG_PROFILE 1u   /* record CUDA events around every kernel (arbor_stage_times) */
+
+/* Parameter bundle Π (Alg. 1 caption P:498, Alg. 2).  Host struct. */
+typedef struct {
+  double alpha;         /* α  > 0  global scale of Eq. 2                        */
+  double gamma;         /* γ  ≥ 0  importance exponent (integer → exact powers)  */
+  double lambda_d;      /* λ_d     depth decay (any sign)                        */
+  double lambda_delta;  /* λ_Δ     distance-to-active-leaf decay                  */
+  double eta;           /* η ∈ (0,1] off-path discount                            */
+  double r_min;         /* r_min ∈ [0,1] ratio floor                              */
+  int32_t k_min;        /* K_min ≥ 0 count floor (invariant (ii))          */
+  int32_t l_tail;       /* L_tail ≥ 0 block tail always kept          */
+  int32_t n_sinks;      /* global sinks: first n_sinks positions of the root     */
+  int32_t alloc_mode;   /* arbor_alloc_mode                                       */
+  double theta[4];      /* MSVE θ = (θ0 bias, θ_v, θ_u, θ_a) (Q7)     */
+} arbor_params;
+
+/* Context configuration.  Host struct; device buffers are caller-owned and
+ * borrowed for the lifetime of the context. */
+typedef struct {
+  int32_t num_layers, num_kv_heads, num_q_heads, head_dim;          /* global model shape   */
+  int32_t layer_begin, layer_count, kv_head_begin, kv_head_count;   /* this rank's shard    */
+  int32_t kv_dtype;        /* arbor_dtype of K/V/Q/O                                        */
+  int32_t page_size;       /* P tokens per page (1..1024)                                    */
+  int32_t num_pages;       /* pages in each pool                                             */
+  int32_t max_nodes;       /* capacity of the node table                                     */
+  int32_t max_node_tokens; /* capacity of one node (≤ 32767; pos tags are int16)            */
+  int32_t max_active;      /* capacity of active leaves per call                             */
+  int64_t max_tokens;      /* capacity of the absolute position stream                      */
+  /* DEVICE, caller-owned, [layer_count][num_pages][kv_head_count][page_size][head_dim]     */
+  void *k_pool, *v_pool;
+  /* DEVICE, caller-owned, [layer_count][num_pages][kv_head_count][page_size] int16:
+   * within-node offset (t − a_i) of the token held by each slot                          */
+  int16_t *pos_pool;
+  /* DEVICE, caller-owned, zero-initialised, [layer_count][kv_head_count][max_tokens] f32:
+   * accumulated attention A[l][h][t], dense by absolute position            */
+  float *score;
+  /* HOST pinned stash (write-through copy of closed nodes, Q20), caller-owned, or NULL to
+   * let the library cudaHostAlloc it: 2 * layer_count * kv_head_count * max_tokens *
+   * head_dim * sizeof(dtype) bytes, layout [2][layer_count][kv_head_count][max_tokens][d] */
+  void *host_stash; size_t host_stash_bytes;
+  int32_t rank, world_size;
+  /* HOST, 128 bytes from arbor_nccl_unique_id() on rank 0 (ignored when world_size == 1) */
+  const void *nccl_unique_id;
+  /* cudaStream_t: main_stream is used as given (NULL = the legacy default stream); a NULL
+   * side_stream makes the library create a non-blocking one                                */
+  void *main_stream, *side_stream;
+  uint32_t flags;                    /* ARBOR_FLAG_*                                        */
+} arbor_config;
+
+/* Tree snapshot.  HOST arrays, caller-owned, read during the call only. */
+typedef struct {
+  int32_t num_nodes;
+  const int32_t *parent;        /* -1 for the root (node 0); parent < child               */
+  const int64_t *span_start;    /* a_i                                                     */
+  const int32_t *span_len;      /* n_i (current length for open nodes)                     */
+  const uint8_t *is_open;       /* 1 while the block is still being generated             */
+  const float *search_value;    /* v_i ∈ [0,1]                                      */
+  const float *uncertainty;     /* u_i ∈ [0,1] (Eq. 1)                           */
+  int32_t num_active;           /* ≥ 1                                                      */
+  const int32_t *active;        /* active leaves ℓ* (several = DPTS frontier, Q14)  */
+} arbor_tree;
+
+typedef struct arbor_ctx arbor_ctx;
+
+/* ---- lifecycle ---------------------------------------------------------------------- */
+/* Create a context: validates config/params, allocates library-owned device state (page
+ * tables, LIFO free list [num_pages-1 … 0], counters), host tables e^{-λ x} (Q9), and the
+ * NCCL communicator when world_size > 1.  *out is NULL on error. */
+arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arbor_ctx **out);
+void arbor_destroy(arbor_ctx *ctx);
+const char *arbor_last_error(const arbor_ctx *ctx);     /* message of the last failure   */
+const char *arbor_status_string(arbor_status s);
+/* Rank 0 fills 128 HOST bytes; broadcast them to every rank before arbor_init. */
+arbor_status arbor_nccl_unique_id(void *out128);
+
+/* ---- node plumbing (not hot-path steps) -------------------------------------------- */
+/* Register node `node` (must equal the number of known nodes) as an open block starting
+ * at absolute position span_start. */
+arbor_status arbor_open_node(arbor_ctx *ctx, int32_t node, int64_t span_start);
+/* Append ntok decoded tokens to an open node.  k, v: DEVICE [layer_count][kv_head_count]
+ * [ntok][head_dim] in kv_dtype.  Pages are popped from the free list in token order. */
+arbor_status arbor_append_kv(arbor_ctx *ctx, int32_t node, const void *k, const void *v,
+                             int32_t ntok);
+/* Boundary: close an open node (n_i ≥ 1), snapshot its post-close mass baseline
+ * Mclose_i (Q5), reset Nq_i, and enqueue the write-through stash of its full K/V on
+ * side_stream (Q20). */
+arbor_status arbor_close_node(arbor_ctx *ctx, int32_t node);
+
+/* ---- the six hot-path calls ---------------------------------------------------------- */
+
+/* a2+a3+a10 — MSVE scoring.  For every active leaf b (index into
+ * tree->active), layer l and query head g: p_t = exp(q·k_t/√d − LSE_{b,l,g}) over the
+ * visible slots of Path(ℓ_b); A[l][h][a_j + pos] += Σ_g p_t; Nq_i += 1 for closed i on
+ * Path(ℓ_b).  Then per closed node: Mass_i = Σ_rows round(2^24 Σ_{t∈span} A) (int64,
+ * all-reduced across ranks), a_i = clamp((Mass_i − Mclose_i) 2^-24 / (Nq_i L Hq), 0, 1),
+ * s_i = σ(θ0 + θ_v v_i + θ_u u_i + θ_a a_i).
+ *  q:     DEVICE [num_active][layer_count][Hq_local][head_dim] kv_dtype
+ *  lse:   DEVICE [num_active][layer_count][Hq_local] f32 from arbor_tree_decode_attn with the
+ *         same q, or NULL (the library then computes it first)
+ *  s_out: DEVICE [num_nodes] f32, or NULL; open / never-scored nodes get 0.5 (Q31).
+ *         The library also keeps the scores internally for arbor_allocate(s = NULL). */
+arbor_status arbor_score(arbor_ctx *ctx, const arbor_tree *tree, const void *q,
+                         const float *lse, float *s_out);
+
+/* a1+a4 — tree geometry and TAE allocation (Alg. 2).
+ * Pinned (Path* ∪ open) nodes get k = n; others per params.alloc_mode.  WATERFILL returns
+ * Σ k = budget exactly whenever Σ n > budget (else k = n).
+ *  s:     DEVICE [num_nodes] f32 scores, or NULL for the library's last scores
+ *  k_out: DEVICE [num_nodes] int32 target keep counts
+ *  min_feasible_out: HOST, optional; set to the smallest feasible budget when the call
+ *         returns ARBOR_ERR_INFEASIBLE_BUDGET (nothing is enqueued then). */
+arbor_status arbor_allocate(arbor_ctx *ctx, const arbor_tree *tree, const float *s,
+                            int64_t budget_tokens, int32_t *k_out, int64_t *min_feasible_out);
+
+/* a5+a6 — token-extractive eviction (Alg. 1, Alg. 2).
+ * For every non-pinned closed node j with k_app = min(k_cur_j, max(0, k_target_j)) <
+ * k_cur_j, and every row (l, h): keep the last min(L_tail, n_j) positions, plus the top
+ * (k_app − tail) currently kept positions by the key ⟨f32 A, position⟩ (descending, Q3);
+ * if k_app ≤ tail keep the last k_app.  Kept K/V/pos rows are compacted in place,
+ * stable, into the node's page prefix; its page list is truncated to ⌈k_app/P⌉ and the
+ * freed pages pushed on the LIFO free list (nodes ascending).  Pinned nodes are untouched.
+ *  k_target: DEVICE [num_nodes] int32 (e.g. arbor_allocate's k_out)
+ *  evicted_tokens_out: HOST, optional (forces a sync): Σ_j (k_cur_j − k_app_j). */
+arbor_status arbor_evict(arbor_ctx *ctx, const arbor_tree *tree, const int32_t *k_target,
+                         int64_t *evicted_tokens_out);
+
+/* a7/a8 — lazy rehydration (Alg. 2).  For each listed closed
+ * node with k_cur < n (ascending id, duplicates ignored): pop ⌈n/P⌉ − #pages pages and
+ * copy the node's full K/V back from the pinned host stash (bit-exact, Q20); pos = identity,
+ * k_cur = n, rehydrations += 1.  Full nodes are a no-op and are not counted.  Listing an
+ * open node is ARBOR_ERR_STATE.  nodes: HOST [count] int32.
+ * ARBOR_ERR_OUT_OF_PAGES is returned (state unchanged) if the pool cannot hold the worst
+ * case Σ ⌈n/P⌉ − #pages of the listed nodes. */
+arbor_status arbor_rehydrate(arbor_ctx *ctx, const arbor_tree *tree, const int32_t *nodes,
+                             int32_t count);
+
+/* a9 — tree decode attention: for each active leaf b, local layer l in
+ * [layer_begin, layer_begin+layer_count) and local q head g (KV head h = g / G, Q24):
+ * o = Σ_t softmax_t(q·k_t/√d) v_t over the retained slots of Path(ℓ_b), root→leaf, and
+ * LSE = ln Σ_t exp(q·k_t/√d).  A node shared by several active leaves is read once.
+ *  q:   DEVICE [num_active][layer_count][Hq_local][head_dim] kv_dtype
+ *  out: DEVICE same shape and dtype as q
+ *  lse_out: DEVICE [num_active][layer_count][Hq_local] f32 (or NULL)
+ *  An empty visible set gives o = 0 and LSE = -inf. */
+arbor_status arbor_tree_decode_attn(arbor_ctx *ctx, const arbor_tree *tree,
+                                    int32_t layer_begin, int32_t layer_count, const void *q,
+                                    void *out, float *lse_out);
+
+/* ---- inspection / plumbing ------------------------------------------------------------ */
+arbor_status arbor_sync(arbor_ctx *ctx);   /* wait for both streams; returns latched errors */
+/* HOST outs (sync): the node's k_cur, n, and page list (pages may be NULL; *num_pages in). */
+arbor_status arbor_read_node(arbor_ctx *ctx, int32_t node, int32_t *k_cur, int32_t *n,
+                             int32_t *pages, int32_t *num_pages);
+/* HOST out (sync): free stack bottom→top into `pages` (capacity *count in, size out). */
+arbor_status arbor_read_free_list(arbor_ctx *ctx, int32_t *pages, int32_t *count);
+/* HOST outs (sync), each [num_nodes] or NULL: all-reduced Mass_i, Mclose_i (this rank's
+ * partial), Nq_i, a_i, s_i as of the last arbor_score. */
+arbor_status arbor_read_scores(arbor_ctx *ctx, int32_t num_nodes, int64_t *mass,
+                               int64_t *mclose, int64_t *nq, float *a, float *s);
+/* HOST out: total rehydrations performed (sync). */
+arbor_status arbor_read_counters(arbor_ctx *ctx, int64_t *rehydrations, int64_t *pages_in_use);
+/* Save / restore the library-owned state (page tables, free list, k_cur, counters) in a
+ * device-side snapshot slot (0..3), on main_stream.  Caller-owned pools and the score
+ * array are not included.  Used by benchmarks to repeat a mutating step. */
+arbor_status arbor_save_state(arbor_ctx *ctx, int32_t slot);
+arbor_status arbor_load_state(arbor_ctx *ctx, int32_t slot);
+/* Kernel launches issued by this context since creation (all streams). */
+int64_t arbor_launch_count(const arbor_ctx *ctx);
+/* With ARBOR_FLAG_PROFILE: per-stage device milliseconds of the most recent call of each
+ * stage, measured with CUDA events on the launching stream (HOST out [ARBOR_NUM_STAGES]). */
+#define ARBOR_NUM_STAGES 12
+enum { ARBOR_ST_GEOMETRY = 0, ARBOR_ST_SCORE_ACCUM, ARBOR_ST_NODE_MASS, ARBOR_ST_MSVE,
+       ARBOR_ST_ALLOCATE, ARBOR_ST_EVICT_PLAN, ARBOR_ST_SELECT_COMPACT, ARBOR_ST_REHYDRATE,
+       ARBOR_ST_ATTN, ARBOR_ST_ATTN_MERGE, ARBOR_ST_ALLREDUCE, ARBOR_ST_STASH };
+arbor_status arbor_stage_times(arbor_ctx *ctx, float *ms);
+
+/* ---- host-only helpers (no device work; usable without a GPU) ------------------------ */
+/* Validate a tree snapshot: dense ids, parent < child, spans non-overlapping along
+ * every root path, closed n ≥ 1, active ids valid, n_sinks ≤ n_root.  msg may be NULL. */
+arbor_status arbor_validate_tree(const arbor_tree *tree, int32_t n_sinks, char *msg,
+                                 size_t msg_len);
+/* Smallest feasible budget for params.alloc_mode on this tree: Σ_pinned n + Σ floors
+ * (WATERFILL: f_j = min(n, max(K_min, min(L_tail, n), ⌊r_min n + 1e-9⌋)); STATIC_DRAIN:
+ * min(n, K_min); STATIC: 0). */
+arbor_status arbor_min_feasible_budget(const arbor_params *params, const arbor_tree *tree,
+                                       int64_t *out);
+/* Library version string. */
+const char *arbor_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARBOR_H_ */

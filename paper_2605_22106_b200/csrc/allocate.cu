@@ -1,0 +1,361 @@
+// allocate.cu — §8(a) a4: Tree-Aware Eviction budget allocation on one CTA.
+//
+// PAPER.md §4 TAE: Eq. 2 r_i = clip(α η^{𝟙(i∉Path*)} s_i^γ e^{−λ_d d_i} e^{−λ_Δ Δ_i}, r_min, 1)
+// (P:150-154); Eq. 3 k_i = min{n_i, max(K_min, |𝒯_i|, ⌊r_i n_i⌋)}; the
+// optimisation view min Σ −w_i log k_i s.t. Σ k_i ≤ 𝓑, KKT k*_i = min{n_i, w_i/λ}
+// (P:208-239); Alg. 2 Pressure drain.
+//
+// Exactness contract (Q9, Q10, Q12, Q29): the only floating point is one left-to-right fp64
+// product per node with host-libm tables for the exp factors (no FMA contraction: __dmul_rn /
+// __dadd_rn), W = round-half-even(w·2^24) as int64; everything after is integer:
+//   WATERFILL: find λ with Σ clamp(W_j/λ, f_j, n_j) = 𝓑' by testing every breakpoint
+//   W_j/n_j, W_j/f_j (one thread per candidate, 128-bit cross-multiplied sums), classify the
+//   interval above the largest feasible breakpoint, k*_j = W_j·Num/Den on the active set,
+//   then floor + largest remainder (ties: larger W, then smaller id) so Σ k = 𝓑 exactly.
+//   STATIC: Eqs. 2-3 with the ε-floor.  STATIC_DRAIN: STATIC then the unit-step drain in
+//   Priority order (W ascending, larger id first), done as one prefix sum.
+#include "common.cuh"
+
+namespace arbor {
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr double kWeightScale = 16777216.0;   // 2^24
+constexpr double kEps = 1e-9;
+
+struct AllocArgs {
+  int N;
+  long long budget;
+  int mode;
+  double alpha, gamma, eta, r_min;
+  int k_min, l_tail, gamma_int;   // gamma_int ≥ 0: integer exponent (repeated products)
+  const float *s;
+  const int32_t *n;
+  const uint8_t *onpath, *open;
+  const int32_t *depth, *delta;
+  const double *Ed, *ED;
+  int32_t *k_out;
+  Ctrl *ctrl;
+};
+
+__device__ __forceinline__ int eps_floor_count(double r, int n) {
+  // ⌊r·n + 1e-9⌋ (Q10), no contraction
+  return static_cast<int>(floor(__dadd_rn(__dmul_rn(r, static_cast<double>(n)), kEps)));
+}
+
+__device__ __forceinline__ int keep_count(double r, int n, int k_min, int l_tail) {
+  const int tl = min(l_tail, n);
+  return min(n, max(max(k_min, tl), eps_floor_count(r, n)));
+}
+
+template <typename T>
+__device__ T block_sum(T v, T *red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  T tot = 0;
+  for (int i = 0; i < (blockDim.x >> 5); ++i) tot += red[i];
+  __syncthreads();
+  return tot;
+}
+
+// floor(X / den) and X mod den for 0 ≤ X < 2^126, 0 < den < 2^62, with a small quotient
+__device__ __forceinline__ void divmod128(unsigned __int128 X, unsigned long long den,
+                                          unsigned long long &q, unsigned long long &r) {
+  unsigned long long qe = static_cast<unsigned long long>(
+      static_cast<double>(X) / static_cast<double>(den));
+  unsigned __int128 p = static_cast<unsigned __int128>(qe) * den;
+  while (p > X) { --qe; p -= den; }
+  while (p + den <= X) { ++qe; p += den; }
+  q = qe;
+  r = static_cast<unsigned long long>(X - p);
+}
+
+__global__ void __launch_bounds__(kThreads)
+allocate_kernel(AllocArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int N = a.N;
+  long long *W = reinterpret_cast<long long *>(sm);            // [N]
+  long long *rem = W + N;                                       // [N]
+  int *nn = reinterpret_cast<int *>(rem + N);                   // [N]
+  int *f = nn + N;                                              // [N]
+  int *k = f + N;                                               // [N]
+  int *cls = k + N;                                             // [N] class
+  __shared__ long long red64[kThreads / 32];
+  __shared__ unsigned long long best_num, best_den;
+  __shared__ int best_set;
+
+  // per-node weight, floors, pinned
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    const int nj = a.n[j];
+    nn[j] = nj;
+    const bool pin = a.onpath[j] || a.open[j];
+    // w = s^γ · E_d[d] · E_Δ[Δ] · (η if off-path), strictly left to right
+    const double s = static_cast<double>(a.s[j]);
+    double w;
+    if (a.gamma_int >= 0) {
+      w = 1.0;
+      for (int i = 0; i < a.gamma_int; ++i) w = __dmul_rn(w, s);
+    } else {
+      w = s > 0.0 ? exp(a.gamma * log(s)) : 0.0;
+    }
+    w = __dmul_rn(w, a.Ed[a.depth[j]]);
+    w = __dmul_rn(w, a.ED[a.delta[j]]);
+    if (!a.onpath[j]) w = __dmul_rn(w, a.eta);
+    if (!(w >= 0.0) || w > 65536.0) {
+      atomicOr(&a.ctrl->err, DERR_INVARIANT);
+      w = 0.0;
+    }
+    W[j] = __double2ll_rn(__dmul_rn(w, kWeightScale));   // round-half-even(w·2^24)
+    const int tl = min(a.l_tail, nj);
+    f[j] = min(nj, max(max(a.k_min, tl), eps_floor_count(a.r_min, nj)));
+    if (pin) {
+      k[j] = nj;
+      cls[j] = 0;   // pinned
+    } else if (a.mode != 0) {
+      // Eq. 2-3 (STATIC): r = clip(α·w, r_min, 1)
+      const double r = fmin(1.0, fmax(a.r_min, __dmul_rn(a.alpha, w)));
+      k[j] = keep_count(r, nj, a.k_min, a.l_tail);
+      cls[j] = 1;
+    } else {
+      k[j] = nj;
+      cls[j] = W[j] > 0 ? 1 : 2;   // 1 = positive weight (P), 2 = zero weight (Z)
+    }
+  }
+  __syncthreads();
+
+  if (a.mode == 2) {
+    // STATIC_DRAIN: while Σk > 𝓑: j = argmin Priority (W asc, larger id first) over
+    // non-pinned nodes with k > K_min; k_j ← max(K_min, k_j − 1)   (Alg. 2, Q16)
+    long long tot = 0;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) tot += k[j];
+    tot = block_sum(tot, red64);
+    long long excess = tot - a.budget;
+    if (excess > 0) {
+      // rank of each drainable node in priority order (stored in f[], floors are unused in
+      // this mode); capacity k_j − K_min into rem[rank]
+      for (int j = threadIdx.x; j < N; j += blockDim.x) rem[j] = 0;
+      __syncthreads();
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        int rank = -1;
+        if (cls[j] == 1 && k[j] > a.k_min) {
+          rank = 0;
+          for (int i = 0; i < N; ++i) {
+            if (cls[i] == 1 && k[i] > a.k_min &&
+                (W[i] < W[j] || (W[i] == W[j] && i > j)))
+              ++rank;
+          }
+        }
+        f[j] = rank;
+      }
+      __syncthreads();
+      for (int j = threadIdx.x; j < N; j += blockDim.x)
+        if (f[j] >= 0) rem[f[j]] = k[j] - a.k_min;
+      __syncthreads();
+      if (threadIdx.x == 0) {   // exclusive prefix over ranks (N ≤ 4096, serial is fine)
+        long long acc = 0;
+        for (int r = 0; r < N; ++r) {
+          const long long c = rem[r];
+          rem[r] = acc;
+          acc += c;
+        }
+      }
+      __syncthreads();
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        if (f[j] >= 0) {
+          const long long before = rem[f[j]];
+          const long long cap = k[j] - a.k_min;
+          long long dr = excess - before;
+          dr = dr < 0 ? 0 : (dr > cap ? cap : dr);
+          k[j] -= static_cast<int>(dr);
+        }
+      }
+    }
+  } else if (a.mode == 0) {
+    // ---- WATERFILL (optimisation view) ----
+    long long T = 0, pinned_n = 0, free_n = 0, SnP = 0, SfZ = 0, SslZ = 0;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      T += nn[j];
+      if (cls[j] == 0) pinned_n += nn[j];
+      else free_n += nn[j];
+      if (cls[j] == 1) SnP += nn[j];
+      if (cls[j] == 2) { SfZ += f[j]; SslZ += nn[j] - f[j]; }
+    }
+    T = block_sum(T, red64);
+    pinned_n = block_sum(pinned_n, red64);
+    free_n = block_sum(free_n, red64);
+    SnP = block_sum(SnP, red64);
+    SfZ = block_sum(SfZ, red64);
+    SslZ = block_sum(SslZ, red64);
+    const long long Bp = a.budget - pinned_n;
+    if (T <= a.budget || Bp >= free_n) {
+      // full retention (k = n already)
+    } else if (SnP + SfZ <= Bp) {
+      // step 10: positive-weight nodes saturate; spread R over zero-weight nodes by slack
+      const long long R = Bp - SnP - SfZ;
+      long long given = 0;
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        if (cls[j] == 2) {
+          const long long sl = nn[j] - f[j];
+          const long long x = sl * R;
+          const long long b = SslZ > 0 ? x / SslZ : 0;
+          rem[j] = SslZ > 0 ? x % SslZ : 0;
+          k[j] = f[j] + static_cast<int>(b);
+          given += b;
+        }
+      }
+      given = block_sum(given, red64);
+      const long long leftover = R - given;
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        if (cls[j] == 2 && leftover > 0) {
+          long long rank = 0;
+          for (int i = 0; i < N; ++i)
+            if (cls[i] == 2 && (rem[i] > rem[j] || (rem[i] == rem[j] && i < j))) ++rank;
+          if (rank < leftover) k[j] += 1;
+        }
+      }
+    } else {
+      // zero-weight nodes keep their floor; waterfill the positive-weight nodes with 𝓑''
+      for (int j = threadIdx.x; j < N; j += blockDim.x)
+        if (cls[j] == 2) k[j] = f[j];
+      const long long Bpp = Bp - SfZ;
+      // candidate breakpoints: c = 2j → W_j/n_j, c = 2j+1 → W_j/f_j (f_j > 0); each thread
+      // keeps its largest feasible candidate, then a block max over rationals
+      long long my_num = 0, my_den = 1;
+      int my_set = 0;
+      for (int c = threadIdx.x; c < 2 * N; c += blockDim.x) {
+        const int j = c >> 1;
+        if (cls[j] != 1) continue;
+        const long long cden = (c & 1) ? f[j] : nn[j];
+        if (cden <= 0) continue;
+        const long long cnum = W[j];
+        long long SA = 0, Sb = 0;
+        for (int i = 0; i < N; ++i) {
+          if (cls[i] != 1) continue;
+          const long long Wd = W[i] * cden;                      // < 2^55
+          if (Wd >= static_cast<long long>(nn[i]) * cnum) Sb += nn[i];          // capped at β
+          else if (f[i] > 0 && Wd <= static_cast<long long>(f[i]) * cnum) Sb += f[i];  // floored
+          else SA += W[i];
+        }
+        // S(β) ≥ 𝓑''  ⇔  SA·den ≥ (𝓑'' − Sb)·num
+        const __int128 lhs = static_cast<__int128>(SA) * cden;
+        const __int128 rhs = static_cast<__int128>(Bpp - Sb) * cnum;
+        if (lhs >= rhs && (!my_set || cnum * my_den > my_num * cden)) {
+          my_num = cnum;
+          my_den = cden;
+          my_set = 1;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const long long on = __shfl_xor_sync(0xffffffffu, my_num, o);
+        const long long od = __shfl_xor_sync(0xffffffffu, my_den, o);
+        const int os = __shfl_xor_sync(0xffffffffu, my_set, o);
+        if (os && (!my_set || on * my_den > my_num * od)) { my_num = on; my_den = od; my_set = 1; }
+      }
+      __shared__ long long wnum[kThreads / 32], wden[kThreads / 32];
+      __shared__ int wset[kThreads / 32];
+      if ((threadIdx.x & 31) == 0) {
+        wnum[threadIdx.x >> 5] = my_num;
+        wden[threadIdx.x >> 5] = my_den;
+        wset[threadIdx.x >> 5] = my_set;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        long long bn = 0, bd = 1;
+        int bs = 0;
+        for (int w = 0; w < (blockDim.x >> 5); ++w) {
+          if (wset[w] && (!bs || wnum[w] * bd > bn * wden[w])) { bn = wnum[w]; bd = wden[w]; bs = 1; }
+        }
+        if (!bs) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+        best_num = static_cast<unsigned long long>(bn);
+        best_den = static_cast<unsigned long long>(bd);
+        best_set = bs;
+      }
+      __syncthreads();
+      const long long bnum = static_cast<long long>(best_num);
+      const long long bden = static_cast<long long>(best_den);
+      // classify the open interval just above β
+      long long Sb = 0, Den = 0;
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        if (cls[j] != 1) continue;
+        const long long Wd = W[j] * bden;
+        if (Wd > static_cast<long long>(nn[j]) * bnum) { k[j] = nn[j]; Sb += nn[j]; cls[j] = 4; }
+        else if (f[j] > 0 && Wd <= static_cast<long long>(f[j]) * bnum) { k[j] = f[j]; Sb += f[j]; cls[j] = 5; }
+        else { Den += W[j]; cls[j] = 6; }   // active
+      }
+      Sb = block_sum(Sb, red64);
+      Den = block_sum(Den, red64);
+      const long long Num = Bpp - Sb;
+      long long given = 0;
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        if (cls[j] != 6) continue;
+        unsigned long long q = 0, r = 0;
+        if (Num > 0 && Den > 0) {
+          divmod128(static_cast<unsigned __int128>(W[j]) * static_cast<unsigned long long>(Num),
+                    static_cast<unsigned long long>(Den), q, r);
+        }
+        k[j] = static_cast<int>(q);
+        rem[j] = static_cast<long long>(r);
+        given += static_cast<long long>(q);
+      }
+      given = block_sum(given, red64);
+      const long long leftover = Num - given;
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        if (cls[j] != 6 || leftover <= 0) continue;
+        long long rank = 0;
+        for (int i = 0; i < N; ++i) {
+          if (cls[i] != 6) continue;
+          if (rem[i] > rem[j] || (rem[i] == rem[j] && (W[i] > W[j] || (W[i] == W[j] && i < j))))
+            ++rank;
+        }
+        if (rank < leftover) k[j] += 1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < N; j += blockDim.x) a.k_out[j] = k[j];
+}
+
+}  // namespace
+
+void launch_allocate(arbor_ctx *c, int N, const float *s, int64_t budget, int32_t *k_out) {
+  AllocArgs a{};
+  a.N = N;
+  a.budget = budget;
+  a.mode = c->prm.alloc_mode;
+  a.alpha = c->prm.alpha;
+  a.gamma = c->prm.gamma;
+  a.eta = c->prm.eta;
+  a.r_min = c->prm.r_min;
+  a.k_min = c->prm.k_min;
+  a.l_tail = c->prm.l_tail;
+  const double g = c->prm.gamma;
+  a.gamma_int = (g >= 0.0 && g <= 64.0 && g == static_cast<double>(static_cast<int>(g)))
+                    ? static_cast<int>(g) : -1;
+  a.s = s;
+  a.n = c->d.len;
+  a.onpath = c->d.onpath;
+  a.open = c->d.open;
+  a.depth = c->d.depth;
+  a.delta = c->d.delta;
+  a.Ed = c->d.Ed;
+  a.ED = c->d.ED;
+  a.k_out = k_out;
+  a.ctrl = c->d.ctrl;
+  const size_t smem = static_cast<size_t>(N) * (2 * sizeof(long long) + 4 * sizeof(int));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(allocate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  stage_begin(c, ARBOR_ST_ALLOCATE, c->ms);
+  allocate_kernel<<<1, kThreads, smem, c->ms>>>(a);
+  ARBOR_LAUNCHED(c);
+  stage_end(c, ARBOR_ST_ALLOCATE, c->ms);
+}
+
+}  // namespace arbor

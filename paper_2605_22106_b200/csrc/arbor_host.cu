@@ -1,0 +1,940 @@
+// arbor_host.cu — the C ABI of libarbor.so (include/arbor.h): argument and tree validation,
+// host mirrors, launch planning and sequencing, stream/event management, NCCL bootstrap.
+// Every step of the path runs in the kernels of geometry.cu, score.cu, allocate.cu,
+// evict.cu, pages.cu and attn.cu; this file only validates, plans and enqueues.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace arbor;
+
+namespace {
+
+arbor_status fail(arbor_ctx *c, arbor_status s, const std::string &msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(c, ARBOR_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+#define CK_LAUNCH()                                                                            \
+  do {                                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                                       \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(c, ARBOR_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  void *lib = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char *(*getErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (lib) return true;
+    lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return false;
+    getUniqueId = reinterpret_cast<decltype(getUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
+    commInitRank = reinterpret_cast<decltype(commInitRank)>(dlsym(lib, "ncclCommInitRank"));
+    allReduce = reinterpret_cast<decltype(allReduce)>(dlsym(lib, "ncclAllReduce"));
+    commDestroy = reinterpret_cast<decltype(commDestroy)>(dlsym(lib, "ncclCommDestroy"));
+    getErrorString = reinterpret_cast<decltype(getErrorString)>(dlsym(lib, "ncclGetErrorString"));
+    return getUniqueId && commInitRank && allReduce && commDestroy && getErrorString;
+  }
+};
+NcclApi g_nccl;
+
+// ---------------------------------------------------------------- helpers
+template <typename T>
+arbor_status dmalloc(arbor_ctx *c, T **p, size_t count) {
+  if (count == 0) count = 1;
+  CK(cudaMalloc(reinterpret_cast<void **>(p), count * sizeof(T)));
+  CK(cudaMemsetAsync(*p, 0, count * sizeof(T), c->ms));
+  return ARBOR_OK;
+}
+
+#define TRY(x)                                \
+  do {                                        \
+    arbor_status s_ = (x);                    \
+    if (s_ != ARBOR_OK) return s_;            \
+  } while (0)
+
+// Pinned staging ring for host→device uploads: a slot is reused only after the copy that
+// last read it has completed.
+arbor_status ring_acquire(arbor_ctx *c, size_t bytes, void **out) {
+  if (bytes > kRingBytes) return fail(c, ARBOR_ERR_INVALID_ARG, "upload larger than staging ring");
+  const int i = c->ring_i;
+  CK(cudaEventSynchronize(c->ring_ev[i]));
+  *out = c->ring[i];
+  c->ring_i = (i + 1) % kRingSlots;
+  c->ring_last = i;
+  return ARBOR_OK;
+}
+
+arbor_status ring_upload(arbor_ctx *c, void *dst, const void *host_src, size_t bytes) {
+  void *buf = nullptr;
+  TRY(ring_acquire(c, bytes, &buf));
+  std::memcpy(buf, host_src, bytes);
+  CK(cudaMemcpyAsync(dst, buf, bytes, cudaMemcpyHostToDevice, c->ms));
+  CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
+  return ARBOR_OK;
+}
+
+// ---------------------------------------------------------------- validation
+arbor_status validate_params(const arbor_params *p, std::string &msg) {
+  if (!p) { msg = "params is NULL"; return ARBOR_ERR_INVALID_ARG; }
+  auto fin = [](double x) { return std::isfinite(x); };
+  if (!fin(p->alpha) || p->alpha <= 0) { msg = "alpha must be > 0"; return ARBOR_ERR_INVALID_ARG; }
+  if (!fin(p->gamma) || p->gamma < 0) { msg = "gamma must be >= 0"; return ARBOR_ERR_INVALID_ARG; }
+  if (!fin(p->lambda_d) || !fin(p->lambda_delta)) { msg = "lambda must be finite"; return ARBOR_ERR_INVALID_ARG; }
+  if (!fin(p->eta) || p->eta <= 0 || p->eta > 1) { msg = "eta must be in (0,1]"; return ARBOR_ERR_INVALID_ARG; }
+  if (!fin(p->r_min) || p->r_min < 0 || p->r_min > 1) { msg = "r_min must be in [0,1]"; return ARBOR_ERR_INVALID_ARG; }
+  if (p->k_min < 0 || p->l_tail < 0 || p->n_sinks < 0) { msg = "k_min, l_tail, n_sinks must be >= 0"; return ARBOR_ERR_INVALID_ARG; }
+  if (p->alloc_mode < 0 || p->alloc_mode > 2) { msg = "bad alloc_mode"; return ARBOR_ERR_INVALID_ARG; }
+  for (double t : p->theta) if (!fin(t)) { msg = "theta must be finite"; return ARBOR_ERR_INVALID_ARG; }
+  return ARBOR_OK;
+}
+
+arbor_status validate_tree_impl(const arbor_tree *t, int n_sinks, std::string &msg,
+                                std::vector<int32_t> *depth_out = nullptr) {
+  if (!t) { msg = "tree is NULL"; return ARBOR_ERR_INVALID_ARG; }
+  const int N = t->num_nodes;
+  if (N < 1) { msg = "tree needs at least the root"; return ARBOR_ERR_INVALID_ARG; }
+  if (!t->parent || !t->span_start || !t->span_len || !t->is_open || !t->search_value ||
+      !t->uncertainty) {
+    msg = "tree array is NULL"; return ARBOR_ERR_INVALID_ARG;
+  }
+  if (t->num_active < 1 || !t->active) { msg = "need >= 1 active leaf"; return ARBOR_ERR_INVALID_ARG; }
+  if (t->parent[0] != -1) { msg = "node 0 must be the root (parent -1)"; return ARBOR_ERR_INVALID_ARG; }
+  std::vector<int32_t> depth(N, 0);
+  for (int i = 0; i < N; ++i) {
+    const int p = t->parent[i];
+    if (i > 0 && (p < 0 || p >= i)) { msg = "parent id must satisfy 0 <= parent < child (node " + std::to_string(i) + ")"; return ARBOR_ERR_INVALID_ARG; }
+    if (t->span_len[i] < 0 || t->span_start[i] < 0) { msg = "negative span"; return ARBOR_ERR_INVALID_ARG; }
+    if (!t->is_open[i] && t->span_len[i] < 1) { msg = "closed node with n < 1"; return ARBOR_ERR_INVALID_ARG; }
+    const float v = t->search_value[i], u = t->uncertainty[i];
+    if (!(v >= 0.f && v <= 1.f) || !(u >= 0.f && u <= 1.f)) { msg = "v, u must lie in [0,1]"; return ARBOR_ERR_INVALID_ARG; }
+    if (i > 0) {
+      if (t->is_open[p]) { msg = "a node's parent must be closed"; return ARBOR_ERR_INVALID_ARG; }
+      // spans along a root path do not overlap: a child starts after its parent ends
+      if (t->span_start[i] < t->span_start[p] + t->span_len[p]) { msg = "child span overlaps its parent's"; return ARBOR_ERR_INVALID_ARG; }
+      depth[i] = depth[p] + 1;
+    }
+  }
+  std::vector<uint8_t> seen(N, 0);
+  for (int b = 0; b < t->num_active; ++b) {
+    const int a = t->active[b];
+    if (a < 0 || a >= N) { msg = "active leaf is not a node"; return ARBOR_ERR_INVALID_ARG; }
+    if (seen[a]) { msg = "duplicate active leaf"; return ARBOR_ERR_INVALID_ARG; }
+    seen[a] = 1;
+  }
+  if (n_sinks > t->span_len[0]) { msg = "n_sinks > n_root"; return ARBOR_ERR_INVALID_ARG; }
+  if (depth_out) *depth_out = std::move(depth);
+  return ARBOR_OK;
+}
+
+std::vector<uint8_t> host_pinned(const arbor_tree *t) {
+  std::vector<uint8_t> pin(t->num_nodes, 0);
+  for (int b = 0; b < t->num_active; ++b)
+    for (int x = t->active[b]; x >= 0; x = t->parent[x]) pin[x] = 1;
+  for (int i = 0; i < t->num_nodes; ++i) if (t->is_open[i]) pin[i] = 1;
+  return pin;
+}
+
+int64_t floor_count_host(int n, const arbor_params *p) {
+  const int tl = std::min(p->l_tail, n);
+  const int64_t fr = static_cast<int64_t>(std::floor(p->r_min * static_cast<double>(n) + 1e-9));
+  return std::min<int64_t>(n, std::max<int64_t>(std::max(p->k_min, tl), fr));
+}
+
+int64_t min_feasible(const arbor_params *p, const arbor_tree *t) {
+  if (p->alloc_mode == ARBOR_ALLOC_STATIC) return 0;
+  const auto pin = host_pinned(t);
+  int64_t tot = 0;
+  for (int i = 0; i < t->num_nodes; ++i) {
+    const int n = t->span_len[i];
+    if (pin[i]) tot += n;
+    else if (p->alloc_mode == ARBOR_ALLOC_WATERFILL) tot += floor_count_host(n, p);
+    else tot += std::min(n, p->k_min);
+  }
+  return tot;
+}
+
+// The tree must describe exactly the nodes the library knows (spans, lengths, open flags).
+arbor_status check_tree(arbor_ctx *c, const arbor_tree *t, std::vector<int32_t> *depth = nullptr) {
+  std::string msg;
+  arbor_status s = validate_tree_impl(t, c->prm.n_sinks, msg, depth);
+  if (s != ARBOR_OK) return fail(c, s, msg);
+  if (t->num_nodes != c->num_known)
+    return fail(c, ARBOR_ERR_INVALID_ARG, "tree has " + std::to_string(t->num_nodes) +
+                                              " nodes, the context knows " + std::to_string(c->num_known));
+  if (t->num_active > c->max_active) return fail(c, ARBOR_ERR_INVALID_ARG, "too many active leaves");
+  for (int i = 0; i < t->num_nodes; ++i) {
+    if (t->span_start[i] != c->h_span[i] || t->span_len[i] != c->h_n[i] ||
+        (t->is_open[i] != 0) != (c->h_open[i] != 0))
+      return fail(c, ARBOR_ERR_INVALID_ARG, "tree node " + std::to_string(i) +
+                                                " disagrees with the context (span / length / open)");
+  }
+  return ARBOR_OK;
+}
+
+// ---------------------------------------------------------------- tree upload (+ a1)
+arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
+  const int N = t->num_nodes, nA = t->num_active;
+  bool same = c->tree_valid && static_cast<int>(c->t_parent.size()) == N &&
+              static_cast<int>(c->t_active.size()) == nA;
+  if (same) {
+    same = std::memcmp(c->t_parent.data(), t->parent, N * 4) == 0 &&
+           std::memcmp(c->t_len.data(), t->span_len, N * 4) == 0 &&
+           std::memcmp(c->t_active.data(), t->active, nA * 4) == 0 &&
+           std::memcmp(c->t_open.data(), t->is_open, N) == 0 &&
+           std::memcmp(c->t_v.data(), t->search_value, N * 4) == 0 &&
+           std::memcmp(c->t_u.data(), t->uncertainty, N * 4) == 0;
+  }
+  if (same) return ARBOR_OK;
+  // pack [parent | len | active | v | u | open] with the device block's fixed offsets
+  const size_t MN = c->max_nodes, MA = c->max_active;
+  const size_t bytes = MN * 4 * 4 + MA * 4 + MN;
+  void *buf = nullptr;
+  TRY(ring_acquire(c, bytes, &buf));
+  char *b = static_cast<char *>(buf);
+  std::memcpy(b, t->parent, N * 4);
+  std::memcpy(b + MN * 4, t->span_len, N * 4);
+  std::memcpy(b + MN * 8, t->active, nA * 4);
+  std::memcpy(b + MN * 8 + MA * 4, t->search_value, N * 4);
+  std::memcpy(b + MN * 12 + MA * 4, t->uncertainty, N * 4);
+  std::memcpy(b + MN * 16 + MA * 4, t->is_open, N);
+  CK(cudaMemcpyAsync(c->d.parent, b, bytes, cudaMemcpyHostToDevice, c->ms));
+  CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
+  launch_geometry(c, N, nA);
+  CK_LAUNCH();
+  c->t_parent.assign(t->parent, t->parent + N);
+  c->t_len.assign(t->span_len, t->span_len + N);
+  c->t_active.assign(t->active, t->active + nA);
+  c->t_open.assign(t->is_open, t->is_open + N);
+  c->t_v.assign(t->search_value, t->search_value + N);
+  c->t_u.assign(t->uncertainty, t->uncertainty + N);
+  c->tree_valid = true;
+  return ARBOR_OK;
+}
+
+// ---------------------------------------------------------------- attention / score plan
+struct HostPlan {
+  std::vector<int32_t> seg_node, seg_chunk, seg_loff, seg_lcnt, pair_b, bp_off, bp_list;
+  std::vector<std::vector<int32_t>> paths;
+  int max_lcnt = 0;
+};
+
+void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan &p) {
+  const int N = t->num_nodes, nA = t->num_active;
+  std::vector<std::vector<int32_t>> leaves(N);
+  p.paths.assign(nA, {});
+  for (int b = 0; b < nA; ++b) {
+    auto &path = p.paths[b];
+    for (int x = t->active[b]; x >= 0; x = t->parent[x]) path.push_back(x);
+    std::reverse(path.begin(), path.end());
+    for (int x : path) leaves[x].push_back(b);
+  }
+  std::vector<int32_t> seg_of(N, -1);
+  for (int x = 0; x < N; ++x) {
+    if (leaves[x].empty()) continue;
+    const int nch = (n_of[x] + kAttnChunk - 1) / kAttnChunk;
+    if (nch == 0) continue;
+    seg_of[x] = static_cast<int32_t>(p.seg_node.size());
+    const int lc = static_cast<int>(leaves[x].size());
+    p.max_lcnt = std::max(p.max_lcnt, lc);
+    for (int ch = 0; ch < nch; ++ch) {
+      p.seg_node.push_back(x);
+      p.seg_chunk.push_back(ch);
+      p.seg_loff.push_back(static_cast<int32_t>(p.pair_b.size()));
+      p.seg_lcnt.push_back(lc);
+      p.pair_b.insert(p.pair_b.end(), leaves[x].begin(), leaves[x].end());
+    }
+  }
+  p.bp_off.assign(1, 0);
+  for (int b = 0; b < nA; ++b) {
+    for (int x : p.paths[b]) {
+      if (seg_of[x] < 0) continue;
+      const int nch = (n_of[x] + kAttnChunk - 1) / kAttnChunk;
+      const int pos = static_cast<int>(std::lower_bound(leaves[x].begin(), leaves[x].end(), b) -
+                                       leaves[x].begin());
+      for (int ch = 0; ch < nch; ++ch) p.bp_list.push_back(p.seg_loff[seg_of[x] + ch] + pos);
+    }
+    p.bp_off.push_back(static_cast<int32_t>(p.bp_list.size()));
+  }
+}
+
+// Upload [nq int64[N] (optional)] + plan arrays + extra int32 list; fill a PlanView.
+arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
+                         const std::vector<int32_t> *extra, PlanView &pv, const int32_t **d_extra) {
+  const size_t nseg = p.seg_node.size(), np = p.pair_b.size();
+  std::vector<int32_t> packed;
+  packed.reserve(4 * nseg + np + p.bp_off.size() + p.bp_list.size() + (extra ? extra->size() : 0));
+  auto put = [&](const std::vector<int32_t> &v) {
+    const size_t off = packed.size();
+    packed.insert(packed.end(), v.begin(), v.end());
+    return off;
+  };
+  const size_t o_node = put(p.seg_node), o_chunk = put(p.seg_chunk), o_loff = put(p.seg_loff),
+               o_lcnt = put(p.seg_lcnt), o_pb = put(p.pair_b), o_bpo = put(p.bp_off),
+               o_bpl = put(p.bp_list);
+  size_t o_extra = packed.size();
+  if (extra) put(*extra);
+  const size_t plan_bytes = packed.size() * 4;
+  if (plan_bytes > c->seg_cap) {
+    if (c->d.seg) CK(cudaFree(c->d.seg));
+    c->seg_cap = std::max<size_t>(plan_bytes * 2, 1 << 16);
+    CK(cudaMalloc(&c->d.seg, c->seg_cap));
+  }
+  if (!packed.empty()) TRY(ring_upload(c, c->d.seg, packed.data(), plan_bytes));
+  if (with_nq) TRY(ring_upload(c, c->d.nq, c->h_nq.data(), c->num_known * sizeof(int64_t)));
+  const int32_t *base = c->d.seg;
+  pv.seg_node = base + o_node;
+  pv.seg_chunk = base + o_chunk;
+  pv.seg_loff = base + o_loff;
+  pv.seg_lcnt = base + o_lcnt;
+  pv.pair_b = base + o_pb;
+  pv.bp_off = base + o_bpo;
+  pv.bp_list = base + o_bpl;
+  pv.S = static_cast<int>(nseg);
+  pv.nA = nA;
+  pv.P = static_cast<int>(np);
+  if (d_extra) *d_extra = base + o_extra;
+  return ARBOR_OK;
+}
+
+arbor_status ensure_partials(arbor_ctx *c, size_t pairs, int layer_count) {
+  const size_t need = pairs * layer_count * c->Hq * (c->D + 2) * sizeof(float);
+  if (need > c->partial_cap) {
+    if (c->d.partials) CK(cudaFree(c->d.partials));
+    c->partial_cap = std::max<size_t>(need + need / 2, 1 << 20);
+    CK(cudaMalloc(&c->d.partials, c->partial_cap));
+  }
+  return ARBOR_OK;
+}
+
+arbor_status run_attention(arbor_ctx *c, const HostPlan &hp, const PlanView &pv, int layer_begin,
+                           int layer_count, const void *q, void *out, float *lse) {
+  TRY(ensure_partials(c, hp.pair_b.size(), layer_count));
+  launch_attn_partial(c, pv, hp.max_lcnt * c->G, q, layer_begin, layer_count);
+  CK_LAUNCH();
+  launch_attn_merge(c, pv, layer_count, out, lse);
+  CK_LAUNCH();
+  return ARBOR_OK;
+}
+
+void wait_side(arbor_ctx *c) {
+  if (c->side_pending) {
+    cudaStreamWaitEvent(c->ms, c->ev_side_done, 0);
+  }
+}
+
+arbor_status latched(arbor_ctx *c) {
+  Ctrl h{};
+  CK(cudaMemcpy(&h, c->d.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+  if (h.err) {
+    const int32_t zero = 0;
+    CK(cudaMemcpy(&c->d.ctrl->err, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+    if (h.err & DERR_INVARIANT)
+      return fail(c, ARBOR_ERR_INVARIANT, "device: invalid accumulated attention / weight (NaN, negative or out of range)");
+    if (h.err & DERR_OUT_OF_PAGES) return fail(c, ARBOR_ERR_OUT_OF_PAGES, "device: page pool exhausted");
+    return fail(c, ARBOR_ERR_STATE, "device: state error");
+  }
+  return ARBOR_OK;
+}
+
+arbor_status sync_all(arbor_ctx *c) {
+  CK(cudaStreamSynchronize(c->ss));
+  CK(cudaStreamSynchronize(c->ms));
+  return latched(c);
+}
+
+__global__ void init_node_kernel(int node, int64_t span, int32_t *n, int32_t *kcur, int32_t *npages,
+                                 int64_t *span_arr, int64_t *mclose, float *s, float *a) {
+  n[node] = 0;
+  kcur[node] = 0;
+  npages[node] = 0;
+  span_arr[node] = span;
+  mclose[node] = 0;
+  s[node] = 0.5f;
+  a[node] = 0.f;
+}
+
+__global__ void init_free_kernel(int32_t *free_stack, int num_pages, Ctrl *ctrl) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < num_pages) free_stack[i] = num_pages - 1 - i;   // pops yield 0, 1, 2, …
+  if (i == 0) {
+    ctrl->free_top = num_pages;
+    ctrl->err = 0;
+    ctrl->work_count = 0;
+    ctrl->rehyd_count = 0;
+    ctrl->evicted = 0;
+    ctrl->rehydrations = 0;
+    ctrl->pages_in_use = 0;
+  }
+}
+
+__global__ void fill_f32(float *p, int n, float v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- profiling hooks
+namespace arbor {
+void stage_begin(arbor_ctx *c, int st, cudaStream_t s) {
+  if (c->cfg.flags & ARBOR_FLAG_PROFILE) cudaEventRecord(c->st_ev[st][0], s);
+}
+void stage_end(arbor_ctx *c, int st, cudaStream_t s) {
+  if (c->cfg.flags & ARBOR_FLAG_PROFILE) {
+    cudaEventRecord(c->st_ev[st][1], s);
+    c->st_used[st] = true;
+  }
+}
+}  // namespace arbor
+
+// ================================================================ C ABI
+extern "C" {
+
+const char *arbor_version(void) { return ARBOR_VERSION; }
+
+const char *arbor_status_string(arbor_status s) {
+  switch (s) {
+    case ARBOR_OK: return "ok";
+    case ARBOR_ERR_INVALID_ARG: return "invalid argument";
+    case ARBOR_ERR_INFEASIBLE_BUDGET: return "infeasible budget";
+    case ARBOR_ERR_INVARIANT: return "invariant violated";
+    case ARBOR_ERR_IO: return "host stash I/O error";
+    case ARBOR_ERR_OUT_OF_PAGES: return "out of pages";
+    case ARBOR_ERR_STATE: return "lifecycle state error";
+    case ARBOR_ERR_CUDA: return "CUDA error";
+    case ARBOR_ERR_NCCL: return "NCCL error";
+  }
+  return "unknown status";
+}
+
+const char *arbor_last_error(const arbor_ctx *ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+arbor_status arbor_validate_tree(const arbor_tree *tree, int32_t n_sinks, char *msg, size_t msg_len) {
+  std::string m;
+  arbor_status s = validate_tree_impl(tree, n_sinks, m);
+  if (msg && msg_len) {
+    std::snprintf(msg, msg_len, "%s", m.c_str());
+  }
+  return s;
+}
+
+arbor_status arbor_min_feasible_budget(const arbor_params *params, const arbor_tree *tree,
+                                       int64_t *out) {
+  std::string m;
+  arbor_status s = validate_params(params, m);
+  if (s != ARBOR_OK) return s;
+  s = validate_tree_impl(tree, params->n_sinks, m);
+  if (s != ARBOR_OK) return s;
+  if (!out) return ARBOR_ERR_INVALID_ARG;
+  *out = min_feasible(params, tree);
+  return ARBOR_OK;
+}
+
+arbor_status arbor_nccl_unique_id(void *out128) {
+  if (!out128) return ARBOR_ERR_INVALID_ARG;
+  if (!g_nccl.load()) return ARBOR_ERR_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.getUniqueId(&id) != ncclSuccess) return ARBOR_ERR_NCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return ARBOR_OK;
+}
+
+arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arbor_ctx **out) {
+  if (!out) return ARBOR_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!cfg) return ARBOR_ERR_INVALID_ARG;
+  std::string msg;
+  if (validate_params(params, msg) != ARBOR_OK) return ARBOR_ERR_INVALID_ARG;
+  const arbor_config &k = *cfg;
+  if (k.num_layers < 1 || k.num_kv_heads < 1 || k.num_q_heads < 1 || k.num_q_heads % k.num_kv_heads)
+    return ARBOR_ERR_INVALID_ARG;
+  if (k.head_dim != 64 && k.head_dim != 128) return ARBOR_ERR_INVALID_ARG;
+  if (k.layer_begin < 0 || k.layer_count < 1 || k.layer_begin + k.layer_count > k.num_layers)
+    return ARBOR_ERR_INVALID_ARG;
+  if (k.kv_head_begin < 0 || k.kv_head_count < 1 || k.kv_head_begin + k.kv_head_count > k.num_kv_heads)
+    return ARBOR_ERR_INVALID_ARG;
+  if (k.kv_dtype != ARBOR_F32 && k.kv_dtype != ARBOR_BF16) return ARBOR_ERR_INVALID_ARG;
+  if (k.page_size < 1 || k.page_size > 1024 || k.num_pages < 1) return ARBOR_ERR_INVALID_ARG;
+  if (k.max_nodes < 1 || k.max_nodes > 4096) return ARBOR_ERR_INVALID_ARG;
+  if (k.max_node_tokens < 1 || k.max_node_tokens > 32767) return ARBOR_ERR_INVALID_ARG;
+  if (k.max_active < 1 || k.max_active > 1024 || k.max_tokens < 1) return ARBOR_ERR_INVALID_ARG;
+  if (!k.k_pool || !k.v_pool || !k.pos_pool || !k.score) return ARBOR_ERR_INVALID_ARG;
+  if (k.world_size < 1 || k.rank < 0 || k.rank >= k.world_size) return ARBOR_ERR_INVALID_ARG;
+  if (k.world_size > 1 && !k.nccl_unique_id) return ARBOR_ERR_INVALID_ARG;
+
+  arbor_ctx *c = new arbor_ctx();
+  c->cfg = k;
+  c->prm = *params;
+  c->L = k.layer_count;
+  c->H = k.kv_head_count;
+  c->G = k.num_q_heads / k.num_kv_heads;
+  c->Hq = c->H * c->G;
+  c->D = k.head_dim;
+  c->P = k.page_size;
+  c->NP = k.num_pages;
+  c->esize = k.kv_dtype == ARBOR_BF16 ? 2 : 4;
+  c->Lg = k.num_layers;
+  c->Hg = k.num_kv_heads;
+  c->Hqg = k.num_q_heads;
+  c->max_nodes = k.max_nodes;
+  c->max_pages_node = (k.max_node_tokens + k.page_size - 1) / k.page_size;
+  c->max_active = k.max_active;
+  c->max_tokens = k.max_tokens;
+  auto bail = [&](arbor_status s) { arbor_destroy(c); return s; };
+  // main_stream is used as given: NULL is the legacy default stream (a valid cudaStream_t)
+  c->ms = static_cast<cudaStream_t>(k.main_stream);
+  if (k.side_stream) c->ss = static_cast<cudaStream_t>(k.side_stream);
+  else { if (cudaStreamCreateWithFlags(&c->ss, cudaStreamNonBlocking) != cudaSuccess) return bail(ARBOR_ERR_CUDA); c->own_ss = true; }
+
+  const int MN = c->max_nodes, MA = c->max_active;
+  DevState &d = c->d;
+  arbor_status s = ARBOR_OK;
+#define ALLOC(ptr, cnt) do { s = dmalloc(c, &(ptr), (cnt)); if (s != ARBOR_OK) return bail(s); } while (0)
+  ALLOC(d.n, MN); ALLOC(d.kcur, MN); ALLOC(d.npages, MN);
+  ALLOC(d.ptab, static_cast<size_t>(MN) * c->max_pages_node);
+  ALLOC(d.free_stack, c->NP);
+  ALLOC(d.span, MN); ALLOC(d.mass2, 2 * MN); ALLOC(d.mclose, MN); ALLOC(d.nq, MN);
+  ALLOC(d.a, MN); ALLOC(d.s, MN);
+  ALLOC(d.ctrl, 1);
+  {
+    // tree mirror block: [parent | len | active | v | u | open] (fixed offsets, see upload_tree)
+    char *blk = nullptr;
+    const size_t bytes = static_cast<size_t>(MN) * 16 + static_cast<size_t>(MA) * 4 + MN;
+    if (cudaMalloc(&blk, bytes) != cudaSuccess) return bail(ARBOR_ERR_CUDA);
+    d.parent = reinterpret_cast<int32_t *>(blk);
+    d.len = reinterpret_cast<int32_t *>(blk + MN * 4);
+    d.active = reinterpret_cast<int32_t *>(blk + MN * 8);
+    d.v = reinterpret_cast<float *>(blk + MN * 8 + MA * 4);
+    d.u = reinterpret_cast<float *>(blk + MN * 12 + MA * 4);
+    d.open = reinterpret_cast<uint8_t *>(blk + MN * 16 + MA * 4);
+  }
+  ALLOC(d.onpath, MN); ALLOC(d.pinned, MN); ALLOC(d.depth, MN); ALLOC(d.delta, MN);
+  ALLOC(d.Ed, 2 * MN + 2); ALLOC(d.ED, 2 * MN + 2);
+  ALLOC(d.work_node, MN); ALLOC(d.work_old, MN); ALLOC(d.work_new, MN);
+  ALLOC(d.rehyd_nodes, MN + 1); ALLOC(d.rehyd_flag, MN + 2);
+#undef ALLOC
+  init_free_kernel<<<(c->NP + 255) / 256, 256, 0, c->ms>>>(d.free_stack, c->NP, d.ctrl);
+  fill_f32<<<(MN + 255) / 256, 256, 0, c->ms>>>(d.s, MN, 0.5f);
+  c->launches += 2;
+  {
+    // E_d[x] = e^{−λ_d x}, E_Δ[x] = e^{−λ_Δ x} from host libm (Q9)
+    std::vector<double> Ed(2 * MN + 2), ED(2 * MN + 2);
+    for (int x = 0; x < 2 * MN + 2; ++x) {
+      Ed[x] = std::exp(-params->lambda_d * x);
+      ED[x] = std::exp(-params->lambda_delta * x);
+    }
+    if (cudaMemcpy(d.Ed, Ed.data(), Ed.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(d.ED, ED.data(), ED.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(ARBOR_ERR_CUDA);
+  }
+  for (int i = 0; i < kRingSlots; ++i) {
+    if (cudaHostAlloc(&c->ring[i], kRingBytes, cudaHostAllocDefault) != cudaSuccess) return bail(ARBOR_ERR_CUDA);
+    if (cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming) != cudaSuccess) return bail(ARBOR_ERR_CUDA);
+    cudaEventRecord(c->ring_ev[i], c->ms);
+  }
+  if (cudaEventCreateWithFlags(&c->ev_main_to_side, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_side_done, cudaEventDisableTiming) != cudaSuccess)
+    return bail(ARBOR_ERR_CUDA);
+  for (int i = 0; i < ARBOR_NUM_STAGES; ++i)
+    for (int j = 0; j < 2; ++j)
+      if (cudaEventCreate(&c->st_ev[i][j]) != cudaSuccess) return bail(ARBOR_ERR_CUDA);
+  // pinned host stash [2][L][H][max_tokens][D]
+  const size_t stash_bytes = 2ull * c->L * c->H * static_cast<size_t>(c->max_tokens) * c->D * c->esize;
+  if (k.host_stash) {
+    if (k.host_stash_bytes < stash_bytes) { c->err = "host_stash too small"; return bail(ARBOR_ERR_INVALID_ARG); }
+    c->stash_host = k.host_stash;
+  } else {
+    if (cudaHostAlloc(&c->stash_host, stash_bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+      return bail(ARBOR_ERR_IO);
+    c->own_stash = true;
+  }
+  if (cudaHostGetDevicePointer(&c->stash_dev, c->stash_host, 0) != cudaSuccess) return bail(ARBOR_ERR_IO);
+  // NCCL communicator for the mass all-reduce (a10)
+  if (k.world_size > 1) {
+    if (!g_nccl.load()) return bail(ARBOR_ERR_NCCL);
+    ncclUniqueId id;
+    std::memcpy(&id, k.nccl_unique_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    if (g_nccl.commInitRank(&comm, k.world_size, id, k.rank) != ncclSuccess) return bail(ARBOR_ERR_NCCL);
+    c->nccl_comm = comm;
+  }
+  if (cudaStreamSynchronize(c->ms) != cudaSuccess) return bail(ARBOR_ERR_CUDA);
+  *out = c;
+  return ARBOR_OK;
+}
+
+void arbor_destroy(arbor_ctx *c) {
+  if (!c) return;
+  if (c->ms) cudaStreamSynchronize(c->ms);
+  if (c->ss) cudaStreamSynchronize(c->ss);
+  if (c->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(static_cast<ncclComm_t>(c->nccl_comm));
+  DevState &d = c->d;
+  void *ptrs[] = {d.n, d.kcur, d.npages, d.ptab, d.free_stack, d.span, d.mass2, d.mclose, d.nq,
+                  d.a, d.s, d.ctrl, d.parent, d.onpath, d.pinned, d.depth, d.delta, d.Ed, d.ED,
+                  d.work_node, d.work_old, d.work_new, d.rehyd_nodes, d.rehyd_flag, d.seg,
+                  d.partials, d.lse_scratch, d.out_scratch};
+  for (void *p : ptrs) if (p) cudaFree(p);
+  for (auto &sn : c->snap) {
+    if (!sn.valid) continue;
+    void *sp[] = {sn.n, sn.kcur, sn.npages, sn.ptab, sn.free_stack, sn.mclose, sn.nq_dev, sn.s, sn.ctrl};
+    for (void *p : sp) if (p) cudaFree(p);
+  }
+  for (int i = 0; i < kRingSlots; ++i) {
+    if (c->ring[i]) cudaFreeHost(c->ring[i]);
+    if (c->ring_ev[i]) cudaEventDestroy(c->ring_ev[i]);
+  }
+  if (c->ev_main_to_side) cudaEventDestroy(c->ev_main_to_side);
+  if (c->ev_side_done) cudaEventDestroy(c->ev_side_done);
+  for (int i = 0; i < ARBOR_NUM_STAGES; ++i)
+    for (int j = 0; j < 2; ++j) if (c->st_ev[i][j]) cudaEventDestroy(c->st_ev[i][j]);
+  if (c->own_stash && c->stash_host) cudaFreeHost(c->stash_host);
+  if (c->own_ms) cudaStreamDestroy(c->ms);
+  if (c->own_ss) cudaStreamDestroy(c->ss);
+  delete c;
+}
+
+// ---------------------------------------------------------------- node plumbing
+arbor_status arbor_open_node(arbor_ctx *c, int32_t node, int64_t span_start) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  if (node != c->num_known) return fail(c, ARBOR_ERR_INVALID_ARG, "node ids are dense: expected " + std::to_string(c->num_known));
+  if (node >= c->max_nodes) return fail(c, ARBOR_ERR_INVALID_ARG, "max_nodes exceeded");
+  if (span_start < 0 || span_start >= c->max_tokens) return fail(c, ARBOR_ERR_INVALID_ARG, "span_start out of range");
+  init_node_kernel<<<1, 1, 0, c->ms>>>(node, span_start, c->d.n, c->d.kcur, c->d.npages, c->d.span,
+                                       c->d.mclose, c->d.s, c->d.a);
+  ARBOR_LAUNCHED(c);
+  CK_LAUNCH();
+  c->h_n.push_back(0);
+  c->h_open.push_back(1);
+  c->h_span.push_back(span_start);
+  c->h_nq.push_back(0);
+  ++c->num_known;
+  c->tree_valid = false;
+  return ARBOR_OK;
+}
+
+arbor_status arbor_append_kv(arbor_ctx *c, int32_t node, const void *k, const void *v, int32_t ntok) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  if (node < 0 || node >= c->num_known) return fail(c, ARBOR_ERR_INVALID_ARG, "unknown node");
+  if (!c->h_open[node]) return fail(c, ARBOR_ERR_STATE, "append to a closed node");
+  if (ntok < 1 || !k || !v) return fail(c, ARBOR_ERR_INVALID_ARG, "ntok >= 1 and K/V pointers required");
+  const int64_t new_n = static_cast<int64_t>(c->h_n[node]) + ntok;
+  if (new_n > c->cfg.max_node_tokens) return fail(c, ARBOR_ERR_INVALID_ARG, "node exceeds max_node_tokens");
+  if (c->h_span[node] + new_n > c->max_tokens) return fail(c, ARBOR_ERR_INVALID_ARG, "position stream exceeds max_tokens");
+  launch_append(c, node, k, v, c->h_n[node], ntok);
+  CK_LAUNCH();
+  c->h_n[node] = static_cast<int32_t>(new_n);
+  c->tree_valid = false;
+  return ARBOR_OK;
+}
+
+arbor_status arbor_close_node(arbor_ctx *c, int32_t node) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  if (node < 0 || node >= c->num_known) return fail(c, ARBOR_ERR_INVALID_ARG, "unknown node");
+  if (!c->h_open[node]) return fail(c, ARBOR_ERR_STATE, "closing a node that is not open");
+  if (c->h_n[node] < 1) return fail(c, ARBOR_ERR_INVALID_ARG, "closing an empty node");
+  // Mclose_i: this rank's partial mass of the node at close (Q5)
+  TRY(ring_upload(c, c->d.rehyd_nodes + c->max_nodes, &node, sizeof(int32_t)));
+  CK(cudaMemsetAsync(c->d.mclose + node, 0, sizeof(int64_t), c->ms));
+  launch_node_mass(c, c->d.rehyd_nodes + c->max_nodes, 1, c->d.mclose, 1);
+  CK_LAUNCH();
+  // write-through stash on the side stream (a7), after the node's last append
+  CK(cudaEventRecord(c->ev_main_to_side, c->ms));
+  CK(cudaStreamWaitEvent(c->ss, c->ev_main_to_side, 0));
+  launch_stash(c, node, c->h_n[node], c->h_span[node]);
+  CK_LAUNCH();
+  CK(cudaEventRecord(c->ev_side_done, c->ss));
+  c->side_pending = true;
+  c->h_open[node] = 0;
+  c->h_nq[node] = 0;
+  c->tree_valid = false;
+  return ARBOR_OK;
+}
+
+// ---------------------------------------------------------------- hot path
+arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, const float *lse,
+                         float *s_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  TRY(check_tree(c, tree));
+  if (!q) return fail(c, ARBOR_ERR_INVALID_ARG, "q is NULL");
+  const int N = tree->num_nodes, nA = tree->num_active;
+  TRY(upload_tree(c, tree));
+  HostPlan hp;
+  build_plan(tree, c->h_n, hp);
+  // Nq_i += 1 for every closed i on Path(ℓ_b) (one query per active leaf and step)
+  for (int b = 0; b < nA; ++b)
+    for (int x : hp.paths[b]) if (!c->h_open[x]) c->h_nq[x] += 1;
+  std::vector<int32_t> closed;
+  for (int i = 0; i < N; ++i) if (!c->h_open[i]) closed.push_back(i);
+  PlanView pv{};
+  const int32_t *d_closed = nullptr;
+  TRY(upload_plan(c, hp, nA, true, &closed, pv, &d_closed));
+  const float *lse_use = lse;
+  if (!lse) {
+    const size_t qn = static_cast<size_t>(nA) * c->L * c->Hq;
+    if (c->d.lse_scratch) { cudaFree(c->d.lse_scratch); c->d.lse_scratch = nullptr; }
+    if (c->d.out_scratch) { cudaFree(c->d.out_scratch); c->d.out_scratch = nullptr; }
+    CK(cudaMalloc(&c->d.lse_scratch, qn * sizeof(float)));
+    CK(cudaMalloc(&c->d.out_scratch, qn * c->D * c->esize));
+    TRY(run_attention(c, hp, pv, 0, c->L, q, c->d.out_scratch, c->d.lse_scratch));
+    lse_use = c->d.lse_scratch;
+  }
+  launch_score_accum(c, pv, hp.max_lcnt * c->G, q, lse_use, c->L);
+  CK_LAUNCH();
+  stage_begin(c, ARBOR_ST_NODE_MASS, c->ms);
+  CK(cudaMemsetAsync(c->d.mass2, 0, N * sizeof(int64_t), c->ms));
+  launch_node_mass(c, d_closed, static_cast<int>(closed.size()), c->d.mass2, 1);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(c->d.mass2 + N, c->d.mclose, N * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->ms));
+  stage_end(c, ARBOR_ST_NODE_MASS, c->ms);
+  if (c->cfg.world_size > 1) {
+    stage_begin(c, ARBOR_ST_ALLREDUCE, c->ms);
+    if (g_nccl.allReduce(c->d.mass2, c->d.mass2, 2 * static_cast<size_t>(N), ncclInt64, ncclSum,
+                         static_cast<ncclComm_t>(c->nccl_comm), c->ms) != ncclSuccess)
+      return fail(c, ARBOR_ERR_NCCL, "ncclAllReduce failed");
+    stage_end(c, ARBOR_ST_ALLREDUCE, c->ms);
+  }
+  launch_msve(c, N, s_out);
+  CK_LAUNCH();
+  return ARBOR_OK;
+}
+
+arbor_status arbor_allocate(arbor_ctx *c, const arbor_tree *tree, const float *s, int64_t budget,
+                            int32_t *k_out, int64_t *min_feasible_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  std::vector<int32_t> depth;
+  TRY(check_tree(c, tree, &depth));
+  if (!k_out) return fail(c, ARBOR_ERR_INVALID_ARG, "k_out is NULL");
+  if (budget < 0) return fail(c, ARBOR_ERR_INVALID_ARG, "negative budget");
+  // weights must stay ≤ 2^16 (Q29): bound e^{−λ_d d} e^{−λ_Δ Δ} over the tree's depths
+  int maxd = 0;
+  for (int x : depth) maxd = std::max(maxd, x);
+  double bd = 0, bD = 0;
+  for (int x = 0; x <= maxd; ++x) bd = std::max(bd, std::exp(-c->prm.lambda_d * x));
+  for (int x = 0; x <= 2 * maxd; ++x) bD = std::max(bD, std::exp(-c->prm.lambda_delta * x));
+  if (!(bd * bD <= 65536.0)) return fail(c, ARBOR_ERR_INVALID_ARG, "lambda_d / lambda_delta make weights exceed 2^16");
+  const int64_t mf = min_feasible(&c->prm, tree);
+  if (c->prm.alloc_mode != ARBOR_ALLOC_STATIC && budget < mf) {
+    if (min_feasible_out) *min_feasible_out = mf;
+    return fail(c, ARBOR_ERR_INFEASIBLE_BUDGET, "budget " + std::to_string(budget) +
+                                                    " < minimum feasible " + std::to_string(mf));
+  }
+  TRY(upload_tree(c, tree));
+  launch_allocate(c, tree->num_nodes, s ? s : c->d.s, budget, k_out);
+  CK_LAUNCH();
+  return ARBOR_OK;
+}
+
+arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_target,
+                         int64_t *evicted_tokens_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  TRY(check_tree(c, tree));
+  if (!k_target) return fail(c, ARBOR_ERR_INVALID_ARG, "k_target is NULL");
+  TRY(upload_tree(c, tree));
+  const auto pin = host_pinned(tree);
+  int max_n = 0;
+  for (int i = 0; i < tree->num_nodes; ++i)
+    if (!pin[i]) max_n = std::max(max_n, c->h_n[i]);
+  wait_side(c);   // pending stash copies read pages this call may free
+  launch_evict_plan(c, tree->num_nodes, k_target);
+  CK_LAUNCH();
+  if (max_n > 0) {
+    launch_select_compact(c, max_n);
+    CK_LAUNCH();
+  }
+  if (evicted_tokens_out) {
+    CK(cudaStreamSynchronize(c->ms));
+    long long ev = 0;
+    CK(cudaMemcpy(&ev, &c->d.ctrl->evicted, sizeof(ev), cudaMemcpyDeviceToHost));
+    *evicted_tokens_out = ev;
+    TRY(latched(c));
+  }
+  return ARBOR_OK;
+}
+
+arbor_status arbor_rehydrate(arbor_ctx *c, const arbor_tree *tree, const int32_t *nodes, int32_t count) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  TRY(check_tree(c, tree));
+  if (count < 0 || (count > 0 && !nodes)) return fail(c, ARBOR_ERR_INVALID_ARG, "bad node list");
+  std::vector<int32_t> list(nodes, nodes + count);
+  for (int x : list) {
+    if (x < 0 || x >= c->num_known) return fail(c, ARBOR_ERR_INVALID_ARG, "unknown node in list");
+    if (c->h_open[x]) return fail(c, ARBOR_ERR_STATE, "rehydrating an open node");
+  }
+  std::sort(list.begin(), list.end());
+  list.erase(std::unique(list.begin(), list.end()), list.end());
+  if (list.empty()) return ARBOR_OK;
+  int max_n = 0;
+  for (int x : list) max_n = std::max(max_n, c->h_n[x]);
+  TRY(upload_tree(c, tree));
+  TRY(ring_upload(c, c->d.rehyd_nodes, list.data(), list.size() * sizeof(int32_t)));
+  wait_side(c);
+  stage_begin(c, ARBOR_ST_REHYDRATE, c->ms);
+  launch_rehydrate_plan(c, static_cast<int>(list.size()));
+  CK_LAUNCH();
+  CK(cudaEventRecord(c->ev_main_to_side, c->ms));
+  CK(cudaStreamWaitEvent(c->ss, c->ev_main_to_side, 0));
+  launch_rehydrate_copy(c, static_cast<int>(list.size()), max_n);
+  CK_LAUNCH();
+  CK(cudaEventRecord(c->ev_side_done, c->ss));
+  c->side_pending = true;
+  CK(cudaStreamWaitEvent(c->ms, c->ev_side_done, 0));   // ready before the next decode
+  stage_end(c, ARBOR_ST_REHYDRATE, c->ms);
+  return ARBOR_OK;
+}
+
+arbor_status arbor_tree_decode_attn(arbor_ctx *c, const arbor_tree *tree, int32_t layer_begin,
+                                    int32_t layer_count, const void *q, void *out, float *lse_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  TRY(check_tree(c, tree));
+  if (!q || !out) return fail(c, ARBOR_ERR_INVALID_ARG, "q / out is NULL");
+  if (layer_begin < 0 || layer_count < 1 || layer_begin + layer_count > c->L)
+    return fail(c, ARBOR_ERR_INVALID_ARG, "layer range outside the shard");
+  HostPlan hp;
+  build_plan(tree, c->h_n, hp);
+  PlanView pv{};
+  TRY(upload_plan(c, hp, tree->num_active, false, nullptr, pv, nullptr));
+  return run_attention(c, hp, pv, layer_begin, layer_count, q, out, lse_out);
+}
+
+// ---------------------------------------------------------------- inspection
+arbor_status arbor_sync(arbor_ctx *c) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  return sync_all(c);
+}
+
+arbor_status arbor_read_node(arbor_ctx *c, int32_t node, int32_t *k_cur, int32_t *n, int32_t *pages,
+                             int32_t *num_pages) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  if (node < 0 || node >= c->num_known) return fail(c, ARBOR_ERR_INVALID_ARG, "unknown node");
+  TRY(sync_all(c));
+  int32_t kc = 0, nn = 0, np = 0;
+  CK(cudaMemcpy(&kc, c->d.kcur + node, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&nn, c->d.n + node, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&np, c->d.npages + node, 4, cudaMemcpyDeviceToHost));
+  if (k_cur) *k_cur = kc;
+  if (n) *n = nn;
+  if (num_pages) {
+    if (pages) {
+      if (*num_pages < np) return fail(c, ARBOR_ERR_INVALID_ARG, "pages buffer too small");
+      if (np) CK(cudaMemcpy(pages, c->d.ptab + static_cast<int64_t>(node) * c->max_pages_node, np * 4, cudaMemcpyDeviceToHost));
+    }
+    *num_pages = np;
+  }
+  return ARBOR_OK;
+}
+
+arbor_status arbor_read_free_list(arbor_ctx *c, int32_t *pages, int32_t *count) {
+  if (!c || !count) return ARBOR_ERR_INVALID_ARG;
+  TRY(sync_all(c));
+  Ctrl h{};
+  CK(cudaMemcpy(&h, c->d.ctrl, sizeof(h), cudaMemcpyDeviceToHost));
+  if (pages) {
+    if (*count < h.free_top) return fail(c, ARBOR_ERR_INVALID_ARG, "buffer too small");
+    if (h.free_top) CK(cudaMemcpy(pages, c->d.free_stack, h.free_top * 4, cudaMemcpyDeviceToHost));
+  }
+  *count = h.free_top;
+  return ARBOR_OK;
+}
+
+arbor_status arbor_read_scores(arbor_ctx *c, int32_t num_nodes, int64_t *mass, int64_t *mclose,
+                               int64_t *nq, float *a, float *s) {
+  if (!c || num_nodes < 0 || num_nodes > c->num_known) return ARBOR_ERR_INVALID_ARG;
+  TRY(sync_all(c));
+  const int N = num_nodes;
+  if (mass && N) CK(cudaMemcpy(mass, c->d.mass2, N * 8, cudaMemcpyDeviceToHost));
+  if (mclose && N) CK(cudaMemcpy(mclose, c->d.mclose, N * 8, cudaMemcpyDeviceToHost));
+  if (nq) for (int i = 0; i < N; ++i) nq[i] = c->h_nq[i];
+  if (a && N) CK(cudaMemcpy(a, c->d.a, N * 4, cudaMemcpyDeviceToHost));
+  if (s && N) CK(cudaMemcpy(s, c->d.s, N * 4, cudaMemcpyDeviceToHost));
+  return ARBOR_OK;
+}
+
+arbor_status arbor_read_counters(arbor_ctx *c, int64_t *rehydrations, int64_t *pages_in_use) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  TRY(sync_all(c));
+  Ctrl h{};
+  CK(cudaMemcpy(&h, c->d.ctrl, sizeof(h), cudaMemcpyDeviceToHost));
+  if (rehydrations) *rehydrations = h.rehydrations;
+  if (pages_in_use) *pages_in_use = h.pages_in_use;
+  return ARBOR_OK;
+}
+
+arbor_status arbor_save_state(arbor_ctx *c, int32_t slot) {
+  if (!c || slot < 0 || slot >= kStashSlots) return ARBOR_ERR_INVALID_ARG;
+  Snapshot &sn = c->snap[slot];
+  const size_t MN = c->max_nodes, PT = MN * c->max_pages_node;
+  if (!sn.valid) {
+    CK(cudaMalloc(&sn.n, MN * 4)); CK(cudaMalloc(&sn.kcur, MN * 4)); CK(cudaMalloc(&sn.npages, MN * 4));
+    CK(cudaMalloc(&sn.ptab, PT * 4)); CK(cudaMalloc(&sn.free_stack, c->NP * 4));
+    CK(cudaMalloc(&sn.mclose, MN * 8)); CK(cudaMalloc(&sn.nq_dev, MN * 8)); CK(cudaMalloc(&sn.s, MN * 4));
+    CK(cudaMalloc(&sn.ctrl, sizeof(Ctrl)));
+    sn.valid = true;
+  }
+  wait_side(c);
+  auto cp = [&](void *dst, const void *src, size_t b) {
+    return cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToDevice, c->ms);
+  };
+  CK(cp(sn.n, c->d.n, MN * 4)); CK(cp(sn.kcur, c->d.kcur, MN * 4)); CK(cp(sn.npages, c->d.npages, MN * 4));
+  CK(cp(sn.ptab, c->d.ptab, PT * 4)); CK(cp(sn.free_stack, c->d.free_stack, c->NP * 4));
+  CK(cp(sn.mclose, c->d.mclose, MN * 8)); CK(cp(sn.s, c->d.s, MN * 4)); CK(cp(sn.ctrl, c->d.ctrl, sizeof(Ctrl)));
+  sn.h_n = c->h_n; sn.h_open = c->h_open; sn.h_span = c->h_span; sn.h_nq = c->h_nq;
+  sn.num_known = c->num_known;
+  return ARBOR_OK;
+}
+
+arbor_status arbor_load_state(arbor_ctx *c, int32_t slot) {
+  if (!c || slot < 0 || slot >= kStashSlots || !c->snap[slot].valid) return ARBOR_ERR_INVALID_ARG;
+  Snapshot &sn = c->snap[slot];
+  const size_t MN = c->max_nodes, PT = MN * c->max_pages_node;
+  wait_side(c);
+  auto cp = [&](void *dst, const void *src, size_t b) {
+    return cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToDevice, c->ms);
+  };
+  CK(cp(c->d.n, sn.n, MN * 4)); CK(cp(c->d.kcur, sn.kcur, MN * 4)); CK(cp(c->d.npages, sn.npages, MN * 4));
+  CK(cp(c->d.ptab, sn.ptab, PT * 4)); CK(cp(c->d.free_stack, sn.free_stack, c->NP * 4));
+  CK(cp(c->d.mclose, sn.mclose, MN * 8)); CK(cp(c->d.s, sn.s, MN * 4)); CK(cp(c->d.ctrl, sn.ctrl, sizeof(Ctrl)));
+  c->h_n = sn.h_n; c->h_open = sn.h_open; c->h_span = sn.h_span; c->h_nq = sn.h_nq;
+  c->num_known = sn.num_known;
+  c->tree_valid = false;
+  return ARBOR_OK;
+}
+
+int64_t arbor_launch_count(const arbor_ctx *c) { return c ? c->launches : 0; }
+
+arbor_status arbor_stage_times(arbor_ctx *c, float *ms) {
+  if (!c || !ms) return ARBOR_ERR_INVALID_ARG;
+  TRY(sync_all(c));
+  for (int i = 0; i < ARBOR_NUM_STAGES; ++i) {
+    ms[i] = 0.f;
+    if (c->st_used[i]) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, c->st_ev[i][0], c->st_ev[i][1]) == cudaSuccess) ms[i] = t;
+    }
+  }
+  return ARBOR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,110 @@
+// tile.cuh — paged K/V tile staging shared by the attention and score kernels.
+#pragma once
+#include "common.cuh"
+
+namespace arbor {
+
+template <typename T> struct ElemT;
+template <> struct ElemT<float> {
+  static constexpr int kPer16 = 4;
+  __device__ __forceinline__ static void cvt16(const uint4 &r, float *f) {
+    f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
+    f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
+  }
+  __device__ __forceinline__ static float2 ld2(const float *p) {
+    return *reinterpret_cast<const float2 *>(p);
+  }
+  __device__ __forceinline__ static float to_f(float x) { return x; }
+  __device__ __forceinline__ static float from_f(float x) { return x; }
+};
+template <> struct ElemT<__nv_bfloat16> {
+  static constexpr int kPer16 = 8;
+  __device__ __forceinline__ static float2 b2f(uint32_t u) {
+    // bf16 → f32 is a 16-bit shift: exact
+    return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+  }
+  __device__ __forceinline__ static void cvt16(const uint4 &r, float *f) {
+    float2 a = b2f(r.x), b = b2f(r.y), c = b2f(r.z), d = b2f(r.w);
+    f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y; f[4] = c.x; f[5] = c.y; f[6] = d.x; f[7] = d.y;
+  }
+  __device__ __forceinline__ static float2 ld2(const __nv_bfloat16 *p) {
+    return b2f(*reinterpret_cast<const uint32_t *>(p));
+  }
+  __device__ __forceinline__ static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+  __device__ __forceinline__ static __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// Row index of (layer l, page, kv head h, slot offset) in a [L][NP][H][P] pool.
+__device__ __forceinline__ int64_t pool_row(const PoolView &g, int l, int page, int h, int off) {
+  return ((static_cast<int64_t>(l) * g.NP + page) * g.H + h) * g.P + off;
+}
+
+// Stage nt rows (slots c0..c0+nt-1 of `node`) of K (16-byte chunks XOR-swizzled by row&7 so
+// that a thread-per-row read is bank-conflict free) and optionally V (plain) into smem with
+// cp.async.  rowoff[r] receives the pool row index (also the pos-pool index).
+template <typename T, int D, bool kWithV>
+__device__ __forceinline__ void stage_tile(T *Ks, T *Vs, int64_t *rowoff, const T *kpool,
+                                           const T *vpool, const int32_t *ptab_node, int c0,
+                                           int nt, const PoolView &g, int l, int h) {
+  constexpr int CPR = D * static_cast<int>(sizeof(T)) / 16;
+  for (int r = threadIdx.x; r < nt; r += blockDim.x) {
+    const int slot = c0 + r;
+    rowoff[r] = pool_row(g, l, ptab_node[slot / g.P], h, slot % g.P);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nt * CPR; idx += blockDim.x) {
+    const int r = idx / CPR, cc = idx - r * CPR;
+    const char *srck = reinterpret_cast<const char *>(kpool + rowoff[r] * D) + cc * 16;
+    cp_async16(reinterpret_cast<char *>(Ks + r * D) + ((cc ^ (r & 7)) * 16), srck);
+    if (kWithV) {
+      const char *srcv = reinterpret_cast<const char *>(vpool + rowoff[r] * D) + cc * 16;
+      cp_async16(reinterpret_cast<char *>(Vs + r * D) + cc * 16, srcv);
+    }
+  }
+  cp_async_commit();
+}
+
+// Dot products of the thread's K row (row t of the swizzled tile) with nq ≤ QB query rows
+// held in smem as f32 [QB][D]; acc[qi] = q_qi · k_t.
+template <typename T, int D, int QB>
+__device__ __forceinline__ void row_dots(const T *Ks, const float *qs, int t, int nq,
+                                         float (&acc)[QB]) {
+  constexpr int EPV = ElemT<T>::kPer16;
+  constexpr int CPR = D / EPV;
+#pragma unroll
+  for (int qi = 0; qi < QB; ++qi) acc[qi] = 0.f;
+#pragma unroll 4
+  for (int cc = 0; cc < CPR; ++cc) {
+    const uint4 raw = *reinterpret_cast<const uint4 *>(
+        reinterpret_cast<const char *>(Ks + t * D) + ((cc ^ (t & 7)) * 16));
+    float kf[EPV];
+    ElemT<T>::cvt16(raw, kf);
+#pragma unroll
+    for (int qi = 0; qi < QB; ++qi) {
+      if (qi < nq) {
+        const float4 *qp = reinterpret_cast<const float4 *>(qs + qi * D + cc * EPV);
+#pragma unroll
+        for (int v4 = 0; v4 < EPV / 4; ++v4) {
+          const float4 qq = qp[v4];
+          float a = acc[qi];
+          a = fmaf(kf[4 * v4 + 0], qq.x, a);
+          a = fmaf(kf[4 * v4 + 1], qq.y, a);
+          a = fmaf(kf[4 * v4 + 2], qq.z, a);
+          a = fmaf(kf[4 * v4 + 3], qq.w, a);
+          acc[qi] = a;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace arbor

@@ -1,0 +1,169 @@
+"""Synthetic ToT / DPTS workloads driven through libarbor (BASELINE.json configs).
+
+Presets C1–C5 concretise BASELINE.json ``configs`` (the paper's Config-S/L shapes,
+PAPER.md §5.1, on Llama-3.1-8B / Qwen2.5-32B-shaped KV).  Inputs are seeded and
+synthetic (``synth``); every step runs in the library's kernels.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+import synth
+from .arbor import ArborKV, make_params
+
+PRESETS = {
+    # configs[0]: tiny tree, depth 3 branching 2, 32 tokens/node, 1 layer, 2 KV heads, d 64, fp32
+    "c1": dict(tree=("full", 3, 2, 32), L=1, H=2, Hq=2, d=64, dtype="f32", P=8, rho=0.5,
+               params=dict(k_min=2, l_tail=2, r_min=0.0, eta=1.0), active="node3"),
+    # configs[1]: Llama-3.1-8B-shaped KV, ToT depth 4 width 5, 25% budget
+    "c2": dict(tree=("full", 4, 5, 128), L=32, H=8, Hq=32, d=128, dtype="bf16", P=16, rho=0.25,
+               params={}, active="highest_v"),
+    # configs[2]: DPTS frontier, 16 active branches on 8B-shaped KV, 50% budget
+    "c3": dict(tree=("full", 4, 5, 128), L=32, H=8, Hq=32, d=128, dtype="bf16", P=16, rho=0.5,
+               params={}, active="dpts16"),
+    # configs[3]: Qwen2.5-32B-shaped GQA KV, deep tree (depth 8, width 4), 25% budget
+    "c4": dict(tree=("search", 256, 4, 8, 128), L=64, H=8, Hq=40, d=128, dtype="bf16", P=16,
+               rho=0.25, params={}, active="highest_v"),
+    # configs[4]: budget sweep on 8B-shaped trees up to 64k tokens
+    "c5": dict(tree=("search", 512, 3, 8, 128), L=32, H=8, Hq=32, d=128, dtype="bf16", P=16,
+               rho=0.25, params={}, active="highest_v"),
+}
+
+
+def build_tree(preset: dict, seed: int = 0):
+    kind = preset["tree"]
+    if kind[0] == "full":
+        t = synth.full_tree(kind[1], kind[2], kind[3], seed)
+    else:
+        t = synth.search_tree(kind[1], kind[2], kind[3], kind[4], seed)
+    act = preset["active"]
+    if act == "node3":
+        t.active = [3]
+    elif act == "highest_v":
+        t.active = [synth.highest_v_leaf(t)]
+    elif act == "dpts16":
+        t.active = synth.dpts_initial_leaves(t, 16, seed)
+    return t
+
+
+def preset_params(preset: dict, **over):
+    d = dict(preset["params"])
+    d.update(over)
+    return make_params(**d)
+
+
+def make_context(preset: dict, tree, *, extra_tokens=0, extra_nodes=0, max_active=16,
+                 params=None, layer_begin=0, layer_count=None, kv_head_begin=0,
+                 kv_head_count=None, rank=0, world_size=1, nccl_id=None, profile=False,
+                 page_margin=64) -> ArborKV:
+    P = preset["P"]
+    n = np.asarray(tree.span_len, np.int64)
+    max_node = int(max(n.max(), 1))
+    pages = int(sum(-(-int(x) // P) for x in n)) + -(-extra_tokens // P) + extra_nodes + page_margin
+    max_tokens = int(tree.end_position() + extra_tokens + 8)
+    return ArborKV(num_layers=preset["L"], num_kv_heads=preset["H"], num_q_heads=preset["Hq"],
+                   head_dim=preset["d"], dtype=preset["dtype"], page_size=P, num_pages=pages,
+                   max_nodes=tree.num_nodes + extra_nodes + 1,
+                   max_node_tokens=max(max_node, 1) + max(extra_tokens, 0) + 1,
+                   max_active=max_active, max_tokens=max_tokens,
+                   params=params if params is not None else preset_params(preset),
+                   layer_begin=layer_begin, layer_count=layer_count, kv_head_begin=kv_head_begin,
+                   kv_head_count=kv_head_count, rank=rank, world_size=world_size, nccl_id=nccl_id,
+                   profile=profile)
+
+
+def load_tree(ctx: ArborKV, tree, K, V):
+    """Open, fill and close every node of a snapshot (prefill of the tree's KV).
+    K, V: device [L][H][T][d] by absolute position (this rank's shard)."""
+    for i in range(tree.num_nodes):
+        a, n = int(tree.span_start[i]), int(tree.span_len[i])
+        ctx.arbor_open_node(i, a)
+        if n > 0:
+            ctx.arbor_append_kv(i, K[:, :, a:a + n].contiguous(), V[:, :, a:a + n].contiguous())
+        if not tree.is_open[i]:
+            ctx.arbor_close_node(i)
+
+
+def decode_step(ctx: ArborKV, tree, q, out=None, lse=None):
+    """One decode step for the active leaves: tree decode attention (a9) then score (a2/a3)."""
+    import torch
+    nA = len(tree.active)
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((nA, ctx.L, ctx.Hq), dtype=torch.float32, device=q.device)
+    ctx.arbor_tree_decode_attn(tree, q, out, lse)
+    ctx.arbor_score(tree, q, lse)
+    return out, lse
+
+
+def leaf_cycle_order(tree, seed: int):
+    leaves = synth.leaves_of(tree)
+    rng = np.random.default_rng(seed + 31337)
+    return [int(x) for x in rng.permutation(leaves)]
+
+
+def query_seed(seed: int, step: int) -> int:
+    return seed * 1000003 + step
+
+
+@dataclass
+class Scenario:
+    preset: dict
+    tree: object
+    ctx: ArborKV
+    K: object
+    V: object
+    E: object
+    seed: int
+    steps: int = 0
+
+    @property
+    def budget(self) -> int:
+        return int(math.floor(self.preset["rho"] * self.tree.total_tokens))
+
+    def queries(self, step: int, n_active: int):
+        p = self.preset
+        return synth.make_queries(n_active, self.ctx.L, self.ctx.Hq, p["d"], p["dtype"],
+                                  query_seed(self.seed, step), self.E_local, device=self.ctx.device)
+
+    @property
+    def E_local(self):
+        return self.E
+
+
+def setup(preset_name: str, seed: int = 0, *, kv_head_begin=0, kv_head_count=None, rank=0,
+          world_size=1, nccl_id=None, profile=False, extra_tokens=0, extra_nodes=0,
+          params=None, max_active=16, device="cuda") -> Scenario:
+    """Build the preset's tree, its seeded K/V (on the device), a context, and prefill it."""
+    preset = PRESETS[preset_name]
+    tree = build_tree(preset, seed)
+    H = preset["H"]
+    hc = kv_head_count if kv_head_count is not None else H
+    K, V, E = synth.make_kv(preset["L"], H, tree.total_tokens, preset["d"], preset["dtype"], seed,
+                            tree.span_start, tree.span_len, device=device)
+    K = K[:, kv_head_begin:kv_head_begin + hc].contiguous()
+    V = V[:, kv_head_begin:kv_head_begin + hc].contiguous()
+    E = E[:, kv_head_begin:kv_head_begin + hc].contiguous()
+    ctx = make_context(preset, tree, extra_tokens=extra_tokens, extra_nodes=extra_nodes,
+                       max_active=max_active, params=params, kv_head_begin=kv_head_begin,
+                       kv_head_count=hc, rank=rank, world_size=world_size, nccl_id=nccl_id,
+                       profile=profile)
+    load_tree(ctx, tree, K, V)
+    return Scenario(preset, tree, ctx, K, V, E, seed)
+
+
+def warmup_leaf_cycling(sc: Scenario, steps_per_leaf: int = 4):
+    """§8(c).1 item 10: every leaf is the sole active leaf for ``steps_per_leaf`` decode
+    steps, in a seeded order, so every node accumulates mass from its own subtree."""
+    saved = list(sc.tree.active)
+    for leaf in leaf_cycle_order(sc.tree, sc.seed):
+        sc.tree.active = [leaf]
+        for _ in range(steps_per_leaf):
+            q = sc.queries(sc.steps, 1)
+            decode_step(sc.ctx, sc.tree, q)
+            sc.steps += 1
+    sc.tree.active = saved
