@@ -1,0 +1,513 @@
+#!/usr/bin/env python
+"""ArborKV per-step KV-eviction benchmark on B200 (BASELINE.json metric).
+
+A step is one pass of the whole hot path over the workload:
+  a9 tree decode attention (→ LSE) → a2 score accumulation → a3 node mass + MSVE
+  (→ a10 NCCL all-reduce when N > 1) → a1 geometry (the active leaf changes every step) →
+  a4 TAE allocation → a5+a6 select + compact,
+on configs[1] (C2: Llama-3.1-8B-shaped KV, ToT depth 4 × width 5, 19,968 cached tokens,
+ρ = 0.25) by default.  Each step starts from the same full-retention state (restored
+outside the timed region with device copies of the pools, A and the library state), so
+`value` = cached tokens evicted-over per second of device time.  Rehydration (a7/a8,
+PCIe-bound) is measured separately and reported under "rehydrate".
+
+  python bench.py [--gpus N --steps K --warmup W --config c2 --impl arbor|reference]
+Multi-GPU: launched by torchrun, one rank per GPU, KV heads sharded across ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "eviction tokens/s; tree decode-attn HBM GB/s vs ~8 TB/s peak; 1/2/4/8 GPUs"
+NOMINAL_HBM = 8000.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- distributed
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (oracle/), as it stands, on the host cores, on a
+    bounded sample of the same workload (one layer's KV heads), same metric."""
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            return
+    res = cpu_oracle_sample(args.config, args.seed, args.warmup, args.steps)
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": res["ms_per_step_full"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args.config, ws),
+            "cpu_baseline": {"value": res["value"], "unit": "tokens/s", "cores": res["cores"],
+                             "kind": "oracle", "sample": res["sample"]},
+            "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def workload_config(name, ws):
+    from paper_2605_22106_b200.workload import PRESETS
+    p = PRESETS[name]
+    t = p["tree"]
+    desc = {"c1": "C1 tiny tree (configs[0])", "c2": "C2 Llama-3.1-8B-shaped ToT depth4 x width5 (configs[1])",
+            "c3": "C3 DPTS frontier 16 branches (configs[2])",
+            "c4": "C4 Qwen2.5-32B-shaped deep tree (configs[3])",
+            "c5": "C5 8B-shaped 64k-token tree (configs[4])"}[name]
+    return {"workload": desc, "tree": f"{t[0]}_tree{tuple(t[1:])}", "layers": p["L"],
+            "kv_heads": p["H"], "q_heads": p["Hq"], "head_dim": p["d"], "kv_dtype": p["dtype"],
+            "page_size": p["P"], "rho": p["rho"],
+            "parallelism": f"kv-head shards x{ws}" if ws > 1 else "single GPU",
+            "l2": "inputs > L2 (KV pools >> 126 MB) and a pool-restore copy between steps"}
+
+
+# ---------------------------------------------------------------- CPU oracle sample
+def cpu_oracle_sample(config, seed, warmup, steps, target_s=12.0):
+    """Time the oracle (as it stands) on a bounded sample: the full tree and node-level
+    allocation, but only the rows (l, h) of layer 0 for score / mass / evict / attention.
+    Scaled to the full workload by the row ratio (per-row work is independent)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            return _cpu_oracle_sample(config, seed, warmup, steps, target_s)
+    except ImportError:
+        return _cpu_oracle_sample(config, seed, warmup, steps, target_s)
+
+
+def _cpu_oracle_sample(config, seed, warmup, steps, target_s):
+    import synth
+    from oracle.state import ArborOracle, default_params
+    from paper_2605_22106_b200 import workload
+    p = workload.PRESETS[config]
+    tree = workload.build_tree(p, seed)
+    T = tree.total_tokens
+    K, V, E = synth.make_kv(1, p["H"], T, p["d"], p["dtype"], seed, tree.span_start, tree.span_len)
+    op = default_params(**p["params"])
+    rows_total = p["L"] * p["H"]
+    rows_sample = p["H"]
+    orc = ArborOracle(K.double().numpy(), V.double().numpy(), p["Hq"], p["P"],
+                      sum(-(-int(x) // p["P"]) for x in tree.span_len) + 64, op,
+                      num_layers_global=p["L"], num_q_heads_global=p["Hq"])
+    for i in range(tree.num_nodes):
+        orc.open_node(i, int(tree.span_start[i]))
+        orc.append(i, int(tree.span_len[i]))
+        orc.close_node(i)
+    leaves = sorted(synth.leaves_of(tree), key=lambda x: -float(tree.v[x]))[:2]
+    # a short leaf-cycling warm-up on the sample so A is not all zero
+    for j, leaf in enumerate(workload.leaf_cycle_order(tree, seed)[:16]):
+        tree.active = [leaf]
+        q = synth.make_queries(1, 1, p["Hq"], p["d"], p["dtype"], j, E).double().numpy()
+        orc.score_accumulate(tree, q)
+    B = int(math.floor(p["rho"] * T))
+    import copy
+    base = copy.deepcopy(orc)
+    times = []
+    t_start = time.perf_counter()
+    nsteps = max(1, warmup + steps)
+    for i in range(nsteps):
+        o = copy.deepcopy(base)
+        tree.active = [leaves[i % 2]]
+        q = synth.make_queries(1, 1, p["Hq"], p["d"], p["dtype"], 10_000 + i, E).double().numpy()
+        t0 = time.perf_counter()
+        _, lse = o.decode(tree, q)
+        o.score_accumulate(tree, q, lse)
+        a, s = o.msve(tree)
+        k = o.allocate(tree, s, B)
+        o.evict(tree, k)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+        if time.perf_counter() - t_start > target_s and len(times) >= 1:
+            break
+    t_step = statistics.median(times)
+    t_full = t_step * rows_total / rows_sample
+    return {"value": T / t_full, "ms_per_step_full": t_full * 1e3, "cores": 1,
+            "sample": f"{config}: full tree ({tree.num_nodes} nodes, {T} tokens), rows of layer 0 "
+                      f"only ({rows_sample} of {rows_total} (layer, KV-head) rows); one step = "
+                      f"decode attention + score + mass/MSVE + allocate + evict; median of "
+                      f"{len(times)} steps ({t_step:.2f} s each), scaled x{rows_total // rows_sample} "
+                      f"to all rows; numpy/BLAS limited to 1 thread"}
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="arbor", choices=["arbor", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="just run N steps (for ncu launch lists); no JSON")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    from paper_2605_22106_b200 import workload
+    from paper_2605_22106_b200.arbor import nccl_unique_id
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        pg = dist
+    preset = workload.PRESETS[args.config]
+    H = preset["H"]
+    if H % ws:
+        raise SystemExit(f"{H} KV heads do not split over {ws} GPUs")
+    hc = H // ws
+    nid = None
+    if ws > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        pg.broadcast(buf, 0)
+        nid = bytes(buf.cpu().numpy().tobytes())
+
+    sc = workload.setup(args.config, args.seed, kv_head_begin=rank * hc, kv_head_count=hc,
+                        rank=rank, world_size=ws, nccl_id=nid, profile=True, device=dev)
+    ctx, tree = sc.ctx, sc.tree
+    workload.warmup_leaf_cycling(sc)
+    import synth
+    leaves = sorted(synth.leaves_of(tree), key=lambda x: -float(tree.v[x]))[:2]
+    B = sc.budget
+    N = tree.num_nodes
+    nA = 1
+    qs = [sc.queries(10_000 + i, nA) for i in range(2)]
+    out = torch.empty_like(qs[0])
+    lse = torch.empty((nA, ctx.L, ctx.Hq), dtype=torch.float32, device=dev)
+    s_buf = torch.empty(N, dtype=torch.float32, device=dev)
+    k_buf = torch.empty(N, dtype=torch.int32, device=dev)
+    # full-retention snapshot (restored between steps, outside the timed region)
+    snap_k, snap_v = ctx.k_pool.clone(), ctx.v_pool.clone()
+    snap_pos, snap_A = ctx.pos_pool.clone(), ctx.score.clone()
+    ctx.arbor_save_state(0)
+    cached = int(np.asarray(tree.span_len).sum())
+    trees = []
+    from paper_2605_22106_b200.arbor import TreeArgs
+    for leaf in leaves:
+        tree.active = [leaf]
+        trees.append(TreeArgs.from_tree(tree))
+    stream = torch.cuda.current_stream(dev)
+
+    def restore():
+        ctx.k_pool.copy_(snap_k)
+        ctx.v_pool.copy_(snap_v)
+        ctx.pos_pool.copy_(snap_pos)
+        ctx.score.copy_(snap_A)
+        ctx.arbor_load_state(0)
+
+    def step(i):
+        ta = trees[i % 2]
+        q = qs[i % 2]
+        ctx.arbor_tree_decode_attn(ta, q, out, lse)
+        ctx.arbor_score(ta, q, lse, s_buf)
+        ctx.arbor_allocate(ta, s_buf, B, k_buf)
+        ctx.arbor_evict(ta, k_buf)
+
+    if args.profile_steps:
+        # for ncu: --nvtx --nvtx-include "bench_step/" selects exactly the step's kernels
+        for i in range(args.profile_steps):
+            restore()
+            torch.cuda.synchronize()
+            torch.cuda.nvtx.range_push("bench_step")
+            step(i)
+            torch.cuda.synchronize()
+            torch.cuda.nvtx.range_pop()
+        return
+
+    for i in range(max(3, args.warmup)):
+        restore()
+        step(i)
+    torch.cuda.synchronize()
+    ctx.arbor_sync()
+
+    # ---------------- timed region: K steps, each bracketed by CUDA events
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    stage_ms = {k: [] for k in ("attn", "attn_merge", "score_accum", "node_mass", "msve",
+                                "allreduce", "geometry", "allocate", "evict_plan",
+                                "select_compact")}
+    launches = 0
+    clocks = ClockSampler(local)
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.2)
+    for i in range(args.steps):
+        restore()
+        l0 = ctx.arbor_launch_count()
+        ev[i][0].record(stream)
+        step(i)
+        ev[i][1].record(stream)
+        launches += ctx.arbor_launch_count() - l0
+        st = ctx.arbor_stage_times()           # syncs; outside the events
+        for k in stage_ms:
+            stage_ms[k].append(st[k])
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if pg is not None:
+        pg.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    if pg is not None:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = cached * args.steps / (tot_ms / 1e3)
+
+    # ---------------- algorithmic bytes for the roofline, from the
+    # device state after one step from full retention (per active leaf)
+    def alg_bytes(i):
+        restore()
+        step(i)
+        torch.cuda.synchronize()
+        rb = ctx.D * (2 if preset["dtype"] == "bf16" else 4)
+        L, Hh, P = ctx.L, ctx.H, ctx.P
+        byts = {"select_compact": 0, "moved_rows": 0}
+        for j in range(N):
+            kc, n, pages = ctx.arbor_read_node(j)
+            if kc == n:
+                continue
+            idx = torch.as_tensor(pages, device=dev, dtype=torch.long)
+            pos = ctx.pos_pool[:, idx].permute(0, 2, 1, 3).reshape(L, Hh, -1)[:, :, :kc]
+            moved = int((pos.long() != torch.arange(kc, device=dev)).sum().item())
+            # per (row, changed node): A + pos reads of the k_cur candidates (4 + 2 B each);
+            # per moved row: K and V read + write (4·rb) and its pos write (2 B)
+            byts["select_compact"] += L * Hh * 6 * n + moved * (4 * rb + 2)
+            byts["moved_rows"] += moved
+        vis = 0
+        for x in synth_path(tree.parent, leaves[i % 2]):
+            vis += int(tree.span_len[x])
+        rows = L * Hh
+        byts["attn"] = rows * vis * 2 * rb + nA * ctx.Hq * L * ctx.D * 2 * rb // ctx.D
+        byts["score_accum"] = rows * vis * (rb + 8)
+        byts["node_mass"] = rows * cached * 4
+        return byts
+
+    ab = [alg_bytes(0), alg_bytes(1)]
+    peak, peak_src = peaks()
+
+    def kstat(name, bytes_fn):
+        t_ms = []
+        for i, x in enumerate(stage_ms[name]):
+            t_ms.append(x)
+        avg = statistics.mean(t_ms) if t_ms else float("nan")
+        b = statistics.mean(bytes_fn(i) for i in range(2))
+        gbs = b / (avg / 1e3) / 1e9 if avg > 0 else float("nan")
+        return {"ms": avg, "bytes": b, "GBps": gbs, "frac_measured": gbs / peak,
+                "frac_nominal": gbs / NOMINAL_HBM}
+
+    kernels = {
+        "select_compact": kstat("select_compact", lambda i: ab[i]["select_compact"]),
+        "attn_partial": kstat("attn", lambda i: ab[i]["attn"]),
+        "score_accum": kstat("score_accum", lambda i: ab[i]["score_accum"]),
+        "node_mass": kstat("node_mass", lambda i: ab[i]["node_mass"]),
+    }
+    top = kernels["select_compact"]
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_select_compact_ncu.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            if pj.get("config") == args.config:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"kernel": "select_compact (a5+a6)", "bound": "hbm", "achieved": top["GBps"],
+                "peak": peak, "unit": "GB/s", "frac": top["GBps"] / peak,
+                "frac_of_nominal_8TBps": top["GBps"] / NOMINAL_HBM, "traffic": traffic,
+                "peak_source": peak_src, "alg_bytes_per_launch": top["bytes"],
+                "ms_per_launch": top["ms"]}
+
+    # ---------------- e2e: host buffers through the public API (pinned H2D q, D2H k, s)
+    q_host = [q.cpu().pin_memory() for q in qs]
+    k_host = torch.empty(N, dtype=torch.int32).pin_memory()
+    s_host = torch.empty(N, dtype=torch.float32).pin_memory()
+    q_dev = torch.empty_like(qs[0])
+    e2e_ms = []
+    for i in range(args.steps):
+        restore()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        q_dev.copy_(q_host[i % 2], non_blocking=True)
+        ta = trees[i % 2]
+        ctx.arbor_tree_decode_attn(ta, q_dev, out, lse)
+        ctx.arbor_score(ta, q_dev, lse, s_buf)
+        ctx.arbor_allocate(ta, s_buf, B, k_buf)
+        ctx.arbor_evict(ta, k_buf)
+        k_host.copy_(k_buf, non_blocking=True)
+        s_host.copy_(s_buf, non_blocking=True)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_tot = sum(e2e_ms)
+    if pg is not None:
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_tot = float(t.item())
+    e2e = {"value": cached * args.steps / (e2e_tot / 1e3), "unit": "tokens/s",
+           "h2d_bytes_per_step": int(qs[0].numel() * qs[0].element_size()),
+           "d2h_bytes_per_step": int(N * 8)}
+
+    # ---------------- rehydration (a7/a8): backtrack into the evicted subtree
+    rehyd = None
+    try:
+        restore()
+        step(0)
+        other = [x for x in synth.leaves_of(tree) if x not in leaves]
+        tree.active = [other[len(other) // 2]]
+        ta = TreeArgs.from_tree(tree)
+        path = synth_path(tree.parent, tree.active[0])
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0 = ctx.arbor_read_counters()[0]
+        torch.cuda.synchronize()
+        a.record(stream)
+        ctx.arbor_rehydrate(ta, path)
+        b.record(stream)
+        b.synchronize()
+        r1 = ctx.arbor_read_counters()[0]
+        nbytes = sum(int(tree.span_len[x]) for x in path) * ctx.L * ctx.H * ctx.D * 2 * (
+            2 if preset["dtype"] == "bf16" else 4)
+        ms = a.elapsed_time(b)
+        rehyd = {"nodes_rehydrated": int(r1 - r0), "ms": ms,
+                 "bytes_upper_bound": nbytes,
+                 "PCIe_GBps_upper_bound": nbytes / (ms / 1e3) / 1e9 if ms > 0 else None}
+    except Exception as e:  # pragma: no cover
+        rehyd = {"error": str(e)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = cpu_oracle_sample(args.config, args.seed, 0, 3)
+        cpu = {"value": r["value"], "unit": "tokens/s", "cores": r["cores"], "kind": "oracle",
+               "sample": r["sample"]}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": preset["dtype"], "data": "synthetic",
+                "config": dict(workload_config(args.config, ws), cached_tokens=cached, budget=B,
+                               nodes=N, step="a9 attn + a2 score + a3 mass/MSVE + a1 geometry + "
+                                            "a4 allocate + a5/a6 select+compact (+a10 all-reduce)"),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+                "clocks": clk, "kernels": kernels,
+                "stage_ms_median": {k: statistics.median(v) for k, v in stage_ms.items() if v},
+                "step_ms_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
+                "rehydrate": rehyd,
+                "decode_attn": {"GBps": kernels["attn_partial"]["GBps"],
+                                "frac_measured": kernels["attn_partial"]["frac_measured"],
+                                "frac_nominal": kernels["attn_partial"]["frac_nominal"]}}
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+def synth_path(parent, leaf):
+    out = []
+    x = int(leaf)
+    while x >= 0:
+        out.append(x)
+        x = int(parent[x])
+    return out[::-1]
+
+
+if __name__ == "__main__":
+    main()

@@ -115,10 +115,11 @@ class Scenario:
     preset: dict
     tree: object
     ctx: ArborKV
-    K: object
+    K: object          # this rank's shard [L][H_local][T][d]
     V: object
-    E: object
-    seed: int
+    E_full: object     # [L][H][d] directions of ALL heads (queries are drawn for all heads
+    seed: int          # and sliced, so every world size sees identical inputs)
+    kv_head_begin: int = 0
     steps: int = 0
 
     @property
@@ -127,12 +128,11 @@ class Scenario:
 
     def queries(self, step: int, n_active: int):
         p = self.preset
-        return synth.make_queries(n_active, self.ctx.L, self.ctx.Hq, p["d"], p["dtype"],
-                                  query_seed(self.seed, step), self.E_local, device=self.ctx.device)
-
-    @property
-    def E_local(self):
-        return self.E
+        q = synth.make_queries(n_active, p["L"], p["Hq"], p["d"], p["dtype"],
+                               query_seed(self.seed, step), self.E_full, device=self.ctx.device)
+        G = self.ctx.G
+        h0 = self.kv_head_begin
+        return q[:, :, h0 * G:(h0 + self.ctx.H) * G].contiguous()
 
 
 def setup(preset_name: str, seed: int = 0, *, kv_head_begin=0, kv_head_count=None, rank=0,
@@ -145,15 +145,15 @@ def setup(preset_name: str, seed: int = 0, *, kv_head_begin=0, kv_head_count=Non
     hc = kv_head_count if kv_head_count is not None else H
     K, V, E = synth.make_kv(preset["L"], H, tree.total_tokens, preset["d"], preset["dtype"], seed,
                             tree.span_start, tree.span_len, device=device)
-    K = K[:, kv_head_begin:kv_head_begin + hc].contiguous()
-    V = V[:, kv_head_begin:kv_head_begin + hc].contiguous()
-    E = E[:, kv_head_begin:kv_head_begin + hc].contiguous()
+    if hc != H:
+        K = K[:, kv_head_begin:kv_head_begin + hc].contiguous()
+        V = V[:, kv_head_begin:kv_head_begin + hc].contiguous()
     ctx = make_context(preset, tree, extra_tokens=extra_tokens, extra_nodes=extra_nodes,
                        max_active=max_active, params=params, kv_head_begin=kv_head_begin,
                        kv_head_count=hc, rank=rank, world_size=world_size, nccl_id=nccl_id,
                        profile=profile)
     load_tree(ctx, tree, K, V)
-    return Scenario(preset, tree, ctx, K, V, E, seed)
+    return Scenario(preset, tree, ctx, K, V, E, seed, kv_head_begin)
 
 
 def warmup_leaf_cycling(sc: Scenario, steps_per_leaf: int = 4):
