@@ -62,6 +62,12 @@ __device__ T block_sum(T v, T *red) {
   return tot;
 }
 
+__device__ __forceinline__ long long warp_sum64(long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // floor(X / den) and X mod den for 0 ≤ X < 2^126, 0 < den < 2^62, with a small quotient
 __device__ __forceinline__ void divmod128(unsigned __int128 X, unsigned long long den,
                                           unsigned long long &q, unsigned long long &r) {
@@ -226,20 +232,23 @@ allocate_kernel(AllocArgs a) {
       // keeps its largest feasible candidate, then a block max over rationals
       long long my_num = 0, my_den = 1;
       int my_set = 0;
-      for (int c = threadIdx.x; c < 2 * N; c += blockDim.x) {
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int c = wid; c < 2 * N; c += nw) {   // one warp per candidate, lanes over nodes
         const int j = c >> 1;
         if (cls[j] != 1) continue;
         const long long cden = (c & 1) ? f[j] : nn[j];
         if (cden <= 0) continue;
         const long long cnum = W[j];
         long long SA = 0, Sb = 0;
-        for (int i = 0; i < N; ++i) {
+        for (int i = lane; i < N; i += 32) {
           if (cls[i] != 1) continue;
           const long long Wd = W[i] * cden;                      // < 2^55
           if (Wd >= static_cast<long long>(nn[i]) * cnum) Sb += nn[i];          // capped at β
           else if (f[i] > 0 && Wd <= static_cast<long long>(f[i]) * cnum) Sb += f[i];  // floored
           else SA += W[i];
         }
+        SA = warp_sum64(SA);
+        Sb = warp_sum64(Sb);
         // S(β) ≥ 𝓑''  ⇔  SA·den ≥ (𝓑'' − Sb)·num
         const __int128 lhs = static_cast<__int128>(SA) * cden;
         const __int128 rhs = static_cast<__int128>(Bpp - Sb) * cnum;
@@ -304,15 +313,17 @@ allocate_kernel(AllocArgs a) {
       }
       given = block_sum(given, red64);
       const long long leftover = Num - given;
-      for (int j = threadIdx.x; j < N; j += blockDim.x) {
-        if (cls[j] != 6 || leftover <= 0) continue;
-        long long rank = 0;
-        for (int i = 0; i < N; ++i) {
-          if (cls[i] != 6) continue;
-          if (rem[i] > rem[j] || (rem[i] == rem[j] && (W[i] > W[j] || (W[i] == W[j] && i < j))))
-            ++rank;
+      __syncthreads();
+      for (int j = wid; j < N && leftover > 0; j += nw) {   // warp per node, lanes over nodes
+        if (cls[j] != 6) continue;
+        int rank = 0;
+        for (int i0 = 0; i0 < N; i0 += 32) {
+          const int i = i0 + lane;
+          const bool gt = i < N && cls[i] == 6 &&
+                          (rem[i] > rem[j] || (rem[i] == rem[j] && (W[i] > W[j] || (W[i] == W[j] && i < j))));
+          rank += __popc(__ballot_sync(0xffffffffu, gt));
         }
-        if (rank < leftover) k[j] += 1;
+        if (lane == 0 && rank < leftover) k[j] += 1;
       }
     }
   }

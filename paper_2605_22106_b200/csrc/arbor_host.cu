@@ -477,7 +477,8 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   if (k.kv_head_begin < 0 || k.kv_head_count < 1 || k.kv_head_begin + k.kv_head_count > k.num_kv_heads)
     return ARBOR_ERR_INVALID_ARG;
   if (k.kv_dtype != ARBOR_F32 && k.kv_dtype != ARBOR_BF16) return ARBOR_ERR_INVALID_ARG;
-  if (k.page_size < 1 || k.page_size > 1024 || k.num_pages < 1) return ARBOR_ERR_INVALID_ARG;
+  if (k.page_size < 1 || k.page_size > 1024 || (k.page_size & (k.page_size - 1)) || k.num_pages < 1)
+    return ARBOR_ERR_INVALID_ARG;   // page size: a power of two (shift addressing)
   if (k.max_nodes < 1 || k.max_nodes > 4096) return ARBOR_ERR_INVALID_ARG;
   if (k.max_node_tokens < 1 || k.max_node_tokens > 32767) return ARBOR_ERR_INVALID_ARG;
   if (k.max_active < 1 || k.max_active > 1024 || k.max_tokens < 1) return ARBOR_ERR_INVALID_ARG;
@@ -657,7 +658,6 @@ arbor_status arbor_close_node(arbor_ctx *c, int32_t node) {
   if (c->h_n[node] < 1) return fail(c, ARBOR_ERR_INVALID_ARG, "closing an empty node");
   // Mclose_i: this rank's partial mass of the node at close (Q5)
   TRY(ring_upload(c, c->d.rehyd_nodes + c->max_nodes, &node, sizeof(int32_t)));
-  CK(cudaMemsetAsync(c->d.mclose + node, 0, sizeof(int64_t), c->ms));
   launch_node_mass(c, c->d.rehyd_nodes + c->max_nodes, 1, c->d.mclose, 1);
   CK_LAUNCH();
   // write-through stash on the side stream (a7), after the node's last append
@@ -704,7 +704,8 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
   launch_score_accum(c, pv, hp.max_lcnt * c->G, q, lse_use, c->L);
   CK_LAUNCH();
   stage_begin(c, ARBOR_ST_NODE_MASS, c->ms);
-  CK(cudaMemsetAsync(c->d.mass2, 0, N * sizeof(int64_t), c->ms));
+  if (closed.size() < static_cast<size_t>(N))   // open nodes have no mass entry
+    CK(cudaMemsetAsync(c->d.mass2, 0, N * sizeof(int64_t), c->ms));
   launch_node_mass(c, d_closed, static_cast<int>(closed.size()), c->d.mass2, 1);
   CK_LAUNCH();
   CK(cudaMemcpyAsync(c->d.mass2 + N, c->d.mclose, N * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->ms));

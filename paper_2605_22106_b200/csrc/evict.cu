@@ -12,12 +12,14 @@
 //  * evict_plan (1 CTA): decides k_app per node, builds the work list of changed non-pinned
 //    nodes in ascending id, truncates page lists to ⌈k_app/P⌉ and pushes the freed pages on
 //    the LIFO free list in ascending (node, list) order — all on the device, no host sync.
-//  * select_compact (persistent grid, one CTA per (node, row) work item): gathers the pos
-//    tags and A keys of the kept slots, ranks the non-tail candidates (unique keys → exact
-//    rank = top-m membership), block-scans the keep mask into new slot indices, then moves
-//    K, V and pos rows in ascending slot order, in place: a kept row's new slot is never
-//    after its old one, and each 32-row chunk is fully read (into registers, 16-byte
-//    coalesced loads) before any of it is written.
+//  * select_compact (persistent grid, one WARP per (node, row) work item, no block
+//    barriers): gathers the pos tags and A keys of the non-tail kept slots, finds the m-th
+//    largest unique 48-bit key ⟨A bits, pos⟩ by a warp radix select (8-bit digits, per-warp
+//    256-bin smem histogram, warp scan) — exact top-m membership in O(c) — warp-scans the keep
+//    mask (ballot/popc) into new slot indices, then moves K, V and pos rows in ascending
+//    slot order, in place: a kept row's new slot is never after its old one, and each chunk
+//    of rows is fully read (16-byte coalesced loads, 8 rows in flight per warp) before any
+//    of it is written.
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -26,7 +28,6 @@ namespace arbor {
 namespace {
 
 constexpr int kPlanThreads = 1024;
-constexpr int kCompactThreads = 128;
 
 struct PlanArgs {
   int N, P, MPN;
@@ -118,6 +119,7 @@ struct CompactArgs {
   int16_t *pos;
   int esize;
   int cap;          // max n over evicted nodes (smem capacity, slots)
+  int lgP;          // log2(page size)
 };
 
 __device__ __forceinline__ int64_t row_of(const CompactArgs &a, const int32_t *pl, int l, int h,
@@ -125,22 +127,36 @@ __device__ __forceinline__ int64_t row_of(const CompactArgs &a, const int32_t *p
   return ((static_cast<int64_t>(l) * a.NP + pl[slot / a.P]) * a.H + h) * a.P + (slot % a.P);
 }
 
-// smem: key (u64) [max_n], pos (i32) [max_n], keep/new slot (i32) [max_n], moves (i32) [max_n]
-__global__ void __launch_bounds__(kCompactThreads)
+constexpr int kWarps = 8;     // warps per CTA; one warp owns one (node, row) work item
+constexpr int kUnroll = 4;    // row-chunks in flight per lane during the move
+
+// Warp-per-item select + compact.  smem per warp: key[cap] (u64), the move list[cap]
+// (u32: src slot | dst slot << 16) and the node's page list[cap / P + 1].
+__global__ void __launch_bounds__(kWarps * 32, 4)
 select_compact_kernel(CompactArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
-  using Scan = cub::BlockScan<int, kCompactThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int s_moves, s_carry;
-  const int items = a.ctrl_ro->work_count * a.R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cap = a.cap;
-  unsigned long long *key = reinterpret_cast<unsigned long long *>(sm);
-  int *pos = reinterpret_cast<int *>(key + cap);
-  int *nslot = pos + cap;
-  int *mv_src = nslot + cap;
+  const int lgP = a.lgP, Pm = (1 << lgP) - 1;
+  const int pcap = (cap >> lgP) + 1;
+  unsigned long long *key = reinterpret_cast<unsigned long long *>(sm) + warp * cap;
+  uint32_t *mlist = reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned long long *>(sm) +
+                                                 kWarps * cap) + warp * cap;
+  int32_t *pgs = reinterpret_cast<int32_t *>(reinterpret_cast<uint32_t *>(
+                     reinterpret_cast<unsigned long long *>(sm) + kWarps * cap) + kWarps * cap) +
+                 warp * pcap;
+  __shared__ uint32_t hist_all[kWarps][256];
+  uint32_t *hist = hist_all[warp];
+  const int items = a.ctrl_ro->work_count * a.R;
   const int rb = a.D * a.esize;          // row bytes
-  const int cpr = rb / 16;               // 16-byte chunks per row
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+  const int cpr = rb >> 4;               // 16-byte pieces per row (≤ 32)
+  const int rpi = 32 / cpr;              // rows per warp instruction
+  const int my_piece = lane % cpr, my_row = lane / cpr;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  char *kp8 = static_cast<char *>(a.kpool);
+  char *vp8 = static_cast<char *>(a.vpool);
+  const int64_t pstride = static_cast<int64_t>(a.H) << lgP;   // rows between consecutive pages
+  for (int it = blockIdx.x * kWarps + warp; it < items; it += gridDim.x * kWarps) {
     const int w = it / a.R, r = it - w * a.R;
     const int l = r / a.H, h = r - l * a.H;
     const int node = a.work_node[w];
@@ -148,102 +164,142 @@ select_compact_kernel(CompactArgs a) {
     const int n = a.n[node];
     const int tl = min(a.l_tail, n);
     const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.MPN;
-    const float *Arow = a.A + (static_cast<int64_t>(l) * a.H + h) * a.max_tokens + a.span[node];
-    // 1. gather pos tags and keys of the kept slots
-    for (int s = threadIdx.x; s < kc; s += blockDim.x) {
-      const int p = a.pos[row_of(a, pl, l, h, s)];
-      pos[s] = p;
-      const float av = Arow[p];
-      if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-      const unsigned bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
-      key[s] = (static_cast<unsigned long long>(bits) << 32) | static_cast<unsigned>(p);
-    }
-    __syncthreads();
-    // 2. keep decision: tail, or top-(ka − tl) non-tail by key (exact rank, keys are unique)
+    const int64_t base = (static_cast<int64_t>(l) * a.NP * a.H + h) << lgP;
+    for (int i = lane; i < ((kc + Pm) >> lgP); i += 32) pgs[i] = pl[i];
+    __syncwarp();
+    auto row = [&](int slot) -> int64_t {
+      return base + static_cast<int64_t>(pgs[slot >> lgP]) * pstride + (slot & Pm);
+    };
+    // 1. candidates: when k_app > |𝒯| the tail (the last |𝒯| slots, all present) is kept and
+    //    the non-tail slots 0..nc-1 compete by key; otherwise the last k_app slots are kept
+    //    (Alg. 1) and no key is needed.
+    const bool ranked = ka > tl;
+    const int nc = ranked ? kc - tl : 0;
     const int m = ka - tl;
-    for (int s = threadIdx.x; s < kc; s += blockDim.x) {
-      int keep;
-      if (ka <= tl) {
-        keep = pos[s] >= n - ka;                       // Alg. 1
-      } else if (pos[s] >= n - tl) {
-        keep = 1;                                      // tail 𝒯_i
+    // threshold: keep a candidate iff (key & tmask) >= tkey — the top m keys (unique)
+    unsigned long long tkey = ~0ull, tmask = ~0ull;
+    if (ranked) {
+      const float *Arow =
+          a.A + (static_cast<int64_t>(l) * a.H + h) * a.max_tokens + a.span[node];
+      for (int s = lane; s < nc; s += 32) {
+        const int p = a.pos[row(s)];
+        const float av = Arow[p];
+        if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+        const unsigned bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
+        key[s] = (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
+      }
+      __syncwarp();
+      if (m <= 0) {
+        tkey = ~0ull;                      // no heavy hitter survives
+      } else if (m >= nc) {
+        tkey = 0; tmask = 0;               // every candidate survives
       } else {
-        const unsigned long long ks = key[s];
-        int rank = 0;
-        for (int i = 0; i < kc; ++i)
-          rank += (pos[i] < n - tl) && (key[i] > ks);
-        keep = rank < m;                               // Top-m_i by A_i(t)
-      }
-      nslot[s] = keep;
-    }
-    __syncthreads();
-    // 3. block scan of the keep mask in slot order → new slot; collect moving rows
-    if (threadIdx.x == 0) { s_carry = 0; s_moves = 0; }
-    __syncthreads();
-    for (int base = 0; base < kc; base += blockDim.x) {
-      const int s = base + threadIdx.x;
-      const int kp = (s < kc) ? nslot[s] : 0;
-      int ex;
-      Scan(tmp).ExclusiveSum(kp, ex);
-      const int carry = s_carry;
-      __syncthreads();
-      if (s < kc) nslot[s] = kp ? (carry + ex) : -1;
-      if (threadIdx.x == blockDim.x - 1) s_carry = carry + ex + kp;
-      __syncthreads();
-    }
-    // moving rows (new slot != old slot), in ascending slot order
-    for (int base = 0; base < kc; base += blockDim.x) {
-      const int s = base + threadIdx.x;
-      const int mvf = (s < kc && nslot[s] >= 0 && nslot[s] != s) ? 1 : 0;
-      int ex;
-      Scan(tmp).ExclusiveSum(mvf, ex);
-      const int carry = s_moves;
-      __syncthreads();
-      if (mvf) mv_src[carry + ex] = s;
-      if (threadIdx.x == blockDim.x - 1) s_moves = carry + ex + mvf;
-      __syncthreads();
-    }
-    const int moves = s_moves;
-    // 4. in-place stable gather, chunks of 32 rows: read all, sync, write all
-    constexpr int kChunkRows = 32;
-    char *kp8 = static_cast<char *>(a.kpool);
-    char *vp8 = static_cast<char *>(a.vpool);
-    for (int c0 = 0; c0 < moves; c0 += kChunkRows) {
-      const int nr = min(kChunkRows, moves - c0);
-      const int pieces = nr * cpr;   // per tensor
-      uint4 bufk[8], bufv[8];       // kChunkRows * cpr / threads ≤ 32*16/128 = 4 (bf16, d=128)
-      int npc = 0;
+        // warp radix select of the m-th largest 48-bit key, 8-bit digits MSB first
+        unsigned long long prefix = 0, pmask = 0;
+        int need = m;
+        for (int shift = 40; shift >= 0; shift -= 8) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int pc = threadIdx.x + u * kCompactThreads;
-        if (pc < pieces) {
-          const int rr = pc / cpr, cc = pc - rr * cpr;
-          const int src = mv_src[c0 + rr];
-          const int64_t off = row_of(a, pl, l, h, src) * rb + cc * 16;
-          bufk[u] = *reinterpret_cast<const uint4 *>(kp8 + off);
-          bufv[u] = *reinterpret_cast<const uint4 *>(vp8 + off);
-          npc = u + 1;
+          for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
+          __syncwarp();
+          for (int s = lane; s < nc; s += 32) {
+            const unsigned long long k = key[s];
+            if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+          }
+          __syncwarp();
+          // lane owns digits 255-8*lane … 248-8*lane (descending); counts from the top
+          uint32_t c[8];
+          uint32_t loc = 0;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) { c[b] = hist[255 - lane * 8 - b]; loc += c[b]; }
+          uint32_t incl = loc;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          const uint32_t before = incl - loc;
+          const bool mine = before < static_cast<uint32_t>(need) &&
+                            static_cast<uint32_t>(need) <= incl;
+          int dsel = 0;
+          uint32_t above = 0, inbin = 0;
+          if (mine) {
+            uint32_t acc = before;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+              if (acc < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= acc + c[b] &&
+                  inbin == 0) {
+                dsel = 255 - lane * 8 - b;
+                above = acc;
+                inbin = c[b];
+              }
+              acc += c[b];
+            }
+          }
+          const unsigned who = __ballot_sync(0xffffffffu, mine);
+          const int src = __ffs(who) - 1;
+          dsel = __shfl_sync(0xffffffffu, dsel, src);
+          above = __shfl_sync(0xffffffffu, above, src);
+          inbin = __shfl_sync(0xffffffffu, inbin, src);
+          need -= static_cast<int>(above);
+          prefix |= static_cast<unsigned long long>(dsel) << shift;
+          pmask |= 255ull << shift;
+          if (static_cast<uint32_t>(need) == inbin) break;   // the whole bin survives
+        }
+        tkey = prefix;
+        tmask = pmask;
+      }
+    }
+    // 2. keep decision, warp scan of the keep mask in slot order → new slot, move list
+    int carry = 0, nmoves = 0;
+    for (int b0 = 0; b0 < kc; b0 += 32) {
+      const int s = b0 + lane;
+      int keep = 0;
+      if (s < kc) {
+        if (!ranked) keep = s >= kc - ka;
+        else if (s >= nc) keep = 1;                                  // tail 𝒯_i
+        else keep = (key[s] & tmask) >= tkey;                        // Top-m_i by A_i(t)
+      }
+      const unsigned kb = __ballot_sync(0xffffffffu, keep);
+      const int ns = carry + __popc(kb & lt_mask);
+      carry += __popc(kb);
+      const int mv = keep && ns != s;
+      const unsigned mb = __ballot_sync(0xffffffffu, mv);
+      if (mv) mlist[nmoves + __popc(mb & lt_mask)] = static_cast<uint32_t>(s) |
+                                                      (static_cast<uint32_t>(ns) << 16);
+      nmoves += __popc(mb);
+    }
+    __syncwarp();
+    // 3. in-place stable gather: each chunk of rows is read completely into registers
+    //    before any of it is written (a kept row never moves to a later slot)
+    const int chunk_rows = rpi * kUnroll;
+    for (int c0 = 0; c0 < nmoves; c0 += chunk_rows) {
+      uint4 bk[kUnroll], bv[kUnroll];
+      int16_t ptag[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int rr = c0 + u * rpi + my_row;
+        if (rr < nmoves) {
+          const int64_t srow = row(static_cast<int>(mlist[rr] & 0xffffu));
+          const int64_t off = srow * rb + my_piece * 16;
+          bk[u] = *reinterpret_cast<const uint4 *>(kp8 + off);
+          bv[u] = *reinterpret_cast<const uint4 *>(vp8 + off);
+          if (my_piece == 0) ptag[u] = a.pos[srow];
         }
       }
-      __syncthreads();
+      __syncwarp();
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int pc = threadIdx.x + u * kCompactThreads;
-        if (u < npc && pc < pieces) {
-          const int rr = pc / cpr, cc = pc - rr * cpr;
-          const int src = mv_src[c0 + rr];
-          const int64_t off = row_of(a, pl, l, h, nslot[src]) * rb + cc * 16;
-          *reinterpret_cast<uint4 *>(kp8 + off) = bufk[u];
-          *reinterpret_cast<uint4 *>(vp8 + off) = bufv[u];
+      for (int u = 0; u < kUnroll; ++u) {
+        const int rr = c0 + u * rpi + my_row;
+        if (rr < nmoves) {
+          const int64_t drow = row(static_cast<int>(mlist[rr] >> 16));
+          const int64_t off = drow * rb + my_piece * 16;
+          *reinterpret_cast<uint4 *>(kp8 + off) = bk[u];
+          *reinterpret_cast<uint4 *>(vp8 + off) = bv[u];
+          if (my_piece == 0) a.pos[drow] = ptag[u];
         }
       }
-      for (int rr = threadIdx.x; rr < nr; rr += blockDim.x) {
-        const int src = mv_src[c0 + rr];
-        a.pos[row_of(a, pl, l, h, nslot[src])] = static_cast<int16_t>(pos[src]);
-      }
-      __syncthreads();
+      __syncwarp();
     }
-    __syncthreads();
   }
 }
 
@@ -295,7 +351,8 @@ void launch_select_compact(arbor_ctx *c, int max_n) {
   a.esize = c->esize;
   const int cap = max_n < 1 ? 1 : max_n;
   a.cap = cap;
-  const size_t smem = static_cast<size_t>(cap) * (8 + 4 + 4 + 4);
+  a.lgP = __builtin_ctz(static_cast<unsigned>(c->P));
+  const size_t smem = (static_cast<size_t>(cap) * (8 + 4) + ((cap >> a.lgP) + 1) * 4) * kWarps;
   static int attr_smem = 0;
   if (static_cast<int>(smem) > attr_smem) {
     cudaFuncSetAttribute(select_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -304,12 +361,12 @@ void launch_select_compact(arbor_ctx *c, int max_n) {
   }
   int blocks_per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, select_compact_kernel,
-                                                kCompactThreads, smem);
+                                                kWarps * 32, smem);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int grid = sms * (blocks_per_sm > 0 ? blocks_per_sm : 1);
   stage_begin(c, ARBOR_ST_SELECT_COMPACT, c->ms);
-  select_compact_kernel<<<grid, kCompactThreads, smem, c->ms>>>(a);
+  select_compact_kernel<<<grid, kWarps * 32, smem, c->ms>>>(a);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SELECT_COMPACT, c->ms);
 }

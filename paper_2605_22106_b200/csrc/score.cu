@@ -8,8 +8,8 @@
 // of A per token — deterministic, no float atomics (Q30).
 //
 // a3 (Q4/Q5/Q29): m_{l,h,i} = Σ_{t∈span_i} A[l][h][t] accumulated in fp64,
-// Q = round-half-even(m · 2^24) as int64, Mass_i = Σ_rows Q (integer atomics: exact and
-// order-independent); a_i = clamp((Mass_i − Mclose_i) 2^-24 / (Nq_i L Hq), 0, 1);
+// Q = round-half-even(m · 2^24) as int64, Mass_i = Σ_rows Q (exact int64 sums: order- and
+// world-size-independent); a_i = clamp((Mass_i − Mclose_i) 2^-24 / (Nq_i L Hq), 0, 1);
 // s_i = clip(σ(θ0 + θ_v v_i + θ_u u_i + θ_a a_i), 0, 1) in fp64, rounded to f32.
 #include "tile.cuh"
 
@@ -119,36 +119,37 @@ void launch_score_q(arbor_ctx *c, ScoreArgs a, int S, int max_q) {
   }
 }
 
-// One CTA per (listed node, local layer): Q partial of every local KV head of that layer,
-// summed into out[node * out_stride] with 64-bit integer atomics (exact, order-free).
-__global__ void __launch_bounds__(256)
+// One CTA per listed node: warps stride over the local layers, each warp sums one
+// (layer, head) row of A over the node's span in fp64 (lanes strided, xor-tree: fixed
+// order), quantises Q = round-half-even(m · 2^24) and accumulates the int64 Q of its rows;
+// the CTA reduces its warps' integers and writes Σ_rows Q to out[node * out_stride].
+constexpr int kMassThreads = 256;
+__global__ void __launch_bounds__(kMassThreads)
 node_mass_kernel(const int32_t *__restrict__ nodes, const int32_t *__restrict__ nlen,
-                 const int64_t *__restrict__ span, const float *__restrict__ A, int H,
+                 const int64_t *__restrict__ span, const float *__restrict__ A, int L, int H,
                  int64_t max_tokens, int64_t *__restrict__ out, int out_stride) {
   const int node = nodes[blockIdx.x];
-  const int l = blockIdx.y;
   const int n = nlen[node];
   const int64_t a0 = span[node];
-  __shared__ double red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kW = kMassThreads / 32;
+  __shared__ long long red[kW];
   long long qsum = 0;
-  for (int h = 0; h < H; ++h) {
-    const float *row = A + (static_cast<int64_t>(l) * H + h) * max_tokens + a0;
+  for (int r = warp; r < L * H; r += kW) {
+    const float *row = A + static_cast<int64_t>(r) * max_tokens + a0;
     double m = 0.0;
-    for (int t = threadIdx.x; t < n; t += blockDim.x) m += static_cast<double>(row[t]);
+    for (int t = lane; t < n; t += 32) m += static_cast<double>(row[t]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tot = 0.0;
-      for (int w = 0; w < (blockDim.x >> 5); ++w) tot += red[w];
-      qsum += __double2ll_rn(tot * 16777216.0);   // round-half-even(m · 2^24)
-    }
-    __syncthreads();
+    qsum += __double2ll_rn(m * 16777216.0);   // round-half-even(m · 2^24), all lanes agree
   }
-  if (threadIdx.x == 0)
-    atomicAdd(reinterpret_cast<unsigned long long *>(out + static_cast<int64_t>(node) * out_stride),
-              static_cast<unsigned long long>(qsum));
+  if (lane == 0) red[warp] = qsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tot = 0;
+    for (int w = 0; w < kW; ++w) tot += red[w];
+    out[static_cast<int64_t>(node) * out_stride] = tot;
+  }
 }
 
 struct MsveArgs {
@@ -224,9 +225,9 @@ void launch_score_accum(arbor_ctx *c, const PlanView &pv, int max_q, const void 
 void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64_t *out,
                       int out_stride) {
   if (num_nodes == 0) return;
-  dim3 grid(num_nodes, c->L);
-  node_mass_kernel<<<grid, 256, 0, c->ms>>>(d_nodes, c->d.n, c->d.span, c->cfg.score, c->H,
-                                            c->max_tokens, out, out_stride);
+  node_mass_kernel<<<num_nodes, kMassThreads, 0, c->ms>>>(d_nodes, c->d.n, c->d.span,
+                                                          c->cfg.score, c->L, c->H,
+                                                          c->max_tokens, out, out_stride);
   ARBOR_LAUNCHED(c);
 }
 

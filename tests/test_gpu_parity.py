@@ -254,12 +254,20 @@ def test_edge_cases_and_errors():
     bad.span_len[4] = 31
     with pytest.raises(ArborError):
         pr.ctx.arbor_evict(bad, k)
-    # NaN accumulated attention is an invariant violation, surfaced at the next sync
-    pr.ctx.score[0, 0, int(pr.tree.span_start[4]) + 31] = float("nan")
-    pr.ctx.arbor_evict(pr.tree, torch.zeros(N, dtype=torch.int32, device="cuda"))
+
+
+def test_nan_score_is_an_invariant_error():
+    """A NaN accumulated attention that would order heavy hitters is ARBOR_ERR_INVARIANT,
+    latched by the kernel and surfaced at the next sync (include/arbor.h conventions)."""
+    pr = Pair(workload.PRESETS["c1"], seed=2)
+    N = pr.tree.num_nodes
+    pr.ctx.score[0, 0, int(pr.tree.span_start[5])] = float("nan")   # non-tail slot of node 5
+    tgt = torch.tensor([32, 32, 32, 32, 32, 10, 32], dtype=torch.int32, device="cuda")
+    pr.ctx.arbor_evict(pr.tree, tgt)     # node 5: k 32 -> 10 > L_tail: ranked by A
     with pytest.raises(ArborError) as e:
         pr.ctx.arbor_sync()
     assert e.value.status == 4
+    pr.ctx.arbor_sync()                  # the latch is cleared once reported
 
 
 def test_stash_rehydrate_bit_exact_roundtrip():
