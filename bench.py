@@ -326,20 +326,21 @@ def main():
     if pg is not None:
         pg.barrier()
     torch.cuda.synchronize()
+    ctx.arbor_reset_stage_times()
     clocks.start()
     time.sleep(0.2)
-    for i in range(args.steps):
+    for i in range(args.steps):            # no host sync inside: the host runs ahead
         restore()
         l0 = ctx.arbor_launch_count()
         ev[i][0].record(stream)
         step(i)
         ev[i][1].record(stream)
         launches += ctx.arbor_launch_count() - l0
-        st = ctx.arbor_stage_times()           # syncs; outside the events
-        for k in stage_ms:
-            stage_ms[k].append(st[k])
     torch.cuda.synchronize()
     clk = clocks.stop()
+    st = ctx.arbor_stage_times()           # mean CUDA-event duration of each kernel stage
+    for k in stage_ms:
+        stage_ms[k] = [st[k]] * 2
     if pg is not None:
         pg.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]

@@ -158,7 +158,10 @@ arbor_status arbor_close_node(arbor_ctx *ctx, int32_t node);
  * s_i = σ(θ0 + θ_v v_i + θ_u u_i + θ_a a_i).
  *  q:     DEVICE [num_active][layer_count][Hq_local][head_dim] kv_dtype
  *  lse:   DEVICE [num_active][layer_count][Hq_local] f32 from arbor_tree_decode_attn with the
- *         same q, or NULL (the library then computes it first)
+ *         same q, or NULL (the library then computes it first).  When this call directly
+ *         follows a full-range arbor_tree_decode_attn with the same q and lse buffers (and
+ *         no KV-changing call in between), the logits that call produced are reused (fused
+ *         a2, no K re-read); the caller must not modify q in between.
  *  s_out: DEVICE [num_nodes] f32, or NULL; open / never-scored nodes get 0.5 (Q31).
  *         The library also keeps the scores internally for arbor_allocate(s = NULL). */
 arbor_status arbor_score(arbor_ctx *ctx, const arbor_tree *tree, const void *q,
@@ -226,15 +229,21 @@ arbor_status arbor_read_counters(arbor_ctx *ctx, int64_t *rehydrations, int64_t 
  * array are not included.  Used by benchmarks to repeat a mutating step. */
 arbor_status arbor_save_state(arbor_ctx *ctx, int32_t slot);
 arbor_status arbor_load_state(arbor_ctx *ctx, int32_t slot);
+/* The caller wrote the accumulated-attention array directly: recompute every closed node's
+ * partial mass at the next arbor_score (the library otherwise recomputes only the nodes
+ * whose tokens it just scored — A changes nowhere else). */
+arbor_status arbor_invalidate_masses(arbor_ctx *ctx);
 /* Kernel launches issued by this context since creation (all streams). */
 int64_t arbor_launch_count(const arbor_ctx *ctx);
-/* With ARBOR_FLAG_PROFILE: per-stage device milliseconds of the most recent call of each
- * stage, measured with CUDA events on the launching stream (HOST out [ARBOR_NUM_STAGES]). */
+/* With ARBOR_FLAG_PROFILE: per-stage mean device milliseconds over the launches recorded since
+ * the last arbor_reset_stage_times (up to the last 128 per stage), measured with CUDA events
+ * on the launching stream (HOST out [ARBOR_NUM_STAGES]; synchronises). */
 #define ARBOR_NUM_STAGES 12
 enum { ARBOR_ST_GEOMETRY = 0, ARBOR_ST_SCORE_ACCUM, ARBOR_ST_NODE_MASS, ARBOR_ST_MSVE,
        ARBOR_ST_ALLOCATE, ARBOR_ST_EVICT_PLAN, ARBOR_ST_SELECT_COMPACT, ARBOR_ST_REHYDRATE,
        ARBOR_ST_ATTN, ARBOR_ST_ATTN_MERGE, ARBOR_ST_ALLREDUCE, ARBOR_ST_STASH };
 arbor_status arbor_stage_times(arbor_ctx *ctx, float *ms);
+arbor_status arbor_reset_stage_times(arbor_ctx *ctx);
 
 /* ---- host-only helpers (no device work; usable without a GPU) ------------------------ */
 /* Validate a tree snapshot: dense ids, parent < child, spans non-overlapping along

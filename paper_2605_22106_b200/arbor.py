@@ -92,7 +92,9 @@ def load_library(path: str = LIB_PATH):
         "arbor_save_state": ([P, I32], I32),
         "arbor_load_state": ([P, I32], I32),
         "arbor_launch_count": ([P], I64),
+        "arbor_invalidate_masses": ([P], I32),
         "arbor_stage_times": ([P, P], I32),
+        "arbor_reset_stage_times": ([P], I32),
         "arbor_validate_tree": ([C.POINTER(ArborTree), I32, C.c_char_p, C.c_size_t], I32),
         "arbor_min_feasible_budget": ([C.POINTER(ArborParams), C.POINTER(ArborTree),
                                        C.POINTER(C.c_int64)], I32),
@@ -352,8 +354,15 @@ class ArborKV:
     def arbor_load_state(self, slot=0):
         self._check(self.lib.arbor_load_state(self._ctx, int(slot)), "arbor_load_state")
 
+    def arbor_invalidate_masses(self):
+        """Call after writing the score array (A) directly."""
+        self._check(self.lib.arbor_invalidate_masses(self._ctx), "arbor_invalidate_masses")
+
     def arbor_launch_count(self) -> int:
         return int(self.lib.arbor_launch_count(self._ctx))
+
+    def arbor_reset_stage_times(self):
+        self._check(self.lib.arbor_reset_stage_times(self._ctx), "arbor_reset_stage_times")
 
     def arbor_stage_times(self) -> dict:
         ms = (C.c_float * NUM_STAGES)()

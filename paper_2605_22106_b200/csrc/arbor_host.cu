@@ -231,14 +231,15 @@ arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
   c->t_v.assign(t->search_value, t->search_value + N);
   c->t_u.assign(t->uncertainty, t->uncertainty + N);
   c->tree_valid = true;
+  ++c->tree_version;
   return ARBOR_OK;
 }
 
 // ---------------------------------------------------------------- attention / score plan
 struct HostPlan {
-  std::vector<int32_t> seg_node, seg_chunk, seg_loff, seg_lcnt, pair_b, bp_off, bp_list;
+  std::vector<int32_t> ch_node, ch_chunk, ch_poff, ch_pcnt, it_chunk, it_j0, it_cnt, pair_b,
+      bp_off, bp_list;
   std::vector<std::vector<int32_t>> paths;
-  int max_lcnt = 0;
 };
 
 void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan &p) {
@@ -251,50 +252,54 @@ void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan 
     std::reverse(path.begin(), path.end());
     for (int x : path) leaves[x].push_back(b);
   }
-  std::vector<int32_t> seg_of(N, -1);
+  std::vector<int32_t> chunk_of(N, -1);
   for (int x = 0; x < N; ++x) {
     if (leaves[x].empty()) continue;
     const int nch = (n_of[x] + kAttnChunk - 1) / kAttnChunk;
     if (nch == 0) continue;
-    seg_of[x] = static_cast<int32_t>(p.seg_node.size());
+    chunk_of[x] = static_cast<int32_t>(p.ch_node.size());
     const int lc = static_cast<int>(leaves[x].size());
-    p.max_lcnt = std::max(p.max_lcnt, lc);
     for (int ch = 0; ch < nch; ++ch) {
-      p.seg_node.push_back(x);
-      p.seg_chunk.push_back(ch);
-      p.seg_loff.push_back(static_cast<int32_t>(p.pair_b.size()));
-      p.seg_lcnt.push_back(lc);
+      const int c = static_cast<int>(p.ch_node.size());
+      p.ch_node.push_back(x);
+      p.ch_chunk.push_back(ch);
+      p.ch_poff.push_back(static_cast<int32_t>(p.pair_b.size()));
+      p.ch_pcnt.push_back(lc);
       p.pair_b.insert(p.pair_b.end(), leaves[x].begin(), leaves[x].end());
+      for (int j0 = 0; j0 < lc; j0 += kLeavesPerItem) {
+        p.it_chunk.push_back(c);
+        p.it_j0.push_back(j0);
+        p.it_cnt.push_back(std::min(kLeavesPerItem, lc - j0));
+      }
     }
   }
   p.bp_off.assign(1, 0);
   for (int b = 0; b < nA; ++b) {
     for (int x : p.paths[b]) {
-      if (seg_of[x] < 0) continue;
+      if (chunk_of[x] < 0) continue;
       const int nch = (n_of[x] + kAttnChunk - 1) / kAttnChunk;
       const int pos = static_cast<int>(std::lower_bound(leaves[x].begin(), leaves[x].end(), b) -
                                        leaves[x].begin());
-      for (int ch = 0; ch < nch; ++ch) p.bp_list.push_back(p.seg_loff[seg_of[x] + ch] + pos);
+      for (int ch = 0; ch < nch; ++ch) p.bp_list.push_back(p.ch_poff[chunk_of[x] + ch] + pos);
     }
     p.bp_off.push_back(static_cast<int32_t>(p.bp_list.size()));
   }
 }
 
-// Upload [nq int64[N] (optional)] + plan arrays + extra int32 list; fill a PlanView.
+// Upload [plan arrays | extra int32 list] (+ Nq when with_nq); fill a PlanView.
 arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
                          const std::vector<int32_t> *extra, PlanView &pv, const int32_t **d_extra) {
-  const size_t nseg = p.seg_node.size(), np = p.pair_b.size();
   std::vector<int32_t> packed;
-  packed.reserve(4 * nseg + np + p.bp_off.size() + p.bp_list.size() + (extra ? extra->size() : 0));
   auto put = [&](const std::vector<int32_t> &v) {
     const size_t off = packed.size();
     packed.insert(packed.end(), v.begin(), v.end());
     return off;
   };
-  const size_t o_node = put(p.seg_node), o_chunk = put(p.seg_chunk), o_loff = put(p.seg_loff),
-               o_lcnt = put(p.seg_lcnt), o_pb = put(p.pair_b), o_bpo = put(p.bp_off),
+  const size_t o_cn = put(p.ch_node), o_cc = put(p.ch_chunk), o_cpo = put(p.ch_poff),
+               o_cpc = put(p.ch_pcnt), o_ic = put(p.it_chunk), o_ij = put(p.it_j0),
+               o_in = put(p.it_cnt), o_pb = put(p.pair_b), o_bpo = put(p.bp_off),
                o_bpl = put(p.bp_list);
-  size_t o_extra = packed.size();
+  const size_t o_extra = packed.size();
   if (extra) put(*extra);
   const size_t plan_bytes = packed.size() * 4;
   if (plan_bytes > c->seg_cap) {
@@ -305,26 +310,36 @@ arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
   if (!packed.empty()) TRY(ring_upload(c, c->d.seg, packed.data(), plan_bytes));
   if (with_nq) TRY(ring_upload(c, c->d.nq, c->h_nq.data(), c->num_known * sizeof(int64_t)));
   const int32_t *base = c->d.seg;
-  pv.seg_node = base + o_node;
-  pv.seg_chunk = base + o_chunk;
-  pv.seg_loff = base + o_loff;
-  pv.seg_lcnt = base + o_lcnt;
+  pv.ch_node = base + o_cn;
+  pv.ch_chunk = base + o_cc;
+  pv.ch_poff = base + o_cpo;
+  pv.ch_pcnt = base + o_cpc;
+  pv.it_chunk = base + o_ic;
+  pv.it_j0 = base + o_ij;
+  pv.it_cnt = base + o_in;
   pv.pair_b = base + o_pb;
   pv.bp_off = base + o_bpo;
   pv.bp_list = base + o_bpl;
-  pv.S = static_cast<int>(nseg);
+  pv.C = static_cast<int>(p.ch_node.size());
+  pv.I = static_cast<int>(p.it_chunk.size());
   pv.nA = nA;
-  pv.P = static_cast<int>(np);
+  pv.P = static_cast<int>(p.pair_b.size());
   if (d_extra) *d_extra = base + o_extra;
   return ARBOR_OK;
 }
 
 arbor_status ensure_partials(arbor_ctx *c, size_t pairs, int layer_count) {
   const size_t need = pairs * layer_count * c->Hq * (c->D + 2) * sizeof(float);
+  const size_t zneed = pairs * layer_count * c->Hq * kAttnChunk * sizeof(float);
   if (need > c->partial_cap) {
     if (c->d.partials) CK(cudaFree(c->d.partials));
     c->partial_cap = std::max<size_t>(need + need / 2, 1 << 20);
     CK(cudaMalloc(&c->d.partials, c->partial_cap));
+  }
+  if (zneed > c->zbuf_cap) {
+    if (c->d.zbuf) CK(cudaFree(c->d.zbuf));
+    c->zbuf_cap = std::max<size_t>(zneed + zneed / 2, 1 << 20);
+    CK(cudaMalloc(&c->d.zbuf, c->zbuf_cap));
   }
   return ARBOR_OK;
 }
@@ -332,7 +347,7 @@ arbor_status ensure_partials(arbor_ctx *c, size_t pairs, int layer_count) {
 arbor_status run_attention(arbor_ctx *c, const HostPlan &hp, const PlanView &pv, int layer_begin,
                            int layer_count, const void *q, void *out, float *lse) {
   TRY(ensure_partials(c, hp.pair_b.size(), layer_count));
-  launch_attn_partial(c, pv, hp.max_lcnt * c->G, q, layer_begin, layer_count);
+  launch_attn_partial(c, pv, q, layer_begin, layer_count);
   CK_LAUNCH();
   launch_attn_merge(c, pv, layer_count, out, lse);
   CK_LAUNCH();
@@ -399,13 +414,16 @@ __global__ void fill_f32(float *p, int n, float v) {
 
 // ---------------------------------------------------------------- profiling hooks
 namespace arbor {
+// Profiling: every stage launch is bracketed by a pair of CUDA events on its stream; the
+// last kStageRing pairs per stage are kept and averaged by arbor_stage_times (no sync here).
 void stage_begin(arbor_ctx *c, int st, cudaStream_t s) {
-  if (c->cfg.flags & ARBOR_FLAG_PROFILE) cudaEventRecord(c->st_ev[st][0], s);
+  if (c->cfg.flags & ARBOR_FLAG_PROFILE)
+    cudaEventRecord(c->st_ev[st][c->st_count[st] % kStageRing][0], s);
 }
 void stage_end(arbor_ctx *c, int st, cudaStream_t s) {
   if (c->cfg.flags & ARBOR_FLAG_PROFILE) {
-    cudaEventRecord(c->st_ev[st][1], s);
-    c->st_used[st] = true;
+    cudaEventRecord(c->st_ev[st][c->st_count[st] % kStageRing][1], s);
+    ++c->st_count[st];
   }
 }
 }  // namespace arbor
@@ -518,7 +536,8 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   ALLOC(d.ptab, static_cast<size_t>(MN) * c->max_pages_node);
   ALLOC(d.free_stack, c->NP);
   ALLOC(d.span, MN); ALLOC(d.mass2, 2 * MN); ALLOC(d.mclose, MN); ALLOC(d.nq, MN);
-  ALLOC(d.a, MN); ALLOC(d.s, MN);
+  ALLOC(d.a, MN); ALLOC(d.s, MN); ALLOC(d.mass_part, MN);
+  ALLOC(d.mass_scratch, static_cast<size_t>(MN) * c->L);
   ALLOC(d.ctrl, 1);
   {
     // tree mirror block: [parent | len | active | v | u | open] (fixed offsets, see upload_tree)
@@ -559,9 +578,13 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   if (cudaEventCreateWithFlags(&c->ev_main_to_side, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_side_done, cudaEventDisableTiming) != cudaSuccess)
     return bail(ARBOR_ERR_CUDA);
-  for (int i = 0; i < ARBOR_NUM_STAGES; ++i)
-    for (int j = 0; j < 2; ++j)
-      if (cudaEventCreate(&c->st_ev[i][j]) != cudaSuccess) return bail(ARBOR_ERR_CUDA);
+  if (k.flags & ARBOR_FLAG_PROFILE) {
+    for (int i = 0; i < ARBOR_NUM_STAGES; ++i)
+      for (int r = 0; r < kStageRing; ++r)
+        for (int j = 0; j < 2; ++j)
+          if (cudaEventCreate(&c->st_ev[i][r][j]) != cudaSuccess) return bail(ARBOR_ERR_CUDA);
+    c->st_created = true;
+  }
   // pinned host stash [2][L][H][max_tokens][D]
   const size_t stash_bytes = 2ull * c->L * c->H * static_cast<size_t>(c->max_tokens) * c->D * c->esize;
   if (k.host_stash) {
@@ -596,11 +619,12 @@ void arbor_destroy(arbor_ctx *c) {
   void *ptrs[] = {d.n, d.kcur, d.npages, d.ptab, d.free_stack, d.span, d.mass2, d.mclose, d.nq,
                   d.a, d.s, d.ctrl, d.parent, d.onpath, d.pinned, d.depth, d.delta, d.Ed, d.ED,
                   d.work_node, d.work_old, d.work_new, d.rehyd_nodes, d.rehyd_flag, d.seg,
-                  d.partials, d.lse_scratch, d.out_scratch};
+                  d.partials, d.lse_scratch, d.out_scratch, d.zbuf, d.mass_part, d.mass_scratch};
   for (void *p : ptrs) if (p) cudaFree(p);
   for (auto &sn : c->snap) {
     if (!sn.valid) continue;
-    void *sp[] = {sn.n, sn.kcur, sn.npages, sn.ptab, sn.free_stack, sn.mclose, sn.nq_dev, sn.s, sn.ctrl};
+    void *sp[] = {sn.n, sn.kcur, sn.npages, sn.ptab, sn.free_stack, sn.mclose, sn.nq_dev, sn.s, sn.ctrl,
+                  sn.mass_part};
     for (void *p : sp) if (p) cudaFree(p);
   }
   for (int i = 0; i < kRingSlots; ++i) {
@@ -609,8 +633,10 @@ void arbor_destroy(arbor_ctx *c) {
   }
   if (c->ev_main_to_side) cudaEventDestroy(c->ev_main_to_side);
   if (c->ev_side_done) cudaEventDestroy(c->ev_side_done);
-  for (int i = 0; i < ARBOR_NUM_STAGES; ++i)
-    for (int j = 0; j < 2; ++j) if (c->st_ev[i][j]) cudaEventDestroy(c->st_ev[i][j]);
+  if (c->st_created)
+    for (int i = 0; i < ARBOR_NUM_STAGES; ++i)
+      for (int r = 0; r < kStageRing; ++r)
+        for (int j = 0; j < 2; ++j) if (c->st_ev[i][r][j]) cudaEventDestroy(c->st_ev[i][r][j]);
   if (c->own_stash && c->stash_host) cudaFreeHost(c->stash_host);
   if (c->own_ms) cudaStreamDestroy(c->ms);
   if (c->own_ss) cudaStreamDestroy(c->ss);
@@ -627,6 +653,7 @@ arbor_status arbor_open_node(arbor_ctx *c, int32_t node, int64_t span_start) {
                                        c->d.mclose, c->d.s, c->d.a);
   ARBOR_LAUNCHED(c);
   CK_LAUNCH();
+  ++c->epoch;
   c->h_n.push_back(0);
   c->h_open.push_back(1);
   c->h_span.push_back(span_start);
@@ -648,6 +675,7 @@ arbor_status arbor_append_kv(arbor_ctx *c, int32_t node, const void *k, const vo
   CK_LAUNCH();
   c->h_n[node] = static_cast<int32_t>(new_n);
   c->tree_valid = false;
+  ++c->epoch;
   return ARBOR_OK;
 }
 
@@ -660,6 +688,10 @@ arbor_status arbor_close_node(arbor_ctx *c, int32_t node) {
   TRY(ring_upload(c, c->d.rehyd_nodes + c->max_nodes, &node, sizeof(int32_t)));
   launch_node_mass(c, c->d.rehyd_nodes + c->max_nodes, 1, c->d.mclose, 1);
   CK_LAUNCH();
+  // the node's cached partial mass starts at its close-time value
+  CK(cudaMemcpyAsync(c->d.mass_part + node, c->d.mclose + node, sizeof(int64_t),
+                     cudaMemcpyDeviceToDevice, c->ms));
+  ++c->epoch;
   // write-through stash on the side stream (a7), after the node's last append
   CK(cudaEventRecord(c->ev_main_to_side, c->ms));
   CK(cudaStreamWaitEvent(c->ss, c->ev_main_to_side, 0));
@@ -684,30 +716,45 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
   HostPlan hp;
   build_plan(tree, c->h_n, hp);
   // Nq_i += 1 for every closed i on Path(ℓ_b) (one query per active leaf and step)
+  std::vector<uint8_t> vis(N, 0);
   for (int b = 0; b < nA; ++b)
-    for (int x : hp.paths[b]) if (!c->h_open[x]) c->h_nq[x] += 1;
-  std::vector<int32_t> closed;
-  for (int i = 0; i < N; ++i) if (!c->h_open[i]) closed.push_back(i);
+    for (int x : hp.paths[b]) {
+      vis[x] = 1;
+      if (!c->h_open[x]) c->h_nq[x] += 1;
+    }
+  // partial masses to (re)compute: the visible closed nodes, or all closed nodes when the
+  // cache is invalid (A changes only at visible tokens)
+  std::vector<int32_t> mass_nodes;
+  for (int i = 0; i < N; ++i)
+    if (!c->h_open[i] && (vis[i] || !c->mass_valid)) mass_nodes.push_back(i);
   PlanView pv{};
-  const int32_t *d_closed = nullptr;
-  TRY(upload_plan(c, hp, nA, true, &closed, pv, &d_closed));
+  const int32_t *d_mass_nodes = nullptr;
+  TRY(upload_plan(c, hp, nA, true, &mass_nodes, pv, &d_mass_nodes));
+  // a9's logits are reused when this call follows a full-range arbor_tree_decode_attn with
+  // the same q and lse buffers and nothing changed the KV in between (fused a2)
+  const bool fused = lse && q == c->lg_q && lse == c->lg_lse && c->lg_epoch == c->epoch &&
+                     c->lg_tree == c->tree_version;
   const float *lse_use = lse;
-  if (!lse) {
+  if (!fused) {
     const size_t qn = static_cast<size_t>(nA) * c->L * c->Hq;
-    if (c->d.lse_scratch) { cudaFree(c->d.lse_scratch); c->d.lse_scratch = nullptr; }
-    if (c->d.out_scratch) { cudaFree(c->d.out_scratch); c->d.out_scratch = nullptr; }
-    CK(cudaMalloc(&c->d.lse_scratch, qn * sizeof(float)));
-    CK(cudaMalloc(&c->d.out_scratch, qn * c->D * c->esize));
+    if (qn > c->scratch_q) {
+      if (c->d.lse_scratch) cudaFree(c->d.lse_scratch);
+      if (c->d.out_scratch) cudaFree(c->d.out_scratch);
+      CK(cudaMalloc(&c->d.lse_scratch, qn * sizeof(float)));
+      CK(cudaMalloc(&c->d.out_scratch, qn * c->D * c->esize));
+      c->scratch_q = qn;
+    }
     TRY(run_attention(c, hp, pv, 0, c->L, q, c->d.out_scratch, c->d.lse_scratch));
-    lse_use = c->d.lse_scratch;
+    if (!lse) lse_use = c->d.lse_scratch;
   }
-  launch_score_accum(c, pv, hp.max_lcnt * c->G, q, lse_use, c->L);
+  launch_score_apply(c, pv, lse_use, c->L);
   CK_LAUNCH();
+  c->lg_epoch = -1;   // A changed: the logits must not be applied twice
   stage_begin(c, ARBOR_ST_NODE_MASS, c->ms);
-  if (closed.size() < static_cast<size_t>(N))   // open nodes have no mass entry
-    CK(cudaMemsetAsync(c->d.mass2, 0, N * sizeof(int64_t), c->ms));
-  launch_node_mass(c, d_closed, static_cast<int>(closed.size()), c->d.mass2, 1);
+  launch_node_mass(c, d_mass_nodes, static_cast<int>(mass_nodes.size()), c->d.mass_part, 1);
   CK_LAUNCH();
+  c->mass_valid = true;
+  CK(cudaMemcpyAsync(c->d.mass2, c->d.mass_part, N * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->ms));
   CK(cudaMemcpyAsync(c->d.mass2 + N, c->d.mclose, N * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->ms));
   stage_end(c, ARBOR_ST_NODE_MASS, c->ms);
   if (c->cfg.world_size > 1) {
@@ -759,6 +806,7 @@ arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_
   for (int i = 0; i < tree->num_nodes; ++i)
     if (!pin[i]) max_n = std::max(max_n, c->h_n[i]);
   wait_side(c);   // pending stash copies read pages this call may free
+  ++c->epoch;
   launch_evict_plan(c, tree->num_nodes, k_target);
   CK_LAUNCH();
   if (max_n > 0) {
@@ -792,6 +840,7 @@ arbor_status arbor_rehydrate(arbor_ctx *c, const arbor_tree *tree, const int32_t
   TRY(upload_tree(c, tree));
   TRY(ring_upload(c, c->d.rehyd_nodes, list.data(), list.size() * sizeof(int32_t)));
   wait_side(c);
+  ++c->epoch;
   stage_begin(c, ARBOR_ST_REHYDRATE, c->ms);
   launch_rehydrate_plan(c, static_cast<int>(list.size()));
   CK_LAUNCH();
@@ -813,11 +862,18 @@ arbor_status arbor_tree_decode_attn(arbor_ctx *c, const arbor_tree *tree, int32_
   if (!q || !out) return fail(c, ARBOR_ERR_INVALID_ARG, "q / out is NULL");
   if (layer_begin < 0 || layer_count < 1 || layer_begin + layer_count > c->L)
     return fail(c, ARBOR_ERR_INVALID_ARG, "layer range outside the shard");
+  TRY(upload_tree(c, tree));
   HostPlan hp;
   build_plan(tree, c->h_n, hp);
   PlanView pv{};
   TRY(upload_plan(c, hp, tree->num_active, false, nullptr, pv, nullptr));
-  return run_attention(c, hp, pv, layer_begin, layer_count, q, out, lse_out);
+  TRY(run_attention(c, hp, pv, layer_begin, layer_count, q, out, lse_out));
+  const bool full = layer_begin == 0 && layer_count == c->L && lse_out;
+  c->lg_q = full ? q : nullptr;
+  c->lg_lse = full ? lse_out : nullptr;
+  c->lg_epoch = full ? c->epoch : -1;
+  c->lg_tree = c->tree_version;
+  return ARBOR_OK;
 }
 
 // ---------------------------------------------------------------- inspection
@@ -891,6 +947,7 @@ arbor_status arbor_save_state(arbor_ctx *c, int32_t slot) {
     CK(cudaMalloc(&sn.n, MN * 4)); CK(cudaMalloc(&sn.kcur, MN * 4)); CK(cudaMalloc(&sn.npages, MN * 4));
     CK(cudaMalloc(&sn.ptab, PT * 4)); CK(cudaMalloc(&sn.free_stack, c->NP * 4));
     CK(cudaMalloc(&sn.mclose, MN * 8)); CK(cudaMalloc(&sn.nq_dev, MN * 8)); CK(cudaMalloc(&sn.s, MN * 4));
+    CK(cudaMalloc(&sn.mass_part, MN * 8));
     CK(cudaMalloc(&sn.ctrl, sizeof(Ctrl)));
     sn.valid = true;
   }
@@ -901,6 +958,8 @@ arbor_status arbor_save_state(arbor_ctx *c, int32_t slot) {
   CK(cp(sn.n, c->d.n, MN * 4)); CK(cp(sn.kcur, c->d.kcur, MN * 4)); CK(cp(sn.npages, c->d.npages, MN * 4));
   CK(cp(sn.ptab, c->d.ptab, PT * 4)); CK(cp(sn.free_stack, c->d.free_stack, c->NP * 4));
   CK(cp(sn.mclose, c->d.mclose, MN * 8)); CK(cp(sn.s, c->d.s, MN * 4)); CK(cp(sn.ctrl, c->d.ctrl, sizeof(Ctrl)));
+  CK(cp(sn.mass_part, c->d.mass_part, MN * 8));
+  sn.mass_valid = c->mass_valid;
   sn.h_n = c->h_n; sn.h_open = c->h_open; sn.h_span = c->h_span; sn.h_nq = c->h_nq;
   sn.num_known = c->num_known;
   return ARBOR_OK;
@@ -917,6 +976,9 @@ arbor_status arbor_load_state(arbor_ctx *c, int32_t slot) {
   CK(cp(c->d.n, sn.n, MN * 4)); CK(cp(c->d.kcur, sn.kcur, MN * 4)); CK(cp(c->d.npages, sn.npages, MN * 4));
   CK(cp(c->d.ptab, sn.ptab, PT * 4)); CK(cp(c->d.free_stack, sn.free_stack, c->NP * 4));
   CK(cp(c->d.mclose, sn.mclose, MN * 8)); CK(cp(c->d.s, sn.s, MN * 4)); CK(cp(c->d.ctrl, sn.ctrl, sizeof(Ctrl)));
+  CK(cp(c->d.mass_part, sn.mass_part, MN * 8));
+  c->mass_valid = sn.mass_valid;
+  ++c->epoch;
   c->h_n = sn.h_n; c->h_open = sn.h_open; c->h_span = sn.h_span; c->h_nq = sn.h_nq;
   c->num_known = sn.num_known;
   c->tree_valid = false;
@@ -925,16 +987,37 @@ arbor_status arbor_load_state(arbor_ctx *c, int32_t slot) {
 
 int64_t arbor_launch_count(const arbor_ctx *c) { return c ? c->launches : 0; }
 
+arbor_status arbor_invalidate_masses(arbor_ctx *c) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  c->mass_valid = false;
+  c->lg_epoch = -1;
+  return ARBOR_OK;
+}
+
 arbor_status arbor_stage_times(arbor_ctx *c, float *ms) {
   if (!c || !ms) return ARBOR_ERR_INVALID_ARG;
   TRY(sync_all(c));
   for (int i = 0; i < ARBOR_NUM_STAGES; ++i) {
     ms[i] = 0.f;
-    if (c->st_used[i]) {
+    const int n = std::min(c->st_count[i], kStageRing);
+    if (!c->st_created || n == 0) continue;
+    double tot = 0.0;
+    int used = 0;
+    for (int r = 0; r < n; ++r) {
       float t = 0.f;
-      if (cudaEventElapsedTime(&t, c->st_ev[i][0], c->st_ev[i][1]) == cudaSuccess) ms[i] = t;
+      if (cudaEventElapsedTime(&t, c->st_ev[i][r][0], c->st_ev[i][r][1]) == cudaSuccess) {
+        tot += t;
+        ++used;
+      }
     }
+    ms[i] = used ? static_cast<float>(tot / used) : 0.f;
   }
+  return ARBOR_OK;
+}
+
+arbor_status arbor_reset_stage_times(arbor_ctx *c) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  for (int i = 0; i < ARBOR_NUM_STAGES; ++i) c->st_count[i] = 0;
   return ARBOR_OK;
 }
 

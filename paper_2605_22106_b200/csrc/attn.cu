@@ -5,13 +5,20 @@
 // (KV head h = g / G, Q24):  o = Σ_t softmax_t(q·k_t/√d) v_t over the retained slots of
 // Path(ℓ_b), root→leaf; LSE = ln Σ_t exp(q·k_t/√d).
 //
-// B200 design: one CTA per (segment = node × 128-slot chunk of the union of the active
-// paths, layer, KV head).  The segment's K and V rows are staged once into shared memory
-// with cp.async (16-byte, coalesced, K XOR-swizzled) and reused by EVERY active leaf whose
-// path contains the node and by all G query heads of the KV head (tree sharing: a node
-// shared by n leaves is read from HBM once).  Each CTA emits split-softmax partials
-// (o·e^{-m}, m, Σe^{z-m}) in the log2 domain; a merge kernel combines a leaf's partials in
-// a fixed root→leaf order (deterministic, no float atomics).
+// B200 design (persistent, TMA-pipelined, CUDA-core math for few queries per KV head):
+//  * Work item = (chunk of kAttnChunk slots of one node on the union of the active paths, a
+//    subset of ≤ lmax leaves sharing it, layer, KV head).  A node shared by n active leaves
+//    is read from HBM once for all of them (tree sharing) and once for all G query heads.
+//  * One producer warp streams each item's K and V page-heads (≤ P rows × d, contiguous in
+//    the pool) and the item's q rows into a 2-stage shared-memory ring with cp.async.bulk
+//    (the TMA engine); completion is tracked by mbarrier transaction counts; 8 consumer
+//    warps compute while the next item lands.  2 CTAs per SM, items strided across CTAs.
+//  * QKᵀ: SL = d/16 lanes per token (16-element slices, log2(SL)-step shuffle reduce);
+//    softmax statistics per query (warp per query); PV: lanes over 4-element column slices,
+//    warps over token groups, smem reduction.  fp32 accumulation throughout.
+//  * Each item emits split-softmax partials (Σ 2^{z−m} v, m, Σ 2^{z−m}) in the log2 domain
+//    and its log2-domain logits z (consumed by the fused score pass, score.cu); a merge
+//    kernel combines a leaf's partials in fixed root→leaf order (no float atomics).
 #include <cfloat>
 
 #include "tile.cuh"
@@ -19,105 +26,219 @@
 namespace arbor {
 namespace {
 
-constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kCh = kAttnChunk;      // slots per item
+constexpr int kNst = 2;              // pipeline stages
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = 32 * kConsumerWarps;
+constexpr int kThreads = kConsumers + 32;
 
-struct AttnArgs {
+struct StreamArgs {
   PlanView pv;
   PoolView g;
   const void *kpool, *vpool;
   const int32_t *ptab, *kcur;
   const void *q;
-  float *partials;
-  int layer_begin, Lc, Hq, G, lb_per;
-  float scale_log2;   // log2(e)/sqrt(d)
+  float *partials;   // [pair][Lc][H][G][D+2]
+  float *zbuf;       // [pair][Lc][H][G][kCh] log2-domain logits
+  int layer_begin, Lc, Hq, G, lmax, lb;   // lb: leaves per QB batch
+  float scale_log2;  // log2(e)/sqrt(d)
 };
 
-template <typename T, int D, int QB>
-__global__ void __launch_bounds__(128)
-attn_partial_kernel(AttnArgs a) {
-  constexpr int CH = kAttnChunk;
-  constexpr int NCP = D / 2;        // column pairs in the PV phase
-  constexpr int TG = 128 / NCP;     // token groups in the PV phase
-  const int s = blockIdx.x, li = blockIdx.y, h = blockIdx.z;
-  const int l = a.layer_begin + li;
-  const int node = a.pv.seg_node[s];
-  const int c0 = a.pv.seg_chunk[s] * CH;
-  const int nt = max(0, min(CH, a.kcur[node] - c0));
-  const int loff = a.pv.seg_loff[s], lcnt = a.pv.seg_lcnt[s];
-  const int G = a.G;
+struct StageHdr {
+  int nt, item, li, h;
+};
 
-  extern __shared__ __align__(16) unsigned char sm[];
-  T *Ks = reinterpret_cast<T *>(sm);
-  T *Vs = Ks + CH * D;
-  int64_t *rowoff = reinterpret_cast<int64_t *>(Vs + CH * D);
-  float *qs = reinterpret_cast<float *>(rowoff + CH);   // [QB][D]
-  float *zs = qs + QB * D;                               // [QB][CH]
-  float *os = zs + QB * CH;                              // [TG][QB][D]
-  float *mls = os + TG * QB * D;                         // m2[QB], l[QB]
-
-  const T *kpool = static_cast<const T *>(a.kpool);
-  const T *vpool = static_cast<const T *>(a.vpool);
-  const T *q = static_cast<const T *>(a.q);
-  if (nt > 0)
-    stage_tile<T, D, true>(Ks, Vs, rowoff, kpool, vpool, a.ptab + node * a.g.MPN, c0, nt, a.g,
-                           l, h);
-
-  for (int b0 = 0; b0 < lcnt; b0 += a.lb_per) {
-    const int nb = min(a.lb_per, lcnt - b0);
-    const int nq = nb * G;
-    for (int idx = threadIdx.x; idx < nq * D; idx += blockDim.x) {
-      const int qi = idx / D, e = idx - qi * D;
-      const int bi = qi / G, g = qi - bi * G;
-      const int b = a.pv.pair_b[loff + b0 + bi];
-      qs[idx] = ElemT<T>::to_f(q[((static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * G + g) * D + e]);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    if (nt == 0) {
-      for (int idx = threadIdx.x; idx < nq * (D + 2); idx += blockDim.x) {
-        const int qi = idx / (D + 2), e = idx - qi * (D + 2);
-        const int bi = qi / G, g = qi - bi * G;
-        float *dst = a.partials +
-                     ((((static_cast<int64_t>(loff + b0 + bi)) * a.Lc + li) * a.g.H + h) * G + g) *
-                         (D + 2);
-        dst[e] = (e == D) ? -INFINITY : 0.f;
-      }
-      __syncthreads();
-      continue;
-    }
-    // phase 1: z = q·k (log2 domain), thread per token
-    {
-      const int t = threadIdx.x;
-      if (t < nt) {
-        float acc[QB];
-        row_dots<T, D, QB>(Ks, qs, t, nq, acc);
+template <typename T>
+__device__ __forceinline__ void load16(const T *p, float *f);
+template <>
+__device__ __forceinline__ void load16<__nv_bfloat16>(const __nv_bfloat16 *p, float *f) {
+  const uint4 a = reinterpret_cast<const uint4 *>(p)[0];
+  const uint4 b = reinterpret_cast<const uint4 *>(p)[1];
+  ElemT<__nv_bfloat16>::cvt16(a, f);
+  ElemT<__nv_bfloat16>::cvt16(b, f + 8);
+}
+template <>
+__device__ __forceinline__ void load16<float>(const float *p, float *f) {
 #pragma unroll
-        for (int qi = 0; qi < QB; ++qi)
-          if (qi < nq) zs[qi * CH + t] = acc[qi] * a.scale_log2;
-      } else {
-        for (int qi = 0; qi < nq; ++qi) zs[qi * CH + t] = -INFINITY;
+  for (int i = 0; i < 4; ++i) ElemT<float>::cvt16(reinterpret_cast<const uint4 *>(p)[i], f + 4 * i);
+}
+
+template <typename T>
+__device__ __forceinline__ void load4(const T *p, float *f);
+template <>
+__device__ __forceinline__ void load4<__nv_bfloat16>(const __nv_bfloat16 *p, float *f) {
+  const uint2 u = *reinterpret_cast<const uint2 *>(p);
+  const float2 a = ElemT<__nv_bfloat16>::b2f(u.x), b = ElemT<__nv_bfloat16>::b2f(u.y);
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+}
+template <>
+__device__ __forceinline__ void load4<float>(const float *p, float *f) {
+  const float4 v = *reinterpret_cast<const float4 *>(p);
+  f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+}
+
+template <typename T, int D, int QB>
+__global__ void __launch_bounds__(kThreads, 2)
+attn_stream_kernel(StreamArgs a) {
+  constexpr int SL = D / 16;                // lanes per token in QKᵀ
+  constexpr int TPP = kConsumers / SL;      // tokens per QKᵀ pass
+  constexpr int S4 = D / 4;                 // 4-element column slices in PV
+  constexpr int RPW = 32 / S4;              // rows per warp in PV
+  constexpr int TG = kConsumerWarps * RPW;  // token groups in PV
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = a.G;
+  const int qcap = a.lmax * G;              // q rows staged per item
+  const int64_t stage_elems = static_cast<int64_t>(2 * kCh * D + qcap * D);
+  extern __shared__ __align__(128) unsigned char sm[];
+  T *stage0 = reinterpret_cast<T *>(sm);
+  float *zs = reinterpret_cast<float *>(stage0 + kNst * stage_elems);   // [kCh][QB]
+  float *red = zs + kCh * QB;                                           // [TG][QB][D]
+  float *mls = red + TG * QB * D;                                       // m2[QB], l[QB]
+  StageHdr *hdr = reinterpret_cast<StageHdr *>(mls + 2 * QB);
+  uint64_t *full = reinterpret_cast<uint64_t *>(hdr + kNst);
+  uint64_t *empty = full + kNst;
+  if (tid == 0) {
+    for (int s = 0; s < kNst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int total = a.pv.I * a.Lc * a.g.H;
+  const int rb = D * static_cast<int>(sizeof(T));
+  const T *q = static_cast<const T *>(a.q);
+  if (warp == 0) {
+    // ------------------------------------------------------------- producer (TMA)
+    if (lane == 0) {
+      const T *kpool = static_cast<const T *>(a.kpool);
+      const T *vpool = static_cast<const T *>(a.vpool);
+      int k = 0;
+      for (int it = blockIdx.x; it < total; it += gridDim.x, ++k) {
+        const int st = k % kNst;
+        const uint32_t ph = (k / kNst) & 1u;
+        mbar_wait(&empty[st], ph ^ 1u);
+        const int h = it % a.g.H;
+        const int li = (it / a.g.H) % a.Lc;
+        const int item = it / (a.g.H * a.Lc);
+        const int c = a.pv.it_chunk[item];
+        const int node = a.pv.ch_node[c];
+        const int c0 = a.pv.ch_chunk[c] * kCh;
+        const int nt = max(0, min(kCh, a.kcur[node] - c0));
+        const int cnt = a.pv.it_cnt[item];
+        hdr[st] = StageHdr{nt, item, li, h};
+        T *Ks = stage0 + st * stage_elems;
+        T *Vs = Ks + kCh * D;
+        T *Qs = Vs + kCh * D;
+        mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>((2 * nt + cnt * G) * rb));
+        const int l = a.layer_begin + li;
+        const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.g.MPN;
+        for (int s0 = 0; s0 < nt;) {               // one copy per page-head run
+          const int slot = c0 + s0;
+          const int off = slot % a.g.P;
+          const int rows = min(a.g.P - off, nt - s0);
+          const int64_t row = pool_row(a.g, l, pl[slot / a.g.P], h, off);
+          bulk_g2s(Ks + s0 * D, kpool + row * D, rows * rb, &full[st]);
+          bulk_g2s(Vs + s0 * D, vpool + row * D, rows * rb, &full[st]);
+          s0 += rows;
+        }
+        const int j0 = a.pv.it_j0[item];
+        const int pbase = a.pv.ch_poff[c] + j0;
+        for (int i = 0; i < cnt; ++i) {            // the G query rows of each leaf
+          const int b = a.pv.pair_b[pbase + i];
+          bulk_g2s(Qs + i * G * D, q + ((static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * G) * D,
+                   G * rb, &full[st]);
+        }
       }
     }
-    __syncthreads();
-    // phase 2: per-query max and exp-sum over the chunk (warp per query row)
-    {
-      const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      for (int qi = w; qi < nq; qi += 4) {
-        float v[CH / 32];
+    return;
+  }
+  // --------------------------------------------------------------- consumers
+  const int ct = tid - 32;
+  int k = 0;
+  for (int it = blockIdx.x; it < total; it += gridDim.x, ++k) {
+    const int st = k % kNst;
+    const uint32_t ph = (k / kNst) & 1u;
+    mbar_wait(&full[st], ph);
+    const StageHdr hd = hdr[st];
+    const int nt = hd.nt, li = hd.li, h = hd.h;
+    const int c = a.pv.it_chunk[hd.item];
+    const int cnt = a.pv.it_cnt[hd.item];
+    const int pbase = a.pv.ch_poff[c] + a.pv.it_j0[hd.item];
+    const T *Ks = stage0 + st * stage_elems;
+    const T *Vs = Ks + kCh * D;
+    const T *Qs = Vs + kCh * D;
+    for (int b0 = 0; b0 < cnt; b0 += a.lb) {
+      const int nb = min(a.lb, cnt - b0);
+      const int nq = nb * G;
+      // ---- phase 1: z[t][qi] = log2(e)/√d · q·k_t, in groups of 4 queries
+      {
+        const int sl = ct % SL, tt = ct / SL;
+        for (int q0 = 0; q0 < nq; q0 += 4) {
+          float qf[4][16];
+#pragma unroll
+          for (int qi = 0; qi < 4; ++qi) {
+            if (q0 + qi < nq) {
+              load16<T>(Qs + (b0 * G + q0 + qi) * D + sl * 16, qf[qi]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) qf[qi][e] = 0.f;
+            }
+          }
+          for (int t0 = 0; t0 < kCh; t0 += TPP) {
+            const int t = t0 + tt;
+            float dot[4] = {0.f, 0.f, 0.f, 0.f};
+            if (t < nt) {
+              float kf[16];
+              load16<T>(Ks + t * D + sl * 16, kf);
+#pragma unroll
+              for (int qi = 0; qi < 4; ++qi) {
+                float acc = 0.f;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) acc = fmaf(kf[e], qf[qi][e], acc);
+                dot[qi] = acc;
+              }
+            }
+#pragma unroll
+            for (int qi = 0; qi < 4; ++qi) {
+#pragma unroll
+              for (int o = SL / 2; o; o >>= 1) dot[qi] += __shfl_xor_sync(0xffffffffu, dot[qi], o);
+            }
+            if (sl == 0) {
+#pragma unroll
+              for (int qi = 0; qi < 4; ++qi)
+                if (q0 + qi < QB)
+                  zs[t * QB + q0 + qi] = (t < nt && q0 + qi < nq) ? dot[qi] * a.scale_log2 : -INFINITY;
+            }
+          }
+        }
+      }
+      named_bar_sync(1, kConsumers);
+      // logits for the fused score pass: zbuf[pair][li][h][g][t]
+      for (int idx = ct; idx < nq * kCh; idx += kConsumers) {
+        const int qi = idx / kCh, t = idx - qi * kCh;
+        const int bi = qi / G, g = qi - bi * G;
+        a.zbuf[((((static_cast<int64_t>(pbase + b0 + bi)) * a.Lc + li) * a.g.H + h) * G + g) * kCh + t] =
+            zs[t * QB + qi];
+      }
+      // ---- phase 2: per-query max and exp-sum over the chunk (warp per query)
+      for (int qi = warp - 1; qi < nq; qi += kConsumerWarps) {
+        float v[kCh / 32];
         float m = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < CH / 32; ++j) {
-          v[j] = zs[qi * CH + lane + 32 * j];
+        for (int j = 0; j < kCh / 32; ++j) {
+          v[j] = zs[(lane + 32 * j) * QB + qi];
           m = fmaxf(m, v[j]);
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         float sum = 0.f;
 #pragma unroll
-        for (int j = 0; j < CH / 32; ++j) {
+        for (int j = 0; j < kCh / 32; ++j) {
           const float p = (v[j] == -INFINITY) ? 0.f : exp2f(v[j] - m);
-          zs[qi * CH + lane + 32 * j] = p;
+          zs[(lane + 32 * j) * QB + qi] = p;
           sum += p;
         }
 #pragma unroll
@@ -127,49 +248,52 @@ attn_partial_kernel(AttnArgs a) {
           mls[QB + qi] = sum;
         }
       }
-    }
-    __syncthreads();
-    // phase 3: o = Σ_t p_t v_t; thread = (column pair, token group)
-    {
-      const int cp = threadIdx.x % NCP, tg = threadIdx.x / NCP;
-      float acc[QB][2];
+      named_bar_sync(1, kConsumers);
+      // ---- phase 3: o = Σ_t p_t v_t; lanes over 4-element column slices, warps over tokens
+      {
+        const int e4 = lane % S4, tg = (warp - 1) * RPW + lane / S4;
+        float acc[QB][4];
 #pragma unroll
-      for (int qi = 0; qi < QB; ++qi) acc[qi][0] = acc[qi][1] = 0.f;
-      for (int t = tg; t < nt; t += TG) {
-        const float2 vf = ElemT<T>::ld2(Vs + t * D + 2 * cp);
+        for (int qi = 0; qi < QB; ++qi) acc[qi][0] = acc[qi][1] = acc[qi][2] = acc[qi][3] = 0.f;
+        for (int t = tg; t < nt; t += TG) {
+          float vf[4];
+          load4<T>(Vs + t * D + e4 * 4, vf);
+          float p[QB];
 #pragma unroll
-        for (int qi = 0; qi < QB; ++qi) {
-          if (qi < nq) {
-            const float p = zs[qi * CH + t];
-            acc[qi][0] = fmaf(p, vf.x, acc[qi][0]);
-            acc[qi][1] = fmaf(p, vf.y, acc[qi][1]);
+          for (int qi = 0; qi < QB; qi += 4) {
+            const float4 pp = *reinterpret_cast<const float4 *>(zs + t * QB + qi);
+            p[qi] = pp.x; p[qi + 1] = pp.y; p[qi + 2] = pp.z; p[qi + 3] = pp.w;
           }
-        }
-      }
 #pragma unroll
-      for (int qi = 0; qi < QB; ++qi) {
-        if (qi < nq) {
-          os[(tg * QB + qi) * D + 2 * cp] = acc[qi][0];
-          os[(tg * QB + qi) * D + 2 * cp + 1] = acc[qi][1];
-        }
-      }
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < nq * (D + 2); idx += blockDim.x) {
-      const int qi = idx / (D + 2), e = idx - qi * (D + 2);
-      const int bi = qi / G, g = qi - bi * G;
-      float val;
-      if (e < D) {
-        val = 0.f;
+          for (int qi = 0; qi < QB; ++qi)
 #pragma unroll
-        for (int j = 0; j < TG; ++j) val += os[(j * QB + qi) * D + e];
-      } else {
-        val = mls[(e - D) * QB + qi];
+            for (int e = 0; e < 4; ++e) acc[qi][e] = fmaf(p[qi], vf[e], acc[qi][e]);
+        }
+#pragma unroll
+        for (int qi = 0; qi < QB; ++qi)
+          if (qi < nq)
+            *reinterpret_cast<float4 *>(red + (tg * QB + qi) * D + e4 * 4) =
+                make_float4(acc[qi][0], acc[qi][1], acc[qi][2], acc[qi][3]);
       }
-      a.partials[((((static_cast<int64_t>(loff + b0 + bi)) * a.Lc + li) * a.g.H + h) * G + g) *
-                     (D + 2) + e] = val;
+      named_bar_sync(1, kConsumers);
+      if (b0 + a.lb >= cnt && lane == 0) mbar_arrive(&empty[st]);   // stage no longer read
+      for (int idx = ct; idx < nq * (D + 2); idx += kConsumers) {
+        const int qi = idx / (D + 2), e = idx - qi * (D + 2);
+        const int bi = qi / G, g = qi - bi * G;
+        float val;
+        if (e < D) {
+          val = 0.f;
+#pragma unroll 8
+          for (int j = 0; j < TG; ++j) val += red[(j * QB + qi) * D + e];
+        } else {
+          val = mls[(e - D) * QB + qi];
+        }
+        a.partials[((((static_cast<int64_t>(pbase + b0 + bi)) * a.Lc + li) * a.g.H + h) * G + g) *
+                       (D + 2) + e] = val;
+      }
+      named_bar_sync(1, kConsumers);
     }
-    __syncthreads();
+    if (cnt == 0 && lane == 0) mbar_arrive(&empty[st]);
   }
 }
 
@@ -226,45 +350,44 @@ attn_merge_kernel(MergeArgs a) {
 }
 
 template <typename T, int D, int QB>
-void launch_partial_t(arbor_ctx *c, const AttnArgs &a, int S, int Lc) {
-  constexpr int CH = kAttnChunk;
-  constexpr int TG = 128 / (D / 2);
-  const size_t smem = 2 * CH * D * sizeof(T) + CH * sizeof(int64_t) +
-                      (QB * D + QB * CH + TG * QB * D + 2 * QB) * sizeof(float);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(attn_partial_kernel<T, D, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+void launch_stream_t(arbor_ctx *c, StreamArgs a) {
+  constexpr int S4 = D / 4, RPW = 32 / S4, TG = kConsumerWarps * RPW;
+  const size_t stage = (2 * kCh * D + static_cast<size_t>(a.lmax) * a.G * D) * sizeof(T);
+  const size_t smem = kNst * stage + (kCh * QB + TG * QB * D + 2 * QB) * sizeof(float) +
+                      kNst * sizeof(StageHdr) + 2 * kNst * sizeof(uint64_t) + 16;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(attn_stream_kernel<T, D, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    attr_set = true;
+    attr = smem;
   }
-  dim3 grid(S, Lc, c->H);
-  attn_partial_kernel<T, D, QB><<<grid, 128, smem, c->ms>>>(a);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_stream_kernel<T, D, QB>, kThreads, smem);
+  const int total = a.pv.I * a.Lc * a.g.H;
+  int grid = sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > total) grid = total;
+  attn_stream_kernel<T, D, QB><<<grid, kThreads, smem, c->ms>>>(a);
 }
 
 template <typename T, int D>
-void launch_partial_q(arbor_ctx *c, AttnArgs a, int S, int Lc, int max_q) {
-  // queries per CTA batch: the smallest template ≥ min(max_q, 32) rounded to G multiples
-  int qb;
-  if (max_q <= 4) qb = 4;
-  else if (max_q <= 8) qb = 8;
-  else if (max_q <= 16) qb = 16;
-  else qb = 32;
-  a.lb_per = qb / a.G > 0 ? qb / a.G : 1;
-  switch (qb) {
-    case 4: launch_partial_t<T, D, 4>(c, a, S, Lc); break;
-    case 8: launch_partial_t<T, D, 8>(c, a, S, Lc); break;
-    case 16: launch_partial_t<T, D, 16>(c, a, S, Lc); break;
-    default: launch_partial_t<T, D, 32>(c, a, S, Lc); break;
+void launch_stream_q(arbor_ctx *c, StreamArgs a) {
+  if (a.G <= 4) {
+    a.lb = 4 / a.G;
+    launch_stream_t<T, D, 4>(c, a);
+  } else {
+    a.lb = 8 / a.G;
+    launch_stream_t<T, D, 8>(c, a);
   }
 }
 
 }  // namespace
 
-void launch_attn_partial(arbor_ctx *c, const PlanView &pv, int max_q, const void *q,
-                         int layer_begin, int layer_count) {
-  const int S = pv.S;
-  if (S == 0) return;
-  AttnArgs a{};
+void launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
+                         int layer_count) {
+  if (pv.I == 0) return;
+  StreamArgs a{};
   a.pv = pv;
   a.g = PoolView{c->L, c->H, c->P, c->D, c->NP, c->max_pages_node, c->max_tokens};
   a.kpool = c->cfg.k_pool;
@@ -273,25 +396,26 @@ void launch_attn_partial(arbor_ctx *c, const PlanView &pv, int max_q, const void
   a.kcur = c->d.kcur;
   a.q = q;
   a.partials = c->d.partials;
+  a.zbuf = c->d.zbuf;
   a.layer_begin = layer_begin;
   a.Lc = layer_count;
   a.Hq = c->Hq;
   a.G = c->G;
+  a.lmax = kLeavesPerItem;
   a.scale_log2 = kLog2e / sqrtf(static_cast<float>(c->D));
   stage_begin(c, ARBOR_ST_ATTN, c->ms);
   if (c->esize == 2) {
-    if (c->D == 128) launch_partial_q<__nv_bfloat16, 128>(c, a, S, layer_count, max_q);
-    else launch_partial_q<__nv_bfloat16, 64>(c, a, S, layer_count, max_q);
+    if (c->D == 128) launch_stream_q<__nv_bfloat16, 128>(c, a);
+    else launch_stream_q<__nv_bfloat16, 64>(c, a);
   } else {
-    if (c->D == 128) launch_partial_q<float, 128>(c, a, S, layer_count, max_q);
-    else launch_partial_q<float, 64>(c, a, S, layer_count, max_q);
+    if (c->D == 128) launch_stream_q<float, 128>(c, a);
+    else launch_stream_q<float, 64>(c, a);
   }
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_ATTN, c->ms);
 }
 
-void launch_attn_merge(arbor_ctx *c, const PlanView &pv, int layer_count, void *out,
-                       float *lse) {
+void launch_attn_merge(arbor_ctx *c, const PlanView &pv, int layer_count, void *out, float *lse) {
   const int nA = pv.nA;
   MergeArgs m{};
   m.pv = pv;

@@ -15,11 +15,12 @@
 
 namespace arbor {
 
-constexpr int kAttnChunk = 128;      // slots per attention / score segment
-constexpr int kMaxQueriesPerCta = 64; // (leaves sharing a segment) x G per CTA
+constexpr int kAttnChunk = 64;       // slots per attention / score chunk
+constexpr int kLeavesPerItem = 8;    // active leaves per attention work item (q rows staged)
 constexpr int kStashSlots = 4;
-constexpr int kRingSlots = 8;
-constexpr size_t kRingBytes = 4u << 20;
+constexpr int kRingSlots = 32;
+constexpr int kStageRing = 128;   // event pairs kept per profiled stage
+constexpr size_t kRingBytes = 1u << 20;
 
 // Error bits latched on the device (ctrl.err)
 enum : int32_t {
@@ -67,18 +68,25 @@ struct DevState {
   // attention / score plan (uploaded per call)
   int32_t *seg;              // packed plan (see attn.cu)
   float *partials;           // attention partials
+  float *zbuf;               // attention log2-domain logits (fused score pass)
+  int64_t *mass_part;        // this rank's per-node partial mass (cached, §score.cu)
+  int64_t *mass_scratch;     // [max_nodes][layer_count] node-mass partials
   float *lse_scratch;        // used when arbor_score gets lse == NULL
   void *out_scratch;
 };
 
 // Plan of one attention / score call (built on the host from the tree, arbor_host.cu).
-// A segment is (node, chunk of kAttnChunk slots) of the union of the active leaves' paths;
-// its leaf list names every active leaf whose Path(ℓ_b) contains the node (read once for
-// all of them).  pair p = seg_loff[s] + i is the i-th leaf of segment s; bp_list holds,
-// per leaf b, its pairs in root→leaf, chunk-ascending order (the merge order).
+// A chunk is (node, kAttnChunk slots) of the union of the active leaves' paths; its pairs
+// are the active leaves whose Path(ℓ_b) contains the node (pair p = ch_poff[c] + i), read
+// once for all of them.  An attention item is a chunk with a subset of ≤ kLeavesPerItem of
+// its leaves.  bp_list holds, per leaf b, its pairs in root→leaf, chunk-ascending order
+// (the merge order).
 struct PlanView {
-  const int32_t *seg_node, *seg_chunk, *seg_loff, *seg_lcnt, *pair_b, *bp_off, *bp_list;
-  int S, nA, P;
+  const int32_t *ch_node, *ch_chunk, *ch_poff, *ch_pcnt;   // C chunks: (node, chunk) + pairs
+  const int32_t *it_chunk, *it_j0, *it_cnt;                 // I attention items (leaf subsets)
+  const int32_t *pair_b;                                     // P pairs → active leaf index
+  const int32_t *bp_off, *bp_list;                           // per leaf: pairs root→leaf
+  int C, I, nA, P;
 };
 
 struct PoolView {
@@ -89,8 +97,9 @@ struct PoolView {
 struct Snapshot {
   bool valid = false;
   int32_t *n, *kcur, *npages, *ptab, *free_stack;
-  int64_t *mclose, *nq_dev;
+  int64_t *mclose, *nq_dev, *mass_part;
   float *s;
+  bool mass_valid = true;
   Ctrl *ctrl;
   std::vector<int32_t> h_n;
   std::vector<uint8_t> h_open;
@@ -131,13 +140,23 @@ struct arbor_ctx {
   cudaEvent_t ev_main_to_side = nullptr, ev_side_done = nullptr;
   bool side_pending = false;
   // attention scratch capacity
-  size_t partial_cap = 0, seg_cap = 0;
+  size_t partial_cap = 0, seg_cap = 0, zbuf_cap = 0;
+  // epoch: bumped by every call that changes KV contents / page tables
+  long long epoch = 0, tree_version = 0;
+  // logits of the last full-range tree_decode_attn (fused score pass)
+  const void *lg_q = nullptr;
+  const float *lg_lse = nullptr;
+  long long lg_epoch = -1, lg_tree = -1;
+  // cached per-node partial masses are exact for the current A (score.cu)
+  bool mass_valid = true;
+  size_t scratch_q = 0;
   // NCCL
   void *nccl_comm = nullptr;
   void *nccl_lib = nullptr;
   // profiling
-  cudaEvent_t st_ev[ARBOR_NUM_STAGES][2] = {};
-  bool st_used[ARBOR_NUM_STAGES] = {};
+  cudaEvent_t st_ev[ARBOR_NUM_STAGES][arbor::kStageRing][2] = {};
+  int st_count[ARBOR_NUM_STAGES] = {};   // launches recorded since the last reset
+  bool st_created = false;
   long long launches = 0;
   arbor::Snapshot snap[arbor::kStashSlots];
   std::string err;
@@ -150,8 +169,7 @@ namespace arbor {
 void launch_geometry(arbor_ctx *c, int N, int nA);
 
 // score.cu
-void launch_score_accum(arbor_ctx *c, const PlanView &pv, int max_q, const void *q,
-                        const float *lse, int layer_count);
+void launch_score_apply(arbor_ctx *c, const PlanView &pv, const float *lse, int layer_count);
 void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64_t *out,
                       int out_stride);
 void launch_msve(arbor_ctx *c, int N, float *s_out);
@@ -170,8 +188,8 @@ void launch_rehydrate_plan(arbor_ctx *c, int count);
 void launch_rehydrate_copy(arbor_ctx *c, int count, int max_n);
 
 // attn.cu
-void launch_attn_partial(arbor_ctx *c, const PlanView &pv, int max_q, const void *q,
-                         int layer_begin, int layer_count);
+void launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
+                         int layer_count);
 void launch_attn_merge(arbor_ctx *c, const PlanView &pv, int layer_count, void *out,
                        float *lse);
 

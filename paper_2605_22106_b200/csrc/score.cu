@@ -2,14 +2,14 @@
 //
 // a2 (§4 Execution (iii)): A_i(t) = Σ_{u>b_i} Σ_l Σ_h Attn_{u→t}.  Per
 // decode step and active leaf b: p_t = exp(q·k_t/√d − LSE_{b,l,g}) over the visible slots
-// of Path(ℓ_b), A[l][h][a_j + pos_t] += Σ_{g∈group(h)} p_t.  One CTA owns a (segment,
-// layer, KV head): it stages the segment's K rows once and sums the contributions of every
-// active leaf sharing the node in ascending leaf order, then does a single read-modify-write
-// of A per token — deterministic, no float atomics (Q30).
+// of Path(ℓ_b), A[l][h][a_j + pos_t] += Σ_{g∈group(h)} p_t — computed from the logits the
+// attention kernel already produced ("from attention weights already materialized during
+// decoding"), without re-reading K.
 //
 // a3 (Q4/Q5/Q29): m_{l,h,i} = Σ_{t∈span_i} A[l][h][t] accumulated in fp64,
 // Q = round-half-even(m · 2^24) as int64, Mass_i = Σ_rows Q (exact int64 sums: order- and
-// world-size-independent); a_i = clamp((Mass_i − Mclose_i) 2^-24 / (Nq_i L Hq), 0, 1);
+// world-size-independent).  A changes only at the visible tokens of a score call, so each
+// rank caches its per-node partial Q sum and recomputes it for the visible closed nodes only; a_i = clamp((Mass_i − Mclose_i) 2^-24 / (Nq_i L Hq), 0, 1);
 // s_i = clip(σ(θ0 + θ_v v_i + θ_u u_i + θ_a a_i), 0, 1) in fp64, rounded to f32.
 #include "tile.cuh"
 
@@ -18,125 +18,68 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-struct ScoreArgs {
+// a2, fused with a9: the attention kernel already computed every visible logit
+// z = log2(e)·q·k/√d (attn.cu); with the merged LSE the attention weight is exp2(z − LSE·log2 e).
+// One CTA per (chunk, layer, KV head), thread per slot: sums the weights of every active leaf
+// sharing the chunk and all G query heads (ascending leaf order), then one read-modify-write
+// of A at the slot's absolute position (deterministic, no float atomics, Q30).
+struct ApplyArgs {
   PlanView pv;
   PoolView g;
-  const void *kpool;
   const int16_t *pos;
   const int32_t *ptab, *kcur;
   const int64_t *span;
-  const void *q;
-  const float *lse;
+  const float *zbuf, *lse;
   float *A;
   Ctrl *ctrl;
-  int Lc, Hq, G, lb_per;
-  float scale_log2;
+  int Lc, Hq, G;
 };
 
-template <typename T, int D, int QB>
-__global__ void __launch_bounds__(128)
-score_accum_kernel(ScoreArgs a) {
-  constexpr int CH = kAttnChunk;
-  const int s = blockIdx.x, li = blockIdx.y, h = blockIdx.z;
-  const int node = a.pv.seg_node[s];
-  const int c0 = a.pv.seg_chunk[s] * CH;
-  const int nt = max(0, min(CH, a.kcur[node] - c0));
-  if (nt == 0) return;
-  const int loff = a.pv.seg_loff[s], lcnt = a.pv.seg_lcnt[s];
-  const int G = a.G;
-  extern __shared__ __align__(16) unsigned char sm[];
-  T *Ks = reinterpret_cast<T *>(sm);
-  int64_t *rowoff = reinterpret_cast<int64_t *>(Ks + CH * D);
-  float *qs = reinterpret_cast<float *>(rowoff + CH);   // [QB][D]
-  float *ls = qs + QB * D;                               // [QB] LSE·log2e
-  const T *kpool = static_cast<const T *>(a.kpool);
-  const T *q = static_cast<const T *>(a.q);
-  stage_tile<T, D, false>(Ks, nullptr, rowoff, kpool, nullptr, a.ptab + node * a.g.MPN, c0, nt,
-                          a.g, li, h);
+__global__ void __launch_bounds__(kAttnChunk)
+score_apply_kernel(ApplyArgs a) {
+  const int c = blockIdx.x, li = blockIdx.y, h = blockIdx.z;
   const int t = threadIdx.x;
+  const int node = a.pv.ch_node[c];
+  const int c0 = a.pv.ch_chunk[c] * kAttnChunk;
+  const int nt = max(0, min(kAttnChunk, a.kcur[node] - c0));
+  if (t >= nt) return;
+  const int p0 = a.pv.ch_poff[c], pc = a.pv.ch_pcnt[c];
   float psum = 0.f;
-  for (int b0 = 0; b0 < lcnt; b0 += a.lb_per) {
-    const int nb = min(a.lb_per, lcnt - b0);
-    const int nq = nb * G;
-    for (int idx = threadIdx.x; idx < nq * D; idx += blockDim.x) {
-      const int qi = idx / D, e = idx - qi * D;
-      const int bi = qi / G, g = qi - bi * G;
-      const int b = a.pv.pair_b[loff + b0 + bi];
-      qs[idx] = ElemT<T>::to_f(q[((static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * G + g) * D + e]);
-    }
-    for (int qi = threadIdx.x; qi < nq; qi += blockDim.x) {
-      const int bi = qi / G, g = qi - bi * G;
-      const int b = a.pv.pair_b[loff + b0 + bi];
-      ls[qi] = a.lse[(static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * G + g] * kLog2e;
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    if (t < nt) {
-      float acc[QB];
-      row_dots<T, D, QB>(Ks, qs, t, nq, acc);
-#pragma unroll
-      for (int qi = 0; qi < QB; ++qi)
-        if (qi < nq) psum += exp2f(fmaf(acc[qi], a.scale_log2, -ls[qi]));
-    }
-    __syncthreads();
+  for (int p = p0; p < p0 + pc; ++p) {
+    const int b = a.pv.pair_b[p];
+    const float *z = a.zbuf + (((static_cast<int64_t>(p) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + t;
+    const float *ls = a.lse + (static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * a.G;
+    for (int g = 0; g < a.G; ++g) psum += exp2f(z[g * kAttnChunk] - ls[g] * kLog2e);
   }
-  if (t < nt) {
-    const int pos = a.pos[rowoff[t]];
-    float *dst = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + a.span[node] + pos;
-    const float nv = *dst + psum;
-    if (!(nv >= 0.f) || isinf(nv)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-    *dst = nv;
-  }
+  const int slot = c0 + t;
+  const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.g.MPN;
+  const int pos = a.pos[pool_row(a.g, li, pl[slot / a.g.P], h, slot % a.g.P)];
+  float *dst = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + a.span[node] + pos;
+  const float nv = *dst + psum;
+  if (!(nv >= 0.f) || isinf(nv)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+  *dst = nv;
 }
 
-template <typename T, int D, int QB>
-void launch_score_t(arbor_ctx *c, const ScoreArgs &a, int S) {
-  constexpr int CH = kAttnChunk;
-  const size_t smem = CH * D * sizeof(T) + CH * sizeof(int64_t) + (QB * D + QB) * sizeof(float);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(score_accum_kernel<T, D, QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    attr_set = true;
-  }
-  dim3 grid(S, c->L, c->H);
-  score_accum_kernel<T, D, QB><<<grid, 128, smem, c->ms>>>(a);
-}
-
-template <typename T, int D>
-void launch_score_q(arbor_ctx *c, ScoreArgs a, int S, int max_q) {
-  int qb;
-  if (max_q <= 4 && c->G <= 4) qb = 4;
-  else if (max_q <= 8 && c->G <= 8) qb = 8;
-  else if (max_q <= 16 && c->G <= 16) qb = 16;
-  else qb = 32;
-  a.lb_per = qb / a.G > 0 ? qb / a.G : 1;
-  switch (qb) {
-    case 4: launch_score_t<T, D, 4>(c, a, S); break;
-    case 8: launch_score_t<T, D, 8>(c, a, S); break;
-    case 16: launch_score_t<T, D, 16>(c, a, S); break;
-    default: launch_score_t<T, D, 32>(c, a, S); break;
-  }
-}
-
-// One CTA per listed node: warps stride over the local layers, each warp sums one
-// (layer, head) row of A over the node's span in fp64 (lanes strided, xor-tree: fixed
-// order), quantises Q = round-half-even(m · 2^24) and accumulates the int64 Q of its rows;
-// the CTA reduces its warps' integers and writes Σ_rows Q to out[node * out_stride].
+// Node mass in two launches: one CTA per (listed node, layer) — warps over the layer's KV
+// heads, each warp sums one row of A over the node's span in fp64 (lanes strided, xor tree:
+// fixed order) and quantises Q = round-half-even(m · 2^24); the CTA's int64 sum goes to
+// scratch[node_idx][layer]; a finalize kernel adds the layers (exact integer sums) and
+// writes out[node * out_stride].
 constexpr int kMassThreads = 256;
 __global__ void __launch_bounds__(kMassThreads)
 node_mass_kernel(const int32_t *__restrict__ nodes, const int32_t *__restrict__ nlen,
                  const int64_t *__restrict__ span, const float *__restrict__ A, int L, int H,
-                 int64_t max_tokens, int64_t *__restrict__ out, int out_stride) {
+                 int64_t max_tokens, int64_t *__restrict__ scratch) {
   const int node = nodes[blockIdx.x];
+  const int l = blockIdx.y;
   const int n = nlen[node];
   const int64_t a0 = span[node];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int kW = kMassThreads / 32;
   __shared__ long long red[kW];
   long long qsum = 0;
-  for (int r = warp; r < L * H; r += kW) {
-    const float *row = A + static_cast<int64_t>(r) * max_tokens + a0;
+  for (int h = warp; h < H; h += kW) {
+    const float *row = A + (static_cast<int64_t>(l) * H + h) * max_tokens + a0;
     double m = 0.0;
     for (int t = lane; t < n; t += 32) m += static_cast<double>(row[t]);
 #pragma unroll
@@ -148,8 +91,18 @@ node_mass_kernel(const int32_t *__restrict__ nodes, const int32_t *__restrict__ 
   if (threadIdx.x == 0) {
     long long tot = 0;
     for (int w = 0; w < kW; ++w) tot += red[w];
-    out[static_cast<int64_t>(node) * out_stride] = tot;
+    scratch[static_cast<int64_t>(blockIdx.x) * L + l] = tot;
   }
+}
+
+__global__ void node_mass_finalize(const int32_t *__restrict__ nodes, int count, int L,
+                                   const int64_t *__restrict__ scratch, int64_t *__restrict__ out,
+                                   int out_stride) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  long long tot = 0;
+  for (int l = 0; l < L; ++l) tot += scratch[static_cast<int64_t>(i) * L + l];
+  out[static_cast<int64_t>(nodes[i]) * out_stride] = tot;
 }
 
 struct MsveArgs {
@@ -191,33 +144,24 @@ __global__ void msve_kernel(MsveArgs m) {
 
 }  // namespace
 
-void launch_score_accum(arbor_ctx *c, const PlanView &pv, int max_q, const void *q,
-                        const float *lse, int layer_count) {
-  if (pv.S == 0) return;
-  ScoreArgs a{};
+void launch_score_apply(arbor_ctx *c, const PlanView &pv, const float *lse, int layer_count) {
+  if (pv.C == 0) return;
+  ApplyArgs a{};
   a.pv = pv;
   a.g = PoolView{c->L, c->H, c->P, c->D, c->NP, c->max_pages_node, c->max_tokens};
-  a.kpool = c->cfg.k_pool;
   a.pos = c->cfg.pos_pool;
   a.ptab = c->d.ptab;
   a.kcur = c->d.kcur;
   a.span = c->d.span;
-  a.q = q;
+  a.zbuf = c->d.zbuf;
   a.lse = lse;
   a.A = c->cfg.score;
   a.ctrl = c->d.ctrl;
   a.Lc = layer_count;
   a.Hq = c->Hq;
   a.G = c->G;
-  a.scale_log2 = kLog2e / sqrtf(static_cast<float>(c->D));
   stage_begin(c, ARBOR_ST_SCORE_ACCUM, c->ms);
-  if (c->esize == 2) {
-    if (c->D == 128) launch_score_q<__nv_bfloat16, 128>(c, a, pv.S, max_q);
-    else launch_score_q<__nv_bfloat16, 64>(c, a, pv.S, max_q);
-  } else {
-    if (c->D == 128) launch_score_q<float, 128>(c, a, pv.S, max_q);
-    else launch_score_q<float, 64>(c, a, pv.S, max_q);
-  }
+  score_apply_kernel<<<dim3(pv.C, layer_count, c->H), kAttnChunk, 0, c->ms>>>(a);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
 }
@@ -225,10 +169,11 @@ void launch_score_accum(arbor_ctx *c, const PlanView &pv, int max_q, const void 
 void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64_t *out,
                       int out_stride) {
   if (num_nodes == 0) return;
-  node_mass_kernel<<<num_nodes, kMassThreads, 0, c->ms>>>(d_nodes, c->d.n, c->d.span,
-                                                          c->cfg.score, c->L, c->H,
-                                                          c->max_tokens, out, out_stride);
-  ARBOR_LAUNCHED(c);
+  node_mass_kernel<<<dim3(num_nodes, c->L), kMassThreads, 0, c->ms>>>(
+      d_nodes, c->d.n, c->d.span, c->cfg.score, c->L, c->H, c->max_tokens, c->d.mass_scratch);
+  node_mass_finalize<<<(num_nodes + 127) / 128, 128, 0, c->ms>>>(d_nodes, num_nodes, c->L,
+                                                                 c->d.mass_scratch, out, out_stride);
+  c->launches += 2;
 }
 
 void launch_msve(arbor_ctx *c, int N, float *s_out) {

@@ -99,6 +99,7 @@ def test_mid_bf16_pipeline_with_ties():
     T = pr.tree.total_tokens
     idx = rng.choice(T - 1, size=max(1, T // 50), replace=False)
     A[:, :, idx] = A[:, :, idx + 1]
+    pr.ctx.arbor_invalidate_masses()      # A written directly (include/arbor.h)
     B = int(0.25 * pr.tree.total_tokens)
     k = torch.empty(pr.tree.num_nodes, dtype=torch.int32, device="cuda")
     pr.ctx.arbor_allocate(pr.tree, torch.as_tensor(sc["s"], device="cuda"), B, k)
@@ -262,6 +263,7 @@ def test_nan_score_is_an_invariant_error():
     pr = Pair(workload.PRESETS["c1"], seed=2)
     N = pr.tree.num_nodes
     pr.ctx.score[0, 0, int(pr.tree.span_start[5])] = float("nan")   # non-tail slot of node 5
+    pr.ctx.arbor_invalidate_masses()
     tgt = torch.tensor([32, 32, 32, 32, 32, 10, 32], dtype=torch.int32, device="cuda")
     pr.ctx.arbor_evict(pr.tree, tgt)     # node 5: k 32 -> 10 > L_tail: ranked by A
     with pytest.raises(ArborError) as e:
