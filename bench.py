@@ -320,7 +320,7 @@ def main():
           for _ in range(args.steps)]
     stage_ms = {k: [] for k in ("attn", "attn_merge", "score_accum", "node_mass", "msve",
                                 "allreduce", "geometry", "allocate", "evict_plan",
-                                "select_compact")}
+                                "select_compact", "compact_move")}
     launches = 0
     clocks = ClockSampler(local)
     if pg is not None:
@@ -360,7 +360,7 @@ def main():
         torch.cuda.synchronize()
         rb = ctx.D * (2 if preset["dtype"] == "bf16" else 4)
         L, Hh, P = ctx.L, ctx.H, ctx.P
-        byts = {"select_compact": 0, "moved_rows": 0}
+        byts = {"select": 0, "compact_move": 0, "moved_rows": 0}
         for j in range(N):
             kc, n, pages = ctx.arbor_read_node(j)
             if kc == n:
@@ -368,9 +368,10 @@ def main():
             idx = torch.as_tensor(pages, device=dev, dtype=torch.long)
             pos = ctx.pos_pool[:, idx].permute(0, 2, 1, 3).reshape(L, Hh, -1)[:, :, :kc]
             moved = int((pos.long() != torch.arange(kc, device=dev)).sum().item())
-            # per (row, changed node): A + pos reads of the k_cur candidates (4 + 2 B each);
-            # per moved row: K and V read + write (4·rb) and its pos write (2 B)
-            byts["select_compact"] += L * Hh * 6 * n + moved * (4 * rb + 2)
+            # select, per (row, changed node): pos + A of the k_cur kept slots (2 + 4 B each);
+            # move, per moved row: K and V read + write (4·rb) and its pos tag (2 + 2 B)
+            byts["select"] += L * Hh * 6 * n
+            byts["compact_move"] += moved * (4 * rb + 4)
             byts["moved_rows"] += moved
         vis = 0
         for x in synth_path(tree.parent, leaves[i % 2]):
@@ -394,15 +395,22 @@ def main():
         return {"ms": avg, "bytes": b, "GBps": gbs, "frac_measured": gbs / peak,
                 "frac_nominal": gbs / NOMINAL_HBM}
 
-    kernels = {
-        "select_compact": kstat("select_compact", lambda i: ab[i]["select_compact"]),
+    if stage_ms["compact_move"][0] > 0:       # split select → move kernels
+        kernels = {"compact_move": kstat("compact_move", lambda i: ab[i]["compact_move"]),
+                   "select": kstat("select_compact", lambda i: ab[i]["select"])}
+        top_name, top_desc = "compact_move", "compact_move (a6)"
+    else:                                     # one select+compact kernel (default)
+        kernels = {"select_compact": kstat("select_compact",
+                                           lambda i: ab[i]["select"] + ab[i]["compact_move"])}
+        top_name, top_desc = "select_compact", "select_move_ws (a5+a6, warp-specialised)"
+    kernels.update({
         "attn_partial": kstat("attn", lambda i: ab[i]["attn"]),
         "score_accum": kstat("score_accum", lambda i: ab[i]["score_accum"]),
         "node_mass": kstat("node_mass", lambda i: ab[i]["node_mass"]),
-    }
-    top = kernels["select_compact"]
+    })
+    top = kernels[top_name]
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_select_compact_ncu.json")
+    prof = os.path.join(ROOT, "profiles", "r01_compact_move_ncu.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
@@ -410,7 +418,7 @@ def main():
                 traffic = pj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"kernel": "select_compact (a5+a6)", "bound": "hbm", "achieved": top["GBps"],
+    roofline = {"kernel": top_desc, "bound": "hbm", "achieved": top["GBps"],
                 "peak": peak, "unit": "GB/s", "frac": top["GBps"] / peak,
                 "frac_of_nominal_8TBps": top["GBps"] / NOMINAL_HBM, "traffic": traffic,
                 "peak_source": peak_src, "alg_bytes_per_launch": top["bytes"],

@@ -238,10 +238,11 @@ int64_t arbor_launch_count(const arbor_ctx *ctx);
 /* With ARBOR_FLAG_PROFILE: per-stage mean device milliseconds over the launches recorded since
  * the last arbor_reset_stage_times (up to the last 128 per stage), measured with CUDA events
  * on the launching stream (HOST out [ARBOR_NUM_STAGES]; synchronises). */
-#define ARBOR_NUM_STAGES 12
+#define ARBOR_NUM_STAGES 13
 enum { ARBOR_ST_GEOMETRY = 0, ARBOR_ST_SCORE_ACCUM, ARBOR_ST_NODE_MASS, ARBOR_ST_MSVE,
        ARBOR_ST_ALLOCATE, ARBOR_ST_EVICT_PLAN, ARBOR_ST_SELECT_COMPACT, ARBOR_ST_REHYDRATE,
-       ARBOR_ST_ATTN, ARBOR_ST_ATTN_MERGE, ARBOR_ST_ALLREDUCE, ARBOR_ST_STASH };
+       ARBOR_ST_ATTN, ARBOR_ST_ATTN_MERGE, ARBOR_ST_ALLREDUCE, ARBOR_ST_STASH,
+       ARBOR_ST_COMPACT_MOVE };
 arbor_status arbor_stage_times(arbor_ctx *ctx, float *ms);
 arbor_status arbor_reset_stage_times(arbor_ctx *ctx);
 

@@ -31,7 +31,7 @@ def key(a_f32: float, offset: int):
 def retained_set(kept, n: int, k_app: int, l_tail: int, A_node_f32):
     """Alg. 1 Evict for one (row, node).
 
-    kept: ascending within-node offsets currently retained (C);
+    kept: within-node offsets currently retained (C, any order);
     A_node_f32: f32 accumulated attention indexed by within-node offset.
     Returns the new ascending retained offsets ℛ with |ℛ| = k_app."""
     kept = [int(x) for x in kept]

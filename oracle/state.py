@@ -11,9 +11,9 @@ library's calls do (include/arbor.h), in the canonical order of SURVEY.md
 K/V are never moved here: compaction is token-extractive and rehydration
 restores "the same conditioning state as full retention", so the
 content of any retained slot is the original K/V at its absolute position.
-The oracle therefore tracks, per (row, node), the ascending list of retained
-within-node offsets, plus the per-node page lists and the LIFO free stack of
-the paged layout.
+The oracle therefore tracks, per (row, node), the within-node offset held by
+each slot (slot order: DESIGN.md reading Q23'), plus the per-node page lists
+and the LIFO free stack of the paged layout (§8(c).1 step 8).
 """
 from __future__ import annotations
 
@@ -62,7 +62,7 @@ class ArborOracle:
         self.Lg = num_layers_global or self.L
         self.Hqg = num_q_heads_global or self.Hq
         self.span_start, self.n, self.open = [], [], []
-        self.kept = []            # per node: int64 [L][H][k_cur] within-node offsets
+        self.kept = []            # per node: int64 [L][H][k_cur] offset held by each slot
         self.pages = []           # per node: list of page ids
         self.free = list(range(num_pages - 1, -1, -1))   # LIFO, top at the end
         self.A = np.zeros((self.L, self.H, self.Tmax), dtype=np.float64)
@@ -212,7 +212,13 @@ class ArborOracle:
         k_app = min(k_cur, k_target) drops (Alg. 2 P:567 'evict only if
         k_new < k', Q17), nodes ascending; freed pages pushed in ascending
         list order.  A_f32: the f32 accumulated attention that orders heavy
-        hitters (default: the oracle's own A rounded to f32)."""
+        hitters (default: the oracle's own A rounded to f32).
+
+        Slot layout after eviction (reading Q23'): retained rows
+        already in slots [0, k_app) stay in place; the i-th hole there (a slot
+        whose row was evicted, ascending) receives the i-th retained row from
+        slots >= k_app (ascending).  The paper fixes only the retained set
+        (P:171); the slot order is this build's paging choice."""
         if A_f32 is None:
             A_f32 = self.A.astype(np.float32)
         _, _, on_path = self.geometry(tree)
@@ -228,9 +234,16 @@ class ArborOracle:
             new = np.zeros((self.L, self.H, k_app), dtype=np.int64)
             for l in range(self.L):
                 for h in range(self.H):
-                    new[l, h] = select.retained_set(self.kept[j][l, h], n, k_app,
-                                                    self.params["l_tail"],
-                                                    A_f32[l, h, a:a + n])
+                    old = [int(x) for x in self.kept[j][l, h]]
+                    R = set(select.retained_set(old, n, k_app, self.params["l_tail"],
+                                                A_f32[l, h, a:a + n]))
+                    holes = [s for s in range(k_app) if old[s] not in R]
+                    movers = [old[s] for s in range(k_app, kc) if old[s] in R]
+                    assert len(holes) == len(movers)
+                    row = old[:k_app]
+                    for hs, mv in zip(holes, movers):
+                        row[hs] = mv
+                    new[l, h] = row
             self.kept[j] = new
             keep_pages = -(-k_app // self.P)
             for p in self.pages[j][keep_pages:]:

@@ -21,9 +21,10 @@ STATUS = {0: "OK", 2: "INVALID_ARG", 3: "INFEASIBLE_BUDGET", 4: "INVARIANT", 5: 
           6: "OUT_OF_PAGES", 7: "STATE", 8: "CUDA", 9: "NCCL"}
 ALLOC_MODES = {"waterfill": 0, "static": 1, "static_drain": 2}
 FLAG_PROFILE = 1
-NUM_STAGES = 12
+NUM_STAGES = 13
 STAGES = ["geometry", "score_accum", "node_mass", "msve", "allocate", "evict_plan",
-          "select_compact", "rehydrate", "attn", "attn_merge", "allreduce", "stash"]
+          "select_compact", "rehydrate", "attn", "attn_merge", "allreduce", "stash",
+          "compact_move"]
 
 
 class ArborError(RuntimeError):

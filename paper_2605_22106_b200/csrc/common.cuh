@@ -35,10 +35,11 @@ struct Ctrl {
   int32_t err;             // DERR_* bits
   int32_t work_count;      // evict work items of the last plan
   int32_t rehyd_count;     // nodes rehydrated by the last plan
+  int32_t move_count;      // (src, dst) row moves listed by the last select
+  int32_t pad0;
   long long evicted;       // tokens evicted by the last evict
   long long rehydrations;  // total rehydrations
   long long pages_in_use;  // pages held by nodes
-  long long pad;
 };
 
 // Per-launch geometry of the K/V pools
@@ -63,6 +64,8 @@ struct DevState {
   double *Ed, *ED;
   // evict plan
   int32_t *work_node, *work_old, *work_new;
+  int2 *moves;               // compaction move list (src row, dst row)
+  size_t moves_cap;
   // rehydrate / append plans
   int32_t *rehyd_nodes, *rehyd_flag;
   // attention / score plan (uploaded per call)

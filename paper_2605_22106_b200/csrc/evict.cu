@@ -12,17 +12,17 @@
 //  * evict_plan (1 CTA): decides k_app per node, builds the work list of changed non-pinned
 //    nodes in ascending id, truncates page lists to ⌈k_app/P⌉ and pushes the freed pages on
 //    the LIFO free list in ascending (node, list) order — all on the device, no host sync.
-//  * select_compact (persistent grid, one WARP per (node, row) work item, no block
-//    barriers): gathers the pos tags and A keys of the non-tail kept slots, finds the m-th
-//    largest unique 48-bit key ⟨A bits, pos⟩ by a warp radix select (8-bit digits, per-warp
-//    256-bin smem histogram, warp scan) — exact top-m membership in O(c) — warp-scans the keep
-//    mask (ballot/popc) into new slot indices, then moves K, V and pos rows in ascending
-//    slot order, in place: a kept row's new slot is never after its old one, and each chunk
-//    of rows is fully read (16-byte coalesced loads, 8 rows in flight per warp) before any
-//    of it is written.
+//  * select (persistent grid, one WARP per (node, row) work item, no block barriers):
+//    pos tags + A keys of the kept slots, the m-th largest unique 48-bit key ⟨A bits, pos⟩
+//    by a warp radix select (8-bit digits, per-warp smem histogram, warp scan) — exact top-m
+//    membership in O(c) — then hole-filling: kept rows inside the new prefix [0, k_app)
+//    stay, the i-th hole takes the i-th kept row from beyond it (Q23').  Sources
+//    and destinations are disjoint, so the (src, dst) row pairs go to a global list.
+//  * move (persistent grid): a pure 16-byte-coalesced streaming copy of the listed K, V
+//    rows and pos tags — no ordering constraints, full occupancy.
 #include <cub/block/block_scan.cuh>
 
-#include "common.cuh"
+#include "tile.cuh"
 
 namespace arbor {
 namespace {
@@ -100,6 +100,7 @@ evict_plan_kernel(PlanArgs a) {
   if (threadIdx.x == 0) {
     a.ctrl->free_top = top + tot_free;
     a.ctrl->work_count = tot_work;
+    a.ctrl->move_count = 0;
     a.ctrl->evicted = tot_ev;
     a.ctrl->pages_in_use -= tot_free;
   }
@@ -117,45 +118,46 @@ struct CompactArgs {
   const int32_t *ptab;
   void *kpool, *vpool;
   int16_t *pos;
+  int2 *moves;      // (src row, dst row) pairs
   int esize;
   int cap;          // max n over evicted nodes (smem capacity, slots)
   int lgP;          // log2(page size)
 };
 
-__device__ __forceinline__ int64_t row_of(const CompactArgs &a, const int32_t *pl, int l, int h,
-                                          int slot) {
-  return ((static_cast<int64_t>(l) * a.NP + pl[slot / a.P]) * a.H + h) * a.P + (slot % a.P);
-}
+constexpr int kWarps = 8;     // warps per CTA in the select kernel (one warp per work item)
+// fused: each warp streams its own item's moves right after selecting it (other warps'
+// selection latency hides under those moves); split: select → global list → move_kernel
+constexpr bool kFusedCompact = true;
+constexpr bool kWarpSpecialised = true;   // select_move_ws_kernel (below) is the default
 
-constexpr int kWarps = 8;     // warps per CTA; one warp owns one (node, row) work item
-constexpr int kUnroll = 4;    // row-chunks in flight per lane during the move
-
-// Warp-per-item select + compact.  smem per warp: key[cap] (u64), the move list[cap]
-// (u32: src slot | dst slot << 16) and the node's page list[cap / P + 1].
-__global__ void __launch_bounds__(kWarps * 32, 4)
-select_compact_kernel(CompactArgs a) {
+// Select: one WARP per (node, row) work item.  Keep = the block tail 𝒯 (positions ≥ n − |𝒯|,
+// P:177-182) ∪ the top-m non-tail candidates by the 48-bit key ⟨A bits, pos⟩,
+// or the last k_app positions when k_app ≤ |𝒯| (Alg. 1).  The m-th largest key is
+// found by a warp radix select (8-bit digits, per-warp 256-bin smem histogram, warp scan):
+// exact, O(c).  Slot layout (Q23'): kept rows in slots [0, k_app) stay; the i-th
+// hole there takes the i-th kept row from slots ≥ k_app — sources and destinations are
+// disjoint, so the moves are appended to a global list and executed by move_kernel.
+// smem per warp: key[cap] (u64), hole list[cap], mover list[cap] (u16 pairs), pages.
+template <bool kFused>
+__global__ void __launch_bounds__(kWarps * 32, kFused ? 4 : 5)
+select_kernel(CompactArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cap = a.cap;
   const int lgP = a.lgP, Pm = (1 << lgP) - 1;
   const int pcap = (cap >> lgP) + 1;
   unsigned long long *key = reinterpret_cast<unsigned long long *>(sm) + warp * cap;
-  uint32_t *mlist = reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned long long *>(sm) +
-                                                 kWarps * cap) + warp * cap;
-  int32_t *pgs = reinterpret_cast<int32_t *>(reinterpret_cast<uint32_t *>(
-                     reinterpret_cast<unsigned long long *>(sm) + kWarps * cap) + kWarps * cap) +
-                 warp * pcap;
+  int32_t *holes = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned long long *>(sm) +
+                                               kWarps * cap) + warp * 2 * cap;
+  int32_t *movers = holes + cap;
+  int32_t *pgs = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned long long *>(sm) +
+                                             kWarps * cap) + kWarps * 2 * cap + warp * pcap;
   __shared__ uint32_t hist_all[kWarps][256];
   uint32_t *hist = hist_all[warp];
   const int items = a.ctrl_ro->work_count * a.R;
-  const int rb = a.D * a.esize;          // row bytes
-  const int cpr = rb >> 4;               // 16-byte pieces per row (≤ 32)
-  const int rpi = 32 / cpr;              // rows per warp instruction
-  const int my_piece = lane % cpr, my_row = lane / cpr;
   const unsigned lt_mask = (1u << lane) - 1u;
-  char *kp8 = static_cast<char *>(a.kpool);
-  char *vp8 = static_cast<char *>(a.vpool);
-  const int64_t pstride = static_cast<int64_t>(a.H) << lgP;   // rows between consecutive pages
+  const int64_t pstride = static_cast<int64_t>(a.H) << lgP;
+  constexpr unsigned long long kCand = 1ull << 63;
   for (int it = blockIdx.x * kWarps + warp; it < items; it += gridDim.x * kWarps) {
     const int w = it / a.R, r = it - w * a.R;
     const int l = r / a.H, h = r - l * a.H;
@@ -170,135 +172,399 @@ select_compact_kernel(CompactArgs a) {
     auto row = [&](int slot) -> int64_t {
       return base + static_cast<int64_t>(pgs[slot >> lgP]) * pstride + (slot & Pm);
     };
-    // 1. candidates: when k_app > |𝒯| the tail (the last |𝒯| slots, all present) is kept and
-    //    the non-tail slots 0..nc-1 compete by key; otherwise the last k_app slots are kept
-    //    (Alg. 1) and no key is needed.
     const bool ranked = ka > tl;
-    const int nc = ranked ? kc - tl : 0;
     const int m = ka - tl;
-    // threshold: keep a candidate iff (key & tmask) >= tkey — the top m keys (unique)
-    unsigned long long tkey = ~0ull, tmask = ~0ull;
-    if (ranked) {
-      const float *Arow =
-          a.A + (static_cast<int64_t>(l) * a.H + h) * a.max_tokens + a.span[node];
-      for (int s = lane; s < nc; s += 32) {
-        const int p = a.pos[row(s)];
-        const float av = Arow[p];
-        if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-        const unsigned bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
-        key[s] = (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
-      }
-      __syncwarp();
-      if (m <= 0) {
-        tkey = ~0ull;                      // no heavy hitter survives
-      } else if (m >= nc) {
-        tkey = 0; tmask = 0;               // every candidate survives
-      } else {
-        // warp radix select of the m-th largest 48-bit key, 8-bit digits MSB first
-        unsigned long long prefix = 0, pmask = 0;
-        int need = m;
-        for (int shift = 40; shift >= 0; shift -= 8) {
-#pragma unroll
-          for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
-          __syncwarp();
-          for (int s = lane; s < nc; s += 32) {
-            const unsigned long long k = key[s];
-            if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
-          }
-          __syncwarp();
-          // lane owns digits 255-8*lane … 248-8*lane (descending); counts from the top
-          uint32_t c[8];
-          uint32_t loc = 0;
-#pragma unroll
-          for (int b = 0; b < 8; ++b) { c[b] = hist[255 - lane * 8 - b]; loc += c[b]; }
-          uint32_t incl = loc;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-          }
-          const uint32_t before = incl - loc;
-          const bool mine = before < static_cast<uint32_t>(need) &&
-                            static_cast<uint32_t>(need) <= incl;
-          int dsel = 0;
-          uint32_t above = 0, inbin = 0;
-          if (mine) {
-            uint32_t acc = before;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-              if (acc < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= acc + c[b] &&
-                  inbin == 0) {
-                dsel = 255 - lane * 8 - b;
-                above = acc;
-                inbin = c[b];
-              }
-              acc += c[b];
-            }
-          }
-          const unsigned who = __ballot_sync(0xffffffffu, mine);
-          const int src = __ffs(who) - 1;
-          dsel = __shfl_sync(0xffffffffu, dsel, src);
-          above = __shfl_sync(0xffffffffu, above, src);
-          inbin = __shfl_sync(0xffffffffu, inbin, src);
-          need -= static_cast<int>(above);
-          prefix |= static_cast<unsigned long long>(dsel) << shift;
-          pmask |= 255ull << shift;
-          if (static_cast<uint32_t>(need) == inbin) break;   // the whole bin survives
-        }
-        tkey = prefix;
-        tmask = pmask;
-      }
-    }
-    // 2. keep decision, warp scan of the keep mask in slot order → new slot, move list
-    int carry = 0, nmoves = 0;
-    for (int b0 = 0; b0 < kc; b0 += 32) {
-      const int s = b0 + lane;
-      int keep = 0;
+    const int tail_from = n - (ranked ? tl : ka);   // keep positions ≥ tail_from outright
+    // 1. pos tags of every kept slot; keys of the non-tail candidates (bit 63 = candidate)
+    const float *Arow = a.A + (static_cast<int64_t>(l) * a.H + h) * a.max_tokens + a.span[node];
+    int ncand = 0;
+    for (int s0 = 0; s0 < kc; s0 += 32) {
+      const int s = s0 + lane;
+      unsigned long long kk = 0;
       if (s < kc) {
-        if (!ranked) keep = s >= kc - ka;
-        else if (s >= nc) keep = 1;                                  // tail 𝒯_i
-        else keep = (key[s] & tmask) >= tkey;                        // Top-m_i by A_i(t)
+        const int p = a.pos[row(s)];
+        kk = static_cast<unsigned>(p);   // pos in the low bits; no candidate bit
+        if (ranked && p < tail_from) {
+          const float av = Arow[p];
+          if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+          const unsigned bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
+          kk = kCand | (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
+        }
+        key[s] = kk;
       }
-      const unsigned kb = __ballot_sync(0xffffffffu, keep);
-      const int ns = carry + __popc(kb & lt_mask);
-      carry += __popc(kb);
-      const int mv = keep && ns != s;
-      const unsigned mb = __ballot_sync(0xffffffffu, mv);
-      if (mv) mlist[nmoves + __popc(mb & lt_mask)] = static_cast<uint32_t>(s) |
-                                                      (static_cast<uint32_t>(ns) << 16);
-      nmoves += __popc(mb);
+      ncand += __popc(__ballot_sync(0xffffffffu, (kk & kCand) != 0));
     }
     __syncwarp();
-    // 3. in-place stable gather: each chunk of rows is read completely into registers
-    //    before any of it is written (a kept row never moves to a later slot)
-    const int chunk_rows = rpi * kUnroll;
-    for (int c0 = 0; c0 < nmoves; c0 += chunk_rows) {
-      uint4 bk[kUnroll], bv[kUnroll];
-      int16_t ptag[kUnroll];
+    // 2. threshold: keep a candidate iff (key & tmask) >= tkey (the top m unique keys)
+    unsigned long long tkey = kCand, tmask = kCand;     // m ≥ ncand: all candidates
+    if (ranked && m <= 0) {
+      tkey = ~0ull; tmask = ~0ull;                      // none survives
+    } else if (ranked && m < ncand) {
+      unsigned long long prefix = kCand, pmask = kCand;
+      int need = m;
+      for (int shift = 40; shift >= 0; shift -= 8) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int rr = c0 + u * rpi + my_row;
-        if (rr < nmoves) {
-          const int64_t srow = row(static_cast<int>(mlist[rr] & 0xffffu));
-          const int64_t off = srow * rb + my_piece * 16;
-          bk[u] = *reinterpret_cast<const uint4 *>(kp8 + off);
-          bv[u] = *reinterpret_cast<const uint4 *>(vp8 + off);
-          if (my_piece == 0) ptag[u] = a.pos[srow];
+        for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
+        __syncwarp();
+        for (int s = lane; s < kc; s += 32) {
+          const unsigned long long k = key[s];
+          if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+        }
+        __syncwarp();
+        uint32_t c[8];
+        uint32_t loc = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) { c[b] = hist[255 - lane * 8 - b]; loc += c[b]; }
+        uint32_t incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t before = incl - loc;
+        const bool mine = before < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= incl;
+        int dsel = 0;
+        uint32_t above = 0, inbin = 0;
+        if (mine) {
+          uint32_t acc = before;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            if (inbin == 0 && acc < static_cast<uint32_t>(need) &&
+                static_cast<uint32_t>(need) <= acc + c[b]) {
+              dsel = 255 - lane * 8 - b;
+              above = acc;
+              inbin = c[b];
+            }
+            acc += c[b];
+          }
+        }
+        const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        dsel = __shfl_sync(0xffffffffu, dsel, src);
+        above = __shfl_sync(0xffffffffu, above, src);
+        inbin = __shfl_sync(0xffffffffu, inbin, src);
+        need -= static_cast<int>(above);
+        prefix |= static_cast<unsigned long long>(dsel) << shift;
+        pmask |= 255ull << shift;
+        if (static_cast<uint32_t>(need) == inbin) break;   // the whole bin survives
+      }
+      tkey = prefix;
+      tmask = pmask;
+    }
+    // 3. keep flags → holes (dropped slots < k_app) and movers (kept slots ≥ k_app), ascending
+    int nh = 0, nm = 0;
+    for (int s0 = 0; s0 < kc; s0 += 32) {
+      const int s = s0 + lane;
+      int keep = 0;
+      if (s < kc) {
+        const unsigned long long k = key[s];
+        const int p = static_cast<int>(k & 0xffffu);
+        keep = (p >= tail_from) || (ranked && (k & kCand) && (k & tmask) >= tkey);
+      }
+      const int hole = s < ka && !keep;
+      const int mover = s >= ka && s < kc && keep;
+      const unsigned hb = __ballot_sync(0xffffffffu, hole);
+      const unsigned mb = __ballot_sync(0xffffffffu, mover);
+      if (hole) holes[nh + __popc(hb & lt_mask)] = s;
+      if (mover) movers[nm + __popc(mb & lt_mask)] = s;
+      nh += __popc(hb);
+      nm += __popc(mb);
+    }
+    __syncwarp();
+    if (nh != nm && lane == 0) atomicOr(&a.ctrl->err, DERR_STATE);
+    if (kFused) {
+      // 4'. stream this item's moves directly (disjoint sources/destinations: no barriers)
+      const int rb = a.D * a.esize, cpr = rb >> 4, rpi = 32 / cpr;
+      const int piece = lane % cpr, sub = lane / cpr;
+      char *kp8 = static_cast<char *>(a.kpool);
+      char *vp8 = static_cast<char *>(a.vpool);
+      constexpr int kU = 4;
+      for (int c0 = 0; c0 < nm; c0 += rpi * kU) {
+        uint4 bk[kU], bv[kU];
+        int64_t srow[kU], drow[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int i = c0 + u * rpi + sub;
+          srow[u] = -1;
+          if (i < nm) {
+            srow[u] = row(movers[i]);
+            drow[u] = row(holes[i]);
+            bk[u] = *reinterpret_cast<const uint4 *>(kp8 + srow[u] * rb + piece * 16);
+            bv[u] = *reinterpret_cast<const uint4 *>(vp8 + srow[u] * rb + piece * 16);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if (srow[u] >= 0) {
+            *reinterpret_cast<uint4 *>(kp8 + drow[u] * rb + piece * 16) = bk[u];
+            *reinterpret_cast<uint4 *>(vp8 + drow[u] * rb + piece * 16) = bv[u];
+            if (piece == 0) a.pos[drow[u]] = static_cast<int16_t>(key[movers[c0 + u * rpi + sub]] & 0xffffu);
+          }
         }
       }
       __syncwarp();
+    } else {
+      // 4. append the (src, dst) row pairs to the global move list
+      int baseidx = 0;
+      if (lane == 0 && nm > 0) baseidx = atomicAdd(&a.ctrl->move_count, nm);
+      baseidx = __shfl_sync(0xffffffffu, baseidx, 0);
+      for (int i = lane; i < nm; i += 32)
+        a.moves[baseidx + i] = make_int2(static_cast<int>(row(movers[i])), static_cast<int>(row(holes[i])));
+      __syncwarp();
+    }
+  }
+}
+
+// Warp-specialised select + move (default).  A CTA holds kPairs (select warp, move warp)
+// pairs.  Select warp p processes the work items it, it + stride, … exactly like select_kernel
+// and hands each item's (src row, dst row) list to its move warp through a 2-slot job queue
+// in shared memory guarded by mbarriers (full / empty); move warp p streams those rows (K, V:
+// 16-byte coalesced, kUw rows in flight per lane group; pos tags) while its select warp
+// already ranks the next item.  Selection (latency-bound) and data movement (HBM-bound) thus
+// overlap inside every SM.
+constexpr int kPairs = 8;
+constexpr int kUw = 4;
+__global__ void __launch_bounds__(kPairs * 64, 2)
+select_move_ws_kernel(CompactArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool mover = warp >= kPairs;
+  const int pid = mover ? warp - kPairs : warp;
+  const int cap = a.cap;
+  const int jcap = cap / 2 + 1;                    // moves per item ≤ min(k_app, k_cur − k_app)
+  const int lgP = a.lgP, Pm = (1 << lgP) - 1;
+  const int pcap = (cap >> lgP) + 1;
+  // smem: per select warp key[cap] u64, holes/movers[cap] i32 x2, pages[pcap];
+  //       per pair jobs[2][jcap] int2 + counts[2]; mbarriers full[pair][2], empty[pair][2]
+  unsigned long long *keys = reinterpret_cast<unsigned long long *>(sm);
+  int32_t *lists = reinterpret_cast<int32_t *>(keys + kPairs * cap);
+  int32_t *pages_all = lists + kPairs * 2 * cap;
+  int2 *jobs = reinterpret_cast<int2 *>(pages_all + ((kPairs * pcap + 1) & ~1));
+  int32_t *jcount = reinterpret_cast<int32_t *>(jobs + kPairs * 2 * jcap);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(jcount + ((kPairs * 2 + 1) & ~1));
+  uint64_t *full = bars + pid * 4, *empty = bars + pid * 4 + 2;
+  __shared__ uint32_t hist_all[kPairs][256];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPairs * 2; ++i) {
+      mbar_init(&bars[(i >> 1) * 4 + (i & 1)], 1);
+      mbar_init(&bars[(i >> 1) * 4 + 2 + (i & 1)], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int items = a.ctrl_ro->work_count * a.R;
+  const int stride = gridDim.x * kPairs;
+  int2 *myjobs = jobs + pid * 2 * jcap;
+  int32_t *mycount = jcount + pid * 2;
+  if (mover) {
+    // ------------------------------------------------------------ move warp
+    const int rb = a.D * a.esize, cpr = rb >> 4, rpi = 32 / cpr;
+    const int piece = lane % cpr, sub = lane / cpr;
+    char *kp8 = static_cast<char *>(a.kpool);
+    char *vp8 = static_cast<char *>(a.vpool);
+    int k = 0;
+    for (int it = blockIdx.x * kPairs + pid; it < items; it += stride, ++k) {
+      const int sl = k & 1;
+      mbar_wait(&full[sl], (k >> 1) & 1);
+      const int nm = mycount[sl];
+      const int2 *jb = myjobs + sl * jcap;
+      for (int c0 = 0; c0 < nm; c0 += rpi * kUw) {
+        uint4 bk[kUw], bv[kUw];
+        int2 mv[kUw];
+        int16_t pt[kUw];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int rr = c0 + u * rpi + my_row;
-        if (rr < nmoves) {
-          const int64_t drow = row(static_cast<int>(mlist[rr] >> 16));
-          const int64_t off = drow * rb + my_piece * 16;
-          *reinterpret_cast<uint4 *>(kp8 + off) = bk[u];
-          *reinterpret_cast<uint4 *>(vp8 + off) = bv[u];
-          if (my_piece == 0) a.pos[drow] = ptag[u];
+        for (int u = 0; u < kUw; ++u) {
+          const int i = c0 + u * rpi + sub;
+          mv[u] = i < nm ? jb[i] : make_int2(-1, -1);
+          if (mv[u].x >= 0) {
+            const int64_t off = static_cast<int64_t>(mv[u].x) * rb + piece * 16;
+            bk[u] = *reinterpret_cast<const uint4 *>(kp8 + off);
+            bv[u] = *reinterpret_cast<const uint4 *>(vp8 + off);
+            if (piece == 0) pt[u] = a.pos[mv[u].x];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUw; ++u) {
+          if (mv[u].x >= 0) {
+            const int64_t off = static_cast<int64_t>(mv[u].y) * rb + piece * 16;
+            *reinterpret_cast<uint4 *>(kp8 + off) = bk[u];
+            *reinterpret_cast<uint4 *>(vp8 + off) = bv[u];
+            if (piece == 0) a.pos[mv[u].y] = pt[u];
+          }
         }
       }
       __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[sl]);
+    }
+    return;
+  }
+  // -------------------------------------------------------------- select warp
+  unsigned long long *key = keys + pid * cap;
+  int32_t *holes = lists + pid * 2 * cap;
+  int32_t *movers = holes + cap;
+  int32_t *pgs = pages_all + pid * pcap;
+  uint32_t *hist = hist_all[pid];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t pstride = static_cast<int64_t>(a.H) << lgP;
+  constexpr unsigned long long kCand = 1ull << 63;
+  int k = 0;
+  for (int it = blockIdx.x * kPairs + pid; it < items; it += stride, ++k) {
+    const int w = it / a.R, r = it - w * a.R;
+    const int l = r / a.H, h = r - l * a.H;
+    const int node = a.work_node[w];
+    const int kc = a.work_old[w], ka = a.work_new[w];
+    const int n = a.n[node];
+    const int tl = min(a.l_tail, n);
+    const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.MPN;
+    const int64_t base = (static_cast<int64_t>(l) * a.NP * a.H + h) << lgP;
+    for (int i = lane; i < ((kc + Pm) >> lgP); i += 32) pgs[i] = pl[i];
+    __syncwarp();
+    auto row = [&](int slot) -> int64_t {
+      return base + static_cast<int64_t>(pgs[slot >> lgP]) * pstride + (slot & Pm);
+    };
+    const bool ranked = ka > tl;
+    const int m = ka - tl;
+    const int tail_from = n - (ranked ? tl : ka);
+    const float *Arow = a.A + (static_cast<int64_t>(l) * a.H + h) * a.max_tokens + a.span[node];
+    int ncand = 0;
+    for (int s0 = 0; s0 < kc; s0 += 32) {
+      const int s = s0 + lane;
+      unsigned long long kk = 0;
+      if (s < kc) {
+        const int p = a.pos[row(s)];
+        kk = static_cast<unsigned>(p);
+        if (ranked && p < tail_from) {
+          const float av = Arow[p];
+          if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+          const unsigned bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
+          kk = kCand | (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
+        }
+        key[s] = kk;
+      }
+      ncand += __popc(__ballot_sync(0xffffffffu, (kk & kCand) != 0));
+    }
+    __syncwarp();
+    unsigned long long tkey = kCand, tmask = kCand;
+    if (ranked && m <= 0) {
+      tkey = ~0ull; tmask = ~0ull;
+    } else if (ranked && m < ncand) {
+      unsigned long long prefix = kCand, pmask = kCand;
+      int need = m;
+      for (int shift = 40; shift >= 0; shift -= 8) {
+#pragma unroll
+        for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
+        __syncwarp();
+        for (int s = lane; s < kc; s += 32) {
+          const unsigned long long kk = key[s];
+          if ((kk & pmask) == prefix) atomicAdd(&hist[(kk >> shift) & 255u], 1u);
+        }
+        __syncwarp();
+        uint32_t cnt8[8];
+        uint32_t loc = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) { cnt8[b] = hist[255 - lane * 8 - b]; loc += cnt8[b]; }
+        uint32_t incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t before = incl - loc;
+        const bool mine = before < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= incl;
+        int dsel = 0;
+        uint32_t above = 0, inbin = 0;
+        if (mine) {
+          uint32_t acc = before;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            if (inbin == 0 && acc < static_cast<uint32_t>(need) &&
+                static_cast<uint32_t>(need) <= acc + cnt8[b]) {
+              dsel = 255 - lane * 8 - b;
+              above = acc;
+              inbin = cnt8[b];
+            }
+            acc += cnt8[b];
+          }
+        }
+        const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        dsel = __shfl_sync(0xffffffffu, dsel, src);
+        above = __shfl_sync(0xffffffffu, above, src);
+        inbin = __shfl_sync(0xffffffffu, inbin, src);
+        need -= static_cast<int>(above);
+        prefix |= static_cast<unsigned long long>(dsel) << shift;
+        pmask |= 255ull << shift;
+        if (static_cast<uint32_t>(need) == inbin) break;
+      }
+      tkey = prefix;
+      tmask = pmask;
+    }
+    int nh = 0, nm = 0;
+    for (int s0 = 0; s0 < kc; s0 += 32) {
+      const int s = s0 + lane;
+      int keep = 0;
+      if (s < kc) {
+        const unsigned long long kk = key[s];
+        const int p = static_cast<int>(kk & 0xffffu);
+        keep = (p >= tail_from) || (ranked && (kk & kCand) && (kk & tmask) >= tkey);
+      }
+      const int hole = s < ka && !keep;
+      const int mv = s >= ka && s < kc && keep;
+      const unsigned hb = __ballot_sync(0xffffffffu, hole);
+      const unsigned mb = __ballot_sync(0xffffffffu, mv);
+      if (hole) holes[nh + __popc(hb & lt_mask)] = s;
+      if (mv) movers[nm + __popc(mb & lt_mask)] = s;
+      nh += __popc(hb);
+      nm += __popc(mb);
+    }
+    __syncwarp();
+    if (nh != nm && lane == 0) atomicOr(&a.ctrl->err, DERR_STATE);
+    // hand the job to the move warp
+    const int sl = k & 1;
+    mbar_wait(&empty[sl], ((k >> 1) & 1) ^ 1);
+    int2 *jb = myjobs + sl * jcap;
+    for (int i = lane; i < nm; i += 32)
+      jb[i] = make_int2(static_cast<int>(row(movers[i])), static_cast<int>(row(holes[i])));
+    if (lane == 0) mycount[sl] = nm;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&full[sl]);
+  }
+}
+
+// Move: a pure streaming copy of K, V (rb bytes each) and the pos tag for every listed pair;
+// sources and destinations are disjoint, so any order is correct.  cpr lanes per row,
+// kUnrollM rows in flight per lane-group.
+constexpr int kUnrollM = 4;
+__global__ void __launch_bounds__(256, 4)
+move_kernel(const Ctrl *__restrict__ ctrl, const int2 *__restrict__ moves, char *__restrict__ kp8,
+            char *__restrict__ vp8, int16_t *__restrict__ pos, int rb) {
+  const int total = ctrl->move_count;
+  const int cpr = rb >> 4;
+  const int rpw = 32 / cpr;                    // rows per warp instruction
+  const int lane = threadIdx.x & 31;
+  const int piece = lane % cpr, sub = lane / cpr;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int per_iter = rpw * kUnrollM;
+  for (int m0 = wg * per_iter; m0 < total; m0 += warps * per_iter) {
+    uint4 bk[kUnrollM], bv[kUnrollM];
+    int2 mv[kUnrollM];
+#pragma unroll
+    for (int u = 0; u < kUnrollM; ++u) {
+      const int mi = m0 + u * rpw + sub;
+      mv[u] = mi < total ? moves[mi] : make_int2(-1, -1);
+      if (mv[u].x >= 0) {
+        const int64_t off = static_cast<int64_t>(mv[u].x) * rb + piece * 16;
+        bk[u] = *reinterpret_cast<const uint4 *>(kp8 + off);
+        bv[u] = *reinterpret_cast<const uint4 *>(vp8 + off);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnrollM; ++u) {
+      if (mv[u].x >= 0) {
+        const int64_t off = static_cast<int64_t>(mv[u].y) * rb + piece * 16;
+        *reinterpret_cast<uint4 *>(kp8 + off) = bk[u];
+        *reinterpret_cast<uint4 *>(vp8 + off) = bv[u];
+        if (piece == 0) pos[mv[u].y] = pos[mv[u].x];
+      }
     }
   }
 }
@@ -348,27 +614,61 @@ void launch_select_compact(arbor_ctx *c, int max_n) {
   a.kpool = c->cfg.k_pool;
   a.vpool = c->cfg.v_pool;
   a.pos = c->cfg.pos_pool;
+  a.moves = c->d.moves;
   a.esize = c->esize;
   const int cap = max_n < 1 ? 1 : max_n;
   a.cap = cap;
   a.lgP = __builtin_ctz(static_cast<unsigned>(c->P));
-  const size_t smem = (static_cast<size_t>(cap) * (8 + 4) + ((cap >> a.lgP) + 1) * 4) * kWarps;
-  static int attr_smem = 0;
-  if (static_cast<int>(smem) > attr_smem) {
-    cudaFuncSetAttribute(select_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem) < 48 * 1024 ? 48 * 1024 : static_cast<int>(smem));
-    attr_smem = static_cast<int>(smem) < 48 * 1024 ? 48 * 1024 : static_cast<int>(smem);
+  const size_t smem = (static_cast<size_t>(cap) * (8 + 8) + ((cap >> a.lgP) + 1) * 4) * kWarps;
+  static size_t attr_smem = 0;
+  if (smem > attr_smem) {
+    cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem < 48 * 1024 ? 48 * 1024 : smem));
+    cudaFuncSetAttribute(select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem < 48 * 1024 ? 48 * 1024 : smem));
+    attr_smem = smem < 48 * 1024 ? 48 * 1024 : smem;
   }
-  int blocks_per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, select_compact_kernel,
-                                                kWarps * 32, smem);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int grid = sms * (blocks_per_sm > 0 ? blocks_per_sm : 1);
+  int per_sm = 0;
+  if (kWarpSpecialised) {
+    const int jcap = cap / 2 + 1;
+    const int pcap = (cap >> a.lgP) + 1;
+    const size_t wsm = static_cast<size_t>(kPairs) * cap * (8 + 8) +
+                       static_cast<size_t>(((kPairs * pcap + 1) & ~1)) * 4 +
+                       static_cast<size_t>(kPairs) * 2 * jcap * 8 + ((kPairs * 2 + 1) & ~1) * 4 +
+                       kPairs * 4 * 8;
+    static size_t wattr = 0;
+    if (wsm > wattr) {
+      cudaFuncSetAttribute(select_move_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(wsm < 48 * 1024 ? 48 * 1024 : wsm));
+      wattr = wsm < 48 * 1024 ? 48 * 1024 : wsm;
+    }
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, select_move_ws_kernel, kPairs * 64, wsm);
+    stage_begin(c, ARBOR_ST_SELECT_COMPACT, c->ms);
+    select_move_ws_kernel<<<sms * (per > 0 ? per : 1), kPairs * 64, wsm, c->ms>>>(a);
+    ARBOR_LAUNCHED(c);
+    stage_end(c, ARBOR_ST_SELECT_COMPACT, c->ms);
+    return;
+  }
+  const bool fused = kFusedCompact;
+  if (fused) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<true>, kWarps * 32, smem);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<false>, kWarps * 32, smem);
   stage_begin(c, ARBOR_ST_SELECT_COMPACT, c->ms);
-  select_compact_kernel<<<grid, kWarps * 32, smem, c->ms>>>(a);
+  if (fused) select_kernel<true><<<sms * (per_sm > 0 ? per_sm : 1), kWarps * 32, smem, c->ms>>>(a);
+  else select_kernel<false><<<sms * (per_sm > 0 ? per_sm : 1), kWarps * 32, smem, c->ms>>>(a);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SELECT_COMPACT, c->ms);
+  if (fused) return;
+  int per_sm_m = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_m, move_kernel, 256, 0);
+  stage_begin(c, ARBOR_ST_COMPACT_MOVE, c->ms);
+  move_kernel<<<sms * (per_sm_m > 0 ? per_sm_m : 1), 256, 0, c->ms>>>(
+      c->d.ctrl, c->d.moves, static_cast<char *>(c->cfg.k_pool), static_cast<char *>(c->cfg.v_pool),
+      c->cfg.pos_pool, c->D * c->esize);
+  ARBOR_LAUNCHED(c);
+  stage_end(c, ARBOR_ST_COMPACT_MOVE, c->ms);
 }
 
 }  // namespace arbor

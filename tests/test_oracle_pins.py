@@ -472,3 +472,34 @@ def test_state_lifecycle_errors():
     o.open_node(tree.num_nodes, tree.end_position())
     with pytest.raises(OracleError):
         o.rehydrate([tree.num_nodes])
+
+
+def test_state_hole_filling_layout():
+    """DESIGN.md Q23': after eviction every row holds exactly the retained set; retained rows
+    already inside [0, k_app) keep their slot; the holes are filled, in ascending order, by the
+    retained rows from slots >= k_app in ascending order."""
+    tree, o, E = _small_state(levels=3, width=3, t_node=20, seed=6)
+    tree.active = [synth.leaves_of(tree)[0]]
+    q = synth.make_queries(1, o.L, o.Hq, o.d, "f32", 9, E).double().numpy()
+    for _ in range(4):
+        o.score_accumulate(tree, q)
+    before = [o.kept[i].copy() for i in range(tree.num_nodes)]
+    a, s = o.msve(tree)
+    k = o.allocate(tree, s, int(tree.total_tokens * 0.6))
+    o.evict(tree, k)
+    Af = o.A.astype(np.float32)
+    for i in range(tree.num_nodes):
+        if o.k_cur(i) == before[i].shape[-1]:
+            continue
+        ka, a0, n = o.k_cur(i), o.span_start[i], o.n[i]
+        for l in range(o.L):
+            for h in range(o.H):
+                old = [int(x) for x in before[i][l, h]]
+                new = [int(x) for x in o.kept[i][l, h]]
+                R = select.retained_set(old, n, ka, o.params["l_tail"], Af[l, h, a0:a0 + n])
+                assert sorted(new) == R
+                stay = [s_ for s_ in range(ka) if old[s_] in R]
+                assert all(new[s_] == old[s_] for s_ in stay)
+                holes = [s_ for s_ in range(ka) if old[s_] not in R]
+                movers = [old[s_] for s_ in range(ka, len(old)) if old[s_] in R]
+                assert [new[s_] for s_ in holes] == movers
