@@ -82,7 +82,7 @@ typedef struct {
   int32_t num_layers, num_kv_heads, num_q_heads, head_dim;          /* global model shape   */
   int32_t layer_begin, layer_count, kv_head_begin, kv_head_count;   /* this rank's shard    */
   int32_t kv_dtype;        /* arbor_dtype of K/V/Q/O                                        */
-  int32_t page_size;       /* P tokens per page: a power of two in 1..1024                   */
+  int32_t page_size;       /* P tokens per page: a power of two in 2..1024                   */
   int32_t num_pages;       /* pages in each pool                                             */
   int32_t max_nodes;       /* capacity of the node table                                     */
   int32_t max_node_tokens; /* capacity of one node (≤ 32767; pos tags are int16)            */

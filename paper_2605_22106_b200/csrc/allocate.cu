@@ -19,7 +19,7 @@
 namespace arbor {
 namespace {
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;
 constexpr double kWeightScale = 16777216.0;   // 2^24
 constexpr double kEps = 1e-9;
 
@@ -36,6 +36,7 @@ struct AllocArgs {
   const double *Ed, *ED;
   int32_t *k_out;
   Ctrl *ctrl;
+  long long *trace; // ARBOR_ALLOC_TRACE builds only: clock64() at phase boundaries
 };
 
 __device__ __forceinline__ int eps_floor_count(double r, int n) {
@@ -50,22 +51,21 @@ __device__ __forceinline__ int keep_count(double r, int n, int k_min, int l_tail
 
 template <typename T>
 __device__ T block_sum(T v, T *red) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // warp shuffle tree → one value per warp → warp 0 reduces → broadcast through red[0]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
-  T tot = 0;
-  for (int i = 0; i < (blockDim.x >> 5); ++i) tot += red[i];
-  __syncthreads();
-  return tot;
-}
-
-__device__ __forceinline__ long long warp_sum64(long long v) {
+  if (w == 0) {
+    T x = lane < nw ? red[lane] : T(0);
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) red[32] = x;
+  }
+  __syncthreads();
+  return red[32];
 }
 
 // floor(X / den) and X mod den for 0 ≤ X < 2^126, 0 < den < 2^62, with a small quotient
@@ -80,8 +80,15 @@ __device__ __forceinline__ void divmod128(unsigned __int128 X, unsigned long lon
   r = static_cast<unsigned long long>(X - p);
 }
 
+#ifdef ARBOR_ALLOC_TRACE
+#define TRACE(i) do { if (threadIdx.x == 0 && a.trace) a.trace[i] = clock64(); } while (0)
+#else
+#define TRACE(i) do { } while (0)
+#endif
+
 __global__ void __launch_bounds__(kThreads)
 allocate_kernel(AllocArgs a) {
+  TRACE(0);
   extern __shared__ __align__(16) unsigned char sm[];
   const int N = a.N;
   long long *W = reinterpret_cast<long long *>(sm);            // [N]
@@ -90,7 +97,7 @@ allocate_kernel(AllocArgs a) {
   int *f = nn + N;                                              // [N]
   int *k = f + N;                                               // [N]
   int *cls = k + N;                                             // [N] class
-  __shared__ long long red64[kThreads / 32];
+  __shared__ long long red64[33];
   __shared__ unsigned long long best_num, best_den;
   __shared__ int best_set;
 
@@ -132,6 +139,7 @@ allocate_kernel(AllocArgs a) {
     }
   }
   __syncthreads();
+  TRACE(1);
 
   if (a.mode == 2) {
     // STATIC_DRAIN: while Σk > 𝓑: j = argmin Priority (W asc, larger id first) over
@@ -196,6 +204,7 @@ allocate_kernel(AllocArgs a) {
     SnP = block_sum(SnP, red64);
     SfZ = block_sum(SfZ, red64);
     SslZ = block_sum(SslZ, red64);
+    TRACE(2);
     const long long Bp = a.budget - pinned_n;
     if (T <= a.budget || Bp >= free_n) {
       // full retention (k = n already)
@@ -228,28 +237,32 @@ allocate_kernel(AllocArgs a) {
       for (int j = threadIdx.x; j < N; j += blockDim.x)
         if (cls[j] == 2) k[j] = f[j];
       const long long Bpp = Bp - SfZ;
-      // candidate breakpoints: c = 2j → W_j/n_j, c = 2j+1 → W_j/f_j (f_j > 0); each thread
-      // keeps its largest feasible candidate, then a block max over rationals
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      // S(λ) = Σ_j clamp(W_j/λ, f_j, n_j) is nonincreasing; its breakpoints are W_j/n_j and
+      // W_j/f_j (f_j > 0).  One thread per candidate β evaluates S(β) exactly over all
+      // positive-weight nodes (smem broadcast reads, independent iterations) and keeps the
+      // largest feasible β: S(β) ≥ 𝓑'' ⇔ SA·den ≥ (𝓑'' − Sb)·num (128-bit products).
       long long my_num = 0, my_den = 1;
       int my_set = 0;
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-      for (int c = wid; c < 2 * N; c += nw) {   // one warp per candidate, lanes over nodes
+      for (int c = threadIdx.x; c < 2 * N; c += blockDim.x) {
         const int j = c >> 1;
         if (cls[j] != 1) continue;
         const long long cden = (c & 1) ? f[j] : nn[j];
         if (cden <= 0) continue;
         const long long cnum = W[j];
         long long SA = 0, Sb = 0;
-        for (int i = lane; i < N; i += 32) {
-          if (cls[i] != 1) continue;
-          const long long Wd = W[i] * cden;                      // < 2^55
-          if (Wd >= static_cast<long long>(nn[i]) * cnum) Sb += nn[i];          // capped at β
-          else if (f[i] > 0 && Wd <= static_cast<long long>(f[i]) * cnum) Sb += f[i];  // floored
-          else SA += W[i];
+#pragma unroll 4
+        for (int i = 0; i < N; ++i) {
+          const int ci = cls[i];
+          const long long Wi = W[i];
+          const long long ni = nn[i], fi = f[i];
+          const long long Wd = Wi * cden;                              // < 2^55
+          const bool capped = Wd >= ni * cnum;
+          const bool floored = !capped && fi > 0 && Wd <= fi * cnum;
+          const bool on = ci == 1;
+          Sb += on ? (capped ? ni : (floored ? fi : 0)) : 0;
+          SA += (on && !capped && !floored) ? Wi : 0;
         }
-        SA = warp_sum64(SA);
-        Sb = warp_sum64(Sb);
-        // S(β) ≥ 𝓑''  ⇔  SA·den ≥ (𝓑'' − Sb)·num
         const __int128 lhs = static_cast<__int128>(SA) * cden;
         const __int128 rhs = static_cast<__int128>(Bpp - Sb) * cnum;
         if (lhs >= rhs && (!my_set || cnum * my_den > my_num * cden)) {
@@ -267,24 +280,20 @@ allocate_kernel(AllocArgs a) {
       }
       __shared__ long long wnum[kThreads / 32], wden[kThreads / 32];
       __shared__ int wset[kThreads / 32];
-      if ((threadIdx.x & 31) == 0) {
-        wnum[threadIdx.x >> 5] = my_num;
-        wden[threadIdx.x >> 5] = my_den;
-        wset[threadIdx.x >> 5] = my_set;
-      }
+      if (lane == 0) { wnum[wid] = my_num; wden[wid] = my_den; wset[wid] = my_set; }
       __syncthreads();
       if (threadIdx.x == 0) {
         long long bn = 0, bd = 1;
         int bs = 0;
-        for (int w = 0; w < (blockDim.x >> 5); ++w) {
+        for (int w = 0; w < nw; ++w)
           if (wset[w] && (!bs || wnum[w] * bd > bn * wden[w])) { bn = wnum[w]; bd = wden[w]; bs = 1; }
-        }
         if (!bs) atomicOr(&a.ctrl->err, DERR_INVARIANT);
         best_num = static_cast<unsigned long long>(bn);
         best_den = static_cast<unsigned long long>(bd);
         best_set = bs;
       }
       __syncthreads();
+      TRACE(4);
       const long long bnum = static_cast<long long>(best_num);
       const long long bden = static_cast<long long>(best_den);
       // classify the open interval just above β
@@ -312,22 +321,24 @@ allocate_kernel(AllocArgs a) {
         given += static_cast<long long>(q);
       }
       given = block_sum(given, red64);
+      TRACE(5);
       const long long leftover = Num - given;
       __syncthreads();
-      for (int j = wid; j < N && leftover > 0; j += nw) {   // warp per node, lanes over nodes
+      for (int j = threadIdx.x; j < N && leftover > 0; j += blockDim.x) {   // thread per node
         if (cls[j] != 6) continue;
+        const long long rj = rem[j], Wj = W[j];
         int rank = 0;
-        for (int i0 = 0; i0 < N; i0 += 32) {
-          const int i = i0 + lane;
-          const bool gt = i < N && cls[i] == 6 &&
-                          (rem[i] > rem[j] || (rem[i] == rem[j] && (W[i] > W[j] || (W[i] == W[j] && i < j))));
-          rank += __popc(__ballot_sync(0xffffffffu, gt));
+#pragma unroll 4
+        for (int i = 0; i < N; ++i) {
+          const long long ri = rem[i], Wi = W[i];
+          rank += (cls[i] == 6) && (ri > rj || (ri == rj && (Wi > Wj || (Wi == Wj && i < j))));
         }
-        if (lane == 0 && rank < leftover) k[j] += 1;
+        if (rank < leftover) k[j] += 1;
       }
     }
   }
   __syncthreads();
+  TRACE(6);
   for (int j = threadIdx.x; j < N; j += blockDim.x) a.k_out[j] = k[j];
 }
 
@@ -357,10 +368,11 @@ void launch_allocate(arbor_ctx *c, int N, const float *s, int64_t budget, int32_
   a.ED = c->d.ED;
   a.k_out = k_out;
   a.ctrl = c->d.ctrl;
+  a.trace = c->d.alloc_trace;
   const size_t smem = static_cast<size_t>(N) * (2 * sizeof(long long) + 4 * sizeof(int));
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(allocate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(allocate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
   stage_begin(c, ARBOR_ST_ALLOCATE, c->ms);

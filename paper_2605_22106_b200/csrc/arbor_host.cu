@@ -237,8 +237,7 @@ arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
 
 // ---------------------------------------------------------------- attention / score plan
 struct HostPlan {
-  std::vector<int32_t> ch_node, ch_chunk, ch_poff, ch_pcnt, it_chunk, it_j0, it_cnt, pair_b,
-      bp_off, bp_list;
+  std::vector<int32_t> ch_node, ch_chunk, ch_poff, ch_pcnt, it_rec, pair_b, bp_off, bp_list;
   std::vector<std::vector<int32_t>> paths;
 };
 
@@ -266,10 +265,11 @@ void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan 
       p.ch_poff.push_back(static_cast<int32_t>(p.pair_b.size()));
       p.ch_pcnt.push_back(lc);
       p.pair_b.insert(p.pair_b.end(), leaves[x].begin(), leaves[x].end());
-      for (int j0 = 0; j0 < lc; j0 += kLeavesPerItem) {
-        p.it_chunk.push_back(c);
-        p.it_j0.push_back(j0);
-        p.it_cnt.push_back(std::min(kLeavesPerItem, lc - j0));
+      for (int j0 = 0; j0 < lc; j0 += kLeavesPerItem) {   // {node, c0, pair base, cnt}
+        p.it_rec.push_back(x);
+        p.it_rec.push_back(ch * kAttnChunk);
+        p.it_rec.push_back(p.ch_poff[c] + j0);
+        p.it_rec.push_back(std::min(kLeavesPerItem, lc - j0));
       }
     }
   }
@@ -295,9 +295,9 @@ arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
     packed.insert(packed.end(), v.begin(), v.end());
     return off;
   };
+  const size_t o_ir = put(p.it_rec);   // first: 16-byte aligned int4 records
   const size_t o_cn = put(p.ch_node), o_cc = put(p.ch_chunk), o_cpo = put(p.ch_poff),
-               o_cpc = put(p.ch_pcnt), o_ic = put(p.it_chunk), o_ij = put(p.it_j0),
-               o_in = put(p.it_cnt), o_pb = put(p.pair_b), o_bpo = put(p.bp_off),
+               o_cpc = put(p.ch_pcnt), o_pb = put(p.pair_b), o_bpo = put(p.bp_off),
                o_bpl = put(p.bp_list);
   const size_t o_extra = packed.size();
   if (extra) put(*extra);
@@ -314,14 +314,12 @@ arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
   pv.ch_chunk = base + o_cc;
   pv.ch_poff = base + o_cpo;
   pv.ch_pcnt = base + o_cpc;
-  pv.it_chunk = base + o_ic;
-  pv.it_j0 = base + o_ij;
-  pv.it_cnt = base + o_in;
+  pv.it_rec = reinterpret_cast<const int4 *>(base + o_ir);
   pv.pair_b = base + o_pb;
   pv.bp_off = base + o_bpo;
   pv.bp_list = base + o_bpl;
   pv.C = static_cast<int>(p.ch_node.size());
-  pv.I = static_cast<int>(p.it_chunk.size());
+  pv.I = static_cast<int>(p.it_rec.size() / 4);
   pv.nA = nA;
   pv.P = static_cast<int>(p.pair_b.size());
   if (d_extra) *d_extra = base + o_extra;
@@ -495,7 +493,7 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   if (k.kv_head_begin < 0 || k.kv_head_count < 1 || k.kv_head_begin + k.kv_head_count > k.num_kv_heads)
     return ARBOR_ERR_INVALID_ARG;
   if (k.kv_dtype != ARBOR_F32 && k.kv_dtype != ARBOR_BF16) return ARBOR_ERR_INVALID_ARG;
-  if (k.page_size < 1 || k.page_size > 1024 || (k.page_size & (k.page_size - 1)) || k.num_pages < 1)
+  if (k.page_size < 2 || k.page_size > 1024 || (k.page_size & (k.page_size - 1)) || k.num_pages < 1)
     return ARBOR_ERR_INVALID_ARG;   // page size: a power of two (shift addressing)
   if (k.max_nodes < 1 || k.max_nodes > 4096) return ARBOR_ERR_INVALID_ARG;
   if (k.max_node_tokens < 1 || k.max_node_tokens > 32767) return ARBOR_ERR_INVALID_ARG;
@@ -996,6 +994,13 @@ arbor_status arbor_load_state(arbor_ctx *c, int32_t slot) {
 }
 
 int64_t arbor_launch_count(const arbor_ctx *c) { return c ? c->launches : 0; }
+
+#ifdef ARBOR_ALLOC_TRACE
+arbor_status arbor_debug_set_alloc_trace(arbor_ctx *c, long long *trace) {
+  c->d.alloc_trace = trace;
+  return ARBOR_OK;
+}
+#endif
 
 arbor_status arbor_invalidate_masses(arbor_ctx *c) {
   if (!c) return ARBOR_ERR_INVALID_ARG;

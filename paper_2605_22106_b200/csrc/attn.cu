@@ -47,7 +47,7 @@ struct StreamArgs {
 };
 
 struct StageHdr {
-  int nt, item, li, h;
+  int nt, li, h, pbase, cnt, pad0, pad1, pad2;
 };
 
 template <typename T>
@@ -112,46 +112,59 @@ attn_stream_kernel(StreamArgs a) {
   const T *q = static_cast<const T *>(a.q);
   if (warp == 0) {
     // ------------------------------------------------------------- producer (TMA)
-    if (lane == 0) {
-      const T *kpool = static_cast<const T *>(a.kpool);
-      const T *vpool = static_cast<const T *>(a.vpool);
-      int k = 0;
-      for (int it = blockIdx.x; it < total; it += gridDim.x, ++k) {
-        const int st = k % kNst;
-        const uint32_t ph = (k / kNst) & 1u;
-        mbar_wait(&empty[st], ph ^ 1u);
-        const int h = it % a.g.H;
-        const int li = (it / a.g.H) % a.Lc;
-        const int item = it / (a.g.H * a.Lc);
-        const int c = a.pv.it_chunk[item];
-        const int node = a.pv.ch_node[c];
-        const int c0 = a.pv.ch_chunk[c] * kCh;
-        const int nt = max(0, min(kCh, a.kcur[node] - c0));
-        const int cnt = a.pv.it_cnt[item];
-        hdr[st] = StageHdr{nt, item, li, h};
-        T *Ks = stage0 + st * stage_elems;
-        T *Vs = Ks + kCh * D;
-        T *Qs = Vs + kCh * D;
+    // The whole warp fetches an item's metadata (one int4 record, then k_cur, page ids and
+    // pair ids in parallel) one item ahead; lane i issues the bulk copies of page i.
+    const T *kpool = static_cast<const T *>(a.kpool);
+    const T *vpool = static_cast<const T *>(a.vpool);
+    const int lgP = 31 - __clz(a.g.P);
+    const int pages_per_item = a.g.P >= kCh ? 1 : kCh / a.g.P;
+    struct Meta { int4 rec; int kc, page, b; };
+    auto fetch = [&](int it, Meta &m) {
+      if (it >= total) return;
+      const int item = it / (a.g.H * a.Lc);
+      m.rec = a.pv.it_rec[item];
+      m.kc = a.kcur[m.rec.x];
+      m.page = lane < pages_per_item
+                   ? a.ptab[static_cast<int64_t>(m.rec.x) * a.g.MPN + (m.rec.y >> lgP) + lane] : 0;
+      m.b = lane < m.rec.w ? a.pv.pair_b[m.rec.z + lane] : 0;
+    };
+    Meta cur{}, nxt{};
+    fetch(blockIdx.x, cur);
+    int k = 0;
+    for (int it = blockIdx.x; it < total; it += gridDim.x, ++k) {
+      fetch(it + gridDim.x, nxt);                  // loads in flight during the wait below
+      const int st = k % kNst;
+      const uint32_t ph = (k / kNst) & 1u;
+      const int h = it % a.g.H;
+      const int li = (it / a.g.H) % a.Lc;
+      const int node = cur.rec.x, c0 = cur.rec.y, pbase = cur.rec.z, cnt = cur.rec.w;
+      (void)node;
+      const int nt = max(0, min(kCh, cur.kc - c0));
+      mbar_wait(&empty[st], ph ^ 1u);
+      T *Ks = stage0 + st * stage_elems;
+      T *Vs = Ks + kCh * D;
+      T *Qs = Vs + kCh * D;
+      if (lane == 0) {
+        hdr[st] = StageHdr{nt, li, h, pbase, cnt, 0, 0, 0};
         mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>((2 * nt + cnt * G) * rb));
-        const int l = a.layer_begin + li;
-        const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.g.MPN;
-        for (int s0 = 0; s0 < nt;) {               // one copy per page-head run
-          const int slot = c0 + s0;
-          const int off = slot % a.g.P;
-          const int rows = min(a.g.P - off, nt - s0);
-          const int64_t row = pool_row(a.g, l, pl[slot / a.g.P], h, off);
+      }
+      __syncwarp();
+      const int l = a.layer_begin + li;
+      if (lane < pages_per_item) {
+        const int off = a.g.P >= kCh ? (c0 & (a.g.P - 1)) : 0;
+        const int s0 = lane * (a.g.P >= kCh ? 0 : a.g.P);
+        const int rows = min(a.g.P >= kCh ? kCh : a.g.P, nt - s0);
+        if (rows > 0) {
+          const int64_t row = pool_row(a.g, l, cur.page, h, off);
           bulk_g2s(Ks + s0 * D, kpool + row * D, rows * rb, &full[st]);
           bulk_g2s(Vs + s0 * D, vpool + row * D, rows * rb, &full[st]);
-          s0 += rows;
-        }
-        const int j0 = a.pv.it_j0[item];
-        const int pbase = a.pv.ch_poff[c] + j0;
-        for (int i = 0; i < cnt; ++i) {            // the G query rows of each leaf
-          const int b = a.pv.pair_b[pbase + i];
-          bulk_g2s(Qs + i * G * D, q + ((static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * G) * D,
-                   G * rb, &full[st]);
         }
       }
+      if (lane < cnt)
+        bulk_g2s(Qs + lane * G * D,
+                 q + ((static_cast<int64_t>(cur.b) * a.Lc + li) * a.Hq + h * G) * D, G * rb,
+                 &full[st]);
+      cur = nxt;
     }
     return;
   }
@@ -163,10 +176,7 @@ attn_stream_kernel(StreamArgs a) {
     const uint32_t ph = (k / kNst) & 1u;
     mbar_wait(&full[st], ph);
     const StageHdr hd = hdr[st];
-    const int nt = hd.nt, li = hd.li, h = hd.h;
-    const int c = a.pv.it_chunk[hd.item];
-    const int cnt = a.pv.it_cnt[hd.item];
-    const int pbase = a.pv.ch_poff[c] + a.pv.it_j0[hd.item];
+    const int nt = hd.nt, li = hd.li, h = hd.h, cnt = hd.cnt, pbase = hd.pbase;
     const T *Ks = stage0 + st * stage_elems;
     const T *Vs = Ks + kCh * D;
     const T *Qs = Vs + kCh * D;

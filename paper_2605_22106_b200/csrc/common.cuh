@@ -74,6 +74,7 @@ struct DevState {
   float *zbuf;               // attention log2-domain logits (fused score pass)
   int64_t *mass_part;        // this rank's per-node partial mass (cached, §score.cu)
   int64_t *mass_scratch;     // [max_nodes][layer_count] node-mass partials
+  long long *alloc_trace;    // debug builds only (ARBOR_ALLOC_TRACE)
   float *lse_scratch;        // used when arbor_score gets lse == NULL
   void *out_scratch;
 };
@@ -86,7 +87,7 @@ struct DevState {
 // (the merge order).
 struct PlanView {
   const int32_t *ch_node, *ch_chunk, *ch_poff, *ch_pcnt;   // C chunks: (node, chunk) + pairs
-  const int32_t *it_chunk, *it_j0, *it_cnt;                 // I attention items (leaf subsets)
+  const int4 *it_rec;                                       // I items: {node, c0, pair base, cnt}
   const int32_t *pair_b;                                     // P pairs → active leaf index
   const int32_t *bp_off, *bp_list;                           // per leaf: pairs root→leaf
   int C, I, nA, P;
