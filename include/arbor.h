@@ -137,7 +137,9 @@ arbor_status arbor_nccl_unique_id(void *out128);
 
 /* ---- node plumbing (not hot-path steps) -------------------------------------------- */
 /* Register node `node` (must equal the number of known nodes) as an open block starting
- * at absolute position span_start. */
+ * at absolute position span_start.  Spans of all nodes must stay disjoint: opening
+ * inside another span, or appending into the next node's start, is ARBOR_ERR_INVALID_ARG
+ * (concurrently decoded siblings need reserved position ranges). */
 arbor_status arbor_open_node(arbor_ctx *ctx, int32_t node, int64_t span_start);
 /* Append ntok decoded tokens to an open node.  k, v: DEVICE [layer_count][kv_head_count]
  * [ntok][head_dim] in kv_dtype.  Pages are popped from the free list in token order. */

@@ -211,6 +211,7 @@ class ArborKV:
         L = layer_count if layer_count is not None else num_layers
         H = kv_head_count if kv_head_count is not None else num_kv_heads
         self.L, self.H, self.D, self.P, self.NP = L, H, head_dim, page_size, num_pages
+        self.max_nodes = max_nodes
         self.G = num_q_heads // num_kv_heads
         self.Hq = H * self.G
         self.max_tokens = max_tokens

@@ -657,6 +657,11 @@ arbor_status arbor_open_node(arbor_ctx *c, int32_t node, int64_t span_start) {
   if (node != c->num_known) return fail(c, ARBOR_ERR_INVALID_ARG, "node ids are dense: expected " + std::to_string(c->num_known));
   if (node >= c->max_nodes) return fail(c, ARBOR_ERR_INVALID_ARG, "max_nodes exceeded");
   if (span_start < 0 || span_start >= c->max_tokens) return fail(c, ARBOR_ERR_INVALID_ARG, "span_start out of range");
+  // token spans of all nodes are disjoint ranges of the absolute position stream (the
+  // accumulated-attention array A is dense by absolute position)
+  for (int j = 0; j < c->num_known; ++j)
+    if (span_start >= c->h_span[j] && span_start < c->h_span[j] + c->h_n[j])
+      return fail(c, ARBOR_ERR_INVALID_ARG, "span_start lies inside node " + std::to_string(j) + "'s span");
   init_node_kernel<<<1, 1, 0, c->ms>>>(node, span_start, c->d.n, c->d.kcur, c->d.npages, c->d.span,
                                        c->d.mclose, c->d.s, c->d.a);
   ARBOR_LAUNCHED(c);
@@ -679,6 +684,12 @@ arbor_status arbor_append_kv(arbor_ctx *c, int32_t node, const void *k, const vo
   const int64_t new_n = static_cast<int64_t>(c->h_n[node]) + ntok;
   if (new_n > c->cfg.max_node_tokens) return fail(c, ARBOR_ERR_INVALID_ARG, "node exceeds max_node_tokens");
   if (c->h_span[node] + new_n > c->max_tokens) return fail(c, ARBOR_ERR_INVALID_ARG, "position stream exceeds max_tokens");
+  {
+    const int64_t lo = c->h_span[node] + c->h_n[node], hi = c->h_span[node] + new_n;
+    for (int j = 0; j < c->num_known; ++j)
+      if (j != node && c->h_span[j] < hi && c->h_span[j] + std::max<int64_t>(c->h_n[j], 1) > lo)
+        return fail(c, ARBOR_ERR_INVALID_ARG, "append would overlap node " + std::to_string(j) + "'s span");
+  }
   launch_append(c, node, k, v, c->h_n[node], ntok);
   CK_LAUNCH();
   c->h_n[node] = static_cast<int32_t>(new_n);

@@ -167,3 +167,106 @@ def warmup_leaf_cycling(sc: Scenario, steps_per_leaf: int = 4):
             decode_step(sc.ctx, sc.tree, q)
             sc.steps += 1
     sc.tree.active = saved
+
+
+# ---------------------------------------------------------------- C3: DPTS transition loop
+class DptsRun:
+    """configs[2]: n_active leaves under distinct level-2
+    parents; each transition replaces `swap` of them (backtracks into possibly evicted
+    subtrees), opens a fresh child under every newly activated leaf (where decoding writes)
+    and closes the children of deactivated leaves (Boundary); then
+      allocate (a1+a4, with the last scores) → evict (a5+a6) → rehydrate the new Path* (a7/a8)
+    followed by `decode_steps` decode steps (append one token to every open child; a9; a2/a3).
+    The budget B = ⌊ρ·T_tot(base tree)⌋ stays fixed while the tree grows."""
+
+    def __init__(self, sc: "Scenario", n_active=16, transitions=32, swap=4, decode_steps=8,
+                 seed=0, on_append=None):
+        import torch
+        self.sc = sc
+        self.torch = torch
+        self.tree = sc.tree
+        self.base_leaves = synth.dpts_initial_leaves(sc.tree, n_active, seed)
+        self.schedule = synth.dpts_schedule(sc.tree, self.base_leaves, transitions, swap, seed)
+        self.decode_steps = decode_steps
+        self.budget = sc.budget
+        self.child_of = {}            # active base leaf -> its open child node
+        self.step = 0
+        self.on_append = on_append
+        self.log = []                 # ("append", node, pos) / ("close", node) / ("open", node, a)
+        # every open child gets a reserved, disjoint range of the position stream
+        self.child_cap = decode_steps * (transitions + 1) + 2
+        self.next_pos = sc.tree.end_position()
+        self.k_buf = torch.empty(sc.ctx.max_nodes, dtype=torch.int32, device=sc.ctx.device)
+
+    def _kv_token(self, node: int, t: int):
+        """Seeded K/V of one appended token of an open child: [L][H_local][1][d] (CPU-drawn
+        for all heads, sliced to this rank's heads, so every world size sees the same data)."""
+        p = self.sc.preset
+        g = self.torch.Generator().manual_seed(int(self.sc.seed * 7_000_003 + node * 10_007 + t))
+        shape = (p["L"], p["H"], 1, p["d"])
+        k = self.torch.randn(shape, generator=g)
+        v = self.torch.randn(shape, generator=g)
+        h0, hc = self.sc.kv_head_begin, self.sc.ctx.H
+        td = self.sc.ctx.tdtype
+        return k[:, h0:h0 + hc].to(td).contiguous(), v[:, h0:h0 + hc].to(td).contiguous()
+
+    def _append(self, node: int):
+        ctx, tree = self.sc.ctx, self.tree
+        t = int(tree.span_len[node])
+        k, v = self._kv_token(node, t)
+        ctx.arbor_append_kv(node, k.to(ctx.device), v.to(ctx.device))
+        if self.on_append:
+            self.on_append(node, int(tree.span_start[node]) + t, k, v)
+        self.log.append(("append", node, int(tree.span_start[node]) + t))
+        tree.span_len[node] += 1
+
+    def activate(self, leaves):
+        """Open children for newly active leaves, close those of deactivated leaves."""
+        ctx, tree = self.sc.ctx, self.tree
+        new = set(leaves)
+        for leaf, ch in list(self.child_of.items()):
+            if leaf not in new:
+                if int(tree.span_len[ch]) == 0:    # never decoded: give it one token first
+                    self._append(ch)
+                ctx.arbor_close_node(ch)
+                self.log.append(("close", ch))
+                tree.is_open[ch] = 0
+                del self.child_of[leaf]
+        for leaf in leaves:
+            if leaf not in self.child_of:
+                a = self.next_pos
+                self.next_pos += self.child_cap
+                node = tree.add_node(leaf, a, 0, True, float(tree.v[leaf]), float(tree.u[leaf]))
+                ctx.arbor_open_node(node, a)
+                self.log.append(("open", node, a))
+                self.child_of[leaf] = node
+        tree.active = [self.child_of[l] for l in leaves]
+
+    def path_union(self):
+        tree = self.tree
+        out = set()
+        for leaf in tree.active:
+            x = int(leaf)
+            while x >= 0:
+                out.add(x)
+                x = int(tree.parent[x])
+        return sorted(out)
+
+    def transition(self, leaves):
+        """activate → allocate (last scores; 0.5 for never-scored nodes) → evict → rehydrate."""
+        ctx, tree = self.sc.ctx, self.tree
+        self.activate(leaves)
+        k = self.k_buf[:tree.num_nodes]
+        ctx.arbor_allocate(tree, None, self.budget, k)
+        ctx.arbor_evict(tree, k)
+        ctx.arbor_rehydrate(tree, [x for x in self.path_union() if not tree.is_open[x]])
+        return k
+
+    def decode(self):
+        """One decode step of every open child: append a token, a9, then a2/a3."""
+        ctx, tree = self.sc.ctx, self.tree
+        for ch in tree.active:
+            self._append(ch)
+        q = self.sc.queries(1_000_000 + self.step, len(tree.active))
+        self.step += 1
+        return q, decode_step(ctx, tree, q)

@@ -286,3 +286,54 @@ def test_stash_rehydrate_bit_exact_roundtrip():
     for i in range(N):
         kc, pages, pos, kr, vr = pr.gpu_node(i)
         assert kc == int(pr.tree.span_len[i]) and np.array_equal(pos[0, 0], np.arange(kc))
+
+
+def test_c3_dpts_transitions_reduced():
+    """configs[2] shape at reduced size: 16 active leaves under distinct level-2 parents,
+    transitions replacing 4 of them (backtracking → rehydration), open children growing by
+    decode appends; every transition's k, kept sets, pages, free list and rehydration count
+    bit-exact, decode outputs and scores within tolerance."""
+    preset = dict(workload.PRESETS["c3"], tree=("full", 4, 5, 24), L=2, H=2, Hq=8, rho=0.7)
+    T_extra, N_extra = (16 + 3 * 4) * (2 * 4 + 2) + 64, 16 + 4 * 4 + 4
+    pr = Pair(preset, seed=3, extra_tokens=T_extra, extra_nodes=N_extra, max_active=16)
+    sc = workload.Scenario(pr.preset, pr.tree, pr.ctx, pr.Kd, pr.Vd, pr.E, 3, 0)
+
+    def on_append(node, pos, k, v):
+        pr.orc.K[:, :, pos] = k[:, :, 0].double().numpy()
+        pr.orc.V[:, :, pos] = v[:, :, 0].double().numpy()
+        pr.K[:, :, pos] = k[:, :, 0]
+        pr.V[:, :, pos] = v[:, :, 0]
+
+    run = workload.DptsRun(sc, n_active=16, transitions=3, swap=4, decode_steps=2, seed=3,
+                           on_append=on_append)
+    pr.warmup(steps_per_leaf=1)
+    for t, leaves in enumerate([run.base_leaves] + run.schedule):
+        n_log = len(run.log)
+        kd = run.transition(leaves)
+        for ev in run.log[n_log:]:                      # replay lifecycle events in order
+            if ev[0] == "append":
+                pr.orc.append(ev[1], 1)
+            elif ev[0] == "close":
+                pr.orc.close_node(ev[1])
+            else:
+                pr.orc.open_node(ev[1], ev[2])
+        sc_gpu = pr.ctx.arbor_read_scores(pr.tree.num_nodes)
+        st, k_ref, _ = pr.discrete_allocate(sc_gpu["s"], run.budget)
+        assert st == 0 and kd.cpu().tolist() == k_ref, f"transition {t}: k differs"
+        pr.orc.evict(pr.tree, k_ref, A_f32=pr.gpu_A())
+        path = [x for x in run.path_union() if not pr.tree.is_open[x]]
+        pr.orc.rehydrate(path)
+        pr.check_kv_state()
+        assert pr.ctx.arbor_read_counters()[0] == pr.orc.rehydrations
+        for _ in range(run.decode_steps):
+            n_log = len(run.log)
+            q, (out, lse) = run.decode()
+            for ev in run.log[n_log:]:
+                pr.orc.append(ev[1], 1)
+            qn = q.float().cpu().double().numpy()
+            o_ref, lse_ref = pr.orc.decode(pr.tree, qn)
+            pr.orc.score_accumulate(pr.tree, qn)
+            assert_close(out.float().cpu().numpy(), o_ref, pr.rtol, "C3 attention output")
+            assert_close(lse.cpu().numpy(), lse_ref, pr.rtol, "C3 LSE")
+        _score_stage_checks(pr)
+    assert pr.orc.rehydrations > 0
