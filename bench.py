@@ -377,9 +377,14 @@ def main():
         for x in synth_path(tree.parent, leaves[i % 2]):
             vis += int(tree.span_len[x])
         rows = L * Hh
-        byts["attn"] = rows * vis * 2 * rb + nA * ctx.Hq * L * ctx.D * 2 * rb // ctx.D
-        byts["score_accum"] = rows * vis * (rb + 8)
-        byts["node_mass"] = rows * cached * 4
+        # a9: K + V of every visible token-row, plus Q read and O written
+        byts["attn"] = rows * vis * 2 * rb + nA * ctx.Hq * L * 2 * rb
+        # a9 + a2 fused (a2 reuses a9's logits, so the K read is shared): a9's bytes + the
+        # read-modify-write of A (8 B) per visible token-row
+        byts["attn_score"] = byts["attn"] + rows * vis * 8
+        # a3: A changes only at visible tokens, so only the visible closed nodes' partial
+        # masses are recomputed (4 B per visible token-row); the rest are cached
+        byts["node_mass"] = rows * vis * 4
         return byts
 
     ab = [alg_bytes(0), alg_bytes(1)]
@@ -405,17 +410,25 @@ def main():
         top_name, top_desc = "select_compact", "select_move_ws (a5+a6, warp-specialised)"
     kernels.update({
         "attn_partial": kstat("attn", lambda i: ab[i]["attn"]),
-        "score_accum": kstat("score_accum", lambda i: ab[i]["score_accum"]),
         "node_mass": kstat("node_mass", lambda i: ab[i]["node_mass"]),
     })
+    # a9 + a2 as one unit: the fused path's bytes over attn + merge + score-apply time
+    t_as = statistics.mean(stage_ms["attn"]) + statistics.mean(stage_ms["attn_merge"]) + \
+        statistics.mean(stage_ms["score_accum"])
+    b_as = statistics.mean(ab[i]["attn_score"] for i in range(2))
+    kernels["attn_score_fused"] = {"ms": t_as, "bytes": b_as, "GBps": b_as / (t_as / 1e3) / 1e9,
+                                   "frac_measured": b_as / (t_as / 1e3) / 1e9 / peak,
+                                   "frac_nominal": b_as / (t_as / 1e3) / 1e9 / NOMINAL_HBM,
+                                   "stages": ["attn", "attn_merge", "score_accum"]}
     top = kernels[top_name]
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_compact_move_ncu.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            if pj.get("config") == args.config:
-                traffic = pj.get("dram_bytes_per_launch")
+            ent = pj.get(args.config, {}).get(top_name)
+            if ent:
+                traffic = ent["dram_bytes_per_launch"]
         except Exception:
             traffic = None
     roofline = {"kernel": top_desc, "bound": "hbm", "achieved": top["GBps"],
