@@ -237,6 +237,12 @@ arbor_status arbor_load_state(arbor_ctx *ctx, int32_t slot);
 arbor_status arbor_invalidate_masses(arbor_ctx *ctx);
 /* Kernel launches issued by this context since creation (all streams). */
 int64_t arbor_launch_count(const arbor_ctx *ctx);
+/* 1 when arbor_tree_decode_attn / arbor_score run the tcgen05 tensor-core attention kernel
+ * (bf16 KV, head_dim 128, page_size a multiple of 8 and ≤ 64, G ≤ 6, driver tensor-map
+ * support; environment ARBOR_ATTN=cuda at arbor_init forces the CUDA-core kernel), 0 when
+ * the CUDA-core kernel is used, −1 for a NULL context.  Both compute the same operation
+ * within the north_star tolerance. */
+int32_t arbor_attn_tensor_cores(const arbor_ctx *ctx);
 /* With ARBOR_FLAG_PROFILE: per-stage mean device milliseconds over the launches recorded since
  * the last arbor_reset_stage_times (up to the last 128 per stage), measured with CUDA events
  * on the launching stream (HOST out [ARBOR_NUM_STAGES]; synchronises). */

@@ -93,6 +93,7 @@ def load_library(path: str = LIB_PATH):
         "arbor_save_state": ([P, I32], I32),
         "arbor_load_state": ([P, I32], I32),
         "arbor_launch_count": ([P], I64),
+        "arbor_attn_tensor_cores": ([P], I32),
         "arbor_invalidate_masses": ([P], I32),
         "arbor_stage_times": ([P, P], I32),
         "arbor_reset_stage_times": ([P], I32),
@@ -362,6 +363,9 @@ class ArborKV:
 
     def arbor_launch_count(self) -> int:
         return int(self.lib.arbor_launch_count(self._ctx))
+
+    def arbor_attn_tensor_cores(self) -> bool:
+        return int(self.lib.arbor_attn_tensor_cores(self._ctx)) == 1
 
     def arbor_reset_stage_times(self):
         self._check(self.lib.arbor_reset_stage_times(self._ctx), "arbor_reset_stage_times")

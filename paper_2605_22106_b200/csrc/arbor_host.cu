@@ -238,6 +238,8 @@ arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
 // ---------------------------------------------------------------- attention / score plan
 struct HostPlan {
   std::vector<int32_t> ch_node, ch_chunk, ch_poff, ch_pcnt, it_rec, pair_b, bp_off, bp_list;
+  std::vector<int32_t> tl_rec;   // tensor-core tiles: {item A, item B or -1, 0, 0}
+  int max_cnt = 0;               // most leaves in one item
   std::vector<std::vector<int32_t>> paths;
 };
 
@@ -258,6 +260,16 @@ void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan 
     if (nch == 0) continue;
     chunk_of[x] = static_cast<int32_t>(p.ch_node.size());
     const int lc = static_cast<int>(leaves[x].size());
+    const int ng = (lc + kLeavesPerItem - 1) / kLeavesPerItem;
+    const int first_item = static_cast<int>(p.it_rec.size() / 4);
+    p.max_cnt = std::max(p.max_cnt, std::min(kLeavesPerItem, lc));
+    for (int ch = 0; ch < nch; ch += 2)    // a tile = chunks (ch, ch+1) of one leaf group
+      for (int gi = 0; gi < ng; ++gi) {
+        p.tl_rec.push_back(first_item + ch * ng + gi);
+        p.tl_rec.push_back(ch + 1 < nch ? first_item + (ch + 1) * ng + gi : -1);
+        p.tl_rec.push_back(0);
+        p.tl_rec.push_back(0);
+      }
     for (int ch = 0; ch < nch; ++ch) {
       const int c = static_cast<int>(p.ch_node.size());
       p.ch_node.push_back(x);
@@ -296,6 +308,7 @@ arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
     return off;
   };
   const size_t o_ir = put(p.it_rec);   // first: 16-byte aligned int4 records
+  const size_t o_tl = put(p.tl_rec);   // int4 records (it_rec has 4 ints per item)
   const size_t o_cn = put(p.ch_node), o_cc = put(p.ch_chunk), o_cpo = put(p.ch_poff),
                o_cpc = put(p.ch_pcnt), o_pb = put(p.pair_b), o_bpo = put(p.bp_off),
                o_bpl = put(p.bp_list);
@@ -315,6 +328,8 @@ arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
   pv.ch_poff = base + o_cpo;
   pv.ch_pcnt = base + o_cpc;
   pv.it_rec = reinterpret_cast<const int4 *>(base + o_ir);
+  pv.tl_rec = reinterpret_cast<const int4 *>(base + o_tl);
+  pv.T = static_cast<int>(p.tl_rec.size() / 4);
   pv.pair_b = base + o_pb;
   pv.bp_off = base + o_bpo;
   pv.bp_list = base + o_bpl;
@@ -345,7 +360,7 @@ arbor_status ensure_partials(arbor_ctx *c, size_t pairs, int layer_count) {
 arbor_status run_attention(arbor_ctx *c, const HostPlan &hp, const PlanView &pv, int layer_begin,
                            int layer_count, const void *q, void *out, float *lse) {
   TRY(ensure_partials(c, hp.pair_b.size(), layer_count));
-  launch_attn_partial(c, pv, q, layer_begin, layer_count);
+  launch_attn_partial(c, pv, q, layer_begin, layer_count, hp.max_cnt);
   CK_LAUNCH();
   launch_attn_merge(c, pv, layer_count, out, lse);
   CK_LAUNCH();
@@ -613,6 +628,7 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
     if (g_nccl.commInitRank(&comm, k.world_size, id, k.rank) != ncclSuccess) return bail(ARBOR_ERR_NCCL);
     c->nccl_comm = comm;
   }
+  attn_tc_init(c);   // tcgen05 attention when the shape allows it (else the CUDA-core kernel)
   if (cudaStreamSynchronize(c->ms) != cudaSuccess) return bail(ARBOR_ERR_CUDA);
   *out = c;
   return ARBOR_OK;
@@ -1005,6 +1021,7 @@ arbor_status arbor_load_state(arbor_ctx *c, int32_t slot) {
 }
 
 int64_t arbor_launch_count(const arbor_ctx *c) { return c ? c->launches : 0; }
+int32_t arbor_attn_tensor_cores(const arbor_ctx *c) { return c ? (c->tc_ok ? 1 : 0) : -1; }
 
 #ifdef ARBOR_ALLOC_TRACE
 arbor_status arbor_debug_set_alloc_trace(arbor_ctx *c, long long *trace) {

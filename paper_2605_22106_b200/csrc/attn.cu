@@ -395,8 +395,14 @@ void launch_stream_q(arbor_ctx *c, StreamArgs a) {
 }  // namespace
 
 void launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
-                         int layer_count) {
+                         int layer_count, int max_cnt) {
   if (pv.I == 0) return;
+  stage_begin(c, ARBOR_ST_ATTN, c->ms);
+  if (launch_attn_tc(c, pv, q, layer_begin, layer_count, max_cnt)) {   // attn_tc.cu
+    ARBOR_LAUNCHED(c);
+    stage_end(c, ARBOR_ST_ATTN, c->ms);
+    return;
+  }
   StreamArgs a{};
   a.pv = pv;
   a.g = PoolView{c->L, c->H, c->P, c->D, c->NP, c->max_pages_node, c->max_tokens};
@@ -413,7 +419,6 @@ void launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int la
   a.G = c->G;
   a.lmax = kLeavesPerItem;
   a.scale_log2 = kLog2e / sqrtf(static_cast<float>(c->D));
-  stage_begin(c, ARBOR_ST_ATTN, c->ms);
   if (c->esize == 2) {
     if (c->D == 128) launch_stream_q<__nv_bfloat16, 128>(c, a);
     else launch_stream_q<__nv_bfloat16, 64>(c, a);

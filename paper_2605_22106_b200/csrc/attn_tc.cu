@@ -1,0 +1,801 @@
+// attn_tc.cu — §8(a) a9 on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), bf16, d = 128.
+//
+// Same operation as attn.cu (Q24): for every active leaf b, layer l
+// and query head g (KV head h = g / G), o = Σ_t softmax_t(q·k_t/√d) v_t over the retained slots
+// of Path(ℓ_b), emitted as split-softmax partials per (chunk of kAttnChunk = 64 slots, leaf) and
+// merged root→leaf by attn_merge_kernel (attn.cu), plus the log2-domain logits z the fused score
+// pass (score.cu) turns into A.
+//
+// Why tensor cores: a work tile holds up to two 64-slot chunks of one node (128 K/V rows of one
+// (layer, KV head)) and the nq = (leaves sharing the node) × G query rows that read them.  Both
+// products are dense contractions — S = K·Qᵀ (128 × nq × d) and Oᵀ = Vᵀ·P (d × 2nq × 128) — so
+// they are issued as two tcgen05.mma chains (M = 128, N = NQ resp. 2·NQ, K = 16 per instruction)
+// with fp32 accumulators in TMEM, and the CUDA cores only run the softmax.  That removes the
+// issue-bound FMA/convert work of the CUDA-core kernel, which kept it far below HBM speed.
+//
+// CTA layout (persistent, one CTA per SM, tiles strided over CTAs):
+//   warp 0      TMA producer: per page-head, two cp.async.bulk.tensor boxes (64 cols × P rows,
+//               SWIZZLE_128B) for K and for V into an NST-stage ring; q rows staged with 16-byte
+//               loads into the same 128B-swizzled K-major layout; mbarrier transaction counts.
+//   warp 1      TMEM allocator + MMA issuer (one thread): MMA1(k+1) is issued before MMA2(k)
+//               waits for the softmax of tile k, so the S of the next tile is ready in TMEM.
+//   warps 2..5  softmax + epilogue, one thread per TMEM lane (= tile row = slot, then = d index):
+//               tcgen05.ld S → mask → column max / sum over each 64-slot half (shuffles + smem) →
+//               z to zbuf, P (bf16) into the K-major B operand of MMA2 → tcgen05.ld Oᵀ → partials.
+// Operand layouts (canonical UMMA, SWIZZLE_128B, atoms of 8 rows × 128 B, 1024-B aligned):
+//   K tile  [2 d-halves][128 rows][64]   A of MMA1, K-major,  SBO 1024
+//   Q tile  [2 d-halves][NQ rows][64]    B of MMA1, K-major,  SBO 1024
+//   V tile  [2 d-halves][128 rows][64]   A of MMA2 = Vᵀ, MN-major, LBO 16 KB (d-halves), SBO 1024
+//   P tile  [2 slot-halves][2NQ][64]     B of MMA2 = Pᵀ, K-major: rows [h·NQ, h·NQ+NQ) of slot half
+//                                        h hold chunk h's probabilities, the other rows are zero.
+// Numerics: K, V, q are bf16 (exact products, fp32 accumulation); P is rounded to bf16 for the
+// PV product (relative error ≤ 2^-9 per weight, inside the bf16 tolerance 2e-2); m and l are the
+// fp32 column max and the fp32 sum of the unrounded exp2 values.
+#include <cuda.h>
+
+#include <cfloat>
+
+#include "tile.cuh"
+
+namespace arbor {
+namespace {
+
+constexpr int kTcThreads = 320;   // producer, MMA, 4 softmax warps, 4 epilogue warps
+constexpr int kTileRows = 128;
+constexpr int kHalf = 64;                       // = kAttnChunk
+constexpr uint32_t kKVBytes = kTileRows * 256;  // one K (or V) tile: 128 rows × 128 bf16
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kMaxTilePages = 2 * 64 / 16;      // page size ≥ 16 on this path
+
+static_assert(kAttnChunk == kHalf, "a tensor-core tile is two score/attention chunks");
+
+struct TcArgs {
+  PlanView pv;
+  PoolView g;
+  const int32_t *ptab, *kcur;
+  const __nv_bfloat16 *q;
+  float *partials, *zbuf;
+  int layer_begin, Lc, Hq, G, T;   // T: tiles
+  float scale_log2;
+  long long *trace;                // debug: clock64 per (CTA, tile, event) or NULL
+};
+
+// debug timeline (ARBOR_TC_TRACE=1): trace[(cta·64 + tile)·16 + event] = clock64 − CTA start
+#define TC_TRACE(k, e)                                                                      \
+  do {                                                                                      \
+    if (a.trace && (k) < 64)                                                                \
+      a.trace[(static_cast<int64_t>(blockIdx.x) * 64 + (k)) * 16 + (e)] = clock64() - t_start; \
+  } while (0)
+
+struct TcHdr {
+  int ntA, ntB, li, h, pbA, pbB, cnt, hasB;
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+// non-blocking probe of an mbarrier phase
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, int c0, int c1,
+                                            int c2, int c3, int c4, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// 16 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B (sm_100 UMMA format: start>>4 [0,14),
+// LBO>>4 [16,30), SBO>>4 [32,46), version 1 at bit 46, layout type 2 at [61,64)).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) |
+         (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
+// Instruction descriptor, kind::f16: D f32, A/B bf16, majors, N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t bf16_idesc(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {   // ex2.approx.ftz: 2 ulp, −inf → +0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// N consecutive fp32 TMEM columns of this thread's lane (N a multiple of 8)
+template <int N>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float *v) {
+#pragma unroll
+  for (int c = 0; c + 16 <= N; c += 16) {
+    float t[16];
+    tmem_ld16(taddr + c, t);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[c + i] = t[i];
+  }
+  if constexpr (N % 16 == 8) {
+    uint32_t r[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+        : "r"(taddr + (N - 8)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[N - 8 + i] = __uint_as_float(r[i]);
+  }
+}
+
+// Transpose-reduce of 8 columns held by every lane: afterwards each lane holds the reduction
+// over all 32 lanes of column col8(lane) (9 shuffles instead of 40).
+__device__ __forceinline__ int col8(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+}
+template <bool kMax>
+__device__ __forceinline__ float warp_reduce8(const float *v, int lane) {
+  float b[4], c[2], d;
+  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = u16 ? v[i] : v[i + 4];
+    const float keep = u16 ? v[i + 4] : v[i];
+    const float r = __shfl_xor_sync(0xffffffffu, send, 16);
+    b[i] = kMax ? fmaxf(keep, r) : keep + r;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = u8 ? b[i] : b[i + 2];
+    const float keep = u8 ? b[i + 2] : b[i];
+    const float r = __shfl_xor_sync(0xffffffffu, send, 8);
+    c[i] = kMax ? fmaxf(keep, r) : keep + r;
+  }
+  {
+    const float send = u4 ? c[0] : c[1];
+    const float keep = u4 ? c[1] : c[0];
+    const float r = __shfl_xor_sync(0xffffffffu, send, 4);
+    d = kMax ? fmaxf(keep, r) : keep + r;
+  }
+#pragma unroll
+  for (int o = 2; o; o >>= 1) {
+    const float r = __shfl_xor_sync(0xffffffffu, d, o);
+    d = kMax ? fmaxf(d, r) : d + r;
+  }
+  return d;
+}
+
+// Transpose-reduce of 16 columns held by every lane of a warp: after the butterfly each lane
+// holds the reduction over all 32 lanes of column col16(lane) (16 shuffles instead of 80).
+__device__ __forceinline__ int col16(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+template <bool kMax>
+__device__ __forceinline__ float warp_reduce16(const float *v, int lane) {
+  float a[8], b[4], c[2], d;
+  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float send = u16 ? v[i] : v[i + 8];
+    const float keep = u16 ? v[i + 8] : v[i];
+    const float r = __shfl_xor_sync(0xffffffffu, send, 16);
+    a[i] = kMax ? fmaxf(keep, r) : keep + r;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = u8 ? a[i] : a[i + 4];
+    const float keep = u8 ? a[i + 4] : a[i];
+    const float r = __shfl_xor_sync(0xffffffffu, send, 8);
+    b[i] = kMax ? fmaxf(keep, r) : keep + r;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = u4 ? b[i] : b[i + 2];
+    const float keep = u4 ? b[i + 2] : b[i];
+    const float r = __shfl_xor_sync(0xffffffffu, send, 4);
+    c[i] = kMax ? fmaxf(keep, r) : keep + r;
+  }
+  {
+    const float send = u2 ? c[0] : c[1];
+    const float keep = u2 ? c[1] : c[0];
+    const float r = __shfl_xor_sync(0xffffffffu, send, 2);
+    d = kMax ? fmaxf(keep, r) : keep + r;
+  }
+  const float r = __shfl_xor_sync(0xffffffffu, d, 1);
+  return kMax ? fmaxf(d, r) : d + r;
+}
+
+template <int NQ> constexpr int kW = NQ % 16 == 0 ? 16 : 8;   // reduction group width
+template <int NQ>
+__device__ __forceinline__ int colW(int lane) { return kW<NQ> == 16 ? col16(lane) : col8(lane); }
+template <int W, bool kMax>
+__device__ __forceinline__ float warp_reduceW(const float *v, int lane) {
+  if constexpr (W == 16) return warp_reduce16<kMax>(v, lane);
+  else return warp_reduce8<kMax>(v, lane);
+}
+// valid columns of an item with cnt leaves: 8-row slot per leaf, G q heads used per slot
+__device__ __forceinline__ unsigned long long colmask(int cnt, int G) {
+  const unsigned long long slot = (1ull << G) - 1ull;
+  unsigned long long m = 0;
+  for (int bi = 0; bi < cnt; ++bi) m |= slot << (8 * bi);
+  return m;
+}
+
+template <int NQ>
+constexpr int tmem_cols() {
+  return 6 * NQ <= 32 ? 32 : 6 * NQ <= 64 ? 64 : 6 * NQ <= 128 ? 128 : 6 * NQ <= 256 ? 256 : 512;
+}
+
+template <int NQ, int NST>
+struct TcSmem {
+  static constexpr uint32_t kQ = NQ * 256;                    // Q tile bytes
+  static constexpr uint32_t kStage = 2 * kKVBytes + kQ;       // K | V | Q
+  static constexpr uint32_t kP = 2 * NQ * 256;                // P tile bytes (2NQ rows × 128 slots)
+  static constexpr uint32_t kBytes = NST * kStage + 2 * kP;
+  static constexpr uint32_t kAlloc = kBytes + 1024;           // + alignment slack
+};
+
+template <int NQ, int NST>
+__global__ void __launch_bounds__(kTcThreads, 1)
+attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+               const __grid_constant__ CUtensorMap tmk4, const __grid_constant__ CUtensorMap tmv4,
+               const __grid_constant__ CUtensorMap tmq, TcArgs a) {
+  using S = TcSmem<NQ, NST>;
+  extern __shared__ unsigned char sm_raw[];
+  unsigned char *sm = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  unsigned char *Pbuf = sm + NST * S::kStage;
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], o_full[2], o_empty[2];
+  __shared__ TcHdr hdr[NST];
+  __shared__ TcHdr ohdr[4];                             // tile k's header for the epilogue warps
+  __shared__ float red_m[2][4][NQ], red_l[2][4][NQ];   // [tile parity][warp quadrant][column]
+  __shared__ uint32_t tmem_base_sh;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long t_start = clock64();
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long g0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+    a.trace[(static_cast<int64_t>(blockIdx.x) * 64 + 63) * 16 + 0] = static_cast<long long>(g0);
+  }
+  const int HL = a.g.H * a.Lc;
+  const int total = a.T * HL;
+  const int ntiles = total > static_cast<int>(blockIdx.x)
+                         ? (total - 1 - static_cast<int>(blockIdx.x)) / gridDim.x + 1 : 0;
+  const int P = a.g.P;
+  const int lgP = 31 - __clz(P);
+
+  // ---- producer state (warp 0).  Everything the producer needs per tile — node, chunk,
+  // pair bases, leaf ids, k_cur and the page ids — is loaded lane-parallel for 32 tiles at a
+  // time (lane i: tile k0 + i) before any of those tiles' TMA traffic is in flight: a plain
+  // global load issued behind ~200 KB of in-flight TMA data per SM waits ~2 µs.
+  int b_c0 = 0, b_pbA = 0, b_pbB = -1, b_cnt = 0, b_ntA = 0, b_ntB = 0;
+  int b_leaf[kLeavesPerItem];
+  int b_page[kMaxTilePages];
+  auto load_batch = [&](int k0) {
+    const int kk = k0 + lane;
+    if (kk < ntiles) {
+      const int it = blockIdx.x + kk * gridDim.x;
+      const int4 tr = a.pv.tl_rec[it / HL];
+      const int4 ra = a.pv.it_rec[tr.x];
+      b_pbB = tr.y >= 0 ? a.pv.it_rec[tr.y].z : -1;
+      const int node = ra.x;
+      b_c0 = ra.y; b_pbA = ra.z; b_cnt = ra.w;
+#pragma unroll
+      for (int i = 0; i < kLeavesPerItem; ++i) b_leaf[i] = i < b_cnt ? a.pv.pair_b[b_pbA + i] : 0;
+      const int kc = a.kcur[node];
+      b_ntA = max(0, min(kHalf, kc - b_c0));
+      b_ntB = b_pbB >= 0 ? max(0, min(kHalf, kc - b_c0 - kHalf)) : 0;
+      const int pgA = (b_ntA + P - 1) >> lgP, pgB = (b_ntB + P - 1) >> lgP;
+      const int ppH = kHalf >> lgP;   // pages per 64-slot half
+      const int32_t *pt = a.ptab + static_cast<int64_t>(node) * a.g.MPN + (b_c0 >> lgP);
+#pragma unroll
+      for (int i = 0; i < kMaxTilePages; ++i) {
+        const int half = i >= ppH, pi = i - half * ppH;
+        b_page[i] = (pi < (half ? pgB : pgA)) ? pt[half * ppH + pi] : 0;
+      }
+    }
+  };
+  if (warp == 0) load_batch(0);    // in flight while the other warps set the CTA up
+  else {
+    // zero V, Q and P once: MMA2 reads every V row (0·v must stay 0, so rows never loaded
+    // must be finite) and the off-half rows of the Pᵀ tile are never written again
+    for (int s = 0; s < NST; ++s) {
+      unsigned char *base = sm + s * S::kStage + kKVBytes;
+      for (uint32_t i = (tid - 32) * 16; i < kKVBytes + S::kQ; i += (kTcThreads - 32) * 16)
+        *reinterpret_cast<uint4 *>(base + i) = make_uint4(0, 0, 0, 0);
+    }
+    for (uint32_t i = (tid - 32) * 16; i < 2 * S::kP; i += (kTcThreads - 32) * 16)
+      *reinterpret_cast<uint4 *>(Pbuf + i) = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+  }
+  if (tid == 32) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);   // the 4 softmax warps
+      mbar_init(&o_full[b], 1);
+      mbar_init(&s_empty[b], 128);
+      mbar_init(&o_empty[b], 128);  // the 4 epilogue warps
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(&tmem_base_sh)), "r"(tmem_cols<NQ>()));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------- TMA producer
+    const int ppH = kHalf >> lgP;
+    for (int k = 0; k < ntiles; ++k) {
+      if (k > 0 && (k & 31) == 0) load_batch(k);
+      const int src = k & 31;
+      const int ntA = __shfl_sync(0xffffffffu, b_ntA, src);
+      const int ntB = __shfl_sync(0xffffffffu, b_ntB, src);
+      const int pbA = __shfl_sync(0xffffffffu, b_pbA, src);
+      const int pbB = __shfl_sync(0xffffffffu, b_pbB, src);
+      const int cnt = __shfl_sync(0xffffffffu, b_cnt, src);
+      int page = 0, leaf = 0;       // lane i < pages: page i of the tile; lane i < cnt: leaf i
+#pragma unroll
+      for (int i = 0; i < kMaxTilePages; ++i) {
+        const int v = __shfl_sync(0xffffffffu, b_page[i], src);
+        if (lane == i) page = v;
+      }
+#pragma unroll
+      for (int i = 0; i < kLeavesPerItem; ++i) {
+        const int v = __shfl_sync(0xffffffffu, b_leaf[i], src);
+        if (lane == i) leaf = v;
+      }
+      const int it = blockIdx.x + k * gridDim.x;
+      const int li = (it / a.g.H) % a.Lc, h = it % a.g.H;
+      const int pgA = (ntA + P - 1) >> lgP, pgB = (ntB + P - 1) >> lgP;
+      const int s = k % NST;
+      const uint32_t ph = (k / NST) & 1u;
+      if (lane == 0) TC_TRACE(k, 0);
+      mbar_wait(&empty[s], ph ^ 1u);
+      if (lane == 0) TC_TRACE(k, 1);
+      unsigned char *Ks = sm + s * S::kStage;
+      unsigned char *Vs = Ks + kKVBytes;
+      unsigned char *Qs = Vs + kKVBytes;
+      if (lane == 0) {
+        hdr[s] = TcHdr{ntA, ntB, li, h, pbA, pbB, cnt, pbB >= 0 ? 1 : 0};
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(pgA + pgB) * P * 512u +
+                                            static_cast<uint32_t>(cnt) * 2048u);
+      }
+      __syncwarp();
+      const int l = a.layer_begin + li;
+      const int half = lane >= ppH, pi = lane - half * ppH;
+      const int pgh = half ? pgB : pgA;
+      // a chunk whose pages are all present and consecutive (the usual case: pages are popped
+      // in order) is fetched with one 64-row box per (K|V, d-half) through the 5-D view of the
+      // pool; otherwise one 16-row box per page-head through the 2-D view
+      const int first = __shfl_sync(0xffffffffu, page, half * ppH);
+      const bool cons = lane >= 2 * ppH || pi >= pgh || page == first + pi;
+      const unsigned bal = __ballot_sync(0xffffffffu, cons);
+      const unsigned hmask = ((1u << ppH) - 1u) << (half * ppH);
+      const bool big = lane < 2 * ppH && pgh == ppH && (bal & hmask) == hmask;
+      if (big) {
+        if (pi == 0) {
+          const int lp = l * a.g.NP + page;
+          const uint32_t dst = static_cast<uint32_t>(half * kHalf) * 128u;
+          tma_load_5d(Ks + dst, &tmk4, 0, 0, 0, h, lp, &full[s]);
+          tma_load_5d(Ks + 16384 + dst, &tmk4, 0, 1, 0, h, lp, &full[s]);
+          tma_load_5d(Vs + dst, &tmv4, 0, 0, 0, h, lp, &full[s]);
+          tma_load_5d(Vs + 16384 + dst, &tmv4, 0, 1, 0, h, lp, &full[s]);
+        }
+      } else if (lane < 2 * ppH && pi < pgh) {
+        const int row = static_cast<int>(pool_row(a.g, l, page, h, 0));
+        const uint32_t dst = static_cast<uint32_t>(half * kHalf + pi * P) * 128u;
+        tma_load_2d(Ks + dst, &tmk, 0, row, &full[s]);
+        tma_load_2d(Ks + 16384 + dst, &tmk, 64, row, &full[s]);
+        tma_load_2d(Vs + dst, &tmv, 0, row, &full[s]);
+        tma_load_2d(Vs + 16384 + dst, &tmv, 64, row, &full[s]);
+      }
+      if (lane < cnt) {
+        // leaf `lane`: its G q rows (8-row box, 1024-B aligned slot) → Q rows [8·lane, 8·lane+8)
+        const int row = (leaf * a.Lc + li) * a.Hq + h * a.G;
+        tma_load_2d(Qs + lane * 1024, &tmq, 0, row, &full[s]);
+        tma_load_2d(Qs + NQ * 128 + lane * 1024, &tmq, 64, row, &full[s]);
+      }
+      if (lane == 0) TC_TRACE(k, 2);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t id1 = bf16_idesc(128, NQ, 0, 0);       // S = K · Qᵀ
+      constexpr uint32_t id2 = bf16_idesc(128, 2 * NQ, 1, 0);   // Oᵀ = Vᵀ · Pᵀ
+      // Two independent streams of work, issued as soon as each is ready (non-blocking
+      // polls): MMA1(j) needs tile j's stage (full) and S buffer j&1 drained (s_empty of
+      // j−2); MMA2(j) needs P(j) (p_full) and Oᵀ buffer j&1 drained (o_empty of j−2).
+      int js = 0, jo = 0;
+      while (jo < ntiles) {
+        if (js < ntiles && js <= jo + 1 && mbar_test(&full[js % NST], (js / NST) & 1u) &&
+            (js < 2 || mbar_test(&s_empty[js & 1], ((js - 2) >> 1) & 1u))) {
+          const int s = js % NST, b = js & 1;
+          TC_TRACE(js, 3);
+          tc_fence_after();
+          const uint32_t ks = smem_u32(sm + s * S::kStage);
+          const uint32_t qs = ks + 2 * kKVBytes;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t ad = sw128_desc(ks + (kk >> 2) * 16384u + (kk & 3) * 32u, 16, 1024);
+            const uint64_t bd = sw128_desc(qs + (kk >> 2) * (NQ * 128u) + (kk & 3) * 32u, 16, 1024);
+            tc_mma(tmem + b * 3 * NQ, ad, bd, id1, kk > 0);
+          }
+          tc_commit(&s_full[b]);
+          if (a.trace) { mbar_wait(&s_full[b], (js >> 1) & 1u); TC_TRACE(js, 12); }
+          ++js;
+        }
+        if (jo < js && mbar_test(&p_full[jo & 1], (jo >> 1) & 1u) &&
+            (jo < 2 || mbar_test(&o_empty[jo & 1], ((jo - 2) >> 1) & 1u))) {
+          const int s = jo % NST, b = jo & 1;
+          TC_TRACE(jo, 5);
+          tc_fence_after();
+          const uint32_t vs = smem_u32(sm + s * S::kStage) + kKVBytes;
+          const uint32_t ps = smem_u32(Pbuf + b * S::kP);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t ad = sw128_desc(vs + kk * 2048u, 16384, 1024);
+            const uint64_t bd = sw128_desc(ps + (kk >> 2) * (2 * NQ * 128u) + (kk & 3) * 32u, 16, 1024);
+            tc_mma(tmem + b * 3 * NQ + NQ, ad, bd, id2, kk > 0);
+          }
+          tc_commit(&o_full[b]);
+          tc_commit(&empty[s]);
+          if (a.trace) { mbar_wait(&o_full[b], (jo >> 1) & 1u); TC_TRACE(jo, 13); }
+          ++jo;
+        }
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------- softmax (warps 2..5)
+    // One thread per TMEM lane = tile row = slot.  Straight-line predicated code, unrolled
+    // over NQ columns (the loop body must stay small for the instruction cache).
+    const int quad = warp & 3;                 // TMEM lane quadrant of this warp
+    const int half = quad >> 1;                // slot half (chunk A or B) of this thread
+    const int trow = quad * 32 + lane;         // tile row (slot)
+    const int tc = trow & (kHalf - 1);         // slot within the chunk
+    const int G = a.G;
+    const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
+    const int SP = a.Lc * a.g.H * G;
+    int offn[NQ];
+#pragma unroll
+    for (int n = 0; n < NQ; ++n) offn[n] = (n >> 3) * SP + (n & 7);
+    const int myc = colW<NQ>(lane);
+    for (int k = 0; k < ntiles; ++k) {
+      const int s = k % NST, b = k & 1;
+      mbar_wait(&full[s], (k / NST) & 1u);
+      if (tid == 64) TC_TRACE(k, 7);
+      const TcHdr hd = hdr[s];
+      if (half == 0 && lane == 0 && quad == 0) ohdr[k & 3] = hd;   // for the epilogue warps
+      const unsigned long long cm = colmask(hd.cnt, G);
+      const int nt = half ? hd.ntB : hd.ntA;
+      const bool present = half == 0 || hd.hasB;
+      const int pb = half ? hd.pbB : hd.pbA;
+      const bool valid = present && tc < nt;
+      mbar_wait(&s_full[b], (k >> 1) & 1u);
+      if (tid == 64) TC_TRACE(k, 8);
+      tc_fence_after();
+      float z[NQ];
+      tmem_ld<NQ>(tmem + lane_addr + b * 3 * NQ, z);
+#pragma unroll
+      for (int n = 0; n < NQ; ++n)
+        z[n] = (valid && ((cm >> n) & 1ull)) ? z[n] * a.scale_log2 : -INFINITY;
+      tc_fence_before();
+      mbar_arrive(&s_empty[b]);             // S of this buffer has been read
+      // column max and sum over the 64 slots of this half: butterfly transpose-reduce in
+      // the warp, then the half's two warps combine through smem (double-buffered by parity)
+#pragma unroll
+      for (int c = 0; c < NQ; c += kW<NQ>) {
+        const float m = warp_reduceW<kW<NQ>, true>(z + c, lane);
+        if (!(lane & 1)) red_m[b][quad][c + myc] = m;
+      }
+      named_bar_sync(1 + half, 64);
+      float p[NQ];
+#pragma unroll
+      for (int n = 0; n < NQ; ++n) {
+        const float m = fmaxf(red_m[b][half * 2][n], red_m[b][half * 2 + 1][n]);
+        p[n] = fast_exp2(z[n] - m);          // z = −inf (masked) → 0; m = −inf only if all masked
+        if (z[n] == -INFINITY) p[n] = 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < NQ; c += kW<NQ>) {
+        const float l = warp_reduceW<kW<NQ>, false>(p + c, lane);
+        if (!(lane & 1)) red_l[b][quad][c + myc] = l;
+      }
+      // P buffer b was last read by MMA2(k−2)
+      if (k >= 2) mbar_wait(&o_full[b], ((k - 2) >> 1) & 1u);
+      // P (bf16) into rows [half·NQ, half·NQ + NQ) of slot-half `half` of the Pᵀ tile
+      {
+        unsigned char *Pt = Pbuf + b * S::kP + half * (2 * NQ * 128);
+        const uint32_t cb = static_cast<uint32_t>(tc * 2);
+#pragma unroll
+        for (int n = 0; n < NQ; ++n) {
+          const int r = half * NQ + n;
+          *reinterpret_cast<__nv_bfloat16 *>(Pt + r * 128 + ((((cb >> 4) ^ (r & 7))) << 4) + (cb & 15)) =
+              __float2bfloat16_rn(p[n]);
+        }
+      }
+      // V rows of a partly filled last page hold pool bytes past k_cur: zero them so that
+      // 0 · v stays 0 in Oᵀ = Vᵀ·Pᵀ (the rows past the last page were zeroed before)
+      if (present && (nt & (P - 1))) {
+        const int r0 = nt, r1 = (nt + P - 1) & ~(P - 1);
+        unsigned char *Vs = sm + s * S::kStage + kKVBytes;
+        const int tl = trow - half * 64;   // 0..63 within the half
+        for (int idx = tl; idx < (r1 - r0) * 16; idx += 64) {
+          const int r = half * kHalf + r0 + (idx >> 4), c16 = idx & 15;
+          *reinterpret_cast<uint4 *>(Vs + (c16 >> 3) * 16384 + r * 128 + (c16 & 7) * 16) =
+              make_uint4(0, 0, 0, 0);
+        }
+      }
+      fence_proxy_async();
+      named_bar_sync(1 + half, 64);
+      mbar_arrive(&p_full[b]);
+      if (tid == 64) TC_TRACE(k, 9);
+      // global writes after the MMA has been released
+      const int64_t rowbase = ((static_cast<int64_t>(pb) * a.Lc + hd.li) * a.g.H + hd.h) * G;
+      if (valid) {   // logits for the fused score pass: zbuf[pair][li][h][g][slot]
+        float *zr = a.zbuf + rowbase * kAttnChunk + tc;
+#pragma unroll
+        for (int n = 0; n < NQ; ++n)
+          if ((cm >> n) & 1ull) zr[static_cast<int64_t>(offn[n]) * kAttnChunk] = z[n];
+      }
+      const int col = lane + 32 * (quad & 1);   // the half's two warps cover columns 0..63
+      if (present && col < NQ && ((cm >> col) & 1ull)) {
+        // m (log2 domain) and l of column `col` for this half's chunk
+        const float mm = fmaxf(red_m[b][half * 2][col], red_m[b][half * 2 + 1][col]);
+        const float ll = red_l[b][half * 2][col] + red_l[b][half * 2 + 1][col];
+        float *dst = a.partials + (rowbase + (col >> 3) * SP + (col & 7)) * 130;
+        dst[128] = mm;
+        dst[129] = ll;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------- epilogue (warps 6..9)
+    // Oᵀ[d][half·NQ + n] (TMEM lane = d) → partials[pair][li][h][g][d]
+    const int quad = warp & 3;
+    const int trow = quad * 32 + lane;
+    const int G = a.G;
+    const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
+    const int SP = a.Lc * a.g.H * G;
+    int offn[NQ];
+#pragma unroll
+    for (int n = 0; n < NQ; ++n) offn[n] = (n >> 3) * SP + (n & 7);
+    for (int k = 0; k < ntiles; ++k) {
+      const int b = k & 1;
+      mbar_wait(&o_full[b], (k >> 1) & 1u);
+      if (tid == 192) TC_TRACE(k, 10);
+      tc_fence_after();
+      const TcHdr hd = ohdr[k & 3];   // read before o_empty: softmax(k+4) rewrites this slot
+      float o[2 * NQ];
+      tmem_ld<2 * NQ>(tmem + lane_addr + b * 3 * NQ + NQ, o);
+      tc_fence_before();
+      mbar_arrive(&o_empty[b]);
+      const unsigned long long cm = colmask(hd.cnt, G);
+      float *pa = a.partials + ((static_cast<int64_t>(hd.pbA) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
+      float *pbp = a.partials + ((static_cast<int64_t>(hd.pbB) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
+#pragma unroll
+      for (int n = 0; n < NQ; ++n) {
+        if ((cm >> n) & 1ull) pa[static_cast<int64_t>(offn[n]) * 130] = o[n];
+        if (((cm >> n) & 1ull) && hd.hasB) pbp[static_cast<int64_t>(offn[n]) * 130] = o[NQ + n];
+      }
+      if (tid == 192) TC_TRACE(k, 11);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+    a.trace[(static_cast<int64_t>(blockIdx.x) * 64 + 63) * 16 + 1] = static_cast<long long>(g1);
+    a.trace[(static_cast<int64_t>(blockIdx.x) * 64 + 63) * 16 + 2] = clock64() - t_start;
+  }
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(tmem_cols<NQ>()));
+  }
+}
+
+template <int NQ, int NST>
+void launch_tc(arbor_ctx *c, const TcArgs &a) {
+  using S = TcSmem<NQ, NST>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_tc_kernel<NQ, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(S::kAlloc));
+    attr = true;
+  }
+  static int sms = 0;
+  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
+  const int total = a.T * a.Lc * a.g.H;
+  const int grid = total < sms ? total : sms;
+  attn_tc_kernel<NQ, NST><<<grid, kTcThreads, S::kAlloc, c->ms>>>(
+      *reinterpret_cast<const CUtensorMap *>(c->tmap_k),
+      *reinterpret_cast<const CUtensorMap *>(c->tmap_v),
+      *reinterpret_cast<const CUtensorMap *>(c->tmap_k4),
+      *reinterpret_cast<const CUtensorMap *>(c->tmap_v4),
+      *reinterpret_cast<const CUtensorMap *>(c->tmap_q[c->tmap_q_cur]), a);
+}
+
+long long *g_tc_trace = nullptr;
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+
+// [rows][128] bf16 viewed 2-D, box 64 × box_rows, SWIZZLE_128B (out-of-range rows read as 0)
+bool encode_rows(void *map, const void *base, unsigned long long rows, unsigned box_rows) {
+  const cuuint64_t dims[2] = {128, rows};
+  const cuuint64_t strides[1] = {256};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return g_encode(reinterpret_cast<CUtensorMap *>(map), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The pool [L·NP][H][P][128] as 5-D (d-low 64, d-half 2, slot P, head H, layer·page L·NP),
+// box {64, 1, P, 1, 64/P}: the 64 rows of 64/P consecutive pages of one (layer, head) and one
+// d-half, landing as 64 consecutive 128-B swizzled rows (the K-major operand layout).
+bool encode_pool5(void *map, const void *base, int L, int NP, int H, int P) {
+  const cuuint64_t dims[5] = {64, 2, static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(H),
+                              static_cast<cuuint64_t>(L) * NP};
+  const cuuint64_t strides[4] = {128, 256, static_cast<cuuint64_t>(P) * 256,
+                                 static_cast<cuuint64_t>(H) * P * 256};
+  const cuuint32_t box[5] = {64, 1, static_cast<cuuint32_t>(P), 1, static_cast<cuuint32_t>(64 / P)};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return g_encode(reinterpret_cast<CUtensorMap *>(map), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                  const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// Tensor maps over the caller's K / V pools viewed as [rows = L·NP·H·P][d] bf16, box 64 × P,
+// SWIZZLE_128B.  Returns false (the CUDA-core kernel is used) when the shape does not fit the
+// tensor-core path or the driver entry point is unavailable.
+bool attn_tc_init(arbor_ctx *c) {
+  c->tc_ok = false;
+  if (const char *e = getenv("ARBOR_ATTN")) {
+    if (e[0] == 'c') return false;   // ARBOR_ATTN=cuda: force the CUDA-core kernel
+  }
+  if (c->esize != 2 || c->D != 128 || c->P % 16 != 0 || c->P > 64 || c->G > 8) return false;
+  static_assert(sizeof(CUtensorMap) <= sizeof(c->tmap_k), "tensor map storage");
+  if (!g_encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  const unsigned long long rows = static_cast<unsigned long long>(c->L) * c->NP * c->H * c->P;
+  if (!encode_rows(c->tmap_k, c->cfg.k_pool, rows, static_cast<unsigned>(c->P)) ||
+      !encode_rows(c->tmap_v, c->cfg.v_pool, rows, static_cast<unsigned>(c->P)) ||
+      !encode_pool5(c->tmap_k4, c->cfg.k_pool, c->L, c->NP, c->H, c->P) ||
+      !encode_pool5(c->tmap_v4, c->cfg.v_pool, c->L, c->NP, c->H, c->P))
+    return false;
+  c->tc_ok = true;
+  return true;
+}
+
+// Launch the tensor-core attention if it applies to this plan; false → use the CUDA-core kernel.
+bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
+                    int layer_count, int max_cnt) {
+  if (!c->tc_ok || pv.T == 0) return false;
+  const int nq = 8 * max_cnt;          // one 8-row q slot per leaf of an item
+  // q as [nA · layer_count · Hq rows][128]; re-encoded only when the buffer or its rows change
+  const long long qrows = static_cast<long long>(pv.nA) * layer_count * c->Hq;
+  int slot = -1;   // small cache of q tensor maps keyed by (buffer, rows)
+  for (int i = 0; i < kQMaps; ++i)
+    if (c->tmap_q_ptr[i] == q && c->tmap_q_rows[i] == qrows) slot = i;
+  if (slot < 0) {
+    slot = c->tmap_q_next;
+    c->tmap_q_next = (c->tmap_q_next + 1) % kQMaps;
+    if (!encode_rows(c->tmap_q[slot], q, static_cast<unsigned long long>(qrows), 8)) return false;
+    c->tmap_q_ptr[slot] = q;
+    c->tmap_q_rows[slot] = qrows;
+  }
+  c->tmap_q_cur = slot;
+  TcArgs a{};
+  a.pv = pv;
+  a.g = PoolView{c->L, c->H, c->P, c->D, c->NP, c->max_pages_node, c->max_tokens};
+  a.ptab = c->d.ptab;
+  a.kcur = c->d.kcur;
+  a.q = static_cast<const __nv_bfloat16 *>(q);
+  a.partials = c->d.partials;
+  a.zbuf = c->d.zbuf;
+  a.layer_begin = layer_begin;
+  a.Lc = layer_count;
+  a.Hq = c->Hq;
+  a.G = c->G;
+  a.T = pv.T;
+  a.scale_log2 = kLog2e / sqrtf(128.f);
+  static long long *trace = nullptr;
+  if (getenv("ARBOR_TC_TRACE")) {
+    if (!trace) cudaMalloc(&trace, sizeof(long long) * 148 * 64 * 16);
+    cudaMemsetAsync(trace, 0, sizeof(long long) * 148 * 64 * 16, c->ms);
+    a.trace = trace;
+    g_tc_trace = trace;
+  }
+  if (nq <= 8) launch_tc<8, 3>(c, a);
+  else if (nq <= 16) launch_tc<16, 3>(c, a);
+  else if (nq <= 32) launch_tc<32, 2>(c, a);
+  else if (nq <= 48) launch_tc<48, 2>(c, a);
+  else return false;
+  return true;
+}
+
+}  // namespace arbor
+
+// debug only (not part of include/arbor.h): copy the last ARBOR_TC_TRACE timeline to the host
+extern "C" int arbor_debug_tc_trace(long long *host, long long count) {
+  if (!arbor::g_tc_trace) return -1;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(host, arbor::g_tc_trace, sizeof(long long) * count, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
+}

@@ -16,8 +16,9 @@
 namespace arbor {
 
 constexpr int kAttnChunk = 64;       // slots per attention / score chunk
-constexpr int kLeavesPerItem = 8;    // active leaves per attention work item (q rows staged)
+constexpr int kLeavesPerItem = 6;    // active leaves per attention work item (q rows staged)
 constexpr int kStashSlots = 4;
+constexpr int kQMaps = 4;            // cached q tensor maps (attn_tc.cu)
 constexpr int kRingSlots = 32;
 constexpr int kStageRing = 128;   // event pairs kept per profiled stage
 constexpr size_t kRingBytes = 1u << 20;
@@ -88,9 +89,10 @@ struct DevState {
 struct PlanView {
   const int32_t *ch_node, *ch_chunk, *ch_poff, *ch_pcnt;   // C chunks: (node, chunk) + pairs
   const int4 *it_rec;                                       // I items: {node, c0, pair base, cnt}
+  const int4 *tl_rec;                                       // T tensor-core tiles: {item A, item B|-1}
   const int32_t *pair_b;                                     // P pairs → active leaf index
   const int32_t *bp_off, *bp_list;                           // per leaf: pairs root→leaf
-  int C, I, nA, P;
+  int C, I, nA, P, T;
 };
 
 struct PoolView {
@@ -163,6 +165,16 @@ struct arbor_ctx {
   bool st_created = false;
   long long launches = 0;
   arbor::Snapshot snap[arbor::kStashSlots];
+  // tensor-core attention (attn_tc.cu): CUtensorMap storage for the K / V pools
+  alignas(64) unsigned char tmap_k[128] = {};
+  alignas(64) unsigned char tmap_v[128] = {};
+  alignas(64) unsigned char tmap_k4[128] = {};  // 5-D views: 64-row boxes over consecutive pages
+  alignas(64) unsigned char tmap_v4[128] = {};
+  alignas(64) unsigned char tmap_q[arbor::kQMaps][128] = {};   // q maps of recent q buffers
+  const void *tmap_q_ptr[arbor::kQMaps] = {};
+  long long tmap_q_rows[arbor::kQMaps] = {};
+  int tmap_q_next = 0, tmap_q_cur = 0;
+  bool tc_ok = false;
   std::string err;
 };
 
@@ -193,7 +205,11 @@ void launch_rehydrate_copy(arbor_ctx *c, int count, int max_n);
 
 // attn.cu
 void launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
-                         int layer_count);
+                         int layer_count, int max_cnt);
+// attn_tc.cu (tcgen05 path for bf16, d = 128)
+bool attn_tc_init(arbor_ctx *c);
+bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
+                    int layer_count, int max_cnt);
 void launch_attn_merge(arbor_ctx *c, const PlanView &pv, int layer_count, void *out,
                        float *lse);
 
