@@ -253,6 +253,11 @@ enum { ARBOR_ST_GEOMETRY = 0, ARBOR_ST_SCORE_ACCUM, ARBOR_ST_NODE_MASS, ARBOR_ST
        ARBOR_ST_COMPACT_MOVE };
 arbor_status arbor_stage_times(arbor_ctx *ctx, float *ms);
 arbor_status arbor_reset_stage_times(arbor_ctx *ctx);
+/* Turn the per-stage event recording of a context created with ARBOR_FLAG_PROFILE on (1) or
+ * off (0).  A timing event costs the stream ~3 µs on B200, so throughput passes run with it
+ * off and a separate pass measures the per-kernel durations.  ARBOR_ERR_STATE without the
+ * flag. */
+arbor_status arbor_set_profiling(arbor_ctx *ctx, int32_t on);
 
 /* ---- host-only helpers (no device work; usable without a GPU) ------------------------ */
 /* Validate a tree snapshot: dense ids, parent < child, spans non-overlapping along

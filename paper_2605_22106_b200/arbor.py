@@ -97,6 +97,7 @@ def load_library(path: str = LIB_PATH):
         "arbor_invalidate_masses": ([P], I32),
         "arbor_stage_times": ([P, P], I32),
         "arbor_reset_stage_times": ([P], I32),
+        "arbor_set_profiling": ([P, I32], I32),
         "arbor_validate_tree": ([C.POINTER(ArborTree), I32, C.c_char_p, C.c_size_t], I32),
         "arbor_min_feasible_budget": ([C.POINTER(ArborParams), C.POINTER(ArborTree),
                                        C.POINTER(C.c_int64)], I32),
@@ -369,6 +370,9 @@ class ArborKV:
 
     def arbor_reset_stage_times(self):
         self._check(self.lib.arbor_reset_stage_times(self._ctx), "arbor_reset_stage_times")
+
+    def arbor_set_profiling(self, on: bool):
+        self._check(self.lib.arbor_set_profiling(self._ctx, 1 if on else 0), "arbor_set_profiling")
 
     def arbor_stage_times(self) -> dict:
         ms = (C.c_float * NUM_STAGES)()

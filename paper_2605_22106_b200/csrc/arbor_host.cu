@@ -430,11 +430,11 @@ namespace arbor {
 // Profiling: every stage launch is bracketed by a pair of CUDA events on its stream; the
 // last kStageRing pairs per stage are kept and averaged by arbor_stage_times (no sync here).
 void stage_begin(arbor_ctx *c, int st, cudaStream_t s) {
-  if (c->cfg.flags & ARBOR_FLAG_PROFILE)
+  if ((c->cfg.flags & ARBOR_FLAG_PROFILE) && c->profiling)
     cudaEventRecord(c->st_ev[st][c->st_count[st] % kStageRing][0], s);
 }
 void stage_end(arbor_ctx *c, int st, cudaStream_t s) {
-  if (c->cfg.flags & ARBOR_FLAG_PROFILE) {
+  if ((c->cfg.flags & ARBOR_FLAG_PROFILE) && c->profiling) {
     cudaEventRecord(c->st_ev[st][c->st_count[st] % kStageRing][1], s);
     ++c->st_count[st];
   }
@@ -1022,6 +1022,12 @@ arbor_status arbor_load_state(arbor_ctx *c, int32_t slot) {
 
 int64_t arbor_launch_count(const arbor_ctx *c) { return c ? c->launches : 0; }
 int32_t arbor_attn_tensor_cores(const arbor_ctx *c) { return c ? (c->tc_ok ? 1 : 0) : -1; }
+arbor_status arbor_set_profiling(arbor_ctx *c, int32_t on) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  if (!(c->cfg.flags & ARBOR_FLAG_PROFILE)) return fail(c, ARBOR_ERR_STATE, "context created without ARBOR_FLAG_PROFILE");
+  c->profiling = on != 0;
+  return ARBOR_OK;
+}
 
 #ifdef ARBOR_ALLOC_TRACE
 arbor_status arbor_debug_set_alloc_trace(arbor_ctx *c, long long *trace) {

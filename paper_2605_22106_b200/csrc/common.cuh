@@ -163,6 +163,7 @@ struct arbor_ctx {
   cudaEvent_t st_ev[ARBOR_NUM_STAGES][arbor::kStageRing][2] = {};
   int st_count[ARBOR_NUM_STAGES] = {};   // launches recorded since the last reset
   bool st_created = false;
+  bool profiling = true;                  // with ARBOR_FLAG_PROFILE: record stage events now
   long long launches = 0;
   arbor::Snapshot snap[arbor::kStashSlots];
   // tensor-core attention (attn_tc.cu): CUtensorMap storage for the K / V pools
