@@ -390,12 +390,12 @@ def main():
         rows = L * Hh
         # a9: K + V of every visible token-row, plus Q read and O written
         byts["attn"] = rows * vis * 2 * rb + nA * ctx.Hq * L * 2 * rb
-        # a9 + a2 fused (a2 reuses a9's logits, so the K read is shared): a9's bytes + the
-        # read-modify-write of A (8 B) per visible token-row
-        byts["attn_score"] = byts["attn"] + rows * vis * 8
         # a3: A changes only at visible tokens, so only the visible closed nodes' partial
         # masses are recomputed (4 B per visible token-row); the rest are cached
         byts["node_mass"] = rows * vis * 4
+        # a9 + a2 + a3 fused (a2 reuses a9's logits, so the K read is shared): a9's bytes +
+        # the read-modify-write of A (8 B) + the node-mass read (4 B) per visible token-row
+        byts["attn_score"] = byts["attn"] + rows * vis * 8 + byts["node_mass"]
         return byts
 
     ab = [alg_bytes(0), alg_bytes(1)]
@@ -419,18 +419,17 @@ def main():
         kernels = {"select_compact": kstat("select_compact",
                                            lambda i: ab[i]["select"] + ab[i]["compact_move"])}
         top_name, top_desc = "select_compact", "select_move_ws (a5+a6, warp-specialised)"
-    kernels.update({
-        "attn_partial": kstat("attn", lambda i: ab[i]["attn"]),
-        "node_mass": kstat("node_mass", lambda i: ab[i]["node_mass"]),
-    })
+    kernels["attn_partial"] = kstat("attn", lambda i: ab[i]["attn"])
+    if stage_ms["node_mass"][0] > 0:          # unfused a3 (multi-rank runs)
+        kernels["node_mass"] = kstat("node_mass", lambda i: ab[i]["node_mass"])
     # a9 + a2 as one unit: the fused path's bytes over attn + merge + score-apply time
-    t_as = statistics.mean(stage_ms["attn"]) + statistics.mean(stage_ms["attn_merge"]) + \
-        statistics.mean(stage_ms["score_accum"])
+    t_as = sum(statistics.mean(stage_ms[k]) for k in ("attn", "attn_merge", "score_accum",
+                                                       "node_mass", "msve"))
     b_as = statistics.mean(ab[i]["attn_score"] for i in range(2))
     kernels["attn_score_fused"] = {"ms": t_as, "bytes": b_as, "GBps": b_as / (t_as / 1e3) / 1e9,
                                    "frac_measured": b_as / (t_as / 1e3) / 1e9 / peak,
                                    "frac_nominal": b_as / (t_as / 1e3) / 1e9 / NOMINAL_HBM,
-                                   "stages": ["attn", "attn_merge", "score_accum"]}
+                                   "stages": ["attn", "attn_merge", "score_accum", "node_mass", "msve"]}
     top = kernels[top_name]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")

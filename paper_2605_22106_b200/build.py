@@ -29,7 +29,8 @@ def _deps():
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OBJ, src.replace(".cu", ".o"))
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    extra = os.environ.get("ARBOR_NVCC_FLAGS", "").split()   # debug builds, e.g. -DARBOR_ALLOC_TRACE
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

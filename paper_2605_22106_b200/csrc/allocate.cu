@@ -24,7 +24,7 @@ constexpr double kWeightScale = 16777216.0;   // 2^24
 constexpr double kEps = 1e-9;
 
 struct AllocArgs {
-  int N;
+  int N, Mpad;   // Mpad: breakpoint capacity (2N)
   long long budget;
   int mode;
   double alpha, gamma, eta, r_min;
@@ -97,6 +97,9 @@ allocate_kernel(AllocArgs a) {
   int *f = nn + N;                                              // [N]
   int *k = f + N;                                               // [N]
   int *cls = k + N;                                             // [N] class
+  // breakpoint candidates (num int64 | den int32), 8-byte aligned; reused as rank[] later
+  int *cand = reinterpret_cast<int *>((reinterpret_cast<uintptr_t>(cls + N) + 7) & ~uintptr_t(7));
+  const int Mpad = a.Mpad;
   __shared__ long long red64[33];
   __shared__ unsigned long long best_num, best_den;
   __shared__ int best_set;
@@ -237,60 +240,108 @@ allocate_kernel(AllocArgs a) {
       for (int j = threadIdx.x; j < N; j += blockDim.x)
         if (cls[j] == 2) k[j] = f[j];
       const long long Bpp = Bp - SfZ;
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-      // S(λ) = Σ_j clamp(W_j/λ, f_j, n_j) is nonincreasing; its breakpoints are W_j/n_j and
-      // W_j/f_j (f_j > 0).  One thread per candidate β evaluates S(β) exactly over all
-      // positive-weight nodes (smem broadcast reads, independent iterations) and keeps the
-      // largest feasible β: S(β) ≥ 𝓑'' ⇔ SA·den ≥ (𝓑'' − Sb)·num (128-bit products).
-      long long my_num = 0, my_den = 1;
-      int my_set = 0;
+      // S(λ) = Σ_j clamp(W_j/λ, f_j, n_j) is continuous and nonincreasing; its breakpoints
+      // are W_j/n_j and W_j/f_j (f_j > 0).  β* = the largest breakpoint with S(β*) ≥ 𝓑''
+      // (exact: S(β) ≥ 𝓑'' ⇔ SA·den ≥ (𝓑'' − Sb)·num in 128-bit, W < 2^40, n, f < 2^15).
+      // Multisection: each round a warp per pivot tests 16 pivots exactly; the candidates
+      // outside [largest feasible pivot, smallest infeasible pivot) are dropped; ≤ 16 left →
+      // test them all.  ~3 rounds for a few hundred breakpoints.
+      long long *cnum = reinterpret_cast<long long *>(cand);          // [2N]
+      int *cden = reinterpret_cast<int *>(cnum + 2 * N);              // [2N]
+      __shared__ int ncand, nnext, piv_ok[kThreads / 32];
+      __shared__ long long lo_num, hi_num;
+      __shared__ int lo_den, hi_den, lo_set, hi_set;
+      if (threadIdx.x == 0) ncand = 0;
+      __syncthreads();
       for (int c = threadIdx.x; c < 2 * N; c += blockDim.x) {
         const int j = c >> 1;
-        if (cls[j] != 1) continue;
-        const long long cden = (c & 1) ? f[j] : nn[j];
-        if (cden <= 0) continue;
-        const long long cnum = W[j];
+        if (cls[j] == 1 && ((c & 1) == 0 || f[j] > 0)) {
+          const int slot = atomicAdd(&ncand, 1);
+          cnum[slot] = W[j];
+          cden[slot] = (c & 1) ? f[j] : nn[j];
+        }
+      }
+      __syncthreads();
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      // exact feasibility of β = num/den, one warp (lanes over nodes)
+      auto feasible = [&](long long cn, long long cd) -> bool {
         long long SA = 0, Sb = 0;
-#pragma unroll 4
-        for (int i = 0; i < N; ++i) {
-          const int ci = cls[i];
-          const long long Wi = W[i];
+        for (int i = lane; i < N; i += 32) {
+          if (cls[i] != 1) continue;
+          const long long Wd = W[i] * cd;
           const long long ni = nn[i], fi = f[i];
-          const long long Wd = Wi * cden;                              // < 2^55
-          const bool capped = Wd >= ni * cnum;
-          const bool floored = !capped && fi > 0 && Wd <= fi * cnum;
-          const bool on = ci == 1;
-          Sb += on ? (capped ? ni : (floored ? fi : 0)) : 0;
-          SA += (on && !capped && !floored) ? Wi : 0;
+          if (Wd >= ni * cn) Sb += ni;                       // capped
+          else if (fi > 0 && Wd <= fi * cn) Sb += fi;        // floored
+          else SA += W[i];                                   // active
         }
-        const __int128 lhs = static_cast<__int128>(SA) * cden;
-        const __int128 rhs = static_cast<__int128>(Bpp - Sb) * cnum;
-        if (lhs >= rhs && (!my_set || cnum * my_den > my_num * cden)) {
-          my_num = cnum;
-          my_den = cden;
-          my_set = 1;
-        }
-      }
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const long long on = __shfl_xor_sync(0xffffffffu, my_num, o);
-        const long long od = __shfl_xor_sync(0xffffffffu, my_den, o);
-        const int os = __shfl_xor_sync(0xffffffffu, my_set, o);
-        if (os && (!my_set || on * my_den > my_num * od)) { my_num = on; my_den = od; my_set = 1; }
+        for (int o = 16; o; o >>= 1) {
+          SA += __shfl_xor_sync(0xffffffffu, SA, o);
+          Sb += __shfl_xor_sync(0xffffffffu, Sb, o);
+        }
+        return static_cast<__int128>(SA) * cd >= static_cast<__int128>(Bpp - Sb) * cn;
+      };
+      int M = ncand;
+      int stall = 0;
+      while (M > 0) {
+        const bool all = M <= nw || stall;   // test every remaining candidate this round
+        const int P = all ? M : nw;
+        // pivots: evenly spaced list entries (all entries when testing all)
+        for (int p0 = 0; p0 < P; p0 += nw) {
+          const int p = p0 + wid;
+          if (p < P) {
+            const int e = all ? p : static_cast<int>((static_cast<long long>(p) * M) / P);
+            const bool ok = feasible(cnum[e], cden[e]);
+            if (lane == 0) piv_ok[wid] = ok;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            if (p0 == 0) { lo_set = 0; hi_set = 0; }
+            for (int w = 0; w < nw && p0 + w < P; ++w) {
+              const int e = all ? p0 + w : static_cast<int>((static_cast<long long>(p0 + w) * M) / P);
+              const long long cn = cnum[e];
+              const int cd = cden[e];
+              if (piv_ok[w]) {
+                if (!lo_set || cn * lo_den > lo_num * cd) { lo_num = cn; lo_den = cd; lo_set = 1; }
+              } else {
+                if (!hi_set || cn * hi_den < hi_num * cd) { hi_num = cn; hi_den = cd; hi_set = 1; }
+              }
+            }
+          }
+          __syncthreads();
+        }
+        if (all) break;
+        // keep lo ≤ ratio < hi (compacted in place: read all, then write)
+        if (threadIdx.x == 0) nnext = 0;
+        __syncthreads();
+        constexpr int kCap = (2 * 4096 + kThreads - 1) / kThreads;   // max_nodes ≤ 4096
+        long long kn[kCap];
+        int kd[kCap], kc = 0;
+        for (int e = threadIdx.x; e < M; e += blockDim.x) {
+          const long long cn = cnum[e];
+          const int cd = cden[e];
+          const bool ge_lo = !lo_set || cn * lo_den >= lo_num * cd;
+          const bool lt_hi = !hi_set || cn * hi_den < hi_num * cd;
+          if (ge_lo && lt_hi) { kn[kc] = cn; kd[kc] = cd; ++kc; }
+        }
+        __syncthreads();
+        const int base = kc ? atomicAdd(&nnext, kc) : 0;
+        for (int i = 0; i < kc; ++i) { cnum[base + i] = kn[i]; cden[base + i] = kd[i]; }
+        __syncthreads();
+        stall = nnext == M;   // every pivot tied with lo: test all the rest next round
+        M = nnext;
       }
-      __shared__ long long wnum[kThreads / 32], wden[kThreads / 32];
-      __shared__ int wset[kThreads / 32];
-      if (lane == 0) { wnum[wid] = my_num; wden[wid] = my_den; wset[wid] = my_set; }
       __syncthreads();
       if (threadIdx.x == 0) {
-        long long bn = 0, bd = 1;
-        int bs = 0;
-        for (int w = 0; w < nw; ++w)
-          if (wset[w] && (!bs || wnum[w] * bd > bn * wden[w])) { bn = wnum[w]; bd = wden[w]; bs = 1; }
-        if (!bs) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-        best_num = static_cast<unsigned long long>(bn);
-        best_den = static_cast<unsigned long long>(bd);
-        best_set = bs;
+        if (!lo_set) {
+          atomicOr(&a.ctrl->err, DERR_INVARIANT);
+          best_num = 0;
+          best_den = 1;
+        } else {
+          best_num = static_cast<unsigned long long>(lo_num);
+          best_den = static_cast<unsigned long long>(lo_den);
+        }
+        best_set = 1;
       }
       __syncthreads();
       TRACE(4);
@@ -323,17 +374,29 @@ allocate_kernel(AllocArgs a) {
       given = block_sum(given, red64);
       TRACE(5);
       const long long leftover = Num - given;
-      __syncthreads();
-      for (int j = threadIdx.x; j < N && leftover > 0; j += blockDim.x) {   // thread per node
-        if (cls[j] != 6) continue;
-        const long long rj = rem[j], Wj = W[j];
-        int rank = 0;
-#pragma unroll 4
-        for (int i = 0; i < N; ++i) {
-          const long long ri = rem[i], Wi = W[i];
-          rank += (cls[i] == 6) && (ri > rj || (ri == rj && (Wi > Wj || (Wi == Wj && i < j))));
+      if (leftover > 0) {
+        // largest remainder: rank of each active node by (rem desc, W desc, id asc); the
+        // O(N²) comparisons are split over S = blockDim/N threads per node (partial counts)
+        int *rank = cand;                       // the breakpoint list is no longer needed
+        const int S = max(1, static_cast<int>(blockDim.x) / N);
+        const int span = (N + S - 1) / S;
+        for (int j = threadIdx.x; j < N; j += blockDim.x) rank[j] = 0;
+        __syncthreads();
+        for (int t = threadIdx.x; t < N * S; t += blockDim.x) {
+          const int j = t / S, sl = t - j * S;
+          if (cls[j] != 6) continue;
+          const long long rj = rem[j], Wj = W[j];
+          int cnt = 0;
+          const int i1 = min(N, (sl + 1) * span);
+          for (int i = sl * span; i < i1; ++i) {
+            const long long ri = rem[i], Wi = W[i];
+            cnt += (cls[i] == 6) && (ri > rj || (ri == rj && (Wi > Wj || (Wi == Wj && i < j))));
+          }
+          if (cnt) atomicAdd(&rank[j], cnt);
         }
-        if (rank < leftover) k[j] += 1;
+        __syncthreads();
+        for (int j = threadIdx.x; j < N; j += blockDim.x)
+          if (cls[j] == 6 && rank[j] < leftover) k[j] += 1;
       }
     }
   }
@@ -369,7 +432,9 @@ void launch_allocate(arbor_ctx *c, int N, const float *s, int64_t budget, int32_
   a.k_out = k_out;
   a.ctrl = c->d.ctrl;
   a.trace = c->d.alloc_trace;
-  const size_t smem = static_cast<size_t>(N) * (2 * sizeof(long long) + 4 * sizeof(int));
+  a.Mpad = 2 * N;
+  const size_t smem = static_cast<size_t>(N) * (2 * sizeof(long long) + 4 * sizeof(int)) + 8 +
+                      static_cast<size_t>(2 * N) * (sizeof(long long) + sizeof(int));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(allocate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);

@@ -551,6 +551,8 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   ALLOC(d.span, MN); ALLOC(d.mass2, 2 * MN); ALLOC(d.mclose, MN); ALLOC(d.nq, MN);
   ALLOC(d.a, MN); ALLOC(d.s, MN); ALLOC(d.mass_part, MN);
   ALLOC(d.mass_scratch, static_cast<size_t>(MN) * c->L);
+  ALLOC(d.mass_acc, MN);
+  ALLOC(d.ticket, 1);
   ALLOC(d.ctrl, 1);
   {
     // tree mirror block: [parent | len | active | v | u | open] (fixed offsets, see upload_tree)
@@ -643,7 +645,8 @@ void arbor_destroy(arbor_ctx *c) {
   void *ptrs[] = {d.n, d.kcur, d.npages, d.ptab, d.free_stack, d.span, d.mass2, d.mclose, d.nq,
                   d.a, d.s, d.ctrl, d.parent, d.onpath, d.pinned, d.depth, d.delta, d.Ed, d.ED,
                   d.work_node, d.work_old, d.work_new, d.moves, d.rehyd_nodes, d.rehyd_flag, d.seg,
-                  d.partials, d.lse_scratch, d.out_scratch, d.zbuf, d.mass_part, d.mass_scratch};
+                  d.partials, d.lse_scratch, d.out_scratch, d.zbuf, d.mass_part, d.mass_scratch,
+                  d.mass_acc, d.ticket};
   for (void *p : ptrs) if (p) cudaFree(p);
   for (auto &sn : c->snap) {
     if (!sn.valid) continue;
@@ -782,25 +785,23 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
     TRY(run_attention(c, hp, pv, 0, c->L, q, c->d.out_scratch, c->d.lse_scratch));
     if (!lse) lse_use = c->d.lse_scratch;
   }
-  launch_score_apply(c, pv, lse_use, c->L);
+  // a2 + a3 in one launch (score.cu): score pass, partial masses, Mass/Mclose → mass2, and —
+  // single rank — the MSVE score; with several ranks the all-reduce sits before the MSVE
+  const bool single = c->cfg.world_size == 1;
+  launch_score_fused(c, pv, lse_use, d_mass_nodes, static_cast<int>(mass_nodes.size()), N, single,
+                     s_out);
   CK_LAUNCH();
   c->lg_epoch = -1;   // A changed: the logits must not be applied twice
-  stage_begin(c, ARBOR_ST_NODE_MASS, c->ms);
-  launch_node_mass(c, d_mass_nodes, static_cast<int>(mass_nodes.size()), c->d.mass_part, 1);
-  CK_LAUNCH();
   c->mass_valid = true;
-  CK(cudaMemcpyAsync(c->d.mass2, c->d.mass_part, N * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->ms));
-  CK(cudaMemcpyAsync(c->d.mass2 + N, c->d.mclose, N * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->ms));
-  stage_end(c, ARBOR_ST_NODE_MASS, c->ms);
-  if (c->cfg.world_size > 1) {
+  if (!single) {
     stage_begin(c, ARBOR_ST_ALLREDUCE, c->ms);
     if (g_nccl.allReduce(c->d.mass2, c->d.mass2, 2 * static_cast<size_t>(N), ncclInt64, ncclSum,
                          static_cast<ncclComm_t>(c->nccl_comm), c->ms) != ncclSuccess)
       return fail(c, ARBOR_ERR_NCCL, "ncclAllReduce failed");
     stage_end(c, ARBOR_ST_ALLREDUCE, c->ms);
+    launch_msve(c, N, s_out);
+    CK_LAUNCH();
   }
-  launch_msve(c, N, s_out);
-  CK_LAUNCH();
   return ARBOR_OK;
 }
 

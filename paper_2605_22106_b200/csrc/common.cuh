@@ -75,6 +75,8 @@ struct DevState {
   float *zbuf;               // attention log2-domain logits (fused score pass)
   int64_t *mass_part;        // this rank's per-node partial mass (cached, §score.cu)
   int64_t *mass_scratch;     // [max_nodes][layer_count] node-mass partials
+  int64_t *mass_acc;         // [max_nodes] int64 accumulators of the fused score kernel (zero at rest)
+  unsigned int *ticket;      // last-CTA ticket of the fused score kernel (zero at rest)
   long long *alloc_trace;    // debug builds only (ARBOR_ALLOC_TRACE)
   float *lse_scratch;        // used when arbor_score gets lse == NULL
   void *out_scratch;
@@ -190,6 +192,8 @@ void launch_score_apply(arbor_ctx *c, const PlanView &pv, const float *lse, int 
 void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64_t *out,
                       int out_stride);
 void launch_msve(arbor_ctx *c, int N, float *s_out);
+void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
+                        int num_nodes, int N, bool do_msve, float *s_out);
 
 // allocate.cu
 void launch_allocate(arbor_ctx *c, int N, const float *s, int64_t budget, int32_t *k_out);

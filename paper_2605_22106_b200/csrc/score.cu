@@ -142,7 +142,172 @@ __global__ void msve_kernel(MsveArgs m) {
   if (m.s_out) m.s_out[i] = m.open[i] ? 0.5f : s;
 }
 
+// ---------------------------------------------------------------- fused a2 + a3 (one launch)
+// One CTA per (layer, KV head) row: (1) apply the fused score pass to every visible chunk of
+// the row (as score_apply_kernel), (2) after a CTA barrier, the row's fp64 span sums of A
+// for the listed closed nodes → Q = round-half-even(m·2^24), added to an int64 accumulator
+// (integer addition: exact and order-independent, so the result equals the two-kernel path
+// bit for bit); (3) the last CTA to finish (threadfence + ticket) publishes Mass and Mclose
+// into mass2, resets the accumulators and — single rank — evaluates the MSVE score (a3).
+struct FusedArgs {
+  ApplyArgs ap;
+  const int32_t *mass_nodes;
+  int n_mass, N, L, H;
+  int64_t max_tokens;
+  const int32_t *nlen;
+  unsigned long long *acc;     // [max_nodes] int64 accumulators (zero between calls)
+  int64_t *mass_part, *mass2;
+  const int64_t *mclose;
+  unsigned int *ticket;
+  int do_msve;
+  MsveArgs m;
+};
+
+constexpr int kFusedThreads = 256;
+
+__device__ __forceinline__ void msve_one(const MsveArgs &m, int i) {
+  float s = 0.5f, af = 0.f;
+  if (!m.open[i]) {
+    double a = 0.0;
+    const long long nq = m.nq[i];
+    if (nq > 0) {
+      const double num = static_cast<double>(m.mass2[i] - m.mass2[m.N + i]) * (1.0 / 16777216.0);
+      a = __ddiv_rn(num, __dmul_rn(static_cast<double>(nq), m.norm));
+      a = fmin(1.0, fmax(0.0, a));
+    }
+    double z = __dadd_rn(m.th0, __dmul_rn(m.thv, static_cast<double>(m.v[i])));
+    z = __dadd_rn(z, __dmul_rn(m.thu, static_cast<double>(m.u[i])));
+    z = __dadd_rn(z, __dmul_rn(m.tha, a));
+    double sd = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-z)));
+    sd = fmin(1.0, fmax(0.0, sd));
+    s = __double2float_rn(sd);
+    af = static_cast<float>(a);
+    m.s_state[i] = s;
+  }
+  m.a_out[i] = af;
+  if (m.s_out) m.s_out[i] = m.open[i] ? 0.5f : s;
+}
+
+__global__ void __launch_bounds__(kFusedThreads)
+score_fused_kernel(FusedArgs f) {
+  const ApplyArgs &a = f.ap;
+  const int row = blockIdx.x;                 // li * H + h
+  const int li = row / f.H, h = row - li * f.H;
+  const int tid = threadIdx.x;
+  // (1) A[li][h][a_j + pos] += Σ_pairs Σ_g exp2(z − LSE·log2 e)
+  for (int idx = tid; idx < a.pv.C * kAttnChunk; idx += kFusedThreads) {
+    const int c = idx / kAttnChunk, t = idx - c * kAttnChunk;
+    const int node = a.pv.ch_node[c];
+    const int c0 = a.pv.ch_chunk[c] * kAttnChunk;
+    const int nt = max(0, min(kAttnChunk, a.kcur[node] - c0));
+    if (t >= nt) continue;
+    const int p0 = a.pv.ch_poff[c], pc = a.pv.ch_pcnt[c];
+    float psum = 0.f;
+    for (int p = p0; p < p0 + pc; ++p) {
+      const int b = a.pv.pair_b[p];
+      const float *z = a.zbuf + (((static_cast<int64_t>(p) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + t;
+      const float *ls = a.lse + (static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * a.G;
+      for (int g = 0; g < a.G; ++g) psum += exp2f(z[g * kAttnChunk] - ls[g] * kLog2e);
+    }
+    const int slot = c0 + t;
+    const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.g.MPN;
+    const int pos = a.pos[pool_row(a.g, li, pl[slot / a.g.P], h, slot % a.g.P)];
+    float *dst = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + a.span[node] + pos;
+    const float nv = *dst + psum;
+    if (!(nv >= 0.f) || isinf(nv)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+    *dst = nv;
+  }
+  __syncthreads();
+  // (2) this row's partial node masses: warp per node, lanes strided, fixed xor tree (Q29)
+  const int warp = tid >> 5, lane = tid & 31;
+  const float *Arow = a.A + (static_cast<int64_t>(li) * f.H + h) * f.max_tokens;
+  for (int mi = warp; mi < f.n_mass; mi += kFusedThreads / 32) {
+    const int node = f.mass_nodes[mi];
+    const int n = f.nlen[node];
+    const float *r = Arow + a.span[node];
+    double m = 0.0;
+    for (int t = lane; t < n; t += 32) m += static_cast<double>(r[t]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+    if (lane == 0) atomicAdd(&f.acc[node], static_cast<unsigned long long>(__double2ll_rn(m * 16777216.0)));
+  }
+  // (3) last CTA: publish, reset, MSVE
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(f.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int mi = tid; mi < f.n_mass; mi += kFusedThreads) {
+    const int node = f.mass_nodes[mi];
+    volatile unsigned long long *acc = f.acc;
+    f.mass_part[node] = static_cast<int64_t>(acc[node]);
+    acc[node] = 0ull;
+  }
+  if (tid == 0) *f.ticket = 0u;
+  __syncthreads();
+  for (int i = tid; i < f.N; i += kFusedThreads) {
+    f.mass2[i] = f.mass_part[i];
+    f.mass2[f.N + i] = f.mclose[i];
+  }
+  if (!f.do_msve) return;
+  __syncthreads();
+  for (int i = tid; i < f.N; i += kFusedThreads) msve_one(f.m, i);
+}
+
 }  // namespace
+
+void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
+                        int num_nodes, int N, bool do_msve, float *s_out) {
+  FusedArgs f{};
+  ApplyArgs &a = f.ap;
+  a.pv = pv;
+  a.g = PoolView{c->L, c->H, c->P, c->D, c->NP, c->max_pages_node, c->max_tokens};
+  a.pos = c->cfg.pos_pool;
+  a.ptab = c->d.ptab;
+  a.kcur = c->d.kcur;
+  a.span = c->d.span;
+  a.zbuf = c->d.zbuf;
+  a.lse = lse;
+  a.A = c->cfg.score;
+  a.ctrl = c->d.ctrl;
+  a.Lc = c->L;
+  a.Hq = c->Hq;
+  a.G = c->G;
+  f.mass_nodes = d_nodes;
+  f.n_mass = num_nodes;
+  f.N = N;
+  f.L = c->L;
+  f.H = c->H;
+  f.max_tokens = c->max_tokens;
+  f.nlen = c->d.n;
+  f.acc = reinterpret_cast<unsigned long long *>(c->d.mass_acc);
+  f.mass_part = c->d.mass_part;
+  f.mass2 = c->d.mass2;
+  f.mclose = c->d.mclose;
+  f.ticket = c->d.ticket;
+  f.do_msve = do_msve ? 1 : 0;
+  MsveArgs &m = f.m;
+  m.N = N;
+  m.open = c->d.open;
+  m.v = c->d.v;
+  m.u = c->d.u;
+  m.mass2 = c->d.mass2;
+  m.nq = c->d.nq;
+  m.norm = static_cast<double>(c->Lg) * static_cast<double>(c->Hqg);
+  m.th0 = c->prm.theta[0];
+  m.thv = c->prm.theta[1];
+  m.thu = c->prm.theta[2];
+  m.tha = c->prm.theta[3];
+  m.a_out = c->d.a;
+  m.s_state = c->d.s;
+  m.s_out = s_out;
+  stage_begin(c, ARBOR_ST_SCORE_ACCUM, c->ms);
+  score_fused_kernel<<<c->L * c->H, kFusedThreads, 0, c->ms>>>(f);
+  ARBOR_LAUNCHED(c);
+  stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
+}
 
 void launch_score_apply(arbor_ctx *c, const PlanView &pv, const float *lse, int layer_count) {
   if (pv.C == 0) return;
