@@ -84,7 +84,7 @@ typedef struct {
   int32_t kv_dtype;        /* arbor_dtype of K/V/Q/O                                        */
   int32_t page_size;       /* P tokens per page: a power of two in 2..1024                   */
   int32_t num_pages;       /* pages in each pool                                             */
-  int32_t max_nodes;       /* capacity of the node table                                     */
+  int32_t max_nodes;       /* capacity of the node table, 1..3072 (a4 runs in one CTA's smem) */
   int32_t max_node_tokens; /* capacity of one node (≤ 32767; pos tags are int16)            */
   int32_t max_active;      /* capacity of active leaves per call                             */
   int64_t max_tokens;      /* capacity of the absolute position stream                      */

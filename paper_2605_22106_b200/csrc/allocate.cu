@@ -31,8 +31,11 @@ struct AllocArgs {
   int k_min, l_tail, gamma_int;   // gamma_int ≥ 0: integer exponent (repeated products)
   const float *s;
   const int32_t *n;
-  const uint8_t *onpath, *open;
-  const int32_t *depth, *delta;
+  const int32_t *parent, *active;
+  int nA;
+  const uint8_t *open;
+  uint8_t *onpath, *pinned;     // written (a1 fused)
+  int32_t *depth, *delta;       // written (a1 fused)
   const double *Ed, *ED;
   int32_t *k_out;
   Ctrl *ctrl;
@@ -104,11 +107,50 @@ allocate_kernel(AllocArgs a) {
   __shared__ unsigned long long best_num, best_den;
   __shared__ int best_set;
 
+  // ---- a1 geometry (Alg. 2; Q14), fused: parent pointers in smem; depth by
+  // walking to the root, Path* = ∪ root→ℓ chains, Δ_i = min_ℓ d_i + d_ℓ − 2·d_lca(i, ℓ).
+  // Results also go to global memory (depth, Δ, Path*, pinned) for arbor_evict.
+  int *par = reinterpret_cast<int *>(cand + 3 * a.Mpad);         // [N] (after the candidates)
+  int *dep = par + N;                                            // [N]
+  int *dlt = dep + N;                                            // [N]
+  int *act = dlt + N;                                            // [nA]
+  unsigned char *onp = reinterpret_cast<unsigned char *>(act + a.nA);   // [N]
+  for (int j = threadIdx.x; j < N; j += blockDim.x) { par[j] = a.parent[j]; onp[j] = 0; }
+  for (int b = threadIdx.x; b < a.nA; b += blockDim.x) act[b] = a.active[b];
+  __syncthreads();
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    int d = 0;
+    for (int x = par[j]; x >= 0; x = par[x]) ++d;
+    dep[j] = d;
+  }
+  for (int b = threadIdx.x; b < a.nA; b += blockDim.x)
+    for (int x = act[b]; x >= 0; x = par[x]) onp[x] = 1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    int best = 0x7fffffff;
+    const int di = dep[i];
+    for (int b = 0; b < a.nA; ++b) {
+      int x = i, y = act[b];
+      int dx = di, dy = dep[y];
+      while (dx > dy) { x = par[x]; --dx; }
+      while (dy > dx) { y = par[y]; --dy; }
+      while (x != y) { x = par[x]; y = par[y]; --dx; }
+      const int dist = di + dep[act[b]] - 2 * dx;
+      best = dist < best ? dist : best;
+    }
+    dlt[i] = best;
+    a.depth[i] = di;
+    a.delta[i] = best;
+    a.onpath[i] = onp[i];
+    a.pinned[i] = (onp[i] || a.open[i]) ? 1 : 0;
+  }
+  __syncthreads();
+
   // per-node weight, floors, pinned
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
     const int nj = a.n[j];
     nn[j] = nj;
-    const bool pin = a.onpath[j] || a.open[j];
+    const bool pin = onp[j] || a.open[j];
     // w = s^γ · E_d[d] · E_Δ[Δ] · (η if off-path), strictly left to right
     const double s = static_cast<double>(a.s[j]);
     double w;
@@ -118,9 +160,9 @@ allocate_kernel(AllocArgs a) {
     } else {
       w = s > 0.0 ? exp(a.gamma * log(s)) : 0.0;
     }
-    w = __dmul_rn(w, a.Ed[a.depth[j]]);
-    w = __dmul_rn(w, a.ED[a.delta[j]]);
-    if (!a.onpath[j]) w = __dmul_rn(w, a.eta);
+    w = __dmul_rn(w, a.Ed[dep[j]]);
+    w = __dmul_rn(w, a.ED[dlt[j]]);
+    if (!onp[j]) w = __dmul_rn(w, a.eta);
     if (!(w >= 0.0) || w > 65536.0) {
       atomicOr(&a.ctrl->err, DERR_INVARIANT);
       w = 0.0;
@@ -314,7 +356,7 @@ allocate_kernel(AllocArgs a) {
         // keep lo ≤ ratio < hi (compacted in place: read all, then write)
         if (threadIdx.x == 0) nnext = 0;
         __syncthreads();
-        constexpr int kCap = (2 * 4096 + kThreads - 1) / kThreads;   // max_nodes ≤ 4096
+        constexpr int kCap = (2 * 3072 + kThreads - 1) / kThreads;   // max_nodes ≤ 3072
         long long kn[kCap];
         int kd[kCap], kc = 0;
         for (int e = threadIdx.x; e < M; e += blockDim.x) {
@@ -407,7 +449,7 @@ allocate_kernel(AllocArgs a) {
 
 }  // namespace
 
-void launch_allocate(arbor_ctx *c, int N, const float *s, int64_t budget, int32_t *k_out) {
+void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget, int32_t *k_out) {
   AllocArgs a{};
   a.N = N;
   a.budget = budget;
@@ -423,7 +465,11 @@ void launch_allocate(arbor_ctx *c, int N, const float *s, int64_t budget, int32_
                     ? static_cast<int>(g) : -1;
   a.s = s;
   a.n = c->d.len;
+  a.parent = c->d.parent;
+  a.active = c->d.active;
+  a.nA = nA;
   a.onpath = c->d.onpath;
+  a.pinned = c->d.pinned;
   a.open = c->d.open;
   a.depth = c->d.depth;
   a.delta = c->d.delta;
@@ -433,8 +479,10 @@ void launch_allocate(arbor_ctx *c, int N, const float *s, int64_t budget, int32_
   a.ctrl = c->d.ctrl;
   a.trace = c->d.alloc_trace;
   a.Mpad = 2 * N;
+  // [W rem | nn f k cls | candidates (2N × 12 B, as 3·Mpad ints) | par dep dlt | act | onp]
   const size_t smem = static_cast<size_t>(N) * (2 * sizeof(long long) + 4 * sizeof(int)) + 8 +
-                      static_cast<size_t>(2 * N) * (sizeof(long long) + sizeof(int));
+                      static_cast<size_t>(3 * a.Mpad) * sizeof(int) +
+                      static_cast<size_t>(3 * N + nA) * sizeof(int) + N + 16;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(allocate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);

@@ -222,8 +222,7 @@ arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
   std::memcpy(b + MN * 16 + MA * 4, t->is_open, N);
   CK(cudaMemcpyAsync(c->d.parent, b, bytes, cudaMemcpyHostToDevice, c->ms));
   CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
-  launch_geometry(c, N, nA);
-  CK_LAUNCH();
+  // a1 runs inside arbor_allocate's kernel; arbor_evict launches it only if needed
   c->t_parent.assign(t->parent, t->parent + N);
   c->t_len.assign(t->span_len, t->span_len + N);
   c->t_active.assign(t->active, t->active + nA);
@@ -360,10 +359,12 @@ arbor_status ensure_partials(arbor_ctx *c, size_t pairs, int layer_count) {
 arbor_status run_attention(arbor_ctx *c, const HostPlan &hp, const PlanView &pv, int layer_begin,
                            int layer_count, const void *q, void *out, float *lse) {
   TRY(ensure_partials(c, hp.pair_b.size(), layer_count));
-  launch_attn_partial(c, pv, q, layer_begin, layer_count, hp.max_cnt);
+  const bool merged = launch_attn_partial(c, pv, q, layer_begin, layer_count, hp.max_cnt, out, lse);
   CK_LAUNCH();
-  launch_attn_merge(c, pv, layer_count, out, lse);
-  CK_LAUNCH();
+  if (!merged) {
+    launch_attn_merge(c, pv, layer_count, out, lse);
+    CK_LAUNCH();
+  }
   return ARBOR_OK;
 }
 
@@ -510,7 +511,7 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   if (k.kv_dtype != ARBOR_F32 && k.kv_dtype != ARBOR_BF16) return ARBOR_ERR_INVALID_ARG;
   if (k.page_size < 2 || k.page_size > 1024 || (k.page_size & (k.page_size - 1)) || k.num_pages < 1)
     return ARBOR_ERR_INVALID_ARG;   // page size: a power of two (shift addressing)
-  if (k.max_nodes < 1 || k.max_nodes > 4096) return ARBOR_ERR_INVALID_ARG;
+  if (k.max_nodes < 1 || k.max_nodes > 3072) return ARBOR_ERR_INVALID_ARG;   // a4 smem
   if (k.max_node_tokens < 1 || k.max_node_tokens > 32767) return ARBOR_ERR_INVALID_ARG;
   if (k.max_active < 1 || k.max_active > 1024 || k.max_tokens < 1) return ARBOR_ERR_INVALID_ARG;
   if (!k.k_pool || !k.v_pool || !k.pos_pool || !k.score) return ARBOR_ERR_INVALID_ARG;
@@ -553,6 +554,7 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   ALLOC(d.mass_scratch, static_cast<size_t>(MN) * c->L);
   ALLOC(d.mass_acc, MN);
   ALLOC(d.ticket, 1);
+  ALLOC(d.row_done, static_cast<size_t>(c->L) * c->H);
   ALLOC(d.ctrl, 1);
   {
     // tree mirror block: [parent | len | active | v | u | open] (fixed offsets, see upload_tree)
@@ -646,7 +648,7 @@ void arbor_destroy(arbor_ctx *c) {
                   d.a, d.s, d.ctrl, d.parent, d.onpath, d.pinned, d.depth, d.delta, d.Ed, d.ED,
                   d.work_node, d.work_old, d.work_new, d.moves, d.rehyd_nodes, d.rehyd_flag, d.seg,
                   d.partials, d.lse_scratch, d.out_scratch, d.zbuf, d.mass_part, d.mass_scratch,
-                  d.mass_acc, d.ticket};
+                  d.mass_acc, d.ticket, d.row_done};
   for (void *p : ptrs) if (p) cudaFree(p);
   for (auto &sn : c->snap) {
     if (!sn.valid) continue;
@@ -826,8 +828,9 @@ arbor_status arbor_allocate(arbor_ctx *c, const arbor_tree *tree, const float *s
                                                     " < minimum feasible " + std::to_string(mf));
   }
   TRY(upload_tree(c, tree));
-  launch_allocate(c, tree->num_nodes, s ? s : c->d.s, budget, k_out);
+  launch_allocate(c, tree->num_nodes, tree->num_active, s ? s : c->d.s, budget, k_out);
   CK_LAUNCH();
+  c->geom_version = c->tree_version;   // the allocate kernel wrote depth, Δ, Path*, pinned
   return ARBOR_OK;
 }
 
@@ -843,6 +846,11 @@ arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_
     if (!pin[i]) max_n = std::max(max_n, c->h_n[i]);
   wait_side(c);   // pending stash copies read pages this call may free
   ++c->epoch;
+  if (c->geom_version != c->tree_version) {   // pinned set of this tree not on the device yet
+    launch_geometry(c, tree->num_nodes, tree->num_active);
+    CK_LAUNCH();
+    c->geom_version = c->tree_version;
+  }
   launch_evict_plan(c, tree->num_nodes, k_target);
   CK_LAUNCH();
   if (max_n > 0) {

@@ -394,14 +394,14 @@ void launch_stream_q(arbor_ctx *c, StreamArgs a) {
 
 }  // namespace
 
-void launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
-                         int layer_count, int max_cnt) {
-  if (pv.I == 0) return;
+bool launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
+                         int layer_count, int max_cnt, void *out, float *lse) {
+  if (pv.I == 0) return false;
   stage_begin(c, ARBOR_ST_ATTN, c->ms);
-  if (launch_attn_tc(c, pv, q, layer_begin, layer_count, max_cnt)) {   // attn_tc.cu
+  if (launch_attn_tc(c, pv, q, layer_begin, layer_count, max_cnt, out, lse)) {   // attn_tc.cu
     ARBOR_LAUNCHED(c);
     stage_end(c, ARBOR_ST_ATTN, c->ms);
-    return;
+    return false;   // partials only: merged by attn_merge_kernel
   }
   StreamArgs a{};
   a.pv = pv;
@@ -428,6 +428,7 @@ void launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int la
   }
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_ATTN, c->ms);
+  return false;
 }
 
 void launch_attn_merge(arbor_ctx *c, const PlanView &pv, int layer_count, void *out, float *lse) {

@@ -55,6 +55,9 @@ struct TcArgs {
   const int32_t *ptab, *kcur;
   const __nv_bfloat16 *q;
   float *partials, *zbuf;
+  __nv_bfloat16 *out;              // merged output [nA][Lc][Hq][128] and LSE [nA][Lc][Hq]
+  float *lse;
+  unsigned int *row_done;          // [Lc·H] tiles finished per row (zero at rest)
   int layer_begin, Lc, Hq, G, T;   // T: tiles
   float scale_log2;
   long long *trace;                // debug: clock64 per (CTA, tile, event) or NULL
@@ -300,7 +303,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], o_full[2], o_empty[2];
   __shared__ TcHdr hdr[NST];
   __shared__ TcHdr ohdr[4];                             // tile k's header for the epilogue warps
-  __shared__ float red_m[2][4][NQ], red_l[2][4][NQ];   // [tile parity][warp quadrant][column]
+  // column max / sum of each warp quadrant, ring of 4 tiles (the epilogue warps read tile k's
+  // before releasing Oᵀ buffer k&1, which softmax(k+4) needs first)
+  __shared__ float red_m[4][4][NQ], red_l[4][4][NQ];
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -548,20 +553,20 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 #pragma unroll
       for (int c = 0; c < NQ; c += kW<NQ>) {
         const float m = warp_reduceW<kW<NQ>, true>(z + c, lane);
-        if (!(lane & 1)) red_m[b][quad][c + myc] = m;
+        if (!(lane & 1)) red_m[k & 3][quad][c + myc] = m;
       }
       named_bar_sync(1 + half, 64);
       float p[NQ];
 #pragma unroll
       for (int n = 0; n < NQ; ++n) {
-        const float m = fmaxf(red_m[b][half * 2][n], red_m[b][half * 2 + 1][n]);
+        const float m = fmaxf(red_m[k & 3][half * 2][n], red_m[k & 3][half * 2 + 1][n]);
         p[n] = fast_exp2(z[n] - m);          // z = −inf (masked) → 0; m = −inf only if all masked
         if (z[n] == -INFINITY) p[n] = 0.f;
       }
 #pragma unroll
       for (int c = 0; c < NQ; c += kW<NQ>) {
         const float l = warp_reduceW<kW<NQ>, false>(p + c, lane);
-        if (!(lane & 1)) red_l[b][quad][c + myc] = l;
+        if (!(lane & 1)) red_l[k & 3][quad][c + myc] = l;
       }
       // P buffer b was last read by MMA2(k−2)
       if (k >= 2) mbar_wait(&o_full[b], ((k - 2) >> 1) & 1u);
@@ -600,15 +605,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         for (int n = 0; n < NQ; ++n)
           if ((cm >> n) & 1ull) zr[static_cast<int64_t>(offn[n]) * kAttnChunk] = z[n];
       }
-      const int col = lane + 32 * (quad & 1);   // the half's two warps cover columns 0..63
-      if (present && col < NQ && ((cm >> col) & 1ull)) {
-        // m (log2 domain) and l of column `col` for this half's chunk
-        const float mm = fmaxf(red_m[b][half * 2][col], red_m[b][half * 2 + 1][col]);
-        const float ll = red_l[b][half * 2][col] + red_l[b][half * 2 + 1][col];
-        float *dst = a.partials + (rowbase + (col >> 3) * SP + (col & 7)) * 130;
-        dst[128] = mm;
-        dst[129] = ll;
-      }
     }
   } else {
     // ------------------------------------------------------------- epilogue (warps 6..9)
@@ -621,12 +617,20 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     int offn[NQ];
 #pragma unroll
     for (int n = 0; n < NQ; ++n) offn[n] = (n >> 3) * SP + (n & 7);
+    const int etid = tid - 192;                // 0..127
     for (int k = 0; k < ntiles; ++k) {
       const int b = k & 1;
       mbar_wait(&o_full[b], (k >> 1) & 1u);
       if (tid == 192) TC_TRACE(k, 10);
       tc_fence_after();
       const TcHdr hd = ohdr[k & 3];   // read before o_empty: softmax(k+4) rewrites this slot
+      // m (log2 domain) and l of column idx = half·NQ + n, from the softmax ring slot k&3
+      float mm = 0.f, ll = 0.f;
+      const int hh = etid / NQ, cn = etid - hh * NQ;
+      if (etid < 2 * NQ) {
+        mm = fmaxf(red_m[k & 3][hh * 2][cn], red_m[k & 3][hh * 2 + 1][cn]);
+        ll = red_l[k & 3][hh * 2][cn] + red_l[k & 3][hh * 2 + 1][cn];
+      }
       float o[2 * NQ];
       tmem_ld<2 * NQ>(tmem + lane_addr + b * 3 * NQ + NQ, o);
       tc_fence_before();
@@ -638,6 +642,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       for (int n = 0; n < NQ; ++n) {
         if ((cm >> n) & 1ull) pa[static_cast<int64_t>(offn[n]) * 130] = o[n];
         if (((cm >> n) & 1ull) && hd.hasB) pbp[static_cast<int64_t>(offn[n]) * 130] = o[NQ + n];
+      }
+      if (etid < 2 * NQ && ((cm >> cn) & 1ull) && (hh == 0 || hd.hasB)) {
+        float *dst = (hh ? pbp : pa) - trow + static_cast<int64_t>((cn >> 3) * SP + (cn & 7)) * 130;
+        dst[128] = mm;
+        dst[129] = ll;
       }
       if (tid == 192) TC_TRACE(k, 11);
     }
@@ -746,7 +755,7 @@ bool attn_tc_init(arbor_ctx *c) {
 
 // Launch the tensor-core attention if it applies to this plan; false → use the CUDA-core kernel.
 bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
-                    int layer_count, int max_cnt) {
+                    int layer_count, int max_cnt, void *out, float *lse) {
   if (!c->tc_ok || pv.T == 0) return false;
   const int nq = 8 * max_cnt;          // one 8-row q slot per leaf of an item
   // q as [nA · layer_count · Hq rows][128]; re-encoded only when the buffer or its rows change
@@ -770,6 +779,9 @@ bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_b
   a.q = static_cast<const __nv_bfloat16 *>(q);
   a.partials = c->d.partials;
   a.zbuf = c->d.zbuf;
+  a.out = static_cast<__nv_bfloat16 *>(out);
+  a.lse = lse;
+  a.row_done = c->d.row_done;
   a.layer_begin = layer_begin;
   a.Lc = layer_count;
   a.Hq = c->Hq;

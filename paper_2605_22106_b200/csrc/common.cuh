@@ -77,6 +77,7 @@ struct DevState {
   int64_t *mass_scratch;     // [max_nodes][layer_count] node-mass partials
   int64_t *mass_acc;         // [max_nodes] int64 accumulators of the fused score kernel (zero at rest)
   unsigned int *ticket;      // last-CTA ticket of the fused score kernel (zero at rest)
+  unsigned int *row_done;    // [L·H] per-row tile counters of the tensor-core attention (zero at rest)
   long long *alloc_trace;    // debug builds only (ARBOR_ALLOC_TRACE)
   float *lse_scratch;        // used when arbor_score gets lse == NULL
   void *out_scratch;
@@ -137,6 +138,7 @@ struct arbor_ctx {
   std::vector<uint8_t> t_open;
   std::vector<float> t_v, t_u;
   bool tree_valid = false;
+  long long geom_version = -1;   // tree_version whose geometry (a1) is on the device
   // staging ring
   void *ring[arbor::kRingSlots] = {};
   cudaEvent_t ring_ev[arbor::kRingSlots] = {};
@@ -196,7 +198,7 @@ void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, cons
                         int num_nodes, int N, bool do_msve, float *s_out);
 
 // allocate.cu
-void launch_allocate(arbor_ctx *c, int N, const float *s, int64_t budget, int32_t *k_out);
+void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget, int32_t *k_out);
 
 // evict.cu
 void launch_evict_plan(arbor_ctx *c, int N, const int32_t *k_target);
@@ -209,12 +211,13 @@ void launch_rehydrate_plan(arbor_ctx *c, int count);
 void launch_rehydrate_copy(arbor_ctx *c, int count, int max_n);
 
 // attn.cu
-void launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
-                         int layer_count, int max_cnt);
+// returns true when the partials were also merged into out / lse (tensor-core path)
+bool launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
+                         int layer_count, int max_cnt, void *out, float *lse);
 // attn_tc.cu (tcgen05 path for bf16, d = 128)
 bool attn_tc_init(arbor_ctx *c);
 bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
-                    int layer_count, int max_cnt);
+                    int layer_count, int max_cnt, void *out, float *lse);
 void launch_attn_merge(arbor_ctx *c, const PlanView &pv, int layer_count, void *out,
                        float *lse);
 
