@@ -101,7 +101,7 @@ allocate_kernel(AllocArgs a) {
   int *k = f + N;                                               // [N]
   int *cls = k + N;                                             // [N] class
   // breakpoint candidates (num int64 | den int32), 8-byte aligned; reused as rank[] later
-  int *cand = reinterpret_cast<int *>((reinterpret_cast<uintptr_t>(cls + N) + 7) & ~uintptr_t(7));
+  int *cand = cls + N;   // byte offset 32N: 8-byte aligned (the int64 candidate numerators)
   const int Mpad = a.Mpad;
   __shared__ long long red64[33];
   __shared__ unsigned long long best_num, best_den;
@@ -295,16 +295,23 @@ allocate_kernel(AllocArgs a) {
       __shared__ int lo_den, hi_den, lo_set, hi_set;
       if (threadIdx.x == 0) ncand = 0;
       __syncthreads();
-      for (int c = threadIdx.x; c < 2 * N; c += blockDim.x) {
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      const unsigned lt = (1u << lane) - 1u;
+      for (int c0 = 0; c0 < 2 * N; c0 += blockDim.x) {   // warp-aggregated append
+        const int c = c0 + threadIdx.x;
         const int j = c >> 1;
-        if (cls[j] == 1 && ((c & 1) == 0 || f[j] > 0)) {
-          const int slot = atomicAdd(&ncand, 1);
+        const bool take = c < 2 * N && cls[j] == 1 && ((c & 1) == 0 || f[j] > 0);
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&ncand, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (take) {
+          const int slot = base + __popc(bal & lt);
           cnum[slot] = W[j];
           cden[slot] = (c & 1) ? f[j] : nn[j];
         }
       }
       __syncthreads();
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
       // exact feasibility of β = num/den, one warp (lanes over nodes)
       auto feasible = [&](long long cn, long long cd) -> bool {
         long long SA = 0, Sb = 0;
@@ -316,12 +323,12 @@ allocate_kernel(AllocArgs a) {
           else if (fi > 0 && Wd <= fi * cn) Sb += fi;        // floored
           else SA += W[i];                                   // active
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          SA += __shfl_xor_sync(0xffffffffu, SA, o);
-          Sb += __shfl_xor_sync(0xffffffffu, Sb, o);
-        }
-        return static_cast<__int128>(SA) * cd >= static_cast<__int128>(Bpp - Sb) * cn;
+        // warp sums with 32-bit reductions: per-lane SA < 2^48 split at bit 24, Sb < 2^30
+        const unsigned lo = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(SA & 0xFFFFFF));
+        const unsigned hi = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(SA >> 24));
+        const unsigned sb = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(Sb));
+        const long long SAt = (static_cast<long long>(hi) << 24) + lo, Sbt = sb;
+        return static_cast<__int128>(SAt) * cd >= static_cast<__int128>(Bpp - Sbt) * cn;
       };
       int M = ncand;
       int stall = 0;
@@ -337,17 +344,37 @@ allocate_kernel(AllocArgs a) {
             if (lane == 0) piv_ok[wid] = ok;
           }
           __syncthreads();
-          if (threadIdx.x == 0) {
-            if (p0 == 0) { lo_set = 0; hi_set = 0; }
-            for (int w = 0; w < nw && p0 + w < P; ++w) {
-              const int e = all ? p0 + w : static_cast<int>((static_cast<long long>(p0 + w) * M) / P);
-              const long long cn = cnum[e];
-              const int cd = cden[e];
-              if (piv_ok[w]) {
-                if (!lo_set || cn * lo_den > lo_num * cd) { lo_num = cn; lo_den = cd; lo_set = 1; }
-              } else {
-                if (!hi_set || cn * hi_den < hi_num * cd) { hi_num = cn; hi_den = cd; hi_set = 1; }
-              }
+          if (wid == 0) {
+            // lane w < P: pivot w; warp max over the feasible ratios, min over the infeasible
+            const int pw = p0 + lane;
+            const bool have = lane < nw && pw < P;
+            long long cn = 0;
+            int cd = 1, okf = 0;
+            if (have) {
+              const int e = all ? pw : static_cast<int>((static_cast<long long>(pw) * M) / P);
+              cn = cnum[e];
+              cd = cden[e];
+              okf = piv_ok[lane];
+            }
+            long long ln = cn, hn = cn;
+            int ld = cd, hd = cd;
+            int ls = have && okf, hs = have && !okf;
+            if (p0 > 0) {   // fold in the previous batch (lane 0 carries it)
+              if (lane == 0 && lo_set && (!ls || lo_num * ld > ln * lo_den)) { ln = lo_num; ld = lo_den; ls = 1; }
+              if (lane == 0 && hi_set && (!hs || hi_num * hd < hn * hi_den)) { hn = hi_num; hd = hi_den; hs = 1; }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              const long long on = __shfl_xor_sync(0xffffffffu, ln, o);
+              const int od = __shfl_xor_sync(0xffffffffu, ld, o), os = __shfl_xor_sync(0xffffffffu, ls, o);
+              if (os && (!ls || on * ld > ln * od)) { ln = on; ld = od; ls = 1; }
+              const long long hn2 = __shfl_xor_sync(0xffffffffu, hn, o);
+              const int hd2 = __shfl_xor_sync(0xffffffffu, hd, o), hs2 = __shfl_xor_sync(0xffffffffu, hs, o);
+              if (hs2 && (!hs || hn2 * hd < hn * hd2)) { hn = hn2; hd = hd2; hs = 1; }
+            }
+            if (lane == 0) {
+              lo_num = ln; lo_den = ld; lo_set = ls;
+              hi_num = hn; hi_den = hd; hi_set = hs;
             }
           }
           __syncthreads();
@@ -417,24 +444,20 @@ allocate_kernel(AllocArgs a) {
       TRACE(5);
       const long long leftover = Num - given;
       if (leftover > 0) {
-        // largest remainder: rank of each active node by (rem desc, W desc, id asc); the
-        // O(N²) comparisons are split over S = blockDim/N threads per node (partial counts)
+        // largest remainder: rank of each active node by (rem desc, W desc, id asc) — a warp
+        // per node, lanes over the other nodes, one __reduce_add_sync per node
         int *rank = cand;                       // the breakpoint list is no longer needed
-        const int S = max(1, static_cast<int>(blockDim.x) / N);
-        const int span = (N + S - 1) / S;
-        for (int j = threadIdx.x; j < N; j += blockDim.x) rank[j] = 0;
-        __syncthreads();
-        for (int t = threadIdx.x; t < N * S; t += blockDim.x) {
-          const int j = t / S, sl = t - j * S;
-          if (cls[j] != 6) continue;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int j = wid; j < N; j += nw) {
+          if (cls[j] != 6) continue;            // warp-uniform
           const long long rj = rem[j], Wj = W[j];
-          int cnt = 0;
-          const int i1 = min(N, (sl + 1) * span);
-          for (int i = sl * span; i < i1; ++i) {
+          unsigned cnt = 0;
+          for (int i = lane; i < N; i += 32) {
             const long long ri = rem[i], Wi = W[i];
-            cnt += (cls[i] == 6) && (ri > rj || (ri == rj && (Wi > Wj || (Wi == Wj && i < j))));
+            cnt += (cls[i] == 6) & ((ri > rj) | ((ri == rj) & ((Wi > Wj) | ((Wi == Wj) & (i < j)))));
           }
-          if (cnt) atomicAdd(&rank[j], cnt);
+          cnt = __reduce_add_sync(0xffffffffu, cnt);
+          if (lane == 0) rank[j] = static_cast<int>(cnt);
         }
         __syncthreads();
         for (int j = threadIdx.x; j < N; j += blockDim.x)

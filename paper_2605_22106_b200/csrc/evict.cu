@@ -90,11 +90,27 @@ evict_plan_kernel(PlanArgs a) {
     a.work_old[work_off] = kc[i];
     a.work_new[work_off] = kapp[i];
     ++work_off;
-    const int32_t *pl = a.ptab + static_cast<int64_t>(j) * a.MPN;
-    for (int t = 0; t < fr[i]; ++t) a.free_stack[top + free_off + t] = pl[newp[i] + t];
-    free_off += fr[i];
     a.npages[j] = newp[i];
     a.kcur[j] = kapp[i];
+  }
+  // freed pages → LIFO free stack, (node, list) ascending: all of a node's page ids are loaded
+  // before any store (the stores could alias the page table for the compiler, which would
+  // otherwise serialise one global load round trip per page)
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int j = threadIdx.x * kPer + i;
+    if (!ev[i] || fr[i] == 0) continue;
+    const int32_t *__restrict__ pl = a.ptab + static_cast<int64_t>(j) * a.MPN + newp[i];
+    int32_t *__restrict__ dst = a.free_stack + top + free_off;
+    constexpr int kB = 16;
+    for (int t0 = 0; t0 < fr[i]; t0 += kB) {
+      int32_t v[kB];
+#pragma unroll
+      for (int t = 0; t < kB; ++t) v[t] = t0 + t < fr[i] ? __ldg(pl + t0 + t) : 0;
+#pragma unroll
+      for (int t = 0; t < kB; ++t) if (t0 + t < fr[i]) dst[t0 + t] = v[t];
+    }
+    free_off += fr[i];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
