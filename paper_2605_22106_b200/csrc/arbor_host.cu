@@ -570,16 +570,11 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   }
   ALLOC(d.onpath, MN); ALLOC(d.pinned, MN); ALLOC(d.depth, MN); ALLOC(d.delta, MN);
   ALLOC(d.Ed, 2 * MN + 2); ALLOC(d.ED, 2 * MN + 2);
-  ALLOC(d.work_node, MN); ALLOC(d.work_old, MN); ALLOC(d.work_new, MN);
+  ALLOC(d.work, MN);
   {
-    // compaction move list: at most one move per retained slot of every row
+    // compaction rows are addressed with int32 row ids
     const int64_t rows_total = static_cast<int64_t>(c->L) * c->NP * c->H * c->P;
     if (rows_total >= (1ll << 31)) { c->err = "pool too large for int32 row ids"; return bail(ARBOR_ERR_INVALID_ARG); }
-    const size_t cap = static_cast<size_t>(c->L) * c->H *
-                       static_cast<size_t>(std::min<int64_t>(c->max_tokens, static_cast<int64_t>(c->NP) * c->P));
-    s = dmalloc(c, &d.moves, cap);
-    if (s != ARBOR_OK) return bail(s);
-    d.moves_cap = cap;
   }
   ALLOC(d.rehyd_nodes, MN + 1); ALLOC(d.rehyd_flag, MN + 2);
 #undef ALLOC
@@ -646,7 +641,7 @@ void arbor_destroy(arbor_ctx *c) {
   DevState &d = c->d;
   void *ptrs[] = {d.n, d.kcur, d.npages, d.ptab, d.free_stack, d.span, d.mass2, d.mclose, d.nq,
                   d.a, d.s, d.ctrl, d.parent, d.onpath, d.pinned, d.depth, d.delta, d.Ed, d.ED,
-                  d.work_node, d.work_old, d.work_new, d.moves, d.rehyd_nodes, d.rehyd_flag, d.seg,
+                  d.work, d.rehyd_nodes, d.rehyd_flag, d.seg,
                   d.partials, d.lse_scratch, d.out_scratch, d.zbuf, d.mass_part, d.mass_scratch,
                   d.mass_acc, d.ticket, d.row_done};
   for (void *p : ptrs) if (p) cudaFree(p);

@@ -43,6 +43,14 @@ struct Ctrl {
   long long pages_in_use;  // pages held by nodes
 };
 
+// One evict work entry (a changed, non-pinned node): written by evict_plan, read by the
+// select warps through 16-byte cp.async copies.
+struct __align__(16) WorkEnt {
+  int32_t node, kc, ka, n;   // node id, k_cur before, k_app after, n_i
+  int64_t span;              // a_i (absolute position of the node's first token)
+  int64_t pad;
+};
+
 // Per-launch geometry of the K/V pools
 struct PoolGeom {
   int L, H, P, D, NP;   // local layers, local kv heads, page size, head dim, pages
@@ -64,9 +72,7 @@ struct DevState {
   int32_t *depth, *delta;
   double *Ed, *ED;
   // evict plan
-  int32_t *work_node, *work_old, *work_new;
-  int2 *moves;               // compaction move list (src row, dst row)
-  size_t moves_cap;
+  WorkEnt *work;             // changed non-pinned nodes of the last plan, ascending id
   // rehydrate / append plans
   int32_t *rehyd_nodes, *rehyd_flag;
   // attention / score plan (uploaded per call)

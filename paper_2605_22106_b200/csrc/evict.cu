@@ -28,13 +28,17 @@ namespace arbor {
 namespace {
 
 constexpr int kPlanThreads = 1024;
+constexpr int kPairsWs = 8;   // (select warp, move warp) pairs per CTA of select_move_ws_kernel
+constexpr int kUw = 4;        // rows in flight per lane group of a move warp
 
 struct PlanArgs {
   int N, P, MPN;
   const int32_t *k_target;
   const uint8_t *pinned;
   int32_t *kcur, *npages, *ptab, *free_stack;
-  int32_t *work_node, *work_old, *work_new;
+  const int32_t *n;
+  const int64_t *span;
+  WorkEnt *work;
   Ctrl *ctrl;
 };
 
@@ -86,9 +90,14 @@ evict_plan_kernel(PlanArgs a) {
   for (int i = 0; i < kPer; ++i) {
     const int j = threadIdx.x * kPer + i;
     if (!ev[i]) continue;
-    a.work_node[work_off] = j;
-    a.work_old[work_off] = kc[i];
-    a.work_new[work_off] = kapp[i];
+    WorkEnt e;
+    e.node = j;
+    e.kc = kc[i];
+    e.ka = kapp[i];
+    e.n = a.n[j];
+    e.span = a.span[j];
+    e.pad = 0;
+    a.work[work_off] = e;
     ++work_off;
     a.npages[j] = newp[i];
     a.kcur[j] = kapp[i];
@@ -126,241 +135,86 @@ struct CompactArgs {
   int R;            // rows = L * H
   int H, P, D, NP, MPN, l_tail;
   int64_t max_tokens;
-  const int32_t *work_node, *work_old, *work_new, *n;
-  const int64_t *span;
+  const WorkEnt *work;
   const float *A;
   const Ctrl *ctrl_ro;
   Ctrl *ctrl;
   const int32_t *ptab;
   void *kpool, *vpool;
   int16_t *pos;
-  int2 *moves;      // (src row, dst row) pairs
   int esize;
   int cap;          // max n over evicted nodes (smem capacity, slots)
   int lgP;          // log2(page size)
+  int exp;          // ARBOR_EVICT_EXP (measurement only): bit0 skip moves, bit1 skip radix select
 };
 
-constexpr int kWarps = 8;     // warps per CTA in the select kernel (one warp per work item)
-// fused: each warp streams its own item's moves right after selecting it (other warps'
-// selection latency hides under those moves); split: select → global list → move_kernel
-constexpr bool kFusedCompact = true;
-constexpr bool kWarpSpecialised = true;   // select_move_ws_kernel (below) is the default
-
-// Select: one WARP per (node, row) work item.  Keep = the block tail 𝒯 (positions ≥ n − |𝒯|,
-// P:177-182) ∪ the top-m non-tail candidates by the 48-bit key ⟨A bits, pos⟩,
-// or the last k_app positions when k_app ≤ |𝒯| (Alg. 1).  The m-th largest key is
-// found by a warp radix select (8-bit digits, per-warp 256-bin smem histogram, warp scan):
-// exact, O(c).  Slot layout (Q23'): kept rows in slots [0, k_app) stay; the i-th
-// hole there takes the i-th kept row from slots ≥ k_app — sources and destinations are
-// disjoint, so the moves are appended to a global list and executed by move_kernel.
-// smem per warp: key[cap] (u64), hole list[cap], mover list[cap] (u16 pairs), pages.
-template <bool kFused>
-__global__ void __launch_bounds__(kWarps * 32, kFused ? 4 : 5)
-select_kernel(CompactArgs a) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cap = a.cap;
-  const int lgP = a.lgP, Pm = (1 << lgP) - 1;
-  const int pcap = (cap >> lgP) + 1;
-  unsigned long long *key = reinterpret_cast<unsigned long long *>(sm) + warp * cap;
-  int32_t *holes = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned long long *>(sm) +
-                                               kWarps * cap) + warp * 2 * cap;
-  int32_t *movers = holes + cap;
-  int32_t *pgs = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned long long *>(sm) +
-                                             kWarps * cap) + kWarps * 2 * cap + warp * pcap;
-  __shared__ uint32_t hist_all[kWarps][256];
-  uint32_t *hist = hist_all[warp];
-  const int items = a.ctrl_ro->work_count * a.R;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const int64_t pstride = static_cast<int64_t>(a.H) << lgP;
-  constexpr unsigned long long kCand = 1ull << 63;
-  for (int it = blockIdx.x * kWarps + warp; it < items; it += gridDim.x * kWarps) {
-    const int w = it / a.R, r = it - w * a.R;
-    const int l = r / a.H, h = r - l * a.H;
-    const int node = a.work_node[w];
-    const int kc = a.work_old[w], ka = a.work_new[w];
-    const int n = a.n[node];
-    const int tl = min(a.l_tail, n);
-    const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.MPN;
-    const int64_t base = (static_cast<int64_t>(l) * a.NP * a.H + h) << lgP;
-    for (int i = lane; i < ((kc + Pm) >> lgP); i += 32) pgs[i] = pl[i];
-    __syncwarp();
-    auto row = [&](int slot) -> int64_t {
-      return base + static_cast<int64_t>(pgs[slot >> lgP]) * pstride + (slot & Pm);
-    };
-    const bool ranked = ka > tl;
-    const int m = ka - tl;
-    const int tail_from = n - (ranked ? tl : ka);   // keep positions ≥ tail_from outright
-    // 1. pos tags of every kept slot; keys of the non-tail candidates (bit 63 = candidate)
-    const float *Arow = a.A + (static_cast<int64_t>(l) * a.H + h) * a.max_tokens + a.span[node];
-    int ncand = 0;
-    for (int s0 = 0; s0 < kc; s0 += 32) {
-      const int s = s0 + lane;
-      unsigned long long kk = 0;
-      if (s < kc) {
-        const int p = a.pos[row(s)];
-        kk = static_cast<unsigned>(p);   // pos in the low bits; no candidate bit
-        if (ranked && p < tail_from) {
-          const float av = Arow[p];
-          if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-          const unsigned bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
-          kk = kCand | (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
-        }
-        key[s] = kk;
-      }
-      ncand += __popc(__ballot_sync(0xffffffffu, (kk & kCand) != 0));
-    }
-    __syncwarp();
-    // 2. threshold: keep a candidate iff (key & tmask) >= tkey (the top m unique keys)
-    unsigned long long tkey = kCand, tmask = kCand;     // m ≥ ncand: all candidates
-    if (ranked && m <= 0) {
-      tkey = ~0ull; tmask = ~0ull;                      // none survives
-    } else if (ranked && m < ncand) {
-      unsigned long long prefix = kCand, pmask = kCand;
-      int need = m;
-      for (int shift = 40; shift >= 0; shift -= 8) {
-#pragma unroll
-        for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
-        __syncwarp();
-        for (int s = lane; s < kc; s += 32) {
-          const unsigned long long k = key[s];
-          if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
-        }
-        __syncwarp();
-        uint32_t c[8];
-        uint32_t loc = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) { c[b] = hist[255 - lane * 8 - b]; loc += c[b]; }
-        uint32_t incl = loc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        const uint32_t before = incl - loc;
-        const bool mine = before < static_cast<uint32_t>(need) && static_cast<uint32_t>(need) <= incl;
-        int dsel = 0;
-        uint32_t above = 0, inbin = 0;
-        if (mine) {
-          uint32_t acc = before;
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            if (inbin == 0 && acc < static_cast<uint32_t>(need) &&
-                static_cast<uint32_t>(need) <= acc + c[b]) {
-              dsel = 255 - lane * 8 - b;
-              above = acc;
-              inbin = c[b];
-            }
-            acc += c[b];
-          }
-        }
-        const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
-        dsel = __shfl_sync(0xffffffffu, dsel, src);
-        above = __shfl_sync(0xffffffffu, above, src);
-        inbin = __shfl_sync(0xffffffffu, inbin, src);
-        need -= static_cast<int>(above);
-        prefix |= static_cast<unsigned long long>(dsel) << shift;
-        pmask |= 255ull << shift;
-        if (static_cast<uint32_t>(need) == inbin) break;   // the whole bin survives
-      }
-      tkey = prefix;
-      tmask = pmask;
-    }
-    // 3. keep flags → holes (dropped slots < k_app) and movers (kept slots ≥ k_app), ascending
-    int nh = 0, nm = 0;
-    for (int s0 = 0; s0 < kc; s0 += 32) {
-      const int s = s0 + lane;
-      int keep = 0;
-      if (s < kc) {
-        const unsigned long long k = key[s];
-        const int p = static_cast<int>(k & 0xffffu);
-        keep = (p >= tail_from) || (ranked && (k & kCand) && (k & tmask) >= tkey);
-      }
-      const int hole = s < ka && !keep;
-      const int mover = s >= ka && s < kc && keep;
-      const unsigned hb = __ballot_sync(0xffffffffu, hole);
-      const unsigned mb = __ballot_sync(0xffffffffu, mover);
-      if (hole) holes[nh + __popc(hb & lt_mask)] = s;
-      if (mover) movers[nm + __popc(mb & lt_mask)] = s;
-      nh += __popc(hb);
-      nm += __popc(mb);
-    }
-    __syncwarp();
-    if (nh != nm && lane == 0) atomicOr(&a.ctrl->err, DERR_STATE);
-    if (kFused) {
-      // 4'. stream this item's moves directly (disjoint sources/destinations: no barriers)
-      const int rb = a.D * a.esize, cpr = rb >> 4, rpi = 32 / cpr;
-      const int piece = lane % cpr, sub = lane / cpr;
-      char *kp8 = static_cast<char *>(a.kpool);
-      char *vp8 = static_cast<char *>(a.vpool);
-      constexpr int kU = 4;
-      for (int c0 = 0; c0 < nm; c0 += rpi * kU) {
-        uint4 bk[kU], bv[kU];
-        int64_t srow[kU], drow[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int i = c0 + u * rpi + sub;
-          srow[u] = -1;
-          if (i < nm) {
-            srow[u] = row(movers[i]);
-            drow[u] = row(holes[i]);
-            bk[u] = *reinterpret_cast<const uint4 *>(kp8 + srow[u] * rb + piece * 16);
-            bv[u] = *reinterpret_cast<const uint4 *>(vp8 + srow[u] * rb + piece * 16);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          if (srow[u] >= 0) {
-            *reinterpret_cast<uint4 *>(kp8 + drow[u] * rb + piece * 16) = bk[u];
-            *reinterpret_cast<uint4 *>(vp8 + drow[u] * rb + piece * 16) = bv[u];
-            if (piece == 0) a.pos[drow[u]] = static_cast<int16_t>(key[movers[c0 + u * rpi + sub]] & 0xffffu);
-          }
-        }
-      }
-      __syncwarp();
-    } else {
-      // 4. append the (src, dst) row pairs to the global move list
-      int baseidx = 0;
-      if (lane == 0 && nm > 0) baseidx = atomicAdd(&a.ctrl->move_count, nm);
-      baseidx = __shfl_sync(0xffffffffu, baseidx, 0);
-      for (int i = lane; i < nm; i += 32)
-        a.moves[baseidx + i] = make_int2(static_cast<int>(row(movers[i])), static_cast<int>(row(holes[i])));
-      __syncwarp();
-    }
-  }
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16ca(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
 }
 
-// Warp-specialised select + move (default).  A CTA holds kPairs (select warp, move warp)
-// pairs.  Select warp p processes the work items it, it + stride, … exactly like select_kernel
-// and hands each item's (src row, dst row) list to its move warp through a 2-slot job queue
-// in shared memory guarded by mbarriers (full / empty); move warp p streams those rows (K, V:
-// 16-byte coalesced, kUw rows in flight per lane group; pos tags) while its select warp
-// already ranks the next item.  Selection (latency-bound) and data movement (HBM-bound) thus
-// overlap inside every SM.
-constexpr int kPairs = 8;
-constexpr int kUw = 4;
-__global__ void __launch_bounds__(kPairs * 64, 2)
+// Shared-memory layout of select_move_ws_kernel (per CTA), all offsets 16-byte aligned.
+struct WsLayout {
+  int cap, capP, pcap, jcap;
+  size_t keys, lists, abuf, pbuf, gbuf, mbuf, jobs, jcount, bars, total;
+  __host__ __device__ WsLayout(int cap_, int lgP) {
+    cap = cap_;
+    capP = (cap + 9) & ~7;                 // pos pairs may read one slot past k_cur
+    pcap = (cap >> lgP) + 2;
+    jcap = cap / 2 + 1;                    // moves per item ≤ min(k_app, k_cur − k_app)
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
+    keys = take(size_t(kPairsWs) * cap * 8);              // u64 keys
+    lists = take(size_t(kPairsWs) * 2 * cap * 4);         // holes | movers
+    abuf = take(size_t(kPairsWs) * 2 * cap * 4);          // A span, 2 pipeline slots
+    pbuf = take(size_t(kPairsWs) * 2 * capP * 2);         // pos tags, 2 pipeline slots
+    gbuf = take(size_t(kPairsWs) * 3 * pcap * 4);         // page lists, 3 pipeline slots
+    mbuf = take(size_t(kPairsWs) * 4 * sizeof(WorkEnt));  // work entries, 4 pipeline slots
+    jobs = take(size_t(kPairsWs) * 2 * jcap * 8);         // (src row, dst row) job queues
+    jcount = take(size_t(kPairsWs) * 2 * 4);
+    bars = take(size_t(kPairsWs) * 4 * 8);
+    total = o;
+  }
+};
+
+// Warp-specialised select + move.  A CTA holds kPairsWs (select warp, move warp) pairs.
+//
+// Select warp p processes the work items it = first + k·stride (item = (changed node, row)).
+// Its global reads run three items ahead through a cp.async pipeline (no register cost, no
+// exposed latency): work entry of item k+3 → page list of item k+2 → pos tags and A span of
+// item k+1 (A is read by position over the span, independent of the pos tags), while item k
+// is ranked from shared memory.  Keep = the block tail 𝒯 (positions ≥ n − |𝒯|)
+// ∪ the top-m non-tail candidates by the 48-bit key ⟨A bits, pos⟩, or the last
+// k_app positions when k_app ≤ |𝒯| (Alg. 1).  The m-th largest key is found by a
+// warp radix select (8-bit digits, per-warp smem histogram, warp scan) that starts at the
+// highest key bit on which the candidates differ (warp min/max reductions of the A bits), so
+// the shared exponent bits cost no pass.  Slot layout (Q23'): kept rows in slots
+// [0, k_app) stay; the i-th hole there takes the i-th kept row from slots ≥ k_app.  The item's
+// (src row, dst row) list goes to move warp p through a 2-slot job queue in shared memory
+// guarded by mbarriers (full / empty).
+//
+// Move warp p streams those rows (K, V: 16-byte coalesced, kUw rows in flight per lane group;
+// pos tags).  Sources and destinations are disjoint, so moves need no ordering.
+__global__ void __launch_bounds__(kPairsWs * 64, 2)
 select_move_ws_kernel(CompactArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool mover = warp >= kPairs;
-  const int pid = mover ? warp - kPairs : warp;
-  const int cap = a.cap;
-  const int jcap = cap / 2 + 1;                    // moves per item ≤ min(k_app, k_cur − k_app)
+  const bool mover = warp >= kPairsWs;
+  const int pid = mover ? warp - kPairsWs : warp;
+  const WsLayout Ly(a.cap, a.lgP);
+  const int cap = Ly.cap, capP = Ly.capP, pcap = Ly.pcap, jcap = Ly.jcap;
   const int lgP = a.lgP, Pm = (1 << lgP) - 1;
-  const int pcap = (cap >> lgP) + 1;
-  // smem: per select warp key[cap] u64, holes/movers[cap] i32 x2, pages[pcap];
-  //       per pair jobs[2][jcap] int2 + counts[2]; mbarriers full[pair][2], empty[pair][2]
-  unsigned long long *keys = reinterpret_cast<unsigned long long *>(sm);
-  int32_t *lists = reinterpret_cast<int32_t *>(keys + kPairs * cap);
-  int32_t *pages_all = lists + kPairs * 2 * cap;
-  int2 *jobs = reinterpret_cast<int2 *>(pages_all + ((kPairs * pcap + 1) & ~1));
-  int32_t *jcount = reinterpret_cast<int32_t *>(jobs + kPairs * 2 * jcap);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(jcount + ((kPairs * 2 + 1) & ~1));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + Ly.bars);
   uint64_t *full = bars + pid * 4, *empty = bars + pid * 4 + 2;
-  __shared__ uint32_t hist_all[kPairs][256];
+  int2 *myjobs = reinterpret_cast<int2 *>(sm + Ly.jobs) + pid * 2 * jcap;
+  int32_t *mycount = reinterpret_cast<int32_t *>(sm + Ly.jcount) + pid * 2;
+  __shared__ uint32_t hist_all[kPairsWs][256];
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kPairs * 2; ++i) {
+    for (int i = 0; i < kPairsWs * 2; ++i) {
       mbar_init(&bars[(i >> 1) * 4 + (i & 1)], 1);
       mbar_init(&bars[(i >> 1) * 4 + 2 + (i & 1)], 1);
     }
@@ -368,9 +222,8 @@ select_move_ws_kernel(CompactArgs a) {
   }
   __syncthreads();
   const int items = a.ctrl_ro->work_count * a.R;
-  const int stride = gridDim.x * kPairs;
-  int2 *myjobs = jobs + pid * 2 * jcap;
-  int32_t *mycount = jcount + pid * 2;
+  const int stride = gridDim.x * kPairsWs;
+  const int first = blockIdx.x * kPairsWs + pid;
   if (mover) {
     // ------------------------------------------------------------ move warp
     const int rb = a.D * a.esize, cpr = rb >> 4, rpi = 32 / cpr;
@@ -378,10 +231,10 @@ select_move_ws_kernel(CompactArgs a) {
     char *kp8 = static_cast<char *>(a.kpool);
     char *vp8 = static_cast<char *>(a.vpool);
     int k = 0;
-    for (int it = blockIdx.x * kPairs + pid; it < items; it += stride, ++k) {
+    for (int it = first; it < items; it += stride, ++k) {
       const int sl = k & 1;
       mbar_wait(&full[sl], (k >> 1) & 1);
-      const int nm = mycount[sl];
+      const int nm = (a.exp & 1) ? 0 : mycount[sl];
       const int2 *jb = myjobs + sl * jcap;
       for (int c0 = 0; c0 < nm; c0 += rpi * kUw) {
         uint4 bk[kUw], bv[kUw];
@@ -414,64 +267,139 @@ select_move_ws_kernel(CompactArgs a) {
     return;
   }
   // -------------------------------------------------------------- select warp
-  unsigned long long *key = keys + pid * cap;
-  int32_t *holes = lists + pid * 2 * cap;
+  unsigned long long *key = reinterpret_cast<unsigned long long *>(sm + Ly.keys) + pid * cap;
+  int32_t *holes = reinterpret_cast<int32_t *>(sm + Ly.lists) + pid * 2 * cap;
   int32_t *movers = holes + cap;
-  int32_t *pgs = pages_all + pid * pcap;
+  float *Abuf = reinterpret_cast<float *>(sm + Ly.abuf) + pid * 2 * cap;
+  int16_t *Pbuf = reinterpret_cast<int16_t *>(sm + Ly.pbuf) + pid * 2 * capP;
+  int32_t *Gbuf = reinterpret_cast<int32_t *>(sm + Ly.gbuf) + pid * 3 * pcap;
+  WorkEnt *Mbuf = reinterpret_cast<WorkEnt *>(sm + Ly.mbuf) + pid * 4;
   uint32_t *hist = hist_all[pid];
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t pstride = static_cast<int64_t>(a.H) << lgP;
   constexpr unsigned long long kCand = 1ull << 63;
-  int k = 0;
-  for (int it = blockIdx.x * kPairs + pid; it < items; it += stride, ++k) {
-    const int w = it / a.R, r = it - w * a.R;
+  const int my_items = first < items ? (items - first + stride - 1) / stride : 0;
+  auto row_base = [&](int it) -> int64_t {
+    const int r = it % a.R;
     const int l = r / a.H, h = r - l * a.H;
-    const int node = a.work_node[w];
-    const int kc = a.work_old[w], ka = a.work_new[w];
-    const int n = a.n[node];
-    const int tl = min(a.l_tail, n);
-    const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.MPN;
-    const int64_t base = (static_cast<int64_t>(l) * a.NP * a.H + h) << lgP;
-    for (int i = lane; i < ((kc + Pm) >> lgP); i += 32) pgs[i] = pl[i];
+    return (static_cast<int64_t>(l) * a.NP * a.H + h) << lgP;
+  };
+  // pipeline stages (each lane issues its share; completion via cp.async.wait_all + __syncwarp)
+  auto issue_meta = [&](int k) {
+    if (k >= my_items || lane >= 2) return;
+    const int w = (first + k * stride) / a.R;
+    cp_async16ca(reinterpret_cast<char *>(&Mbuf[k & 3]) + lane * 16,
+                 reinterpret_cast<const char *>(&a.work[w]) + lane * 16);
+  };
+  auto issue_pages = [&](int k) {
+    if (k >= my_items) return;
+    const WorkEnt &e = Mbuf[k & 3];
+    const int np = (e.kc + Pm) >> lgP;
+    const int32_t *pl = a.ptab + static_cast<int64_t>(e.node) * a.MPN;
+    int32_t *g = Gbuf + (k % 3) * pcap;
+    for (int i = lane; i < np; i += 32) cp_async4(g + i, pl + i);
+  };
+  auto issue_data = [&](int k) {
+    if (k >= my_items) return;
+    const int it = first + k * stride;
+    const WorkEnt &e = Mbuf[k & 3];
+    const int32_t *g = Gbuf + (k % 3) * pcap;
+    const int64_t base = row_base(it);
+    int16_t *pb = Pbuf + (k & 1) * capP;
+    for (int q = lane; 2 * q < e.kc; q += 32) {     // slot pairs (P even: same page)
+      const int s = 2 * q;
+      cp_async4(pb + s, a.pos + base + static_cast<int64_t>(g[s >> lgP]) * pstride + (s & Pm));
+    }
+    const int tl = min(a.l_tail, e.n);
+    if (e.ka > tl) {               // ranked: A of the non-tail positions
+      const int r = it % a.R;
+      const float *Arow = a.A + static_cast<int64_t>(r) * a.max_tokens + e.span;
+      float *ab = Abuf + (k & 1) * cap;
+      for (int p = lane; p < e.n - tl; p += 32) cp_async4(ab + p, Arow + p);
+    }
+  };
+  if (my_items > 0) {
+    issue_meta(0);
+    cp_async_commit();
+    cp_async_wait_all();
     __syncwarp();
+    issue_pages(0);
+    issue_meta(1);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    issue_data(0);
+    issue_pages(1);
+    issue_meta(2);
+    cp_async_commit();
+  }
+  for (int k = 0; k < my_items; ++k) {
+    cp_async_wait_all();
+    __syncwarp();
+    issue_data(k + 1);
+    issue_pages(k + 2);
+    issue_meta(k + 3);
+    cp_async_commit();
+    // ---- rank item k from shared memory
+    const int it = first + k * stride;
+    const WorkEnt e = Mbuf[k & 3];
+    const int kc = e.kc, ka = e.ka, n = e.n;
+    const int tl = min(a.l_tail, n);
+    const int32_t *pgs = Gbuf + (k % 3) * pcap;
+    const int16_t *pb = Pbuf + (k & 1) * capP;
+    const float *ab = Abuf + (k & 1) * cap;
+    const int64_t base = row_base(it);
     auto row = [&](int slot) -> int64_t {
       return base + static_cast<int64_t>(pgs[slot >> lgP]) * pstride + (slot & Pm);
     };
     const bool ranked = ka > tl;
     const int m = ka - tl;
-    const int tail_from = n - (ranked ? tl : ka);
-    const float *Arow = a.A + (static_cast<int64_t>(l) * a.H + h) * a.max_tokens + a.span[node];
+    const int tail_from = n - (ranked ? tl : ka);   // keep positions ≥ tail_from outright
     int ncand = 0;
+    uint32_t bmin = 0xffffffffu, bmax = 0u;
     for (int s0 = 0; s0 < kc; s0 += 32) {
       const int s = s0 + lane;
       unsigned long long kk = 0;
       if (s < kc) {
-        const int p = a.pos[row(s)];
+        const int p = pb[s];
         kk = static_cast<unsigned>(p);
         if (ranked && p < tail_from) {
-          const float av = Arow[p];
+          const float av = ab[p];
           if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
           const unsigned bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
           kk = kCand | (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
+          bmin = min(bmin, bits);
+          bmax = max(bmax, bits);
         }
         key[s] = kk;
       }
       ncand += __popc(__ballot_sync(0xffffffffu, (kk & kCand) != 0));
     }
     __syncwarp();
-    unsigned long long tkey = kCand, tmask = kCand;
+    // threshold: keep a candidate iff (key & tmask) >= tkey (the top m unique keys)
+    unsigned long long tkey = kCand, tmask = kCand;     // m ≥ ncand: all candidates
     if (ranked && m <= 0) {
-      tkey = ~0ull; tmask = ~0ull;
-    } else if (ranked && m < ncand) {
+      tkey = ~0ull; tmask = ~0ull;                      // none survives
+    } else if (ranked && m < ncand && !(a.exp & 2)) {
+      // candidates share every key bit above `top` (bits of A above the highest bit where
+      // min and max differ); the radix passes start there
+      bmin = __reduce_min_sync(0xffffffffu, bmin);
+      bmax = __reduce_max_sync(0xffffffffu, bmax);
+      const int top = bmin != bmax ? 16 + 31 - __clz(static_cast<int>(bmin ^ bmax)) : 15;
       unsigned long long prefix = kCand, pmask = kCand;
       int need = m;
-      for (int shift = 40; shift >= 0; shift -= 8) {
+      for (int shift = top - 7; shift > -8; shift -= 8) {
+        const unsigned long long dmask = shift >= 0 ? 255ull << shift : 255ull >> -shift;
 #pragma unroll
         for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
         __syncwarp();
         for (int s = lane; s < kc; s += 32) {
           const unsigned long long kk = key[s];
-          if ((kk & pmask) == prefix) atomicAdd(&hist[(kk >> shift) & 255u], 1u);
+          if ((kk & pmask) == prefix) {
+            const unsigned dg = shift >= 0 ? static_cast<unsigned>(kk >> shift) & 255u
+                                           : static_cast<unsigned>(kk << -shift) & 255u;
+            atomicAdd(&hist[dg], 1u);
+          }
         }
         __syncwarp();
         uint32_t cnt8[8];
@@ -506,13 +434,15 @@ select_move_ws_kernel(CompactArgs a) {
         above = __shfl_sync(0xffffffffu, above, src);
         inbin = __shfl_sync(0xffffffffu, inbin, src);
         need -= static_cast<int>(above);
-        prefix |= static_cast<unsigned long long>(dsel) << shift;
-        pmask |= 255ull << shift;
-        if (static_cast<uint32_t>(need) == inbin) break;
+        prefix |= shift >= 0 ? static_cast<unsigned long long>(dsel) << shift
+                             : static_cast<unsigned long long>(dsel) >> -shift;
+        pmask |= dmask;
+        if (static_cast<uint32_t>(need) == inbin) break;   // the whole bin survives
       }
       tkey = prefix;
       tmask = pmask;
     }
+    // keep flags → holes (dropped slots < k_app) and movers (kept slots ≥ k_app), ascending
     int nh = 0, nm = 0;
     for (int s0 = 0; s0 < kc; s0 += 32) {
       const int s = s0 + lane;
@@ -532,7 +462,8 @@ select_move_ws_kernel(CompactArgs a) {
       nm += __popc(mb);
     }
     __syncwarp();
-    if (nh != nm && lane == 0) atomicOr(&a.ctrl->err, DERR_STATE);
+    if (nh != nm && lane == 0 && !a.exp) atomicOr(&a.ctrl->err, DERR_STATE);
+    if (a.exp) nm = nm < nh ? nm : nh;
     // hand the job to the move warp
     const int sl = k & 1;
     mbar_wait(&empty[sl], ((k >> 1) & 1) ^ 1);
@@ -542,46 +473,6 @@ select_move_ws_kernel(CompactArgs a) {
     if (lane == 0) mycount[sl] = nm;
     __syncwarp();
     if (lane == 0) mbar_arrive(&full[sl]);
-  }
-}
-
-// Move: a pure streaming copy of K, V (rb bytes each) and the pos tag for every listed pair;
-// sources and destinations are disjoint, so any order is correct.  cpr lanes per row,
-// kUnrollM rows in flight per lane-group.
-constexpr int kUnrollM = 4;
-__global__ void __launch_bounds__(256, 4)
-move_kernel(const Ctrl *__restrict__ ctrl, const int2 *__restrict__ moves, char *__restrict__ kp8,
-            char *__restrict__ vp8, int16_t *__restrict__ pos, int rb) {
-  const int total = ctrl->move_count;
-  const int cpr = rb >> 4;
-  const int rpw = 32 / cpr;                    // rows per warp instruction
-  const int lane = threadIdx.x & 31;
-  const int piece = lane % cpr, sub = lane / cpr;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int per_iter = rpw * kUnrollM;
-  for (int m0 = wg * per_iter; m0 < total; m0 += warps * per_iter) {
-    uint4 bk[kUnrollM], bv[kUnrollM];
-    int2 mv[kUnrollM];
-#pragma unroll
-    for (int u = 0; u < kUnrollM; ++u) {
-      const int mi = m0 + u * rpw + sub;
-      mv[u] = mi < total ? moves[mi] : make_int2(-1, -1);
-      if (mv[u].x >= 0) {
-        const int64_t off = static_cast<int64_t>(mv[u].x) * rb + piece * 16;
-        bk[u] = *reinterpret_cast<const uint4 *>(kp8 + off);
-        bv[u] = *reinterpret_cast<const uint4 *>(vp8 + off);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnrollM; ++u) {
-      if (mv[u].x >= 0) {
-        const int64_t off = static_cast<int64_t>(mv[u].y) * rb + piece * 16;
-        *reinterpret_cast<uint4 *>(kp8 + off) = bk[u];
-        *reinterpret_cast<uint4 *>(vp8 + off) = bv[u];
-        if (piece == 0) pos[mv[u].y] = pos[mv[u].x];
-      }
-    }
   }
 }
 
@@ -598,9 +489,9 @@ void launch_evict_plan(arbor_ctx *c, int N, const int32_t *k_target) {
   a.npages = c->d.npages;
   a.ptab = c->d.ptab;
   a.free_stack = c->d.free_stack;
-  a.work_node = c->d.work_node;
-  a.work_old = c->d.work_old;
-  a.work_new = c->d.work_new;
+  a.n = c->d.n;
+  a.span = c->d.span;
+  a.work = c->d.work;
   a.ctrl = c->d.ctrl;
   stage_begin(c, ARBOR_ST_EVICT_PLAN, c->ms);
   evict_plan_kernel<<<1, kPlanThreads, 0, c->ms>>>(a);
@@ -618,11 +509,7 @@ void launch_select_compact(arbor_ctx *c, int max_n) {
   a.MPN = c->max_pages_node;
   a.l_tail = c->prm.l_tail;
   a.max_tokens = c->max_tokens;
-  a.work_node = c->d.work_node;
-  a.work_old = c->d.work_old;
-  a.work_new = c->d.work_new;
-  a.n = c->d.n;
-  a.span = c->d.span;
+  a.work = c->d.work;
   a.A = c->cfg.score;
   a.ctrl_ro = c->d.ctrl;
   a.ctrl = c->d.ctrl;
@@ -630,61 +517,36 @@ void launch_select_compact(arbor_ctx *c, int max_n) {
   a.kpool = c->cfg.k_pool;
   a.vpool = c->cfg.v_pool;
   a.pos = c->cfg.pos_pool;
-  a.moves = c->d.moves;
   a.esize = c->esize;
-  const int cap = max_n < 1 ? 1 : max_n;
-  a.cap = cap;
+  a.cap = max_n < 1 ? 1 : max_n;
   a.lgP = __builtin_ctz(static_cast<unsigned>(c->P));
-  const size_t smem = (static_cast<size_t>(cap) * (8 + 8) + ((cap >> a.lgP) + 1) * 4) * kWarps;
+  static const int exp_flags = [] {
+    const char *e = getenv("ARBOR_EVICT_EXP");
+    return e ? atoi(e) : 0;
+  }();
+  a.exp = exp_flags;
+  const WsLayout ly(a.cap, a.lgP);
+  // occupancy / smem attribute cached per capacity (host-side cost stays off the launch path)
   static size_t attr_smem = 0;
-  if (smem > attr_smem) {
-    cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem < 48 * 1024 ? 48 * 1024 : smem));
-    cudaFuncSetAttribute(select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem < 48 * 1024 ? 48 * 1024 : smem));
-    attr_smem = smem < 48 * 1024 ? 48 * 1024 : smem;
+  static int cached_cap = -1, cached_lg = -1, cached_grid = 0;
+  if (ly.total > attr_smem) {
+    const size_t want = ly.total < 48 * 1024 ? 48 * 1024 : ly.total;
+    cudaFuncSetAttribute(select_move_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(want));
+    attr_smem = want;
   }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  int per_sm = 0;
-  if (kWarpSpecialised) {
-    const int jcap = cap / 2 + 1;
-    const int pcap = (cap >> a.lgP) + 1;
-    const size_t wsm = static_cast<size_t>(kPairs) * cap * (8 + 8) +
-                       static_cast<size_t>(((kPairs * pcap + 1) & ~1)) * 4 +
-                       static_cast<size_t>(kPairs) * 2 * jcap * 8 + ((kPairs * 2 + 1) & ~1) * 4 +
-                       kPairs * 4 * 8;
-    static size_t wattr = 0;
-    if (wsm > wattr) {
-      cudaFuncSetAttribute(select_move_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(wsm < 48 * 1024 ? 48 * 1024 : wsm));
-      wattr = wsm < 48 * 1024 ? 48 * 1024 : wsm;
-    }
-    int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, select_move_ws_kernel, kPairs * 64, wsm);
-    stage_begin(c, ARBOR_ST_SELECT_COMPACT, c->ms);
-    select_move_ws_kernel<<<sms * (per > 0 ? per : 1), kPairs * 64, wsm, c->ms>>>(a);
-    ARBOR_LAUNCHED(c);
-    stage_end(c, ARBOR_ST_SELECT_COMPACT, c->ms);
-    return;
+  if (a.cap != cached_cap || a.lgP != cached_lg) {
+    int sms = 148, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, select_move_ws_kernel, kPairsWs * 64, ly.total);
+    cached_grid = sms * (per > 0 ? per : 1);
+    cached_cap = a.cap;
+    cached_lg = a.lgP;
   }
-  const bool fused = kFusedCompact;
-  if (fused) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<true>, kWarps * 32, smem);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<false>, kWarps * 32, smem);
   stage_begin(c, ARBOR_ST_SELECT_COMPACT, c->ms);
-  if (fused) select_kernel<true><<<sms * (per_sm > 0 ? per_sm : 1), kWarps * 32, smem, c->ms>>>(a);
-  else select_kernel<false><<<sms * (per_sm > 0 ? per_sm : 1), kWarps * 32, smem, c->ms>>>(a);
+  select_move_ws_kernel<<<cached_grid, kPairsWs * 64, ly.total, c->ms>>>(a);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SELECT_COMPACT, c->ms);
-  if (fused) return;
-  int per_sm_m = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_m, move_kernel, 256, 0);
-  stage_begin(c, ARBOR_ST_COMPACT_MOVE, c->ms);
-  move_kernel<<<sms * (per_sm_m > 0 ? per_sm_m : 1), 256, 0, c->ms>>>(
-      c->d.ctrl, c->d.moves, static_cast<char *>(c->cfg.k_pool), static_cast<char *>(c->cfg.v_pool),
-      c->cfg.pos_pool, c->D * c->esize);
-  ARBOR_LAUNCHED(c);
-  stage_end(c, ARBOR_ST_COMPACT_MOVE, c->ms);
 }
 
 }  // namespace arbor
