@@ -570,7 +570,11 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   }
   ALLOC(d.onpath, MN); ALLOC(d.pinned, MN); ALLOC(d.depth, MN); ALLOC(d.delta, MN);
   ALLOC(d.Ed, 2 * MN + 2); ALLOC(d.ED, 2 * MN + 2);
-  ALLOC(d.work, MN);
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    ALLOC(d.work, static_cast<size_t>(sms) * kEvictCtasPerSm * MN);
+  }
   {
     // compaction rows are addressed with int32 row ids
     const int64_t rows_total = static_cast<int64_t>(c->L) * c->NP * c->H * c->P;
@@ -846,12 +850,8 @@ arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_
     CK_LAUNCH();
     c->geom_version = c->tree_version;
   }
-  launch_evict_plan(c, tree->num_nodes, k_target);
+  launch_evict(c, tree->num_nodes, k_target, max_n);
   CK_LAUNCH();
-  if (max_n > 0) {
-    launch_select_compact(c, max_n);
-    CK_LAUNCH();
-  }
   if (evicted_tokens_out) {
     CK(cudaStreamSynchronize(c->ms));
     long long ev = 0;

@@ -36,8 +36,8 @@ struct Ctrl {
   int32_t err;             // DERR_* bits
   int32_t work_count;      // evict work items of the last plan
   int32_t rehyd_count;     // nodes rehydrated by the last plan
-  int32_t move_count;      // (src, dst) row moves listed by the last select
-  int32_t pad0;
+  int32_t move_count;      // unused
+  int32_t plan_ticket;     // last-CTA ticket of the fused evict kernel (zero at rest)
   long long evicted;       // tokens evicted by the last evict
   long long rehydrations;  // total rehydrations
   long long pages_in_use;  // pages held by nodes
@@ -48,8 +48,9 @@ struct Ctrl {
 struct __align__(16) WorkEnt {
   int32_t node, kc, ka, n;   // node id, k_cur before, k_app after, n_i
   int64_t span;              // a_i (absolute position of the node's first token)
-  int64_t pad;
+  int32_t foff, nfree;       // offset of its freed pages among all freed pages; their count
 };
+constexpr int kEvictCtasPerSm = 2;   // the fused evict kernel's work-list copies: [SMs·2][max_nodes]
 
 // Per-launch geometry of the K/V pools
 struct PoolGeom {
@@ -207,8 +208,7 @@ void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, cons
 void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget, int32_t *k_out);
 
 // evict.cu
-void launch_evict_plan(arbor_ctx *c, int N, const int32_t *k_target);
-void launch_select_compact(arbor_ctx *c, int max_n);
+void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n);
 
 // pages.cu
 void launch_append(arbor_ctx *c, int node, const void *k, const void *v, int n_old, int ntok);

@@ -27,115 +27,19 @@
 namespace arbor {
 namespace {
 
-constexpr int kPlanThreads = 1024;
 constexpr int kPairsWs = 8;   // (select warp, move warp) pairs per CTA of select_move_ws_kernel
 constexpr int kUw = 4;        // rows in flight per lane group of a move warp
-
-struct PlanArgs {
-  int N, P, MPN;
-  const int32_t *k_target;
-  const uint8_t *pinned;
-  int32_t *kcur, *npages, *ptab, *free_stack;
-  const int32_t *n;
-  const int64_t *span;
-  WorkEnt *work;
-  Ctrl *ctrl;
-};
-
-__global__ void __launch_bounds__(kPlanThreads)
-evict_plan_kernel(PlanArgs a) {
-  // each thread owns a contiguous block of nodes so that prefix sums keep ascending order
-  constexpr int kPer = 4;   // N ≤ 4096
-  using Scan = cub::BlockScan<int, kPlanThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int tot_work, tot_free;
-  __shared__ long long tot_ev;
-  if (threadIdx.x == 0) { tot_ev = 0; }
-  __syncthreads();
-  int kapp[kPer], kc[kPer], ev[kPer], fr[kPer], newp[kPer];
-  int my_work = 0, my_free = 0;
-  long long my_ev = 0;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int j = threadIdx.x * kPer + i;
-    ev[i] = 0; fr[i] = 0; kc[i] = 0; kapp[i] = 0; newp[i] = 0;
-    if (j < a.N) {
-      kc[i] = a.kcur[j];
-      int kt = a.k_target[j];
-      kt = kt < 0 ? 0 : kt;
-      kapp[i] = kt < kc[i] ? kt : kc[i];
-      if (!a.pinned[j] && kapp[i] < kc[i]) {
-        ev[i] = 1;
-        newp[i] = (kapp[i] + a.P - 1) / a.P;
-        fr[i] = a.npages[j] - newp[i];
-      }
-    }
-    my_work += ev[i];
-    my_free += fr[i];
-    my_ev += ev[i] ? (kc[i] - kapp[i]) : 0;
-  }
-  int work_off, free_off;
-  Scan(tmp).ExclusiveSum(my_work, work_off);
-  __syncthreads();
-  Scan(tmp).ExclusiveSum(my_free, free_off);
-  __syncthreads();
-  atomicAdd(reinterpret_cast<unsigned long long *>(&tot_ev), static_cast<unsigned long long>(my_ev));
-  if (threadIdx.x == kPlanThreads - 1) {
-    tot_work = work_off + my_work;
-    tot_free = free_off + my_free;
-  }
-  const int top = a.ctrl->free_top;
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int j = threadIdx.x * kPer + i;
-    if (!ev[i]) continue;
-    WorkEnt e;
-    e.node = j;
-    e.kc = kc[i];
-    e.ka = kapp[i];
-    e.n = a.n[j];
-    e.span = a.span[j];
-    e.pad = 0;
-    a.work[work_off] = e;
-    ++work_off;
-    a.npages[j] = newp[i];
-    a.kcur[j] = kapp[i];
-  }
-  // freed pages → LIFO free stack, (node, list) ascending: all of a node's page ids are loaded
-  // before any store (the stores could alias the page table for the compiler, which would
-  // otherwise serialise one global load round trip per page)
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const int j = threadIdx.x * kPer + i;
-    if (!ev[i] || fr[i] == 0) continue;
-    const int32_t *__restrict__ pl = a.ptab + static_cast<int64_t>(j) * a.MPN + newp[i];
-    int32_t *__restrict__ dst = a.free_stack + top + free_off;
-    constexpr int kB = 16;
-    for (int t0 = 0; t0 < fr[i]; t0 += kB) {
-      int32_t v[kB];
-#pragma unroll
-      for (int t = 0; t < kB; ++t) v[t] = t0 + t < fr[i] ? __ldg(pl + t0 + t) : 0;
-#pragma unroll
-      for (int t = 0; t < kB; ++t) if (t0 + t < fr[i]) dst[t0 + t] = v[t];
-    }
-    free_off += fr[i];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    a.ctrl->free_top = top + tot_free;
-    a.ctrl->work_count = tot_work;
-    a.ctrl->move_count = 0;
-    a.ctrl->evicted = tot_ev;
-    a.ctrl->pages_in_use -= tot_free;
-  }
-}
 
 struct CompactArgs {
   int R;            // rows = L * H
   int H, P, D, NP, MPN, l_tail;
   int64_t max_tokens;
-  const WorkEnt *work;
+  WorkEnt *work;    // [grid][max_nodes]: each CTA's private copy of the work list
+  int N, MN;        // tree nodes, max_nodes (work-list stride)
+  const int32_t *k_target, *n;
+  const uint8_t *pinned;
+  const int64_t *span;
+  int32_t *kcur, *npages, *free_stack;
   const float *A;
   const Ctrl *ctrl_ro;
   Ctrl *ctrl;
@@ -147,6 +51,8 @@ struct CompactArgs {
   int lgP;          // log2(page size)
   int exp;          // ARBOR_EVICT_EXP (measurement only): bit0 skip moves, bit1 skip radix select
 };
+
+constexpr int kPlanPer = 6;   // nodes per thread in the plan scan (N ≤ 3072 = 6 × 512)
 
 __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem)
@@ -213,18 +119,105 @@ select_move_ws_kernel(CompactArgs a) {
   int2 *myjobs = reinterpret_cast<int2 *>(sm + Ly.jobs) + pid * 2 * jcap;
   int32_t *mycount = reinterpret_cast<int32_t *>(sm + Ly.jcount) + pid * 2;
   __shared__ uint32_t hist_all[kPairsWs][256];
+  using Scan = cub::BlockScan<int, kPairsWs * 64>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int s_work, s_free, s_apply;
+  __shared__ unsigned long long s_ev;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kPairsWs * 2; ++i) {
       mbar_init(&bars[(i >> 1) * 4 + (i & 1)], 1);
       mbar_init(&bars[(i >> 1) * 4 + 2 + (i & 1)], 1);
     }
     mbar_fence_init();
+    s_ev = 0;
   }
   __syncthreads();
-  const int items = a.ctrl_ro->work_count * a.R;
+  // ---- plan (Alg. 2, Q17): k_app = min(k_cur, k_target) for every non-pinned node;
+  // the changed ones, ascending id, are the work list.  Every CTA derives it from the same
+  // unmodified state into its own copy; the last CTA to get there (ticket) applies it —
+  // k_cur, page-list truncation to ⌈k_app/P⌉, freed pages pushed on the LIFO free stack in
+  // ascending (node, list) order — after every CTA has read that state.
+  WorkEnt *wl = a.work + static_cast<int64_t>(blockIdx.x) * a.MN;
+  {
+    int kc[kPlanPer], ka[kPlanPer], ev[kPlanPer], fr[kPlanPer], wo[kPlanPer], fo[kPlanPer];
+    unsigned long long my_ev = 0;
+    
+#pragma unroll
+    for (int i = 0; i < kPlanPer; ++i) {
+      const int j = threadIdx.x * kPlanPer + i;
+      kc[i] = 0; ka[i] = 0; ev[i] = 0; fr[i] = 0;
+      if (j < a.N) {
+        kc[i] = a.kcur[j];
+        const int kt = max(a.k_target[j], 0);
+        ka[i] = min(kt, kc[i]);
+        if (!a.pinned[j] && ka[i] < kc[i]) {
+          ev[i] = 1;
+          fr[i] = a.npages[j] - ((ka[i] + a.P - 1) >> lgP);
+          my_ev += static_cast<unsigned long long>(kc[i] - ka[i]);
+        }
+      }
+    }
+    int tot_work, tot_free;
+    Scan(scan_tmp).ExclusiveSum(ev, wo, tot_work);
+    __syncthreads();
+    Scan(scan_tmp).ExclusiveSum(fr, fo, tot_free);
+    if (my_ev) atomicAdd(&s_ev, my_ev);
+#pragma unroll
+    for (int i = 0; i < kPlanPer; ++i) {
+      if (!ev[i]) continue;
+      const int j = threadIdx.x * kPlanPer + i;
+      WorkEnt e;
+      e.node = j;
+      e.kc = kc[i];
+      e.ka = ka[i];
+      e.n = a.n[j];
+      e.span = a.span[j];
+      e.foff = fo[i];
+      e.nfree = fr[i];
+      wl[wo[i]] = e;
+    }
+    if (threadIdx.x == 0) { s_work = tot_work; s_free = tot_free; }
+  }
+  __syncthreads();
+  const int items = s_work * a.R;
   const int stride = gridDim.x * kPairsWs;
   const int first = blockIdx.x * kPairsWs + pid;
   if (mover) {
+    // the move warps take the ticket (they would otherwise wait for their first job)
+    const int mt = threadIdx.x - kPairsWs * 32;
+    if (mt == 0) {
+      __threadfence();
+      const unsigned t = atomicAdd(reinterpret_cast<unsigned *>(&a.ctrl->plan_ticket), 1u);
+      s_apply = t == gridDim.x - 1;
+    }
+    named_bar_sync(1, kPairsWs * 32);
+    if (s_apply) {
+      __threadfence();
+      const int top = a.ctrl->free_top;
+      for (int w = mt; w < s_work; w += kPairsWs * 32) {
+        const WorkEnt e = wl[w];
+        const int newp = (e.ka + a.P - 1) >> lgP;
+        const int32_t *__restrict__ pl = a.ptab + static_cast<int64_t>(e.node) * a.MPN + newp;
+        int32_t *__restrict__ dst = a.free_stack + top + e.foff;
+        constexpr int kB = 8;
+        for (int t0 = 0; t0 < e.nfree; t0 += kB) {
+          int32_t v[kB];
+#pragma unroll
+          for (int t = 0; t < kB; ++t) v[t] = t0 + t < e.nfree ? __ldg(pl + t0 + t) : 0;
+#pragma unroll
+          for (int t = 0; t < kB; ++t) if (t0 + t < e.nfree) dst[t0 + t] = v[t];
+        }
+        a.npages[e.node] = newp;
+        a.kcur[e.node] = e.ka;
+      }
+      if (mt == 0) {
+        a.ctrl->free_top = top + s_free;
+        a.ctrl->work_count = s_work;
+        a.ctrl->evicted = static_cast<long long>(s_ev);
+        a.ctrl->pages_in_use -= s_free;
+        a.ctrl->plan_ticket = 0;
+      }
+    }
     // ------------------------------------------------------------ move warp
     const int rb = a.D * a.esize, cpr = rb >> 4, rpi = 32 / cpr;
     const int piece = lane % cpr, sub = lane / cpr;
@@ -289,7 +282,7 @@ select_move_ws_kernel(CompactArgs a) {
     if (k >= my_items || lane >= 2) return;
     const int w = (first + k * stride) / a.R;
     cp_async16ca(reinterpret_cast<char *>(&Mbuf[k & 3]) + lane * 16,
-                 reinterpret_cast<const char *>(&a.work[w]) + lane * 16);
+                 reinterpret_cast<const char *>(&wl[w]) + lane * 16);
   };
   auto issue_pages = [&](int k) {
     if (k >= my_items) return;
@@ -478,28 +471,7 @@ select_move_ws_kernel(CompactArgs a) {
 
 }  // namespace
 
-void launch_evict_plan(arbor_ctx *c, int N, const int32_t *k_target) {
-  PlanArgs a{};
-  a.N = N;
-  a.P = c->P;
-  a.MPN = c->max_pages_node;
-  a.k_target = k_target;
-  a.pinned = c->d.pinned;
-  a.kcur = c->d.kcur;
-  a.npages = c->d.npages;
-  a.ptab = c->d.ptab;
-  a.free_stack = c->d.free_stack;
-  a.n = c->d.n;
-  a.span = c->d.span;
-  a.work = c->d.work;
-  a.ctrl = c->d.ctrl;
-  stage_begin(c, ARBOR_ST_EVICT_PLAN, c->ms);
-  evict_plan_kernel<<<1, kPlanThreads, 0, c->ms>>>(a);
-  ARBOR_LAUNCHED(c);
-  stage_end(c, ARBOR_ST_EVICT_PLAN, c->ms);
-}
-
-void launch_select_compact(arbor_ctx *c, int max_n) {
+void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
   CompactArgs a{};
   a.R = c->L * c->H;
   a.H = c->H;
@@ -510,6 +482,15 @@ void launch_select_compact(arbor_ctx *c, int max_n) {
   a.l_tail = c->prm.l_tail;
   a.max_tokens = c->max_tokens;
   a.work = c->d.work;
+  a.N = N;
+  a.MN = c->max_nodes;
+  a.k_target = k_target;
+  a.n = c->d.n;
+  a.pinned = c->d.pinned;
+  a.span = c->d.span;
+  a.kcur = c->d.kcur;
+  a.npages = c->d.npages;
+  a.free_stack = c->d.free_stack;
   a.A = c->cfg.score;
   a.ctrl_ro = c->d.ctrl;
   a.ctrl = c->d.ctrl;
@@ -539,7 +520,7 @@ void launch_select_compact(arbor_ctx *c, int max_n) {
     int sms = 148, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, select_move_ws_kernel, kPairsWs * 64, ly.total);
-    cached_grid = sms * (per > 0 ? per : 1);
+    cached_grid = sms * std::min(std::max(per, 1), kEvictCtasPerSm);
     cached_cap = a.cap;
     cached_lg = a.lgP;
   }
