@@ -182,6 +182,34 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float *v) {
   }
 }
 
+// As tmem_ld<N>, but only the 16-column groups (8 for a tail) that start below `ncol`: a tile
+// of fewer leaves than the kernel's NQ slots loads (and later reduces) only its own columns.
+// `ncol` must be warp-uniform (tcgen05.ld is .sync.aligned); skipped entries are left as is.
+template <int N>
+__device__ __forceinline__ void tmem_ld_upto(uint32_t taddr, float *v, int ncol) {
+#pragma unroll
+  for (int c = 0; c + 16 <= N; c += 16) {
+    if (c < ncol) {
+      float t[16];
+      tmem_ld16(taddr + c, t);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[c + i] = t[i];
+    }
+  }
+  if constexpr (N % 16 == 8) {
+    if (N - 8 < ncol) {
+      uint32_t r[8];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+          : "r"(taddr + (N - 8)));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[N - 8 + i] = __uint_as_float(r[i]);
+    }
+  }
+}
+
 // Transpose-reduce of 8 columns held by every lane: afterwards each lane holds the reduction
 // over all 32 lanes of column col8(lane) (9 shuffles instead of 40).
 __device__ __forceinline__ int col8(int lane) {
@@ -541,8 +569,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       mbar_wait(&s_full[b], (k >> 1) & 1u);
       if (tid == 64) TC_TRACE(k, 8);
       tc_fence_after();
+      // the tile's own columns: 8 q rows per leaf (tiles of fewer leaves skip the rest)
+      const int ncol = min(NQ, 8 * hd.cnt);
       float z[NQ];
-      tmem_ld<NQ>(tmem + lane_addr + b * 3 * NQ, z);
+      tmem_ld_upto<NQ>(tmem + lane_addr + b * 3 * NQ, z, ncol);
 #pragma unroll
       for (int n = 0; n < NQ; ++n)
         z[n] = (valid && ((cm >> n) & 1ull)) ? z[n] * a.scale_log2 : -INFINITY;
@@ -552,33 +582,52 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       // the warp, then the half's two warps combine through smem (double-buffered by parity)
 #pragma unroll
       for (int c = 0; c < NQ; c += kW<NQ>) {
-        const float m = warp_reduceW<kW<NQ>, true>(z + c, lane);
-        if (!(lane & 1)) red_m[k & 3][quad][c + myc] = m;
+        if (c < ncol) {
+          const float m = warp_reduceW<kW<NQ>, true>(z + c, lane);
+          if (!(lane & 1)) red_m[k & 3][quad][c + myc] = m;
+        }
       }
       named_bar_sync(1 + half, 64);
       float p[NQ];
 #pragma unroll
-      for (int n = 0; n < NQ; ++n) {
-        const float m = fmaxf(red_m[k & 3][half * 2][n], red_m[k & 3][half * 2 + 1][n]);
-        p[n] = fast_exp2(z[n] - m);          // z = −inf (masked) → 0; m = −inf only if all masked
-        if (z[n] == -INFINITY) p[n] = 0.f;
+      for (int c = 0; c < NQ; c += 8) {
+        if (c < ncol) {
+#pragma unroll
+          for (int n = c; n < c + 8; ++n) {
+            const float m = fmaxf(red_m[k & 3][half * 2][n], red_m[k & 3][half * 2 + 1][n]);
+            p[n] = fast_exp2(z[n] - m);      // z = −inf (masked) → 0; m = −inf only if all masked
+            if (z[n] == -INFINITY) p[n] = 0.f;
+          }
+        } else {
+#pragma unroll
+          for (int n = c; n < c + 8; ++n) p[n] = 0.f;
+        }
       }
 #pragma unroll
       for (int c = 0; c < NQ; c += kW<NQ>) {
-        const float l = warp_reduceW<kW<NQ>, false>(p + c, lane);
-        if (!(lane & 1)) red_l[k & 3][quad][c + myc] = l;
+        if (c < ncol) {
+          const float l = warp_reduceW<kW<NQ>, false>(p + c, lane);
+          if (!(lane & 1)) red_l[k & 3][quad][c + myc] = l;
+        }
       }
       // P buffer b was last read by MMA2(k−2)
       if (k >= 2) mbar_wait(&o_full[b], ((k - 2) >> 1) & 1u);
       // P (bf16) into rows [half·NQ, half·NQ + NQ) of slot-half `half` of the Pᵀ tile
       {
+        // rows of columns ≥ ncol keep stale values: they only feed output columns that are
+        // never stored (Oᵀ column n depends on Pᵀ row n alone)
         unsigned char *Pt = Pbuf + b * S::kP + half * (2 * NQ * 128);
         const uint32_t cb = static_cast<uint32_t>(tc * 2);
 #pragma unroll
-        for (int n = 0; n < NQ; ++n) {
-          const int r = half * NQ + n;
-          *reinterpret_cast<__nv_bfloat16 *>(Pt + r * 128 + ((((cb >> 4) ^ (r & 7))) << 4) + (cb & 15)) =
-              __float2bfloat16_rn(p[n]);
+        for (int c = 0; c < NQ; c += 8) {
+          if (c < ncol) {
+#pragma unroll
+            for (int n = c; n < c + 8; ++n) {
+              const int r = half * NQ + n;
+              *reinterpret_cast<__nv_bfloat16 *>(Pt + r * 128 + ((((cb >> 4) ^ (r & 7))) << 4) + (cb & 15)) =
+                  __float2bfloat16_rn(p[n]);
+            }
+          }
         }
       }
       // V rows of a partly filled last page hold pool bytes past k_cur: zero them so that
@@ -602,8 +651,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       if (valid) {   // logits for the fused score pass: zbuf[pair][li][h][g][slot]
         float *zr = a.zbuf + rowbase * kAttnChunk + tc;
 #pragma unroll
-        for (int n = 0; n < NQ; ++n)
-          if ((cm >> n) & 1ull) zr[static_cast<int64_t>(offn[n]) * kAttnChunk] = z[n];
+        for (int c = 0; c < NQ; c += 8) {
+          if (c < ncol) {
+#pragma unroll
+            for (int n = c; n < c + 8; ++n)
+              if ((cm >> n) & 1ull) zr[static_cast<int64_t>(offn[n]) * kAttnChunk] = z[n];
+          }
+        }
       }
     }
   } else {
@@ -631,17 +685,24 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         mm = fmaxf(red_m[k & 3][hh * 2][cn], red_m[k & 3][hh * 2 + 1][cn]);
         ll = red_l[k & 3][hh * 2][cn] + red_l[k & 3][hh * 2 + 1][cn];
       }
+      const int ncol = min(NQ, 8 * hd.cnt);
       float o[2 * NQ];
-      tmem_ld<2 * NQ>(tmem + lane_addr + b * 3 * NQ + NQ, o);
+      tmem_ld_upto<NQ>(tmem + lane_addr + b * 3 * NQ + NQ, o, ncol);
+      if (hd.hasB) tmem_ld_upto<NQ>(tmem + lane_addr + b * 3 * NQ + 2 * NQ, o + NQ, ncol);
       tc_fence_before();
       mbar_arrive(&o_empty[b]);
       const unsigned long long cm = colmask(hd.cnt, G);
       float *pa = a.partials + ((static_cast<int64_t>(hd.pbA) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
       float *pbp = a.partials + ((static_cast<int64_t>(hd.pbB) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
 #pragma unroll
-      for (int n = 0; n < NQ; ++n) {
-        if ((cm >> n) & 1ull) pa[static_cast<int64_t>(offn[n]) * 130] = o[n];
-        if (((cm >> n) & 1ull) && hd.hasB) pbp[static_cast<int64_t>(offn[n]) * 130] = o[NQ + n];
+      for (int c = 0; c < NQ; c += 8) {
+        if (c < ncol) {
+#pragma unroll
+          for (int n = c; n < c + 8; ++n) {
+            if ((cm >> n) & 1ull) pa[static_cast<int64_t>(offn[n]) * 130] = o[n];
+            if (((cm >> n) & 1ull) && hd.hasB) pbp[static_cast<int64_t>(offn[n]) * 130] = o[NQ + n];
+          }
+        }
       }
       if (etid < 2 * NQ && ((cm >> cn) & 1ull) && (hh == 0 || hd.hasB)) {
         float *dst = (hh ? pbp : pa) - trow + static_cast<int64_t>((cn >> 3) * SP + (cn & 7)) * 130;
