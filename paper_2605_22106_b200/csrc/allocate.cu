@@ -91,6 +91,8 @@ __device__ __forceinline__ void divmod128(unsigned __int128 X, unsigned long lon
 
 __global__ void __launch_bounds__(kThreads)
 allocate_kernel(AllocArgs a) {
+  pdl_wait();
+  pdl_trigger();
   TRACE(0);
   extern __shared__ __align__(16) unsigned char sm[];
   const int N = a.N;
@@ -512,7 +514,7 @@ void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget
     attr = true;
   }
   stage_begin(c, ARBOR_ST_ALLOCATE, c->ms);
-  allocate_kernel<<<1, kThreads, smem, c->ms>>>(a);
+  launch_pdl(allocate_kernel, dim3(1), dim3(kThreads), smem, c->ms, a);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_ALLOCATE, c->ms);
 }

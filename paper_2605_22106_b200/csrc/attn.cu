@@ -319,6 +319,8 @@ struct MergeArgs {
 template <typename T, int D>
 __global__ void __launch_bounds__(128)
 attn_merge_kernel(MergeArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int total = a.pv.nA * a.Lc * a.Hq;
@@ -446,11 +448,11 @@ void launch_attn_merge(arbor_ctx *c, const PlanView &pv, int layer_count, void *
   const int blocks = (warps + 3) / 4;
   stage_begin(c, ARBOR_ST_ATTN_MERGE, c->ms);
   if (c->esize == 2) {
-    if (c->D == 128) attn_merge_kernel<__nv_bfloat16, 128><<<blocks, 128, 0, c->ms>>>(m);
-    else attn_merge_kernel<__nv_bfloat16, 64><<<blocks, 128, 0, c->ms>>>(m);
+    if (c->D == 128) launch_pdl(attn_merge_kernel<__nv_bfloat16, 128>, dim3(blocks), dim3(128), 0, c->ms, m);
+    else launch_pdl(attn_merge_kernel<__nv_bfloat16, 64>, dim3(blocks), dim3(128), 0, c->ms, m);
   } else {
-    if (c->D == 128) attn_merge_kernel<float, 128><<<blocks, 128, 0, c->ms>>>(m);
-    else attn_merge_kernel<float, 64><<<blocks, 128, 0, c->ms>>>(m);
+    if (c->D == 128) launch_pdl(attn_merge_kernel<float, 128>, dim3(blocks), dim3(128), 0, c->ms, m);
+    else launch_pdl(attn_merge_kernel<float, 64>, dim3(blocks), dim3(128), 0, c->ms, m);
   }
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_ATTN_MERGE, c->ms);

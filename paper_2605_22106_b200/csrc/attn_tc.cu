@@ -40,7 +40,8 @@
 namespace arbor {
 namespace {
 
-constexpr int kTcThreads = 320;   // producer, MMA, 4 softmax warps, 4 epilogue warps
+constexpr int kTcThreads = 448;   // producer, MMA, 4 softmax warps (even tiles), 4 epilogue warps,
+                                  // 4 softmax warps (odd tiles)
 constexpr int kTileRows = 128;
 constexpr int kHalf = 64;                       // = kAttnChunk
 constexpr uint32_t kKVBytes = kTileRows * 256;  // one K (or V) tile: 128 rows × 128 bf16
@@ -182,31 +183,21 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float *v) {
   }
 }
 
-// As tmem_ld<N>, but only the 16-column groups (8 for a tail) that start below `ncol`: a tile
-// of fewer leaves than the kernel's NQ slots loads (and later reduces) only its own columns.
-// `ncol` must be warp-uniform (tcgen05.ld is .sync.aligned); skipped entries are left as is.
-template <int N>
-__device__ __forceinline__ void tmem_ld_upto(uint32_t taddr, float *v, int ncol) {
+// W (16 or 8) consecutive fp32 TMEM columns of this thread's lane
+template <int W>
+__device__ __forceinline__ void tmem_ldW(uint32_t taddr, float (&v)[W]) {
+  if constexpr (W == 16) {
+    tmem_ld16(taddr, v);
+  } else {
+    static_assert(W == 8, "group width");
+    uint32_t r[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-  for (int c = 0; c + 16 <= N; c += 16) {
-    if (c < ncol) {
-      float t[16];
-      tmem_ld16(taddr + c, t);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[c + i] = t[i];
-    }
-  }
-  if constexpr (N % 16 == 8) {
-    if (N - 8 < ncol) {
-      uint32_t r[8];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-          : "r"(taddr + (N - 8)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[N - 8 + i] = __uint_as_float(r[i]);
-    }
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
   }
 }
 
@@ -297,10 +288,9 @@ __device__ __forceinline__ float warp_reduceW(const float *v, int lane) {
 }
 // valid columns of an item with cnt leaves: 8-row slot per leaf, G q heads used per slot
 __device__ __forceinline__ unsigned long long colmask(int cnt, int G) {
+  // the G-bit slot mask repeated in each of the cnt bytes (cnt ≤ 6, G ≤ 8: no carries)
   const unsigned long long slot = (1ull << G) - 1ull;
-  unsigned long long m = 0;
-  for (int bi = 0; bi < cnt; ++bi) m |= slot << (8 * bi);
-  return m;
+  return slot * (0x0101010101010101ull & ((1ull << (8 * cnt)) - 1ull));
 }
 
 template <int NQ>
@@ -381,8 +371,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       }
     }
   };
-  if (warp == 0) load_batch(0);    // in flight while the other warps set the CTA up
-  else {
+  if (warp != 0) {
     // zero V, Q and P once: MMA2 reads every V row (0·v must stay 0, so rows never loaded
     // must be finite) and the off-half rows of the Pᵀ tile are never written again
     for (int s = 0; s < NST; ++s) {
@@ -417,12 +406,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  pdl_wait();   // everything above overlapped the previous kernel's tail
+  pdl_trigger();
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA producer
     const int ppH = kHalf >> lgP;
     for (int k = 0; k < ntiles; ++k) {
-      if (k > 0 && (k & 31) == 0) load_batch(k);
+      if ((k & 31) == 0) load_batch(k);
       const int src = k & 31;
       const int ntA = __shfl_sync(0xffffffffu, b_ntA, src);
       const int ntB = __shfl_sync(0xffffffffu, b_ntB, src);
@@ -540,22 +531,27 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         }
       }
     }
-  } else if (warp < 6) {
-    // ------------------------------------------------------------- softmax (warps 2..5)
-    // One thread per TMEM lane = tile row = slot.  Straight-line predicated code, unrolled
-    // over NQ columns (the loop body must stay small for the instruction cache).
+  } else if (warp < 6 || warp >= 10) {
+    // ------------------------------------------------------- softmax (warps 2..5 and 10..13)
+    // One thread per TMEM lane = tile row = slot.  Columns (queries) are independent, so a
+    // tile is processed in groups of GW columns by a rolled loop — only the tile's own
+    // columns (8 q rows per leaf), and a loop body that stays small for the instruction
+    // cache whatever NQ is (a fully unrolled NQ = 48 body thrashed it).
+    // Two warpgroups alternate over the tiles (group g takes k ≡ g mod 2, i.e. TMEM and P
+    // buffer g): one tile's latency-bound softmax chain overlaps the next one's.
+    constexpr int GW = kW<NQ>;
+    const int grp = warp >= 10 ? 1 : 0;
     const int quad = warp & 3;                 // TMEM lane quadrant of this warp
     const int half = quad >> 1;                // slot half (chunk A or B) of this thread
+    const int bar_id = 1 + 2 * grp + half;     // named barrier of this group's half
     const int trow = quad * 32 + lane;         // tile row (slot)
     const int tc = trow & (kHalf - 1);         // slot within the chunk
     const int G = a.G;
     const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
     const int SP = a.Lc * a.g.H * G;
-    int offn[NQ];
-#pragma unroll
-    for (int n = 0; n < NQ; ++n) offn[n] = (n >> 3) * SP + (n & 7);
     const int myc = colW<NQ>(lane);
-    for (int k = 0; k < ntiles; ++k) {
+    const uint32_t cb = static_cast<uint32_t>(tc * 2);
+    for (int k = grp; k < ntiles; k += 2) {
       const int s = k % NST, b = k & 1;
       mbar_wait(&full[s], (k / NST) & 1u);
       if (tid == 64) TC_TRACE(k, 7);
@@ -566,70 +562,53 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       const bool present = half == 0 || hd.hasB;
       const int pb = half ? hd.pbB : hd.pbA;
       const bool valid = present && tc < nt;
+      const int ngrp = (min(NQ, 8 * hd.cnt) + GW - 1) / GW;
       mbar_wait(&s_full[b], (k >> 1) & 1u);
       if (tid == 64) TC_TRACE(k, 8);
       tc_fence_after();
-      // the tile's own columns: 8 q rows per leaf (tiles of fewer leaves skip the rest)
-      const int ncol = min(NQ, 8 * hd.cnt);
-      float z[NQ];
-      tmem_ld_upto<NQ>(tmem + lane_addr + b * 3 * NQ, z, ncol);
-#pragma unroll
-      for (int n = 0; n < NQ; ++n)
-        z[n] = (valid && ((cm >> n) & 1ull)) ? z[n] * a.scale_log2 : -INFINITY;
-      tc_fence_before();
-      mbar_arrive(&s_empty[b]);             // S of this buffer has been read
-      // column max and sum over the 64 slots of this half: butterfly transpose-reduce in
-      // the warp, then the half's two warps combine through smem (double-buffered by parity)
-#pragma unroll
-      for (int c = 0; c < NQ; c += kW<NQ>) {
-        if (c < ncol) {
-          const float m = warp_reduceW<kW<NQ>, true>(z + c, lane);
-          if (!(lane & 1)) red_m[k & 3][quad][c + myc] = m;
-        }
-      }
-      named_bar_sync(1 + half, 64);
-      float p[NQ];
-#pragma unroll
-      for (int c = 0; c < NQ; c += 8) {
-        if (c < ncol) {
-#pragma unroll
-          for (int n = c; n < c + 8; ++n) {
-            const float m = fmaxf(red_m[k & 3][half * 2][n], red_m[k & 3][half * 2 + 1][n]);
-            p[n] = fast_exp2(z[n] - m);      // z = −inf (masked) → 0; m = −inf only if all masked
-            if (z[n] == -INFINITY) p[n] = 0.f;
-          }
-        } else {
-#pragma unroll
-          for (int n = c; n < c + 8; ++n) p[n] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < NQ; c += kW<NQ>) {
-        if (c < ncol) {
-          const float l = warp_reduceW<kW<NQ>, false>(p + c, lane);
-          if (!(lane & 1)) red_l[k & 3][quad][c + myc] = l;
-        }
-      }
       // P buffer b was last read by MMA2(k−2)
       if (k >= 2) mbar_wait(&o_full[b], ((k - 2) >> 1) & 1u);
-      // P (bf16) into rows [half·NQ, half·NQ + NQ) of slot-half `half` of the Pᵀ tile
-      {
-        // rows of columns ≥ ncol keep stale values: they only feed output columns that are
-        // never stored (Oᵀ column n depends on Pᵀ row n alone)
-        unsigned char *Pt = Pbuf + b * S::kP + half * (2 * NQ * 128);
-        const uint32_t cb = static_cast<uint32_t>(tc * 2);
+      // P (bf16) goes to rows [half·NQ, half·NQ + NQ) of slot-half `half` of the Pᵀ tile;
+      // rows of columns past the tile's own keep stale values: they only feed output columns
+      // that are never stored (Oᵀ column n depends on Pᵀ row n alone)
+      unsigned char *Pt = Pbuf + b * S::kP + half * (2 * NQ * 128);
+      float *zr = a.zbuf + ((static_cast<int64_t>(pb) * a.Lc + hd.li) * a.g.H + hd.h) * G * kAttnChunk + tc;
+#pragma unroll 1
+      for (int gi = 0; gi < ngrp; ++gi) {
+        const int c = gi * GW;
+        float z[GW], p[GW];
+        tmem_ldW<GW>(tmem + lane_addr + b * 3 * NQ + c, z);
 #pragma unroll
-        for (int c = 0; c < NQ; c += 8) {
-          if (c < ncol) {
+        for (int i = 0; i < GW; ++i)
+          z[i] = (valid && ((cm >> (c + i)) & 1ull)) ? z[i] * a.scale_log2 : -INFINITY;
+        // column max and sum over the 64 slots of this half: butterfly transpose-reduce in
+        // the warp, then the half's two warps combine through smem (ring of 4 tiles)
+        const float mw = warp_reduceW<GW, true>(z, lane);
+        if (!(lane & 1)) red_m[k & 3][quad][c + myc] = mw;
+        named_bar_sync(bar_id, 64);
 #pragma unroll
-            for (int n = c; n < c + 8; ++n) {
-              const int r = half * NQ + n;
-              *reinterpret_cast<__nv_bfloat16 *>(Pt + r * 128 + ((((cb >> 4) ^ (r & 7))) << 4) + (cb & 15)) =
-                  __float2bfloat16_rn(p[n]);
-            }
+        for (int i = 0; i < GW; ++i) {
+          const float m = fmaxf(red_m[k & 3][half * 2][c + i], red_m[k & 3][half * 2 + 1][c + i]);
+          p[i] = z[i] == -INFINITY ? 0.f : fast_exp2(z[i] - m);   // m = −inf only if all masked
+        }
+        const float lw = warp_reduceW<GW, false>(p, lane);
+        if (!(lane & 1)) red_l[k & 3][quad][c + myc] = lw;
+#pragma unroll
+        for (int i = 0; i < GW; ++i) {
+          const int r = half * NQ + c + i;
+          *reinterpret_cast<__nv_bfloat16 *>(Pt + r * 128 + ((((cb >> 4) ^ (r & 7))) << 4) + (cb & 15)) =
+              __float2bfloat16_rn(p[i]);
+        }
+        if (valid) {   // logits for the fused score pass: zbuf[pair][li][h][g][slot]
+#pragma unroll
+          for (int i = 0; i < GW; ++i) {
+            const int n = c + i;
+            if ((cm >> n) & 1ull) zr[static_cast<int64_t>((n >> 3) * SP + (n & 7)) * kAttnChunk] = z[i];
           }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&s_empty[b]);             // S of this buffer has been read
       // V rows of a partly filled last page hold pool bytes past k_cur: zero them so that
       // 0 · v stays 0 in Oᵀ = Vᵀ·Pᵀ (the rows past the last page were zeroed before)
       if (present && (nt & (P - 1))) {
@@ -643,34 +622,19 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         }
       }
       fence_proxy_async();
-      named_bar_sync(1 + half, 64);
+      named_bar_sync(bar_id, 64);
       mbar_arrive(&p_full[b]);
       if (tid == 64) TC_TRACE(k, 9);
-      // global writes after the MMA has been released
-      const int64_t rowbase = ((static_cast<int64_t>(pb) * a.Lc + hd.li) * a.g.H + hd.h) * G;
-      if (valid) {   // logits for the fused score pass: zbuf[pair][li][h][g][slot]
-        float *zr = a.zbuf + rowbase * kAttnChunk + tc;
-#pragma unroll
-        for (int c = 0; c < NQ; c += 8) {
-          if (c < ncol) {
-#pragma unroll
-            for (int n = c; n < c + 8; ++n)
-              if ((cm >> n) & 1ull) zr[static_cast<int64_t>(offn[n]) * kAttnChunk] = z[n];
-          }
-        }
-      }
     }
   } else {
     // ------------------------------------------------------------- epilogue (warps 6..9)
-    // Oᵀ[d][half·NQ + n] (TMEM lane = d) → partials[pair][li][h][g][d]
+    // Oᵀ[d][half·NQ + n] (TMEM lane = d) → partials[pair][li][h][g][d], in GW-column groups
+    constexpr int GW = kW<NQ>;
     const int quad = warp & 3;
     const int trow = quad * 32 + lane;
     const int G = a.G;
     const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
     const int SP = a.Lc * a.g.H * G;
-    int offn[NQ];
-#pragma unroll
-    for (int n = 0; n < NQ; ++n) offn[n] = (n >> 3) * SP + (n & 7);
     const int etid = tid - 192;                // 0..127
     for (int k = 0; k < ntiles; ++k) {
       const int b = k & 1;
@@ -685,25 +649,31 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         mm = fmaxf(red_m[k & 3][hh * 2][cn], red_m[k & 3][hh * 2 + 1][cn]);
         ll = red_l[k & 3][hh * 2][cn] + red_l[k & 3][hh * 2 + 1][cn];
       }
-      const int ncol = min(NQ, 8 * hd.cnt);
-      float o[2 * NQ];
-      tmem_ld_upto<NQ>(tmem + lane_addr + b * 3 * NQ + NQ, o, ncol);
-      if (hd.hasB) tmem_ld_upto<NQ>(tmem + lane_addr + b * 3 * NQ + 2 * NQ, o + NQ, ncol);
-      tc_fence_before();
-      mbar_arrive(&o_empty[b]);
+      const int ngrp = (min(NQ, 8 * hd.cnt) + GW - 1) / GW;
       const unsigned long long cm = colmask(hd.cnt, G);
       float *pa = a.partials + ((static_cast<int64_t>(hd.pbA) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
       float *pbp = a.partials + ((static_cast<int64_t>(hd.pbB) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
+#pragma unroll 1
+      for (int gi = 0; gi < ngrp; ++gi) {
+        const int c = gi * GW;
+        float o[GW];
+        tmem_ldW<GW>(tmem + lane_addr + b * 3 * NQ + NQ + c, o);
 #pragma unroll
-      for (int c = 0; c < NQ; c += 8) {
-        if (c < ncol) {
+        for (int i = 0; i < GW; ++i) {
+          const int n = c + i;
+          if ((cm >> n) & 1ull) pa[static_cast<int64_t>((n >> 3) * SP + (n & 7)) * 130] = o[i];
+        }
+        if (hd.hasB) {
+          tmem_ldW<GW>(tmem + lane_addr + b * 3 * NQ + 2 * NQ + c, o);
 #pragma unroll
-          for (int n = c; n < c + 8; ++n) {
-            if ((cm >> n) & 1ull) pa[static_cast<int64_t>(offn[n]) * 130] = o[n];
-            if (((cm >> n) & 1ull) && hd.hasB) pbp[static_cast<int64_t>(offn[n]) * 130] = o[NQ + n];
+          for (int i = 0; i < GW; ++i) {
+            const int n = c + i;
+            if ((cm >> n) & 1ull) pbp[static_cast<int64_t>((n >> 3) * SP + (n & 7)) * 130] = o[i];
           }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&o_empty[b]);
       if (etid < 2 * NQ && ((cm >> cn) & 1ull) && (hh == 0 || hd.hasB)) {
         float *dst = (hh ? pbp : pa) - trow + static_cast<int64_t>((cn >> 3) * SP + (cn & 7)) * 130;
         dst[128] = mm;
@@ -740,12 +710,12 @@ void launch_tc(arbor_ctx *c, const TcArgs &a) {
   if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
   const int total = a.T * a.Lc * a.g.H;
   const int grid = total < sms ? total : sms;
-  attn_tc_kernel<NQ, NST><<<grid, kTcThreads, S::kAlloc, c->ms>>>(
-      *reinterpret_cast<const CUtensorMap *>(c->tmap_k),
-      *reinterpret_cast<const CUtensorMap *>(c->tmap_v),
-      *reinterpret_cast<const CUtensorMap *>(c->tmap_k4),
-      *reinterpret_cast<const CUtensorMap *>(c->tmap_v4),
-      *reinterpret_cast<const CUtensorMap *>(c->tmap_q[c->tmap_q_cur]), a);
+  launch_pdl(attn_tc_kernel<NQ, NST>, dim3(grid), dim3(kTcThreads), S::kAlloc, c->ms,
+             *reinterpret_cast<const CUtensorMap *>(c->tmap_k),
+             *reinterpret_cast<const CUtensorMap *>(c->tmap_v),
+             *reinterpret_cast<const CUtensorMap *>(c->tmap_k4),
+             *reinterpret_cast<const CUtensorMap *>(c->tmap_v4),
+             *reinterpret_cast<const CUtensorMap *>(c->tmap_q[c->tmap_q_cur]), a);
 }
 
 long long *g_tc_trace = nullptr;

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/arbor.h"
@@ -229,6 +230,38 @@ void launch_attn_merge(arbor_ctx *c, const PlanView &pv, int layer_count, void *
 
 void stage_begin(arbor_ctx *c, int st, cudaStream_t s);
 void stage_end(arbor_ctx *c, int st, cudaStream_t s);
+
+// Programmatic dependent launch: the kernel may start while the previous kernel on the stream
+// drains (its prologue — smem carve-up, mbarrier init, TMEM alloc — overlaps that tail); every
+// thread of a kernel launched this way calls pdl_wait() before it touches global memory the
+// earlier kernels write or read.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args &&...args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+#ifdef __CUDACC__
+// griddepcontrol.wait: all prerequisite grids complete and their memory visible (a no-op when
+// the kernel was launched without the programmatic-serialization attribute)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// griddepcontrol.launch_dependents: this CTA no longer holds back the next PDL-launched kernel
+// (which launches once every CTA of this grid has triggered or exited, so all of this grid's
+// CTAs are resident by then: no resource deadlock)
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+#endif
 
 }  // namespace arbor
 

@@ -132,6 +132,8 @@ select_move_ws_kernel(CompactArgs a) {
     s_ev = 0;
   }
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
   // ---- plan (Alg. 2, Q17): k_app = min(k_cur, k_target) for every non-pinned node;
   // the changed ones, ascending id, are the work list.  Every CTA derives it from the same
   // unmodified state into its own copy; the last CTA to get there (ticket) applies it —
@@ -525,7 +527,7 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
     cached_lg = a.lgP;
   }
   stage_begin(c, ARBOR_ST_SELECT_COMPACT, c->ms);
-  select_move_ws_kernel<<<cached_grid, kPairsWs * 64, ly.total, c->ms>>>(a);
+  launch_pdl(select_move_ws_kernel, dim3(cached_grid), dim3(kPairsWs * 64), ly.total, c->ms, a);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SELECT_COMPACT, c->ms);
 }

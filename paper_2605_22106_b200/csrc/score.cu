@@ -190,6 +190,8 @@ __device__ __forceinline__ void msve_one(const MsveArgs &m, int i) {
 
 __global__ void __launch_bounds__(kFusedThreads)
 score_fused_kernel(FusedArgs f) {
+  pdl_wait();
+  pdl_trigger();
   const ApplyArgs &a = f.ap;
   const int row = blockIdx.x;                 // li * H + h
   const int li = row / f.H, h = row - li * f.H;
@@ -304,7 +306,7 @@ void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, cons
   m.s_state = c->d.s;
   m.s_out = s_out;
   stage_begin(c, ARBOR_ST_SCORE_ACCUM, c->ms);
-  score_fused_kernel<<<c->L * c->H, kFusedThreads, 0, c->ms>>>(f);
+  launch_pdl(score_fused_kernel, dim3(c->L * c->H), dim3(kFusedThreads), 0, c->ms, f);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
 }
