@@ -213,6 +213,26 @@ arbor_status arbor_tree_decode_attn(arbor_ctx *ctx, const arbor_tree *tree,
                                     int32_t layer_begin, int32_t layer_count, const void *q,
                                     void *out, float *lse_out);
 
+/* f1 — event-driven controller: one policy update event (PUE) of Alg. 2 (§3
+ * P:112-116).  Composes the calls above on main_stream, no host sync:
+ *  ARBOR_PUE_BOUNDARY (node: a just-closed block, else ARBOR_ERR_STATE): ScoreAllocEvict of
+ *    that block only (Alg. 2 l.4) — its k from Eqs. 2-3 with the library's last
+ *    scores and the tree's geometry; every other node keeps its retained set.
+ *  ARBOR_PUE_TRANSITION (node ignored; tree->active holds the new leaf/leaves): rehydrate
+ *    every closed Path* node with k < n (lazy rehydration, Alg. 2 l.8-14), then Eqs. 2-3 for
+ *    every off-path node, evicting only where the new k is smaller (Alg. 2 l.15-21).
+ *  ARBOR_PUE_PRESSURE (node ignored): reallocate to `budget` — params.alloc_mode WATERFILL
+ *    (budget-exact) or STATIC_DRAIN (Alg. 2 l.22-30 literally; STATIC is treated as
+ *    STATIC_DRAIN) — then evict.  ARBOR_ERR_INFEASIBLE_BUDGET as arbor_allocate.
+ *  k_out: DEVICE [num_nodes] int32 scratch, receives the targets that were applied. */
+typedef enum { ARBOR_PUE_BOUNDARY = 0, ARBOR_PUE_TRANSITION = 1, ARBOR_PUE_PRESSURE = 2 } arbor_pue;
+arbor_status arbor_policy_event(arbor_ctx *ctx, const arbor_tree *tree, int32_t kind,
+                                int32_t node, int64_t budget_tokens, int32_t *k_out,
+                                int64_t *min_feasible_out);
+/* Alg. 2 l.31-33 waterline input: M = Σ_i k_i over every known node (open nodes count their
+ * current length).  HOST out, syncs main_stream. */
+arbor_status arbor_retained_tokens(arbor_ctx *ctx, int64_t *total);
+
 /* ---- inspection / plumbing ------------------------------------------------------------ */
 arbor_status arbor_sync(arbor_ctx *ctx);   /* wait for both streams; returns latched errors */
 /* HOST outs (sync): the node's k_cur, n, and page list (pages may be NULL; *num_pages in). */

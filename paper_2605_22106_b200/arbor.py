@@ -84,6 +84,8 @@ def load_library(path: str = LIB_PATH):
         "arbor_allocate": ([P, C.POINTER(ArborTree), P, I64, P, C.POINTER(C.c_int64)], I32),
         "arbor_evict": ([P, C.POINTER(ArborTree), P, C.POINTER(C.c_int64)], I32),
         "arbor_rehydrate": ([P, C.POINTER(ArborTree), P, I32], I32),
+        "arbor_policy_event": ([P, C.POINTER(ArborTree), I32, I32, I64, P, C.POINTER(C.c_int64)], I32),
+        "arbor_retained_tokens": ([P, C.POINTER(C.c_int64)], I32),
         "arbor_tree_decode_attn": ([P, C.POINTER(ArborTree), I32, I32, P, P, P], I32),
         "arbor_sync": ([P], I32),
         "arbor_read_node": ([P, I32, P, P, P, P], I32),
@@ -292,6 +294,27 @@ class ArborKV:
             raise e
         self._check(st, "arbor_allocate")
         return k_out
+
+    def arbor_policy_event(self, tree, kind, node, budget: int, k_out):
+        """f1: one policy update event of Alg. 2 (kind: 'boundary' | 'transition' | 'pressure'
+        or the arbor_pue value); k_out receives the applied targets."""
+        kinds = {"boundary": 0, "transition": 1, "pressure": 2}
+        kd = kinds[kind] if isinstance(kind, str) else int(kind)
+        ta = _tree(tree)
+        mf = C.c_int64(-1)
+        st = self.lib.arbor_policy_event(self._ctx, C.byref(ta.struct), kd, int(node), int(budget),
+                                         k_out.data_ptr(), C.byref(mf))
+        if st == 3:
+            e = ArborError(st, f"infeasible budget {budget}, min feasible {mf.value}")
+            e.min_feasible = int(mf.value)
+            raise e
+        self._check(st, "arbor_policy_event")
+        return k_out
+
+    def arbor_retained_tokens(self) -> int:
+        t = C.c_int64(0)
+        self._check(self.lib.arbor_retained_tokens(self._ctx, C.byref(t)), "arbor_retained_tokens")
+        return int(t.value)
 
     def arbor_evict(self, tree, k_target, want_count=False):
         ta = _tree(tree)

@@ -38,6 +38,7 @@ struct AllocArgs {
   int32_t *depth, *delta;       // written (a1 fused)
   const double *Ed, *ED;
   int32_t *k_out;
+  int only_node;   // ≥ 0: only this node's target is computed; the others get n (no change)
   Ctrl *ctrl;
   long long *trace; // ARBOR_ALLOC_TRACE builds only: clock64() at phase boundaries
 };
@@ -469,16 +470,19 @@ allocate_kernel(AllocArgs a) {
   }
   __syncthreads();
   TRACE(6);
-  for (int j = threadIdx.x; j < N; j += blockDim.x) a.k_out[j] = k[j];
+  for (int j = threadIdx.x; j < N; j += blockDim.x)
+    a.k_out[j] = (a.only_node < 0 || j == a.only_node) ? k[j] : nn[j];
 }
 
 }  // namespace
 
-void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget, int32_t *k_out) {
+void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget, int32_t *k_out,
+                     int mode, int only_node) {
   AllocArgs a{};
   a.N = N;
   a.budget = budget;
-  a.mode = c->prm.alloc_mode;
+  a.mode = mode < 0 ? c->prm.alloc_mode : mode;
+  a.only_node = only_node;
   a.alpha = c->prm.alpha;
   a.gamma = c->prm.gamma;
   a.eta = c->prm.eta;

@@ -806,9 +806,9 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
   return ARBOR_OK;
 }
 
-arbor_status arbor_allocate(arbor_ctx *c, const arbor_tree *tree, const float *s, int64_t budget,
-                            int32_t *k_out, int64_t *min_feasible_out) {
-  if (!c) return ARBOR_ERR_INVALID_ARG;
+static arbor_status allocate_impl(arbor_ctx *c, const arbor_tree *tree, const float *s,
+                                  int64_t budget, int32_t *k_out, int64_t *min_feasible_out,
+                                  int mode, int only_node) {
   std::vector<int32_t> depth;
   TRY(check_tree(c, tree, &depth));
   if (!k_out) return fail(c, ARBOR_ERR_INVALID_ARG, "k_out is NULL");
@@ -821,16 +821,23 @@ arbor_status arbor_allocate(arbor_ctx *c, const arbor_tree *tree, const float *s
   for (int x = 0; x <= 2 * maxd; ++x) bD = std::max(bD, std::exp(-c->prm.lambda_delta * x));
   if (!(bd * bD <= 65536.0)) return fail(c, ARBOR_ERR_INVALID_ARG, "lambda_d / lambda_delta make weights exceed 2^16");
   const int64_t mf = min_feasible(&c->prm, tree);
-  if (c->prm.alloc_mode != ARBOR_ALLOC_STATIC && budget < mf) {
+  if (mode != ARBOR_ALLOC_STATIC && budget < mf) {
     if (min_feasible_out) *min_feasible_out = mf;
     return fail(c, ARBOR_ERR_INFEASIBLE_BUDGET, "budget " + std::to_string(budget) +
                                                     " < minimum feasible " + std::to_string(mf));
   }
   TRY(upload_tree(c, tree));
-  launch_allocate(c, tree->num_nodes, tree->num_active, s ? s : c->d.s, budget, k_out);
+  launch_allocate(c, tree->num_nodes, tree->num_active, s ? s : c->d.s, budget, k_out, mode,
+                  only_node);
   CK_LAUNCH();
   c->geom_version = c->tree_version;   // the allocate kernel wrote depth, Δ, Path*, pinned
   return ARBOR_OK;
+}
+
+arbor_status arbor_allocate(arbor_ctx *c, const arbor_tree *tree, const float *s, int64_t budget,
+                            int32_t *k_out, int64_t *min_feasible_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  return allocate_impl(c, tree, s, budget, k_out, min_feasible_out, c->prm.alloc_mode, -1);
 }
 
 arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_target,
@@ -891,6 +898,58 @@ arbor_status arbor_rehydrate(arbor_ctx *c, const arbor_tree *tree, const int32_t
   c->side_pending = true;
   CK(cudaStreamWaitEvent(c->ms, c->ev_side_done, 0));   // ready before the next decode
   stage_end(c, ARBOR_ST_REHYDRATE, c->ms);
+  return ARBOR_OK;
+}
+
+// ---------------------------------------------------------------- f1: event-driven controller
+arbor_status arbor_policy_event(arbor_ctx *c, const arbor_tree *tree, int32_t kind, int32_t node,
+                                int64_t budget, int32_t *k_out, int64_t *min_feasible_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  TRY(check_tree(c, tree));
+  if (!k_out) return fail(c, ARBOR_ERR_INVALID_ARG, "k_out is NULL");
+  switch (kind) {
+    case ARBOR_PUE_BOUNDARY: {
+      // Alg. 2 l.3-4: ScoreAllocEvict(i) — Eqs. 2-3 for block i only
+      if (node < 0 || node >= tree->num_nodes) return fail(c, ARBOR_ERR_INVALID_ARG, "unknown node");
+      if (tree->is_open[node] || (node < c->num_known && c->h_open[node]))
+        return fail(c, ARBOR_ERR_STATE, "boundary of an open block");
+      TRY(allocate_impl(c, tree, nullptr, budget, k_out, min_feasible_out, ARBOR_ALLOC_STATIC, node));
+      return arbor_evict(c, tree, k_out, nullptr);
+    }
+    case ARBOR_PUE_TRANSITION: {
+      // Alg. 2 l.5-21: Path* ← RootToLeaf(ℓ*); rehydrate its evicted blocks; Eqs. 2-3 for the
+      // off-path blocks, evicting where k drops (arbor_evict applies min(k_cur, k_new))
+      std::vector<uint8_t> on(tree->num_nodes, 0);
+      std::vector<int32_t> path;
+      for (int b = 0; b < tree->num_active; ++b)
+        for (int x = tree->active[b]; x >= 0 && !on[x]; x = tree->parent[x]) on[x] = 1;
+      for (int x = 0; x < tree->num_nodes; ++x)
+        if (on[x] && !tree->is_open[x]) path.push_back(x);
+      TRY(arbor_rehydrate(c, tree, path.data(), static_cast<int32_t>(path.size())));
+      TRY(allocate_impl(c, tree, nullptr, budget, k_out, min_feasible_out, ARBOR_ALLOC_STATIC, -1));
+      return arbor_evict(c, tree, k_out, nullptr);
+    }
+    case ARBOR_PUE_PRESSURE: {
+      // Alg. 2 l.22-30: reallocate the off-path blocks to the budget, then evict
+      const int mode = c->prm.alloc_mode == ARBOR_ALLOC_WATERFILL ? ARBOR_ALLOC_WATERFILL
+                                                                   : ARBOR_ALLOC_STATIC_DRAIN;
+      TRY(allocate_impl(c, tree, nullptr, budget, k_out, min_feasible_out, mode, -1));
+      return arbor_evict(c, tree, k_out, nullptr);
+    }
+    default:
+      return fail(c, ARBOR_ERR_INVALID_ARG, "unknown policy event");
+  }
+}
+
+arbor_status arbor_retained_tokens(arbor_ctx *c, int64_t *total) {
+  if (!c || !total) return ARBOR_ERR_INVALID_ARG;
+  TRY(sync_all(c));
+  std::vector<int32_t> kc(std::max(c->num_known, 1));
+  if (c->num_known)
+    CK(cudaMemcpy(kc.data(), c->d.kcur, c->num_known * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  int64_t t = 0;
+  for (int i = 0; i < c->num_known; ++i) t += kc[i];
+  *total = t;
   return ARBOR_OK;
 }
 

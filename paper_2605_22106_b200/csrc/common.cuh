@@ -206,7 +206,9 @@ void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, cons
                         int num_nodes, int N, bool do_msve, float *s_out);
 
 // allocate.cu
-void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget, int32_t *k_out);
+// mode < 0: params.alloc_mode; only_node ≥ 0: targets of the other nodes are n (unchanged)
+void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget, int32_t *k_out,
+                     int mode = -1, int only_node = -1);
 
 // evict.cu
 void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n);

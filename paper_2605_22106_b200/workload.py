@@ -270,3 +270,45 @@ class DptsRun:
         q = self.sc.queries(1_000_000 + self.step, len(tree.active))
         self.step += 1
         return q, decode_step(ctx, tree, q)
+
+
+# ---------------------------------------------------------------- f1: event-driven controller
+class Controller:
+    """Alg. 2 on the library: every policy update event is one
+    ``arbor_policy_event`` call (rehydrate / allocate / evict kernels, no host sync); the
+    waterline (Alg. 2 l.31-33, Σ k ≥ 𝓑 − δ, at most one pending Pressure) reads the retained
+    total (``arbor_retained_tokens``)."""
+
+    def __init__(self, ctx: ArborKV, budget: int, delta: int):
+        import torch
+        self.ctx = ctx
+        self.budget = int(budget)
+        self.delta = int(delta)
+        self.pending = False
+        self.k_buf = torch.empty(ctx.max_nodes, dtype=torch.int32, device=ctx.device)
+        self.log = []      # (event, node or -1, Σ k after) — read lazily by callers
+
+    def _event(self, tree, kind, node=-1):
+        self.ctx.arbor_policy_event(tree, kind, node, self.budget, self.k_buf[:tree.num_nodes])
+
+    def boundary(self, tree, i: int):
+        self._event(tree, "boundary", i)
+        self.log.append(("boundary", i))
+
+    def transition(self, tree):
+        self._event(tree, "transition")
+        self.log.append(("transition", -1))
+
+    def pressure(self, tree):
+        self._event(tree, "pressure")
+        self.pending = False
+        self.log.append(("pressure", -1))
+
+    def total(self) -> int:
+        return self.ctx.arbor_retained_tokens()
+
+    def waterline(self) -> bool:
+        if not self.pending and self.total() >= self.budget - self.delta:
+            self.pending = True
+            return True
+        return False

@@ -193,3 +193,20 @@ def dpts_schedule(tree: SynthTree, initial: list, transitions: int, swap: int,
         cur = nxt
         out.append(list(cur))
     return out
+
+
+def tot_expansion(tree: SynthTree, rng: np.random.Generator, width: int, max_depth: int):
+    """f1 traces: the next block a Tree-of-Thoughts search expands — a closed node with fewer
+    than ``width`` children and depth < ``max_depth``, drawn ∝ v (ties of the draw by id).
+    Returns (parent, v, u) of the new child, or None when the tree is complete.  Workload
+    generation only (the search policy is outside ArborKV)."""
+    d = _depths(tree.parent)
+    kids = np.bincount(tree.parent[tree.parent >= 0], minlength=tree.num_nodes)
+    elig = [i for i in range(tree.num_nodes)
+            if not tree.is_open[i] and kids[i] < width and d[i] < max_depth]
+    if not elig:
+        return None
+    w = np.asarray([float(tree.v[i]) + 1e-3 for i in elig])
+    parent = int(elig[int(rng.choice(len(elig), p=w / w.sum()))])
+    v, u = _features(rng, 1)
+    return parent, float(v[0]), float(u[0])
