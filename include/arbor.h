@@ -233,6 +233,15 @@ arbor_status arbor_policy_event(arbor_ctx *ctx, const arbor_tree *tree, int32_t 
  * current length).  HOST out, syncs main_stream. */
 arbor_status arbor_retained_tokens(arbor_ctx *ctx, int64_t *total);
 
+/* f3 — Eq. 1 on the device: the MSVE uncertainty feature at a block boundary,
+ * u = 1 − H/log|𝒱| with H = −Σ_w p(w) log p(w), p = softmax(logits) over the full vocabulary
+ * (exact; the top-K + "other" bucket of P:140 is an optional approximation the device does not
+ * need).  logits: DEVICE [batch][vocab], dtype ARBOR_F32 or ARBOR_BF16 (−inf entries are
+ * masked tokens); u_out: DEVICE [batch] f32.  Asynchronous on main_stream.
+ * ARBOR_ERR_INVALID_ARG for vocab < 2, batch < 1, NULL pointers or an unknown dtype. */
+arbor_status arbor_boundary_uncertainty(arbor_ctx *ctx, const void *logits, int32_t dtype,
+                                        int32_t batch, int32_t vocab, float *u_out);
+
 /* ---- inspection / plumbing ------------------------------------------------------------ */
 arbor_status arbor_sync(arbor_ctx *ctx);   /* wait for both streams; returns latched errors */
 /* HOST outs (sync): the node's k_cur, n, and page list (pages may be NULL; *num_pages in). */

@@ -86,6 +86,7 @@ def load_library(path: str = LIB_PATH):
         "arbor_rehydrate": ([P, C.POINTER(ArborTree), P, I32], I32),
         "arbor_policy_event": ([P, C.POINTER(ArborTree), I32, I32, I64, P, C.POINTER(C.c_int64)], I32),
         "arbor_retained_tokens": ([P, C.POINTER(C.c_int64)], I32),
+        "arbor_boundary_uncertainty": ([P, P, I32, I32, I32, P], I32),
         "arbor_tree_decode_attn": ([P, C.POINTER(ArborTree), I32, I32, P, P, P], I32),
         "arbor_sync": ([P], I32),
         "arbor_read_node": ([P, I32, P, P, P, P], I32),
@@ -310,6 +311,16 @@ class ArborKV:
             raise e
         self._check(st, "arbor_policy_event")
         return k_out
+
+    def arbor_boundary_uncertainty(self, logits, u_out):
+        """f3: Eq. 1 uncertainty of each row of logits [batch][vocab] (f32 or bf16) → u_out."""
+        import torch
+        dt = {torch.float32: 0, torch.bfloat16: 1}[logits.dtype]
+        b, v = logits.shape
+        self._check(self.lib.arbor_boundary_uncertainty(self._ctx, logits.data_ptr(), dt, int(b),
+                                                        int(v), u_out.data_ptr()),
+                    "arbor_boundary_uncertainty")
+        return u_out
 
     def arbor_retained_tokens(self) -> int:
         t = C.c_int64(0)

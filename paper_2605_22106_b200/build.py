@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v"]
 SOURCES = ["arbor_host.cu", "geometry.cu", "score.cu", "allocate.cu", "evict.cu", "pages.cu",
-           "attn.cu", "attn_tc.cu"]
+           "attn.cu", "attn_tc.cu", "uncertainty.cu"]
 
 
 def _deps():

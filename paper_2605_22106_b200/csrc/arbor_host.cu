@@ -643,6 +643,8 @@ void arbor_destroy(arbor_ctx *c) {
   if (c->ss) cudaStreamSynchronize(c->ss);
   if (c->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(static_cast<ncclComm_t>(c->nccl_comm));
   DevState &d = c->d;
+  if (c->unc_part) cudaFree(c->unc_part);
+  if (c->unc_ticket) cudaFree(c->unc_ticket);
   void *ptrs[] = {d.n, d.kcur, d.npages, d.ptab, d.free_stack, d.span, d.mass2, d.mclose, d.nq,
                   d.a, d.s, d.ctrl, d.parent, d.onpath, d.pinned, d.depth, d.delta, d.Ed, d.ED,
                   d.work, d.rehyd_nodes, d.rehyd_flag, d.seg,
@@ -939,6 +941,18 @@ arbor_status arbor_policy_event(arbor_ctx *c, const arbor_tree *tree, int32_t ki
     default:
       return fail(c, ARBOR_ERR_INVALID_ARG, "unknown policy event");
   }
+}
+
+arbor_status arbor_boundary_uncertainty(arbor_ctx *c, const void *logits, int32_t dtype,
+                                        int32_t batch, int32_t vocab, float *u_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  if (!logits || !u_out) return fail(c, ARBOR_ERR_INVALID_ARG, "logits / u_out is NULL");
+  if (batch < 1 || vocab < 2) return fail(c, ARBOR_ERR_INVALID_ARG, "need batch >= 1 and vocab >= 2");
+  if (dtype != ARBOR_F32 && dtype != ARBOR_BF16) return fail(c, ARBOR_ERR_INVALID_ARG, "bad dtype");
+  const arbor_status s = launch_uncertainty(c, logits, dtype, batch, vocab, u_out);
+  if (s != ARBOR_OK) return fail(c, s, "uncertainty launch failed");
+  CK_LAUNCH();
+  return ARBOR_OK;
 }
 
 arbor_status arbor_retained_tokens(arbor_ctx *c, int64_t *total) {

@@ -135,6 +135,8 @@ struct arbor_ctx {
   int64_t max_tokens;
   cudaStream_t ms, ss;
   bool own_ms = false, own_ss = false;
+  void *unc_part = nullptr, *unc_ticket = nullptr;   // f3 uncertainty scratch (grown on demand)
+  size_t unc_cap = 0;
   arbor::DevState d{};
   // host mirror
   std::vector<int32_t> h_n;
@@ -204,6 +206,10 @@ void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64
 void launch_msve(arbor_ctx *c, int N, float *s_out);
 void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
                         int num_nodes, int N, bool do_msve, float *s_out);
+
+// uncertainty.cu (f3)
+arbor_status launch_uncertainty(arbor_ctx *c, const void *logits, int dtype, int batch, int vocab,
+                                float *u_out);
 
 // allocate.cu
 // mode < 0: params.alloc_mode; only_node ≥ 0: targets of the other nodes are n (unchanged)
