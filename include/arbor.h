@@ -74,7 +74,21 @@ typedef struct {
   int32_t n_sinks;      /* global sinks: first n_sinks positions of the root     */
   int32_t alloc_mode;   /* arbor_alloc_mode                                       */
   double theta[4];      /* MSVE θ = (θ0 bias, θ_v, θ_u, θ_a) (Q7)     */
+  /* f4 policy variants (0 = the paper's full method):            */
+  int32_t select_mode;  /* arbor_select_mode: intra-block retention rule              */
+  int32_t no_rehydrate; /* 1: evicted tokens never come back (P:423-428 ablation):
+                         * arbor_rehydrate and Transition's rehydration are no-ops      */
 } arbor_params;
+
+/* Intra-block retention rule of arbor_evict (P:660-675 ablation).  The block tail
+ * (L_tail) is always kept; the remaining k − |tail| slots go to the currently kept
+ * non-tail positions ranked by:
+ *  HEAVY      ⟨A, position⟩ descending — heavy hitters (the method);
+ *  TAIL       position descending — recency only ("Tail-only");
+ *  SINKS_TAIL the block's first n_sinks positions first, then position descending
+ *             ("Sinks + Tail"; block-level sinks: the global sinks are the root's, which
+ *             is on Path* and never evicted). */
+typedef enum { ARBOR_SELECT_HEAVY = 0, ARBOR_SELECT_TAIL = 1, ARBOR_SELECT_SINKS_TAIL = 2 } arbor_select_mode;
 
 /* Context configuration.  Host struct; device buffers are caller-owned and
  * borrowed for the lifetime of the context. */

@@ -28,11 +28,26 @@ def key(a_f32: float, offset: int):
     return (f32_bits(a_f32), int(offset))
 
 
-def retained_set(kept, n: int, k_app: int, l_tail: int, A_node_f32):
+HEAVY, TAIL, SINKS_TAIL = 0, 1, 2   # intra-block rules (arbor_select_mode; P:660-675 ablation)
+
+
+def rank_key(mode: int, a_f32: float, t: int, n_sinks: int):
+    """Order of the non-tail candidates, descending: ⟨A, t⟩ for the method's heavy hitters
+    (Q3); t alone for Tail-only; ⟨t is a block sink, t⟩ for Sinks + Tail
+    (block-level sinks: the first n_sinks positions of the block; DESIGN.md f4)."""
+    if mode == HEAVY:
+        return key(a_f32, t)
+    if mode == TAIL:
+        return (0, int(t))
+    return (1 if t < n_sinks else 0, int(t))
+
+
+def retained_set(kept, n: int, k_app: int, l_tail: int, A_node_f32, mode: int = HEAVY,
+                 n_sinks: int = 0):
     """Alg. 1 Evict for one (row, node).
 
     kept: within-node offsets currently retained (C, any order);
-    A_node_f32: f32 accumulated attention indexed by within-node offset.
+    A_node_f32: f32 accumulated attention indexed by within-node offset (HEAVY only).
     Returns the new ascending retained offsets ℛ with |ℛ| = k_app."""
     kept = [int(x) for x in kept]
     assert 0 <= k_app <= len(kept)
@@ -45,8 +60,9 @@ def retained_set(kept, n: int, k_app: int, l_tail: int, A_node_f32):
     assert set(tail) <= set(kept)
     m = k_app - tl                            # m_i = k_i − |𝒯_i|
     cand = [t for t in kept if t < n - tl]
-    ranked = sorted(cand, key=lambda t: key(A_node_f32[t], t), reverse=True)
-    heavy = ranked[:m]                        # Top-m_i by A_i(t)
+    ranked = sorted(cand, key=lambda t: rank_key(mode, A_node_f32[t] if mode == HEAVY else 0.0,
+                                                 t, n_sinks), reverse=True)
+    heavy = ranked[:m]                        # Top-m_i by A_i(t), or the variant's order
     return sorted(tail + heavy)
 
 

@@ -37,7 +37,7 @@ def default_params(**over) -> dict:
     """SURVEY Appendix B defaults (documented choices; the paper gives none)."""
     p = dict(alpha=1.0, gamma=2.0, lambda_d=0.0, lambda_delta=0.5, eta=0.8, r_min=0.05,
              k_min=4, l_tail=8, n_sinks=4, theta=(-1.0, 2.0, 1.0, 4.0),
-             alloc_mode=tae.MODE_WATERFILL)
+             alloc_mode=tae.MODE_WATERFILL, select_mode=0, no_rehydrate=False)
     p.update(over)
     return p
 
@@ -236,7 +236,9 @@ class ArborOracle:
                 for h in range(self.H):
                     old = [int(x) for x in self.kept[j][l, h]]
                     R = set(select.retained_set(old, n, k_app, self.params["l_tail"],
-                                                A_f32[l, h, a:a + n]))
+                                                A_f32[l, h, a:a + n],
+                                                self.params.get("select_mode", select.HEAVY),
+                                                self.params["n_sinks"]))
                     holes = [s for s in range(k_app) if old[s] not in R]
                     movers = [old[s] for s in range(k_app, kc) if old[s] in R]
                     assert len(holes) == len(movers)
@@ -262,6 +264,8 @@ class ArborOracle:
         for i in nodes:
             if self.open[i]:
                 raise OracleError(ERR_STATE, "rehydrating an open node")
+        if self.params.get("no_rehydrate"):       # f4 ablation: eviction is irreversible
+            return 0
         count = 0
         for i in nodes:
             n = self.n[i]

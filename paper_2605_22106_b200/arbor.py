@@ -20,6 +20,7 @@ ARBOR_OK = 0
 STATUS = {0: "OK", 2: "INVALID_ARG", 3: "INFEASIBLE_BUDGET", 4: "INVARIANT", 5: "IO",
           6: "OUT_OF_PAGES", 7: "STATE", 8: "CUDA", 9: "NCCL"}
 ALLOC_MODES = {"waterfill": 0, "static": 1, "static_drain": 2}
+SELECT_MODES = {"heavy": 0, "tail": 1, "sinks_tail": 2}
 FLAG_PROFILE = 1
 NUM_STAGES = 13
 STAGES = ["geometry", "score_accum", "node_mass", "msve", "allocate", "evict_plan",
@@ -38,7 +39,8 @@ class ArborParams(C.Structure):
     _fields_ = [("alpha", C.c_double), ("gamma", C.c_double), ("lambda_d", C.c_double),
                 ("lambda_delta", C.c_double), ("eta", C.c_double), ("r_min", C.c_double),
                 ("k_min", C.c_int32), ("l_tail", C.c_int32), ("n_sinks", C.c_int32),
-                ("alloc_mode", C.c_int32), ("theta", C.c_double * 4)]
+                ("alloc_mode", C.c_int32), ("theta", C.c_double * 4),
+                ("select_mode", C.c_int32), ("no_rehydrate", C.c_int32)]
 
 
 class ArborConfig(C.Structure):
@@ -116,11 +118,14 @@ def load_library(path: str = LIB_PATH):
 
 def make_params(alpha=1.0, gamma=2.0, lambda_d=0.0, lambda_delta=0.5, eta=0.8, r_min=0.05,
                 k_min=4, l_tail=8, n_sinks=4, theta=(-1.0, 2.0, 1.0, 4.0),
-                alloc_mode="waterfill") -> ArborParams:
+                alloc_mode="waterfill", select_mode="heavy", no_rehydrate=False) -> ArborParams:
     """Parameter bundle Π (Alg. 1 caption P:498); defaults are DESIGN.md's documented choices."""
     mode = ALLOC_MODES[alloc_mode] if isinstance(alloc_mode, str) else int(alloc_mode)
+    sel = SELECT_MODES[select_mode] if isinstance(select_mode, str) else int(select_mode)
     p = ArborParams(alpha, gamma, lambda_d, lambda_delta, eta, r_min, int(k_min), int(l_tail),
                     int(n_sinks), mode)
+    p.select_mode = sel
+    p.no_rehydrate = 1 if no_rehydrate else 0
     for i, t in enumerate(theta):
         p.theta[i] = float(t)
     return p
@@ -128,7 +133,7 @@ def make_params(alpha=1.0, gamma=2.0, lambda_d=0.0, lambda_delta=0.5, eta=0.8, r
 
 def params_from_dict(d: dict) -> ArborParams:
     keys = ("alpha", "gamma", "lambda_d", "lambda_delta", "eta", "r_min", "k_min", "l_tail",
-            "n_sinks", "theta", "alloc_mode")
+            "n_sinks", "theta", "alloc_mode", "select_mode", "no_rehydrate")
     return make_params(**{k: d[k] for k in keys if k in d})
 
 

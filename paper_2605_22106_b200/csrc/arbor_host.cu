@@ -108,6 +108,8 @@ arbor_status validate_params(const arbor_params *p, std::string &msg) {
   if (p->k_min < 0 || p->l_tail < 0 || p->n_sinks < 0) { msg = "k_min, l_tail, n_sinks must be >= 0"; return ARBOR_ERR_INVALID_ARG; }
   if (p->alloc_mode < 0 || p->alloc_mode > 2) { msg = "bad alloc_mode"; return ARBOR_ERR_INVALID_ARG; }
   for (double t : p->theta) if (!fin(t)) { msg = "theta must be finite"; return ARBOR_ERR_INVALID_ARG; }
+  if (p->select_mode < 0 || p->select_mode > 2) { msg = "bad select_mode"; return ARBOR_ERR_INVALID_ARG; }
+  if (p->no_rehydrate != 0 && p->no_rehydrate != 1) { msg = "no_rehydrate must be 0 or 1"; return ARBOR_ERR_INVALID_ARG; }
   return ARBOR_OK;
 }
 
@@ -882,7 +884,7 @@ arbor_status arbor_rehydrate(arbor_ctx *c, const arbor_tree *tree, const int32_t
   }
   std::sort(list.begin(), list.end());
   list.erase(std::unique(list.begin(), list.end()), list.end());
-  if (list.empty()) return ARBOR_OK;
+  if (list.empty() || c->prm.no_rehydrate) return ARBOR_OK;   // f4: irreversible eviction
   int max_n = 0;
   for (int x : list) max_n = std::max(max_n, c->h_n[x]);
   TRY(upload_tree(c, tree));

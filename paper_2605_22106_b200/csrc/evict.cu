@@ -50,6 +50,8 @@ struct CompactArgs {
   int cap;          // max n over evicted nodes (smem capacity, slots)
   int lgP;          // log2(page size)
   int exp;          // ARBOR_EVICT_EXP (measurement only): bit0 skip moves, bit1 skip radix select
+  int select_mode;  // arbor_select_mode (f4)
+  int n_sinks;      // block-level sinks of ARBOR_SELECT_SINKS_TAIL
 };
 
 constexpr int kPlanPer = 6;   // nodes per thread in the plan scan (N ≤ 3072 = 6 × 512)
@@ -306,7 +308,7 @@ select_move_ws_kernel(CompactArgs a) {
       cp_async4(pb + s, a.pos + base + static_cast<int64_t>(g[s >> lgP]) * pstride + (s & Pm));
     }
     const int tl = min(a.l_tail, e.n);
-    if (e.ka > tl) {               // ranked: A of the non-tail positions
+    if (e.ka > tl && a.select_mode == ARBOR_SELECT_HEAVY) {   // ranked by A: the non-tail span
       const int r = it % a.R;
       const float *Arow = a.A + static_cast<int64_t>(r) * a.max_tokens + e.span;
       float *ab = Abuf + (k & 1) * cap;
@@ -359,9 +361,15 @@ select_move_ws_kernel(CompactArgs a) {
         const int p = pb[s];
         kk = static_cast<unsigned>(p);
         if (ranked && p < tail_from) {
-          const float av = ab[p];
-          if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-          const unsigned bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
+          // the key's high part: f32 bits of A (HEAVY), 0 (TAIL: recency), sink flag
+          unsigned bits = p < a.n_sinks ? 1u : 0u;
+          if (a.select_mode == ARBOR_SELECT_HEAVY) {
+            const float av = ab[p];
+            if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+            bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
+          } else if (a.select_mode == ARBOR_SELECT_TAIL) {
+            bits = 0u;
+          }
           kk = kCand | (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
           bmin = min(bmin, bits);
           bmax = max(bmax, bits);
@@ -503,6 +511,8 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
   a.esize = c->esize;
   a.cap = max_n < 1 ? 1 : max_n;
   a.lgP = __builtin_ctz(static_cast<unsigned>(c->P));
+  a.select_mode = c->prm.select_mode;
+  a.n_sinks = c->prm.n_sinks;
   static const int exp_flags = [] {
     const char *e = getenv("ARBOR_EVICT_EXP");
     return e ? atoi(e) : 0;

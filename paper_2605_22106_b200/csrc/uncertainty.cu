@@ -7,33 +7,24 @@
 //
 // With a reference m: S = Σ e^{z−m}, T = Σ e^{z−m}(z − m), and H = log S − T/S.  Changing the
 // reference to m' ≥ m rescales S' = e^{m−m'} S and T' = e^{m−m'} (T + (m − m') S), so each
-// thread streams its slice once (online m, S, T in fp32), CTAs combine their threads' triples
-// in fp64, and the last CTA of a row (ticket) combines the CTAs' triples and writes u.
+// thread streams its slice once (8 logits per load batch, (m, S, T) in fp32), the CTA
+// combines its threads' triples by shuffles, and the last CTA of a row (ticket) combines the
+// CTAs' triples in fp64 and writes u.
 // HBM-bound: one read of the logits (4 or 2 B per vocabulary entry).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace arbor {
 namespace {
 
 constexpr int kUncThreads = 256;
-constexpr int kUncSplit = 16;        // CTAs per row (grid = batch × kUncSplit)
+constexpr int kUncPer = 8;           // logits per thread: loaded together, then absorbed
+constexpr int kUncMaxSplit = 256;    // CTAs per row: ⌈vocab / (256·8)⌉, at most this
 
 struct Triple {
   double m, S, T;
 };
-
-__device__ __forceinline__ void absorb(float &m, float &S, float &T, float z) {
-  if (z == -INFINITY) return;               // a masked logit: p = 0 contributes nothing
-  if (z > m) {
-    const float r = m == -INFINITY ? 0.f : expf(m - z);
-    T = r * (T + (m == -INFINITY ? 0.f : (m - z)) * S);
-    S = r * S;
-    m = z;
-  }
-  const float e = expf(z - m);
-  S += e;
-  T += e * (z - m);
-}
 
 __device__ __forceinline__ Triple merge(Triple a, Triple b) {
   if (b.m == -INFINITY) return a;
@@ -54,40 +45,93 @@ __device__ __forceinline__ float to_f<float>(float x) { return x; }
 template <>
 __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
 
+struct TripleF {
+  float m, S, T;
+};
+
+__device__ __forceinline__ TripleF merge_f(TripleF a, TripleF b) {
+  if (b.m == -INFINITY) return a;
+  if (a.m == -INFINITY) return b;
+  const float m = fmaxf(a.m, b.m);
+  const float ra = expf(a.m - m), rb = expf(b.m - m);
+  return TripleF{m, ra * a.S + rb * b.S, ra * (a.T + (a.m - m) * a.S) + rb * (b.T + (b.m - m) * b.S)};
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kUncThreads)
 uncertainty_kernel(const T *__restrict__ logits, int vocab, Triple *__restrict__ part,
                    unsigned *__restrict__ ticket, float *__restrict__ u_out) {
   pdl_wait();
   pdl_trigger();
-  const int row = blockIdx.y, split = blockIdx.x;
+  const int row = blockIdx.y, split = blockIdx.x, nsplit = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const T *z = logits + static_cast<int64_t>(row) * vocab;
-  const int per = (vocab + kUncSplit - 1) / kUncSplit;
+  const int per = (vocab + nsplit - 1) / nsplit;
   const int lo = split * per, hi = min(vocab, lo + per);
-  float m = -INFINITY, S = 0.f, Tt = 0.f;
-  for (int i = lo + threadIdx.x; i < hi; i += kUncThreads) absorb(m, S, Tt, to_f(__ldg(z + i)));
-  // block combine (fp64) through shared memory
-  __shared__ Triple red[kUncThreads];
-  red[threadIdx.x] = Triple{static_cast<double>(m), static_cast<double>(S), static_cast<double>(Tt)};
-  __syncthreads();
-  for (int s = kUncThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] = merge(red[threadIdx.x], red[threadIdx.x + s]);
-    __syncthreads();
+  TripleF acc{-INFINITY, 0.f, 0.f};
+  for (int i0 = lo + threadIdx.x; i0 < hi; i0 += kUncThreads * kUncPer) {
+    float v[kUncPer];
+    float m8 = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kUncPer; ++j) {       // all loads in flight before any use
+      const int i = i0 + j * kUncThreads;
+      v[j] = i < hi ? to_f(__ldg(z + i)) : -INFINITY;
+    }
+#pragma unroll
+    for (int j = 0; j < kUncPer; ++j) m8 = fmaxf(m8, v[j]);
+    if (m8 == -INFINITY) continue;            // all masked
+    TripleF t{m8, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < kUncPer; ++j) {
+      if (v[j] == -INFINITY) continue;        // a masked logit: p = 0
+      const float d = v[j] - m8, e = expf(d);
+      t.S += e;
+      t.T = fmaf(e, d, t.T);
+    }
+    acc = merge_f(acc, t);
   }
+  // warp, then CTA combine (fixed shuffle / slot order: deterministic)
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    TripleF other{__shfl_xor_sync(0xffffffffu, acc.m, o), __shfl_xor_sync(0xffffffffu, acc.S, o),
+                  __shfl_xor_sync(0xffffffffu, acc.T, o)};
+    acc = lane & o ? merge_f(other, acc) : merge_f(acc, other);
+  }
+  __shared__ TripleF wred[kUncThreads / 32];
+  if (lane == 0) wred[warp] = acc;
+  __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) {
-    part[row * kUncSplit + split] = red[0];
+    TripleF c = wred[0];
+    for (int w = 1; w < kUncThreads / 32; ++w) c = merge_f(c, wred[w]);
+    part[row * nsplit + split] = Triple{static_cast<double>(c.m), static_cast<double>(c.S),
+                                        static_cast<double>(c.T)};
     __threadfence();
-    last = atomicAdd(&ticket[row], 1u) == kUncSplit - 1;
+    last = atomicAdd(&ticket[row], 1u) == static_cast<unsigned>(nsplit - 1);
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
+  if (!last) return;
+  // the row's last CTA: the CTAs' triples, loaded in parallel (L2), combined by a warp tree
+  // in fp32 per 32 CTAs and in fp64 across those groups (fixed order: deterministic)
   __threadfence();
+  if (warp != 0) return;
   Triple t{-INFINITY, 0.0, 0.0};
-  for (int k = 0; k < kUncSplit; ++k) {   // fixed order: deterministic
-    const volatile Triple *p = part + row * kUncSplit + k;
-    t = merge(t, Triple{p->m, p->S, p->T});
+  for (int k0 = 0; k0 < nsplit; k0 += 32) {
+    TripleF c{-INFINITY, 0.f, 0.f};
+    if (k0 + lane < nsplit) {
+      const Triple *p = part + row * nsplit + k0 + lane;
+      c = TripleF{static_cast<float>(__ldcg(&p->m)), static_cast<float>(__ldcg(&p->S)),
+                  static_cast<float>(__ldcg(&p->T))};
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      TripleF other{__shfl_xor_sync(0xffffffffu, c.m, o), __shfl_xor_sync(0xffffffffu, c.S, o),
+                    __shfl_xor_sync(0xffffffffu, c.T, o)};
+      c = lane & o ? merge_f(other, c) : merge_f(c, other);
+    }
+    t = merge(t, Triple{static_cast<double>(c.m), static_cast<double>(c.S), static_cast<double>(c.T)});
   }
+  if (lane != 0) return;
   const double H = log(t.S) - t.T / t.S;
   const double u = 1.0 - H / log(static_cast<double>(vocab));
   u_out[row] = static_cast<float>(fmin(1.0, fmax(0.0, u)));
@@ -98,7 +142,9 @@ uncertainty_kernel(const T *__restrict__ logits, int vocab, Triple *__restrict__
 
 arbor_status launch_uncertainty(arbor_ctx *c, const void *logits, int dtype, int batch, int vocab,
                                 float *u_out) {
-  const size_t need = static_cast<size_t>(batch) * kUncSplit;
+  const int nsplit = std::min(kUncMaxSplit, std::max(1, (vocab + kUncThreads * kUncPer - 1) /
+                                                            (kUncThreads * kUncPer)));
+  const size_t need = static_cast<size_t>(batch) * kUncMaxSplit;
   if (need > c->unc_cap) {
     if (c->unc_part) cudaFree(c->unc_part);
     if (c->unc_ticket) cudaFree(c->unc_ticket);
@@ -111,7 +157,7 @@ arbor_status launch_uncertainty(arbor_ctx *c, const void *logits, int dtype, int
       return ARBOR_ERR_CUDA;
     c->unc_cap = need;
   }
-  const dim3 grid(kUncSplit, batch);
+  const dim3 grid(nsplit, batch);
   Triple *part = static_cast<Triple *>(c->unc_part);
   unsigned *tk = static_cast<unsigned *>(c->unc_ticket);
   cudaError_t e;

@@ -18,6 +18,8 @@ def oracle_params(preset_params: dict) -> dict:
     p.update(preset_params)
     if isinstance(p.get("alloc_mode"), str):
         p["alloc_mode"] = {"waterfill": 0, "static": 1, "static_drain": 2}[p["alloc_mode"]]
+    if isinstance(p.get("select_mode"), str):
+        p["select_mode"] = {"heavy": 0, "tail": 1, "sinks_tail": 2}[p["select_mode"]]
     return p
 
 

@@ -1,0 +1,64 @@
+"""f4 — policy variants as kernel modes against the oracle, bit-exact:
+intra-block retention Tail-only and Sinks + Tail (arbor_params.select_mode) through two
+successive evictions (the second acting on already-compacted blocks), and the no-rehydration
+ablation (arbor_params.no_rehydrate: Transition/rehydrate leave evicted blocks partial).
+MSVE-only (λ_Δ = 0) and TAE-only (constant s) are parameter settings of the method's path,
+covered by the allocation tests in test_gpu_parity.py."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+from gpu_helpers import Pair
+
+pytestmark = pytest.mark.gpu
+
+MID = dict(tree=("full", 3, 4, 56), L=2, H=2, Hq=8, d=128, dtype="bf16", P=16, rho=0.25,
+           params={}, active="highest_v")
+
+
+def _evict_both(pr, k):
+    kd = torch.as_tensor(np.asarray(k, np.int32), device="cuda")
+    ev = pr.ctx.arbor_evict(pr.tree, kd, want_count=True)
+    assert ev == pr.orc.evict(pr.tree, k, A_f32=pr.gpu_A())
+    pr.check_kv_state()
+
+
+@pytest.mark.parametrize("mode", ["tail", "sinks_tail", "heavy"])
+def test_select_mode_two_stage_eviction(mode):
+    pr = Pair(MID, seed=5, params_over=dict(select_mode=mode, n_sinks=5, l_tail=6))
+    pr.warmup(steps_per_leaf=1)
+    N = pr.tree.num_nodes
+    rng = np.random.default_rng(9)
+    n = [int(x) for x in pr.tree.span_len]
+    k1 = [int(rng.integers(n[i] // 3, n[i] + 1)) for i in range(N)]
+    _evict_both(pr, k1)
+    k2 = [int(rng.integers(0, k1[i] + 1)) for i in range(N)]
+    _evict_both(pr, k2)
+    if mode != "heavy":   # closed form on a node evicted from full retention
+        j = next(i for i in range(N) if pr.orc.k_cur(i) > 8 and pr.orc.k_cur(i) < n[i])
+        kc = pr.orc.k_cur(j)
+        kept = sorted(int(x) for x in pr.orc.kept[j][0, 0])
+        tl = min(6, n[j])
+        sk = min(5, kc - tl) if mode == "sinks_tail" else 0
+        assert kept == sorted(set(range(sk)) | set(range(n[j] - (kc - sk), n[j])))
+    pr.tree.active = [synth.leaves_of(pr.tree)[-1]]
+    pr.decode_both()
+
+
+def test_no_rehydrate_keeps_evicted_path_partial():
+    pr = Pair(MID, seed=6, params_over=dict(no_rehydrate=True))
+    pr.warmup(steps_per_leaf=1)
+    N = pr.tree.num_nodes
+    _evict_both(pr, [4] * N)
+    leaf = synth.leaves_of(pr.tree)[0]
+    pr.tree.active = [leaf]
+    path = [x for x in range(N) if pr.orc.k_cur(x) < int(pr.tree.span_len[x])]
+    pr.ctx.arbor_rehydrate(pr.tree, path)
+    assert pr.orc.rehydrate(path) == 0
+    pr.check_kv_state()
+    assert pr.ctx.arbor_read_counters()[0] == 0
+    pr.decode_both()       # attention over the partial Path* blocks

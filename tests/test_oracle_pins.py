@@ -503,3 +503,52 @@ def test_state_hole_filling_layout():
                 holes = [s_ for s_ in range(ka) if old[s_] not in R]
                 movers = [old[s_] for s_ in range(ka, len(old)) if old[s_] in R]
                 assert [new[s_] for s_ in holes] == movers
+
+
+# ---------------------------------------------------------------- f4 intra-block variants
+@pytest.mark.parametrize("n,k,l_tail,s", [(40, 13, 4, 3), (17, 9, 2, 4), (64, 20, 8, 0), (12, 5, 5, 2)])
+def test_select_variants_closed_forms(n, k, l_tail, s):
+    """Tail-only and Sinks + Tail from full retention reduce to intervals:
+    Tail keeps the last k positions; Sinks+Tail keeps the block's first min(s, m) positions
+    and the most recent k − min(s, m) (m = k − |tail|).  Neither depends on A."""
+    rng = np.random.default_rng(n * 7 + k)
+    A = rng.random(n).astype(np.float32)
+    full = list(range(n))
+    tl = min(l_tail, n)
+    assert select.retained_set(full, n, k, l_tail, A, select.TAIL) == list(range(n - k, n))
+    m = max(k - tl, 0)
+    sk = min(s, m) if k > tl else 0
+    want = sorted(set(range(sk)) | set(range(n - (k - sk), n)))
+    assert select.retained_set(full, n, k, l_tail, A, select.SINKS_TAIL, s) == want
+    A2 = rng.permutation(A)
+    for mode in (select.TAIL, select.SINKS_TAIL):
+        assert (select.retained_set(full, n, k, l_tail, A, mode, s) ==
+                select.retained_set(full, n, k, l_tail, A2, mode, s))
+
+
+def test_select_variants_compose():
+    """Evicting to k1 then k2 < k1 equals evicting to k2 directly (the rules rank the same
+    positions the same way at every step)."""
+    rng = np.random.default_rng(3)
+    for mode in (select.HEAVY, select.TAIL, select.SINKS_TAIL):
+        for _ in range(20):
+            n = int(rng.integers(8, 60))
+            A = rng.random(n).astype(np.float32)
+            k1 = int(rng.integers(1, n + 1))
+            k2 = int(rng.integers(0, k1 + 1))
+            r1 = select.retained_set(list(range(n)), n, k1, 3, A, mode, 2)
+            assert (select.retained_set(r1, n, k2, 3, A, mode, 2) ==
+                    select.retained_set(list(range(n)), n, k2, 3, A, mode, 2))
+
+
+def test_no_rehydrate_is_irreversible():
+    """with rehydration disabled an evicted block never comes back."""
+    tree, orc, _ = _small_state(params=default_params(k_min=2, l_tail=3, r_min=0.0,
+                                                       no_rehydrate=True))
+    tree.active = [synth.leaves_of(tree)[0]]
+    N = len(orc.n)
+    k = [2] * N
+    orc.evict(tree, k)
+    before = [orc.k_cur(i) for i in range(N)]
+    assert orc.rehydrate(list(range(N))) == 0
+    assert [orc.k_cur(i) for i in range(N)] == before
