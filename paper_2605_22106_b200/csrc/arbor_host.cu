@@ -793,8 +793,10 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
   // a2 + a3 in one launch (score.cu): score pass, partial masses, Mass/Mclose → mass2, and —
   // single rank — the MSVE score; with several ranks the all-reduce sits before the MSVE
   const bool single = c->cfg.world_size == 1;
+  // node-wise split of each row over CTAs: about two recomputed nodes per CTA, ≤ 8 per row
+  const int nparts = std::max(1, std::min(8, static_cast<int>(mass_nodes.size()) / 2));
   launch_score_fused(c, pv, lse_use, d_mass_nodes, static_cast<int>(mass_nodes.size()), N, single,
-                     s_out);
+                     s_out, nparts);
   CK_LAUNCH();
   c->lg_epoch = -1;   // A changed: the logits must not be applied twice
   c->mass_valid = true;

@@ -204,8 +204,9 @@ void launch_score_apply(arbor_ctx *c, const PlanView &pv, const float *lse, int 
 void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64_t *out,
                       int out_stride);
 void launch_msve(arbor_ctx *c, int N, float *s_out);
+// nparts CTAs per (layer, KV head) row; CTA (row, p) owns the nodes with id % nparts == p
 void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
-                        int num_nodes, int N, bool do_msve, float *s_out);
+                        int num_nodes, int N, bool do_msve, float *s_out, int nparts);
 
 // uncertainty.cu (f3)
 arbor_status launch_uncertainty(arbor_ctx *c, const void *logits, int dtype, int batch, int vocab,

@@ -194,37 +194,59 @@ score_fused_kernel(FusedArgs f) {
   pdl_trigger();
   const ApplyArgs &a = f.ap;
   const int row = blockIdx.x;                 // li * H + h
+  const int part = blockIdx.y, nparts = gridDim.y;   // node owner: node % nparts (node-wise CTA ownership)
   const int li = row / f.H, h = row - li * f.H;
   const int tid = threadIdx.x;
   // (1) A[li][h][a_j + pos] += Σ_pairs Σ_g exp2(z − LSE·log2 e)
-  for (int idx = tid; idx < a.pv.C * kAttnChunk; idx += kFusedThreads) {
-    const int c = idx / kAttnChunk, t = idx - c * kAttnChunk;
+  // A full node (k_cur = n) holds its tokens in position order (appends and rehydration
+  // write the identity; only an eviction permutes slots, and it lowers k_cur), so its pos
+  // tag is the slot itself: no page-table / tag round trip.  The pair loop's loads are
+  // issued together (G ≤ 8 logits and LSEs per pair).
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int c = warp; c < a.pv.C; c += kFusedThreads / 32) {   // warp per owned chunk
     const int node = a.pv.ch_node[c];
+    if (node % nparts != part) continue;
     const int c0 = a.pv.ch_chunk[c] * kAttnChunk;
-    const int nt = max(0, min(kAttnChunk, a.kcur[node] - c0));
-    if (t >= nt) continue;
+    const int kc = a.kcur[node];
+    const int nt = max(0, min(kAttnChunk, kc - c0));
     const int p0 = a.pv.ch_poff[c], pc = a.pv.ch_pcnt[c];
-    float psum = 0.f;
-    for (int p = p0; p < p0 + pc; ++p) {
-      const int b = a.pv.pair_b[p];
-      const float *z = a.zbuf + (((static_cast<int64_t>(p) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + t;
-      const float *ls = a.lse + (static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * a.G;
-      for (int g = 0; g < a.G; ++g) psum += exp2f(z[g * kAttnChunk] - ls[g] * kLog2e);
-    }
-    const int slot = c0 + t;
+    const int64_t sp = a.span[node];
+    const bool ident = kc == f.nlen[node];
     const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.g.MPN;
-    const int pos = a.pos[pool_row(a.g, li, pl[slot / a.g.P], h, slot % a.g.P)];
-    float *dst = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + a.span[node] + pos;
-    const float nv = *dst + psum;
-    if (!(nv >= 0.f) || isinf(nv)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-    *dst = nv;
+    for (int t = lane; t < nt; t += 32) {
+      const int slot = c0 + t;
+      const int pos = ident ? slot : a.pos[pool_row(a.g, li, pl[slot / a.g.P], h, slot % a.g.P)];
+      float psum = 0.f;
+      for (int p = p0; p < p0 + pc; ++p) {
+        const int b = a.pv.pair_b[p];
+        const float *z = a.zbuf + (((static_cast<int64_t>(p) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + t;
+        const float *ls = a.lse + (static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * a.G;
+        for (int g0 = 0; g0 < a.G; g0 += 8) {
+          float zz[8], ll[8];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            if (g0 + g < a.G) {
+              zz[g] = z[(g0 + g) * kAttnChunk];
+              ll[g] = ls[g0 + g];
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            if (g0 + g < a.G) psum += exp2f(zz[g] - ll[g] * kLog2e);
+        }
+      }
+      float *dst = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + sp + pos;
+      const float nv = *dst + psum;
+      if (!(nv >= 0.f) || isinf(nv)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+      *dst = nv;
+    }
   }
   __syncthreads();
   // (2) this row's partial node masses: warp per node, lanes strided, fixed xor tree (Q29)
-  const int warp = tid >> 5, lane = tid & 31;
   const float *Arow = a.A + (static_cast<int64_t>(li) * f.H + h) * f.max_tokens;
   for (int mi = warp; mi < f.n_mass; mi += kFusedThreads / 32) {
     const int node = f.mass_nodes[mi];
+    if (node % nparts != part) continue;
     const int n = f.nlen[node];
     const float *r = Arow + a.span[node];
     double m = 0.0;
@@ -237,7 +259,7 @@ score_fused_kernel(FusedArgs f) {
   __shared__ bool last;
   __threadfence();
   __syncthreads();
-  if (tid == 0) last = atomicAdd(f.ticket, 1u) == gridDim.x - 1;
+  if (tid == 0) last = atomicAdd(f.ticket, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -261,7 +283,7 @@ score_fused_kernel(FusedArgs f) {
 }  // namespace
 
 void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
-                        int num_nodes, int N, bool do_msve, float *s_out) {
+                        int num_nodes, int N, bool do_msve, float *s_out, int nparts) {
   FusedArgs f{};
   ApplyArgs &a = f.ap;
   a.pv = pv;
@@ -306,7 +328,7 @@ void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, cons
   m.s_state = c->d.s;
   m.s_out = s_out;
   stage_begin(c, ARBOR_ST_SCORE_ACCUM, c->ms);
-  launch_pdl(score_fused_kernel, dim3(c->L * c->H), dim3(kFusedThreads), 0, c->ms, f);
+  launch_pdl(score_fused_kernel, dim3(c->L * c->H, nparts), dim3(kFusedThreads), 0, c->ms, f);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
 }
