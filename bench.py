@@ -292,11 +292,16 @@ def main():
         ctx.score.copy_(snap_A)
         ctx.arbor_load_state(0)
 
+    two_call = os.environ.get("ARBOR_BENCH_TWO_CALL") == "1"
+
     def step(i):
         ta = trees[i % 2]
         q = qs[i % 2]
-        ctx.arbor_tree_decode_attn(ta, q, out, lse)
-        ctx.arbor_score(ta, q, lse, s_buf)
+        if two_call:      # diagnostics: the unfused a9 → a2/a3 calls (three launches)
+            ctx.arbor_tree_decode_attn(ta, q, out, lse)
+            ctx.arbor_score(ta, q, lse, s_buf)
+        else:
+            ctx.arbor_decode_step(ta, q, out, lse, s_buf)     # a9 + a2 + a3 (f2: two launches)
         ctx.arbor_allocate(ta, s_buf, B, k_buf)
         ctx.arbor_evict(ta, k_buf)
 
@@ -424,7 +429,7 @@ def main():
     kernels["attn_partial"] = kstat("attn", lambda i: ab[i]["attn"])
     if stage_ms["node_mass"][0] > 0:          # unfused a3 (multi-rank runs)
         kernels["node_mass"] = kstat("node_mass", lambda i: ab[i]["node_mass"])
-    # a9 + a2 as one unit: the fused path's bytes over attn + merge + score-apply time
+    # a9 + a2 + a3 as one unit (arbor_decode_step: attention kernel + merge/score kernel)
     t_as = sum(statistics.mean(stage_ms[k]) for k in ("attn", "attn_merge", "score_accum",
                                                        "node_mass", "msve"))
     b_as = statistics.mean(ab[i]["attn_score"] for i in range(2))
@@ -461,8 +466,7 @@ def main():
         a.record(stream)
         q_dev.copy_(q_host[i % 2], non_blocking=True)
         ta = trees[i % 2]
-        ctx.arbor_tree_decode_attn(ta, q_dev, out, lse)
-        ctx.arbor_score(ta, q_dev, lse, s_buf)
+        ctx.arbor_decode_step(ta, q_dev, out, lse, s_buf)
         ctx.arbor_allocate(ta, s_buf, B, k_buf)
         ctx.arbor_evict(ta, k_buf)
         k_host.copy_(k_buf, non_blocking=True)
@@ -615,9 +619,8 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
             tq = TreeArgs.from_tree(tree)
             d = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             d[0].record(stream)
-            ctx.arbor_tree_decode_attn(tq, q, out, lse)
+            ctx.arbor_decode_step(tq, q, out, lse)
             d[1].record(stream)
-            ctx.arbor_score(tq, q, lse)
             d[2].record(stream)
             dec.append(d)
         torch.cuda.synchronize()
@@ -652,10 +655,9 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
             lse = torch.empty((len(tree.active), ctx.L, ctx.Hq), dtype=torch.float32, device=dev)
             tq = TreeArgs.from_tree(tree)
             torch.cuda.synchronize()
-            h = time.perf_counter(); ctx.arbor_tree_decode_attn(tq, q, out, lse)
+            h = time.perf_counter(); ctx.arbor_decode_step(tq, q, out, lse)
             host_ms["attn"].append((time.perf_counter() - h) * 1e3)
-            h = time.perf_counter(); ctx.arbor_score(tq, q, lse)
-            host_ms["score"].append((time.perf_counter() - h) * 1e3)
+            host_ms["score"].append(0.0)
         torch.cuda.synchronize()
     stage = ctx.arbor_stage_times()
     ctx.arbor_set_profiling(False)
@@ -678,14 +680,15 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
             "config": dict(workload_config("c3", ws), budget=run.budget, active_leaves=16,
                            decode_steps_per_transition=D,
                            step="one DPTS transition: a1+a4 allocate -> a5+a6 evict -> a8 "
-                                "rehydrate (side stream); then 8 decode steps of a9 + a2/a3 "
-                                "(reported separately)"),
+                                "rehydrate (side stream); then 8 decode steps of arbor_decode_step "
+                                "(a9 + a2/a3, reported separately)"),
             "roofline": {"kernel": "attn_tc (a9, 16 leaves, tree-shared tiles)", "bound": "hbm",
                          "achieved": attn_gbs, "peak": peak, "unit": "GB/s",
                          "frac": attn_gbs / peak, "frac_of_nominal_8TBps": attn_gbs / NOMINAL_HBM,
                          "traffic": None, "peak_source": peak_src,
                          "alg_bytes_per_launch": attn_b, "ms_per_launch": attn_ms,
-                         "note": "a9 launch time includes the merge (tree decode step)"},
+                         "note": "time of arbor_decode_step: the attention kernel plus the "
+                                 "merge + score (a2/a3) kernel; bytes: K/V + Q/O only"},
             "cpu_baseline": None,
             "e2e": {"value": cached_tot / wall_tot, "unit": "tokens/s",
                     "h2d_bytes_per_step": int(nodes_n * 25 + 64), "d2h_bytes_per_step": 16,

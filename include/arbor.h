@@ -227,6 +227,22 @@ arbor_status arbor_tree_decode_attn(arbor_ctx *ctx, const arbor_tree *tree,
                                     int32_t layer_begin, int32_t layer_count, const void *q,
                                     void *out, float *lse_out);
 
+/* f2 — one decode step with the score fused into the attention (P:184-191,
+ * "accumulated from attention weights already materialized during decoding"):
+ * exactly arbor_tree_decode_attn over the full layer range followed by arbor_score with its
+ * LSE — same arguments, same results up to fp32 rounding of the LSE — but as two launches:
+ * the attention kernel, then one kernel that merges the split-softmax partials into out /
+ * LSE and, with the LSE still on chip, accumulates A from the logits the attention kernel
+ * wrote, recomputes the visible nodes' partial masses and (single rank) the MSVE scores.
+ * With several ranks the int64 mass all-reduce and the MSVE launch follow, as in arbor_score.
+ *  q:       DEVICE [num_active][layer_count][Hq_local][head_dim] kv_dtype
+ *  out:     DEVICE same shape and dtype as q
+ *  lse_out: DEVICE [num_active][layer_count][Hq_local] f32, or NULL
+ *  s_out:   DEVICE [num_nodes] f32, or NULL (as arbor_score)
+ *  Errors as arbor_tree_decode_attn / arbor_score; nothing is enqueued on an error. */
+arbor_status arbor_decode_step(arbor_ctx *ctx, const arbor_tree *tree, const void *q, void *out,
+                               float *lse_out, float *s_out);
+
 /* f1 — event-driven controller: one policy update event (PUE) of Alg. 2 (§3
  * P:112-116).  Composes the calls above on main_stream, no host sync:
  *  ARBOR_PUE_BOUNDARY (node: a just-closed block, else ARBOR_ERR_STATE): ScoreAllocEvict of

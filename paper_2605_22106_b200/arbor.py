@@ -90,6 +90,7 @@ def load_library(path: str = LIB_PATH):
         "arbor_retained_tokens": ([P, C.POINTER(C.c_int64)], I32),
         "arbor_boundary_uncertainty": ([P, P, I32, I32, I32, P], I32),
         "arbor_tree_decode_attn": ([P, C.POINTER(ArborTree), I32, I32, P, P, P], I32),
+        "arbor_decode_step": ([P, C.POINTER(ArborTree), P, P, P, P], I32),
         "arbor_sync": ([P], I32),
         "arbor_read_node": ([P, I32, P, P, P, P], I32),
         "arbor_read_free_list": ([P, P, P], I32),
@@ -351,6 +352,14 @@ class ArborKV:
         self._check(self.lib.arbor_tree_decode_attn(self._ctx, C.byref(ta.struct), int(layer_begin),
                                                     int(lc), q.data_ptr(), out.data_ptr(),
                                                     self._ptr(lse)), "arbor_tree_decode_attn")
+        return out
+
+    def arbor_decode_step(self, tree, q, out, lse=None, s_out=None):
+        """f2: a9 + a2 + a3 fused (attention kernel, then merge + score in one launch)."""
+        ta = _tree(tree)
+        self._check(self.lib.arbor_decode_step(self._ctx, C.byref(ta.struct), q.data_ptr(),
+                                               out.data_ptr(), self._ptr(lse), self._ptr(s_out)),
+                    "arbor_decode_step")
         return out
 
     # ---------------------------------------------------------------- inspection

@@ -749,6 +749,39 @@ arbor_status arbor_close_node(arbor_ctx *c, int32_t node) {
 }
 
 // ---------------------------------------------------------------- hot path
+// Per score call: Nq_i += 1 for every closed i on Path(ℓ_b) (one query per active leaf and
+// step); the nodes whose partial masses are (re)computed — the visible closed nodes, or all
+// closed nodes when the cache is invalid (A changes only at visible tokens).
+static void score_bookkeeping(arbor_ctx *c, const arbor_tree *tree, const HostPlan &hp,
+                              std::vector<int32_t> &mass_nodes) {
+  const int N = tree->num_nodes, nA = tree->num_active;
+  std::vector<uint8_t> vis(N, 0);
+  for (int b = 0; b < nA; ++b)
+    for (int x : hp.paths[b]) {
+      vis[x] = 1;
+      if (!c->h_open[x]) c->h_nq[x] += 1;
+    }
+  for (int i = 0; i < N; ++i)
+    if (!c->h_open[i] && (vis[i] || !c->mass_valid)) mass_nodes.push_back(i);
+}
+
+// node-wise split of each row over CTAs: about two recomputed nodes per CTA, ≤ 8 per row
+static int score_parts(size_t mass_nodes) {
+  return std::max(1, std::min(8, static_cast<int>(mass_nodes) / 2));
+}
+
+// a10 + MSVE on several ranks: the all-reduce sits between the partial masses and the score
+static arbor_status score_allreduce(arbor_ctx *c, int N, float *s_out) {
+  stage_begin(c, ARBOR_ST_ALLREDUCE, c->ms);
+  if (g_nccl.allReduce(c->d.mass2, c->d.mass2, 2 * static_cast<size_t>(N), ncclInt64, ncclSum,
+                       static_cast<ncclComm_t>(c->nccl_comm), c->ms) != ncclSuccess)
+    return fail(c, ARBOR_ERR_NCCL, "ncclAllReduce failed");
+  stage_end(c, ARBOR_ST_ALLREDUCE, c->ms);
+  launch_msve(c, N, s_out);
+  CK_LAUNCH();
+  return ARBOR_OK;
+}
+
 arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, const float *lse,
                          float *s_out) {
   if (!c) return ARBOR_ERR_INVALID_ARG;
@@ -758,18 +791,8 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
   TRY(upload_tree(c, tree));
   HostPlan hp;
   build_plan(tree, c->h_n, hp);
-  // Nq_i += 1 for every closed i on Path(ℓ_b) (one query per active leaf and step)
-  std::vector<uint8_t> vis(N, 0);
-  for (int b = 0; b < nA; ++b)
-    for (int x : hp.paths[b]) {
-      vis[x] = 1;
-      if (!c->h_open[x]) c->h_nq[x] += 1;
-    }
-  // partial masses to (re)compute: the visible closed nodes, or all closed nodes when the
-  // cache is invalid (A changes only at visible tokens)
   std::vector<int32_t> mass_nodes;
-  for (int i = 0; i < N; ++i)
-    if (!c->h_open[i] && (vis[i] || !c->mass_valid)) mass_nodes.push_back(i);
+  score_bookkeeping(c, tree, hp, mass_nodes);
   PlanView pv{};
   const int32_t *d_mass_nodes = nullptr;
   TRY(upload_plan(c, hp, nA, true, &mass_nodes, pv, &d_mass_nodes));
@@ -793,22 +816,48 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
   // a2 + a3 in one launch (score.cu): score pass, partial masses, Mass/Mclose → mass2, and —
   // single rank — the MSVE score; with several ranks the all-reduce sits before the MSVE
   const bool single = c->cfg.world_size == 1;
-  // node-wise split of each row over CTAs: about two recomputed nodes per CTA, ≤ 8 per row
-  const int nparts = std::max(1, std::min(8, static_cast<int>(mass_nodes.size()) / 2));
   launch_score_fused(c, pv, lse_use, d_mass_nodes, static_cast<int>(mass_nodes.size()), N, single,
-                     s_out, nparts);
+                     s_out, score_parts(mass_nodes.size()));
   CK_LAUNCH();
   c->lg_epoch = -1;   // A changed: the logits must not be applied twice
   c->mass_valid = true;
-  if (!single) {
-    stage_begin(c, ARBOR_ST_ALLREDUCE, c->ms);
-    if (g_nccl.allReduce(c->d.mass2, c->d.mass2, 2 * static_cast<size_t>(N), ncclInt64, ncclSum,
-                         static_cast<ncclComm_t>(c->nccl_comm), c->ms) != ncclSuccess)
-      return fail(c, ARBOR_ERR_NCCL, "ncclAllReduce failed");
-    stage_end(c, ARBOR_ST_ALLREDUCE, c->ms);
-    launch_msve(c, N, s_out);
-    CK_LAUNCH();
+  if (!single) TRY(score_allreduce(c, N, s_out));
+  return ARBOR_OK;
+}
+
+// f2: a9 + a2 + a3 as two launches — the attention kernel (partials + logits), then one
+// kernel that merges the partials into out / LSE and, with the merged LSE still on chip,
+// applies the score pass, the partial masses and (single rank) the MSVE score.  Same
+// results as arbor_tree_decode_attn (full layer range) followed by arbor_score.
+arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void *q, void *out,
+                               float *lse_out, float *s_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  TRY(check_tree(c, tree));
+  if (!q || !out) return fail(c, ARBOR_ERR_INVALID_ARG, "q / out is NULL");
+  const int N = tree->num_nodes, nA = tree->num_active;
+  if (!decode_post_fits(c, nA)) {   // more (leaf, q-head) pairs than the merge keeps on chip
+    TRY(arbor_tree_decode_attn(c, tree, 0, c->L, q, out, lse_out));
+    if (lse_out) return arbor_score(c, tree, q, lse_out, s_out);
+    return arbor_score(c, tree, q, nullptr, s_out);
   }
+  TRY(upload_tree(c, tree));
+  HostPlan hp;
+  build_plan(tree, c->h_n, hp);
+  std::vector<int32_t> mass_nodes;
+  score_bookkeeping(c, tree, hp, mass_nodes);
+  PlanView pv{};
+  const int32_t *d_mass_nodes = nullptr;
+  TRY(upload_plan(c, hp, nA, true, &mass_nodes, pv, &d_mass_nodes));
+  TRY(ensure_partials(c, hp.pair_b.size(), c->L));
+  launch_attn_partial(c, pv, q, 0, c->L, hp.max_cnt, out, lse_out);
+  CK_LAUNCH();
+  const bool single = c->cfg.world_size == 1;
+  launch_decode_post(c, pv, out, lse_out, d_mass_nodes, static_cast<int>(mass_nodes.size()), N,
+                     single, s_out, score_parts(mass_nodes.size()));
+  CK_LAUNCH();
+  c->lg_epoch = -1;
+  c->mass_valid = true;
+  if (!single) TRY(score_allreduce(c, N, s_out));
   return ARBOR_OK;
 }
 

@@ -207,6 +207,12 @@ void launch_msve(arbor_ctx *c, int N, float *s_out);
 // nparts CTAs per (layer, KV head) row; CTA (row, p) owns the nodes with id % nparts == p
 void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
                         int num_nodes, int N, bool do_msve, float *s_out, int nparts);
+// f2 (arbor_decode_step): merge of the attention partials (out, LSE) + the fused score of
+// launch_score_fused in one launch; LSE stays on chip.  Requires decode_post_fits.
+bool decode_post_fits(arbor_ctx *c, int nA);
+void launch_decode_post(arbor_ctx *c, const PlanView &pv, void *out, float *lse_out,
+                        const int32_t *d_nodes, int num_nodes, int N, bool do_msve, float *s_out,
+                        int nparts);
 
 // uncertainty.cu (f3)
 arbor_status launch_uncertainty(arbor_ctx *c, const void *logits, int dtype, int batch, int vocab,
@@ -256,7 +262,8 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  static const int pdl_off = getenv("ARBOR_NO_PDL") ? 1 : 0;   // diagnostics
+  cfg.numAttrs = pdl_off ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -188,14 +188,12 @@ __device__ __forceinline__ void msve_one(const MsveArgs &m, int i) {
   if (m.s_out) m.s_out[i] = m.open[i] ? 0.5f : s;
 }
 
-__global__ void __launch_bounds__(kFusedThreads)
-score_fused_kernel(FusedArgs f) {
-  pdl_wait();
-  pdl_trigger();
+// Steps (1)-(3) of one (row, part) CTA; lse2(b, g) gives the log2-domain LSE of leaf b's
+// query head g of this row's KV head (the caller's LSE buffer, or the merged one in smem).
+template <typename LseFn>
+__device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int part, int nparts,
+                                          LseFn lse2) {
   const ApplyArgs &a = f.ap;
-  const int row = blockIdx.x;                 // li * H + h
-  const int part = blockIdx.y, nparts = gridDim.y;   // node owner: node % nparts (node-wise CTA ownership)
-  const int li = row / f.H, h = row - li * f.H;
   const int tid = threadIdx.x;
   // (1) A[li][h][a_j + pos] += Σ_pairs Σ_g exp2(z − LSE·log2 e)
   // A full node (k_cur = n) holds its tokens in position order (appends and rehydration
@@ -220,19 +218,18 @@ score_fused_kernel(FusedArgs f) {
       for (int p = p0; p < p0 + pc; ++p) {
         const int b = a.pv.pair_b[p];
         const float *z = a.zbuf + (((static_cast<int64_t>(p) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + t;
-        const float *ls = a.lse + (static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * a.G;
         for (int g0 = 0; g0 < a.G; g0 += 8) {
           float zz[8], ll[8];
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             if (g0 + g < a.G) {
               zz[g] = z[(g0 + g) * kAttnChunk];
-              ll[g] = ls[g0 + g];
+              ll[g] = lse2(b, g0 + g);
             }
           }
 #pragma unroll
           for (int g = 0; g < 8; ++g)
-            if (g0 + g < a.G) psum += exp2f(zz[g] - ll[g] * kLog2e);
+            if (g0 + g < a.G) psum += exp2f(zz[g] - ll[g]);
         }
       }
       float *dst = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + sp + pos;
@@ -280,10 +277,120 @@ score_fused_kernel(FusedArgs f) {
   for (int i = tid; i < f.N; i += kFusedThreads) msve_one(f.m, i);
 }
 
+__global__ void __launch_bounds__(kFusedThreads)
+score_fused_kernel(FusedArgs f) {
+  pdl_wait();
+  pdl_trigger();
+  const int row = blockIdx.x;                        // li * H + h
+  const int li = row / f.H, h = row - li * f.H;
+  const float *ls = f.ap.lse + static_cast<int64_t>(li) * f.ap.Hq + h * f.ap.G;
+  const int64_t bstride = static_cast<int64_t>(f.ap.Lc) * f.ap.Hq;
+  // node-wise CTA ownership: node % gridDim.y
+  score_row(f, li, h, blockIdx.y, gridDim.y,
+            [&](int b, int g) { return ls[b * bstride + g] * kLog2e; });
+}
+
+// ---------------------------------------------------------------- f2: a9 merge + a2 + a3
+// arbor_decode_step's second launch ("from attention weights already
+// materialized during decoding"): one CTA per (row, part) first merges, root→leaf, the
+// split-softmax partials the attention kernel left for every (active leaf b, query head g)
+// of its row — M = max m, L = Σ 2^(m−M) l, o = Σ 2^(m−M) o_p / L, LSE₂ = M + log2 L (warp per
+// (b, g), lanes over the path's pairs for M and L, over d for o) — keeps LSE₂ in shared
+// memory, and then runs score_row on the logits with it.  Every part needs every LSE of the
+// row, so M and L are computed by all parts (2 floats per pair), while o and the LSE output
+// are written by part (b·G + g) mod parts only.  Replaces attn_merge_kernel + the score
+// launch (and the LSE round trip through HBM) on the decode step.
+struct PostArgs {
+  FusedArgs f;
+  const float *partials;
+  void *out;
+  float *lse_out;   // natural-log LSE, or NULL
+  int nA;
+};
+constexpr int kPostItems = 512;   // nA · G ≤ kPostItems (host-checked)
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kFusedThreads)
+decode_post_kernel(PostArgs pa) {
+  pdl_trigger();   // launched without PDL (launch_decode_post); lets the next kernel overlap
+  const FusedArgs &f = pa.f;
+  const ApplyArgs &a = f.ap;
+  const int row = blockIdx.x, part = blockIdx.y, nparts = gridDim.y;
+  const int li = row / f.H, h = row - li * f.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = kFusedThreads / 32, EPL = D / 32;
+  const int G = a.G;
+  __shared__ float lse2s[kPostItems];
+  auto part_ptr = [&](int p, int g) -> const float * {
+    return pa.partials + (((static_cast<int64_t>(p) * a.Lc + li) * f.H + h) * G + g) * (D + 2);
+  };
+  for (int it = warp; it < pa.nA * G; it += NW) {
+    const int b = it / G, g = it - b * G;
+    const int p0 = a.pv.bp_off[b], p1 = a.pv.bp_off[b + 1];
+    float M = -INFINITY;
+    for (int i = p0 + lane; i < p1; i += 32) M = fmaxf(M, part_ptr(a.pv.bp_list[i], g)[D]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const bool own = it % nparts == part;
+    float Ls = 0.f;
+    float acc[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+    if (M != -INFINITY) {
+      for (int i0 = p0; i0 < p1; i0 += 32) {
+        const int i = i0 + lane;
+        int pi = 0;
+        float w = 0.f;
+        if (i < p1) {
+          pi = a.pv.bp_list[i];
+          const float *pp = part_ptr(pi, g);
+          const float m2 = pp[D];
+          if (m2 != -INFINITY) {
+            w = exp2f(m2 - M);
+            Ls = fmaf(w, pp[D + 1], Ls);
+          }
+        }
+        if (own) {
+          const int cnt = min(32, p1 - i0);
+#pragma unroll 4
+          for (int j = 0; j < cnt; ++j) {
+            const float wj = __shfl_sync(0xffffffffu, w, j);
+            const int pj = __shfl_sync(0xffffffffu, pi, j);
+            const float *pp = part_ptr(pj, g);
+            float v[EPL];
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) v[e] = pp[lane + 32 * e];
+            if (wj != 0.f) {
+#pragma unroll
+              for (int e = 0; e < EPL; ++e) acc[e] = fmaf(wj, v[e], acc[e]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
+    const float l2 = Ls > 0.f ? M + log2f(Ls) : -INFINITY;
+    if (lane == 0) lse2s[it] = l2;
+    if (own) {
+      const int gq = h * G + g;
+      T *out = static_cast<T *>(pa.out) + ((static_cast<int64_t>(b) * a.Lc + li) * a.Hq + gq) * D;
+      const float inv = Ls > 0.f ? 1.f / Ls : 0.f;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) out[lane + 32 * e] = ElemT<T>::from_f(acc[e] * inv);
+      if (lane == 0 && pa.lse_out)
+        pa.lse_out[(static_cast<int64_t>(b) * a.Lc + li) * a.Hq + gq] = l2 * 0.6931471805599453f;
+    }
+  }
+  __syncthreads();
+  score_row(f, li, h, part, nparts, [&](int b, int g) { return lse2s[b * G + g]; });
+}
+
 }  // namespace
 
-void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
-                        int num_nodes, int N, bool do_msve, float *s_out, int nparts) {
+namespace {
+FusedArgs fused_args(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
+                     int num_nodes, int N, bool do_msve, float *s_out) {
   FusedArgs f{};
   ApplyArgs &a = f.ap;
   a.pv = pv;
@@ -327,8 +434,41 @@ void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, cons
   m.a_out = c->d.a;
   m.s_state = c->d.s;
   m.s_out = s_out;
+  return f;
+}
+}  // namespace
+
+void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
+                        int num_nodes, int N, bool do_msve, float *s_out, int nparts) {
+  const FusedArgs f = fused_args(c, pv, lse, d_nodes, num_nodes, N, do_msve, s_out);
   stage_begin(c, ARBOR_ST_SCORE_ACCUM, c->ms);
   launch_pdl(score_fused_kernel, dim3(c->L * c->H, nparts), dim3(kFusedThreads), 0, c->ms, f);
+  ARBOR_LAUNCHED(c);
+  stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
+}
+
+bool decode_post_fits(arbor_ctx *c, int nA) { return nA * c->G <= kPostItems; }
+
+void launch_decode_post(arbor_ctx *c, const PlanView &pv, void *out, float *lse_out,
+                        const int32_t *d_nodes, int num_nodes, int N, bool do_msve, float *s_out,
+                        int nparts) {
+  PostArgs pa{};
+  pa.f = fused_args(c, pv, nullptr, d_nodes, num_nodes, N, do_msve, s_out);
+  pa.partials = c->d.partials;
+  pa.out = out;
+  pa.lse_out = lse_out;
+  pa.nA = pv.nA;
+  const dim3 grid(c->L * c->H, nparts);
+  stage_begin(c, ARBOR_ST_SCORE_ACCUM, c->ms);
+  // A plain launch, not PDL: 2·(rows) CTAs of 256 threads made resident early next to the
+  // attention kernel's CTAs slowed that kernel (measured: C2 step 269 → 237 µs without PDL)
+  if (c->esize == 2) {
+    if (c->D == 128) decode_post_kernel<__nv_bfloat16, 128><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+    else decode_post_kernel<__nv_bfloat16, 64><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+  } else {
+    if (c->D == 128) decode_post_kernel<float, 128><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+    else decode_post_kernel<float, 64><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+  }
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
 }

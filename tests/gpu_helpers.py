@@ -93,15 +93,18 @@ class Pair:
         self.step += 1
         return q
 
-    def decode_both(self, check=True, score=True):
+    def decode_both(self, check=True, score=True, fused=False):
         nA = len(self.tree.active)
         q = self.queries(nA)
         qd = q.cuda()
         out = torch.empty_like(qd)
         lse = torch.empty((nA, self.ctx.L, self.ctx.Hq), dtype=torch.float32, device="cuda")
-        self.ctx.arbor_tree_decode_attn(self.tree, qd, out, lse)
-        if score:
-            self.ctx.arbor_score(self.tree, qd, lse)
+        if fused and score:      # f2: arbor_decode_step (attention + merged score launch)
+            self.ctx.arbor_decode_step(self.tree, qd, out, lse)
+        else:
+            self.ctx.arbor_tree_decode_attn(self.tree, qd, out, lse)
+            if score:
+                self.ctx.arbor_score(self.tree, qd, lse)
         qn = q.double().numpy()
         o_ref, lse_ref = self.orc.decode(self.tree, qn)
         if score:
@@ -111,12 +114,12 @@ class Pair:
             assert_close(lse.cpu().numpy(), lse_ref, self.rtol, "LSE")
         return out, lse
 
-    def warmup(self, steps_per_leaf=4, check=False):
+    def warmup(self, steps_per_leaf=4, check=False, fused=False):
         saved = list(self.tree.active)
         for leaf in workload.leaf_cycle_order(self.tree, self.seed):
             self.tree.active = [leaf]
             for _ in range(steps_per_leaf):
-                self.decode_both(check=check)
+                self.decode_both(check=check, fused=fused)
         self.tree.active = saved
 
     # ------------------------------------------------------------ device reads
