@@ -244,7 +244,11 @@ struct HostPlan {
   std::vector<std::vector<int32_t>> paths;
 };
 
-void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan &p) {
+// tile_pairs: the tensor-core attention leaves one partial per (tile = chunks ch, ch+1 of a
+// node, leaf), stored at the even chunk's pair — the merge lists then hold even chunks only;
+// the CUDA-core kernel leaves one partial per chunk.
+void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan &p,
+                bool tile_pairs) {
   const int N = t->num_nodes, nA = t->num_active;
   std::vector<std::vector<int32_t>> leaves(N);
   p.paths.assign(nA, {});
@@ -293,7 +297,8 @@ void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan 
       const int nch = (n_of[x] + kAttnChunk - 1) / kAttnChunk;
       const int pos = static_cast<int>(std::lower_bound(leaves[x].begin(), leaves[x].end(), b) -
                                        leaves[x].begin());
-      for (int ch = 0; ch < nch; ++ch) p.bp_list.push_back(p.ch_poff[chunk_of[x] + ch] + pos);
+      for (int ch = 0; ch < nch; ch += tile_pairs ? 2 : 1)
+        p.bp_list.push_back(p.ch_poff[chunk_of[x] + ch] + pos);
     }
     p.bp_off.push_back(static_cast<int32_t>(p.bp_list.size()));
   }
@@ -575,6 +580,7 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    c->num_sms = sms;
     ALLOC(d.work, static_cast<size_t>(sms) * kEvictCtasPerSm * MN);
   }
   {
@@ -766,8 +772,12 @@ static void score_bookkeeping(arbor_ctx *c, const arbor_tree *tree, const HostPl
 }
 
 // node-wise split of each row over CTAs: about two recomputed nodes per CTA, ≤ 8 per row
+// (a power of two: CTA (row, p) owns the nodes with id & (parts − 1) == p)
 static int score_parts(size_t mass_nodes) {
-  return std::max(1, std::min(8, static_cast<int>(mass_nodes) / 2));
+  const int want = std::max(1, std::min(8, static_cast<int>(mass_nodes) / 2));
+  int p = 1;
+  while (p * 2 <= want) p *= 2;
+  return p;
 }
 
 // a10 + MSVE on several ranks: the all-reduce sits between the partial masses and the score
@@ -790,7 +800,7 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
   const int N = tree->num_nodes, nA = tree->num_active;
   TRY(upload_tree(c, tree));
   HostPlan hp;
-  build_plan(tree, c->h_n, hp);
+  build_plan(tree, c->h_n, hp, c->tc_ok);
   std::vector<int32_t> mass_nodes;
   score_bookkeeping(c, tree, hp, mass_nodes);
   PlanView pv{};
@@ -842,7 +852,7 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
   }
   TRY(upload_tree(c, tree));
   HostPlan hp;
-  build_plan(tree, c->h_n, hp);
+  build_plan(tree, c->h_n, hp, c->tc_ok);
   std::vector<int32_t> mass_nodes;
   score_bookkeeping(c, tree, hp, mass_nodes);
   PlanView pv{};
@@ -852,8 +862,12 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
   launch_attn_partial(c, pv, q, 0, c->L, hp.max_cnt, out, lse_out);
   CK_LAUNCH();
   const bool single = c->cfg.world_size == 1;
+  // parts per row: no more CTAs than one resident wave (3 per SM at the kernel's bounds)
+  int parts = score_parts(mass_nodes.size());
+  while (parts > 1 && c->L * c->H * parts > 3 * c->num_sms) parts /= 2;
+  if (const char *e = getenv("ARBOR_POST_PARTS")) parts = atoi(e);   // diagnostics
   launch_decode_post(c, pv, out, lse_out, d_mass_nodes, static_cast<int>(mass_nodes.size()), N,
-                     single, s_out, score_parts(mass_nodes.size()));
+                     single, s_out, parts);
   CK_LAUNCH();
   c->lg_epoch = -1;
   c->mass_valid = true;
@@ -1029,7 +1043,7 @@ arbor_status arbor_tree_decode_attn(arbor_ctx *c, const arbor_tree *tree, int32_
     return fail(c, ARBOR_ERR_INVALID_ARG, "layer range outside the shard");
   TRY(upload_tree(c, tree));
   HostPlan hp;
-  build_plan(tree, c->h_n, hp);
+  build_plan(tree, c->h_n, hp, c->tc_ok);
   PlanView pv{};
   TRY(upload_plan(c, hp, tree->num_active, false, nullptr, pv, nullptr));
   TRY(run_attention(c, hp, pv, layer_begin, layer_count, q, out, lse_out));

@@ -26,8 +26,11 @@
 //   K tile  [2 d-halves][128 rows][64]   A of MMA1, K-major,  SBO 1024
 //   Q tile  [2 d-halves][NQ rows][64]    B of MMA1, K-major,  SBO 1024
 //   V tile  [2 d-halves][128 rows][64]   A of MMA2 = Vᵀ, MN-major, LBO 16 KB (d-halves), SBO 1024
-//   P tile  [2 slot-halves][2NQ][64]     B of MMA2 = Pᵀ, K-major: rows [h·NQ, h·NQ+NQ) of slot half
-//                                        h hold chunk h's probabilities, the other rows are zero.
+//   P tile  [2 slot-halves][NQ][64]      B of MMA2 = Pᵀ, K-major: one softmax over all 128 slots
+//                                        of the tile (both chunks), so MMA2 is 128 × NQ × 128 and
+//                                        the tile leaves ONE partial (o, m, l) per query, stored
+//                                        at its first chunk's pair (the plan's merge lists hold
+//                                        the even chunks only, build_plan(tile_pairs)).
 // Numerics: K, V, q are bf16 (exact products, fp32 accumulation); P is rounded to bf16 for the
 // PV product (relative error ≤ 2^-9 per weight, inside the bf16 tolerance 2e-2); m and l are the
 // fp32 column max and the fp32 sum of the unrounded exp2 values.
@@ -293,16 +296,17 @@ __device__ __forceinline__ unsigned long long colmask(int cnt, int G) {
   return slot * (0x0101010101010101ull & ((1ull << (8 * cnt)) - 1ull));
 }
 
+// two buffers of [S: NQ cols | Oᵀ: NQ cols]
 template <int NQ>
 constexpr int tmem_cols() {
-  return 6 * NQ <= 32 ? 32 : 6 * NQ <= 64 ? 64 : 6 * NQ <= 128 ? 128 : 6 * NQ <= 256 ? 256 : 512;
+  return 4 * NQ <= 32 ? 32 : 4 * NQ <= 64 ? 64 : 4 * NQ <= 128 ? 128 : 4 * NQ <= 256 ? 256 : 512;
 }
 
 template <int NQ, int NST>
 struct TcSmem {
   static constexpr uint32_t kQ = NQ * 256;                    // Q tile bytes
   static constexpr uint32_t kStage = 2 * kKVBytes + kQ;       // K | V | Q
-  static constexpr uint32_t kP = 2 * NQ * 256;                // P tile bytes (2NQ rows × 128 slots)
+  static constexpr uint32_t kP = NQ * 256;                    // P tile bytes (NQ rows × 128 slots)
   static constexpr uint32_t kBytes = NST * kStage + 2 * kP;
   static constexpr uint32_t kAlloc = kBytes + 1024;           // + alignment slack
 };
@@ -488,7 +492,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     // ------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t id1 = bf16_idesc(128, NQ, 0, 0);       // S = K · Qᵀ
-      constexpr uint32_t id2 = bf16_idesc(128, 2 * NQ, 1, 0);   // Oᵀ = Vᵀ · Pᵀ
+      constexpr uint32_t id2 = bf16_idesc(128, NQ, 1, 0);       // Oᵀ = Vᵀ · Pᵀ
       // Two independent streams of work, issued as soon as each is ready (non-blocking
       // polls): MMA1(j) needs tile j's stage (full) and S buffer j&1 drained (s_empty of
       // j−2); MMA2(j) needs P(j) (p_full) and Oᵀ buffer j&1 drained (o_empty of j−2).
@@ -505,7 +509,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t ad = sw128_desc(ks + (kk >> 2) * 16384u + (kk & 3) * 32u, 16, 1024);
             const uint64_t bd = sw128_desc(qs + (kk >> 2) * (NQ * 128u) + (kk & 3) * 32u, 16, 1024);
-            tc_mma(tmem + b * 3 * NQ, ad, bd, id1, kk > 0);
+            tc_mma(tmem + b * 2 * NQ, ad, bd, id1, kk > 0);
           }
           tc_commit(&s_full[b]);
           if (a.trace) { mbar_wait(&s_full[b], (js >> 1) & 1u); TC_TRACE(js, 12); }
@@ -521,8 +525,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t ad = sw128_desc(vs + kk * 2048u, 16384, 1024);
-            const uint64_t bd = sw128_desc(ps + (kk >> 2) * (2 * NQ * 128u) + (kk & 3) * 32u, 16, 1024);
-            tc_mma(tmem + b * 3 * NQ + NQ, ad, bd, id2, kk > 0);
+            const uint64_t bd = sw128_desc(ps + (kk >> 2) * (NQ * 128u) + (kk & 3) * 32u, 16, 1024);
+            tc_mma(tmem + b * 2 * NQ + NQ, ad, bd, id2, kk > 0);
           }
           tc_commit(&o_full[b]);
           tc_commit(&empty[s]);
@@ -539,11 +543,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     // cache whatever NQ is (a fully unrolled NQ = 48 body thrashed it).
     // Two warpgroups alternate over the tiles (group g takes k ≡ g mod 2, i.e. TMEM and P
     // buffer g): one tile's latency-bound softmax chain overlaps the next one's.
+    // One column max / sum over the whole 128-slot tile (both chunks): the four warps of the
+    // group combine their warp results through smem behind one 128-thread named barrier.
     constexpr int GW = kW<NQ>;
     const int grp = warp >= 10 ? 1 : 0;
     const int quad = warp & 3;                 // TMEM lane quadrant of this warp
     const int half = quad >> 1;                // slot half (chunk A or B) of this thread
-    const int bar_id = 1 + 2 * grp + half;     // named barrier of this group's half
+    const int bar_id = 1 + grp;                // named barrier of this group (128 threads)
     const int trow = quad * 32 + lane;         // tile row (slot)
     const int tc = trow & (kHalf - 1);         // slot within the chunk
     const int G = a.G;
@@ -568,34 +574,35 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       tc_fence_after();
       // P buffer b was last read by MMA2(k−2)
       if (k >= 2) mbar_wait(&o_full[b], ((k - 2) >> 1) & 1u);
-      // P (bf16) goes to rows [half·NQ, half·NQ + NQ) of slot-half `half` of the Pᵀ tile;
-      // rows of columns past the tile's own keep stale values: they only feed output columns
-      // that are never stored (Oᵀ column n depends on Pᵀ row n alone)
-      unsigned char *Pt = Pbuf + b * S::kP + half * (2 * NQ * 128);
+      // P (bf16) goes to row n of slot-half `half` of the Pᵀ tile; rows of columns past the
+      // tile's own keep stale values: they only feed output columns that are never stored
+      // (Oᵀ column n depends on Pᵀ row n alone)
+      unsigned char *Pt = Pbuf + b * S::kP + half * (NQ * 128);
       float *zr = a.zbuf + ((static_cast<int64_t>(pb) * a.Lc + hd.li) * a.g.H + hd.h) * G * kAttnChunk + tc;
 #pragma unroll 1
       for (int gi = 0; gi < ngrp; ++gi) {
         const int c = gi * GW;
         float z[GW], p[GW];
-        tmem_ldW<GW>(tmem + lane_addr + b * 3 * NQ + c, z);
+        tmem_ldW<GW>(tmem + lane_addr + b * 2 * NQ + c, z);
 #pragma unroll
         for (int i = 0; i < GW; ++i)
           z[i] = (valid && ((cm >> (c + i)) & 1ull)) ? z[i] * a.scale_log2 : -INFINITY;
-        // column max and sum over the 64 slots of this half: butterfly transpose-reduce in
-        // the warp, then the half's two warps combine through smem (ring of 4 tiles)
+        // column max and sum over the 128 slots: butterfly transpose-reduce in the warp, then
+        // the group's four warps combine through smem (ring of 4 tiles)
         const float mw = warp_reduceW<GW, true>(z, lane);
         if (!(lane & 1)) red_m[k & 3][quad][c + myc] = mw;
-        named_bar_sync(bar_id, 64);
+        named_bar_sync(bar_id, 128);
 #pragma unroll
         for (int i = 0; i < GW; ++i) {
-          const float m = fmaxf(red_m[k & 3][half * 2][c + i], red_m[k & 3][half * 2 + 1][c + i]);
+          const float m = fmaxf(fmaxf(red_m[k & 3][0][c + i], red_m[k & 3][1][c + i]),
+                                fmaxf(red_m[k & 3][2][c + i], red_m[k & 3][3][c + i]));
           p[i] = z[i] == -INFINITY ? 0.f : fast_exp2(z[i] - m);   // m = −inf only if all masked
         }
         const float lw = warp_reduceW<GW, false>(p, lane);
         if (!(lane & 1)) red_l[k & 3][quad][c + myc] = lw;
 #pragma unroll
         for (int i = 0; i < GW; ++i) {
-          const int r = half * NQ + c + i;
+          const int r = c + i;
           *reinterpret_cast<__nv_bfloat16 *>(Pt + r * 128 + ((((cb >> 4) ^ (r & 7))) << 4) + (cb & 15)) =
               __float2bfloat16_rn(p[i]);
         }
@@ -622,13 +629,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         }
       }
       fence_proxy_async();
-      named_bar_sync(bar_id, 64);
+      named_bar_sync(bar_id, 128);
       mbar_arrive(&p_full[b]);
       if (tid == 64) TC_TRACE(k, 9);
     }
   } else {
     // ------------------------------------------------------------- epilogue (warps 6..9)
-    // Oᵀ[d][half·NQ + n] (TMEM lane = d) → partials[pair][li][h][g][d], in GW-column groups
+    // Oᵀ[d][n] (TMEM lane = d) → partials[pair A][li][h][g][d], in GW-column groups; the
+    // tile's (m, l) per column after the four quadrants' max / sums
     constexpr int GW = kW<NQ>;
     const int quad = warp & 3;
     const int trow = quad * 32 + lane;
@@ -642,40 +650,32 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       if (tid == 192) TC_TRACE(k, 10);
       tc_fence_after();
       const TcHdr hd = ohdr[k & 3];   // read before o_empty: softmax(k+4) rewrites this slot
-      // m (log2 domain) and l of column idx = half·NQ + n, from the softmax ring slot k&3
+      // m (log2 domain) and l of column n = etid, from the softmax ring slot k&3
       float mm = 0.f, ll = 0.f;
-      const int hh = etid / NQ, cn = etid - hh * NQ;
-      if (etid < 2 * NQ) {
-        mm = fmaxf(red_m[k & 3][hh * 2][cn], red_m[k & 3][hh * 2 + 1][cn]);
-        ll = red_l[k & 3][hh * 2][cn] + red_l[k & 3][hh * 2 + 1][cn];
+      if (etid < NQ) {
+        mm = fmaxf(fmaxf(red_m[k & 3][0][etid], red_m[k & 3][1][etid]),
+                   fmaxf(red_m[k & 3][2][etid], red_m[k & 3][3][etid]));
+        ll = (red_l[k & 3][0][etid] + red_l[k & 3][1][etid]) +
+             (red_l[k & 3][2][etid] + red_l[k & 3][3][etid]);
       }
       const int ngrp = (min(NQ, 8 * hd.cnt) + GW - 1) / GW;
       const unsigned long long cm = colmask(hd.cnt, G);
       float *pa = a.partials + ((static_cast<int64_t>(hd.pbA) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
-      float *pbp = a.partials + ((static_cast<int64_t>(hd.pbB) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
 #pragma unroll 1
       for (int gi = 0; gi < ngrp; ++gi) {
         const int c = gi * GW;
         float o[GW];
-        tmem_ldW<GW>(tmem + lane_addr + b * 3 * NQ + NQ + c, o);
+        tmem_ldW<GW>(tmem + lane_addr + b * 2 * NQ + NQ + c, o);
 #pragma unroll
         for (int i = 0; i < GW; ++i) {
           const int n = c + i;
           if ((cm >> n) & 1ull) pa[static_cast<int64_t>((n >> 3) * SP + (n & 7)) * 130] = o[i];
         }
-        if (hd.hasB) {
-          tmem_ldW<GW>(tmem + lane_addr + b * 3 * NQ + 2 * NQ + c, o);
-#pragma unroll
-          for (int i = 0; i < GW; ++i) {
-            const int n = c + i;
-            if ((cm >> n) & 1ull) pbp[static_cast<int64_t>((n >> 3) * SP + (n & 7)) * 130] = o[i];
-          }
-        }
       }
       tc_fence_before();
       mbar_arrive(&o_empty[b]);
-      if (etid < 2 * NQ && ((cm >> cn) & 1ull) && (hh == 0 || hd.hasB)) {
-        float *dst = (hh ? pbp : pa) - trow + static_cast<int64_t>((cn >> 3) * SP + (cn & 7)) * 130;
+      if (etid < NQ && ((cm >> etid) & 1ull)) {
+        float *dst = pa - trow + static_cast<int64_t>((etid >> 3) * SP + (etid & 7)) * 130;
         dst[128] = mm;
         dst[129] = ll;
       }

@@ -190,6 +190,7 @@ struct arbor_ctx {
   long long tmap_q_rows[arbor::kQMaps] = {};
   int tmap_q_next = 0, tmap_q_cur = 0;
   bool tc_ok = false;
+  int num_sms = 148;               // multiprocessors of the context's device
   std::string err;
 };
 
@@ -204,7 +205,8 @@ void launch_score_apply(arbor_ctx *c, const PlanView &pv, const float *lse, int 
 void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64_t *out,
                       int out_stride);
 void launch_msve(arbor_ctx *c, int N, float *s_out);
-// nparts CTAs per (layer, KV head) row; CTA (row, p) owns the nodes with id % nparts == p
+// nparts (a power of two) CTAs per (layer, KV head) row; CTA (row, p) owns the nodes with
+// id & (nparts − 1) == p
 void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
                         int num_nodes, int N, bool do_msve, float *s_out, int nparts);
 // f2 (arbor_decode_step): merge of the attention partials (out, LSE) + the fused score of

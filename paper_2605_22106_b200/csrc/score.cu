@@ -203,7 +203,7 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   const int warp = tid >> 5, lane = tid & 31;
   for (int c = warp; c < a.pv.C; c += kFusedThreads / 32) {   // warp per owned chunk
     const int node = a.pv.ch_node[c];
-    if (node % nparts != part) continue;
+    if ((node & (nparts - 1)) != part) continue;   // nparts: a power of two
     const int c0 = a.pv.ch_chunk[c] * kAttnChunk;
     const int kc = a.kcur[node];
     const int nt = max(0, min(kAttnChunk, kc - c0));
@@ -214,10 +214,39 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
     for (int t = lane; t < nt; t += 32) {
       const int slot = c0 + t;
       const int pos = ident ? slot : a.pos[pool_row(a.g, li, pl[slot / a.g.P], h, slot % a.g.P)];
+      // Σ over pairs (ascending) and query heads (ascending); four pairs' logits and LSEs
+      // are loaded before any is used (the sum order is unchanged)
       float psum = 0.f;
-      for (int p = p0; p < p0 + pc; ++p) {
+      const int pe = p0 + pc;
+      int p = p0;
+      auto zrow = [&](int pp) {
+        return a.zbuf + (((static_cast<int64_t>(pp) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + t;
+      };
+      if (a.G <= 4) {
+        for (; p + 4 <= pe; p += 4) {
+          float zz[4][4], ll[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int b = a.pv.pair_b[p + u];
+            const float *z = zrow(p + u);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              if (g < a.G) {
+                zz[u][g] = z[g * kAttnChunk];
+                ll[u][g] = lse2(b, g);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              if (g < a.G) psum += exp2f(zz[u][g] - ll[u][g]);
+        }
+      }
+      for (; p < pe; ++p) {
         const int b = a.pv.pair_b[p];
-        const float *z = a.zbuf + (((static_cast<int64_t>(p) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + t;
+        const float *z = zrow(p);
         for (int g0 = 0; g0 < a.G; g0 += 8) {
           float zz[8], ll[8];
 #pragma unroll
@@ -243,7 +272,7 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   const float *Arow = a.A + (static_cast<int64_t>(li) * f.H + h) * f.max_tokens;
   for (int mi = warp; mi < f.n_mass; mi += kFusedThreads / 32) {
     const int node = f.mass_nodes[mi];
-    if (node % nparts != part) continue;
+    if ((node & (nparts - 1)) != part) continue;   // nparts: a power of two
     const int n = f.nlen[node];
     const float *r = Arow + a.span[node];
     double m = 0.0;
@@ -309,8 +338,8 @@ struct PostArgs {
 };
 constexpr int kPostItems = 512;   // nA · G ≤ kPostItems (host-checked)
 
-template <typename T, int D>
-__global__ void __launch_bounds__(kFusedThreads)
+template <typename T, int D, int MINB>
+__global__ void __launch_bounds__(kFusedThreads, MINB)
 decode_post_kernel(PostArgs pa) {
   pdl_trigger();   // launched without PDL (launch_decode_post); lets the next kernel overlap
   const FusedArgs &f = pa.f;
@@ -320,67 +349,90 @@ decode_post_kernel(PostArgs pa) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = kFusedThreads / 32, EPL = D / 32;
   const int G = a.G;
-  __shared__ float lse2s[kPostItems];
+  __shared__ float lse2s[kPostItems], Ms[kPostItems], invL[kPostItems];
   auto part_ptr = [&](int p, int g) -> const float * {
     return pa.partials + (((static_cast<int64_t>(p) * a.Lc + li) * f.H + h) * G + g) * (D + 2);
   };
-  for (int it = warp; it < pa.nA * G; it += NW) {
+  const int nitems = pa.nA * G;
+  // (a) eight lanes per (b, g): each lane folds every 8th pair of the leaf's path online
+  // (M, L), the group combines them: M = max m, L = Σ 2^(m−M) l → LSE₂ = M + log2 L
+  {
+    const int sub = lane & 7;
+    for (int it0 = (threadIdx.x >> 3); it0 < ((nitems + 3) & ~3); it0 += kFusedThreads / 8) {
+      const int it = it0;
+      const bool ok = it < nitems;
+      const int b = ok ? it / G : 0, g = ok ? it - b * G : 0;
+      const int p0 = ok ? a.pv.bp_off[b] : 0, p1 = ok ? a.pv.bp_off[b + 1] : 0;
+      float M = -INFINITY, Ls = 0.f;
+      for (int i = p0 + sub; i < p1; i += 8) {
+        const float *pp = part_ptr(a.pv.bp_list[i], g);
+        const float m2 = pp[D], l2 = pp[D + 1];
+        if (m2 == -INFINITY) continue;
+        if (m2 > M) {
+          Ls = Ls * exp2f(M - m2) + l2;   // exp2(−inf) = 0 on the first pair
+          M = m2;
+        } else {
+          Ls = fmaf(exp2f(m2 - M), l2, Ls);
+        }
+      }
+#pragma unroll
+      for (int o = 4; o; o >>= 1) {
+        const float Mo = __shfl_xor_sync(0xffffffffu, M, o);
+        const float Lo = __shfl_xor_sync(0xffffffffu, Ls, o);
+        const float Mn = fmaxf(M, Mo);
+        Ls = (Mn == -INFINITY) ? 0.f
+             : (M == -INFINITY ? 0.f : Ls * exp2f(M - Mn)) + (Mo == -INFINITY ? 0.f : Lo * exp2f(Mo - Mn));
+        M = Mn;
+      }
+      if (ok && sub == 0) {
+        lse2s[it] = Ls > 0.f ? M + log2f(Ls) : -INFINITY;
+        Ms[it] = M;
+        invL[it] = Ls > 0.f ? 1.f / Ls : 0.f;
+        if ((it & (nparts - 1)) == part && pa.lse_out)
+          pa.lse_out[(static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * G + g] =
+              Ls > 0.f ? (M + log2f(Ls)) * 0.6931471805599453f : -INFINITY;
+      }
+    }
+  }
+  __syncthreads();
+  // (b) owned items, warp per item: lane j holds pair p0 + j's index and weight 2^(m−M);
+  // then, pairs in path order, lanes over d: o = Σ w o_p / L
+  for (int it = part + warp * nparts; it < nitems; it += NW * nparts) {
     const int b = it / G, g = it - b * G;
     const int p0 = a.pv.bp_off[b], p1 = a.pv.bp_off[b + 1];
-    float M = -INFINITY;
-    for (int i = p0 + lane; i < p1; i += 32) M = fmaxf(M, part_ptr(a.pv.bp_list[i], g)[D]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    const bool own = it % nparts == part;
-    float Ls = 0.f;
+    const float M = Ms[it];
     float acc[EPL];
 #pragma unroll
     for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
     if (M != -INFINITY) {
       for (int i0 = p0; i0 < p1; i0 += 32) {
-        const int i = i0 + lane;
         int pi = 0;
         float w = 0.f;
-        if (i < p1) {
-          pi = a.pv.bp_list[i];
-          const float *pp = part_ptr(pi, g);
-          const float m2 = pp[D];
-          if (m2 != -INFINITY) {
-            w = exp2f(m2 - M);
-            Ls = fmaf(w, pp[D + 1], Ls);
-          }
+        if (i0 + lane < p1) {
+          pi = a.pv.bp_list[i0 + lane];
+          const float m2 = part_ptr(pi, g)[D];
+          w = m2 == -INFINITY ? 0.f : exp2f(m2 - M);
         }
-        if (own) {
-          const int cnt = min(32, p1 - i0);
-#pragma unroll 4
-          for (int j = 0; j < cnt; ++j) {
-            const float wj = __shfl_sync(0xffffffffu, w, j);
-            const int pj = __shfl_sync(0xffffffffu, pi, j);
-            const float *pp = part_ptr(pj, g);
-            float v[EPL];
+        const int cnt = min(32, p1 - i0);
+#pragma unroll 8
+        for (int j = 0; j < cnt; ++j) {
+          const float wj = __shfl_sync(0xffffffffu, w, j);
+          const int pj = __shfl_sync(0xffffffffu, pi, j);
+          const float *pp = part_ptr(pj, g);
+          float v[EPL];
 #pragma unroll
-            for (int e = 0; e < EPL; ++e) v[e] = pp[lane + 32 * e];
-            if (wj != 0.f) {
+          for (int e = 0; e < EPL; ++e) v[e] = pp[lane + 32 * e];
+          if (wj != 0.f) {
 #pragma unroll
-              for (int e = 0; e < EPL; ++e) acc[e] = fmaf(wj, v[e], acc[e]);
-            }
+            for (int e = 0; e < EPL; ++e) acc[e] = fmaf(wj, v[e], acc[e]);
           }
         }
       }
     }
+    T *out = static_cast<T *>(pa.out) + ((static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * G + g) * D;
+    const float inv = invL[it];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
-    const float l2 = Ls > 0.f ? M + log2f(Ls) : -INFINITY;
-    if (lane == 0) lse2s[it] = l2;
-    if (own) {
-      const int gq = h * G + g;
-      T *out = static_cast<T *>(pa.out) + ((static_cast<int64_t>(b) * a.Lc + li) * a.Hq + gq) * D;
-      const float inv = Ls > 0.f ? 1.f / Ls : 0.f;
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) out[lane + 32 * e] = ElemT<T>::from_f(acc[e] * inv);
-      if (lane == 0 && pa.lse_out)
-        pa.lse_out[(static_cast<int64_t>(b) * a.Lc + li) * a.Hq + gq] = l2 * 0.6931471805599453f;
-    }
+    for (int e = 0; e < EPL; ++e) out[lane + 32 * e] = ElemT<T>::from_f(acc[e] * inv);
   }
   __syncthreads();
   score_row(f, li, h, part, nparts, [&](int b, int g) { return lse2s[b * G + g]; });
@@ -463,11 +515,11 @@ void launch_decode_post(arbor_ctx *c, const PlanView &pv, void *out, float *lse_
   // A plain launch, not PDL: 2·(rows) CTAs of 256 threads made resident early next to the
   // attention kernel's CTAs slowed that kernel (measured: C2 step 269 → 237 µs without PDL)
   if (c->esize == 2) {
-    if (c->D == 128) decode_post_kernel<__nv_bfloat16, 128><<<grid, kFusedThreads, 0, c->ms>>>(pa);
-    else decode_post_kernel<__nv_bfloat16, 64><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+    if (c->D == 128) decode_post_kernel<__nv_bfloat16, 128, 3><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+    else decode_post_kernel<__nv_bfloat16, 64, 3><<<grid, kFusedThreads, 0, c->ms>>>(pa);
   } else {
-    if (c->D == 128) decode_post_kernel<float, 128><<<grid, kFusedThreads, 0, c->ms>>>(pa);
-    else decode_post_kernel<float, 64><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+    if (c->D == 128) decode_post_kernel<float, 128, 3><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+    else decode_post_kernel<float, 64, 3><<<grid, kFusedThreads, 0, c->ms>>>(pa);
   }
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);

@@ -1,0 +1,53 @@
+"""Decode-step driver for ncu / timing: N arbor_decode_step calls on a preset (c2: 1 leaf,
+c3: 16 DPTS leaves on the same 8B-shaped tree), full retention, device-resident inputs.
+
+    python profiles/decode_step_prof.py c3 [steps]        # prints per-call CUDA-event µs
+    ncu -k regex:"attn_tc|decode_post" ... python profiles/decode_step_prof.py c3 3
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    from paper_2605_22106_b200 import workload
+
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    sc = workload.setup(cfg, 0, profile=True)
+    ctx, tree = sc.ctx, sc.tree
+    nA = len(tree.active)
+    qs = [sc.queries(i, nA) for i in range(2)]
+    out = torch.empty_like(qs[0])
+    lse = torch.empty((nA, ctx.L, ctx.Hq), dtype=torch.float32, device=qs[0].device)
+    s = torch.empty(tree.num_nodes, dtype=torch.float32, device=qs[0].device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=qs[0].device)
+    for i in range(3):
+        ctx.arbor_decode_step(tree, qs[i % 2], out, lse, s)
+    torch.cuda.synchronize()
+    ctx.arbor_set_profiling(True)
+    ctx.arbor_reset_stage_times()
+    ts = []
+    for i in range(steps):
+        flush.zero_()                                   # L2 flush between steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.arbor_decode_step(tree, qs[i % 2], out, lse, s)
+        e1.record()
+        ts.append((e0, e1))
+    torch.cuda.synchronize()
+    st = ctx.arbor_stage_times()
+    ctx.arbor_set_profiling(False)
+    us = sorted(a.elapsed_time(b) * 1e3 for a, b in ts)
+    print(json.dumps({"config": cfg, "active_leaves": nA, "decode_step_us_p50": us[len(us) // 2],
+                      "stage_us": {k: round(v * 1e3, 2) for k, v in st.items() if v}}))
+
+
+if __name__ == "__main__":
+    main()
