@@ -239,7 +239,7 @@ arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
 // ---------------------------------------------------------------- attention / score plan
 struct HostPlan {
   std::vector<int32_t> ch_node, ch_chunk, ch_poff, ch_pcnt, it_rec, pair_b, bp_off, bp_list;
-  std::vector<int32_t> tl_rec;   // tensor-core tiles: {item A, item B or -1, 0, 0}
+  std::vector<int32_t> tl_rec;   // tensor-core tiles: kTileRecInts ints each (build_plan)
   int max_cnt = 0;               // most leaves in one item
   std::vector<std::vector<int32_t>> paths;
 };
@@ -266,15 +266,7 @@ void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan 
     chunk_of[x] = static_cast<int32_t>(p.ch_node.size());
     const int lc = static_cast<int>(leaves[x].size());
     const int ng = (lc + kLeavesPerItem - 1) / kLeavesPerItem;
-    const int first_item = static_cast<int>(p.it_rec.size() / 4);
     p.max_cnt = std::max(p.max_cnt, std::min(kLeavesPerItem, lc));
-    for (int ch = 0; ch < nch; ch += 2)    // a tile = chunks (ch, ch+1) of one leaf group
-      for (int gi = 0; gi < ng; ++gi) {
-        p.tl_rec.push_back(first_item + ch * ng + gi);
-        p.tl_rec.push_back(ch + 1 < nch ? first_item + (ch + 1) * ng + gi : -1);
-        p.tl_rec.push_back(0);
-        p.tl_rec.push_back(0);
-      }
     for (int ch = 0; ch < nch; ++ch) {
       const int c = static_cast<int>(p.ch_node.size());
       p.ch_node.push_back(x);
@@ -289,6 +281,20 @@ void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan 
         p.it_rec.push_back(std::min(kLeavesPerItem, lc - j0));
       }
     }
+    // tensor-core tiles: chunks (ch, ch+1) of one leaf group, one self-contained record each
+    // {node, c0, pair A, pair B or -1, cnt, leaf 0..5, 0} (one load per tile in the kernel)
+    const int cfirst = chunk_of[x];
+    for (int ch = 0; ch < nch; ch += 2)
+      for (int gi = 0; gi < ng; ++gi) {
+        const int j0 = gi * kLeavesPerItem, cnt = std::min(kLeavesPerItem, lc - j0);
+        p.tl_rec.push_back(x);
+        p.tl_rec.push_back(ch * kAttnChunk);
+        p.tl_rec.push_back(p.ch_poff[cfirst + ch] + j0);
+        p.tl_rec.push_back(ch + 1 < nch ? p.ch_poff[cfirst + ch + 1] + j0 : -1);
+        p.tl_rec.push_back(cnt);
+        for (int j = 0; j < kLeavesPerItem; ++j) p.tl_rec.push_back(j < cnt ? leaves[x][j0 + j] : 0);
+        p.tl_rec.push_back(0);
+      }
   }
   p.bp_off.assign(1, 0);
   for (int b = 0; b < nA; ++b) {
@@ -335,7 +341,7 @@ arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
   pv.ch_pcnt = base + o_cpc;
   pv.it_rec = reinterpret_cast<const int4 *>(base + o_ir);
   pv.tl_rec = reinterpret_cast<const int4 *>(base + o_tl);
-  pv.T = static_cast<int>(p.tl_rec.size() / 4);
+  pv.T = static_cast<int>(p.tl_rec.size() / kTileRecInts);
   pv.pair_b = base + o_pb;
   pv.bp_off = base + o_bpo;
   pv.bp_list = base + o_bpl;

@@ -321,9 +321,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   unsigned char *sm = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   unsigned char *Pbuf = sm + NST * S::kStage;
-  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  // K (+ q rows) and V of a stage have their own barriers: K is free again once MMA1 has
+  // read it, V only after MMA2, so the next K loads go out ~1.5 µs earlier
+  __shared__ __align__(8) uint64_t full_k[NST], empty_k[NST], full_v[NST], empty_v[NST];
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], o_full[2], o_empty[2];
-  __shared__ TcHdr hdr[NST];
+  // per-tile header and page list, ring of 2·NST tiles (written at K issue; read by the V
+  // issue, the softmax and — via ohdr — the epilogue; slot k is rewritten by tile k + 2·NST,
+  // whose K issue needs MMA1(k + NST), i.e. softmax(k) done)
+  __shared__ TcHdr hdr[2 * NST];
+  __shared__ int vpage[2 * NST][kMaxTilePages];
   __shared__ TcHdr ohdr[4];                             // tile k's header for the epilogue warps
   // column max / sum of each warp quadrant, ring of 4 tiles (the epilogue warps read tile k's
   // before releasing Oᵀ buffer k&1, which softmax(k+4) needs first)
@@ -344,30 +350,35 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   const int P = a.g.P;
   const int lgP = 31 - __clz(P);
 
-  // ---- producer state (warp 0).  Everything the producer needs per tile — node, chunk,
-  // pair bases, leaf ids, k_cur and the page ids — is loaded lane-parallel for 32 tiles at a
-  // time (lane i: tile k0 + i) before any of those tiles' TMA traffic is in flight: a plain
-  // global load issued behind ~200 KB of in-flight TMA data per SM waits ~2 µs.
-  int b_c0 = 0, b_pbA = 0, b_pbB = -1, b_cnt = 0, b_ntA = 0, b_ntB = 0;
+  // ---- producer state (warp 0).  Everything the producer needs per tile is loaded
+  // lane-parallel for 32 tiles at a time (lane i: tile k0 + i) before any of those tiles'
+  // TMA traffic is in flight (a plain global load issued behind ~200 KB of in-flight TMA data
+  // per SM waits ~2 µs): the tile's self-contained record (node, chunk, pair bases, leaf
+  // ids — host-built, so it is read before griddepcontrol.wait), then k_cur and the page ids
+  // (written by earlier kernels, so after it).
+  int b_c0 = 0, b_pbA = 0, b_pbB = -1, b_cnt = 0, b_ntA = 0, b_ntB = 0, b_node = 0;
   int b_leaf[kLeavesPerItem];
   int b_page[kMaxTilePages];
-  auto load_batch = [&](int k0) {
+  auto load_rec = [&](int k0) {
     const int kk = k0 + lane;
     if (kk < ntiles) {
       const int it = blockIdx.x + kk * gridDim.x;
-      const int4 tr = a.pv.tl_rec[it / HL];
-      const int4 ra = a.pv.it_rec[tr.x];
-      b_pbB = tr.y >= 0 ? a.pv.it_rec[tr.y].z : -1;
-      const int node = ra.x;
-      b_c0 = ra.y; b_pbA = ra.z; b_cnt = ra.w;
-#pragma unroll
-      for (int i = 0; i < kLeavesPerItem; ++i) b_leaf[i] = i < b_cnt ? a.pv.pair_b[b_pbA + i] : 0;
-      const int kc = a.kcur[node];
+      const int4 *r = a.pv.tl_rec + static_cast<int64_t>(it / HL) * (kTileRecInts / 4);
+      const int4 r0 = r[0], r1 = r[1], r2 = r[2];
+      b_node = r0.x; b_c0 = r0.y; b_pbA = r0.z; b_pbB = r0.w;
+      b_cnt = r1.x; b_leaf[0] = r1.y; b_leaf[1] = r1.z; b_leaf[2] = r1.w;
+      b_leaf[3] = r2.x; b_leaf[4] = r2.y; b_leaf[5] = r2.z;
+    }
+  };
+  auto load_state = [&](int k0) {
+    const int kk = k0 + lane;
+    if (kk < ntiles) {
+      const int kc = a.kcur[b_node];
       b_ntA = max(0, min(kHalf, kc - b_c0));
       b_ntB = b_pbB >= 0 ? max(0, min(kHalf, kc - b_c0 - kHalf)) : 0;
       const int pgA = (b_ntA + P - 1) >> lgP, pgB = (b_ntB + P - 1) >> lgP;
       const int ppH = kHalf >> lgP;   // pages per 64-slot half
-      const int32_t *pt = a.ptab + static_cast<int64_t>(node) * a.g.MPN + (b_c0 >> lgP);
+      const int32_t *pt = a.ptab + static_cast<int64_t>(b_node) * a.g.MPN + (b_c0 >> lgP);
 #pragma unroll
       for (int i = 0; i < kMaxTilePages; ++i) {
         const int half = i >= ppH, pi = i - half * ppH;
@@ -375,6 +386,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       }
     }
   };
+  static_assert(kLeavesPerItem == 6, "tile record layout");
   if (warp != 0) {
     // zero V, Q and P once: MMA2 reads every V row (0·v must stay 0, so rows never loaded
     // must be finite) and the off-half rows of the Pᵀ tile are never written again
@@ -389,8 +401,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   }
   if (tid == 32) {
     for (int s = 0; s < NST; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&full_k[s], 1);
+      mbar_init(&empty_k[s], 1);
+      mbar_init(&full_v[s], 1);
+      mbar_init(&empty_v[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
@@ -406,6 +420,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
                      smem_u32(&tmem_base_sh)), "r"(tmem_cols<NQ>()));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk4)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv4)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
+    }
+    load_rec(0);   // host-built plan records: uploaded before this kernel was enqueued
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -415,78 +439,124 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA producer
+    // Two cursors: K (+ q rows) of tile kk_k goes out as soon as stage kk_k % NST's K buffer
+    // is free (MMA1 of tile kk_k − NST done), V of tile kk_v once its V buffer is (MMA2 done);
+    // K runs at most NST tiles ahead of V.  Non-blocking polls, lane 0's view broadcast.
     const int ppH = kHalf >> lgP;
-    for (int k = 0; k < ntiles; ++k) {
-      if ((k & 31) == 0) load_batch(k);
-      const int src = k & 31;
-      const int ntA = __shfl_sync(0xffffffffu, b_ntA, src);
-      const int ntB = __shfl_sync(0xffffffffu, b_ntB, src);
-      const int pbA = __shfl_sync(0xffffffffu, b_pbA, src);
-      const int pbB = __shfl_sync(0xffffffffu, b_pbB, src);
-      const int cnt = __shfl_sync(0xffffffffu, b_cnt, src);
-      int page = 0, leaf = 0;       // lane i < pages: page i of the tile; lane i < cnt: leaf i
-#pragma unroll
-      for (int i = 0; i < kMaxTilePages; ++i) {
-        const int v = __shfl_sync(0xffffffffu, b_page[i], src);
-        if (lane == i) page = v;
+    int kk_k = 0, kk_v = 0;
+    if (ntiles > 0) load_state(0);
+    while (kk_v < ntiles) {
+      bool go_k = false, go_v = false;
+      if (kk_k < ntiles && kk_k < kk_v + NST) {
+        const int sk = kk_k % NST;
+        go_k = __shfl_sync(0xffffffffu, mbar_test(&empty_k[sk], ((kk_k / NST) & 1u) ^ 1u) ? 1 : 0, 0) != 0;
       }
-#pragma unroll
-      for (int i = 0; i < kLeavesPerItem; ++i) {
-        const int v = __shfl_sync(0xffffffffu, b_leaf[i], src);
-        if (lane == i) leaf = v;
-      }
-      const int it = blockIdx.x + k * gridDim.x;
-      const int li = (it / a.g.H) % a.Lc, h = it % a.g.H;
-      const int pgA = (ntA + P - 1) >> lgP, pgB = (ntB + P - 1) >> lgP;
-      const int s = k % NST;
-      const uint32_t ph = (k / NST) & 1u;
-      if (lane == 0) TC_TRACE(k, 0);
-      mbar_wait(&empty[s], ph ^ 1u);
-      if (lane == 0) TC_TRACE(k, 1);
-      unsigned char *Ks = sm + s * S::kStage;
-      unsigned char *Vs = Ks + kKVBytes;
-      unsigned char *Qs = Vs + kKVBytes;
-      if (lane == 0) {
-        hdr[s] = TcHdr{ntA, ntB, li, h, pbA, pbB, cnt, pbB >= 0 ? 1 : 0};
-        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(pgA + pgB) * P * 512u +
-                                            static_cast<uint32_t>(cnt) * 2048u);
-      }
-      __syncwarp();
-      const int l = a.layer_begin + li;
-      const int half = lane >= ppH, pi = lane - half * ppH;
-      const int pgh = half ? pgB : pgA;
-      // a chunk whose pages are all present and consecutive (the usual case: pages are popped
-      // in order) is fetched with one 64-row box per (K|V, d-half) through the 5-D view of the
-      // pool; otherwise one 16-row box per page-head through the 2-D view
-      const int first = __shfl_sync(0xffffffffu, page, half * ppH);
-      const bool cons = lane >= 2 * ppH || pi >= pgh || page == first + pi;
-      const unsigned bal = __ballot_sync(0xffffffffu, cons);
-      const unsigned hmask = ((1u << ppH) - 1u) << (half * ppH);
-      const bool big = lane < 2 * ppH && pgh == ppH && (bal & hmask) == hmask;
-      if (big) {
-        if (pi == 0) {
-          const int lp = l * a.g.NP + page;
-          const uint32_t dst = static_cast<uint32_t>(half * kHalf) * 128u;
-          tma_load_5d(Ks + dst, &tmk4, 0, 0, 0, h, lp, &full[s]);
-          tma_load_5d(Ks + 16384 + dst, &tmk4, 0, 1, 0, h, lp, &full[s]);
-          tma_load_5d(Vs + dst, &tmv4, 0, 0, 0, h, lp, &full[s]);
-          tma_load_5d(Vs + 16384 + dst, &tmv4, 0, 1, 0, h, lp, &full[s]);
+      if (go_k) {
+        const int k = kk_k;
+        if ((k & 31) == 0 && k > 0) {
+          load_rec(k);
+          load_state(k);
         }
-      } else if (lane < 2 * ppH && pi < pgh) {
-        const int row = static_cast<int>(pool_row(a.g, l, page, h, 0));
-        const uint32_t dst = static_cast<uint32_t>(half * kHalf + pi * P) * 128u;
-        tma_load_2d(Ks + dst, &tmk, 0, row, &full[s]);
-        tma_load_2d(Ks + 16384 + dst, &tmk, 64, row, &full[s]);
-        tma_load_2d(Vs + dst, &tmv, 0, row, &full[s]);
-        tma_load_2d(Vs + 16384 + dst, &tmv, 64, row, &full[s]);
+        const int src = k & 31;
+        const int ntA = __shfl_sync(0xffffffffu, b_ntA, src);
+        const int ntB = __shfl_sync(0xffffffffu, b_ntB, src);
+        const int pbA = __shfl_sync(0xffffffffu, b_pbA, src);
+        const int pbB = __shfl_sync(0xffffffffu, b_pbB, src);
+        const int cnt = __shfl_sync(0xffffffffu, b_cnt, src);
+        int page = 0, leaf = 0;       // lane i < pages: page i of the tile; lane i < cnt: leaf i
+#pragma unroll
+        for (int i = 0; i < kMaxTilePages; ++i) {
+          const int v = __shfl_sync(0xffffffffu, b_page[i], src);
+          if (lane == i) page = v;
+        }
+#pragma unroll
+        for (int i = 0; i < kLeavesPerItem; ++i) {
+          const int v = __shfl_sync(0xffffffffu, b_leaf[i], src);
+          if (lane == i) leaf = v;
+        }
+        const int it = blockIdx.x + k * gridDim.x;
+        const int li = (it / a.g.H) % a.Lc, h = it % a.g.H;
+        const int pgA = (ntA + P - 1) >> lgP, pgB = (ntB + P - 1) >> lgP;
+        const int s = k % NST, r = k % (2 * NST);
+        if (lane == 0) { TC_TRACE(k, 0); TC_TRACE(k, 1); }
+        unsigned char *Ks = sm + s * S::kStage;
+        unsigned char *Qs = Ks + 2 * kKVBytes;
+        if (lane == 0) {
+          hdr[r] = TcHdr{ntA, ntB, li, h, pbA, pbB, cnt, pbB >= 0 ? 1 : 0};
+          mbar_arrive_expect_tx(&full_k[s], static_cast<uint32_t>(pgA + pgB) * P * 256u +
+                                                static_cast<uint32_t>(cnt) * 2048u);
+        }
+        if (lane < kMaxTilePages) vpage[r][lane] = page;
+        __syncwarp();
+        const int l = a.layer_begin + li;
+        const int half = lane >= ppH, pi = lane - half * ppH;
+        const int pgh = half ? pgB : pgA;
+        // a chunk whose pages are all present and consecutive (the usual case: pages are
+        // popped in order) is fetched with one 64-row box per d-half through the 5-D view of
+        // the pool; otherwise one 16-row box per page-head through the 2-D view
+        const int first = __shfl_sync(0xffffffffu, page, half * ppH);
+        const bool cons = lane >= 2 * ppH || pi >= pgh || page == first + pi;
+        const unsigned bal = __ballot_sync(0xffffffffu, cons);
+        const unsigned hmask = ((1u << ppH) - 1u) << (half * ppH);
+        const bool big = lane < 2 * ppH && pgh == ppH && (bal & hmask) == hmask;
+        if (big) {
+          if (pi == 0) {
+            const int lp = l * a.g.NP + page;
+            const uint32_t dst = static_cast<uint32_t>(half * kHalf) * 128u;
+            tma_load_5d(Ks + dst, &tmk4, 0, 0, 0, h, lp, &full_k[s]);
+            tma_load_5d(Ks + 16384 + dst, &tmk4, 0, 1, 0, h, lp, &full_k[s]);
+          }
+        } else if (lane < 2 * ppH && pi < pgh) {
+          const int row = static_cast<int>(pool_row(a.g, l, page, h, 0));
+          const uint32_t dst = static_cast<uint32_t>(half * kHalf + pi * P) * 128u;
+          tma_load_2d(Ks + dst, &tmk, 0, row, &full_k[s]);
+          tma_load_2d(Ks + 16384 + dst, &tmk, 64, row, &full_k[s]);
+        }
+        if (lane < cnt) {
+          // leaf `lane`: its G q rows (8-row box, 1024-B aligned slot) → Q rows [8·lane, 8·lane+8)
+          const int row = (leaf * a.Lc + li) * a.Hq + h * a.G;
+          tma_load_2d(Qs + lane * 1024, &tmq, 0, row, &full_k[s]);
+          tma_load_2d(Qs + NQ * 128 + lane * 1024, &tmq, 64, row, &full_k[s]);
+        }
+        if (lane == 0) TC_TRACE(k, 2);
+        ++kk_k;
       }
-      if (lane < cnt) {
-        // leaf `lane`: its G q rows (8-row box, 1024-B aligned slot) → Q rows [8·lane, 8·lane+8)
-        const int row = (leaf * a.Lc + li) * a.Hq + h * a.G;
-        tma_load_2d(Qs + lane * 1024, &tmq, 0, row, &full[s]);
-        tma_load_2d(Qs + NQ * 128 + lane * 1024, &tmq, 64, row, &full[s]);
+      if (kk_v < kk_k) {
+        const int sv = kk_v % NST;
+        go_v = __shfl_sync(0xffffffffu, mbar_test(&empty_v[sv], ((kk_v / NST) & 1u) ^ 1u) ? 1 : 0, 0) != 0;
       }
-      if (lane == 0) TC_TRACE(k, 2);
+      if (go_v) {
+        const int k = kk_v;
+        const int s = k % NST, r = k % (2 * NST);
+        const TcHdr hd = hdr[r];
+        const int page = lane < kMaxTilePages ? vpage[r][lane] : 0;
+        const int pgA = (hd.ntA + P - 1) >> lgP, pgB = (hd.ntB + P - 1) >> lgP;
+        unsigned char *Vs = sm + s * S::kStage + kKVBytes;
+        if (lane == 0) mbar_arrive_expect_tx(&full_v[s], static_cast<uint32_t>(pgA + pgB) * P * 256u);
+        __syncwarp();
+        const int l = a.layer_begin + hd.li;
+        const int half = lane >= ppH, pi = lane - half * ppH;
+        const int pgh = half ? pgB : pgA;
+        const int first = __shfl_sync(0xffffffffu, page, half * ppH);
+        const bool cons = lane >= 2 * ppH || pi >= pgh || page == first + pi;
+        const unsigned bal = __ballot_sync(0xffffffffu, cons);
+        const unsigned hmask = ((1u << ppH) - 1u) << (half * ppH);
+        const bool big = lane < 2 * ppH && pgh == ppH && (bal & hmask) == hmask;
+        if (big) {
+          if (pi == 0) {
+            const int lp = l * a.g.NP + page;
+            const uint32_t dst = static_cast<uint32_t>(half * kHalf) * 128u;
+            tma_load_5d(Vs + dst, &tmv4, 0, 0, 0, hd.h, lp, &full_v[s]);
+            tma_load_5d(Vs + 16384 + dst, &tmv4, 0, 1, 0, hd.h, lp, &full_v[s]);
+          }
+        } else if (lane < 2 * ppH && pi < pgh) {
+          const int row = static_cast<int>(pool_row(a.g, l, page, hd.h, 0));
+          const uint32_t dst = static_cast<uint32_t>(half * kHalf + pi * P) * 128u;
+          tma_load_2d(Vs + dst, &tmv, 0, row, &full_v[s]);
+          tma_load_2d(Vs + 16384 + dst, &tmv, 64, row, &full_v[s]);
+        }
+        ++kk_v;
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
@@ -498,7 +568,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       // j−2); MMA2(j) needs P(j) (p_full) and Oᵀ buffer j&1 drained (o_empty of j−2).
       int js = 0, jo = 0;
       while (jo < ntiles) {
-        if (js < ntiles && js <= jo + 1 && mbar_test(&full[js % NST], (js / NST) & 1u) &&
+        if (js < ntiles && js <= jo + 1 && mbar_test(&full_k[js % NST], (js / NST) & 1u) &&
             (js < 2 || mbar_test(&s_empty[js & 1], ((js - 2) >> 1) & 1u))) {
           const int s = js % NST, b = js & 1;
           TC_TRACE(js, 3);
@@ -512,6 +582,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
             tc_mma(tmem + b * 2 * NQ, ad, bd, id1, kk > 0);
           }
           tc_commit(&s_full[b]);
+          tc_commit(&empty_k[s]);            // K (and q) of this stage may be reloaded
           if (a.trace) { mbar_wait(&s_full[b], (js >> 1) & 1u); TC_TRACE(js, 12); }
           ++js;
         }
@@ -529,7 +600,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
             tc_mma(tmem + b * 2 * NQ + NQ, ad, bd, id2, kk > 0);
           }
           tc_commit(&o_full[b]);
-          tc_commit(&empty[s]);
+          tc_commit(&empty_v[s]);
           if (a.trace) { mbar_wait(&o_full[b], (jo >> 1) & 1u); TC_TRACE(jo, 13); }
           ++jo;
         }
@@ -559,9 +630,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     const uint32_t cb = static_cast<uint32_t>(tc * 2);
     for (int k = grp; k < ntiles; k += 2) {
       const int s = k % NST, b = k & 1;
-      mbar_wait(&full[s], (k / NST) & 1u);
+      mbar_wait(&full_k[s], (k / NST) & 1u);
       if (tid == 64) TC_TRACE(k, 7);
-      const TcHdr hd = hdr[s];
+      const TcHdr hd = hdr[k % (2 * NST)];
       if (half == 0 && lane == 0 && quad == 0) ohdr[k & 3] = hd;   // for the epilogue warps
       const unsigned long long cm = colmask(hd.cnt, G);
       const int nt = half ? hd.ntB : hd.ntA;
@@ -618,6 +689,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       mbar_arrive(&s_empty[b]);             // S of this buffer has been read
       // V rows of a partly filled last page hold pool bytes past k_cur: zero them so that
       // 0 · v stays 0 in Oᵀ = Vᵀ·Pᵀ (the rows past the last page were zeroed before)
+      // V of this stage has landed (MMA2 needs it anyway; P is only published after)
+      mbar_wait(&full_v[s], (k / NST) & 1u);
       if (present && (nt & (P - 1))) {
         const int r0 = nt, r1 = (nt + P - 1) & ~(P - 1);
         unsigned char *Vs = sm + s * S::kStage + kKVBytes;

@@ -36,6 +36,10 @@ def main():
     for _ in range(3):
         sc.ctx.arbor_tree_decode_attn(tree, q, out, lse)
     torch.cuda.synchronize()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=q.device)
+    if os.environ.get("TRACE_COLD"):
+        flush.zero_()                      # L2 flush: K/V come from HBM
+        torch.cuda.synchronize()
     os.environ["ARBOR_TC_TRACE"] = "1"
     sc.ctx.arbor_tree_decode_attn(tree, q, out, lse)
     torch.cuda.synchronize()
@@ -71,7 +75,8 @@ def main():
     starts = [tr[c, 63, 0] for c in range(148) if tr[c, 63, 0] > 0]
     t0 = min(starts)
     res = {
-        "config": cfg, "active_leaves": nA,
+        "config": cfg, "active_leaves": nA, "cold_l2": bool(os.environ.get("TRACE_COLD")),
+        "tiles_total_est": int(sum(tiles_per_cta)),
         "cta_span_us_p50_max": [float(np.median(spans_ns)) / 1e3, float(np.max(spans_ns)) / 1e3],
         "cta_start_skew_us_max": float(max(starts) - t0) / 1e3,
         "cta_end_us_max": float(max(tr[c, 63, 1] for c in range(148)) - t0) / 1e3,
