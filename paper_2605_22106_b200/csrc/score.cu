@@ -335,13 +335,15 @@ struct PostArgs {
   void *out;
   float *lse_out;   // natural-log LSE, or NULL
   int nA;
+  int exp;          // ARBOR_POST_EXP (measurement only): bit0 skip (b), bit1 skip score_row
 };
 constexpr int kPostItems = 512;   // nA · G ≤ kPostItems (host-checked)
 
 template <typename T, int D, int MINB>
 __global__ void __launch_bounds__(kFusedThreads, MINB)
 decode_post_kernel(PostArgs pa) {
-  pdl_trigger();   // launched without PDL (launch_decode_post); lets the next kernel overlap
+  pdl_wait();
+  pdl_trigger();
   const FusedArgs &f = pa.f;
   const ApplyArgs &a = f.ap;
   const int row = blockIdx.x, part = blockIdx.y, nparts = gridDim.y;
@@ -397,7 +399,7 @@ decode_post_kernel(PostArgs pa) {
   __syncthreads();
   // (b) owned items, warp per item: lane j holds pair p0 + j's index and weight 2^(m−M);
   // then, pairs in path order, lanes over d: o = Σ w o_p / L
-  for (int it = part + warp * nparts; it < nitems; it += NW * nparts) {
+  for (int it = part + warp * nparts; it < ((pa.exp & 1) ? 0 : nitems); it += NW * nparts) {
     const int b = it / G, g = it - b * G;
     const int p0 = a.pv.bp_off[b], p1 = a.pv.bp_off[b + 1];
     const float M = Ms[it];
@@ -435,6 +437,7 @@ decode_post_kernel(PostArgs pa) {
     for (int e = 0; e < EPL; ++e) out[lane + 32 * e] = ElemT<T>::from_f(acc[e] * inv);
   }
   __syncthreads();
+  if (pa.exp & 2) return;
   score_row(f, li, h, part, nparts, [&](int b, int g) { return lse2s[b * G + g]; });
 }
 
@@ -510,16 +513,19 @@ void launch_decode_post(arbor_ctx *c, const PlanView &pv, void *out, float *lse_
   pa.out = out;
   pa.lse_out = lse_out;
   pa.nA = pv.nA;
+  static const int pexp = getenv("ARBOR_POST_EXP") ? atoi(getenv("ARBOR_POST_EXP")) : 0;
+  pa.exp = pexp;
   const dim3 grid(c->L * c->H, nparts);
   stage_begin(c, ARBOR_ST_SCORE_ACCUM, c->ms);
-  // A plain launch, not PDL: 2·(rows) CTAs of 256 threads made resident early next to the
-  // attention kernel's CTAs slowed that kernel (measured: C2 step 269 → 237 µs without PDL)
+  // PDL launch.  (An earlier version — 2 CTAs per row, 110 registers, no min-blocks bound —
+  // was slower as a PDL launch than as a plain one, 269 vs 237 µs per C2 step; this one is
+  // faster with PDL: 238.9 vs 243.7 µs, A/B on one box.)
   if (c->esize == 2) {
-    if (c->D == 128) decode_post_kernel<__nv_bfloat16, 128, 3><<<grid, kFusedThreads, 0, c->ms>>>(pa);
-    else decode_post_kernel<__nv_bfloat16, 64, 3><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+    if (c->D == 128) launch_pdl(decode_post_kernel<__nv_bfloat16, 128, 3>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    else launch_pdl(decode_post_kernel<__nv_bfloat16, 64, 3>, grid, dim3(kFusedThreads), 0, c->ms, pa);
   } else {
-    if (c->D == 128) decode_post_kernel<float, 128, 3><<<grid, kFusedThreads, 0, c->ms>>>(pa);
-    else decode_post_kernel<float, 64, 3><<<grid, kFusedThreads, 0, c->ms>>>(pa);
+    if (c->D == 128) launch_pdl(decode_post_kernel<float, 128, 3>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    else launch_pdl(decode_post_kernel<float, 64, 3>, grid, dim3(kFusedThreads), 0, c->ms, pa);
   }
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
