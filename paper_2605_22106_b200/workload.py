@@ -87,14 +87,18 @@ def load_tree(ctx: ArborKV, tree, K, V):
             ctx.arbor_close_node(i)
 
 
-def decode_step(ctx: ArborKV, tree, q, out=None, lse=None):
-    """One decode step for the active leaves: tree decode attention (a9) then score (a2/a3)."""
+def decode_step(ctx: ArborKV, tree, q, out=None, lse=None, fused=False):
+    """One decode step for the active leaves: tree decode attention (a9) then score (a2/a3) —
+    two calls, or (fused) the f2 call arbor_decode_step."""
     import torch
     nA = len(tree.active)
     if out is None:
         out = torch.empty_like(q)
     if lse is None:
         lse = torch.empty((nA, ctx.L, ctx.Hq), dtype=torch.float32, device=q.device)
+    if fused:
+        ctx.arbor_decode_step(tree, q, out, lse)
+        return out, lse
     ctx.arbor_tree_decode_attn(tree, q, out, lse)
     ctx.arbor_score(tree, q, lse)
     return out, lse
