@@ -1,9 +1,9 @@
 """GPU parity of f2, arbor_decode_step (include/arbor.h): decode attention + score as two
 launches (attention kernel, then merge + score + masses + MSVE in one kernel; SURVEY §8(f)
 f2).  Checked against the CPU oracle like the two-call path (tests in
-test_gpu_parity.py), against the two-call path itself, and at configs[1]'s full size
-(Llama-3.1-8B-shaped, 156 nodes, 19,968 tokens) on sampled (layer, KV-head) rows, each
-mirrored by an oracle over that row alone.
+test_gpu_parity.py), against the two-call path itself, and at the full sizes of configs[1],
+configs[3] and configs[4] (8B-shaped 19,968 tokens; 32B-shaped 64 layers, G = 5, depth 8;
+64k tokens) on sampled (layer, KV-head) rows, each mirrored by an oracle over that row alone.
 """
 import math
 
@@ -98,16 +98,20 @@ def test_decode_step_agrees_with_two_calls():
     assert np.allclose(sa["s"], sb["s"], rtol=1e-5, atol=1e-6)
 
 
-def test_c2_full_size_decode_step_sampled_rows():
-    """configs[1] at full size in the bench's launch configuration: leaf-cycling warm-up,
-    decode steps and a ρ = 0.25 eviction through arbor_decode_step / arbor_allocate /
-    arbor_evict; sampled (layer, KV head) rows are mirrored by per-row oracles: attention
-    output and LSE (2e-2), A (2e-2), kept positions, page lists and free list (bit-exact)."""
-    preset = workload.PRESETS["c2"]
-    sc = workload.setup("c2", 0)
+@pytest.mark.parametrize("cfg", ["c2", "c4", "c5"])
+def test_full_size_decode_step_sampled_rows(cfg):
+    """configs[1] (c2), configs[3] (c4: Qwen2.5-32B-shaped, 64 layers, G = 5, depth-8 tree)
+    and configs[4] (c5: 64k-token 8B-shaped tree) at full size in the bench's launch
+    configuration: leaf-cycling warm-up, decode steps and a ρ = 0.25 eviction through
+    arbor_decode_step / arbor_allocate / arbor_evict; sampled (layer, KV head) rows are
+    mirrored by per-row oracles: attention output and LSE (2e-2), A (2e-2), kept positions,
+    page lists and free list (bit-exact)."""
+    preset = workload.PRESETS[cfg]
+    sc = workload.setup(cfg, 0)
     ctx, tree = sc.ctx, sc.tree
     G = ctx.G
-    rows = [(0, 0), (13, 5), (31, 7)]
+    Lm = ctx.L - 1
+    rows = [(0, 0), (13, 5), (Lm, 7)]
     orcs = {}
     for (l, h) in rows:
         K = sc.K[l:l + 1, h:h + 1].double().cpu().numpy()
