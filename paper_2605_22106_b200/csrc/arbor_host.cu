@@ -868,9 +868,9 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
   launch_attn_partial(c, pv, q, 0, c->L, hp.max_cnt, out, lse_out);
   CK_LAUNCH();
   const bool single = c->cfg.world_size == 1;
-  // parts per row: no more CTAs than one resident wave (3 per SM at the kernel's bounds)
+  // parts per row: no more CTAs than one resident wave (2 per SM at the kernel's bounds)
   int parts = score_parts(mass_nodes.size());
-  while (parts > 1 && c->L * c->H * parts > 3 * c->num_sms) parts /= 2;
+  while (parts > 1 && c->L * c->H * parts > 2 * c->num_sms) parts /= 2;
   if (const char *e = getenv("ARBOR_POST_PARTS")) parts = atoi(e);   // diagnostics
   launch_decode_post(c, pv, out, lse_out, d_mass_nodes, static_cast<int>(mass_nodes.size()), N,
                      single, s_out, parts);

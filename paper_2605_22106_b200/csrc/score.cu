@@ -201,30 +201,58 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   // tag is the slot itself: no page-table / tag round trip.  The pair loop's loads are
   // issued together (G ≤ 8 logits and LSEs per pair).
   const int warp = tid >> 5, lane = tid & 31;
-  for (int c = warp; c < a.pv.C; c += kFusedThreads / 32) {   // warp per owned chunk
-    const int node = a.pv.ch_node[c];
-    if ((node & (nparts - 1)) != part) continue;   // nparts: a power of two
-    const int c0 = a.pv.ch_chunk[c] * kAttnChunk;
-    const int kc = a.kcur[node];
-    const int nt = max(0, min(kAttnChunk, kc - c0));
-    const int p0 = a.pv.ch_poff[c], pc = a.pv.ch_pcnt[c];
-    const int64_t sp = a.span[node];
-    const bool ident = kc == f.nlen[node];
-    const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.g.MPN;
-    for (int t = lane; t < nt; t += 32) {
-      const int slot = c0 + t;
-      const int pos = ident ? slot : a.pos[pool_row(a.g, li, pl[slot / a.g.P], h, slot % a.g.P)];
-      // Σ over pairs (ascending) and query heads (ascending); four pairs' logits and LSEs
-      // are loaded before any is used (the sum order is unchanged)
-      float psum = 0.f;
+  constexpr int NW = kFusedThreads / 32;
+  // Warp w takes chunks w, w + NW, …  Their metadata is loaded 32 chunks at a time, lane i
+  // holding chunk w + NW·i (two round trips per batch instead of two per chunk), then
+  // broadcast chunk by chunk.
+  for (int cb = warp; cb < a.pv.C; cb += NW * 32) {
+    const int cm = cb + NW * lane;
+    int m_node = 0, m_c0 = 0, m_p0 = 0, m_pc = 0, m_nt = 0, m_ident = 0;
+    long long m_sp = 0;
+    if (cm < a.pv.C) {
+      m_node = a.pv.ch_node[cm];
+      m_c0 = a.pv.ch_chunk[cm] * kAttnChunk;
+      m_p0 = a.pv.ch_poff[cm];
+      m_pc = a.pv.ch_pcnt[cm];
+      if ((m_node & (nparts - 1)) == part) {   // nparts: a power of two
+        const int kc = a.kcur[m_node];
+        m_nt = max(0, min(kAttnChunk, kc - m_c0));
+        m_ident = kc == f.nlen[m_node];
+        m_sp = a.span[m_node];
+      }
+    }
+    const int nb = min(32, (a.pv.C - cb + NW - 1) / NW);
+    for (int j = 0; j < nb; ++j) {
+      const int nt = __shfl_sync(0xffffffffu, m_nt, j);
+      if (nt == 0) continue;
+      const int node = __shfl_sync(0xffffffffu, m_node, j);
+      const int c0 = __shfl_sync(0xffffffffu, m_c0, j);
+      const int p0 = __shfl_sync(0xffffffffu, m_p0, j);
+      const int pc = __shfl_sync(0xffffffffu, m_pc, j);
+      const bool ident = __shfl_sync(0xffffffffu, m_ident, j) != 0;
+      const int64_t sp = __shfl_sync(0xffffffffu, m_sp, j);
+      const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.g.MPN;
+      // both 32-slot halves of the chunk at once (lane: slots lane and lane + 32), so their
+      // logit and A loads are in flight together
+      const bool v0 = lane < nt, v1 = lane + 32 < nt;
+      auto pos_of = [&](int slot) {
+        return ident ? slot : a.pos[pool_row(a.g, li, pl[slot / a.g.P], h, slot % a.g.P)];
+      };
+      float *Ar = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + sp;
+      float *dst0 = v0 ? Ar + pos_of(c0 + lane) : nullptr;
+      float *dst1 = v1 ? Ar + pos_of(c0 + lane + 32) : nullptr;
+      const float old0 = v0 ? *dst0 : 0.f, old1 = v1 ? *dst1 : 0.f;
+      // Σ over pairs (ascending) and query heads (ascending) per slot; four pairs' logits and
+      // LSEs are loaded before any is used (the sum order is unchanged)
+      float ps0 = 0.f, ps1 = 0.f;
       const int pe = p0 + pc;
       int p = p0;
       auto zrow = [&](int pp) {
-        return a.zbuf + (((static_cast<int64_t>(pp) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + t;
+        return a.zbuf + (((static_cast<int64_t>(pp) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + lane;
       };
       if (a.G <= 4) {
         for (; p + 4 <= pe; p += 4) {
-          float zz[4][4], ll[4][4];
+          float z0[4][4], z1[4][4], ll[4][4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int b = a.pv.pair_b[p + u];
@@ -232,7 +260,8 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               if (g < a.G) {
-                zz[u][g] = z[g * kAttnChunk];
+                z0[u][g] = v0 ? z[g * kAttnChunk] : 0.f;
+                z1[u][g] = v1 ? z[g * kAttnChunk + 32] : 0.f;
                 ll[u][g] = lse2(b, g);
               }
             }
@@ -241,45 +270,72 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
           for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int g = 0; g < 4; ++g)
-              if (g < a.G) psum += exp2f(zz[u][g] - ll[u][g]);
+              if (g < a.G) {
+                ps0 += exp2f(z0[u][g] - ll[u][g]);
+                ps1 += exp2f(z1[u][g] - ll[u][g]);
+              }
         }
       }
       for (; p < pe; ++p) {
         const int b = a.pv.pair_b[p];
         const float *z = zrow(p);
         for (int g0 = 0; g0 < a.G; g0 += 8) {
-          float zz[8], ll[8];
+          float z0[8], z1[8], ll[8];
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
             if (g0 + g < a.G) {
-              zz[g] = z[(g0 + g) * kAttnChunk];
+              z0[g] = v0 ? z[(g0 + g) * kAttnChunk] : 0.f;
+              z1[g] = v1 ? z[(g0 + g) * kAttnChunk + 32] : 0.f;
               ll[g] = lse2(b, g0 + g);
             }
           }
 #pragma unroll
           for (int g = 0; g < 8; ++g)
-            if (g0 + g < a.G) psum += exp2f(zz[g] - ll[g]);
+            if (g0 + g < a.G) {
+              ps0 += exp2f(z0[g] - ll[g]);
+              ps1 += exp2f(z1[g] - ll[g]);
+            }
         }
       }
-      float *dst = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + sp + pos;
-      const float nv = *dst + psum;
-      if (!(nv >= 0.f) || isinf(nv)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-      *dst = nv;
+      if (v0) {
+        const float nv = old0 + ps0;
+        if (!(nv >= 0.f) || isinf(nv)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+        *dst0 = nv;
+      }
+      if (v1) {
+        const float nv = old1 + ps1;
+        if (!(nv >= 0.f) || isinf(nv)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+        *dst1 = nv;
+      }
     }
   }
   __syncthreads();
-  // (2) this row's partial node masses: warp per node, lanes strided, fixed xor tree (Q29)
+  // (2) this row's partial node masses: warp per node, lanes strided, fixed xor tree (Q29);
+  // node metadata batched like the chunks'
   const float *Arow = a.A + (static_cast<int64_t>(li) * f.H + h) * f.max_tokens;
-  for (int mi = warp; mi < f.n_mass; mi += kFusedThreads / 32) {
-    const int node = f.mass_nodes[mi];
-    if ((node & (nparts - 1)) != part) continue;   // nparts: a power of two
-    const int n = f.nlen[node];
-    const float *r = Arow + a.span[node];
-    double m = 0.0;
-    for (int t = lane; t < n; t += 32) m += static_cast<double>(r[t]);
+  for (int mb = warp; mb < f.n_mass; mb += NW * 32) {
+    const int mm = mb + NW * lane;
+    int m_node = 0, m_n = 0;
+    long long m_sp = 0;
+    if (mm < f.n_mass) {
+      m_node = f.mass_nodes[mm];
+      if ((m_node & (nparts - 1)) == part) {
+        m_n = f.nlen[m_node];
+        m_sp = a.span[m_node];
+      }
+    }
+    const int nb = min(32, (f.n_mass - mb + NW - 1) / NW);
+    for (int j = 0; j < nb; ++j) {
+      const int n = __shfl_sync(0xffffffffu, m_n, j);
+      if (n == 0) continue;
+      const int node = __shfl_sync(0xffffffffu, m_node, j);
+      const float *r = Arow + __shfl_sync(0xffffffffu, m_sp, j);
+      double m = 0.0;
+      for (int t = lane; t < n; t += 32) m += static_cast<double>(r[t]);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
-    if (lane == 0) atomicAdd(&f.acc[node], static_cast<unsigned long long>(__double2ll_rn(m * 16777216.0)));
+      for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+      if (lane == 0) atomicAdd(&f.acc[node], static_cast<unsigned long long>(__double2ll_rn(m * 16777216.0)));
+    }
   }
   // (3) last CTA: publish, reset, MSVE
   __shared__ bool last;
@@ -397,44 +453,59 @@ decode_post_kernel(PostArgs pa) {
     }
   }
   __syncthreads();
-  // (b) owned items, warp per item: lane j holds pair p0 + j's index and weight 2^(m−M);
-  // then, pairs in path order, lanes over d: o = Σ w o_p / L
-  for (int it = part + warp * nparts; it < ((pa.exp & 1) ? 0 : nitems); it += NW * nparts) {
-    const int b = it / G, g = it - b * G;
-    const int p0 = a.pv.bp_off[b], p1 = a.pv.bp_off[b + 1];
-    const float M = Ms[it];
-    float acc[EPL];
+  // (b) owned items, eight lanes per item (four items per warp at once): lane j of the group
+  // holds pair p0 + j's index and weight 2^(m−M); then, pairs in path order, each lane
+  // accumulates D/8 of o with float2 loads: o = Σ w o_p / L
+  {
+    constexpr int EPG = D / 8;             // floats of o per lane
+    const int sub = lane & 7, gbase = lane & ~7;
+    const int nown = nitems > part ? (nitems - part + nparts - 1) / nparts : 0;   // owned items
+    for (int o0 = warp * 4; o0 < ((pa.exp & 1) ? 0 : ((nown + 3) & ~3)); o0 += NW * 4) {
+      const int oi = o0 + (lane >> 3);
+      const bool ok = oi < nown;
+      const int it = part + oi * nparts;
+      const int b = ok ? it / G : 0, g = ok ? it - b * G : 0;
+      const int p0 = ok ? a.pv.bp_off[b] : 0, p1 = ok ? a.pv.bp_off[b + 1] : 0;
+      const float M = ok ? Ms[it] : -INFINITY;
+      float acc[EPG];
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
-    if (M != -INFINITY) {
-      for (int i0 = p0; i0 < p1; i0 += 32) {
+      for (int e = 0; e < EPG; ++e) acc[e] = 0.f;
+      const int np = p1 - p0;
+      int npmax = max(np, __shfl_xor_sync(0xffffffffu, np, 8));     // max over the 4 groups
+      npmax = max(npmax, __shfl_xor_sync(0xffffffffu, npmax, 16));
+      for (int i0 = 0; i0 < npmax; i0 += 8) {
         int pi = 0;
         float w = 0.f;
-        if (i0 + lane < p1) {
-          pi = a.pv.bp_list[i0 + lane];
+        if (i0 + sub < np && M != -INFINITY) {
+          pi = a.pv.bp_list[p0 + i0 + sub];
           const float m2 = part_ptr(pi, g)[D];
           w = m2 == -INFINITY ? 0.f : exp2f(m2 - M);
         }
-        const int cnt = min(32, p1 - i0);
-#pragma unroll 8
-        for (int j = 0; j < cnt; ++j) {
-          const float wj = __shfl_sync(0xffffffffu, w, j);
-          const int pj = __shfl_sync(0xffffffffu, pi, j);
-          const float *pp = part_ptr(pj, g);
-          float v[EPL];
+#pragma unroll 2
+        for (int j = 0; j < 8; ++j) {
+          const float wj = __shfl_sync(0xffffffffu, w, gbase + j);
+          const int pj = __shfl_sync(0xffffffffu, pi, gbase + j);
+          const float2 *pp = reinterpret_cast<const float2 *>(part_ptr(pj, g)) + sub * (EPG / 2);
+          float2 v[EPG / 2];
 #pragma unroll
-          for (int e = 0; e < EPL; ++e) v[e] = pp[lane + 32 * e];
+          for (int e = 0; e < EPG / 2; ++e) v[e] = pp[e];
           if (wj != 0.f) {
 #pragma unroll
-            for (int e = 0; e < EPL; ++e) acc[e] = fmaf(wj, v[e], acc[e]);
+            for (int e = 0; e < EPG / 2; ++e) {
+              acc[2 * e] = fmaf(wj, v[e].x, acc[2 * e]);
+              acc[2 * e + 1] = fmaf(wj, v[e].y, acc[2 * e + 1]);
+            }
           }
         }
       }
-    }
-    T *out = static_cast<T *>(pa.out) + ((static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * G + g) * D;
-    const float inv = invL[it];
+      if (ok) {
+        T *out = static_cast<T *>(pa.out) + ((static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * G + g) * D +
+                 sub * EPG;
+        const float inv = invL[it];
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) out[lane + 32 * e] = ElemT<T>::from_f(acc[e] * inv);
+        for (int e = 0; e < EPG; ++e) out[e] = ElemT<T>::from_f(acc[e] * inv);
+      }
+    }
   }
   __syncthreads();
   if (pa.exp & 2) return;
@@ -521,11 +592,11 @@ void launch_decode_post(arbor_ctx *c, const PlanView &pv, void *out, float *lse_
   // was slower as a PDL launch than as a plain one, 269 vs 237 µs per C2 step; this one is
   // faster with PDL: 238.9 vs 243.7 µs, A/B on one box.)
   if (c->esize == 2) {
-    if (c->D == 128) launch_pdl(decode_post_kernel<__nv_bfloat16, 128, 3>, grid, dim3(kFusedThreads), 0, c->ms, pa);
-    else launch_pdl(decode_post_kernel<__nv_bfloat16, 64, 3>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    if (c->D == 128) launch_pdl(decode_post_kernel<__nv_bfloat16, 128, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    else launch_pdl(decode_post_kernel<__nv_bfloat16, 64, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
   } else {
-    if (c->D == 128) launch_pdl(decode_post_kernel<float, 128, 3>, grid, dim3(kFusedThreads), 0, c->ms, pa);
-    else launch_pdl(decode_post_kernel<float, 64, 3>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    if (c->D == 128) launch_pdl(decode_post_kernel<float, 128, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    else launch_pdl(decode_post_kernel<float, 64, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
   }
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
