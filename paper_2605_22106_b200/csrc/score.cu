@@ -190,9 +190,52 @@ __device__ __forceinline__ void msve_one(const MsveArgs &m, int i) {
 
 // Steps (1)-(3) of one (row, part) CTA; lse2(b, g) gives the log2-domain LSE of leaf b's
 // query head g of this row's KV head (the caller's LSE buffer, or the merged one in smem).
+// Per-lane metadata of one batch of chunks (lane i: chunk w + NW·i of warp w) and of mass
+// nodes (lane i: mass node w + NW·i).  Plan arrays, k_cur, n and spans are not written by
+// the attention kernel, so decode_post loads the first batch before griddepcontrol.wait.
+struct ChunkMeta {
+  int node = 0, c0 = 0, p0 = 0, pc = 0, nt = 0, ident = 0;
+  long long sp = 0;
+};
+struct MassMeta {
+  int node = 0, n = 0;
+  long long sp = 0;
+};
+__device__ __forceinline__ ChunkMeta load_chunk_meta(const FusedArgs &f, int cm, int part,
+                                                     int nparts) {
+  const ApplyArgs &a = f.ap;
+  ChunkMeta m;
+  if (cm < a.pv.C) {
+    m.node = a.pv.ch_node[cm];
+    m.c0 = a.pv.ch_chunk[cm] * kAttnChunk;
+    m.p0 = a.pv.ch_poff[cm];
+    m.pc = a.pv.ch_pcnt[cm];
+    if ((m.node & (nparts - 1)) == part) {   // nparts: a power of two
+      const int kc = a.kcur[m.node];
+      m.nt = max(0, min(kAttnChunk, kc - m.c0));
+      m.ident = kc == f.nlen[m.node];
+      m.sp = a.span[m.node];
+    }
+  }
+  return m;
+}
+__device__ __forceinline__ MassMeta load_mass_meta(const FusedArgs &f, int mm, int part,
+                                                   int nparts) {
+  MassMeta m;
+  if (mm < f.n_mass) {
+    m.node = f.mass_nodes[mm];
+    if ((m.node & (nparts - 1)) == part) {
+      m.n = f.nlen[m.node];
+      m.sp = f.ap.span[m.node];
+    }
+  }
+  return m;
+}
+
 template <typename LseFn>
 __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int part, int nparts,
-                                          LseFn lse2) {
+                                          LseFn lse2, const ChunkMeta *pre_c = nullptr,
+                                          const MassMeta *pre_m = nullptr) {
   const ApplyArgs &a = f.ap;
   const int tid = threadIdx.x;
   // (1) A[li][h][a_j + pos] += Σ_pairs Σ_g exp2(z − LSE·log2 e)
@@ -206,21 +249,10 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   // holding chunk w + NW·i (two round trips per batch instead of two per chunk), then
   // broadcast chunk by chunk.
   for (int cb = warp; cb < a.pv.C; cb += NW * 32) {
-    const int cm = cb + NW * lane;
-    int m_node = 0, m_c0 = 0, m_p0 = 0, m_pc = 0, m_nt = 0, m_ident = 0;
-    long long m_sp = 0;
-    if (cm < a.pv.C) {
-      m_node = a.pv.ch_node[cm];
-      m_c0 = a.pv.ch_chunk[cm] * kAttnChunk;
-      m_p0 = a.pv.ch_poff[cm];
-      m_pc = a.pv.ch_pcnt[cm];
-      if ((m_node & (nparts - 1)) == part) {   // nparts: a power of two
-        const int kc = a.kcur[m_node];
-        m_nt = max(0, min(kAttnChunk, kc - m_c0));
-        m_ident = kc == f.nlen[m_node];
-        m_sp = a.span[m_node];
-      }
-    }
+    const ChunkMeta cmeta = (cb == warp && pre_c) ? *pre_c : load_chunk_meta(f, cb + NW * lane, part, nparts);
+    const int m_node = cmeta.node, m_c0 = cmeta.c0, m_p0 = cmeta.p0, m_pc = cmeta.pc,
+              m_nt = cmeta.nt, m_ident = cmeta.ident;
+    const long long m_sp = cmeta.sp;
     const int nb = min(32, (a.pv.C - cb + NW - 1) / NW);
     for (int j = 0; j < nb; ++j) {
       const int nt = __shfl_sync(0xffffffffu, m_nt, j);
@@ -314,16 +346,9 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   // node metadata batched like the chunks'
   const float *Arow = a.A + (static_cast<int64_t>(li) * f.H + h) * f.max_tokens;
   for (int mb = warp; mb < f.n_mass; mb += NW * 32) {
-    const int mm = mb + NW * lane;
-    int m_node = 0, m_n = 0;
-    long long m_sp = 0;
-    if (mm < f.n_mass) {
-      m_node = f.mass_nodes[mm];
-      if ((m_node & (nparts - 1)) == part) {
-        m_n = f.nlen[m_node];
-        m_sp = a.span[m_node];
-      }
-    }
+    const MassMeta mmeta = (mb == warp && pre_m) ? *pre_m : load_mass_meta(f, mb + NW * lane, part, nparts);
+    const int m_node = mmeta.node, m_n = mmeta.n;
+    const long long m_sp = mmeta.sp;
     const int nb = min(32, (f.n_mass - mb + NW - 1) / NW);
     for (int j = 0; j < nb; ++j) {
       const int n = __shfl_sync(0xffffffffu, m_n, j);
@@ -398,14 +423,17 @@ constexpr int kPostItems = 512;   // nA · G ≤ kPostItems (host-checked)
 template <typename T, int D, int MINB>
 __global__ void __launch_bounds__(kFusedThreads, MINB)
 decode_post_kernel(PostArgs pa) {
-  pdl_wait();
-  pdl_trigger();
   const FusedArgs &f = pa.f;
   const ApplyArgs &a = f.ap;
   const int row = blockIdx.x, part = blockIdx.y, nparts = gridDim.y;
   const int li = row / f.H, h = row - li * f.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = kFusedThreads / 32, EPL = D / 32;
+  // first batch of score_row's metadata: overlaps the attention kernel's tail
+  const ChunkMeta pre_c = load_chunk_meta(f, warp + NW * lane, part, nparts);
+  const MassMeta pre_m = load_mass_meta(f, warp + NW * lane, part, nparts);
+  pdl_wait();
+  pdl_trigger();
   const int G = a.G;
   __shared__ float lse2s[kPostItems], Ms[kPostItems], invL[kPostItems];
   auto part_ptr = [&](int p, int g) -> const float * {
@@ -509,7 +537,7 @@ decode_post_kernel(PostArgs pa) {
   }
   __syncthreads();
   if (pa.exp & 2) return;
-  score_row(f, li, h, part, nparts, [&](int b, int g) { return lse2s[b * G + g]; });
+  score_row(f, li, h, part, nparts, [&](int b, int g) { return lse2s[b * G + g]; }, &pre_c, &pre_m);
 }
 
 }  // namespace
