@@ -15,7 +15,7 @@
 //
 // CTA layout (persistent, one CTA per SM, tiles strided over CTAs):
 //   warp 0      TMA producer: per page-head, two cp.async.bulk.tensor boxes (64 cols × P rows,
-//               SWIZZLE_128B) for K and for V into an NST-stage ring; q rows staged with 16-byte
+//               SWIZZLE_128B) for K and for V into NSK- and NSV-stage rings; q rows staged with 16-byte
 //               loads into the same 128B-swizzled K-major layout; mbarrier transaction counts.
 //   warp 1      TMEM allocator + MMA issuer (one thread): MMA1(k+1) is issued before MMA2(k)
 //               waits for the softmax of tile k, so the S of the next tile is ready in TMEM.
@@ -302,34 +302,42 @@ constexpr int tmem_cols() {
   return 4 * NQ <= 32 ? 32 : 4 * NQ <= 64 ? 64 : 4 * NQ <= 128 ? 128 : 4 * NQ <= 256 ? 256 : 512;
 }
 
-template <int NQ, int NST>
+// Dynamic smem: NSK K stages [K | Q], NSV V stages, two P tiles (all 1024-B aligned).
+template <int NQ, int NSK, int NSV>
 struct TcSmem {
   static constexpr uint32_t kQ = NQ * 256;                    // Q tile bytes
-  static constexpr uint32_t kStage = 2 * kKVBytes + kQ;       // K | V | Q
+  static constexpr uint32_t kKS = kKVBytes + kQ;              // one K stage: K | Q
+  static constexpr uint32_t kVBase = NSK * kKS;               // first V stage
   static constexpr uint32_t kP = NQ * 256;                    // P tile bytes (NQ rows × 128 slots)
-  static constexpr uint32_t kBytes = NST * kStage + 2 * kP;
+  static constexpr uint32_t kPBase = kVBase + NSV * kKVBytes;
+  static constexpr uint32_t kBytes = kPBase + 2 * kP;
   static constexpr uint32_t kAlloc = kBytes + 1024;           // + alignment slack
+  static constexpr int kRing = 2 * (NSK > NSV ? NSK : NSV);  // per-tile header ring
 };
 
-template <int NQ, int NST>
+template <int NQ, int NSK, int NSV>
 __global__ void __launch_bounds__(kTcThreads, 1)
 attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                const __grid_constant__ CUtensorMap tmk4, const __grid_constant__ CUtensorMap tmv4,
                const __grid_constant__ CUtensorMap tmq, TcArgs a) {
-  using S = TcSmem<NQ, NST>;
+  using S = TcSmem<NQ, NSK, NSV>;
+  constexpr int RING = S::kRing;
   extern __shared__ unsigned char sm_raw[];
   unsigned char *sm = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  unsigned char *Pbuf = sm + NST * S::kStage;
+  unsigned char *Pbuf = sm + S::kPBase;
+  auto Kst = [&](int s) { return sm + s * S::kKS; };                 // K stage s (Q after K)
+  auto Vst = [&](int s) { return sm + S::kVBase + s * kKVBytes; };  // V stage s
   // K (+ q rows) and V of a stage have their own barriers: K is free again once MMA1 has
   // read it, V only after MMA2, so the next K loads go out ~1.5 µs earlier
-  __shared__ __align__(8) uint64_t full_k[NST], empty_k[NST], full_v[NST], empty_v[NST];
+  __shared__ __align__(8) uint64_t full_k[NSK], empty_k[NSK], full_v[NSV], empty_v[NSV];
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], o_full[2], o_empty[2];
-  // per-tile header and page list, ring of 2·NST tiles (written at K issue; read by the V
-  // issue, the softmax and — via ohdr — the epilogue; slot k is rewritten by tile k + 2·NST,
-  // whose K issue needs MMA1(k + NST), i.e. softmax(k) done)
-  __shared__ TcHdr hdr[2 * NST];
-  __shared__ int vpage[2 * NST][kMaxTilePages];
+  // per-tile header and page list, ring of RING = 2·max(NSK, NSV) tiles (written at K issue;
+  // read by the V issue, the softmax and — via ohdr — the epilogue; slot k is rewritten by
+  // tile k + RING, whose K issue needs MMA1(k + RING − NSK), i.e. MMA2(k) issued, i.e.
+  // softmax(k) done; K issue runs < RING tiles ahead of V issue)
+  __shared__ TcHdr hdr[RING];
+  __shared__ int vpage[RING][kMaxTilePages];
   __shared__ TcHdr ohdr[4];                             // tile k's header for the epilogue warps
   // column max / sum of each warp quadrant, ring of 4 tiles (the epilogue warps read tile k's
   // before releasing Oᵀ buffer k&1, which softmax(k+4) needs first)
@@ -390,19 +398,22 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   if (warp != 0) {
     // zero V, Q and P once: MMA2 reads every V row (0·v must stay 0, so rows never loaded
     // must be finite) and the off-half rows of the Pᵀ tile are never written again
-    for (int s = 0; s < NST; ++s) {
-      unsigned char *base = sm + s * S::kStage + kKVBytes;
-      for (uint32_t i = (tid - 32) * 16; i < kKVBytes + S::kQ; i += (kTcThreads - 32) * 16)
-        *reinterpret_cast<uint4 *>(base + i) = make_uint4(0, 0, 0, 0);
-    }
+    for (int s = 0; s < NSV; ++s)
+      for (uint32_t i = (tid - 32) * 16; i < kKVBytes; i += (kTcThreads - 32) * 16)
+        *reinterpret_cast<uint4 *>(Vst(s) + i) = make_uint4(0, 0, 0, 0);
+    for (int s = 0; s < NSK; ++s)
+      for (uint32_t i = (tid - 32) * 16; i < S::kQ; i += (kTcThreads - 32) * 16)
+        *reinterpret_cast<uint4 *>(Kst(s) + kKVBytes + i) = make_uint4(0, 0, 0, 0);
     for (uint32_t i = (tid - 32) * 16; i < 2 * S::kP; i += (kTcThreads - 32) * 16)
       *reinterpret_cast<uint4 *>(Pbuf + i) = make_uint4(0, 0, 0, 0);
     fence_proxy_async();
   }
   if (tid == 32) {
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < NSK; ++s) {
       mbar_init(&full_k[s], 1);
       mbar_init(&empty_k[s], 1);
+    }
+    for (int s = 0; s < NSV; ++s) {
       mbar_init(&full_v[s], 1);
       mbar_init(&empty_v[s], 1);
     }
@@ -439,17 +450,17 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 
   if (warp == 0) {
     // ------------------------------------------------------------- TMA producer
-    // Two cursors: K (+ q rows) of tile kk_k goes out as soon as stage kk_k % NST's K buffer
-    // is free (MMA1 of tile kk_k − NST done), V of tile kk_v once its V buffer is (MMA2 done);
-    // K runs at most NST tiles ahead of V.  Non-blocking polls, lane 0's view broadcast.
+    // Two cursors: K (+ q rows) of tile kk_k goes out as soon as K stage kk_k % NSK is free
+    // (MMA1 of tile kk_k − NSK done), V of tile kk_v once V stage kk_v % NSV is (MMA2 of
+    // kk_v − NSV done); K runs < RING tiles ahead of V.  Non-blocking polls, lane 0's view.
     const int ppH = kHalf >> lgP;
     int kk_k = 0, kk_v = 0;
     if (ntiles > 0) load_state(0);
     while (kk_v < ntiles) {
       bool go_k = false, go_v = false;
-      if (kk_k < ntiles && kk_k < kk_v + NST) {
-        const int sk = kk_k % NST;
-        go_k = __shfl_sync(0xffffffffu, mbar_test(&empty_k[sk], ((kk_k / NST) & 1u) ^ 1u) ? 1 : 0, 0) != 0;
+      if (kk_k < ntiles && kk_k < kk_v + RING) {
+        const int sk = kk_k % NSK;
+        go_k = __shfl_sync(0xffffffffu, mbar_test(&empty_k[sk], ((kk_k / NSK) & 1u) ^ 1u) ? 1 : 0, 0) != 0;
       }
       if (go_k) {
         const int k = kk_k;
@@ -477,10 +488,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         const int it = blockIdx.x + k * gridDim.x;
         const int li = (it / a.g.H) % a.Lc, h = it % a.g.H;
         const int pgA = (ntA + P - 1) >> lgP, pgB = (ntB + P - 1) >> lgP;
-        const int s = k % NST, r = k % (2 * NST);
+        const int s = k % NSK, r = k % RING;
         if (lane == 0) { TC_TRACE(k, 0); TC_TRACE(k, 1); }
-        unsigned char *Ks = sm + s * S::kStage;
-        unsigned char *Qs = Ks + 2 * kKVBytes;
+        unsigned char *Ks = Kst(s);
+        unsigned char *Qs = Ks + kKVBytes;
         if (lane == 0) {
           hdr[r] = TcHdr{ntA, ntB, li, h, pbA, pbB, cnt, pbB >= 0 ? 1 : 0};
           mbar_arrive_expect_tx(&full_k[s], static_cast<uint32_t>(pgA + pgB) * P * 256u +
@@ -522,16 +533,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         ++kk_k;
       }
       if (kk_v < kk_k) {
-        const int sv = kk_v % NST;
-        go_v = __shfl_sync(0xffffffffu, mbar_test(&empty_v[sv], ((kk_v / NST) & 1u) ^ 1u) ? 1 : 0, 0) != 0;
+        const int sv = kk_v % NSV;
+        go_v = __shfl_sync(0xffffffffu, mbar_test(&empty_v[sv], ((kk_v / NSV) & 1u) ^ 1u) ? 1 : 0, 0) != 0;
       }
       if (go_v) {
         const int k = kk_v;
-        const int s = k % NST, r = k % (2 * NST);
+        const int s = k % NSV, r = k % RING;
         const TcHdr hd = hdr[r];
         const int page = lane < kMaxTilePages ? vpage[r][lane] : 0;
         const int pgA = (hd.ntA + P - 1) >> lgP, pgB = (hd.ntB + P - 1) >> lgP;
-        unsigned char *Vs = sm + s * S::kStage + kKVBytes;
+        unsigned char *Vs = Vst(s);
         if (lane == 0) mbar_arrive_expect_tx(&full_v[s], static_cast<uint32_t>(pgA + pgB) * P * 256u);
         __syncwarp();
         const int l = a.layer_begin + hd.li;
@@ -568,13 +579,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       // j−2); MMA2(j) needs P(j) (p_full) and Oᵀ buffer j&1 drained (o_empty of j−2).
       int js = 0, jo = 0;
       while (jo < ntiles) {
-        if (js < ntiles && js <= jo + 1 && mbar_test(&full_k[js % NST], (js / NST) & 1u) &&
+        if (js < ntiles && js <= jo + 1 && mbar_test(&full_k[js % NSK], (js / NSK) & 1u) &&
             (js < 2 || mbar_test(&s_empty[js & 1], ((js - 2) >> 1) & 1u))) {
-          const int s = js % NST, b = js & 1;
+          const int s = js % NSK, b = js & 1;
           TC_TRACE(js, 3);
           tc_fence_after();
-          const uint32_t ks = smem_u32(sm + s * S::kStage);
-          const uint32_t qs = ks + 2 * kKVBytes;
+          const uint32_t ks = smem_u32(Kst(s));
+          const uint32_t qs = ks + kKVBytes;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t ad = sw128_desc(ks + (kk >> 2) * 16384u + (kk & 3) * 32u, 16, 1024);
@@ -588,10 +599,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         }
         if (jo < js && mbar_test(&p_full[jo & 1], (jo >> 1) & 1u) &&
             (jo < 2 || mbar_test(&o_empty[jo & 1], ((jo - 2) >> 1) & 1u))) {
-          const int s = jo % NST, b = jo & 1;
+          const int s = jo % NSV, b = jo & 1;
           TC_TRACE(jo, 5);
           tc_fence_after();
-          const uint32_t vs = smem_u32(sm + s * S::kStage) + kKVBytes;
+          const uint32_t vs = smem_u32(Vst(s));
           const uint32_t ps = smem_u32(Pbuf + b * S::kP);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
@@ -629,10 +640,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     const int myc = colW<NQ>(lane);
     const uint32_t cb = static_cast<uint32_t>(tc * 2);
     for (int k = grp; k < ntiles; k += 2) {
-      const int s = k % NST, b = k & 1;
-      mbar_wait(&full_k[s], (k / NST) & 1u);
+      const int s = k % NSK, b = k & 1;
+      mbar_wait(&full_k[s], (k / NSK) & 1u);
       if (tid == 64) TC_TRACE(k, 7);
-      const TcHdr hd = hdr[k % (2 * NST)];
+      const TcHdr hd = hdr[k % RING];
       if (half == 0 && lane == 0 && quad == 0) ohdr[k & 3] = hd;   // for the epilogue warps
       const unsigned long long cm = colmask(hd.cnt, G);
       const int nt = half ? hd.ntB : hd.ntA;
@@ -690,10 +701,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       // V rows of a partly filled last page hold pool bytes past k_cur: zero them so that
       // 0 · v stays 0 in Oᵀ = Vᵀ·Pᵀ (the rows past the last page were zeroed before)
       // V of this stage has landed (MMA2 needs it anyway; P is only published after)
-      mbar_wait(&full_v[s], (k / NST) & 1u);
+      const int sv = k % NSV;
+      mbar_wait(&full_v[sv], (k / NSV) & 1u);
       if (present && (nt & (P - 1))) {
         const int r0 = nt, r1 = (nt + P - 1) & ~(P - 1);
-        unsigned char *Vs = sm + s * S::kStage + kKVBytes;
+        unsigned char *Vs = Vst(sv);
         const int tl = trow - half * 64;   // 0..63 within the half
         for (int idx = tl; idx < (r1 - r0) * 16; idx += 64) {
           const int r = half * kHalf + r0 + (idx >> 4), c16 = idx & 15;
@@ -770,12 +782,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   }
 }
 
-template <int NQ, int NST>
+template <int NQ, int NSK, int NSV>
 void launch_tc(arbor_ctx *c, const TcArgs &a) {
-  using S = TcSmem<NQ, NST>;
+  using S = TcSmem<NQ, NSK, NSV>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_tc_kernel<NQ, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(attn_tc_kernel<NQ, NSK, NSV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(S::kAlloc));
     attr = true;
   }
@@ -783,7 +795,7 @@ void launch_tc(arbor_ctx *c, const TcArgs &a) {
   if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
   const int total = a.T * a.Lc * a.g.H;
   const int grid = total < sms ? total : sms;
-  launch_pdl(attn_tc_kernel<NQ, NST>, dim3(grid), dim3(kTcThreads), S::kAlloc, c->ms,
+  launch_pdl(attn_tc_kernel<NQ, NSK, NSV>, dim3(grid), dim3(kTcThreads), S::kAlloc, c->ms,
              *reinterpret_cast<const CUtensorMap *>(c->tmap_k),
              *reinterpret_cast<const CUtensorMap *>(c->tmap_v),
              *reinterpret_cast<const CUtensorMap *>(c->tmap_k4),
@@ -899,10 +911,11 @@ bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_b
     a.trace = trace;
     g_tc_trace = trace;
   }
-  if (nq <= 8) launch_tc<8, 3>(c, a);
-  else if (nq <= 16) launch_tc<16, 3>(c, a);
-  else if (nq <= 32) launch_tc<32, 2>(c, a);
-  else if (nq <= 48) launch_tc<48, 2>(c, a);
+  // (K, V) ring depths; (4, 2) for NQ = 8 / 16 measured the same as (3, 3) on C2
+  if (nq <= 8) launch_tc<8, 3, 3>(c, a);
+  else if (nq <= 16) launch_tc<16, 3, 3>(c, a);
+  else if (nq <= 32) launch_tc<32, 2, 2>(c, a);
+  else if (nq <= 48) launch_tc<48, 2, 2>(c, a);
   else return false;
   return true;
 }
