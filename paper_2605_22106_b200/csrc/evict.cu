@@ -29,6 +29,11 @@ namespace {
 
 constexpr int kPairsWs = 8;   // (select warp, move warp) pairs per CTA of select_move_ws_kernel
 constexpr int kUw = 4;        // rows in flight per lane group of a move warp
+#ifndef ARBOR_JOB_SLOTS
+#define ARBOR_JOB_SLOTS 2
+#endif
+constexpr int kJobSlots = ARBOR_JOB_SLOTS;   // job queue depth per pair (power of 2; 2, 4, 8 measured equal on C2)
+static_assert((kJobSlots & (kJobSlots - 1)) == 0, "job slots: a power of two");
 
 struct CompactArgs {
   int R;            // rows = L * H
@@ -82,9 +87,9 @@ struct WsLayout {
     pbuf = take(size_t(kPairsWs) * 2 * capP * 2);         // pos tags, 2 pipeline slots
     gbuf = take(size_t(kPairsWs) * 3 * pcap * 4);         // page lists, 3 pipeline slots
     mbuf = take(size_t(kPairsWs) * 4 * sizeof(WorkEnt));  // work entries, 4 pipeline slots
-    jobs = take(size_t(kPairsWs) * 2 * jcap * 8);         // (src row, dst row) job queues
-    jcount = take(size_t(kPairsWs) * 2 * 4);
-    bars = take(size_t(kPairsWs) * 4 * 8);
+    jobs = take(size_t(kPairsWs) * kJobSlots * jcap * 8);  // (src row, dst row) job queues
+    jcount = take(size_t(kPairsWs) * kJobSlots * 4);
+    bars = take(size_t(kPairsWs) * 2 * kJobSlots * 8);
     total = o;
   }
 };
@@ -117,19 +122,16 @@ select_move_ws_kernel(CompactArgs a) {
   const int cap = Ly.cap, capP = Ly.capP, pcap = Ly.pcap, jcap = Ly.jcap;
   const int lgP = a.lgP, Pm = (1 << lgP) - 1;
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm + Ly.bars);
-  uint64_t *full = bars + pid * 4, *empty = bars + pid * 4 + 2;
-  int2 *myjobs = reinterpret_cast<int2 *>(sm + Ly.jobs) + pid * 2 * jcap;
-  int32_t *mycount = reinterpret_cast<int32_t *>(sm + Ly.jcount) + pid * 2;
+  uint64_t *full = bars + pid * 2 * kJobSlots, *empty = full + kJobSlots;
+  int2 *myjobs = reinterpret_cast<int2 *>(sm + Ly.jobs) + pid * kJobSlots * jcap;
+  int32_t *mycount = reinterpret_cast<int32_t *>(sm + Ly.jcount) + pid * kJobSlots;
   __shared__ uint32_t hist_all[kPairsWs][256];
   using Scan = cub::BlockScan<int, kPairsWs * 64>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ int s_work, s_free, s_apply;
   __shared__ unsigned long long s_ev;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kPairsWs * 2; ++i) {
-      mbar_init(&bars[(i >> 1) * 4 + (i & 1)], 1);
-      mbar_init(&bars[(i >> 1) * 4 + 2 + (i & 1)], 1);
-    }
+    for (int i = 0; i < kPairsWs * 2 * kJobSlots; ++i) mbar_init(&bars[i], 1);
     mbar_fence_init();
     s_ev = 0;
   }
@@ -229,8 +231,8 @@ select_move_ws_kernel(CompactArgs a) {
     char *vp8 = static_cast<char *>(a.vpool);
     int k = 0;
     for (int it = first; it < items; it += stride, ++k) {
-      const int sl = k & 1;
-      mbar_wait(&full[sl], (k >> 1) & 1);
+      const int sl = k & (kJobSlots - 1);
+      mbar_wait(&full[sl], (k / kJobSlots) & 1);
       const int nm = (a.exp & 1) ? 0 : mycount[sl];
       const int2 *jb = myjobs + sl * jcap;
       for (int c0 = 0; c0 < nm; c0 += rpi * kUw) {
@@ -468,8 +470,8 @@ select_move_ws_kernel(CompactArgs a) {
     if (nh != nm && lane == 0 && !a.exp) atomicOr(&a.ctrl->err, DERR_STATE);
     if (a.exp) nm = nm < nh ? nm : nh;
     // hand the job to the move warp
-    const int sl = k & 1;
-    mbar_wait(&empty[sl], ((k >> 1) & 1) ^ 1);
+    const int sl = k & (kJobSlots - 1);
+    mbar_wait(&empty[sl], ((k / kJobSlots) & 1) ^ 1);
     int2 *jb = myjobs + sl * jcap;
     for (int i = lane; i < nm; i += 32)
       jb[i] = make_int2(static_cast<int>(row(movers[i])), static_cast<int>(row(holes[i])));
