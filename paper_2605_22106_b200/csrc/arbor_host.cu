@@ -259,6 +259,8 @@ void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan 
     for (int x : path) leaves[x].push_back(b);
   }
   std::vector<int32_t> chunk_of(N, -1);
+  struct SingleItem { int node, pair, cnt, j0; };
+  std::vector<SingleItem> single;
   for (int x = 0; x < N; ++x) {
     if (leaves[x].empty()) continue;
     const int nch = (n_of[x] + kAttnChunk - 1) / kAttnChunk;
@@ -281,20 +283,45 @@ void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan 
         p.it_rec.push_back(std::min(kLeavesPerItem, lc - j0));
       }
     }
-    // tensor-core tiles: chunks (ch, ch+1) of one leaf group, one self-contained record each
-    // {node, c0, pair A, pair B or -1, cnt, leaf 0..5, 0} (one load per tile in the kernel)
+    // tensor-core tiles, one self-contained record each (kTileRecInts ints, one load per tile
+    // in the kernel): {node A, c0 A, pair A, cnt A, node B or -1, c0 B, pair B, cnt B,
+    // leaves[6], 0, 0}.  A node of ≥ 2 chunks: chunks (ch, ch+1) of one leaf group (B shares
+    // A's query columns: cnt B = 0).  Single-chunk items are packed two per tile below.
     const int cfirst = chunk_of[x];
-    for (int ch = 0; ch < nch; ch += 2)
-      for (int gi = 0; gi < ng; ++gi) {
-        const int j0 = gi * kLeavesPerItem, cnt = std::min(kLeavesPerItem, lc - j0);
-        p.tl_rec.push_back(x);
-        p.tl_rec.push_back(ch * kAttnChunk);
-        p.tl_rec.push_back(p.ch_poff[cfirst + ch] + j0);
-        p.tl_rec.push_back(ch + 1 < nch ? p.ch_poff[cfirst + ch + 1] + j0 : -1);
-        p.tl_rec.push_back(cnt);
+    for (int gi = 0; gi < ng; ++gi) {
+      const int j0 = gi * kLeavesPerItem, cnt = std::min(kLeavesPerItem, lc - j0);
+      if (nch == 1) {
+        single.push_back({x, p.ch_poff[cfirst] + j0, cnt, j0});
+        continue;
+      }
+      for (int ch = 0; ch < nch; ch += 2) {
+        const bool hb = ch + 1 < nch;
+        const int32_t r[8] = {x, ch * kAttnChunk, p.ch_poff[cfirst + ch] + j0, cnt,
+                              hb ? x : -1, (ch + 1) * kAttnChunk,
+                              hb ? p.ch_poff[cfirst + ch + 1] + j0 : -1, 0};
+        p.tl_rec.insert(p.tl_rec.end(), r, r + 8);
         for (int j = 0; j < kLeavesPerItem; ++j) p.tl_rec.push_back(j < cnt ? leaves[x][j0 + j] : 0);
         p.tl_rec.push_back(0);
+        p.tl_rec.push_back(0);
       }
+    }
+  }
+  // single-chunk items (short nodes, e.g. the open children of a DPTS frontier): two per tile,
+  // one per 64-slot half, each half with its own query columns, as long as the pair's leaves
+  // fit the plan's widest item (NQ unchanged)
+  for (size_t i = 0; i < single.size();) {
+    const SingleItem &u = single[i];
+    const bool two = i + 1 < single.size() && u.cnt + single[i + 1].cnt <= p.max_cnt;
+    const SingleItem &w = two ? single[i + 1] : u;
+    const int32_t r[8] = {u.node, 0, u.pair, u.cnt, two ? w.node : -1, 0, two ? w.pair : -1,
+                          two ? w.cnt : 0};
+    p.tl_rec.insert(p.tl_rec.end(), r, r + 8);
+    int nl = 0;
+    for (int j = 0; j < u.cnt; ++j) p.tl_rec.push_back(leaves[u.node][u.j0 + j]), ++nl;
+    if (two)
+      for (int j = 0; j < w.cnt; ++j) p.tl_rec.push_back(leaves[w.node][w.j0 + j]), ++nl;
+    for (; nl < kLeavesPerItem + 2; ++nl) p.tl_rec.push_back(0);
+    i += two ? 2 : 1;
   }
   p.bp_off.assign(1, 0);
   for (int b = 0; b < nA; ++b) {

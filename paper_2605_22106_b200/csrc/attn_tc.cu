@@ -74,8 +74,10 @@ struct TcArgs {
       a.trace[(static_cast<int64_t>(blockIdx.x) * 64 + (k)) * 16 + (e)] = clock64() - t_start; \
   } while (0)
 
+// cnt: leaves (8-column query slots) of the tile; meta: bit 0 a B half exists, bit 1 the B
+// half is packed (another node's chunk with its own columns [8·cntA, 8·cnt)), bits 4+: cntA
 struct TcHdr {
-  int ntA, ntB, li, h, pbA, pbB, cnt, hasB;
+  int ntA, ntB, li, h, pbA, pbB, cnt, meta;
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -365,6 +367,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   // ids — host-built, so it is read before griddepcontrol.wait), then k_cur and the page ids
   // (written by earlier kernels, so after it).
   int b_c0 = 0, b_pbA = 0, b_pbB = -1, b_cnt = 0, b_ntA = 0, b_ntB = 0, b_node = 0;
+  int b_nodeB = -1, b_c0B = 0, b_cntB = 0;
   int b_leaf[kLeavesPerItem];
   int b_page[kMaxTilePages];
   auto load_rec = [&](int k0) {
@@ -372,25 +375,28 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     if (kk < ntiles) {
       const int it = blockIdx.x + kk * gridDim.x;
       const int4 *r = a.pv.tl_rec + static_cast<int64_t>(it / HL) * (kTileRecInts / 4);
-      const int4 r0 = r[0], r1 = r[1], r2 = r[2];
-      b_node = r0.x; b_c0 = r0.y; b_pbA = r0.z; b_pbB = r0.w;
-      b_cnt = r1.x; b_leaf[0] = r1.y; b_leaf[1] = r1.z; b_leaf[2] = r1.w;
-      b_leaf[3] = r2.x; b_leaf[4] = r2.y; b_leaf[5] = r2.z;
+      const int4 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3];
+      b_node = r0.x; b_c0 = r0.y; b_pbA = r0.z; b_cnt = r0.w;
+      b_nodeB = r1.x; b_c0B = r1.y; b_pbB = r1.z; b_cntB = r1.w;
+      b_leaf[0] = r2.x; b_leaf[1] = r2.y; b_leaf[2] = r2.z; b_leaf[3] = r2.w;
+      b_leaf[4] = r3.x; b_leaf[5] = r3.y;
     }
   };
   auto load_state = [&](int k0) {
     const int kk = k0 + lane;
     if (kk < ntiles) {
       const int kc = a.kcur[b_node];
+      const int kcB = b_nodeB < 0 ? 0 : (b_nodeB == b_node ? kc : a.kcur[b_nodeB]);
       b_ntA = max(0, min(kHalf, kc - b_c0));
-      b_ntB = b_pbB >= 0 ? max(0, min(kHalf, kc - b_c0 - kHalf)) : 0;
+      b_ntB = b_nodeB >= 0 ? max(0, min(kHalf, kcB - b_c0B)) : 0;
       const int pgA = (b_ntA + P - 1) >> lgP, pgB = (b_ntB + P - 1) >> lgP;
       const int ppH = kHalf >> lgP;   // pages per 64-slot half
-      const int32_t *pt = a.ptab + static_cast<int64_t>(b_node) * a.g.MPN + (b_c0 >> lgP);
+      const int32_t *ptA = a.ptab + static_cast<int64_t>(b_node) * a.g.MPN + (b_c0 >> lgP);
+      const int32_t *ptB = a.ptab + static_cast<int64_t>(b_nodeB < 0 ? 0 : b_nodeB) * a.g.MPN + (b_c0B >> lgP);
 #pragma unroll
       for (int i = 0; i < kMaxTilePages; ++i) {
         const int half = i >= ppH, pi = i - half * ppH;
-        b_page[i] = (pi < (half ? pgB : pgA)) ? pt[half * ppH + pi] : 0;
+        b_page[i] = (pi < (half ? pgB : pgA)) ? (half ? ptB[pi] : ptA[pi]) : 0;
       }
     }
   };
@@ -473,7 +479,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         const int ntB = __shfl_sync(0xffffffffu, b_ntB, src);
         const int pbA = __shfl_sync(0xffffffffu, b_pbA, src);
         const int pbB = __shfl_sync(0xffffffffu, b_pbB, src);
-        const int cnt = __shfl_sync(0xffffffffu, b_cnt, src);
+        const int cntA = __shfl_sync(0xffffffffu, b_cnt, src);
+        const int cntB = __shfl_sync(0xffffffffu, b_cntB, src);   // > 0: packed B half
+        const int cnt = cntA + cntB;
         int page = 0, leaf = 0;       // lane i < pages: page i of the tile; lane i < cnt: leaf i
 #pragma unroll
         for (int i = 0; i < kMaxTilePages; ++i) {
@@ -493,7 +501,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         unsigned char *Ks = Kst(s);
         unsigned char *Qs = Ks + kKVBytes;
         if (lane == 0) {
-          hdr[r] = TcHdr{ntA, ntB, li, h, pbA, pbB, cnt, pbB >= 0 ? 1 : 0};
+          hdr[r] = TcHdr{ntA, ntB, li, h, pbA, pbB, cnt,
+                         (pbB >= 0 ? 1 : 0) | (cntB > 0 ? 2 : 0) | (cntA << 4)};
           mbar_arrive_expect_tx(&full_k[s], static_cast<uint32_t>(pgA + pgB) * P * 256u +
                                                 static_cast<uint32_t>(cnt) * 2048u);
         }
@@ -645,9 +654,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       if (tid == 64) TC_TRACE(k, 7);
       const TcHdr hd = hdr[k % RING];
       if (half == 0 && lane == 0 && quad == 0) ohdr[k & 3] = hd;   // for the epilogue warps
-      const unsigned long long cm = colmask(hd.cnt, G);
+      const int cntA = hd.meta >> 4;
+      const bool pack = (hd.meta & 2) != 0;
+      // this half's query columns: a packed B half has its own, after A's
+      const unsigned long long cm = (half && pack) ? colmask(hd.cnt - cntA, G) << (8 * cntA)
+                                                   : colmask(cntA, G);
+      const int lofs = (half && pack) ? cntA : 0;   // first leaf slot of this half's pair group
       const int nt = half ? hd.ntB : hd.ntA;
-      const bool present = half == 0 || hd.hasB;
+      const bool present = half == 0 || (hd.meta & 1);
       const int pb = half ? hd.pbB : hd.pbA;
       const bool valid = present && tc < nt;
       const int ngrp = (min(NQ, 8 * hd.cnt) + GW - 1) / GW;
@@ -692,7 +706,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 #pragma unroll
           for (int i = 0; i < GW; ++i) {
             const int n = c + i;
-            if ((cm >> n) & 1ull) zr[static_cast<int64_t>((n >> 3) * SP + (n & 7)) * kAttnChunk] = z[i];
+            if ((cm >> n) & 1ull) zr[static_cast<int64_t>(((n >> 3) - lofs) * SP + (n & 7)) * kAttnChunk] = z[i];
           }
         }
       }
@@ -744,8 +758,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
              (red_l[k & 3][2][etid] + red_l[k & 3][3][etid]);
       }
       const int ngrp = (min(NQ, 8 * hd.cnt) + GW - 1) / GW;
-      const unsigned long long cm = colmask(hd.cnt, G);
+      // columns of leaf slot j < cntA belong to pair A's group; a packed B half's columns
+      // (slots cntA..cnt−1) to pair B's group
+      const int cntA = hd.meta >> 4;
+      const bool pack = (hd.meta & 2) != 0;
+      const unsigned long long cm = pack ? colmask(cntA, G) | (colmask(hd.cnt - cntA, G) << (8 * cntA))
+                                         : colmask(cntA, G);
       float *pa = a.partials + ((static_cast<int64_t>(hd.pbA) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
+      float *pbq = a.partials + ((static_cast<int64_t>(pack ? hd.pbB : hd.pbA) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow -
+                   static_cast<int64_t>(cntA) * SP * 130;     // so that slot j ≥ cntA lands at j − cntA
+      auto col_ptr = [&](int n) {
+        return ((n >> 3) < cntA ? pa : pbq) + static_cast<int64_t>((n >> 3) * SP + (n & 7)) * 130;
+      };
 #pragma unroll 1
       for (int gi = 0; gi < ngrp; ++gi) {
         const int c = gi * GW;
@@ -754,13 +778,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 #pragma unroll
         for (int i = 0; i < GW; ++i) {
           const int n = c + i;
-          if ((cm >> n) & 1ull) pa[static_cast<int64_t>((n >> 3) * SP + (n & 7)) * 130] = o[i];
+          if ((cm >> n) & 1ull) *col_ptr(n) = o[i];
         }
       }
       tc_fence_before();
       mbar_arrive(&o_empty[b]);
       if (etid < NQ && ((cm >> etid) & 1ull)) {
-        float *dst = pa - trow + static_cast<int64_t>((etid >> 3) * SP + (etid & 7)) * 130;
+        float *dst = col_ptr(etid) - trow;
         dst[128] = mm;
         dst[129] = ll;
       }

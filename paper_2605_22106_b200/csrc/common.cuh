@@ -18,7 +18,7 @@ namespace arbor {
 
 constexpr int kAttnChunk = 64;       // slots per attention / score chunk
 constexpr int kLeavesPerItem = 6;    // active leaves per attention work item (q rows staged)
-constexpr int kTileRecInts = 12;     // tensor-core tile record: {node, c0, pbA, pbB, cnt, leaves[6], 0}
+constexpr int kTileRecInts = 16;     // tensor-core tile record (build_plan): 2 halves + leaves[6]
 constexpr int kStashSlots = 4;
 constexpr int kQMaps = 4;            // cached q tensor maps (attn_tc.cu)
 constexpr int kRingSlots = 32;
