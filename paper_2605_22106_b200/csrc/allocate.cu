@@ -19,7 +19,10 @@
 namespace arbor {
 namespace {
 
-constexpr int kThreads = 512;
+#ifndef ARBOR_ALLOC_THREADS
+#define ARBOR_ALLOC_THREADS 512
+#endif
+constexpr int kThreads = ARBOR_ALLOC_THREADS;
 constexpr double kWeightScale = 16777216.0;   // 2^24
 constexpr double kEps = 1e-9;
 
