@@ -87,8 +87,7 @@ def main():
             rec = {"N": N, "tokens": T, "rho": rho, "budget": B}
             restore()
             try:
-                ctx.arbor_tree_decode_attn(ta, q, out, lse)
-                ctx.arbor_score(ta, q, lse, s_buf)
+                ctx.arbor_decode_step(ta, q, out, lse, s_buf)
                 ctx.arbor_allocate(ta, s_buf, B, k_buf)
             except ArborError as e:
                 if e.status != 3:
@@ -104,8 +103,7 @@ def main():
                 restore()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                ctx.arbor_tree_decode_attn(ta, q, out, lse)
-                ctx.arbor_score(ta, q, lse, s_buf)
+                ctx.arbor_decode_step(ta, q, out, lse, s_buf)
                 ctx.arbor_allocate(ta, s_buf, B, k_buf)
                 ctx.arbor_evict(ta, k_buf)
                 b.record(stream)
@@ -116,8 +114,7 @@ def main():
             pages = ctx.arbor_read_counters()[1]
 
             def decode():
-                ctx.arbor_tree_decode_attn(ta, q, out, lse)
-                ctx.arbor_score(ta, q, lse, s_buf)
+                ctx.arbor_decode_step(ta, q, out, lse, s_buf)
 
             dms = timed(decode, args.reps)
             if rho == 1.0:

@@ -82,8 +82,7 @@ def run(expansions, rho, t_node, seed, controlled, budget=None):
         q = sc.queries(50_000 + step[0], 1)
         out = torch.empty_like(q)
         lse = torch.empty((1, L, ctx.Hq), dtype=torch.float32, device=dev)
-        dec_ms.append(timed(lambda: (ctx.arbor_tree_decode_attn(tree, q, out, lse),
-                                     ctx.arbor_score(tree, q, lse))))
+        dec_ms.append(timed(lambda: ctx.arbor_decode_step(tree, q, out, lse)))
         step[0] += 1
 
     t0 = time.perf_counter()
