@@ -95,8 +95,6 @@ __device__ __forceinline__ void divmod128(unsigned __int128 X, unsigned long lon
 
 __global__ void __launch_bounds__(kThreads)
 allocate_kernel(AllocArgs a) {
-  pdl_wait();
-  pdl_trigger();
   TRACE(0);
   extern __shared__ __align__(16) unsigned char sm[];
   const int N = a.N;
@@ -115,7 +113,10 @@ allocate_kernel(AllocArgs a) {
 
   // ---- a1 geometry (Alg. 2; Q14), fused: parent pointers in smem; depth by
   // walking to the root, Path* = ∪ root→ℓ chains, Δ_i = min_ℓ d_i + d_ℓ − 2·d_lca(i, ℓ).
-  // Results also go to global memory (depth, Δ, Path*, pinned) for arbor_evict.
+  // Results also go to global memory (depth, Δ, Path*, pinned) for arbor_evict.  The tree
+  // (parent, active) is uploaded by a copy before any kernel of the call, so the walks run
+  // before griddepcontrol.wait and overlap the previous kernel's tail; the global writes
+  // (which an earlier evict may still be reading) and every other read come after it.
   int *par = reinterpret_cast<int *>(cand + 3 * a.Mpad);         // [N] (after the candidates)
   int *dep = par + N;                                            // [N]
   int *dlt = dep + N;                                            // [N]
@@ -145,8 +146,12 @@ allocate_kernel(AllocArgs a) {
       best = dist < best ? dist : best;
     }
     dlt[i] = best;
-    a.depth[i] = di;
-    a.delta[i] = best;
+  }
+  pdl_wait();
+  pdl_trigger();
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    a.depth[i] = dep[i];
+    a.delta[i] = dlt[i];
     a.onpath[i] = onp[i];
     a.pinned[i] = (onp[i] || a.open[i]) ? 1 : 0;
   }

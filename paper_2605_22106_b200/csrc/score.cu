@@ -432,6 +432,17 @@ decode_post_kernel(PostArgs pa) {
   // first batch of score_row's metadata: overlaps the attention kernel's tail
   const ChunkMeta pre_c = load_chunk_meta(f, warp + NW * lane, part, nparts);
   const MassMeta pre_m = load_mass_meta(f, warp + NW * lane, part, nparts);
+  // … and the first (leaf, q head) item's path bounds and this lane's first pair (plan arrays)
+  int pre_p0 = 0, pre_p1 = 0, pre_pi = 0;
+  {
+    const int it = threadIdx.x >> 3;
+    if (it < pa.nA * a.G) {
+      const int b = it / a.G;
+      pre_p0 = a.pv.bp_off[b];
+      pre_p1 = a.pv.bp_off[b + 1];
+      if (pre_p0 + (lane & 7) < pre_p1) pre_pi = a.pv.bp_list[pre_p0 + (lane & 7)];
+    }
+  }
   pdl_wait();
   pdl_trigger();
   const int G = a.G;
@@ -447,11 +458,13 @@ decode_post_kernel(PostArgs pa) {
     for (int it0 = (threadIdx.x >> 3); it0 < ((nitems + 3) & ~3); it0 += kFusedThreads / 8) {
       const int it = it0;
       const bool ok = it < nitems;
+      const bool first = it0 == (threadIdx.x >> 3);   // prefetched before griddepcontrol.wait
       const int b = ok ? it / G : 0, g = ok ? it - b * G : 0;
-      const int p0 = ok ? a.pv.bp_off[b] : 0, p1 = ok ? a.pv.bp_off[b + 1] : 0;
+      const int p0 = ok ? (first ? pre_p0 : a.pv.bp_off[b]) : 0;
+      const int p1 = ok ? (first ? pre_p1 : a.pv.bp_off[b + 1]) : 0;
       float M = -INFINITY, Ls = 0.f;
       for (int i = p0 + sub; i < p1; i += 8) {
-        const float *pp = part_ptr(a.pv.bp_list[i], g);
+        const float *pp = part_ptr((first && i == p0 + sub) ? pre_pi : a.pv.bp_list[i], g);
         const float m2 = pp[D], l2 = pp[D + 1];
         if (m2 == -INFINITY) continue;
         if (m2 > M) {
