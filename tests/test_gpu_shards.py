@@ -1,0 +1,92 @@
+"""KV-head sharding on one GPU: the multi-GPU path splits the
+rows (layer, KV head) across ranks and all-reduces int64 partial node masses.  Here the
+"ranks" are contexts over disjoint KV-head ranges on the same device (world size 1 each, so
+no NCCL): every shard runs the same arbor_decode_step calls on its slice of the queries, and
+
+* its accumulated attention A equals the full context's rows bit for bit (rows are
+  independent: same tiles, same logits, same LSEs, same summation order);
+* the shards' partial masses sum (int64, any order) to the full context's Mass exactly —
+  the identity the NCCL all-reduce relies on for rank-invariant s, k and page tables;
+* s from the summed masses matches the full context's s, and from the same scores every
+  shard allocates the same k and evicts to the same page tables and free list.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import msve as omsve, tae as otae
+from paper_2605_22106_b200 import workload
+
+from gpu_helpers import oracle_params
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("shards", [2, 4])
+def test_head_shards_sum_to_full(shards):
+    preset = dict(tree=("full", 3, 4, 96), L=3, H=8, Hq=32, d=128, dtype="bf16", P=16, rho=0.5,
+                  params={}, active="highest_v")
+    workload.PRESETS["_shard_test"] = preset
+    try:
+        full = workload.setup("_shard_test", 5)
+        hc = preset["H"] // shards
+        parts = [workload.setup("_shard_test", 5, kv_head_begin=r * hc, kv_head_count=hc)
+                 for r in range(shards)]
+    finally:
+        del workload.PRESETS["_shard_test"]
+    tree = full.tree
+    leaves = synth.leaves_of(tree)
+    for step in range(12):
+        act = [leaves[(5 * step + j) % len(leaves)] for j in range(1 + step % 3)]
+        for sc in [full] + parts:
+            sc.tree.active = act
+            q = sc.queries(step, len(act))
+            out = torch.empty_like(q)
+            lse = torch.empty((len(act), sc.ctx.L, sc.ctx.Hq), dtype=torch.float32, device="cuda")
+            sc.ctx.arbor_decode_step(sc.tree, q, out, lse)
+    torch.cuda.synchronize()
+    A = full.ctx.score.cpu()
+    for r, sc in enumerate(parts):
+        assert torch.equal(sc.ctx.score.cpu(), A[:, r * hc:(r + 1) * hc]), f"A rows of shard {r}"
+    N = tree.num_nodes
+    fs = full.ctx.arbor_read_scores(N)
+    ps = [sc.ctx.arbor_read_scores(N) for sc in parts]
+    mass = sum(p["mass"] for p in ps)
+    mclose = sum(p["mclose"] for p in ps)
+    assert np.array_equal(mass, fs["mass"]), "partial masses do not sum to the full Mass"
+    assert np.array_equal(mclose, fs["mclose"])
+    for p in ps:
+        assert np.array_equal(p["nq"], fs["nq"])
+    # s from the summed masses (oracle MSVE, the rank-side arithmetic after the all-reduce)
+    op = oracle_params(preset["params"])
+    s = []
+    for i in range(N):
+        if tree.is_open[i]:
+            s.append(0.5)
+            continue
+        a = omsve.attention_feature(int(mass[i]), int(mclose[i]), int(fs["nq"][i]), preset["L"],
+                                    preset["Hq"])
+        s.append(float(np.float32(omsve.msve_score(op["theta"], float(tree.v[i]),
+                                                   float(tree.u[i]), a))))
+    # the library's fp64 MSVE vs the oracle's: within one f32 ulp (as test_gpu_parity)
+    assert np.all(np.abs(np.asarray(s, np.float64) - fs["s"].astype(np.float64)) <= 2.0 ** -23)
+    # every rank allocates from the same (all-reduced) scores: identical k on every shard
+    B = int(math.floor(preset["rho"] * tree.total_tokens))
+    k_full = torch.empty(N, dtype=torch.int32, device="cuda")
+    s_dev = torch.as_tensor(fs["s"], device="cuda")
+    full.ctx.arbor_allocate(tree, s_dev, B, k_full)
+    assert int(k_full.sum()) == B
+    for sc in parts:
+        k = torch.empty(N, dtype=torch.int32, device="cuda")
+        sc.ctx.arbor_allocate(sc.tree, s_dev, B, k)
+        assert torch.equal(k, k_full), "rank-side allocation"
+    # and the same evictions: page tables and free lists identical across shards
+    for sc in [full] + parts:
+        sc.ctx.arbor_evict(sc.tree, k_full)
+    ref = [full.ctx.arbor_read_node(i) for i in range(N)]
+    for sc in parts:
+        assert [sc.ctx.arbor_read_node(i) for i in range(N)] == ref, "page tables differ"
+        assert sc.ctx.arbor_read_free_list() == full.ctx.arbor_read_free_list()
