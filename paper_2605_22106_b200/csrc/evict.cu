@@ -467,8 +467,11 @@ select_move_ws_kernel(CompactArgs a) {
       nm += __popc(mb);
     }
     __syncwarp();
+    // holes and movers pair up exactly when the kept keys are unique (they are for a
+    // consistent state: one pos tag per position); otherwise latch the error and move only the
+    // pairs that exist, so a corrupted state can never produce out-of-range rows
     if (nh != nm && lane == 0 && !a.exp) atomicOr(&a.ctrl->err, DERR_STATE);
-    if (a.exp) nm = nm < nh ? nm : nh;
+    nm = nm < nh ? nm : nh;
     // hand the job to the move warp
     const int sl = k & (kJobSlots - 1);
     mbar_wait(&empty[sl], ((k / kJobSlots) & 1) ^ 1);
