@@ -165,18 +165,20 @@ struct FusedArgs {
 
 constexpr int kFusedThreads = 256;
 
-__device__ __forceinline__ void msve_one(const MsveArgs &m, int i) {
+// MSVE of node i from its inputs (open flag, Nq, Mass, Mclose, v, u): a_i, s_i (fp64, no
+// contraction, same expression order as msve_kernel and the oracle)
+__device__ __forceinline__ void msve_compute(const MsveArgs &m, int i, bool open, long long nq,
+                                             long long mass, long long mclose, float v, float u) {
   float s = 0.5f, af = 0.f;
-  if (!m.open[i]) {
+  if (!open) {
     double a = 0.0;
-    const long long nq = m.nq[i];
     if (nq > 0) {
-      const double num = static_cast<double>(m.mass2[i] - m.mass2[m.N + i]) * (1.0 / 16777216.0);
+      const double num = static_cast<double>(mass - mclose) * (1.0 / 16777216.0);
       a = __ddiv_rn(num, __dmul_rn(static_cast<double>(nq), m.norm));
       a = fmin(1.0, fmax(0.0, a));
     }
-    double z = __dadd_rn(m.th0, __dmul_rn(m.thv, static_cast<double>(m.v[i])));
-    z = __dadd_rn(z, __dmul_rn(m.thu, static_cast<double>(m.u[i])));
+    double z = __dadd_rn(m.th0, __dmul_rn(m.thv, static_cast<double>(v)));
+    z = __dadd_rn(z, __dmul_rn(m.thu, static_cast<double>(u)));
     z = __dadd_rn(z, __dmul_rn(m.tha, a));
     double sd = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-z)));
     sd = fmin(1.0, fmax(0.0, sd));
@@ -185,7 +187,7 @@ __device__ __forceinline__ void msve_one(const MsveArgs &m, int i) {
     m.s_state[i] = s;
   }
   m.a_out[i] = af;
-  if (m.s_out) m.s_out[i] = m.open[i] ? 0.5f : s;
+  if (m.s_out) m.s_out[i] = open ? 0.5f : s;
 }
 
 // Steps (1)-(3) of one (row, part) CTA; lse2(b, g) gives the log2-domain LSE of leaf b's
@@ -362,29 +364,55 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
       if (lane == 0) atomicAdd(&f.acc[node], static_cast<unsigned long long>(__double2ll_rn(m * 16777216.0)));
     }
   }
-  // (3) last CTA: publish, reset, MSVE
+  // (3) last CTA: publish, reset, MSVE.  Thread t owns nodes t, t + 256, …: the listed
+  // (recomputed) ones take the accumulated sum, the rest keep their cached partial mass.
+  // The inputs of each thread's first node and the listed-node bitmap are loaded before
+  // the ticket (plan data and library state this kernel does not write), so the last CTA's
+  // serial tail is one round trip (the accumulators) plus the MSVE arithmetic.
+  constexpr int kMaxNodes = 3072;                      // arbor_init's max_nodes bound
+  __shared__ unsigned listed[kMaxNodes / 32];
   __shared__ bool last;
+  for (int w = tid; w < (f.N + 31) / 32; w += kFusedThreads) listed[w] = 0u;
+  const int i0 = tid;
+  bool p_open = true;
+  long long p_nq = 0, p_part = 0, p_mclose = 0;
+  float p_v = 0.f, p_u = 0.f;
+  if (i0 < f.N) {
+    p_open = f.m.open[i0] != 0;
+    p_nq = f.m.nq[i0];
+    p_part = f.mass_part[i0];
+    p_mclose = f.mclose[i0];
+    p_v = f.m.v[i0];
+    p_u = f.m.u[i0];
+  }
+  __syncthreads();
+  for (int mi = tid; mi < f.n_mass; mi += kFusedThreads) {
+    const int node = f.mass_nodes[mi];
+    atomicOr(&listed[node >> 5], 1u << (node & 31));
+  }
   __threadfence();
   __syncthreads();
   if (tid == 0) last = atomicAdd(f.ticket, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int mi = tid; mi < f.n_mass; mi += kFusedThreads) {
-    const int node = f.mass_nodes[mi];
-    volatile unsigned long long *acc = f.acc;
-    f.mass_part[node] = static_cast<int64_t>(acc[node]);
-    acc[node] = 0ull;
-  }
   if (tid == 0) *f.ticket = 0u;
-  __syncthreads();
   for (int i = tid; i < f.N; i += kFusedThreads) {
-    f.mass2[i] = f.mass_part[i];
-    f.mass2[f.N + i] = f.mclose[i];
+    const bool first = i == i0;
+    long long mass = first ? p_part : f.mass_part[i];
+    if ((listed[i >> 5] >> (i & 31)) & 1u) {
+      volatile unsigned long long *acc = f.acc;
+      mass = static_cast<long long>(acc[i]);
+      acc[i] = 0ull;
+      f.mass_part[i] = mass;
+    }
+    const long long mclose = first ? p_mclose : f.mclose[i];
+    f.mass2[i] = mass;
+    f.mass2[f.N + i] = mclose;
+    if (f.do_msve)
+      msve_compute(f.m, i, first ? p_open : f.m.open[i] != 0, first ? p_nq : f.m.nq[i], mass,
+                   mclose, first ? p_v : f.m.v[i], first ? p_u : f.m.u[i]);
   }
-  if (!f.do_msve) return;
-  __syncthreads();
-  for (int i = tid; i < f.N; i += kFusedThreads) msve_one(f.m, i);
 }
 
 __global__ void __launch_bounds__(kFusedThreads)
