@@ -75,6 +75,33 @@ __device__ T block_sum(T v, T *red) {
   return red[32];
 }
 
+// K integer block sums in one pass (three barriers instead of 3·K); exact, order-free
+template <int K>
+__device__ void block_sum_k(long long (&v)[K], long long (*red)[K]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) red[w][k] = v[k];
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      long long x = lane < nw ? red[lane][k] : 0ll;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) red[32][k] = x;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = red[32][k];
+}
+
 // floor(X / den) and X mod den for 0 ≤ X < 2^126, 0 < den < 2^62, with a small quotient
 __device__ __forceinline__ void divmod128(unsigned __int128 X, unsigned long long den,
                                           unsigned long long &q, unsigned long long &r) {
@@ -254,12 +281,12 @@ allocate_kernel(AllocArgs a) {
       if (cls[j] == 1) SnP += nn[j];
       if (cls[j] == 2) { SfZ += f[j]; SslZ += nn[j] - f[j]; }
     }
-    T = block_sum(T, red64);
-    pinned_n = block_sum(pinned_n, red64);
-    free_n = block_sum(free_n, red64);
-    SnP = block_sum(SnP, red64);
-    SfZ = block_sum(SfZ, red64);
-    SslZ = block_sum(SslZ, red64);
+    {
+      __shared__ long long red6[33][6];
+      long long v6[6] = {T, pinned_n, free_n, SnP, SfZ, SslZ};
+      block_sum_k<6>(v6, red6);
+      T = v6[0]; pinned_n = v6[1]; free_n = v6[2]; SnP = v6[3]; SfZ = v6[4]; SslZ = v6[5];
+    }
     TRACE(2);
     const long long Bp = a.budget - pinned_n;
     if (T <= a.budget || Bp >= free_n) {
@@ -436,8 +463,13 @@ allocate_kernel(AllocArgs a) {
         else if (f[j] > 0 && Wd <= static_cast<long long>(f[j]) * bnum) { k[j] = f[j]; Sb += f[j]; cls[j] = 5; }
         else { Den += W[j]; cls[j] = 6; }   // active
       }
-      Sb = block_sum(Sb, red64);
-      Den = block_sum(Den, red64);
+      {
+        __shared__ long long red2[33][2];
+        long long v2[2] = {Sb, Den};
+        block_sum_k<2>(v2, red2);
+        Sb = v2[0];
+        Den = v2[1];
+      }
       const long long Num = Bpp - Sb;
       long long given = 0;
       for (int j = threadIdx.x; j < N; j += blockDim.x) {
