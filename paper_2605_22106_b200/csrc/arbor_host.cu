@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -875,7 +876,14 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
 arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void *q, void *out,
                                float *lse_out, float *s_out) {
   if (!c) return ARBOR_ERR_INVALID_ARG;
+  static const bool htrace = getenv("ARBOR_HOST_TRACE") != nullptr;   // diagnostics
+  using clk = std::chrono::steady_clock;
+  clk::time_point ht[8];
+  int hn = 0;
+  auto mark = [&]() { if (htrace) ht[hn++] = clk::now(); };
+  mark();
   TRY(check_tree(c, tree));
+  mark();
   if (!q || !out) return fail(c, ARBOR_ERR_INVALID_ARG, "q / out is NULL");
   const int N = tree->num_nodes, nA = tree->num_active;
   if (!decode_post_fits(c, nA)) {   // more (leaf, q-head) pairs than the merge keeps on chip
@@ -884,24 +892,39 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
     return arbor_score(c, tree, q, nullptr, s_out);
   }
   TRY(upload_tree(c, tree));
+  mark();
   HostPlan hp;
   build_plan(tree, c->h_n, hp, c->tc_ok);
   std::vector<int32_t> mass_nodes;
   score_bookkeeping(c, tree, hp, mass_nodes);
+  mark();
   PlanView pv{};
   const int32_t *d_mass_nodes = nullptr;
   TRY(upload_plan(c, hp, nA, true, &mass_nodes, pv, &d_mass_nodes));
   TRY(ensure_partials(c, hp.pair_b.size(), c->L));
+  mark();
   launch_attn_partial(c, pv, q, 0, c->L, hp.max_cnt, out, lse_out);
   CK_LAUNCH();
+  mark();
   const bool single = c->cfg.world_size == 1;
   // parts per row: no more CTAs than one resident wave (2 per SM at the kernel's bounds)
   int parts = score_parts(mass_nodes.size());
   while (parts > 1 && c->L * c->H * parts > 2 * c->num_sms) parts /= 2;
-  if (const char *e = getenv("ARBOR_POST_PARTS")) parts = atoi(e);   // diagnostics
+  static const int parts_env = getenv("ARBOR_POST_PARTS") ? atoi(getenv("ARBOR_POST_PARTS")) : 0;
+  if (parts_env > 0) parts = parts_env;   // diagnostics
   launch_decode_post(c, pv, out, lse_out, d_mass_nodes, static_cast<int>(mass_nodes.size()), N,
                      single, s_out, parts);
   CK_LAUNCH();
+  mark();
+  if (htrace) {
+    fprintf(stderr, "[arbor host] decode_step us: check %.1f upload_tree %.1f plan %.1f upload_plan %.1f attn_launch %.1f post_launch %.1f\n",
+            std::chrono::duration<double, std::micro>(ht[1] - ht[0]).count(),
+            std::chrono::duration<double, std::micro>(ht[2] - ht[1]).count(),
+            std::chrono::duration<double, std::micro>(ht[3] - ht[2]).count(),
+            std::chrono::duration<double, std::micro>(ht[4] - ht[3]).count(),
+            std::chrono::duration<double, std::micro>(ht[5] - ht[4]).count(),
+            std::chrono::duration<double, std::micro>(ht[6] - ht[5]).count());
+  }
   c->lg_epoch = -1;
   c->mass_valid = true;
   if (!single) TRY(score_allreduce(c, N, s_out));
