@@ -198,34 +198,40 @@ arbor_status check_tree(arbor_ctx *c, const arbor_tree *t, std::vector<int32_t> 
 }
 
 // ---------------------------------------------------------------- tree upload (+ a1)
-arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
+// the device tree mirror already holds this tree
+static bool tree_same(const arbor_ctx *c, const arbor_tree *t) {
   const int N = t->num_nodes, nA = t->num_active;
-  bool same = c->tree_valid && static_cast<int>(c->t_parent.size()) == N &&
-              static_cast<int>(c->t_active.size()) == nA;
-  if (same) {
-    same = std::memcmp(c->t_parent.data(), t->parent, N * 4) == 0 &&
-           std::memcmp(c->t_len.data(), t->span_len, N * 4) == 0 &&
-           std::memcmp(c->t_active.data(), t->active, nA * 4) == 0 &&
-           std::memcmp(c->t_open.data(), t->is_open, N) == 0 &&
-           std::memcmp(c->t_v.data(), t->search_value, N * 4) == 0 &&
-           std::memcmp(c->t_u.data(), t->uncertainty, N * 4) == 0;
-  }
-  if (same) return ARBOR_OK;
-  // pack [parent | len | active | v | u | open] with the device block's fixed offsets
+  return c->tree_valid && static_cast<int>(c->t_parent.size()) == N &&
+         static_cast<int>(c->t_active.size()) == nA &&
+         std::memcmp(c->t_parent.data(), t->parent, N * 4) == 0 &&
+         std::memcmp(c->t_len.data(), t->span_len, N * 4) == 0 &&
+         std::memcmp(c->t_active.data(), t->active, nA * 4) == 0 &&
+         std::memcmp(c->t_open.data(), t->is_open, N) == 0 &&
+         std::memcmp(c->t_v.data(), t->search_value, N * 4) == 0 &&
+         std::memcmp(c->t_u.data(), t->uncertainty, N * 4) == 0;
+}
+
+// bytes of the device tree mirror block [parent | len | active | v | u | open]
+static size_t tree_block_bytes(const arbor_ctx *c) {
+  return static_cast<size_t>(c->max_nodes) * 16 + static_cast<size_t>(c->max_active) * 4 +
+         c->max_nodes;
+}
+
+// pack the tree with the device block's fixed offsets into host memory b
+static void pack_tree(const arbor_ctx *c, const arbor_tree *t, char *b) {
+  const int N = t->num_nodes, nA = t->num_active;
   const size_t MN = c->max_nodes, MA = c->max_active;
-  const size_t bytes = MN * 4 * 4 + MA * 4 + MN;
-  void *buf = nullptr;
-  TRY(ring_acquire(c, bytes, &buf));
-  char *b = static_cast<char *>(buf);
   std::memcpy(b, t->parent, N * 4);
   std::memcpy(b + MN * 4, t->span_len, N * 4);
   std::memcpy(b + MN * 8, t->active, nA * 4);
   std::memcpy(b + MN * 8 + MA * 4, t->search_value, N * 4);
   std::memcpy(b + MN * 12 + MA * 4, t->uncertainty, N * 4);
   std::memcpy(b + MN * 16 + MA * 4, t->is_open, N);
-  CK(cudaMemcpyAsync(c->d.parent, b, bytes, cudaMemcpyHostToDevice, c->ms));
-  CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
-  // a1 runs inside arbor_allocate's kernel; arbor_evict launches it only if needed
+}
+
+// host caches of the uploaded tree
+static void tree_commit(arbor_ctx *c, const arbor_tree *t) {
+  const int N = t->num_nodes, nA = t->num_active;
   c->t_parent.assign(t->parent, t->parent + N);
   c->t_len.assign(t->span_len, t->span_len + N);
   c->t_active.assign(t->active, t->active + nA);
@@ -234,6 +240,18 @@ arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
   c->t_u.assign(t->uncertainty, t->uncertainty + N);
   c->tree_valid = true;
   ++c->tree_version;
+}
+
+arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
+  if (tree_same(c, t)) return ARBOR_OK;
+  const size_t bytes = tree_block_bytes(c);
+  void *buf = nullptr;
+  TRY(ring_acquire(c, bytes, &buf));
+  pack_tree(c, t, static_cast<char *>(buf));
+  CK(cudaMemcpyAsync(c->d.parent, buf, bytes, cudaMemcpyHostToDevice, c->ms));
+  CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
+  // a1 runs inside arbor_allocate's kernel; arbor_evict launches it only if needed
+  tree_commit(c, t);
   return ARBOR_OK;
 }
 
@@ -338,9 +356,13 @@ void build_plan(const arbor_tree *t, const std::vector<int32_t> &n_of, HostPlan 
   }
 }
 
-// Upload [plan arrays | extra int32 list] (+ Nq when with_nq); fill a PlanView.
+// Upload [plan arrays | extra int32 list] (+ Nq when with_nq); fill a PlanView.  With a
+// tree t, the tree mirror is (re)uploaded too — in the SAME copy when the plan fits the
+// inline segment that follows the tree block on the device (every H2D copy on the stream
+// costs ~4 µs of device time: C2 step 220 → 216 µs for one copy fewer, A/B).
 arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
-                         const std::vector<int32_t> *extra, PlanView &pv, const int32_t **d_extra) {
+                         const std::vector<int32_t> *extra, PlanView &pv, const int32_t **d_extra,
+                         const arbor_tree *t = nullptr) {
   std::vector<int32_t> packed;
   auto put = [&](const std::vector<int32_t> &v) {
     const size_t off = packed.size();
@@ -354,15 +376,46 @@ arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
                o_bpl = put(p.bp_list);
   const size_t o_extra = packed.size();
   if (extra) put(*extra);
-  const size_t plan_bytes = packed.size() * 4;
-  if (plan_bytes > c->seg_cap) {
-    if (c->d.seg) CK(cudaFree(c->d.seg));
-    c->seg_cap = std::max<size_t>(plan_bytes * 2, 1 << 16);
-    CK(cudaMalloc(&c->d.seg, c->seg_cap));
+  // Nq (int64, 8-byte aligned) rides in the same copy: one cudaMemcpyAsync per call
+  if (packed.size() & 1) packed.push_back(0);
+  const size_t o_nq = packed.size();
+  static const bool split_nq = getenv("ARBOR_SPLIT_NQ") != nullptr;   // A/B: separate copy
+  if (with_nq && split_nq) {
+    TRY(ring_upload(c, c->d.nq, c->h_nq.data(), c->num_known * sizeof(int64_t)));
+    c->nq_dev = c->d.nq;
+  } else if (with_nq) {
+    packed.resize(o_nq + 2 * static_cast<size_t>(c->num_known));
+    std::memcpy(packed.data() + o_nq, c->h_nq.data(), c->num_known * sizeof(int64_t));
   }
-  if (!packed.empty()) TRY(ring_upload(c, c->d.seg, packed.data(), plan_bytes));
-  if (with_nq) TRY(ring_upload(c, c->d.nq, c->h_nq.data(), c->num_known * sizeof(int64_t)));
-  const int32_t *base = c->d.seg;
+  const size_t plan_bytes = packed.size() * 4;
+  const int32_t *base = nullptr;
+  const bool tree_new = t && !tree_same(c, t);
+  if (plan_bytes <= kInlineSeg) {
+    base = c->d.inline_seg;
+    if (tree_new) {   // one copy: [tree block | pad | plan] → [d.parent … inline_seg]
+      const size_t off = reinterpret_cast<const char *>(c->d.inline_seg) -
+                         reinterpret_cast<const char *>(c->d.parent);
+      void *buf = nullptr;
+      TRY(ring_acquire(c, off + plan_bytes, &buf));
+      pack_tree(c, t, static_cast<char *>(buf));
+      if (plan_bytes) std::memcpy(static_cast<char *>(buf) + off, packed.data(), plan_bytes);
+      CK(cudaMemcpyAsync(c->d.parent, buf, off + plan_bytes, cudaMemcpyHostToDevice, c->ms));
+      CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
+      tree_commit(c, t);
+    } else if (!packed.empty()) {
+      TRY(ring_upload(c, c->d.inline_seg, packed.data(), plan_bytes));
+    }
+  } else {
+    if (tree_new) TRY(upload_tree(c, t));
+    if (plan_bytes > c->seg_cap) {
+      if (c->d.seg) CK(cudaFree(c->d.seg));
+      c->seg_cap = std::max<size_t>(plan_bytes * 2, 1 << 16);
+      CK(cudaMalloc(&c->d.seg, c->seg_cap));
+    }
+    TRY(ring_upload(c, c->d.seg, packed.data(), plan_bytes));
+    base = c->d.seg;
+  }
+  if (with_nq && !split_nq) c->nq_dev = reinterpret_cast<const int64_t *>(base + o_nq);
   pv.ch_node = base + o_cn;
   pv.ch_chunk = base + o_cc;
   pv.ch_poff = base + o_cpo;
@@ -599,9 +652,12 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   ALLOC(d.ctrl, 1);
   {
     // tree mirror block: [parent | len | active | v | u | open] (fixed offsets, see upload_tree)
+    // followed (16-byte aligned) by the inline plan segment (upload_plan: one copy for both)
     char *blk = nullptr;
-    const size_t bytes = static_cast<size_t>(MN) * 16 + static_cast<size_t>(MA) * 4 + MN;
+    const size_t tb = (static_cast<size_t>(MN) * 16 + static_cast<size_t>(MA) * 4 + MN + 255) & ~size_t(255);
+    const size_t bytes = tb + kInlineSeg;
     if (cudaMalloc(&blk, bytes) != cudaSuccess) return bail(ARBOR_ERR_CUDA);
+    d.inline_seg = reinterpret_cast<int32_t *>(blk + tb);
     d.parent = reinterpret_cast<int32_t *>(blk);
     d.len = reinterpret_cast<int32_t *>(blk + MN * 4);
     d.active = reinterpret_cast<int32_t *>(blk + MN * 8);
@@ -891,7 +947,6 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
     if (lse_out) return arbor_score(c, tree, q, lse_out, s_out);
     return arbor_score(c, tree, q, nullptr, s_out);
   }
-  TRY(upload_tree(c, tree));
   mark();
   HostPlan hp;
   build_plan(tree, c->h_n, hp, c->tc_ok);
@@ -900,7 +955,8 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
   mark();
   PlanView pv{};
   const int32_t *d_mass_nodes = nullptr;
-  TRY(upload_plan(c, hp, nA, true, &mass_nodes, pv, &d_mass_nodes));
+  // the tree mirror rides in the plan's copy (upload_plan)
+  TRY(upload_plan(c, hp, nA, true, &mass_nodes, pv, &d_mass_nodes, tree));
   TRY(ensure_partials(c, hp.pair_b.size(), c->L));
   mark();
   launch_attn_partial(c, pv, q, 0, c->L, hp.max_cnt, out, lse_out);

@@ -18,6 +18,7 @@ namespace arbor {
 
 constexpr int kAttnChunk = 64;       // slots per attention / score chunk
 constexpr int kLeavesPerItem = 6;    // active leaves per attention work item (q rows staged)
+constexpr size_t kInlineSeg = 256 * 1024;   // bytes of the inline plan segment
 constexpr int kTileRecInts = 16;     // tensor-core tile record (build_plan): 2 halves + leaves[6]
 constexpr int kStashSlots = 4;
 constexpr int kQMaps = 4;            // cached q tensor maps (attn_tc.cu)
@@ -79,7 +80,8 @@ struct DevState {
   // rehydrate / append plans
   int32_t *rehyd_nodes, *rehyd_flag;
   // attention / score plan (uploaded per call)
-  int32_t *seg;              // packed plan (see attn.cu)
+  int32_t *seg;              // packed plan when it exceeds the inline segment
+  int32_t *inline_seg;       // packed plan, right after the tree mirror block (one H2D copy)
   float *partials;           // attention partials
   float *zbuf;               // attention log2-domain logits (fused score pass)
   int64_t *mass_part;        // this rank's per-node partial mass (cached, §score.cu)
@@ -192,6 +194,7 @@ struct arbor_ctx {
   int tmap_q_next = 0, tmap_q_cur = 0;
   bool tc_ok = false;
   int num_sms = 148;               // multiprocessors of the context's device
+  const int64_t *nq_dev = nullptr;  // device Nq of the last score plan (inside the plan segment)
   std::string err;
 };
 

@@ -620,7 +620,7 @@ FusedArgs fused_args(arbor_ctx *c, const PlanView &pv, const float *lse, const i
   m.v = c->d.v;
   m.u = c->d.u;
   m.mass2 = c->d.mass2;
-  m.nq = c->d.nq;
+  m.nq = c->nq_dev ? c->nq_dev : c->d.nq;
   m.norm = static_cast<double>(c->Lg) * static_cast<double>(c->Hqg);
   m.th0 = c->prm.theta[0];
   m.thv = c->prm.theta[1];
@@ -710,7 +710,7 @@ void launch_msve(arbor_ctx *c, int N, float *s_out) {
   m.v = c->d.v;
   m.u = c->d.u;
   m.mass2 = c->d.mass2;
-  m.nq = c->d.nq;
+  m.nq = c->nq_dev ? c->nq_dev : c->d.nq;
   m.norm = static_cast<double>(c->Lg) * static_cast<double>(c->Hqg);
   m.th0 = c->prm.theta[0];
   m.thv = c->prm.theta[1];
