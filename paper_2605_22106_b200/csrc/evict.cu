@@ -28,7 +28,10 @@ namespace arbor {
 namespace {
 
 constexpr int kPairsWs = 8;   // (select warp, move warp) pairs per CTA of select_move_ws_kernel
-constexpr int kUw = 4;        // rows in flight per lane group of a move warp
+#ifndef ARBOR_KUW
+#define ARBOR_KUW 4
+#endif
+constexpr int kUw = ARBOR_KUW;   // rows in flight per lane group of a move warp
 #ifndef ARBOR_JOB_SLOTS
 #define ARBOR_JOB_SLOTS 2
 #endif
