@@ -176,3 +176,26 @@ def test_full_size_decode_step_sampled_rows(cfg):
     for leaf in order[40:44]:
         tree.active = [leaf]
         step(check=True)
+
+
+def test_decode_step_without_lse_and_wide_fallback():
+    """arbor_decode_step with lse_out = NULL (the merged LSE stays on chip only), and with
+    more (leaf, q-head) pairs than the fused merge keeps on chip (65 leaves × G = 8 > 512:
+    the call falls back to the two-call path) — both against the oracle."""
+    preset = dict(tree=("full", 3, 9, 16), L=1, H=2, Hq=16, d=128, dtype="bf16", P=16, rho=0.5,
+                  params={}, active="highest_v")
+    pr = Pair(preset, seed=11, max_active=80)
+    leaves = synth.leaves_of(pr.tree)
+    # (1) lse_out = NULL
+    pr.tree.active = leaves[:3]
+    q = pr.queries(3)
+    out = torch.empty_like(q.cuda())
+    pr.ctx.arbor_decode_step(pr.tree, q.cuda(), out, None)
+    o_ref, l_ref = pr.orc.decode(pr.tree, q.double().numpy())
+    pr.orc.score_accumulate(pr.tree, q.double().numpy(), l_ref)
+    assert_close(out.float().cpu().numpy(), o_ref, pr.rtol, "out (lse NULL)")
+    _score_stage_checks(pr)
+    # (2) 65 active leaves × 8 q heads: fallback
+    pr.tree.active = leaves[:65]
+    pr.decode_both(check=True, fused=True)
+    _score_stage_checks(pr)
