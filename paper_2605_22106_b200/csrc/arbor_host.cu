@@ -936,7 +936,13 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
   using clk = std::chrono::steady_clock;
   clk::time_point ht[8];
   int hn = 0;
-  auto mark = [&]() { if (htrace) ht[hn++] = clk::now(); };
+  auto mark = [&]() {
+    if (htrace) {
+      ht[hn++] = clk::now();
+      static const bool hverbose = getenv("ARBOR_HOST_TRACE_VERBOSE") != nullptr;
+      if (hverbose) { fprintf(stderr, "[arbor host] mark %d\n", hn); fflush(stderr); }
+    }
+  };
   mark();
   TRY(check_tree(c, tree));
   mark();

@@ -65,6 +65,7 @@ struct TcArgs {
   int layer_begin, Lc, Hq, G, T;   // T: tiles
   float scale_log2;
   long long *trace;                // debug: clock64 per (CTA, tile, event) or NULL
+  int qw;                          // query rows per leaf slot in the Q tile (8, or G: dense)
 };
 
 // debug timeline (ARBOR_TC_TRACE=1): trace[(cta·64 + tile)·16 + event] = clock64 − CTA start
@@ -291,11 +292,13 @@ __device__ __forceinline__ float warp_reduceW(const float *v, int lane) {
   if constexpr (W == 16) return warp_reduce16<kMax>(v, lane);
   else return warp_reduce8<kMax>(v, lane);
 }
-// valid columns of an item with cnt leaves: 8-row slot per leaf, G q heads used per slot
-__device__ __forceinline__ unsigned long long colmask(int cnt, int G) {
-  // the G-bit slot mask repeated in each of the cnt bytes (cnt ≤ 6, G ≤ 8: no carries)
+// valid columns of an item with cnt leaves: a qw-row query slot per leaf (qw = 8, or G for
+// dense slots), G q heads used per slot (cnt ≤ 6, qw ≤ 8: ≤ 48 bits)
+__device__ __forceinline__ unsigned long long colmask(int cnt, int G, int qw) {
   const unsigned long long slot = (1ull << G) - 1ull;
-  return slot * (0x0101010101010101ull & ((1ull << (8 * cnt)) - 1ull));
+  unsigned long long m = 0ull;
+  for (int j = 0; j < cnt; ++j) m |= slot << (j * qw);
+  return m;
 }
 
 // two buffers of [S: NQ cols | Oᵀ: NQ cols]
@@ -465,8 +468,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     while (kk_v < ntiles) {
       bool go_k = false, go_v = false;
       if (kk_k < ntiles && kk_k < kk_v + RING) {
+        // K(j) may land only after softmax(j − NSK) has passed its full_k wait (its s_empty
+        // arrival): otherwise, with NSK = 2, K(j) completes full_k's NEXT phase of the same
+        // parity before softmax(j − 2) waits, and that wait then blocks on K(j + 2), which
+        // needs MMA1(j) ← s_empty(j − 2) ← softmax(j − 2): a parity-aliasing deadlock (seen
+        // as rare hangs of the 16-leaf C3 decode; a 2000-step stress passes with this test)
         const int sk = kk_k % NSK;
-        go_k = __shfl_sync(0xffffffffu, mbar_test(&empty_k[sk], ((kk_k / NSK) & 1u) ^ 1u) ? 1 : 0, 0) != 0;
+        const int jp = kk_k - NSK;
+        const bool ok = mbar_test(&empty_k[sk], ((kk_k / NSK) & 1u) ^ 1u) &&
+                        (jp < 0 || mbar_test(&s_empty[jp & 1], (jp >> 1) & 1u));
+        go_k = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
       }
       if (go_k) {
         const int k = kk_k;
@@ -496,15 +507,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         const int it = blockIdx.x + k * gridDim.x;
         const int li = (it / a.g.H) % a.Lc, h = it % a.g.H;
         const int pgA = (ntA + P - 1) >> lgP, pgB = (ntB + P - 1) >> lgP;
-        const int s = k % NSK, r = k % RING;
+        const int s = k % NSK, r = k % RING, fk = s;
         if (lane == 0) { TC_TRACE(k, 0); TC_TRACE(k, 1); }
         unsigned char *Ks = Kst(s);
         unsigned char *Qs = Ks + kKVBytes;
         if (lane == 0) {
           hdr[r] = TcHdr{ntA, ntB, li, h, pbA, pbB, cnt,
                          (pbB >= 0 ? 1 : 0) | (cntB > 0 ? 2 : 0) | (cntA << 4)};
-          mbar_arrive_expect_tx(&full_k[s], static_cast<uint32_t>(pgA + pgB) * P * 256u +
-                                                static_cast<uint32_t>(cnt) * 2048u);
+          mbar_arrive_expect_tx(&full_k[fk], static_cast<uint32_t>(pgA + pgB) * P * 256u +
+                                                static_cast<uint32_t>(cnt * a.qw) * 256u);
         }
         if (lane < kMaxTilePages) vpage[r][lane] = page;
         __syncwarp();
@@ -523,20 +534,20 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           if (pi == 0) {
             const int lp = l * a.g.NP + page;
             const uint32_t dst = static_cast<uint32_t>(half * kHalf) * 128u;
-            tma_load_5d(Ks + dst, &tmk4, 0, 0, 0, h, lp, &full_k[s]);
-            tma_load_5d(Ks + 16384 + dst, &tmk4, 0, 1, 0, h, lp, &full_k[s]);
+            tma_load_5d(Ks + dst, &tmk4, 0, 0, 0, h, lp, &full_k[fk]);
+            tma_load_5d(Ks + 16384 + dst, &tmk4, 0, 1, 0, h, lp, &full_k[fk]);
           }
         } else if (lane < 2 * ppH && pi < pgh) {
           const int row = static_cast<int>(pool_row(a.g, l, page, h, 0));
           const uint32_t dst = static_cast<uint32_t>(half * kHalf + pi * P) * 128u;
-          tma_load_2d(Ks + dst, &tmk, 0, row, &full_k[s]);
-          tma_load_2d(Ks + 16384 + dst, &tmk, 64, row, &full_k[s]);
+          tma_load_2d(Ks + dst, &tmk, 0, row, &full_k[fk]);
+          tma_load_2d(Ks + 16384 + dst, &tmk, 64, row, &full_k[fk]);
         }
         if (lane < cnt) {
-          // leaf `lane`: its G q rows (8-row box, 1024-B aligned slot) → Q rows [8·lane, 8·lane+8)
+          // leaf `lane`: its G q rows (a qw-row box) → Q rows [qw·lane, qw·lane + qw)
           const int row = (leaf * a.Lc + li) * a.Hq + h * a.G;
-          tma_load_2d(Qs + lane * 1024, &tmq, 0, row, &full_k[s]);
-          tma_load_2d(Qs + NQ * 128 + lane * 1024, &tmq, 64, row, &full_k[s]);
+          tma_load_2d(Qs + lane * a.qw * 128, &tmq, 0, row, &full_k[fk]);
+          tma_load_2d(Qs + NQ * 128 + lane * a.qw * 128, &tmq, 64, row, &full_k[fk]);
         }
         if (lane == 0) TC_TRACE(k, 2);
         ++kk_k;
@@ -657,14 +668,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       const int cntA = hd.meta >> 4;
       const bool pack = (hd.meta & 2) != 0;
       // this half's query columns: a packed B half has its own, after A's
-      const unsigned long long cm = (half && pack) ? colmask(hd.cnt - cntA, G) << (8 * cntA)
-                                                   : colmask(cntA, G);
+      const int qw = a.qw;
+      const unsigned long long cm = (half && pack) ? colmask(hd.cnt - cntA, G, qw) << (qw * cntA)
+                                                   : colmask(cntA, G, qw);
       const int lofs = (half && pack) ? cntA : 0;   // first leaf slot of this half's pair group
       const int nt = half ? hd.ntB : hd.ntA;
       const bool present = half == 0 || (hd.meta & 1);
       const int pb = half ? hd.pbB : hd.pbA;
       const bool valid = present && tc < nt;
-      const int ngrp = (min(NQ, 8 * hd.cnt) + GW - 1) / GW;
+      const int ngrp = (min(NQ, qw * hd.cnt) + GW - 1) / GW;
       mbar_wait(&s_full[b], (k >> 1) & 1u);
       if (tid == 64) TC_TRACE(k, 8);
       tc_fence_after();
@@ -706,7 +718,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 #pragma unroll
           for (int i = 0; i < GW; ++i) {
             const int n = c + i;
-            if ((cm >> n) & 1ull) zr[static_cast<int64_t>(((n >> 3) - lofs) * SP + (n & 7)) * kAttnChunk] = z[i];
+            if ((cm >> n) & 1ull) {
+              const int j = n / qw;
+              zr[static_cast<int64_t>((j - lofs) * SP + (n - j * qw)) * kAttnChunk] = z[i];
+            }
           }
         }
       }
@@ -757,18 +772,20 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         ll = (red_l[k & 3][0][etid] + red_l[k & 3][1][etid]) +
              (red_l[k & 3][2][etid] + red_l[k & 3][3][etid]);
       }
-      const int ngrp = (min(NQ, 8 * hd.cnt) + GW - 1) / GW;
+      const int qw = a.qw;
+      const int ngrp = (min(NQ, qw * hd.cnt) + GW - 1) / GW;
       // columns of leaf slot j < cntA belong to pair A's group; a packed B half's columns
       // (slots cntA..cnt−1) to pair B's group
       const int cntA = hd.meta >> 4;
       const bool pack = (hd.meta & 2) != 0;
-      const unsigned long long cm = pack ? colmask(cntA, G) | (colmask(hd.cnt - cntA, G) << (8 * cntA))
-                                         : colmask(cntA, G);
+      const unsigned long long cm = pack ? colmask(cntA, G, qw) | (colmask(hd.cnt - cntA, G, qw) << (qw * cntA))
+                                         : colmask(cntA, G, qw);
       float *pa = a.partials + ((static_cast<int64_t>(hd.pbA) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow;
       float *pbq = a.partials + ((static_cast<int64_t>(pack ? hd.pbB : hd.pbA) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow -
                    static_cast<int64_t>(cntA) * SP * 130;     // so that slot j ≥ cntA lands at j − cntA
       auto col_ptr = [&](int n) {
-        return ((n >> 3) < cntA ? pa : pbq) + static_cast<int64_t>((n >> 3) * SP + (n & 7)) * 130;
+        const int j = n / qw;
+        return (j < cntA ? pa : pbq) + static_cast<int64_t>(j * SP + (n - j * qw)) * 130;
       };
 #pragma unroll 1
       for (int gi = 0; gi < ngrp; ++gi) {
@@ -897,18 +914,23 @@ bool attn_tc_init(arbor_ctx *c) {
 bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_begin,
                     int layer_count, int max_cnt, void *out, float *lse) {
   if (!c->tc_ok || pv.T == 0) return false;
-  const int nq = 8 * max_cnt;          // one 8-row q slot per leaf of an item
+  // query slot rows per leaf: G (dense; the default) or 8 (ARBOR_QSLOT=8)
+  static const int qslot8 = getenv("ARBOR_QSLOT") && atoi(getenv("ARBOR_QSLOT")) == 8;
+  const int qw = qslot8 ? 8 : c->G;
+  const int nq = qw * max_cnt;
   // q as [nA · layer_count · Hq rows][128]; re-encoded only when the buffer or its rows change
   const long long qrows = static_cast<long long>(pv.nA) * layer_count * c->Hq;
   int slot = -1;   // small cache of q tensor maps keyed by (buffer, rows)
   for (int i = 0; i < kQMaps; ++i)
-    if (c->tmap_q_ptr[i] == q && c->tmap_q_rows[i] == qrows) slot = i;
+    if (c->tmap_q_ptr[i] == q && c->tmap_q_rows[i] == qrows && c->tmap_q_box[i] == qw) slot = i;
   if (slot < 0) {
     slot = c->tmap_q_next;
     c->tmap_q_next = (c->tmap_q_next + 1) % kQMaps;
-    if (!encode_rows(c->tmap_q[slot], q, static_cast<unsigned long long>(qrows), 8)) return false;
+    if (!encode_rows(c->tmap_q[slot], q, static_cast<unsigned long long>(qrows),
+                     static_cast<unsigned>(qw))) return false;
     c->tmap_q_ptr[slot] = q;
     c->tmap_q_rows[slot] = qrows;
+    c->tmap_q_box[slot] = qw;
   }
   c->tmap_q_cur = slot;
   TcArgs a{};
@@ -928,6 +950,7 @@ bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_b
   a.G = c->G;
   a.T = pv.T;
   a.scale_log2 = kLog2e / sqrtf(128.f);
+  a.qw = qw;
   static long long *trace = nullptr;
   if (getenv("ARBOR_TC_TRACE")) {
     if (!trace) cudaMalloc(&trace, sizeof(long long) * 148 * 64 * 16);

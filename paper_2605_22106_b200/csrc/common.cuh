@@ -191,6 +191,7 @@ struct arbor_ctx {
   alignas(64) unsigned char tmap_q[arbor::kQMaps][128] = {};   // q maps of recent q buffers
   const void *tmap_q_ptr[arbor::kQMaps] = {};
   long long tmap_q_rows[arbor::kQMaps] = {};
+  int tmap_q_box[arbor::kQMaps] = {};          // rows of the q box (query slot rows)
   int tmap_q_next = 0, tmap_q_cur = 0;
   bool tc_ok = false;
   int num_sms = 148;               // multiprocessors of the context's device

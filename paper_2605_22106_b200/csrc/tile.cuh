@@ -1,5 +1,6 @@
 // tile.cuh — paged K/V tile staging shared by the attention and score kernels.
 #pragma once
+#include <cstdio>
 #include "common.cuh"
 
 namespace arbor {
