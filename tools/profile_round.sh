@@ -1,7 +1,7 @@
 # Full measurement pass for profiles/ (round 1, v11): benches C2 (with cpu_baseline), C3, C4, C5,
 # the reference arm, an ncu launch list of the C2 step and one ncu --set full capture.
 set -x
-V=${V:-v14}
+V=${V:-v15}
 python bench.py > gpurun_out/r01_bench_$V.json 2> gpurun_out/bench_err.log; tail -c 300 gpurun_out/bench_err.log
 python bench.py --config c3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r01_bench_c3_$V.json 2>>gpurun_out/bench_err.log
 python bench.py --config c4 --no-cpu-baseline > gpurun_out/r01_bench_c4_$V.json 2>>gpurun_out/bench_err.log
