@@ -562,7 +562,9 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
     import synth
     from paper_2605_22106_b200 import workload
     from paper_2605_22106_b200.arbor import TreeArgs
-    K, W, D = args.steps, max(3, args.warmup), 8
+    # transitions are capped at 12 (+ warm-up): each one grows 4 open children by D tokens per
+    # decode step and the context is sized for the whole run (int16 position tags per node)
+    K, W, D = min(args.steps, 12), max(3, min(args.warmup, 5)), 8
     transitions = K + W
     extra_nodes = 16 + 4 * transitions + 4
     extra_tokens = extra_nodes * (D * (transitions + 1) + 2) + 64
