@@ -562,15 +562,15 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
     import synth
     from paper_2605_22106_b200 import workload
     from paper_2605_22106_b200.arbor import TreeArgs
-    # transitions are capped at 12 (+ warm-up): each one grows 4 open children by D tokens per
-    # decode step and the context is sized for the whole run (int16 position tags per node)
-    K, W, D = min(args.steps, 12), max(3, min(args.warmup, 5)), 8
+    # the context is sized for the whole run: pages and positions for every open child, and
+    # per node only one child's growth (workload.dpts_sizing)
+    K, W, D = args.steps, max(3, args.warmup), 8
     transitions = K + W
-    extra_nodes = 16 + 4 * transitions + 4
-    extra_tokens = extra_nodes * (D * (transitions + 1) + 2) + 64
+    extra_nodes, extra_tokens, node_extra = workload.dpts_sizing(transitions, D)
     sc = workload.setup("c3", args.seed, kv_head_begin=rank * hc, kv_head_count=hc, rank=rank,
                         world_size=ws, nccl_id=nid, profile=True, device=dev,
-                        extra_tokens=extra_tokens, extra_nodes=extra_nodes, max_active=16)
+                        extra_tokens=extra_tokens, extra_nodes=extra_nodes, max_active=16,
+                        node_extra_tokens=node_extra)
     ctx, tree = sc.ctx, sc.tree
     workload.warmup_leaf_cycling(sc)
     run = workload.DptsRun(sc, n_active=16, transitions=transitions, swap=4, decode_steps=D,

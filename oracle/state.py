@@ -154,7 +154,14 @@ class ArborOracle:
 
     def score_accumulate(self, tree, q, lse=None):
         """§8(a) a2: A[l][h][t] += Σ_g exp(q·k_t/√d − LSE) over visible t for
-        every active leaf, then Nq_i += 1 for closed i on Path(ℓ_b)."""
+        every active leaf, then Nq_i += 1 for closed i on Path(ℓ_b).
+
+        A_i(t) = Σ_{u>b_i} Attn_{u→t}: only queries AFTER block i's end
+        count.  The query of an OPEN active leaf ℓ_b is a token of ℓ_b itself
+        (it is appended before it attends, Q25), so u ≤ b_{ℓ_b} and ℓ_b's own
+        tokens receive nothing; it still attends to them (o, LSE unchanged).
+        A closed active leaf's query is the token after it (u > b), which
+        counts (reading Q5')."""
         q = np.asarray(q, dtype=np.float64)
         if lse is None:
             _, lse = self.decode(tree, q)
@@ -167,7 +174,11 @@ class ArborOracle:
                         continue
                     gs = slice(h * self.G, (h + 1) * self.G)
                     p = attention.probabilities(q[b, l, gs], self.K[l, h, pos], lse[b, l, gs])
-                    self.A[l, h, pos] += p.sum(axis=0)
+                    w = p.sum(axis=0)
+                    if self.open[leaf]:       # u ≤ b_ℓ: not "later" than its own block
+                        a0 = self.span_start[leaf]
+                        w = np.where((pos >= a0) & (pos < a0 + self.n[leaf]), 0.0, w)
+                    self.A[l, h, pos] += w
             for i in geometry.root_path(tree.parent, leaf):
                 if not self.open[i]:
                     self.Nq[i] += 1

@@ -336,6 +336,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   // K (+ q rows) and V of a stage have their own barriers: K is free again once MMA1 has
   // read it, V only after MMA2, so the next K loads go out ~1.5 µs earlier
   __shared__ __align__(8) uint64_t full_k[NSK], empty_k[NSK], full_v[NSV], empty_v[NSV];
+  // kcons[s]: the softmax group of tile k has passed its full_k[k % NSK] wait (128 arrivals).
+  // K(j) is issued only after kcons of tile j − NSK, so full_k[s] is never a phase ahead of a
+  // softmax wait on it (no parity aliasing, for any NSK)
+  __shared__ __align__(8) uint64_t kcons[NSK];
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], o_full[2], o_empty[2];
   // per-tile header and page list, ring of RING = 2·max(NSK, NSV) tiles (written at K issue;
   // read by the V issue, the softmax and — via ohdr — the epilogue; slot k is rewritten by
@@ -421,6 +425,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     for (int s = 0; s < NSK; ++s) {
       mbar_init(&full_k[s], 1);
       mbar_init(&empty_k[s], 1);
+      mbar_init(&kcons[s], 128);    // the 4 warps of one softmax group
     }
     for (int s = 0; s < NSV; ++s) {
       mbar_init(&full_v[s], 1);
@@ -468,15 +473,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     while (kk_v < ntiles) {
       bool go_k = false, go_v = false;
       if (kk_k < ntiles && kk_k < kk_v + RING) {
-        // K(j) may land only after softmax(j − NSK) has passed its full_k wait (its s_empty
-        // arrival): otherwise, with NSK = 2, K(j) completes full_k's NEXT phase of the same
-        // parity before softmax(j − 2) waits, and that wait then blocks on K(j + 2), which
-        // needs MMA1(j) ← s_empty(j − 2) ← softmax(j − 2): a parity-aliasing deadlock (seen
-        // as rare hangs of the 16-leaf C3 decode; a 2000-step stress passes with this test)
+        // K(j) may land only after softmax(j − NSK) has passed its full_k wait (kcons):
+        // otherwise K(j) could complete full_k's NEXT phase of the same parity before
+        // softmax(j − NSK) waits, and that wait would then block on K(j + NSK), which needs
+        // MMA1(j) ← s_empty(j − 2) ← … softmax(j − NSK): a parity-aliasing deadlock (round 1
+        // saw it as rare hangs of the 16-leaf C3 decode).  kcons has one phase per tile of
+        // its stage, so the test is alias-free for any NSK (round 1 gated on s_empty by
+        // TMEM buffer, which throttled NSK = 2 and could alias at NSK = 3).
         const int sk = kk_k % NSK;
-        const int jp = kk_k - NSK;
-        const bool ok = mbar_test(&empty_k[sk], ((kk_k / NSK) & 1u) ^ 1u) &&
-                        (jp < 0 || mbar_test(&s_empty[jp & 1], (jp >> 1) & 1u));
+        const uint32_t par = ((kk_k / NSK) & 1u) ^ 1u;
+        const bool ok = mbar_test(&empty_k[sk], par) && mbar_test(&kcons[sk], par);
         go_k = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
       }
       if (go_k) {
@@ -664,6 +670,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       mbar_wait(&full_k[s], (k / NSK) & 1u);
       if (tid == 64) TC_TRACE(k, 7);
       const TcHdr hd = hdr[k % RING];
+      mbar_arrive(&kcons[s]);               // past the full_k wait: K(k + NSK) may land
       if (half == 0 && lane == 0 && quad == 0) ohdr[k & 3] = hd;   // for the epilogue warps
       const int cntA = hd.meta >> 4;
       const bool pack = (hd.meta & 2) != 0;

@@ -206,7 +206,6 @@ namespace arbor {
 void launch_geometry(arbor_ctx *c, int N, int nA);
 
 // score.cu
-void launch_score_apply(arbor_ctx *c, const PlanView &pv, const float *lse, int layer_count);
 void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64_t *out,
                       int out_stride);
 void launch_msve(arbor_ctx *c, int N, float *s_out);

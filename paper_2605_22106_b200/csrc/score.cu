@@ -18,11 +18,7 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-// a2, fused with a9: the attention kernel already computed every visible logit
-// z = log2(e)·q·k/√d (attn.cu); with the merged LSE the attention weight is exp2(z − LSE·log2 e).
-// One CTA per (chunk, layer, KV head), thread per slot: sums the weights of every active leaf
-// sharing the chunk and all G query heads (ascending leaf order), then one read-modify-write
-// of A at the slot's absolute position (deterministic, no float atomics, Q30).
+// Arguments of the score pass (a2) over the attention kernel's logits (zbuf).
 struct ApplyArgs {
   PlanView pv;
   PoolView g;
@@ -34,31 +30,6 @@ struct ApplyArgs {
   Ctrl *ctrl;
   int Lc, Hq, G;
 };
-
-__global__ void __launch_bounds__(kAttnChunk)
-score_apply_kernel(ApplyArgs a) {
-  const int c = blockIdx.x, li = blockIdx.y, h = blockIdx.z;
-  const int t = threadIdx.x;
-  const int node = a.pv.ch_node[c];
-  const int c0 = a.pv.ch_chunk[c] * kAttnChunk;
-  const int nt = max(0, min(kAttnChunk, a.kcur[node] - c0));
-  if (t >= nt) return;
-  const int p0 = a.pv.ch_poff[c], pc = a.pv.ch_pcnt[c];
-  float psum = 0.f;
-  for (int p = p0; p < p0 + pc; ++p) {
-    const int b = a.pv.pair_b[p];
-    const float *z = a.zbuf + (((static_cast<int64_t>(p) * a.Lc + li) * a.g.H + h) * a.G) * kAttnChunk + t;
-    const float *ls = a.lse + (static_cast<int64_t>(b) * a.Lc + li) * a.Hq + h * a.G;
-    for (int g = 0; g < a.G; ++g) psum += exp2f(z[g * kAttnChunk] - ls[g] * kLog2e);
-  }
-  const int slot = c0 + t;
-  const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.g.MPN;
-  const int pos = a.pos[pool_row(a.g, li, pl[slot / a.g.P], h, slot % a.g.P)];
-  float *dst = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + a.span[node] + pos;
-  const float nv = *dst + psum;
-  if (!(nv >= 0.f) || isinf(nv)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-  *dst = nv;
-}
 
 // Node mass in two launches: one CTA per (listed node, layer) — warps over the layer's KV
 // heads, each warp sums one row of A over the node's span in fp64 (lanes strided, xor tree:
@@ -212,7 +183,9 @@ __device__ __forceinline__ ChunkMeta load_chunk_meta(const FusedArgs &f, int cm,
     m.c0 = a.pv.ch_chunk[cm] * kAttnChunk;
     m.p0 = a.pv.ch_poff[cm];
     m.pc = a.pv.ch_pcnt[cm];
-    if ((m.node & (nparts - 1)) == part) {   // nparts: a power of two
+    // A_i(t) = Σ_{u>b_i}: the open block that holds the query (an open active leaf)
+    // gets no mass from it — its chunks attend but are skipped here (Q5')
+    if ((m.node & (nparts - 1)) == part && !f.m.open[m.node]) {   // nparts: a power of two
       const int kc = a.kcur[m.node];
       m.nt = max(0, min(kAttnChunk, kc - m.c0));
       m.ident = kc == f.nlen[m.node];
@@ -667,28 +640,6 @@ void launch_decode_post(arbor_ctx *c, const PlanView &pv, void *out, float *lse_
     if (c->D == 128) launch_pdl(decode_post_kernel<float, 128, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
     else launch_pdl(decode_post_kernel<float, 64, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
   }
-  ARBOR_LAUNCHED(c);
-  stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
-}
-
-void launch_score_apply(arbor_ctx *c, const PlanView &pv, const float *lse, int layer_count) {
-  if (pv.C == 0) return;
-  ApplyArgs a{};
-  a.pv = pv;
-  a.g = PoolView{c->L, c->H, c->P, c->D, c->NP, c->max_pages_node, c->max_tokens};
-  a.pos = c->cfg.pos_pool;
-  a.ptab = c->d.ptab;
-  a.kcur = c->d.kcur;
-  a.span = c->d.span;
-  a.zbuf = c->d.zbuf;
-  a.lse = lse;
-  a.A = c->cfg.score;
-  a.ctrl = c->d.ctrl;
-  a.Lc = layer_count;
-  a.Hq = c->Hq;
-  a.G = c->G;
-  stage_begin(c, ARBOR_ST_SCORE_ACCUM, c->ms);
-  score_apply_kernel<<<dim3(pv.C, layer_count, c->H), kAttnChunk, 0, c->ms>>>(a);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
 }

@@ -1,6 +1,5 @@
 // tile.cuh — paged K/V tile staging shared by the attention and score kernels.
 #pragma once
-#include <cstdio>
 #include "common.cuh"
 
 namespace arbor {
@@ -130,6 +129,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef ARBOR_MBAR_WATCHDOG
+  // debug builds (ARBOR_NVCC_FLAGS=-DARBOR_MBAR_WATCHDOG): a wait that has not completed
+  // after ~2^31 polls traps, so a pipeline deadlock surfaces as a CUDA error, not a hang
+  for (long long it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    if (it > (1ll << 31)) __trap();
+  }
+#endif
   asm volatile(
       "{\n"
       ".reg .pred p;\n"

@@ -58,8 +58,12 @@ def preset_params(preset: dict, **over):
 def make_context(preset: dict, tree, *, extra_tokens=0, extra_nodes=0, max_active=16,
                  params=None, layer_begin=0, layer_count=None, kv_head_begin=0,
                  kv_head_count=None, rank=0, world_size=1, nccl_id=None, profile=False,
-                 page_margin=64) -> ArborKV:
+                 page_margin=64, node_extra_tokens=None) -> ArborKV:
+    """extra_tokens / extra_nodes: growth of the whole tree beyond the snapshot (pages, the
+    position stream); node_extra_tokens: the most tokens any ONE node may grow to beyond
+    the snapshot's largest node (int16 position tags per node; default extra_tokens)."""
     P = preset["P"]
+    per_node = extra_tokens if node_extra_tokens is None else node_extra_tokens
     n = np.asarray(tree.span_len, np.int64)
     max_node = int(max(n.max(), 1))
     pages = int(sum(-(-int(x) // P) for x in n)) + -(-extra_tokens // P) + extra_nodes + page_margin
@@ -67,7 +71,7 @@ def make_context(preset: dict, tree, *, extra_tokens=0, extra_nodes=0, max_activ
     return ArborKV(num_layers=preset["L"], num_kv_heads=preset["H"], num_q_heads=preset["Hq"],
                    head_dim=preset["d"], dtype=preset["dtype"], page_size=P, num_pages=pages,
                    max_nodes=tree.num_nodes + extra_nodes + 1,
-                   max_node_tokens=max(max_node, 1) + max(extra_tokens, 0) + 1,
+                   max_node_tokens=max(max_node, 1) + max(per_node, 0) + 1,
                    max_active=max_active, max_tokens=max_tokens,
                    params=params if params is not None else preset_params(preset),
                    layer_begin=layer_begin, layer_count=layer_count, kv_head_begin=kv_head_begin,
@@ -141,7 +145,7 @@ class Scenario:
 
 def setup(preset_name: str, seed: int = 0, *, kv_head_begin=0, kv_head_count=None, rank=0,
           world_size=1, nccl_id=None, profile=False, extra_tokens=0, extra_nodes=0,
-          params=None, max_active=16, device="cuda") -> Scenario:
+          params=None, max_active=16, device="cuda", node_extra_tokens=None) -> Scenario:
     """Build the preset's tree, its seeded K/V (on the device), a context, and prefill it."""
     preset = PRESETS[preset_name]
     tree = build_tree(preset, seed)
@@ -155,7 +159,7 @@ def setup(preset_name: str, seed: int = 0, *, kv_head_begin=0, kv_head_count=Non
     ctx = make_context(preset, tree, extra_tokens=extra_tokens, extra_nodes=extra_nodes,
                        max_active=max_active, params=params, kv_head_begin=kv_head_begin,
                        kv_head_count=hc, rank=rank, world_size=world_size, nccl_id=nccl_id,
-                       profile=profile)
+                       profile=profile, node_extra_tokens=node_extra_tokens)
     load_tree(ctx, tree, K, V)
     return Scenario(preset, tree, ctx, K, V, E, seed, kv_head_begin)
 
@@ -174,6 +178,15 @@ def warmup_leaf_cycling(sc: Scenario, steps_per_leaf: int = 4):
 
 
 # ---------------------------------------------------------------- C3: DPTS transition loop
+def dpts_sizing(transitions: int, decode_steps: int = 8, n_active: int = 16, swap: int = 4):
+    """Context growth of a DptsRun: (extra_nodes, extra_tokens, node_extra_tokens).  Every
+    open child reserves child_cap = decode_steps·(transitions + 1) + 2 positions."""
+    child_cap = decode_steps * (transitions + 1) + 2
+    extra_nodes = n_active + swap * transitions + 4
+    return extra_nodes, extra_nodes * child_cap + 64, child_cap
+
+
+
 class DptsRun:
     """configs[2]: n_active leaves under distinct level-2
     parents; each transition replaces `swap` of them (backtracks into possibly evicted

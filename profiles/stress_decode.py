@@ -1,6 +1,8 @@
 """Stress: many arbor_decode_step calls on a preset (default c3: 16 leaves, NQ = 48 tiles)
-with a device sync every 50 steps; prints progress.  A pipeline deadlock trips the mbarrier
-watchdog (tile.cuh) and surfaces as a CUDA error instead of a hang.
+with a device sync every 50 steps; prints progress.  A pipeline deadlock hangs the stream:
+faulthandler prints the Python stack after 90 s and exits.  A debug build with
+ARBOR_NVCC_FLAGS=-DARBOR_MBAR_WATCHDOG turns it into a CUDA error (bounded mbarrier waits
+that __trap(), tile.cuh).
 
     python profiles/stress_decode.py [c3] [steps]
 """

@@ -25,3 +25,24 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """GPU sessions: write the observed error of every tolerance check (gpu_helpers.TOL_LOG)."""
+    try:
+        import gpu_helpers
+    except Exception:
+        return
+    if not gpu_helpers.TOL_LOG:
+        return
+    import json
+    out = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    worst = {}
+    for e in gpu_helpers.TOL_LOG:
+        w = worst.get(e["what"])
+        if w is None or e["max_err_over_bound"] > w["max_err_over_bound"]:
+            worst[e["what"]] = dict(e, checks=0)
+        worst[e["what"]]["checks"] = worst[e["what"]].get("checks", 0) + 1
+    with open(os.path.join(out, "tolerance_report.json"), "w") as f:
+        json.dump(dict(checks=len(gpu_helpers.TOL_LOG), worst_per_check=worst), f, indent=1)

@@ -28,6 +28,20 @@ def rtol_for(dtype: str) -> float:
     return 1e-5 if dtype == "f32" else 2e-2
 
 
+def rtol_fp32_quantity(dtype: str) -> float:
+    """LSE and accumulated attention A are fp32 quantities on both paths: the bf16 path
+    multiplies bf16 operands exactly and accumulates, exponentiates and sums in fp32 (only
+    the PV operand P is rounded to bf16, which touches the output alone), so they take the
+    fp32 tolerance 1e-5 whatever the KV dtype (observed worst
+    relative errors ~2e-7 for LSE and ~1.2e-6 for A, profiles/r02_tolerance_report.json)."""
+    return 1e-5
+
+
+# observed errors of every assert_close call, written by conftest to
+# gpurun_out/tolerance_report.json at the end of a GPU session
+TOL_LOG = []
+
+
 def assert_close(x, y, rtol, what="", row_frac=1.0):
     """|x − y| ≤ rtol·(|y| + row_frac·max_row|y|), rows = last axis.
 
@@ -46,7 +60,13 @@ def assert_close(x, y, rtol, what="", row_frac=1.0):
     y = np.where(finite, y, 0.0)
     rowmax = np.max(np.abs(y), axis=-1, keepdims=True)
     bound = rtol * (np.abs(y) + rowmax * row_frac)
-    bad = np.abs(x - y) > bound
+    err = np.abs(x - y)
+    TOL_LOG.append(dict(what=what, rtol=rtol, row_frac=row_frac, n=int(y.size),
+                        max_abs_err=float(err.max()),
+                        max_err_over_rowmax=float((err / np.maximum(rowmax, 1e-300)).max()),
+                        max_rel_err=float((err / np.maximum(np.abs(y), 1e-300)).max()),
+                        max_err_over_bound=float((err / np.maximum(bound, 1e-300)).max())))
+    bad = err > bound
     if bad.any():
         i = np.argwhere(bad)[0]
         raise AssertionError(f"{what}: {bad.sum()} of {bad.size} outside tolerance; first at "
@@ -84,6 +104,7 @@ class Pair:
                 self.orc.close_node(i)
         self.step = 0
         self.rtol = rtol_for(p["dtype"])
+        self.rtol_q = rtol_fp32_quantity(p["dtype"])
 
     # ------------------------------------------------------------ queries / steps
     def queries(self, n_active: int):
@@ -111,7 +132,7 @@ class Pair:
             self.orc.score_accumulate(self.tree, qn)
         if check:
             assert_close(out.float().cpu().numpy(), o_ref, self.rtol, "attention output")
-            assert_close(lse.cpu().numpy(), lse_ref, self.rtol, "LSE")
+            assert_close(lse.cpu().numpy(), lse_ref, self.rtol_q, "LSE", row_frac=0.0)
         return out, lse
 
     def warmup(self, steps_per_leaf=4, check=False, fused=False):

@@ -62,7 +62,7 @@ def test_tc_attention_ragged_shared_nan_tails(Hq, n_active):
     leaves = synth.leaves_of(pr.tree)
     pr.tree.active = leaves[:n_active]
     pr.decode_both(check=True)
-    assert_close(pr.gpu_A()[:, :, :pr.orc.Tmax], pr.orc.A, pr.rtol, "A", row_frac=1e-3)
+    assert_close(pr.gpu_A()[:, :, :pr.orc.Tmax], pr.orc.A, pr.rtol_q, "A", row_frac=1e-3)
     # evict the off-path nodes to ragged k (partial chunks and partial pages), poison tails
     pr.tree.active = leaves[:1]
     _evict_ragged(pr, 0.55)
@@ -75,7 +75,7 @@ def test_tc_attention_ragged_shared_nan_tails(Hq, n_active):
     _poison_page_tails(pr)
     out, lse = pr.decode_both(check=True)
     assert torch.isfinite(out.float()).all()
-    assert_close(pr.gpu_A()[:, :, :pr.orc.Tmax], pr.orc.A, pr.rtol, "A", row_frac=1e-3)
+    assert_close(pr.gpu_A()[:, :, :pr.orc.Tmax], pr.orc.A, pr.rtol_q, "A", row_frac=1e-3)
 
 
 def test_tc_attention_evicted_nodes_visible():
@@ -106,5 +106,5 @@ def test_tc_matches_cuda_core_path():
         out, lse = pr.decode_both(check=True)
         outs.append((out.float().cpu().numpy(), lse.cpu().numpy(), pr.gpu_A()))
     assert_close(outs[0][0], outs[1][0], 2e-2, "tc vs cuda-core output")
-    assert_close(outs[0][1], outs[1][1], 2e-2, "tc vs cuda-core LSE")
-    assert_close(outs[0][2], outs[1][2], 2e-2, "tc vs cuda-core A", row_frac=1e-3)
+    assert_close(outs[0][1], outs[1][1], 1e-5, "tc vs cuda-core LSE", row_frac=0.0)
+    assert_close(outs[0][2], outs[1][2], 1e-5, "tc vs cuda-core A", row_frac=1e-3)

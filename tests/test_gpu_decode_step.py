@@ -104,7 +104,7 @@ def test_full_size_decode_step_sampled_rows(cfg):
     and configs[4] (c5: 64k-token 8B-shaped tree) at full size in the bench's launch
     configuration: leaf-cycling warm-up, decode steps and a ρ = 0.25 eviction through
     arbor_decode_step / arbor_allocate / arbor_evict; sampled (layer, KV head) rows are
-    mirrored by per-row oracles: attention output and LSE (2e-2), A (2e-2), kept positions,
+    mirrored by per-row oracles: attention output (2e-2), LSE and A (1e-5), kept positions,
     page lists and free list (bit-exact)."""
     preset = workload.PRESETS[cfg]
     sc = workload.setup(cfg, 0)
@@ -137,8 +137,8 @@ def test_full_size_decode_step_sampled_rows(cfg):
             if check:
                 assert_close(out[:, l:l + 1, h * G:(h + 1) * G].float().cpu().numpy(), o_ref, 2e-2,
                              f"out row {(l, h)}")
-                assert_close(lse[:, l:l + 1, h * G:(h + 1) * G].cpu().numpy(), l_ref, 2e-2,
-                             f"LSE row {(l, h)}")
+                assert_close(lse[:, l:l + 1, h * G:(h + 1) * G].cpu().numpy(), l_ref, 1e-5,
+                             f"LSE row {(l, h)}", row_frac=0.0)
 
     order = workload.leaf_cycle_order(tree, 0)
     for leaf in order[:40]:
@@ -148,7 +148,7 @@ def test_full_size_decode_step_sampled_rows(cfg):
     step(check=True)
     A = ctx.score
     for (l, h), o in orcs.items():
-        assert_close(A[l, h, :o.Tmax].cpu().numpy()[None], o.A[0, 0][None], 2e-2, f"A row {(l, h)}",
+        assert_close(A[l, h, :o.Tmax].cpu().numpy()[None], o.A[0, 0][None], 1e-5, f"A row {(l, h)}",
                      row_frac=1e-3)
     s = torch.empty(tree.num_nodes, dtype=torch.float32, device="cuda")
     ctx.arbor_decode_step(tree, sc.queries(sc.steps, nA), out, lse, s)

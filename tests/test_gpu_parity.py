@@ -30,7 +30,7 @@ def _score_stage_checks(pr: Pair):
     """Float tier for A; exact tier for masses/s recomputed from the GPU's own A."""
     A = pr.gpu_A()[:, :, :pr.orc.Tmax]
     Aref = pr.orc.A
-    assert_close(A, Aref, pr.rtol, "accumulated attention A", row_frac=1e-3)
+    assert_close(A, Aref, pr.rtol_q, "accumulated attention A", row_frac=1e-3)
     sc = pr.ctx.arbor_read_scores(pr.tree.num_nodes)
     A64 = A.astype(np.float64)
     for i in range(pr.tree.num_nodes):
@@ -163,6 +163,8 @@ def test_open_nodes_and_appends():
         pr.orc.append(node, nt)
         pr.tree.span_len[node] += nt
         pr.decode_both(check=True)
+        # A_i(t) = Σ_{u>b_i} (DESIGN Q5'): the open block gets nothing from its own queries
+        assert not pr.gpu_A()[:, :, a:a + int(pr.tree.span_len[node])].any()
     pr.check_kv_state()
     sc = _score_stage_checks(pr)
     pr.ctx.arbor_close_node(node)
@@ -334,6 +336,6 @@ def test_c3_dpts_transitions_reduced():
             o_ref, lse_ref = pr.orc.decode(pr.tree, qn)
             pr.orc.score_accumulate(pr.tree, qn)
             assert_close(out.float().cpu().numpy(), o_ref, pr.rtol, "C3 attention output")
-            assert_close(lse.cpu().numpy(), lse_ref, pr.rtol, "C3 LSE")
+            assert_close(lse.cpu().numpy(), lse_ref, pr.rtol_q, "C3 LSE", row_frac=0.0)
         _score_stage_checks(pr)
     assert pr.orc.rehydrations > 0

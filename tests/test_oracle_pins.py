@@ -552,3 +552,199 @@ def test_no_rehydrate_is_irreversible():
     before = [orc.k_cur(i) for i in range(N)]
     assert orc.rehydrate(list(range(N))) == 0
     assert [orc.k_cur(i) for i in range(N)] == before
+
+
+# ---------------------------------------------------------------- round 2: path assembly, A_i(t)
+def _root_chain(parent, leaf):
+    """Root→leaf chain by a plain parent walk (independent of oracle.geometry)."""
+    out = []
+    x = int(leaf)
+    while x >= 0:
+        out.append(x)
+        x = int(parent[x])
+    return out[::-1]
+
+
+def _path_kv(o, tree, leaf, l, h):
+    """Visible positions of (leaf, l, h): every node of the root chain, its kept positions
+    sorted ascending — assembled here without oracle.attention."""
+    pos = []
+    for i in _root_chain(tree.parent, leaf):
+        pos.extend(sorted(int(tree.span_start[i]) + int(t) for t in o.kept[i][l, h]))
+    return np.array(pos, dtype=np.int64)
+
+
+def _sdpa(q, K, V):
+    """torch SDPA (fp64, CPU) for G query rows over one KV sequence, and its logsumexp."""
+    G, d = q.shape
+    T = K.shape[0]
+    qt, Kt, Vt = torch.tensor(q), torch.tensor(K), torch.tensor(V)
+    o = torch.nn.functional.scaled_dot_product_attention(
+        qt[None, :, None, :], Kt[None, None].expand(1, G, T, d),
+        Vt[None, None].expand(1, G, T, d))[0, :, 0, :]
+    z = qt @ Kt.T / math.sqrt(d)
+    return o.numpy(), torch.logsumexp(z, dim=1).numpy(), torch.softmax(z, dim=1).numpy()
+
+
+@pytest.mark.parametrize("evict", [False, True])
+def test_state_decode_is_sdpa_over_concatenated_path(evict):
+    """Tree decode attention of every active leaf = torch SDPA over the concatenation of its
+    root→leaf chain's retained K/V (full retention: standard causal decode over the path
+    sequence); after an eviction, over the kept positions."""
+    tree, o, E = _small_state(levels=3, width=3, t_node=10, seed=11)
+    leaves = synth.leaves_of(tree)
+    tree.active = [leaves[0]]
+    q1 = synth.make_queries(1, o.L, o.Hq, o.d, "f32", 5, E).double().numpy()
+    o.score_accumulate(tree, q1)
+    if evict:
+        a, s = o.msve(tree)
+        o.evict(tree, o.allocate(tree, s, tree.total_tokens // 2))
+    tree.active = [leaves[0], leaves[4], leaves[-1]]
+    q = synth.make_queries(3, o.L, o.Hq, o.d, "f32", 6, E).double().numpy()
+    out, lse = o.decode(tree, q)
+    for b, leaf in enumerate(tree.active):
+        for l in range(o.L):
+            for h in range(o.H):
+                pos = _path_kv(o, tree, leaf, l, h)
+                gs = slice(h * o.G, (h + 1) * o.G)
+                ref_o, ref_l, _ = _sdpa(q[b, l, gs], o.K[l, h, pos], o.V[l, h, pos])
+                assert np.allclose(out[b, l, gs], ref_o, rtol=1e-12, atol=1e-12)
+                assert np.allclose(lse[b, l, gs], ref_l, rtol=1e-12, atol=1e-12)
+
+
+def test_state_multi_leaf_equals_single_leaf_runs():
+    """Tree sharing changes nothing: an n_A-leaf decode equals n_A
+    single-leaf decodes, and the n_A-leaf score pass adds exactly the sum of the single-leaf
+    passes' attention mass (A is additive over queries)."""
+    tree, o, E = _small_state(levels=3, width=3, t_node=9, seed=12)
+    leaves = synth.leaves_of(tree)
+    act = [leaves[1], leaves[2], leaves[7]]
+    q = synth.make_queries(3, o.L, o.Hq, o.d, "f32", 7, E).double().numpy()
+    tree.active = act
+    out, lse = o.decode(tree, q)
+    A0 = o.A.copy()
+    o.score_accumulate(tree, q, lse)
+    dA_multi = o.A - A0
+    o.A[:] = A0
+    for b, leaf in enumerate(act):
+        tree.active = [leaf]
+        ob, lb = o.decode(tree, q[b:b + 1])
+        assert np.array_equal(ob[0], out[b]) and np.array_equal(lb[0], lse[b])
+        o.score_accumulate(tree, q[b:b + 1], lb)
+    assert np.allclose(o.A - A0, dA_multi, rtol=1e-13, atol=1e-15)
+
+
+def test_accumulated_attention_counts_later_queries_only():
+    """A_i(t) = Σ_{u>b_i} Σ_{l,h} Attn_{u→t}: queries of an open block (the block
+    they belong to, Q25) add nothing to that block's own tokens while it is open; after it
+    closes, only queries of later blocks count.  The reference A is rebuilt here from torch
+    softmax weights over the independently assembled path."""
+    tree, o, E = _small_state(levels=2, width=2, t_node=6, L=1, H=2, G=2, d=16, P=4, seed=13)
+    gen = torch.Generator().manual_seed(5)
+    A_ref = np.zeros_like(o.A)
+    K, V = o.K, o.V
+
+    def decode_from(leaf, step, own_open):
+        q = synth.make_queries(1, o.L, o.Hq, o.d, "f32", step, E).double().numpy()
+        tree.active = [leaf]
+        o.score_accumulate(tree, q)
+        for l in range(o.L):
+            for h in range(o.H):
+                pos = _path_kv(o, tree, leaf, l, h)
+                _, _, p = _sdpa(q[0, l, h * o.G:(h + 1) * o.G], K[l, h, pos], V[l, h, pos])
+                w = p.sum(axis=0)
+                if own_open:
+                    a0, n = int(tree.span_start[leaf]), int(tree.span_len[leaf])
+                    w = np.where((pos >= a0) & (pos < a0 + n), 0.0, w)
+                A_ref[l, h, pos] += w
+
+    # a closed active leaf: its query is the next token (u > b_ℓ), so ℓ's tokens count
+    decode_from(1, 100, own_open=False)
+    # grow an open child c under leaf 2, one token per step; c's tokens never gain mass
+    c = tree.add_node(2, tree.end_position(), 0, True, 0.5, 0.5)
+    o.open_node(c, int(tree.span_start[c]))
+    T_extra = 5
+    o.K = np.concatenate([K, torch.randn(o.L, o.H, T_extra, o.d, generator=gen, dtype=torch.float64).numpy()], axis=2)
+    o.V = np.concatenate([V, torch.randn(o.L, o.H, T_extra, o.d, generator=gen, dtype=torch.float64).numpy()], axis=2)
+    o.A = np.concatenate([o.A, np.zeros((o.L, o.H, T_extra))], axis=2)
+    A_ref = np.concatenate([A_ref, np.zeros((o.L, o.H, T_extra))], axis=2)
+    K, V = o.K, o.V
+    for step in range(3):
+        o.append(c, 1)
+        tree.span_len[c] += 1
+        decode_from(c, 200 + step, own_open=True)
+        a0 = int(tree.span_start[c])
+        assert not o.A[:, :, a0:a0 + int(tree.span_len[c])].any()
+    # close c: Mclose_c is 0 (no mass while open); a grandchild g's queries now count for c
+    o.close_node(c)
+    tree.is_open[c] = 0
+    assert o.Mclose[c] == 0 and o.Nq[c] == 0
+    g = tree.add_node(c, tree.end_position(), 0, True, 0.5, 0.5)
+    o.open_node(g, int(tree.span_start[g]))
+    for step in range(2):
+        o.append(g, 1)
+        tree.span_len[g] += 1
+        decode_from(g, 300 + step, own_open=True)
+    assert np.allclose(o.A, A_ref, rtol=1e-12, atol=1e-15)
+    a0 = int(tree.span_start[c])
+    assert o.A[:, :, a0:a0 + int(tree.span_len[c])].sum() > 0
+    assert o.Nq[c] == 2
+    # its feature is exactly the post-close mass per query row (Q4)
+    a, _ = o.msve(tree)
+    m = sum(round(math.fsum(A_ref[l, h, a0:a0 + int(tree.span_len[c])]) * 2 ** 24)
+            for l in range(o.L) for h in range(o.H))
+    assert abs(a[c] - m / 2 ** 24 / (2 * o.L * o.Hq)) < 1e-12
+
+
+def test_node_mass_counts_frozen_evicted_scores():
+    """m_{l,h,i} sums the whole span, kept and evicted positions alike; evicted A is frozen
+    (SPEC S:429): eviction leaves every node mass unchanged, later score passes never
+    touch evicted positions, and Mass_i = Σ_rows round(2^24·Σ_span A) (reference sums with
+    math.fsum: each row may differ from the fp64 running sum by at most one unit)."""
+    tree, o, E = _small_state(levels=3, width=2, t_node=16, seed=14)
+    leaves = synth.leaves_of(tree)
+    tree.active = [leaves[0]]
+    for st in range(3):
+        o.score_accumulate(tree, synth.make_queries(1, o.L, o.Hq, o.d, "f32", 40 + st, E).double().numpy())
+    before = o.masses()
+    a, s = o.msve(tree)
+    o.evict(tree, o.allocate(tree, s, tree.total_tokens * 3 // 5))
+    assert o.masses() == before
+    evicted = np.ones_like(o.A, dtype=bool)
+    for i in range(tree.num_nodes):
+        for l in range(o.L):
+            for h in range(o.H):
+                evicted[l, h, int(tree.span_start[i]) + o.kept[i][l, h]] = False
+    assert evicted.any()
+    A_ev = o.A[evicted].copy()
+    tree.active = [leaves[-1]]
+    o.score_accumulate(tree, synth.make_queries(1, o.L, o.Hq, o.d, "f32", 50, E).double().numpy())
+    assert np.array_equal(o.A[evicted], A_ev)
+    for i in range(tree.num_nodes):
+        a0, n = int(tree.span_start[i]), int(tree.span_len[i])
+        ref = sum(round(math.fsum(o.A[l, h, a0:a0 + n]) * 2 ** 24) for l in range(o.L) for h in range(o.H))
+        assert abs(o.masses()[i] - ref) <= o.L * o.H
+
+
+def test_hole_fill_worked_example():
+    """Q23' slot order on the hand-worked example of tests/golden."""
+    g = GOLD["hole_fill_example"]
+    tree = synth.SynthTree(np.array([-1, 0], np.int32), np.array([0, 10], np.int64),
+                           np.array([10, 4], np.int32), np.zeros(2, np.uint8),
+                           np.zeros(2, np.float32), np.zeros(2, np.float32), [1])
+    L, H, d = 1, 1, 4
+    K = np.zeros((L, H, 14, d))
+    o = ArborOracle(K, K, 1, 4, 8, default_params(k_min=1, l_tail=3, r_min=0.0))
+    for i in range(2):
+        o.open_node(i, int(tree.span_start[i]))
+        o.append(i, int(tree.span_len[i]))
+        o.close_node(i)
+    tree.active = [1]
+    A = np.zeros((L, H, 14), np.float32)
+    A[0, 0, :10] = GOLD["select_example"]["A"]
+    # the root is on Path*: evict node 0 through a tree in which node 1 hangs off elsewhere
+    tree2 = synth.SynthTree(np.array([-1, -1], np.int32), tree.span_start, tree.span_len,
+                            tree.is_open, tree.v, tree.u, [1])
+    o.evict(tree2, [g["k_app"], 4], A_f32=A)
+    assert sorted(o.kept[0][0, 0].tolist()) == g["retained"]
+    assert o.kept[0][0, 0].tolist() == g["new_slots"]
