@@ -108,8 +108,9 @@ def dist_env():
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle (oracle/), as it stands, on the host cores, on a
-    bounded sample of the same workload (one layer's KV heads), same metric."""
+    """--impl reference: the CPU oracle (oracle/), as it stands, on the host cores (one
+    worker process per core over layers), on the same workload, inputs, warm-up and step
+    as the GPU arm; same metric.  Under torchrun only rank 0 runs it."""
     ws, rank, _ = dist_env()
     if ws > 1:
         import torch.distributed as dist
@@ -117,14 +118,26 @@ def run_reference(args):
         if rank != 0:
             dist.barrier()
             return
-    res = cpu_oracle_sample(args.config, args.seed, args.warmup, args.steps)
+    if args.config == "c3":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference arm covers the bulk "
+                          "eviction configs (c2, c4, c5); c3 is a transition loop"}), flush=True)
+        return
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    K, V, q_warm, q_step, order, leaves, B = bench_inputs(args.config, args.seed, dev)
+    res = oracle_host_run(args.config, args.seed, args.warmup, args.steps, K, V, q_warm, q_step,
+                          order, leaves, B, target_s=150.0)
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": res["ms_per_step_full"], "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args.config, ws),
+            "n_gpus": args.gpus, "steps": res["steps_timed"], "warmup": args.warmup,
+            "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic" + ("" if dev == "cuda" else
+                                                                        " (CPU generator)"),
+            "config": workload_config(args.config, 1),
             "cpu_baseline": {"value": res["value"], "unit": "tokens/s", "cores": res["cores"],
-                             "kind": "oracle", "sample": res["sample"]},
+                             "kind": "oracle", "sample": res["sample"],
+                             "cpu_model": res["cpu_model"],
+                             "single_thread_equiv_tokens_per_s": res["single_thread_equiv_tokens_per_s"],
+                             "wall_s": res["wall_s"]},
             "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -150,72 +163,222 @@ def workload_config(name, ws):
                    if name != "c3" else "inputs > L2 (KV pools >> 126 MB)")}
 
 
-# ---------------------------------------------------------------- CPU oracle sample
-def cpu_oracle_sample(config, seed, warmup, steps, target_s=12.0):
-    """Time the oracle (as it stands) on a bounded sample: the full tree and node-level
-    allocation, but only the rows (l, h) of layer 0 for score / mass / evict / attention.
-    Scaled to the full workload by the row ratio (per-row work is independent)."""
+# ---------------------------------------------------------------- CPU oracle on the host cores
+_FLEET = {}          # set before the workers fork (copy-on-write inputs)
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def _fleet_worker(conn, l0, l1):
+    """One host core: the oracle (as it stands) over layers [l0, l1) — all KV heads of them.
+    Commands: warm-up (the GPU arm's leaf-cycling warm-up, same queries), snapshot, step
+    (restore → decode attention → score), evict (with the parent's k)."""
     try:
         from threadpoolctl import threadpool_limits
-        with threadpool_limits(limits=1):
-            return _cpu_oracle_sample(config, seed, warmup, steps, target_s)
+        threadpool_limits(limits=1)
     except ImportError:
-        return _cpu_oracle_sample(config, seed, warmup, steps, target_s)
+        pass
+    import copy
+    from oracle.state import ArborOracle
+    F = _FLEET
+    tree, p = F["tree"], F["preset"]
+    o = ArborOracle(F["K"][l0:l1].double().numpy(), F["V"][l0:l1].double().numpy(), p["Hq"],
+                    p["P"], F["num_pages"], F["params"], num_layers_global=p["L"],
+                    num_q_heads_global=p["Hq"])
+    for i in range(tree.num_nodes):
+        o.open_node(i, int(tree.span_start[i]))
+        o.append(i, int(tree.span_len[i]))
+        o.close_node(i)
+    state_keys = ("kept", "pages", "free", "A", "Nq", "Mclose", "s_last", "rehydrations")
+    snap = None
+
+    def q_of(qs, j):
+        return qs[j][:, l0:l1].double().numpy()
+
+    conn.send("ready")
+    while True:
+        cmd = conn.recv()
+        t0 = time.perf_counter()
+        if cmd[0] == "warm":
+            for j, leaf in enumerate(cmd[1]):
+                tree.active = [leaf]
+                o.score_accumulate(tree, q_of(F["q_warm"], j))
+            conn.send(time.perf_counter() - t0)
+        elif cmd[0] == "snap":
+            snap = {k: copy.deepcopy(getattr(o, k)) for k in state_keys}
+            conn.send(0.0)
+        elif cmd[0] == "step":
+            for k_, v_ in snap.items():
+                setattr(o, k_, copy.deepcopy(v_))
+            tree.active = [cmd[1]]
+            q = q_of(F["q_step"], cmd[2])
+            _, lse = o.decode(tree, q)
+            o.score_accumulate(tree, q, lse)
+            masses = o.masses()
+            conn.send((time.perf_counter() - t0, masses, list(o.Nq), list(o.Mclose)))
+        elif cmd[0] == "evict":
+            tree.active = [cmd[1]]
+            ev = o.evict(tree, cmd[2])
+            conn.send((time.perf_counter() - t0, ev))
+        else:
+            conn.send(None)
+            return
 
 
-def _cpu_oracle_sample(config, seed, warmup, steps, target_s):
+class OracleFleet:
+    """The CPU oracle (oracle/, as it stands, unmodified and untuned) on the host cores:
+    one forked worker process per core, each owning a contiguous range of layers (every KV
+    head of them, numpy/BLAS limited to one thread), running the rows' work (decode
+    attention, score, node masses, select + compact); the node-level work (MSVE from the
+    summed exact integer masses, TAE allocation) runs once, in the parent.  Same inputs as
+    the GPU arm (its K/V and queries), the same leaf-cycling warm-up, the same step."""
+
+    def __init__(self, config, seed, K, V, q_warm, q_step, cores=None):
+        import multiprocessing as mp
+        from oracle.state import default_params
+        from paper_2605_22106_b200 import workload
+        p = workload.PRESETS[config]
+        self.preset, self.config = p, config
+        self.tree = workload.build_tree(p, seed)
+        self.params = default_params(**p["params"])
+        L = p["L"]
+        self.cores = max(1, min(cores or _host_cores(), L))
+        bounds = [round(i * L / self.cores) for i in range(self.cores + 1)]
+        _FLEET.update(tree=self.tree, preset=p, K=K, V=V, q_warm=q_warm, q_step=q_step,
+                      params=self.params,
+                      num_pages=sum(-(-int(x) // p["P"]) for x in self.tree.span_len) + 64)
+        ctx = mp.get_context("fork")
+        self.conns, self.procs = [], []
+        for w in range(self.cores):
+            a, b = ctx.Pipe()
+            pr = ctx.Process(target=_fleet_worker, args=(b, bounds[w], bounds[w + 1]), daemon=True)
+            pr.start()
+            self.conns.append(a)
+            self.procs.append(pr)
+        for c in self.conns:
+            assert c.recv() == "ready"
+
+    def _all(self, msg):
+        for c in self.conns:
+            c.send(msg)
+        return [c.recv() for c in self.conns]
+
+    def warmup(self, order):
+        return max(self._all(("warm", order)))
+
+    def snapshot(self):
+        self._all(("snap",))
+
+    def step(self, leaf, qi, budget):
+        """One timed step (wall clock of the parent, IPC included); returns (seconds,
+        single-thread-equivalent seconds, k)."""
+        from oracle import geometry, msve, tae
+        tree, p = self.tree, self.preset
+        t0 = time.perf_counter()
+        res = self._all(("step", leaf, qi))
+        t1 = time.perf_counter()
+        N = tree.num_nodes
+        mass = [sum(r[1][i] for r in res) for i in range(N)]
+        Nq, Mclose = res[0][2], [sum(r[3][i] for r in res) for i in range(N)]
+        s = []
+        for i in range(N):
+            a = msve.attention_feature(mass[i], Mclose[i], Nq[i], p["L"], p["Hq"])
+            s.append(float(np.float32(msve.msve_score(self.params["theta"], float(tree.v[i]),
+                                                       float(tree.u[i]), a))))
+        tree.active = [leaf]
+        parent = [int(x) for x in tree.parent]
+        d = geometry.depths(parent)
+        dist = geometry.delta(parent, tree.active)
+        ps = geometry.path_star(parent, tree.active)
+        st, k, _ = tae.allocate(self.params["alloc_mode"], s, d, dist, [i in ps for i in range(N)],
+                                [False] * N, [int(x) for x in tree.span_len], self.params, budget)
+        t2 = time.perf_counter()
+        ev = self._all(("evict", leaf, k))
+        t3 = time.perf_counter()
+        serial = sum(r[0] for r in res) + (t2 - t1) + sum(r[0] for r in ev)
+        return t3 - t0, serial, k
+
+    def close(self):
+        for c in self.conns:
+            try:
+                c.send(("quit",))
+            except Exception:
+                pass
+        for pr in self.procs:
+            pr.join(timeout=5)
+
+
+def oracle_host_run(config, seed, warmup, steps, K, V, q_warm, q_step, warm_order, leaves,
+                    budget, target_s=60.0, k_gpu=None):
+    """Time the oracle fleet on the bench's workload: warm-up (untimed), then W + K steps
+    (restore → step), the first W untimed; stops early (≥ 1 timed step) past target_s."""
+    t_begin = time.perf_counter()
+    fleet = OracleFleet(config, seed, K, V, q_warm, q_step)
+    try:
+        t_warm = fleet.warmup(warm_order)
+        fleet.snapshot()
+        times, serial, ks = [], [], []
+        t_loop = time.perf_counter()
+        for i in range(warmup + steps):
+            dt, ser, k = fleet.step(leaves[i % 2], i % 2, budget)
+            if i >= warmup:
+                times.append(dt)
+                serial.append(ser)
+                ks.append(k)
+            if time.perf_counter() - t_loop > target_s and times:
+                break
+    finally:
+        fleet.close()
+    T = fleet.tree.total_tokens
+    t_step = statistics.median(times)
+    same_k = None if k_gpu is None else all(k == k_gpu[j % 2] for j, k in enumerate(ks))
+    return {"value": T / t_step, "ms_per_step": t_step * 1e3, "cores": fleet.cores,
+            "steps_timed": len(times), "single_thread_equiv_tokens_per_s": T / statistics.median(serial),
+            "cpu_model": _cpu_model(), "host_cores": _host_cores(),
+            "wall_s": time.perf_counter() - t_begin, "warmup_s": t_warm, "k_equals_gpu": same_k,
+            "sample": (f"{config}: the whole step on the whole workload ({fleet.tree.num_nodes} "
+                       f"nodes, {T} tokens, all {fleet.preset['L'] * fleet.preset['H']} (layer, "
+                       f"KV-head) rows): decode attention + score + node mass (rows: "
+                       f"{fleet.cores} worker processes over layers) + MSVE + allocate (once) + "
+                       f"evict; after the GPU arm's leaf-cycling warm-up ({len(warm_order)} steps, "
+                       f"same queries); median of {len(times)} timed steps (wall clock incl. IPC)")}
+
+
+def bench_inputs(config, seed, device):
+    """The GPU arm's seeded inputs, on the host: K/V, the warm-up queries (leaf-cycling
+    order, 4 steps per leaf) and the two step queries (workload.Scenario.queries)."""
+    import torch
     import synth
-    from oracle.state import ArborOracle, default_params
     from paper_2605_22106_b200 import workload
     p = workload.PRESETS[config]
     tree = workload.build_tree(p, seed)
-    T = tree.total_tokens
-    K, V, E = synth.make_kv(1, p["H"], T, p["d"], p["dtype"], seed, tree.span_start, tree.span_len)
-    op = default_params(**p["params"])
-    rows_total = p["L"] * p["H"]
-    rows_sample = p["H"]
-    orc = ArborOracle(K.double().numpy(), V.double().numpy(), p["Hq"], p["P"],
-                      sum(-(-int(x) // p["P"]) for x in tree.span_len) + 64, op,
-                      num_layers_global=p["L"], num_q_heads_global=p["Hq"])
-    for i in range(tree.num_nodes):
-        orc.open_node(i, int(tree.span_start[i]))
-        orc.append(i, int(tree.span_len[i]))
-        orc.close_node(i)
+    K, V, E = synth.make_kv(p["L"], p["H"], tree.total_tokens, p["d"], p["dtype"], seed,
+                            tree.span_start, tree.span_len, device=device)
+    order = [leaf for leaf in workload.leaf_cycle_order(tree, seed) for _ in range(4)]
+
+    def q(step):
+        return synth.make_queries(1, p["L"], p["Hq"], p["d"], p["dtype"],
+                                  workload.query_seed(seed, step), E, device=device).float().cpu()
+    q_warm = [q(j) for j in range(len(order))]
+    q_step = [q(10_000 + i) for i in range(2)]
     leaves = sorted(synth.leaves_of(tree), key=lambda x: -float(tree.v[x]))[:2]
-    # a short leaf-cycling warm-up on the sample so A is not all zero
-    for j, leaf in enumerate(workload.leaf_cycle_order(tree, seed)[:16]):
-        tree.active = [leaf]
-        q = synth.make_queries(1, 1, p["Hq"], p["d"], p["dtype"], j, E).double().numpy()
-        orc.score_accumulate(tree, q)
-    B = int(math.floor(p["rho"] * T))
-    import copy
-    base = copy.deepcopy(orc)
-    times = []
-    t_start = time.perf_counter()
-    nsteps = max(1, warmup + steps)
-    for i in range(nsteps):
-        o = copy.deepcopy(base)
-        tree.active = [leaves[i % 2]]
-        q = synth.make_queries(1, 1, p["Hq"], p["d"], p["dtype"], 10_000 + i, E).double().numpy()
-        t0 = time.perf_counter()
-        _, lse = o.decode(tree, q)
-        o.score_accumulate(tree, q, lse)
-        a, s = o.msve(tree)
-        k = o.allocate(tree, s, B)
-        o.evict(tree, k)
-        dt = time.perf_counter() - t0
-        if i >= warmup:
-            times.append(dt)
-        if time.perf_counter() - t_start > target_s and len(times) >= 1:
-            break
-    t_step = statistics.median(times)
-    t_full = t_step * rows_total / rows_sample
-    return {"value": T / t_full, "ms_per_step_full": t_full * 1e3, "cores": 1,
-            "sample": f"{config}: full tree ({tree.num_nodes} nodes, {T} tokens), rows of layer 0 "
-                      f"only ({rows_sample} of {rows_total} (layer, KV-head) rows); one step = "
-                      f"decode attention + score + mass/MSVE + allocate + evict; median of "
-                      f"{len(times)} steps ({t_step:.2f} s each), scaled x{rows_total // rows_sample} "
-                      f"to all rows; numpy/BLAS limited to 1 thread"}
+    B = int(math.floor(p["rho"] * tree.total_tokens))
+    return K.float().cpu(), V.float().cpu(), q_warm, q_step, order, leaves, B
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -521,9 +684,23 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        r = cpu_oracle_sample(args.config, args.seed, 0, 3)
+        # the oracle on the host cores, same inputs / warm-up / step as this arm (sc.K, sc.V
+        # are this process's device tensors; queries regenerated with the same seeds)
+        Kh, Vh = sc.K.float().cpu(), sc.V.float().cpu()
+        _, _, q_warm, q_step, order, leaves_h, B_h = bench_inputs(args.config, args.seed, dev)
+        k_gpu = []
+        for i in range(2):
+            restore()
+            step(i)
+            torch.cuda.synchronize()
+            k_gpu.append(k_buf.cpu().tolist())
+        r = oracle_host_run(args.config, args.seed, 1, 3, Kh, Vh, q_warm, q_step, order,
+                            leaves_h, B_h, target_s=30.0, k_gpu=k_gpu)
+        del Kh, Vh
         cpu = {"value": r["value"], "unit": "tokens/s", "cores": r["cores"], "kind": "oracle",
-               "sample": r["sample"]}
+               "sample": r["sample"], "cpu_model": r["cpu_model"], "host_cores": r["host_cores"],
+               "single_thread_equiv_tokens_per_s": r["single_thread_equiv_tokens_per_s"],
+               "k_equals_gpu": r["k_equals_gpu"], "wall_s": r["wall_s"]}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws,

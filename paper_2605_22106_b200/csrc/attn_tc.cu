@@ -671,7 +671,6 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       if (tid == 64) TC_TRACE(k, 7);
       const TcHdr hd = hdr[k % RING];
       mbar_arrive(&kcons[s]);               // past the full_k wait: K(k + NSK) may land
-      if (half == 0 && lane == 0 && quad == 0) ohdr[k & 3] = hd;   // for the epilogue warps
       const int cntA = hd.meta >> 4;
       const bool pack = (hd.meta & 2) != 0;
       // this half's query columns: a packed B half has its own, after A's
@@ -689,6 +688,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       tc_fence_after();
       // P buffer b was last read by MMA2(k−2)
       if (k >= 2) mbar_wait(&o_full[b], ((k - 2) >> 1) & 1u);
+      // the header for the epilogue warps: ring slot k&3 was last read by epilogue(k − 4),
+      // which did so before its o_empty arrival, which MMA2(k − 2) — complete, o_full above —
+      // waited for (written earlier, right after the full_k wait, it could overtake
+      // epilogue(k − 4) once K runs ahead: tiles with another tile's header)
+      if (half == 0 && lane == 0 && quad == 0) ohdr[k & 3] = hd;
       // P (bf16) goes to row n of slot-half `half` of the Pᵀ tile; rows of columns past the
       // tile's own keep stale values: they only feed output columns that are never stored
       // (Oᵀ column n depends on Pᵀ row n alone)

@@ -60,7 +60,21 @@ struct CompactArgs {
   int exp;          // ARBOR_EVICT_EXP (measurement only): bit0 skip moves, bit1 skip radix select
   int select_mode;  // arbor_select_mode (f4)
   int n_sinks;      // block-level sinks of ARBOR_SELECT_SINKS_TAIL
+  long long *trace; // ARBOR_EVICT_TRACE=1 (diagnostics): [cta][warp][4] globaltimer ns
 };
+
+__device__ __forceinline__ long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<long long>(t);
+}
+// trace events per warp: 0 kernel start (after griddepcontrol.wait), 1 plan done,
+// 2 first job handed / started, 3 last job handed / done
+#define EV_TRACE(e)                                                                           \
+  do {                                                                                        \
+    if (a.trace && lane == 0)                                                                 \
+      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * 4 + (e)] = gtimer(); \
+  } while (0)
 
 constexpr int kPlanPer = 6;   // nodes per thread in the plan scan (N ≤ 3072 = 6 × 512)
 
@@ -141,6 +155,7 @@ select_move_ws_kernel(CompactArgs a) {
   __syncthreads();
   pdl_wait();
   pdl_trigger();
+  EV_TRACE(0);
   // ---- plan (Alg. 2, Q17): k_app = min(k_cur, k_target) for every non-pinned node;
   // the changed ones, ascending id, are the work list.  Every CTA derives it from the same
   // unmodified state into its own copy; the last CTA to get there (ticket) applies it —
@@ -188,6 +203,7 @@ select_move_ws_kernel(CompactArgs a) {
     if (threadIdx.x == 0) { s_work = tot_work; s_free = tot_free; }
   }
   __syncthreads();
+  EV_TRACE(1);
   const int items = s_work * a.R;
   const int stride = gridDim.x * kPairsWs;
   const int first = blockIdx.x * kPairsWs + pid;
@@ -236,6 +252,7 @@ select_move_ws_kernel(CompactArgs a) {
     for (int it = first; it < items; it += stride, ++k) {
       const int sl = k & (kJobSlots - 1);
       mbar_wait(&full[sl], (k / kJobSlots) & 1);
+      if (k == 0) EV_TRACE(2);
       const int nm = (a.exp & 1) ? 0 : mycount[sl];
       const int2 *jb = myjobs + sl * jcap;
       for (int c0 = 0; c0 < nm; c0 += rpi * kUw) {
@@ -266,6 +283,7 @@ select_move_ws_kernel(CompactArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[sl]);
     }
+    EV_TRACE(3);
     return;
   }
   // -------------------------------------------------------------- select warp
@@ -484,10 +502,15 @@ select_move_ws_kernel(CompactArgs a) {
     if (lane == 0) mycount[sl] = nm;
     __syncwarp();
     if (lane == 0) mbar_arrive(&full[sl]);
+    if (k == 0) EV_TRACE(2);
   }
+  EV_TRACE(3);
 }
 
 }  // namespace
+
+long long *g_evict_trace = nullptr;
+size_t g_evict_trace_n = 0;
 
 void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
   CompactArgs a{};
@@ -526,6 +549,21 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
     return e ? atoi(e) : 0;
   }();
   a.exp = exp_flags;
+  a.trace = nullptr;
+  static long long *trace = nullptr;
+  static size_t trace_n = 0;
+  if (getenv("ARBOR_EVICT_TRACE")) {
+    const size_t need = static_cast<size_t>(c->num_sms) * kEvictCtasPerSm * 2 * kPairsWs * 4;
+    if (need > trace_n) {
+      if (trace) cudaFree(trace);
+      cudaMalloc(&trace, need * sizeof(long long));
+      trace_n = need;
+    }
+    cudaMemsetAsync(trace, 0, trace_n * sizeof(long long), c->ms);
+    a.trace = trace;
+    g_evict_trace = trace;
+    g_evict_trace_n = trace_n;
+  }
   const WsLayout ly(a.cap, a.lgP);
   // occupancy / smem attribute cached per capacity (host-side cost stays off the launch path)
   static size_t attr_smem = 0;
@@ -551,3 +589,11 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
 }
 
 }  // namespace arbor
+
+// debug only (not part of include/arbor.h): the last ARBOR_EVICT_TRACE timeline
+// ([cta][16 warps][4] globaltimer ns; warps 0-7 select, 8-15 move) and its grid size
+extern "C" int arbor_debug_evict_trace(long long *host, long long count) {
+  if (!arbor::g_evict_trace || count < 0 || static_cast<size_t>(count) > arbor::g_evict_trace_n) return -1;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(host, arbor::g_evict_trace, sizeof(long long) * count, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
+}

@@ -1,5 +1,6 @@
 // tile.cuh — paged K/V tile staging shared by the attention and score kernels.
 #pragma once
+#include <cstdio>
 #include "common.cuh"
 
 namespace arbor {
@@ -130,9 +131,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 #ifdef ARBOR_MBAR_WATCHDOG
-  // debug builds (ARBOR_NVCC_FLAGS=-DARBOR_MBAR_WATCHDOG): a wait that has not completed
-  // after ~2^31 polls traps, so a pipeline deadlock surfaces as a CUDA error, not a hang
-  for (long long it = 0;; ++it) {
+  // debug builds (ARBOR_NVCC_FLAGS=-DARBOR_MBAR_WATCHDOG): a wait still pending after 5 s
+  // prints the barrier and traps, so a pipeline deadlock surfaces as a CUDA error, not a hang
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
     uint32_t ok;
     asm volatile(
         "{\n"
@@ -141,7 +144,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "selp.u32 %0, 1, 0, p;\n"
         "}\n" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     if (ok) return;
-    if (it > (1ll << 31)) __trap();
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 5000000000ull) {
+      printf("mbarrier watchdog: block %d thread %d bar smem 0x%x parity %u\n", blockIdx.x,
+             threadIdx.x, smem_u32(bar), parity);
+      __trap();
+    }
   }
 #endif
   asm volatile(
