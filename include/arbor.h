@@ -60,6 +60,12 @@ typedef enum {
 
 /* config.flags */
 #define ARBOR_FLAG_PROFILE 1u   /* record CUDA events around every kernel (arbor_stage_times) */
+/* world_size > 1 without the library's NCCL communicator: arbor_score / arbor_decode_step stop
+ * after the partial node masses (a10's input, arbor_mass_buffer); the caller sums that int64
+ * buffer across the ranks with its own collective (e.g. torch.distributed all_reduce, or —
+ * KV-head shards on one device — a plain device sum) and calls arbor_score_finish, which runs
+ * the MSVE on the reduced masses.  nccl_unique_id is then ignored. */
+#define ARBOR_FLAG_EXTERNAL_REDUCE 2u
 
 /* Parameter bundle Π (Alg. 1 caption P:498, Alg. 2).  Host struct. */
 typedef struct {
@@ -197,9 +203,12 @@ arbor_status arbor_allocate(arbor_ctx *ctx, const arbor_tree *tree, const float 
  * For every non-pinned closed node j with k_app = min(k_cur_j, max(0, k_target_j)) <
  * k_cur_j, and every row (l, h): keep the last min(L_tail, n_j) positions, plus the top
  * (k_app − tail) currently kept positions by the key ⟨f32 A, position⟩ (descending, Q3);
- * if k_app ≤ tail keep the last k_app.  Kept K/V/pos rows are compacted in place,
- * stable, into the node's page prefix; its page list is truncated to ⌈k_app/P⌉ and the
- * freed pages pushed on the LIFO free list (nodes ascending).  Pinned nodes are untouched.
+ * if k_app ≤ tail keep the last k_app.  Kept K/V/pos rows are compacted in place into
+ * the node's slot prefix [0, k_app) by hole filling (Q23'): kept rows already in
+ * the prefix stay, the i-th dropped slot of the prefix (ascending) receives the i-th kept
+ * row from beyond it (ascending); every slot carries its position tag.  The page list is
+ * truncated to ⌈k_app/P⌉ and the freed pages pushed on the LIFO free list (nodes
+ * ascending).  Pinned nodes are untouched.
  *  k_target: DEVICE [num_nodes] int32 (e.g. arbor_allocate's k_out)
  *  evicted_tokens_out: HOST, optional (forces a sync): Σ_j (k_cur_j − k_app_j). */
 arbor_status arbor_evict(arbor_ctx *ctx, const arbor_tree *tree, const int32_t *k_target,
@@ -283,6 +292,18 @@ arbor_status arbor_read_free_list(arbor_ctx *ctx, int32_t *pages, int32_t *count
  * partial), Nq_i, a_i, s_i as of the last arbor_score. */
 arbor_status arbor_read_scores(arbor_ctx *ctx, int32_t num_nodes, int64_t *mass,
                                int64_t *mclose, int64_t *nq, float *a, float *s);
+/* a10 input/output: the device buffer of this rank's per-node partial masses, int64
+ * [2 * num_nodes] = [Mass_0..Mass_{N−1} | Mclose_0..Mclose_{N−1}] (units of 2^-24, Q29) as
+ * of the last arbor_score / arbor_decode_step (N = that call's num_nodes).  The all-reduce
+ * is an int64 SUM of this buffer across ranks, in place.  DEVICE pointer, library-owned,
+ * valid for the context's lifetime; *count = 2N.  No sync. */
+arbor_status arbor_mass_buffer(arbor_ctx *ctx, int64_t **dev, int32_t *count);
+/* ARBOR_FLAG_EXTERNAL_REDUCE only: complete the last arbor_score / arbor_decode_step after
+ * the caller's all-reduce — reduced: DEVICE int64 [2N], the summed buffer (copied into the
+ * library's), or NULL when the caller reduced arbor_mass_buffer in place; then a_i, s_i
+ * (MSVE) as on a single rank.  s_out: DEVICE [N] f32 or NULL.  Asynchronous on
+ * main_stream.  ARBOR_ERR_STATE if no score is pending. */
+arbor_status arbor_score_finish(arbor_ctx *ctx, const int64_t *reduced, float *s_out);
 /* HOST out: total rehydrations performed (sync). */
 arbor_status arbor_read_counters(arbor_ctx *ctx, int64_t *rehydrations, int64_t *pages_in_use);
 /* Save / restore the library-owned state (page tables, free list, k_cur, counters) in a

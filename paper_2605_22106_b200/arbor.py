@@ -22,6 +22,7 @@ STATUS = {0: "OK", 2: "INVALID_ARG", 3: "INFEASIBLE_BUDGET", 4: "INVARIANT", 5: 
 ALLOC_MODES = {"waterfill": 0, "static": 1, "static_drain": 2}
 SELECT_MODES = {"heavy": 0, "tail": 1, "sinks_tail": 2}
 FLAG_PROFILE = 1
+FLAG_EXTERNAL_REDUCE = 2
 NUM_STAGES = 13
 STAGES = ["geometry", "score_accum", "node_mass", "msve", "allocate", "evict_plan",
           "select_compact", "rehydrate", "attn", "attn_merge", "allreduce", "stash",
@@ -96,6 +97,8 @@ def load_library(path: str = LIB_PATH):
         "arbor_read_free_list": ([P, P, P], I32),
         "arbor_read_scores": ([P, I32, P, P, P, P, P], I32),
         "arbor_read_counters": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], I32),
+        "arbor_mass_buffer": ([P, C.POINTER(C.c_void_p), C.POINTER(C.c_int32)], I32),
+        "arbor_score_finish": ([P, P, P], I32),
         "arbor_save_state": ([P, I32], I32),
         "arbor_load_state": ([P, I32], I32),
         "arbor_launch_count": ([P], I64),
@@ -207,7 +210,7 @@ class ArborKV:
                  page_size=16, num_pages, max_nodes, max_node_tokens, max_active=16, max_tokens,
                  params: ArborParams, layer_begin=0, layer_count=None, kv_head_begin=0,
                  kv_head_count=None, rank=0, world_size=1, nccl_id: bytes = None,
-                 profile=False, device=None):
+                 profile=False, device=None, external_reduce=False):
         import torch
         if not torch.cuda.is_available():
             raise ArborError(8, "no CUDA device: the ArborKV path has no CPU fallback")
@@ -241,7 +244,8 @@ class ArborKV:
                           self.score.data_ptr(), None, 0, rank, world_size,
                           C.cast(self._nccl, C.c_void_p) if self._nccl is not None else None,
                           self.stream.cuda_stream, self.side.cuda_stream,
-                          FLAG_PROFILE if profile else 0)
+                          (FLAG_PROFILE if profile else 0) |
+                          (FLAG_EXTERNAL_REDUCE if external_reduce else 0))
         self.params = params
         self._ctx = C.c_void_p()
         st = self.lib.arbor_init(C.byref(cfg), C.byref(params), C.byref(self._ctx))
@@ -394,6 +398,19 @@ class ArborKV:
                                                mclose.ctypes.data, nq.ctypes.data, a.ctypes.data,
                                                s.ctypes.data), "arbor_read_scores")
         return dict(mass=mass, mclose=mclose, nq=nq, a=a, s=s)
+
+    def arbor_mass_buffer(self):
+        """a10's buffer: (device pointer, count) of this rank's int64 partial masses
+        [Mass | Mclose] of the last score call (include/arbor.h)."""
+        ptr, cnt = C.c_void_p(), C.c_int32(0)
+        self._check(self.lib.arbor_mass_buffer(self._ctx, C.byref(ptr), C.byref(cnt)), "arbor_mass_buffer")
+        return int(ptr.value or 0), int(cnt.value)
+
+    def arbor_score_finish(self, reduced=None, s_out=None):
+        """ARBOR_FLAG_EXTERNAL_REDUCE: MSVE on the reduced masses (a DEVICE int64 tensor
+        [2N], or None when arbor_mass_buffer was reduced in place)."""
+        self._check(self.lib.arbor_score_finish(self._ctx, self._ptr(reduced), self._ptr(s_out)),
+                    "arbor_score_finish")
 
     def arbor_read_counters(self):
         r, p = C.c_int64(0), C.c_int64(0)

@@ -610,7 +610,8 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   if (k.max_active < 1 || k.max_active > 1024 || k.max_tokens < 1) return ARBOR_ERR_INVALID_ARG;
   if (!k.k_pool || !k.v_pool || !k.pos_pool || !k.score) return ARBOR_ERR_INVALID_ARG;
   if (k.world_size < 1 || k.rank < 0 || k.rank >= k.world_size) return ARBOR_ERR_INVALID_ARG;
-  if (k.world_size > 1 && !k.nccl_unique_id) return ARBOR_ERR_INVALID_ARG;
+  const bool ext_reduce = (k.flags & ARBOR_FLAG_EXTERNAL_REDUCE) != 0;
+  if (k.world_size > 1 && !k.nccl_unique_id && !ext_reduce) return ARBOR_ERR_INVALID_ARG;
 
   arbor_ctx *c = new arbor_ctx();
   c->cfg = k;
@@ -721,7 +722,7 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   }
   if (cudaHostGetDevicePointer(&c->stash_dev, c->stash_host, 0) != cudaSuccess) return bail(ARBOR_ERR_IO);
   // NCCL communicator for the mass all-reduce (a10)
-  if (k.world_size > 1) {
+  if (k.world_size > 1 && !ext_reduce) {
     if (!g_nccl.load()) return bail(ARBOR_ERR_NCCL);
     ncclUniqueId id;
     std::memcpy(&id, k.nccl_unique_id, sizeof(id));
@@ -871,7 +872,12 @@ static int score_parts(size_t mass_nodes) {
 }
 
 // a10 + MSVE on several ranks: the all-reduce sits between the partial masses and the score
+// (ARBOR_FLAG_EXTERNAL_REDUCE: the caller's collective, then arbor_score_finish)
 static arbor_status score_allreduce(arbor_ctx *c, int N, float *s_out) {
+  if (c->cfg.flags & ARBOR_FLAG_EXTERNAL_REDUCE) {
+    c->reduce_pending_n = N;
+    return ARBOR_OK;
+  }
   stage_begin(c, ARBOR_ST_ALLREDUCE, c->ms);
   if (g_nccl.allReduce(c->d.mass2, c->d.mass2, 2 * static_cast<size_t>(N), ncclInt64, ncclSum,
                        static_cast<ncclComm_t>(c->nccl_comm), c->ms) != ncclSuccess)
@@ -1223,6 +1229,27 @@ arbor_status arbor_read_scores(arbor_ctx *c, int32_t num_nodes, int64_t *mass, i
   if (nq) for (int i = 0; i < N; ++i) nq[i] = c->h_nq[i];
   if (a && N) CK(cudaMemcpy(a, c->d.a, N * 4, cudaMemcpyDeviceToHost));
   if (s && N) CK(cudaMemcpy(s, c->d.s, N * 4, cudaMemcpyDeviceToHost));
+  return ARBOR_OK;
+}
+
+arbor_status arbor_mass_buffer(arbor_ctx *c, int64_t **dev, int32_t *count) {
+  if (!c || !dev || !count) return ARBOR_ERR_INVALID_ARG;
+  *dev = c->d.mass2;
+  *count = 2 * (c->reduce_pending_n >= 0 ? c->reduce_pending_n : c->num_known);
+  return ARBOR_OK;
+}
+
+arbor_status arbor_score_finish(arbor_ctx *c, const int64_t *reduced, float *s_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  if (!(c->cfg.flags & ARBOR_FLAG_EXTERNAL_REDUCE) || c->reduce_pending_n < 0)
+    return fail(c, ARBOR_ERR_STATE, "arbor_score_finish: no score awaits an external reduction");
+  const int N = c->reduce_pending_n;
+  if (reduced && reduced != c->d.mass2)
+    CK(cudaMemcpyAsync(c->d.mass2, reduced, 2 * static_cast<size_t>(N) * sizeof(int64_t),
+                       cudaMemcpyDeviceToDevice, c->ms));
+  launch_msve(c, N, s_out);
+  CK_LAUNCH();
+  c->reduce_pending_n = -1;
   return ARBOR_OK;
 }
 

@@ -284,7 +284,13 @@ __device__ __forceinline__ float warp_reduce16(const float *v, int lane) {
   return kMax ? fmaxf(d, r) : d + r;
 }
 
+#ifdef ARBOR_TC_GW16
 template <int NQ> constexpr int kW = NQ % 16 == 0 ? 16 : 8;   // reduction group width
+#else
+// reduction group width: 8 columns (two leaves of G = 4) — most tiles hold one or two leaves,
+// whose columns a 16-wide group would process mostly masked
+template <int NQ> constexpr int kW = 8;
+#endif
 template <int NQ>
 __device__ __forceinline__ int colW(int lane) { return kW<NQ> == 16 ? col16(lane) : col8(lane); }
 template <int W, bool kMax>
@@ -351,6 +357,10 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   // column max / sum of each warp quadrant, ring of 4 tiles (the epilogue warps read tile k's
   // before releasing Oᵀ buffer k&1, which softmax(k+4) needs first)
   __shared__ float red_m[4][4][NQ], red_l[4][4][NQ];
+  // column n of a tile = leaf slot j = n / qw, q head g = n % qw: col_j[n] = j and
+  // col_js[n] = j·SP + g (SP = Lc·H·G: the pair stride of zbuf / partials in (l, h, g) units);
+  // launch constants, so the per-column address math needs no division
+  __shared__ int col_j[NQ], col_js[NQ];
   __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -421,6 +431,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       *reinterpret_cast<uint4 *>(Pbuf + i) = make_uint4(0, 0, 0, 0);
     fence_proxy_async();
   }
+  if (tid >= 64 && tid < 64 + NQ) {
+    const int n = tid - 64, j = n / a.qw;
+    col_j[n] = j;
+    col_js[n] = j * (a.Lc * a.g.H * a.G) + (n - j * a.qw);
+  }
   if (tid == 32) {
     for (int s = 0; s < NSK; ++s) {
       mbar_init(&full_k[s], 1);
@@ -482,7 +497,11 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         // TMEM buffer, which throttled NSK = 2 and could alias at NSK = 3).
         const int sk = kk_k % NSK;
         const uint32_t par = ((kk_k / NSK) & 1u) ^ 1u;
+#ifdef ARBOR_TC_NOGATE   // diagnostics only: no kcons gate (can deadlock)
+        const bool ok = mbar_test(&empty_k[sk], par);
+#else
         const bool ok = mbar_test(&empty_k[sk], par) && mbar_test(&kcons[sk], par);
+#endif
         go_k = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
       }
       if (go_k) {
@@ -729,10 +748,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 #pragma unroll
           for (int i = 0; i < GW; ++i) {
             const int n = c + i;
-            if ((cm >> n) & 1ull) {
-              const int j = n / qw;
-              zr[static_cast<int64_t>((j - lofs) * SP + (n - j * qw)) * kAttnChunk] = z[i];
-            }
+            if ((cm >> n) & 1ull)
+              zr[static_cast<int64_t>(col_js[n] - lofs * SP) * kAttnChunk] = z[i];
           }
         }
       }
@@ -795,8 +812,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       float *pbq = a.partials + ((static_cast<int64_t>(pack ? hd.pbB : hd.pbA) * a.Lc + hd.li) * a.g.H + hd.h) * G * 130 + trow -
                    static_cast<int64_t>(cntA) * SP * 130;     // so that slot j ≥ cntA lands at j − cntA
       auto col_ptr = [&](int n) {
-        const int j = n / qw;
-        return (j < cntA ? pa : pbq) + static_cast<int64_t>(j * SP + (n - j * qw)) * 130;
+        return (col_j[n] < cntA ? pa : pbq) + static_cast<int64_t>(col_js[n]) * 130;
       };
 #pragma unroll 1
       for (int gi = 0; gi < ngrp; ++gi) {

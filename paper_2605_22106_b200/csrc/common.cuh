@@ -39,8 +39,9 @@ struct Ctrl {
   int32_t err;             // DERR_* bits
   int32_t work_count;      // evict work items of the last plan
   int32_t rehyd_count;     // nodes rehydrated by the last plan
-  int32_t move_count;      // unused
   int32_t plan_ticket;     // last-CTA ticket of the fused evict kernel (zero at rest)
+  int32_t item_next;       // evict: next (node, row) work item to hand out (zero at rest)
+  int32_t item_done;       // evict: select warps past the last item (zero at rest)
   long long evicted;       // tokens evicted by the last evict
   long long rehydrations;  // total rehydrations
   long long pages_in_use;  // pages held by nodes
@@ -172,6 +173,7 @@ struct arbor_ctx {
   long long lg_epoch = -1, lg_tree = -1;
   // cached per-node partial masses are exact for the current A (score.cu)
   bool mass_valid = true;
+  int reduce_pending_n = -1;   // ARBOR_FLAG_EXTERNAL_REDUCE: N of the scores awaiting arbor_score_finish
   size_t scratch_q = 0;
   // NCCL
   void *nccl_comm = nullptr;

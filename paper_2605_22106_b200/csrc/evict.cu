@@ -61,7 +61,9 @@ struct CompactArgs {
   int select_mode;  // arbor_select_mode (f4)
   int n_sinks;      // block-level sinks of ARBOR_SELECT_SINKS_TAIL
   long long *trace; // ARBOR_EVICT_TRACE=1 (diagnostics): [cta][warp][4] globaltimer ns
+  int wl_smem;      // N when the work list also lives in shared memory (N ≤ kSmemWorkNodes), else 0
 };
+constexpr int kSmemWorkNodes = 1024;   // 32 KB of work entries per CTA
 
 __device__ __forceinline__ long long gtimer() {
   unsigned long long t;
@@ -76,7 +78,6 @@ __device__ __forceinline__ long long gtimer() {
       a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * 4 + (e)] = gtimer(); \
   } while (0)
 
-constexpr int kPlanPer = 6;   // nodes per thread in the plan scan (N ≤ 3072 = 6 × 512)
 
 __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem)), "l"(gmem)
@@ -90,9 +91,11 @@ __device__ __forceinline__ void cp_async16ca(void *smem, const void *gmem) {
 // Shared-memory layout of select_move_ws_kernel (per CTA), all offsets 16-byte aligned.
 struct WsLayout {
   int cap, capP, pcap, jcap;
-  size_t keys, lists, abuf, pbuf, gbuf, mbuf, jobs, jcount, bars, total;
-  __host__ __device__ WsLayout(int cap_, int lgP) {
+  int wl_n;                                // nodes of the shared-memory work list (0: global)
+  size_t keys, lists, abuf, pbuf, gbuf, mbuf, jobs, jcount, bars, iring, swl, total;
+  __host__ __device__ WsLayout(int cap_, int lgP, int wl_n_) {
     cap = cap_;
+    wl_n = wl_n_;
     capP = (cap + 9) & ~7;                 // pos pairs may read one slot past k_cur
     pcap = (cap >> lgP) + 2;
     jcap = cap / 2 + 1;                    // moves per item ≤ min(k_app, k_cur − k_app)
@@ -107,13 +110,15 @@ struct WsLayout {
     jobs = take(size_t(kPairsWs) * kJobSlots * jcap * 8);  // (src row, dst row) job queues
     jcount = take(size_t(kPairsWs) * kJobSlots * 4);
     bars = take(size_t(kPairsWs) * 2 * kJobSlots * 8);
+    iring = take(size_t(kPairsWs) * 4 * 4);                // drawn work items, 4 pipeline slots
+    swl = take(size_t(wl_n) * sizeof(WorkEnt));            // this CTA's work list (small trees)
     total = o;
   }
 };
 
 // Warp-specialised select + move.  A CTA holds kPairsWs (select warp, move warp) pairs.
 //
-// Select warp p processes the work items it = first + k·stride (item = (changed node, row)).
+// Select warp p processes work items (item = (changed node, row)) drawn from a global counter.
 // Its global reads run three items ahead through a cp.async pipeline (no register cost, no
 // exposed latency): work entry of item k+3 → page list of item k+2 → pos tags and A span of
 // item k+1 (A is read by position over the span, independent of the pos tags), while item k
@@ -135,7 +140,7 @@ select_move_ws_kernel(CompactArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool mover = warp >= kPairsWs;
   const int pid = mover ? warp - kPairsWs : warp;
-  const WsLayout Ly(a.cap, a.lgP);
+  const WsLayout Ly(a.cap, a.lgP, a.wl_smem);
   const int cap = Ly.cap, capP = Ly.capP, pcap = Ly.pcap, jcap = Ly.jcap;
   const int lgP = a.lgP, Pm = (1 << lgP) - 1;
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm + Ly.bars);
@@ -163,50 +168,55 @@ select_move_ws_kernel(CompactArgs a) {
   // ascending (node, list) order — after every CTA has read that state.
   WorkEnt *wl = a.work + static_cast<int64_t>(blockIdx.x) * a.MN;
   {
-    int kc[kPlanPer], ka[kPlanPer], ev[kPlanPer], fr[kPlanPer], wo[kPlanPer], fo[kPlanPer];
+    // nodes j = i·blockDim + thread, one slice i at a time: the slice's loads in one round
+    // trip, then two block scans (work list offsets, freed-page offsets) in ascending id;
+    // most trees (N ≤ blockDim) are a single slice
+    int tot_work = 0, tot_free = 0;
     unsigned long long my_ev = 0;
-    
-#pragma unroll
-    for (int i = 0; i < kPlanPer; ++i) {
-      const int j = threadIdx.x * kPlanPer + i;
-      kc[i] = 0; ka[i] = 0; ev[i] = 0; fr[i] = 0;
+    WorkEnt *swl = reinterpret_cast<WorkEnt *>(sm + Ly.swl);
+    for (int j0 = 0; j0 < a.N; j0 += blockDim.x) {
+      const int j = j0 + threadIdx.x;
+      int kc = 0, kt = 0, nn = 0, npg = 0;
+      long long sp = 0;
+      bool pin = true;
       if (j < a.N) {
-        kc[i] = a.kcur[j];
-        const int kt = max(a.k_target[j], 0);
-        ka[i] = min(kt, kc[i]);
-        if (!a.pinned[j] && ka[i] < kc[i]) {
-          ev[i] = 1;
-          fr[i] = a.npages[j] - ((ka[i] + a.P - 1) >> lgP);
-          my_ev += static_cast<unsigned long long>(kc[i] - ka[i]);
-        }
+        kc = a.kcur[j];
+        kt = a.k_target[j];
+        pin = a.pinned[j] != 0;
+        npg = a.npages[j];
+        nn = a.n[j];
+        sp = a.span[j];
       }
+      const int ka = min(max(kt, 0), kc);
+      const int ev = (!pin && ka < kc) ? 1 : 0;
+      const int fr = ev ? npg - ((ka + a.P - 1) >> lgP) : 0;
+      if (ev) my_ev += static_cast<unsigned long long>(kc - ka);
+      int wo, fo, tw, tf;
+      Scan(scan_tmp).ExclusiveSum(ev, wo, tw);
+      __syncthreads();
+      Scan(scan_tmp).ExclusiveSum(fr, fo, tf);
+      __syncthreads();
+      if (ev) {
+        WorkEnt e;
+        e.node = j;
+        e.kc = kc;
+        e.ka = ka;
+        e.n = nn;
+        e.span = sp;
+        e.foff = tot_free + fo;
+        e.nfree = fr;
+        wl[tot_work + wo] = e;
+        if (Ly.wl_n) swl[tot_work + wo] = e;
+      }
+      tot_work += tw;
+      tot_free += tf;
     }
-    int tot_work, tot_free;
-    Scan(scan_tmp).ExclusiveSum(ev, wo, tot_work);
-    __syncthreads();
-    Scan(scan_tmp).ExclusiveSum(fr, fo, tot_free);
     if (my_ev) atomicAdd(&s_ev, my_ev);
-#pragma unroll
-    for (int i = 0; i < kPlanPer; ++i) {
-      if (!ev[i]) continue;
-      const int j = threadIdx.x * kPlanPer + i;
-      WorkEnt e;
-      e.node = j;
-      e.kc = kc[i];
-      e.ka = ka[i];
-      e.n = a.n[j];
-      e.span = a.span[j];
-      e.foff = fo[i];
-      e.nfree = fr[i];
-      wl[wo[i]] = e;
-    }
     if (threadIdx.x == 0) { s_work = tot_work; s_free = tot_free; }
   }
   __syncthreads();
   EV_TRACE(1);
   const int items = s_work * a.R;
-  const int stride = gridDim.x * kPairsWs;
-  const int first = blockIdx.x * kPairsWs + pid;
   if (mover) {
     // the move warps take the ticket (they would otherwise wait for their first job)
     const int mt = threadIdx.x - kPairsWs * 32;
@@ -248,12 +258,15 @@ select_move_ws_kernel(CompactArgs a) {
     const int piece = lane % cpr, sub = lane / cpr;
     char *kp8 = static_cast<char *>(a.kpool);
     char *vp8 = static_cast<char *>(a.vpool);
-    int k = 0;
-    for (int it = first; it < items; it += stride, ++k) {
+    // jobs until the select warp posts the end marker (count < 0): the items are handed out
+    // dynamically, so the number of jobs is not known in advance
+    for (int k = 0;; ++k) {
       const int sl = k & (kJobSlots - 1);
       mbar_wait(&full[sl], (k / kJobSlots) & 1);
       if (k == 0) EV_TRACE(2);
-      const int nm = (a.exp & 1) ? 0 : mycount[sl];
+      const int cnt = mycount[sl];
+      if (cnt < 0) break;
+      const int nm = (a.exp & 1) ? 0 : cnt;
       const int2 *jb = myjobs + sl * jcap;
       for (int c0 = 0; c0 < nm; c0 += rpi * kUw) {
         uint4 bk[kUw], bv[kUw];
@@ -298,7 +311,19 @@ select_move_ws_kernel(CompactArgs a) {
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t pstride = static_cast<int64_t>(a.H) << lgP;
   constexpr unsigned long long kCand = 1ull << 63;
-  const int my_items = first < items ? (items - first + stride - 1) / stride : 0;
+  // work items (changed node, row) are handed out dynamically — lane 0 draws the item of
+  // pipeline step k (three steps ahead of the one being ranked) from a global counter — so
+  // every pair finishes within about one item of the others (a static round robin left a
+  // ~40 µs spread of finishing times on C2, profiles/evict_trace.py)
+  // The draw for step k + 4 is issued at the top of step k and stored at its end (its latency
+  // hides behind the ranking).
+  int *iring = reinterpret_cast<int *>(sm + Ly.iring) + pid * 4;
+  auto item_of = [&](int k) { return iring[k & 3]; };
+  const WorkEnt *swl = reinterpret_cast<const WorkEnt *>(sm + Ly.swl);
+  // work entry of pipeline step k: the shared-memory work list, or the cp.async'ed copy
+  auto meta = [&](int k) -> const WorkEnt & {
+    return Ly.wl_n ? swl[item_of(k) / a.R] : Mbuf[k & 3];
+  };
   auto row_base = [&](int it) -> int64_t {
     const int r = it % a.R;
     const int l = r / a.H, h = r - l * a.H;
@@ -306,23 +331,28 @@ select_move_ws_kernel(CompactArgs a) {
   };
   // pipeline stages (each lane issues its share; completion via cp.async.wait_all + __syncwarp)
   auto issue_meta = [&](int k) {
-    if (k >= my_items || lane >= 2) return;
-    const int w = (first + k * stride) / a.R;
+    const int it = item_of(k);
+    if (Ly.wl_n || it >= items || lane >= 2) return;
+    const int w = it / a.R;
     cp_async16ca(reinterpret_cast<char *>(&Mbuf[k & 3]) + lane * 16,
                  reinterpret_cast<const char *>(&wl[w]) + lane * 16);
   };
   auto issue_pages = [&](int k) {
-    if (k >= my_items) return;
-    const WorkEnt &e = Mbuf[k & 3];
+    if (item_of(k) >= items) return;
+    const WorkEnt &e = meta(k);
     const int np = (e.kc + Pm) >> lgP;
     const int32_t *pl = a.ptab + static_cast<int64_t>(e.node) * a.MPN;
     int32_t *g = Gbuf + (k % 3) * pcap;
     for (int i = lane; i < np; i += 32) cp_async4(g + i, pl + i);
   };
-  auto issue_data = [&](int k) {
-    if (k >= my_items) return;
-    const int it = first + k * stride;
-    const WorkEnt &e = Mbuf[k & 3];
+  // pos tags (need the page list) and the A span (needs only the work entry); a full node
+  // (k_cur = n) holds its positions in slot order (appends and rehydration write the
+  // identity, only an eviction permutes slots and it lowers k_cur): no pos tags to load
+  auto issue_pos = [&](int k) {
+    const int it = item_of(k);
+    if (it >= items) return;
+    const WorkEnt &e = meta(k);
+    if (e.kc == e.n) return;
     const int32_t *g = Gbuf + (k % 3) * pcap;
     const int64_t base = row_base(it);
     int16_t *pb = Pbuf + (k & 1) * capP;
@@ -330,6 +360,11 @@ select_move_ws_kernel(CompactArgs a) {
       const int s = 2 * q;
       cp_async4(pb + s, a.pos + base + static_cast<int64_t>(g[s >> lgP]) * pstride + (s & Pm));
     }
+  };
+  auto issue_A = [&](int k) {
+    const int it = item_of(k);
+    if (it >= items) return;
+    const WorkEnt &e = meta(k);
     const int tl = min(a.l_tail, e.n);
     if (e.ka > tl && a.select_mode == ARBOR_SELECT_HEAVY) {   // ranked by A: the non-tail span
       const int r = it % a.R;
@@ -338,31 +373,47 @@ select_move_ws_kernel(CompactArgs a) {
       for (int p = lane; p < e.n - tl; p += 32) cp_async4(ab + p, Arow + p);
     }
   };
-  if (my_items > 0) {
-    issue_meta(0);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncwarp();
-    issue_pages(0);
-    issue_meta(1);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncwarp();
-    issue_data(0);
-    issue_pages(1);
-    issue_meta(2);
-    cp_async_commit();
+  // the first four items of select warp w are 4w … 4w + 3 (no atomic storm at the start);
+  // the counter hands out the rest, from 4·(select warps) on
+  const int nsel = static_cast<int>(gridDim.x) * kPairsWs;
+  const int gw = static_cast<int>(blockIdx.x) * kPairsWs + pid;
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) iring[i] = 4 * gw + i;
   }
-  for (int k = 0; k < my_items; ++k) {
+  __syncwarp();
+  // prologue: work entries 0-2 (smem list: nothing to fetch) → page lists 0, 1 and A of item 0
+  // → pos tags of item 0 (none for a full node)
+  issue_meta(0);
+  issue_meta(1);
+  issue_meta(2);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncwarp();
+  issue_pages(0);
+  issue_pages(1);
+  issue_A(0);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncwarp();
+  issue_pos(0);
+  cp_async_commit();
+  int k = 0;
+  for (;; ++k) {
+    const int it = item_of(k);
+    if (it >= items) break;          // the counter only grows: every later draw is past the end
+    int nxt = 0;
+    if (lane == 0) nxt = 4 * nsel + atomicAdd(&a.ctrl->item_next, 1);   // step k + 4's item
     cp_async_wait_all();
     __syncwarp();
-    issue_data(k + 1);
+    issue_pos(k + 1);
+    issue_A(k + 1);
     issue_pages(k + 2);
     issue_meta(k + 3);
     cp_async_commit();
     // ---- rank item k from shared memory
-    const int it = first + k * stride;
-    const WorkEnt e = Mbuf[k & 3];
+    const WorkEnt e = meta(k);
+    const bool ident = e.kc == e.n;
     const int kc = e.kc, ka = e.ka, n = e.n;
     const int tl = min(a.l_tail, n);
     const int32_t *pgs = Gbuf + (k % 3) * pcap;
@@ -381,7 +432,7 @@ select_move_ws_kernel(CompactArgs a) {
       const int s = s0 + lane;
       unsigned long long kk = 0;
       if (s < kc) {
-        const int p = pb[s];
+        const int p = ident ? s : pb[s];
         kk = static_cast<unsigned>(p);
         if (ranked && p < tail_from) {
           // the key's high part: f32 bits of A (HEAVY), 0 (TAIL: recency), sink flag
@@ -499,10 +550,32 @@ select_move_ws_kernel(CompactArgs a) {
     int2 *jb = myjobs + sl * jcap;
     for (int i = lane; i < nm; i += 32)
       jb[i] = make_int2(static_cast<int>(row(movers[i])), static_cast<int>(row(holes[i])));
-    if (lane == 0) mycount[sl] = nm;
+    if (lane == 0) {
+      mycount[sl] = nm;
+      iring[k & 3] = nxt;            // step k + 4 (read after the next step's __syncwarp)
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&full[sl]);
     if (k == 0) EV_TRACE(2);
+  }
+  cp_async_wait_all();               // prefetches past the end (none were issued, but be tidy)
+  // end marker for the move warp
+  {
+    const int sl = k & (kJobSlots - 1);
+    mbar_wait(&empty[sl], ((k / kJobSlots) & 1) ^ 1);
+    if (lane == 0) {
+      mycount[sl] = -1;
+      mbar_arrive(&full[sl]);
+    }
+  }
+  // the last select warp past the end resets the counters for the next launch (every draw
+  // of this launch has happened by then)
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(&a.ctrl->item_done, 1) == nsel - 1) {
+      a.ctrl->item_next = 0;
+      a.ctrl->item_done = 0;
+    }
   }
   EV_TRACE(3);
 }
@@ -550,6 +623,7 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
   }();
   a.exp = exp_flags;
   a.trace = nullptr;
+  a.wl_smem = N <= kSmemWorkNodes ? N : 0;
   static long long *trace = nullptr;
   static size_t trace_n = 0;
   if (getenv("ARBOR_EVICT_TRACE")) {
@@ -564,23 +638,23 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
     g_evict_trace = trace;
     g_evict_trace_n = trace_n;
   }
-  const WsLayout ly(a.cap, a.lgP);
+  const WsLayout ly(a.cap, a.lgP, a.wl_smem);
   // occupancy / smem attribute cached per capacity (host-side cost stays off the launch path)
   static size_t attr_smem = 0;
-  static int cached_cap = -1, cached_lg = -1, cached_grid = 0;
+  static size_t cached_total = 0;
+  static int cached_grid = 0;
   if (ly.total > attr_smem) {
     const size_t want = ly.total < 48 * 1024 ? 48 * 1024 : ly.total;
     cudaFuncSetAttribute(select_move_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(want));
     attr_smem = want;
   }
-  if (a.cap != cached_cap || a.lgP != cached_lg) {
+  if (ly.total != cached_total) {
     int sms = 148, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, select_move_ws_kernel, kPairsWs * 64, ly.total);
     cached_grid = sms * std::min(std::max(per, 1), kEvictCtasPerSm);
-    cached_cap = a.cap;
-    cached_lg = a.lgP;
+    cached_total = ly.total;
   }
   stage_begin(c, ARBOR_ST_SELECT_COMPACT, c->ms);
   launch_pdl(select_move_ws_kernel, dim3(cached_grid), dim3(kPairsWs * 64), ly.total, c->ms, a);

@@ -27,7 +27,21 @@ def main():
     import paper_2605_22106_b200 as pk
 
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-    sc = workload.setup(cfg, 0)
+    if cfg == "c3dpts":      # the DPTS loop's state: a few transitions, open children decoding
+        T, D = 6, 8
+        extra_nodes, extra_tokens, node_extra = workload.dpts_sizing(T, D)
+        sc = workload.setup("c3", 0, extra_tokens=extra_tokens, extra_nodes=extra_nodes,
+                            max_active=16, node_extra_tokens=node_extra)
+        workload.warmup_leaf_cycling(sc, 1)
+        run = workload.DptsRun(sc, n_active=16, transitions=T, swap=4, decode_steps=D, seed=0)
+        for leaves in [run.base_leaves] + run.schedule:
+            run.transition(leaves)
+            for _ in range(D):
+                run.decode()
+        for ch in sc.tree.active:
+            run._append(ch)
+    else:
+        sc = workload.setup(cfg, 0)
     tree = sc.tree
     nA = len(tree.active)
     q = sc.queries(0, nA)

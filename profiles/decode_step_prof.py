@@ -20,7 +20,19 @@ def main():
 
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-    sc = workload.setup(cfg, 0, profile=True)
+    if cfg == "c3dpts":      # the DPTS loop's state: a few transitions, open children decoding
+        T, D = 6, 8
+        extra_nodes, extra_tokens, node_extra = workload.dpts_sizing(T, D)
+        sc = workload.setup("c3", 0, profile=True, extra_tokens=extra_tokens,
+                            extra_nodes=extra_nodes, max_active=16, node_extra_tokens=node_extra)
+        workload.warmup_leaf_cycling(sc, 1)
+        run = workload.DptsRun(sc, n_active=16, transitions=T, swap=4, decode_steps=D, seed=0)
+        for leaves in [run.base_leaves] + run.schedule:
+            run.transition(leaves)
+            for _ in range(D):
+                run.decode()
+    else:
+        sc = workload.setup(cfg, 0, profile=True)
     ctx, tree = sc.ctx, sc.tree
     nA = len(tree.active)
     qs = [sc.queries(i, nA) for i in range(2)]

@@ -90,3 +90,72 @@ def test_head_shards_sum_to_full(shards):
     for sc in parts:
         assert [sc.ctx.arbor_read_node(i) for i in range(N)] == ref, "page tables differ"
         assert sc.ctx.arbor_read_free_list() == full.ctx.arbor_read_free_list()
+
+
+@pytest.mark.parametrize("shards", [2, 4])
+def test_world_size_gt1_external_reduce_bit_identical(shards):
+    """The world_size > 1 library path on one device: contexts created as
+    ranks r of `shards` (KV-head shards, ARBOR_FLAG_EXTERNAL_REDUCE instead of the NCCL
+    communicator, which needs one GPU per rank) run arbor_decode_step with the multi-rank
+    finisher (no MSVE in decode_post), the test sums their int64 partial-mass buffers
+    (the all-reduce's arithmetic) and each rank runs arbor_score_finish (msve_kernel).
+    s, a, k, page tables and free lists must equal the world_size = 1 context's bit for bit,
+    step after step, with allocation from the library's own scores (s = NULL)."""
+    preset = dict(tree=("full", 3, 4, 96), L=3, H=8, Hq=32, d=128, dtype="bf16", P=16, rho=0.5,
+                  params={}, active="highest_v")
+    workload.PRESETS["_shard_test"] = preset
+    try:
+        full = workload.setup("_shard_test", 7)
+        hc = preset["H"] // shards
+        parts = [workload.setup("_shard_test", 7, kv_head_begin=r * hc, kv_head_count=hc,
+                                rank=r, world_size=shards, external_reduce=True)
+                 for r in range(shards)]
+    finally:
+        del workload.PRESETS["_shard_test"]
+    tree = full.tree
+    N = tree.num_nodes
+    leaves = synth.leaves_of(tree)
+    B = int(math.floor(preset["rho"] * tree.total_tokens))
+    for step in range(6):
+        act = [leaves[(7 * step + j) % len(leaves)] for j in range(1 + step % 2)]
+        for sc in [full] + parts:
+            sc.tree.active = act
+            q = sc.queries(step, len(act))
+            out = torch.empty_like(q)
+            lse = torch.empty((len(act), sc.ctx.L, sc.ctx.Hq), dtype=torch.float32, device="cuda")
+            sc.ctx.arbor_decode_step(sc.tree, q, out, lse)
+        # the all-reduce: int64 sum of every rank's [Mass | Mclose] partials
+        ps = [sc.ctx.arbor_read_scores(N) for sc in parts]
+        for sc in parts:
+            ptr, cnt = sc.ctx.arbor_mass_buffer()
+            assert cnt == 2 * N and ptr != 0
+        red = torch.as_tensor(np.concatenate([sum(p["mass"] for p in ps), sum(p["mclose"] for p in ps)]),
+                              device="cuda")
+        s_parts = []
+        for sc in parts:
+            s = torch.empty(N, dtype=torch.float32, device="cuda")
+            sc.ctx.arbor_score_finish(red, s)
+            s_parts.append(s)
+        fs = full.ctx.arbor_read_scores(N)
+        for sc, s in zip(parts, s_parts):
+            r = sc.ctx.arbor_read_scores(N)
+            assert np.array_equal(r["mass"], fs["mass"]) and np.array_equal(r["nq"], fs["nq"])
+            assert np.array_equal(r["a"].view(np.int32), fs["a"].view(np.int32)), f"a, step {step}"
+            assert np.array_equal(r["s"].view(np.int32), fs["s"].view(np.int32)), f"s, step {step}"
+            assert np.array_equal(s.cpu().numpy().view(np.int32), fs["s"].view(np.int32))
+        if step in (2, 5):
+            ks = []
+            for sc in [full] + parts:
+                k = torch.empty(N, dtype=torch.int32, device="cuda")
+                sc.ctx.arbor_allocate(sc.tree, None, B, k)     # the library's own s
+                sc.ctx.arbor_evict(sc.tree, k)
+                ks.append(k.cpu())
+            for k in ks[1:]:
+                assert torch.equal(k, ks[0]), f"k differs at step {step}"
+            ref = [full.ctx.arbor_read_node(i) for i in range(N)]
+            for sc in parts:
+                assert [sc.ctx.arbor_read_node(i) for i in range(N)] == ref, "page tables differ"
+                assert sc.ctx.arbor_read_free_list() == full.ctx.arbor_read_free_list()
+    # finishing without a pending score is a lifecycle error
+    with pytest.raises(Exception):
+        parts[0].ctx.arbor_score_finish(red)
