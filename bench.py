@@ -667,18 +667,21 @@ def main():
         path = synth_path(tree.parent, tree.active[0])
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         r0 = ctx.arbor_read_counters()[0]
+        # PCIe bytes: the full spans of the path nodes that lost tokens (k_cur < n)
+        need = [x for x in path if ctx.arbor_read_node(x)[0] < int(tree.span_len[x])]
+        nbytes = sum(int(tree.span_len[x]) for x in need) * ctx.L * ctx.H * ctx.D * 2 * (
+            2 if preset["dtype"] == "bf16" else 4)
         torch.cuda.synchronize()
         a.record(stream)
         ctx.arbor_rehydrate(ta, path)
-        b.record(stream)
+        b.record(ctx.side)                      # the copy runs on the side stream
         b.synchronize()
         r1 = ctx.arbor_read_counters()[0]
-        nbytes = sum(int(tree.span_len[x]) for x in path) * ctx.L * ctx.H * ctx.D * 2 * (
-            2 if preset["dtype"] == "bf16" else 4)
         ms = a.elapsed_time(b)
-        rehyd = {"nodes_rehydrated": int(r1 - r0), "ms": ms,
-                 "bytes_upper_bound": nbytes,
-                 "PCIe_GBps_upper_bound": nbytes / (ms / 1e3) / 1e9 if ms > 0 else None}
+        rehyd = {"nodes_rehydrated": int(r1 - r0), "ms": ms, "bytes": nbytes,
+                 "PCIe_GBps": nbytes / (ms / 1e3) / 1e9 if ms > 0 else None,
+                 "note": "zero-copy reads of the pinned-host stash by a side-stream kernel; "
+                         "bytes = full spans of the path nodes with k_cur < n"}
     except Exception as e:  # pragma: no cover
         rehyd = {"error": str(e)}
 
@@ -729,12 +732,13 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
     """configs[2]: the DPTS frontier.  16 active leaves under distinct
     level-2 parents of the 8B-shaped depth-4 × width-5 tree, ρ = 0.5 (B = 9,984 fixed while
     the tree grows).  One step = one transition (4 of the 16 leaves replaced: backtracks into
-    possibly evicted subtrees; a fresh open child under each new leaf) = allocate (a1+a4) →
-    evict (a5+a6) → rehydrate the new Path* (a8, side stream), followed by 8 decode steps
-    (append one token to every open child; a9 over the shared tree; a2+a3).  `value` =
-    cached tokens at the transition ÷ the transition's device time (allocate + evict +
-    rehydrate issue); decode attention is reported with tree sharing (a shared node is read
-    once for all leaves below it)."""
+    possibly evicted subtrees; a fresh open child under each new leaf) = Alg. 2's order:
+    rehydrate the new Path* (a8, side stream) → allocate (a1+a4) → evict (a5+a6), the last two
+    overlapping the copy, followed by 8 decode steps (append one token to every open child;
+    a9 over the shared tree; a2+a3).  `value` = cached tokens at the transition ÷ the
+    allocate + evict device time; rehydration (PCIe) is reported separately, with how long
+    the first decode waits for it; decode attention is reported with tree sharing (a shared
+    node is read once for all leaves below it)."""
     import torch
     import synth
     from paper_2605_22106_b200 import workload
@@ -771,28 +775,33 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
         cached = sum(ctx.arbor_read_node(x)[0] for x in range(tree.num_nodes))
         r0 = ctx.arbor_read_counters()[0]
         k = run.k_buf[:tree.num_nodes]
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        path = [x for x in run.path_union() if not tree.is_open[x]]
+        rbytes = 0                                  # PCIe bytes: only nodes with k_cur < n
+        for x in path:
+            kc_x, n_x, _ = ctx.arbor_read_node(x)
+            if kc_x < n_x:
+                rbytes += n_x * rows * 2 * rb
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        rs, rd = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         l0 = ctx.arbor_launch_count()
+        # Alg. 2 Transition: rehydrate Path* (side stream), then allocate + evict on the main
+        # stream while the copy runs; the first decode waits for the copy
         w0 = time.perf_counter()
+        rs.record(stream)
+        ctx.arbor_rehydrate(ta, path)
+        rd.record(ctx.side)                         # the copy's completion (side stream)
         e[0].record(stream)
         ctx.arbor_allocate(ta, None, run.budget, k)
         e[1].record(stream)
         ctx.arbor_evict(ta, k)
         e[2].record(stream)
-        torch.cuda.synchronize()
+        e[2].synchronize()
         wall = time.perf_counter() - w0
+        e[3].record(stream)                         # where the first decode would start
+        torch.cuda.synchronize()
+        rwall = time.perf_counter() - w0
         launches = ctx.arbor_launch_count() - l0
-        path = [x for x in run.path_union() if not tree.is_open[x]]
-        rbytes = 0
-        for x in path:
-            kc_x, n_x, _ = ctx.arbor_read_node(x)
-            if kc_x < n_x:
-                rbytes += n_x * rows * 2 * rb
-        h0 = time.perf_counter()
-        ctx.arbor_rehydrate(ta, path)
-        ctx.arbor_sync()
-        rwall = time.perf_counter() - h0
         r1 = ctx.arbor_read_counters()[0]
         # a9 bytes with tree sharing: K+V of every kept slot of the union of the active paths
         vis = sum(ctx.arbor_read_node(x)[0] for x in run.path_union())
@@ -815,7 +824,8 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
         torch.cuda.synchronize()
         if timed:
             rec.append(dict(cached=cached, alloc=e[0].elapsed_time(e[1]),
-                            evict=e[1].elapsed_time(e[2]), rehyd=rwall * 1e3,
+                            evict=e[1].elapsed_time(e[2]), rehyd=rs.elapsed_time(rd),
+                            rehyd_wait=max(0.0, e[2].elapsed_time(rd)),
                             trans=e[0].elapsed_time(e[2]), wall=wall, nrehyd=r1 - r0,
                             rehyd_bytes=rbytes, launches=launches, attn=[x[0].elapsed_time(x[1]) for x in dec],
                             score=[x[1].elapsed_time(x[2]) for x in dec], attn_bytes=attn_bytes))
@@ -830,11 +840,11 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
         ta = TreeArgs.from_tree(tree)
         k = run.k_buf[:tree.num_nodes]
         torch.cuda.synchronize()
+        ctx.arbor_rehydrate(ta, [x for x in run.path_union() if not tree.is_open[x]])
         h = time.perf_counter(); ctx.arbor_allocate(ta, None, run.budget, k)
         host_ms["allocate"].append((time.perf_counter() - h) * 1e3)
         h = time.perf_counter(); ctx.arbor_evict(ta, k)
         host_ms["evict"].append((time.perf_counter() - h) * 1e3)
-        ctx.arbor_rehydrate(ta, [x for x in run.path_union() if not tree.is_open[x]])
         for _ in range(D):
             for ch in tree.active:
                 run._append(ch)
@@ -871,8 +881,8 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
             "vs_baseline": None, "dtype": preset["dtype"], "data": "synthetic",
             "config": dict(workload_config("c3", ws), budget=run.budget, active_leaves=16,
                            decode_steps_per_transition=D,
-                           step="one DPTS transition: a1+a4 allocate -> a5+a6 evict -> a8 "
-                                "rehydrate (side stream); then 8 decode steps of arbor_decode_step "
+                           step="one DPTS transition (Alg. 2 order): a8 rehydrate issued on the "
+                                "side stream -> a1+a4 allocate -> a5+a6 evict (timed); then 8 decode steps of arbor_decode_step "
                                 "(a9 + a2/a3, reported separately)"),
             "roofline": {"kernel": "attn_tc (a9, 16 leaves, tree-shared tiles)", "bound": "hbm",
                          "achieved": kern_gbs, "peak": peak, "unit": "GB/s",
@@ -894,12 +904,15 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
                                           for q in (10, 50, 90)],
             "allocate_us_p50": statistics.median(r["alloc"] * 1e3 for r in rec),
             "evict_us_p50": statistics.median(r["evict"] * 1e3 for r in rec),
-            "rehydrate": {"ms_p50_host_wall": statistics.median(r["rehyd"] for r in rec),
+            "rehydrate": {"ms_p50": statistics.median(r["rehyd"] for r in rec),
                           "bytes_per_transition": statistics.mean(r["rehyd_bytes"] for r in rec),
                           "PCIe_GBps": (sum(r["rehyd_bytes"] for r in rec) /
                                         (sum(r["rehyd"] for r in rec) / 1e3) / 1e9)
                                        if sum(r["rehyd"] for r in rec) > 0 else None,
-                          "note": "side-stream pinned-host copies; host wall incl. sync"},
+                          "decode_wait_ms_p50": statistics.median(r["rehyd_wait"] for r in rec),
+                          "ready_before_next_decode": sum(1 for r in rec if r["rehyd_wait"] == 0.0),
+                          "transitions": len(rec),
+                          "note": "side-stream zero-copy reads of the pinned-host stash, issued before allocate + evict (Alg. 2 order) and overlapping them; ms_p50 = CUDA events (rehydrate call on the main stream -> copy done on the side stream); decode_wait = how long the first decode after the transition waits for the copy"},
             "rehydrations_per_transition": statistics.mean(r["nrehyd"] for r in rec),
             "decode_attn_us_p50": attn_ms * 1e3,
             "decode_attn_GBps": attn_gbs,

@@ -223,6 +223,12 @@ arbor_status arbor_evict(arbor_ctx *ctx, const arbor_tree *tree, const int32_t *
  * case Σ ⌈n/P⌉ − #pages of the listed nodes. */
 arbor_status arbor_rehydrate(arbor_ctx *ctx, const arbor_tree *tree, const int32_t *nodes,
                              int32_t count);
+/* The copy runs on side_stream and main_stream does NOT wait for it inside arbor_rehydrate:
+ * the next call that reads or moves pool rows on main_stream (arbor_tree_decode_attn,
+ * arbor_decode_step, arbor_score's attention, arbor_evict) waits first — "before the next
+ * decoding step" — so work enqueued in between (e.g. arbor_allocate) overlaps it.
+ * HOST out: 1 while the last rehydration copy is still running (no sync). */
+arbor_status arbor_rehydrate_in_flight(arbor_ctx *ctx, int32_t *in_flight);
 
 /* a9 — tree decode attention: for each active leaf b, local layer l in
  * [layer_begin, layer_begin+layer_count) and local q head g (KV head h = g / G, Q24):

@@ -98,6 +98,7 @@ def load_library(path: str = LIB_PATH):
         "arbor_read_scores": ([P, I32, P, P, P, P, P], I32),
         "arbor_read_counters": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], I32),
         "arbor_mass_buffer": ([P, C.POINTER(C.c_void_p), C.POINTER(C.c_int32)], I32),
+        "arbor_rehydrate_in_flight": ([P, C.POINTER(C.c_int32)], I32),
         "arbor_score_finish": ([P, P, P], I32),
         "arbor_save_state": ([P, I32], I32),
         "arbor_load_state": ([P, I32], I32),
@@ -398,6 +399,12 @@ class ArborKV:
                                                mclose.ctypes.data, nq.ctypes.data, a.ctypes.data,
                                                s.ctypes.data), "arbor_read_scores")
         return dict(mass=mass, mclose=mclose, nq=nq, a=a, s=s)
+
+    def arbor_rehydrate_in_flight(self) -> bool:
+        """True while the last rehydration copy (side stream) is still running (no sync)."""
+        v = C.c_int32(0)
+        self._check(self.lib.arbor_rehydrate_in_flight(self._ctx, C.byref(v)), "arbor_rehydrate_in_flight")
+        return bool(v.value)
 
     def arbor_mass_buffer(self):
         """a10's buffer: (device pointer, count) of this rank's int64 partial masses

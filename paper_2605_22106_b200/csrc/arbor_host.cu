@@ -450,9 +450,12 @@ arbor_status ensure_partials(arbor_ctx *c, size_t pairs, int layer_count) {
   return ARBOR_OK;
 }
 
+void wait_rehydrated(arbor_ctx *c);
+
 arbor_status run_attention(arbor_ctx *c, const HostPlan &hp, const PlanView &pv, int layer_begin,
                            int layer_count, const void *q, void *out, float *lse) {
   TRY(ensure_partials(c, hp.pair_b.size(), layer_count));
+  wait_rehydrated(c);
   const bool merged = launch_attn_partial(c, pv, q, layer_begin, layer_count, hp.max_cnt, out, lse);
   CK_LAUNCH();
   if (!merged) {
@@ -465,6 +468,25 @@ arbor_status run_attention(arbor_ctx *c, const HostPlan &hp, const PlanView &pv,
 void wait_side(arbor_ctx *c) {
   if (c->side_pending) {
     cudaStreamWaitEvent(c->ms, c->ev_side_done, 0);
+  }
+  c->rehyd_pending = false;   // ev_side_done follows every side-stream copy
+  c->stash_pending = false;
+}
+
+// pending write-through stash copies read the pages of their (closed) nodes
+void wait_stash(arbor_ctx *c) {
+  if (c->stash_pending) {
+    cudaStreamWaitEvent(c->ms, c->ev_stash_done, 0);
+    c->stash_pending = false;
+  }
+}
+
+// before a launch that reads pool rows restored by a pending rehydration (the attention)
+void wait_rehydrated(arbor_ctx *c) {
+  if (c->rehyd_pending) {
+    cudaStreamWaitEvent(c->ms, c->ev_rehyd_done, 0);
+    c->rehyd_pending = false;
+    c->rehyd_list.clear();
   }
 }
 
@@ -701,7 +723,9 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
     cudaEventRecord(c->ring_ev[i], c->ms);
   }
   if (cudaEventCreateWithFlags(&c->ev_main_to_side, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_side_done, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&c->ev_side_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_rehyd_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_stash_done, cudaEventDisableTiming) != cudaSuccess)
     return bail(ARBOR_ERR_CUDA);
   if (k.flags & ARBOR_FLAG_PROFILE) {
     for (int i = 0; i < ARBOR_NUM_STAGES; ++i)
@@ -762,6 +786,8 @@ void arbor_destroy(arbor_ctx *c) {
   }
   if (c->ev_main_to_side) cudaEventDestroy(c->ev_main_to_side);
   if (c->ev_side_done) cudaEventDestroy(c->ev_side_done);
+  if (c->ev_rehyd_done) cudaEventDestroy(c->ev_rehyd_done);
+  if (c->ev_stash_done) cudaEventDestroy(c->ev_stash_done);
   if (c->st_created)
     for (int i = 0; i < ARBOR_NUM_STAGES; ++i)
       for (int r = 0; r < kStageRing; ++r)
@@ -838,6 +864,8 @@ arbor_status arbor_close_node(arbor_ctx *c, int32_t node) {
   launch_stash(c, node, c->h_n[node], c->h_span[node]);
   CK_LAUNCH();
   CK(cudaEventRecord(c->ev_side_done, c->ss));
+  CK(cudaEventRecord(c->ev_stash_done, c->ss));
+  c->stash_pending = true;
   c->side_pending = true;
   c->h_open[node] = 0;
   c->h_nq[node] = 0;
@@ -971,6 +999,7 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
   TRY(upload_plan(c, hp, nA, true, &mass_nodes, pv, &d_mass_nodes, tree));
   TRY(ensure_partials(c, hp.pair_b.size(), c->L));
   mark();
+  wait_rehydrated(c);
   launch_attn_partial(c, pv, q, 0, c->L, hp.max_cnt, out, lse_out);
   CK_LAUNCH();
   mark();
@@ -1043,7 +1072,14 @@ arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_
   int max_n = 0;
   for (int i = 0; i < tree->num_nodes; ++i)
     if (!pin[i]) max_n = std::max(max_n, c->h_n[i]);
-  wait_side(c);   // pending stash copies read pages this call may free
+  // pending stash copies read pages this call may free; a pending rehydration copy writes
+  // the pages of its nodes — only a wait if one of them is not pinned here (the usual
+  // Transition, Alg. 2, rehydrates Path* and then evicts off-path nodes: they overlap)
+  wait_stash(c);
+  if (c->rehyd_pending) {
+    for (int x : c->rehyd_list)
+      if (x >= tree->num_nodes || !pin[x]) { wait_rehydrated(c); break; }
+  }
   ++c->epoch;
   if (c->geom_version != c->tree_version) {   // pinned set of this tree not on the device yet
     launch_geometry(c, tree->num_nodes, tree->num_active);
@@ -1078,7 +1114,8 @@ arbor_status arbor_rehydrate(arbor_ctx *c, const arbor_tree *tree, const int32_t
   for (int x : list) max_n = std::max(max_n, c->h_n[x]);
   TRY(upload_tree(c, tree));
   TRY(ring_upload(c, c->d.rehyd_nodes, list.data(), list.size() * sizeof(int32_t)));
-  wait_side(c);
+  // no main-stream wait: the copy follows any pending stash on the side stream (in order),
+  // and the plan only pops free pages
   ++c->epoch;
   stage_begin(c, ARBOR_ST_REHYDRATE, c->ms);
   launch_rehydrate_plan(c, static_cast<int>(list.size()));
@@ -1088,9 +1125,15 @@ arbor_status arbor_rehydrate(arbor_ctx *c, const arbor_tree *tree, const int32_t
   launch_rehydrate_copy(c, static_cast<int>(list.size()), max_n);
   CK_LAUNCH();
   CK(cudaEventRecord(c->ev_side_done, c->ss));
+  CK(cudaEventRecord(c->ev_rehyd_done, c->ss));
   c->side_pending = true;
-  CK(cudaStreamWaitEvent(c->ms, c->ev_side_done, 0));   // ready before the next decode
-  stage_end(c, ARBOR_ST_REHYDRATE, c->ms);
+  // no wait here: the next attention launch waits for ev_rehyd_done ("before the next
+  // decoding step"), and arbor_evict for the whole side stream, so host work and
+  // allocation between the two overlap the PCIe copy
+  if (!c->rehyd_pending) c->rehyd_list.clear();
+  c->rehyd_list.insert(c->rehyd_list.end(), list.begin(), list.end());
+  c->rehyd_pending = true;
+  stage_end(c, ARBOR_ST_REHYDRATE, c->ss);
   return ARBOR_OK;
 }
 
@@ -1229,6 +1272,14 @@ arbor_status arbor_read_scores(arbor_ctx *c, int32_t num_nodes, int64_t *mass, i
   if (nq) for (int i = 0; i < N; ++i) nq[i] = c->h_nq[i];
   if (a && N) CK(cudaMemcpy(a, c->d.a, N * 4, cudaMemcpyDeviceToHost));
   if (s && N) CK(cudaMemcpy(s, c->d.s, N * 4, cudaMemcpyDeviceToHost));
+  return ARBOR_OK;
+}
+
+arbor_status arbor_rehydrate_in_flight(arbor_ctx *c, int32_t *in_flight) {
+  if (!c || !in_flight) return ARBOR_ERR_INVALID_ARG;
+  const cudaError_t e = cudaEventQuery(c->ev_rehyd_done);
+  if (e != cudaSuccess && e != cudaErrorNotReady) CK(e);
+  *in_flight = e == cudaErrorNotReady ? 1 : 0;
   return ARBOR_OK;
 }
 

@@ -162,6 +162,11 @@ struct arbor_ctx {
   void *stash_dev = nullptr;    // device-visible pointer to the same memory
   bool own_stash = false;
   cudaEvent_t ev_main_to_side = nullptr, ev_side_done = nullptr;
+  // lazy rehydration ("before the next decoding step"): the main stream waits for the
+  // side-stream copy only when a call next reads or moves pool rows (attention, evict)
+  cudaEvent_t ev_rehyd_done = nullptr, ev_stash_done = nullptr;
+  bool rehyd_pending = false, stash_pending = false;
+  std::vector<int32_t> rehyd_list;   // nodes of the pending rehydration copy
   bool side_pending = false;
   // attention scratch capacity
   size_t partial_cap = 0, seg_cap = 0, zbuf_cap = 0;

@@ -110,7 +110,7 @@ struct WsLayout {
     jobs = take(size_t(kPairsWs) * kJobSlots * jcap * 8);  // (src row, dst row) job queues
     jcount = take(size_t(kPairsWs) * kJobSlots * 4);
     bars = take(size_t(kPairsWs) * 2 * kJobSlots * 8);
-    iring = take(size_t(kPairsWs) * 4 * 4);                // drawn work items, 4 pipeline slots
+    iring = take(size_t(kPairsWs) * 4 * 4 * 2);            // drawn work items + their work entries
     swl = take(size_t(wl_n) * sizeof(WorkEnt));            // this CTA's work list (small trees)
     total = o;
   }
@@ -318,14 +318,15 @@ select_move_ws_kernel(CompactArgs a) {
   // The draw for step k + 4 is issued at the top of step k and stored at its end (its latency
   // hides behind the ranking).
   int *iring = reinterpret_cast<int *>(sm + Ly.iring) + pid * 4;
+  int *wring = iring + 4 * kPairsWs;     // work entry of each slot's item (item / R, once)
   auto item_of = [&](int k) { return iring[k & 3]; };
   const WorkEnt *swl = reinterpret_cast<const WorkEnt *>(sm + Ly.swl);
   // work entry of pipeline step k: the shared-memory work list, or the cp.async'ed copy
   auto meta = [&](int k) -> const WorkEnt & {
-    return Ly.wl_n ? swl[item_of(k) / a.R] : Mbuf[k & 3];
+    return Ly.wl_n ? swl[wring[k & 3]] : Mbuf[k & 3];
   };
-  auto row_base = [&](int it) -> int64_t {
-    const int r = it % a.R;
+  auto row_base = [&](int it, int w) -> int64_t {
+    const int r = it - w * a.R;
     const int l = r / a.H, h = r - l * a.H;
     return (static_cast<int64_t>(l) * a.NP * a.H + h) << lgP;
   };
@@ -333,7 +334,7 @@ select_move_ws_kernel(CompactArgs a) {
   auto issue_meta = [&](int k) {
     const int it = item_of(k);
     if (Ly.wl_n || it >= items || lane >= 2) return;
-    const int w = it / a.R;
+    const int w = wring[k & 3];
     cp_async16ca(reinterpret_cast<char *>(&Mbuf[k & 3]) + lane * 16,
                  reinterpret_cast<const char *>(&wl[w]) + lane * 16);
   };
@@ -354,7 +355,7 @@ select_move_ws_kernel(CompactArgs a) {
     const WorkEnt &e = meta(k);
     if (e.kc == e.n) return;
     const int32_t *g = Gbuf + (k % 3) * pcap;
-    const int64_t base = row_base(it);
+    const int64_t base = row_base(it, wring[k & 3]);
     int16_t *pb = Pbuf + (k & 1) * capP;
     for (int q = lane; 2 * q < e.kc; q += 32) {     // slot pairs (P even: same page)
       const int s = 2 * q;
@@ -367,7 +368,7 @@ select_move_ws_kernel(CompactArgs a) {
     const WorkEnt &e = meta(k);
     const int tl = min(a.l_tail, e.n);
     if (e.ka > tl && a.select_mode == ARBOR_SELECT_HEAVY) {   // ranked by A: the non-tail span
-      const int r = it % a.R;
+      const int r = it - wring[k & 3] * a.R;
       const float *Arow = a.A + static_cast<int64_t>(r) * a.max_tokens + e.span;
       float *ab = Abuf + (k & 1) * cap;
       for (int p = lane; p < e.n - tl; p += 32) cp_async4(ab + p, Arow + p);
@@ -379,7 +380,10 @@ select_move_ws_kernel(CompactArgs a) {
   const int gw = static_cast<int>(blockIdx.x) * kPairsWs + pid;
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) iring[i] = 4 * gw + i;
+    for (int i = 0; i < 4; ++i) {
+      iring[i] = 4 * gw + i;
+      wring[i] = (4 * gw + i) / a.R;
+    }
   }
   __syncwarp();
   // prologue: work entries 0-2 (smem list: nothing to fetch) → page lists 0, 1 and A of item 0
@@ -419,7 +423,7 @@ select_move_ws_kernel(CompactArgs a) {
     const int32_t *pgs = Gbuf + (k % 3) * pcap;
     const int16_t *pb = Pbuf + (k & 1) * capP;
     const float *ab = Abuf + (k & 1) * cap;
-    const int64_t base = row_base(it);
+    const int64_t base = row_base(it, wring[k & 3]);
     auto row = [&](int slot) -> int64_t {
       return base + static_cast<int64_t>(pgs[slot >> lgP]) * pstride + (slot & Pm);
     };
@@ -553,6 +557,7 @@ select_move_ws_kernel(CompactArgs a) {
     if (lane == 0) {
       mycount[sl] = nm;
       iring[k & 3] = nxt;            // step k + 4 (read after the next step's __syncwarp)
+      wring[k & 3] = nxt / a.R;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&full[sl]);

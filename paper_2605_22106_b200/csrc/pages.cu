@@ -80,24 +80,34 @@ __global__ void append_copy_kernel(PoolArgs g, const int32_t *ptab, const int32_
   }
 }
 
-// Stash: node slots 0..n-1 (pos = identity at close) → host [2][L][H][max_tokens][D]
+// PCIe copies (stash, rehydrate) run on the side stream on a small persistent grid: PCIe
+// bandwidth (~50 GB/s) needs ~100 KB of reads in flight, not the whole GPU, and a full-GPU
+// grid of long-running zero-copy CTAs would starve the main stream's kernels (allocate, evict)
+// that run concurrently with a rehydration (Alg. 2 Transition order).
+constexpr int kCopyCtas = 32;
+
+// Stash: node slots 0..n-1 (pos = identity at close) → host [2][L][H][max_tokens][D];
+// work unit = (row r, token chunk of 64), grid-stride
 __global__ void stash_kernel(PoolArgs g, const int32_t *ptab, int node, int n, int64_t span,
                              const char *kpool, const char *vpool, char *stash) {
-  const int r = blockIdx.y;
-  const int l = r / g.H, h = r - l * g.H;
   const int rb = g.D * g.esize, cpr = rb / 16;
+  const int lgP = 31 - __clz(g.P);
   const int32_t *pl = ptab + static_cast<int64_t>(node) * g.MPN;
-  const int t0 = blockIdx.x * 64;
-  const int nt = min(64, n - t0);
+  const int nch = (n + 63) / 64;
   const int64_t plane = static_cast<int64_t>(g.L) * g.H * g.max_tokens * rb;
-  for (int idx = threadIdx.x; idx < nt * cpr; idx += blockDim.x) {
-    const int tt = idx / cpr, cc = idx - tt * cpr;
-    const int slot = t0 + tt;
-    const int64_t row = prow(g, l, pl[slot / g.P], h, slot % g.P);
-    const int64_t dst = ((static_cast<int64_t>(r)) * g.max_tokens + span + slot) * rb + cc * 16;
-    *reinterpret_cast<uint4 *>(stash + dst) = *reinterpret_cast<const uint4 *>(kpool + row * rb + cc * 16);
-    *reinterpret_cast<uint4 *>(stash + plane + dst) =
-        *reinterpret_cast<const uint4 *>(vpool + row * rb + cc * 16);
+  for (int u = blockIdx.x; u < nch * g.L * g.H; u += gridDim.x) {
+    const int r = u / nch, t0 = (u - r * nch) * 64;
+    const int l = r / g.H, h = r - l * g.H;
+    const int nt = min(64, n - t0);
+    for (int idx = threadIdx.x; idx < nt * cpr; idx += blockDim.x) {
+      const int tt = idx / cpr, cc = idx - tt * cpr;
+      const int slot = t0 + tt;
+      const int64_t row = prow(g, l, pl[slot >> lgP], h, slot & (g.P - 1));
+      const int64_t dst = ((static_cast<int64_t>(r)) * g.max_tokens + span + slot) * rb + cc * 16;
+      *reinterpret_cast<uint4 *>(stash + dst) = *reinterpret_cast<const uint4 *>(kpool + row * rb + cc * 16);
+      *reinterpret_cast<uint4 *>(stash + plane + dst) =
+          *reinterpret_cast<const uint4 *>(vpool + row * rb + cc * 16);
+    }
   }
 }
 
@@ -119,32 +129,37 @@ __global__ void rehydrate_plan_kernel(Ctrl *ctrl, int32_t *free_stack, int32_t *
   ctrl->rehyd_count = done;
 }
 
-// grid (listed node, token chunk of 64, rows): stash → pages, pos = slot
+// stash → pages, pos = slot; work unit = (listed node i, row r, token chunk of 64), grid-stride
 __global__ void rehydrate_copy_kernel(PoolArgs g, const int32_t *ptab, const int32_t *nodes,
                                       const int32_t *flag, const int32_t *n, const int64_t *span,
-                                      const char *stash, char *kpool, char *vpool, int16_t *pos) {
-  const int i = blockIdx.x;
-  if (!flag[i]) return;
-  const int node = nodes[i];
-  const int nn = n[node];
-  const int t0 = blockIdx.y * 64;
-  if (t0 >= nn) return;
-  const int nt = min(64, nn - t0);
-  const int r = blockIdx.z;
-  const int l = r / g.H, h = r - l * g.H;
+                                      const char *stash, char *kpool, char *vpool, int16_t *pos,
+                                      int count, int nch) {
   const int rb = g.D * g.esize, cpr = rb / 16;
-  const int32_t *pl = ptab + static_cast<int64_t>(node) * g.MPN;
+  const int lgP = 31 - __clz(g.P);
   const int64_t plane = static_cast<int64_t>(g.L) * g.H * g.max_tokens * rb;
-  const int64_t a0 = span[node];
-  for (int idx = threadIdx.x; idx < nt * cpr; idx += blockDim.x) {
-    const int tt = idx / cpr, cc = idx - tt * cpr;
-    const int slot = t0 + tt;
-    const int64_t row = prow(g, l, pl[slot / g.P], h, slot % g.P);
-    const int64_t src = ((static_cast<int64_t>(r)) * g.max_tokens + a0 + slot) * rb + cc * 16;
-    *reinterpret_cast<uint4 *>(kpool + row * rb + cc * 16) = *reinterpret_cast<const uint4 *>(stash + src);
-    *reinterpret_cast<uint4 *>(vpool + row * rb + cc * 16) =
-        *reinterpret_cast<const uint4 *>(stash + plane + src);
-    if (cc == 0) pos[row] = static_cast<int16_t>(slot);
+  const int rows = g.L * g.H;
+  for (int u = blockIdx.x; u < count * rows * nch; u += gridDim.x) {
+    const int i = u / (rows * nch);
+    const int rem = u - i * rows * nch;
+    const int r = rem / nch, t0 = (rem - r * nch) * 64;
+    if (!flag[i]) continue;
+    const int node = nodes[i];
+    const int nn = n[node];
+    if (t0 >= nn) continue;
+    const int nt = min(64, nn - t0);
+    const int l = r / g.H, h = r - l * g.H;
+    const int32_t *pl = ptab + static_cast<int64_t>(node) * g.MPN;
+    const int64_t a0 = span[node];
+    for (int idx = threadIdx.x; idx < nt * cpr; idx += blockDim.x) {
+      const int tt = idx / cpr, cc = idx - tt * cpr;
+      const int slot = t0 + tt;
+      const int64_t row = prow(g, l, pl[slot >> lgP], h, slot & (g.P - 1));
+      const int64_t src = ((static_cast<int64_t>(r)) * g.max_tokens + a0 + slot) * rb + cc * 16;
+      *reinterpret_cast<uint4 *>(kpool + row * rb + cc * 16) = *reinterpret_cast<const uint4 *>(stash + src);
+      *reinterpret_cast<uint4 *>(vpool + row * rb + cc * 16) =
+          *reinterpret_cast<const uint4 *>(stash + plane + src);
+      if (cc == 0) pos[row] = static_cast<int16_t>(slot);
+    }
   }
 }
 
@@ -169,9 +184,8 @@ void launch_append(arbor_ctx *c, int node, const void *k, const void *v, int n_o
 }
 
 void launch_stash(arbor_ctx *c, int node, int n, int64_t span) {
-  dim3 grid((n + 63) / 64, c->L * c->H);
   stage_begin(c, ARBOR_ST_STASH, c->ss);
-  stash_kernel<<<grid, 256, 0, c->ss>>>(pool_args(c), c->d.ptab, node, n, span,
+  stash_kernel<<<kCopyCtas, 256, 0, c->ss>>>(pool_args(c), c->d.ptab, node, n, span,
                                         static_cast<const char *>(c->cfg.k_pool),
                                         static_cast<const char *>(c->cfg.v_pool),
                                         static_cast<char *>(c->stash_dev));
@@ -188,13 +202,12 @@ void launch_rehydrate_plan(arbor_ctx *c, int count) {
 
 void launch_rehydrate_copy(arbor_ctx *c, int count, int max_n) {
   if (count == 0 || max_n == 0) return;
-  dim3 grid(count, (max_n + 63) / 64, c->L * c->H);
-  rehydrate_copy_kernel<<<grid, 256, 0, c->ss>>>(pool_args(c), c->d.ptab, c->d.rehyd_nodes,
-                                                 c->d.rehyd_flag, c->d.n, c->d.span,
-                                                 static_cast<const char *>(c->stash_dev),
-                                                 static_cast<char *>(c->cfg.k_pool),
-                                                 static_cast<char *>(c->cfg.v_pool),
-                                                 c->cfg.pos_pool);
+  rehydrate_copy_kernel<<<kCopyCtas, 256, 0, c->ss>>>(pool_args(c), c->d.ptab, c->d.rehyd_nodes,
+                                                      c->d.rehyd_flag, c->d.n, c->d.span,
+                                                      static_cast<const char *>(c->stash_dev),
+                                                      static_cast<char *>(c->cfg.k_pool),
+                                                      static_cast<char *>(c->cfg.v_pool),
+                                                      c->cfg.pos_pool, count, (max_n + 63) / 64);
   ARBOR_LAUNCHED(c);
 }
 

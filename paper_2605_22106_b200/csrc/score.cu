@@ -220,6 +220,7 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   // issued together (G ≤ 8 logits and LSEs per pair).
   const int warp = tid >> 5, lane = tid & 31;
   constexpr int NW = kFusedThreads / 32;
+  const int lgP = 31 - __clz(a.g.P);
   // Warp w takes chunks w, w + NW, …  Their metadata is loaded 32 chunks at a time, lane i
   // holding chunk w + NW·i (two round trips per batch instead of two per chunk), then
   // broadcast chunk by chunk.
@@ -242,8 +243,8 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
       // both 32-slot halves of the chunk at once (lane: slots lane and lane + 32), so their
       // logit and A loads are in flight together
       const bool v0 = lane < nt, v1 = lane + 32 < nt;
-      auto pos_of = [&](int slot) {
-        return ident ? slot : a.pos[pool_row(a.g, li, pl[slot / a.g.P], h, slot % a.g.P)];
+      auto pos_of = [&](int slot) {   // page size: a power of two (arbor_init)
+        return ident ? slot : a.pos[pool_row(a.g, li, pl[slot >> lgP], h, slot & (a.g.P - 1))];
       };
       float *Ar = a.A + (static_cast<int64_t>(li) * a.g.H + h) * a.g.max_tokens + sp;
       float *dst0 = v0 ? Ar + pos_of(c0 + lane) : nullptr;

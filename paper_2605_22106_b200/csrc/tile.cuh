@@ -49,30 +49,6 @@ __device__ __forceinline__ int64_t pool_row(const PoolView &g, int l, int page, 
   return ((static_cast<int64_t>(l) * g.NP + page) * g.H + h) * g.P + off;
 }
 
-// Stage nt rows (slots c0..c0+nt-1 of `node`) of K (16-byte chunks XOR-swizzled by row&7 so
-// that a thread-per-row read is bank-conflict free) and optionally V (plain) into smem with
-// cp.async.  rowoff[r] receives the pool row index (also the pos-pool index).
-template <typename T, int D, bool kWithV>
-__device__ __forceinline__ void stage_tile(T *Ks, T *Vs, int64_t *rowoff, const T *kpool,
-                                           const T *vpool, const int32_t *ptab_node, int c0,
-                                           int nt, const PoolView &g, int l, int h) {
-  constexpr int CPR = D * static_cast<int>(sizeof(T)) / 16;
-  for (int r = threadIdx.x; r < nt; r += blockDim.x) {
-    const int slot = c0 + r;
-    rowoff[r] = pool_row(g, l, ptab_node[slot / g.P], h, slot % g.P);
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < nt * CPR; idx += blockDim.x) {
-    const int r = idx / CPR, cc = idx - r * CPR;
-    const char *srck = reinterpret_cast<const char *>(kpool + rowoff[r] * D) + cc * 16;
-    cp_async16(reinterpret_cast<char *>(Ks + r * D) + ((cc ^ (r & 7)) * 16), srck);
-    if (kWithV) {
-      const char *srcv = reinterpret_cast<const char *>(vpool + rowoff[r] * D) + cc * 16;
-      cp_async16(reinterpret_cast<char *>(Vs + r * D) + cc * 16, srcv);
-    }
-  }
-  cp_async_commit();
-}
 
 // Dot products of the thread's K row (row t of the swizzled tile) with nq ≤ QB query rows
 // held in smem as f32 [QB][D]; acc[qi] = q_qi · k_t.

@@ -194,8 +194,8 @@ class DptsRun:
     parents; each transition replaces `swap` of them (backtracks into possibly evicted
     subtrees), opens a fresh child under every newly activated leaf (where decoding writes)
     and closes the children of deactivated leaves (Boundary); then
-      allocate (a1+a4, with the last scores) → evict (a5+a6) → rehydrate the new Path* (a7/a8)
-    followed by `decode_steps` decode steps (append one token to every open child; a9; a2/a3).
+      rehydrate the new Path* (a7/a8, side stream) → allocate (a1+a4, with the last scores) →
+    evict (a5+a6), followed by `decode_steps` decode steps (append one token to every open child; a9; a2/a3).
     The budget B = ⌊ρ·T_tot(base tree)⌋ stays fixed while the tree grows."""
 
     def __init__(self, sc: "Scenario", n_active=16, transitions=32, swap=4, decode_steps=8,
@@ -272,13 +272,16 @@ class DptsRun:
         return sorted(out)
 
     def transition(self, leaves):
-        """activate → allocate (last scores; 0.5 for never-scored nodes) → evict → rehydrate."""
+        """Alg. 2 Transition: activate → rehydrate the new Path* (side stream,
+        l.8-14) → allocate (last scores; 0.5 for never-scored nodes) → evict where k drops
+        (l.15-21).  The allocation and eviction overlap the rehydration copy; the next decode
+        waits for it (P:116)."""
         ctx, tree = self.sc.ctx, self.tree
         self.activate(leaves)
+        ctx.arbor_rehydrate(tree, [x for x in self.path_union() if not tree.is_open[x]])
         k = self.k_buf[:tree.num_nodes]
         ctx.arbor_allocate(tree, None, self.budget, k)
         ctx.arbor_evict(tree, k)
-        ctx.arbor_rehydrate(tree, [x for x in self.path_union() if not tree.is_open[x]])
         return k
 
     def decode(self):

@@ -89,8 +89,8 @@ def test_c3_full_size_transitions_sampled_rows():
         Ah = ctx.score.cpu().numpy()
         path = [x for x in run.path_union() if not tree.is_open[x]]
         for (l, h), o in orcs.items():
+            rehyd = o.rehydrate(path)                   # Alg. 2: rehydrate, then evict
             o.evict(tree, k_ref, A_f32=Ah[l:l + 1, h:h + 1])
-            rehyd = o.rehydrate(path)
         rehyd_total += rehyd
         assert ctx.arbor_read_counters()[0] == o0.rehydrations
         free = ctx.arbor_read_free_list()

@@ -322,9 +322,9 @@ def test_c3_dpts_transitions_reduced():
         sc_gpu = pr.ctx.arbor_read_scores(pr.tree.num_nodes)
         st, k_ref, _ = pr.discrete_allocate(sc_gpu["s"], run.budget)
         assert st == 0 and kd.cpu().tolist() == k_ref, f"transition {t}: k differs"
-        pr.orc.evict(pr.tree, k_ref, A_f32=pr.gpu_A())
         path = [x for x in run.path_union() if not pr.tree.is_open[x]]
-        pr.orc.rehydrate(path)
+        pr.orc.rehydrate(path)                          # Alg. 2: rehydrate, then evict
+        pr.orc.evict(pr.tree, k_ref, A_f32=pr.gpu_A())
         pr.check_kv_state()
         assert pr.ctx.arbor_read_counters()[0] == pr.orc.rehydrations
         for _ in range(run.decode_steps):

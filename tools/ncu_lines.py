@@ -1,7 +1,7 @@
 """Aggregate an ncu report's per-SASS warp-stall samples, stall reasons and executed
 instructions by CUDA source line (needs -lineinfo builds and --import-source on).
 
-    python tools/ncu_lines.py report.ncu-rep [top_n]
+    python tools/ncu_lines.py report.ncu-rep [top_n] [kernel_regex]
 """
 import collections
 import csv
@@ -17,7 +17,8 @@ REASONS = ["stall_long_sb", "stall_wait", "stall_no_inst", "stall_short_sb", "st
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass,cuda"],
+    kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+    out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source=sass,cuda"],
                          capture_output=True, text=True).stdout
     samples, insts = collections.Counter(), collections.Counter()
     why = collections.defaultdict(collections.Counter)
