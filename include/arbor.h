@@ -84,6 +84,12 @@ typedef struct {
   int32_t select_mode;  /* arbor_select_mode: intra-block retention rule              */
   int32_t no_rehydrate; /* 1: evicted tokens never come back (P:423-428 ablation):
                          * arbor_rehydrate and Transition's rehydration are no-ops      */
+  int32_t k_protect;    /* invariant (i) "k_i = n_i or a high floor k_protect":
+                         * 0 (default): closed Path* blocks are pinned at k = n (Q19);
+                         * > 0: they are allocated like every other block, with the floor
+                         * raised to min(n, k_protect), and may be evicted down to it; the
+                         * global sinks (first n_sinks positions of the root) are then kept
+                         * by arbor_evict explicitly (Q22).  Open blocks stay pinned.       */
 } arbor_params;
 
 /* Intra-block retention rule of arbor_evict (P:660-675 ablation).  The block tail
@@ -91,9 +97,11 @@ typedef struct {
  * non-tail positions ranked by:
  *  HEAVY      ⟨A, position⟩ descending — heavy hitters (the method);
  *  TAIL       position descending — recency only ("Tail-only");
- *  SINKS_TAIL the block's first n_sinks positions first, then position descending
- *             ("Sinks + Tail"; block-level sinks: the global sinks are the root's, which
- *             is on Path* and never evicted). */
+ *  SINKS_TAIL position descending, with the global sinks first ("Sinks + Tail").
+ * Global sinks 𝒮 = the first n_sinks positions of the root block (the
+ * initial prompt): HEAVY and SINKS_TAIL rank them above every other candidate of the root
+ * (after the tail); TAIL keeps none.  They matter only when the root can be evicted
+ * (params.k_protect > 0): in the default policy the root is on Path* and pinned. */
 typedef enum { ARBOR_SELECT_HEAVY = 0, ARBOR_SELECT_TAIL = 1, ARBOR_SELECT_SINKS_TAIL = 2 } arbor_select_mode;
 
 /* Context configuration.  Host struct; device buffers are caller-owned and

@@ -68,6 +68,9 @@ class ControllerOracle:
         """l.5-21: pin and rehydrate Path*, re-target the off-path blocks (shrink only)."""
         _, _, on_path = self.orc.geometry(tree)
         path = [x for x in range(len(self.orc.n)) if on_path[x] and not self.orc.open[x]]
+        protect = int(self.orc.params.get("k_protect", 0))
+        if protect:   # invariant (i) with the high floor (P:104): only blocks below it
+            path = [x for x in path if self.orc.k_cur(x) < min(self.orc.n[x], protect)]
         self.orc.rehydrate(path)
         k = self._static_targets(tree, s)
         self.orc.evict(tree, k, A_f32=A_f32)

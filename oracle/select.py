@@ -31,19 +31,21 @@ def key(a_f32: float, offset: int):
 HEAVY, TAIL, SINKS_TAIL = 0, 1, 2   # intra-block rules (arbor_select_mode; P:660-675 ablation)
 
 
-def rank_key(mode: int, a_f32: float, t: int, n_sinks: int):
-    """Order of the non-tail candidates, descending: ⟨A, t⟩ for the method's heavy hitters
-    (Q3); t alone for Tail-only; ⟨t is a block sink, t⟩ for Sinks + Tail
-    (block-level sinks: the first n_sinks positions of the block; DESIGN.md f4)."""
+def rank_key(mode: int, a_f32: float, t: int, n_sinks: int, is_root: bool = False):
+    """Order of the non-tail candidates, descending.  Global sinks 𝒮 — the first n_sinks
+    positions of the initial prompt = the root block (Q22) — come first in HEAVY
+    ("plus global sinks 𝒮 shared across all blocks", P:193) and SINKS_TAIL; then ⟨A, t⟩ for
+    the method's heavy hitters (Q3), t alone (recency) for Sinks + Tail and
+    Tail-only (Tail-only keeps no sinks).  The root is on Path* and pinned in the
+    default policy, so sinks only matter when it can be evicted (k_protect > 0)."""
+    sink = 1 if (is_root and t < n_sinks and mode != TAIL) else 0
     if mode == HEAVY:
-        return key(a_f32, t)
-    if mode == TAIL:
-        return (0, int(t))
-    return (1 if t < n_sinks else 0, int(t))
+        return (sink,) + key(a_f32, t)
+    return (sink, 0, int(t))
 
 
 def retained_set(kept, n: int, k_app: int, l_tail: int, A_node_f32, mode: int = HEAVY,
-                 n_sinks: int = 0):
+                 n_sinks: int = 0, is_root: bool = False):
     """Alg. 1 Evict for one (row, node).
 
     kept: within-node offsets currently retained (C, any order);
@@ -61,7 +63,7 @@ def retained_set(kept, n: int, k_app: int, l_tail: int, A_node_f32, mode: int = 
     m = k_app - tl                            # m_i = k_i − |𝒯_i|
     cand = [t for t in kept if t < n - tl]
     ranked = sorted(cand, key=lambda t: rank_key(mode, A_node_f32[t] if mode == HEAVY else 0.0,
-                                                 t, n_sinks), reverse=True)
+                                                 t, n_sinks, is_root), reverse=True)
     heavy = ranked[:m]                        # Top-m_i by A_i(t), or the variant's order
     return sorted(tail + heavy)
 

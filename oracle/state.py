@@ -37,7 +37,7 @@ def default_params(**over) -> dict:
     """SURVEY Appendix B defaults (documented choices; the paper gives none)."""
     p = dict(alpha=1.0, gamma=2.0, lambda_d=0.0, lambda_delta=0.5, eta=0.8, r_min=0.05,
              k_min=4, l_tail=8, n_sinks=4, theta=(-1.0, 2.0, 1.0, 4.0),
-             alloc_mode=tae.MODE_WATERFILL, select_mode=0, no_rehydrate=False)
+             alloc_mode=tae.MODE_WATERFILL, select_mode=0, no_rehydrate=False, k_protect=0)
     p.update(over)
     return p
 
@@ -233,9 +233,10 @@ class ArborOracle:
         if A_f32 is None:
             A_f32 = self.A.astype(np.float32)
         _, _, on_path = self.geometry(tree)
+        protect = self.params.get("k_protect", 0)
         evicted = 0
         for j in range(len(self.n)):
-            if on_path[j] or self.open[j]:
+            if self.open[j] or (on_path[j] and not protect):   # pinned (Q19; P:104 k_protect)
                 continue
             kc = self.k_cur(j)
             k_app = min(kc, max(0, int(k_target[j])))
@@ -249,7 +250,8 @@ class ArborOracle:
                     R = set(select.retained_set(old, n, k_app, self.params["l_tail"],
                                                 A_f32[l, h, a:a + n],
                                                 self.params.get("select_mode", select.HEAVY),
-                                                self.params["n_sinks"]))
+                                                self.params["n_sinks"],
+                                                is_root=int(tree.parent[j]) < 0))
                     holes = [s for s in range(k_app) if old[s] not in R]
                     movers = [old[s] for s in range(k_app, kc) if old[s] in R]
                     assert len(holes) == len(movers)

@@ -178,8 +178,15 @@ def allocate(mode, s, depth, dist, on_path, is_open, n, params, budget):
     Returns (status, k: list[int], min_feasible: int|None)."""
     N = len(n)
     n = [int(x) for x in n]
-    pinned = [bool(on_path[j]) or bool(is_open[j]) for j in range(N)]
+    # invariant (i) (P:104): Path* blocks keep k = n (Q19, default) — or, with k_protect > 0,
+    # a high floor min(n, k_protect) instead; open blocks are always pinned
+    protect = int(params.get("k_protect", 0))
+    pinned = [bool(is_open[j]) or (bool(on_path[j]) and protect == 0) for j in range(N)]
     k_min, l_tail, r_min = params["k_min"], params["l_tail"], params["r_min"]
+
+    def pfloor(j, base):
+        """Floor of node j: base, raised to min(n, k_protect) on Path* when protected."""
+        return max(base, min(n[j], protect)) if (protect and on_path[j]) else base
     size = 2 * N + 2
     E_d = exp_table(params["lambda_d"], size)
     E_D = exp_table(params["lambda_delta"], size)
@@ -197,24 +204,26 @@ def allocate(mode, s, depth, dist, on_path, is_open, n, params, budget):
         # Eq. 2: r = clip(α η^{𝟙} s^γ e^{−λ_d d} e^{−λ_Δ Δ}, r_min, 1); Eq. 3 for k
         for j in free:
             r = min(1.0, max(r_min, params["alpha"] * w_of(j)))
-            k[j] = keep_count(r, n[j], k_min, l_tail)
+            k[j] = pfloor(j, keep_count(r, n[j], k_min, l_tail))
         if mode == MODE_STATIC:
             return STATUS_OK, k, None
-        # Alg. 2 Pressure drain: Priority = W_j (Q16), floor K_min
-        floor_total = pinned_total + sum(min(n[j], k_min) for j in free)
+        # Alg. 2 Pressure drain: Priority = W_j (Q16), floor K_min (protected
+        # Path* blocks: their high floor)
+        df = {j: pfloor(j, min(n[j], k_min)) for j in free}
+        floor_total = pinned_total + sum(df.values())
         if floor_total > budget:
             return STATUS_INFEASIBLE, None, floor_total
         W = {j: quantize_weight(w_of(j)) for j in free}
         while sum(k) > budget:
-            cand = [j for j in free if k[j] > k_min]
+            cand = [j for j in free if k[j] > df[j]]
             j = min(cand, key=lambda x: (W[x], -x))
-            k[j] = max(k_min, k[j] - 1)
+            k[j] = max(df[j], k[j] - 1)
         return STATUS_OK, k, None
 
     # ---- WATERFILL (optimisation view) ----
     if T <= budget:                                  # step 1: full retention
         return STATUS_OK, list(n), None
-    f = {j: floor_count(n[j], k_min, l_tail, r_min) for j in free}
+    f = {j: pfloor(j, floor_count(n[j], k_min, l_tail, r_min)) for j in free}
     Bp = budget - pinned_total                       # step 4
     if Bp < sum(f.values()):
         return STATUS_INFEASIBLE, None, pinned_total + sum(f.values())

@@ -32,6 +32,7 @@ struct AllocArgs {
   int mode;
   double alpha, gamma, eta, r_min;
   int k_min, l_tail, gamma_int;   // gamma_int ≥ 0: integer exponent (repeated products)
+  int k_protect;                  // 0 → Path* pinned at n; > 0 → Path* floor min(n, k_protect)
   const float *s;
   const int32_t *n;
   const int32_t *parent, *active;
@@ -180,7 +181,7 @@ allocate_kernel(AllocArgs a) {
     a.depth[i] = dep[i];
     a.delta[i] = dlt[i];
     a.onpath[i] = onp[i];
-    a.pinned[i] = (onp[i] || a.open[i]) ? 1 : 0;
+    a.pinned[i] = ((onp[i] && a.k_protect == 0) || a.open[i]) ? 1 : 0;
   }
   __syncthreads();
 
@@ -188,7 +189,9 @@ allocate_kernel(AllocArgs a) {
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
     const int nj = a.n[j];
     nn[j] = nj;
-    const bool pin = onp[j] || a.open[j];
+    const bool pin = (onp[j] && a.k_protect == 0) || a.open[j];
+    // protected Path* block: allocated like the others above min(n, k_protect)
+    const int pf = (onp[j] && a.k_protect > 0) ? min(nj, a.k_protect) : 0;
     // w = s^γ · E_d[d] · E_Δ[Δ] · (η if off-path), strictly left to right
     const double s = static_cast<double>(a.s[j]);
     double w;
@@ -207,14 +210,14 @@ allocate_kernel(AllocArgs a) {
     }
     W[j] = __double2ll_rn(__dmul_rn(w, kWeightScale));   // round-half-even(w·2^24)
     const int tl = min(a.l_tail, nj);
-    f[j] = min(nj, max(max(a.k_min, tl), eps_floor_count(a.r_min, nj)));
+    f[j] = max(pf, min(nj, max(max(a.k_min, tl), eps_floor_count(a.r_min, nj))));
     if (pin) {
       k[j] = nj;
       cls[j] = 0;   // pinned
     } else if (a.mode != 0) {
       // Eq. 2-3 (STATIC): r = clip(α·w, r_min, 1)
       const double r = fmin(1.0, fmax(a.r_min, __dmul_rn(a.alpha, w)));
-      k[j] = keep_count(r, nj, a.k_min, a.l_tail);
+      k[j] = max(pf, keep_count(r, nj, a.k_min, a.l_tail));
       cls[j] = 1;
     } else {
       k[j] = nj;
@@ -231,6 +234,11 @@ allocate_kernel(AllocArgs a) {
     for (int j = threadIdx.x; j < N; j += blockDim.x) tot += k[j];
     tot = block_sum(tot, red64);
     long long excess = tot - a.budget;
+    // drain floor of node j: K_min (Alg. 2), raised to min(n, k_protect) on a
+    // protected Path* block
+    auto dfl = [&](int j) {
+      return (onp[j] && a.k_protect > 0) ? max(a.k_min, min(nn[j], a.k_protect)) : a.k_min;
+    };
     if (excess > 0) {
       // rank of each drainable node in priority order (stored in f[], floors are unused in
       // this mode); capacity k_j − K_min into rem[rank]
@@ -238,10 +246,10 @@ allocate_kernel(AllocArgs a) {
       __syncthreads();
       for (int j = threadIdx.x; j < N; j += blockDim.x) {
         int rank = -1;
-        if (cls[j] == 1 && k[j] > a.k_min) {
+        if (cls[j] == 1 && k[j] > dfl(j)) {
           rank = 0;
           for (int i = 0; i < N; ++i) {
-            if (cls[i] == 1 && k[i] > a.k_min &&
+            if (cls[i] == 1 && k[i] > dfl(i) &&
                 (W[i] < W[j] || (W[i] == W[j] && i > j)))
               ++rank;
           }
@@ -250,7 +258,7 @@ allocate_kernel(AllocArgs a) {
       }
       __syncthreads();
       for (int j = threadIdx.x; j < N; j += blockDim.x)
-        if (f[j] >= 0) rem[f[j]] = k[j] - a.k_min;
+        if (f[j] >= 0) rem[f[j]] = k[j] - dfl(j);
       __syncthreads();
       if (threadIdx.x == 0) {   // exclusive prefix over ranks (N ≤ 4096, serial is fine)
         long long acc = 0;
@@ -264,7 +272,7 @@ allocate_kernel(AllocArgs a) {
       for (int j = threadIdx.x; j < N; j += blockDim.x) {
         if (f[j] >= 0) {
           const long long before = rem[f[j]];
-          const long long cap = k[j] - a.k_min;
+          const long long cap = k[j] - dfl(j);
           long long dr = excess - before;
           dr = dr < 0 ? 0 : (dr > cap ? cap : dr);
           k[j] -= static_cast<int>(dr);
@@ -529,6 +537,7 @@ void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget
   a.r_min = c->prm.r_min;
   a.k_min = c->prm.k_min;
   a.l_tail = c->prm.l_tail;
+  a.k_protect = c->prm.k_protect;
   const double g = c->prm.gamma;
   a.gamma_int = (g >= 0.0 && g <= 64.0 && g == static_cast<double>(static_cast<int>(g)))
                     ? static_cast<int>(g) : -1;

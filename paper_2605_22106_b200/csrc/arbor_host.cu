@@ -111,6 +111,7 @@ arbor_status validate_params(const arbor_params *p, std::string &msg) {
   for (double t : p->theta) if (!fin(t)) { msg = "theta must be finite"; return ARBOR_ERR_INVALID_ARG; }
   if (p->select_mode < 0 || p->select_mode > 2) { msg = "bad select_mode"; return ARBOR_ERR_INVALID_ARG; }
   if (p->no_rehydrate != 0 && p->no_rehydrate != 1) { msg = "no_rehydrate must be 0 or 1"; return ARBOR_ERR_INVALID_ARG; }
+  if (p->k_protect < 0) { msg = "k_protect must be >= 0"; return ARBOR_ERR_INVALID_ARG; }
   return ARBOR_OK;
 }
 
@@ -152,10 +153,17 @@ arbor_status validate_tree_impl(const arbor_tree *t, int n_sinks, std::string &m
   return ARBOR_OK;
 }
 
-std::vector<uint8_t> host_pinned(const arbor_tree *t) {
-  std::vector<uint8_t> pin(t->num_nodes, 0);
+// Path* (union of the active root paths, Q14)
+std::vector<uint8_t> host_path_star(const arbor_tree *t) {
+  std::vector<uint8_t> on(t->num_nodes, 0);
   for (int b = 0; b < t->num_active; ++b)
-    for (int x = t->active[b]; x >= 0; x = t->parent[x]) pin[x] = 1;
+    for (int x = t->active[b]; x >= 0; x = t->parent[x]) on[x] = 1;
+  return on;
+}
+
+// pinned (k = n, never evicted): open blocks, and Path* unless params.k_protect > 0
+std::vector<uint8_t> host_pinned(const arbor_tree *t, int k_protect) {
+  std::vector<uint8_t> pin = k_protect > 0 ? std::vector<uint8_t>(t->num_nodes, 0) : host_path_star(t);
   for (int i = 0; i < t->num_nodes; ++i) if (t->is_open[i]) pin[i] = 1;
   return pin;
 }
@@ -168,13 +176,17 @@ int64_t floor_count_host(int n, const arbor_params *p) {
 
 int64_t min_feasible(const arbor_params *p, const arbor_tree *t) {
   if (p->alloc_mode == ARBOR_ALLOC_STATIC) return 0;
-  const auto pin = host_pinned(t);
+  const auto pin = host_pinned(t, p->k_protect);
+  const auto on = host_path_star(t);
   int64_t tot = 0;
   for (int i = 0; i < t->num_nodes; ++i) {
     const int n = t->span_len[i];
-    if (pin[i]) tot += n;
-    else if (p->alloc_mode == ARBOR_ALLOC_WATERFILL) tot += floor_count_host(n, p);
-    else tot += std::min(n, p->k_min);
+    int64_t f;
+    if (pin[i]) f = n;
+    else if (p->alloc_mode == ARBOR_ALLOC_WATERFILL) f = floor_count_host(n, p);
+    else f = std::min(n, p->k_min);
+    if (!pin[i] && on[i] && p->k_protect > 0) f = std::max<int64_t>(f, std::min(n, p->k_protect));
+    tot += f;
   }
   return tot;
 }
@@ -1068,7 +1080,7 @@ arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_
   TRY(check_tree(c, tree));
   if (!k_target) return fail(c, ARBOR_ERR_INVALID_ARG, "k_target is NULL");
   TRY(upload_tree(c, tree));
-  const auto pin = host_pinned(tree);
+  const auto pin = host_pinned(tree, c->prm.k_protect);
   int max_n = 0;
   for (int i = 0; i < tree->num_nodes; ++i)
     if (!pin[i]) max_n = std::max(max_n, c->h_n[i]);
@@ -1098,7 +1110,15 @@ arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_
   return ARBOR_OK;
 }
 
+static arbor_status rehydrate_impl(arbor_ctx *c, const arbor_tree *tree, const int32_t *nodes,
+                                   int32_t count, int keep_floor);
+
 arbor_status arbor_rehydrate(arbor_ctx *c, const arbor_tree *tree, const int32_t *nodes, int32_t count) {
+  return rehydrate_impl(c, tree, nodes, count, 0);
+}
+
+static arbor_status rehydrate_impl(arbor_ctx *c, const arbor_tree *tree, const int32_t *nodes,
+                                   int32_t count, int keep_floor) {
   if (!c) return ARBOR_ERR_INVALID_ARG;
   TRY(check_tree(c, tree));
   if (count < 0 || (count > 0 && !nodes)) return fail(c, ARBOR_ERR_INVALID_ARG, "bad node list");
@@ -1118,7 +1138,7 @@ arbor_status arbor_rehydrate(arbor_ctx *c, const arbor_tree *tree, const int32_t
   // and the plan only pops free pages
   ++c->epoch;
   stage_begin(c, ARBOR_ST_REHYDRATE, c->ms);
-  launch_rehydrate_plan(c, static_cast<int>(list.size()));
+  launch_rehydrate_plan(c, static_cast<int>(list.size()), keep_floor);
   CK_LAUNCH();
   CK(cudaEventRecord(c->ev_main_to_side, c->ms));
   CK(cudaStreamWaitEvent(c->ss, c->ev_main_to_side, 0));
@@ -1161,7 +1181,8 @@ arbor_status arbor_policy_event(arbor_ctx *c, const arbor_tree *tree, int32_t ki
         for (int x = tree->active[b]; x >= 0 && !on[x]; x = tree->parent[x]) on[x] = 1;
       for (int x = 0; x < tree->num_nodes; ++x)
         if (on[x] && !tree->is_open[x]) path.push_back(x);
-      TRY(arbor_rehydrate(c, tree, path.data(), static_cast<int32_t>(path.size())));
+      // Alg. 2 l.8-14; under k_protect only blocks below their floor min(n, k_protect)
+      TRY(rehydrate_impl(c, tree, path.data(), static_cast<int32_t>(path.size()), c->prm.k_protect));
       TRY(allocate_impl(c, tree, nullptr, budget, k_out, min_feasible_out, ARBOR_ALLOC_STATIC, -1));
       return arbor_evict(c, tree, k_out, nullptr);
     }

@@ -242,7 +242,7 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n);
 // pages.cu
 void launch_append(arbor_ctx *c, int node, const void *k, const void *v, int n_old, int ntok);
 void launch_stash(arbor_ctx *c, int node, int n, int64_t span);
-void launch_rehydrate_plan(arbor_ctx *c, int count);
+void launch_rehydrate_plan(arbor_ctx *c, int count, int keep_floor);
 void launch_rehydrate_copy(arbor_ctx *c, int count, int max_n);
 
 // attn.cu

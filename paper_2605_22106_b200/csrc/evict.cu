@@ -59,7 +59,7 @@ struct CompactArgs {
   int lgP;          // log2(page size)
   int exp;          // ARBOR_EVICT_EXP (measurement only): bit0 skip moves, bit1 skip radix select
   int select_mode;  // arbor_select_mode (f4)
-  int n_sinks;      // block-level sinks of ARBOR_SELECT_SINKS_TAIL
+  int n_sinks;      // global sinks: the root's first n_sinks positions (HEAVY, SINKS_TAIL)
   long long *trace; // ARBOR_EVICT_TRACE=1 (diagnostics): [cta][warp][4] globaltimer ns
   int wl_smem;      // N when the work list also lives in shared memory (N ≤ kSmemWorkNodes), else 0
 };
@@ -439,14 +439,19 @@ select_move_ws_kernel(CompactArgs a) {
         const int p = ident ? s : pb[s];
         kk = static_cast<unsigned>(p);
         if (ranked && p < tail_from) {
-          // the key's high part: f32 bits of A (HEAVY), 0 (TAIL: recency), sink flag
-          unsigned bits = p < a.n_sinks ? 1u : 0u;
+          // the key's high part: f32 bits of A (HEAVY), 0 (recency: TAIL, SINKS_TAIL); the
+          // global sinks — the root's first n_sinks positions — rank above
+          // everything else in HEAVY (all-ones: above any finite A) and SINKS_TAIL
+          const bool sink = e.node == 0 && p < a.n_sinks && a.select_mode != ARBOR_SELECT_TAIL;
+          unsigned bits = sink ? 1u : 0u;
           if (a.select_mode == ARBOR_SELECT_HEAVY) {
-            const float av = ab[p];
-            if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-            bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
-          } else if (a.select_mode == ARBOR_SELECT_TAIL) {
-            bits = 0u;
+            if (sink) {
+              bits = 0xffffffffu;
+            } else {
+              const float av = ab[p];
+              if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+              bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
+            }
           }
           kk = kCand | (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
           bmin = min(bmin, bits);

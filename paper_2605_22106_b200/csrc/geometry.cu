@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(1024)
 geometry_kernel(int N, int nA, const int32_t *__restrict__ parent,
                 const int32_t *__restrict__ active, const uint8_t *__restrict__ open,
                 int32_t *__restrict__ depth, int32_t *__restrict__ delta,
-                uint8_t *__restrict__ onpath, uint8_t *__restrict__ pinned) {
+                uint8_t *__restrict__ onpath, uint8_t *__restrict__ pinned, int k_protect) {
   // depth by walking to the root
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
     int d = 0;
@@ -44,7 +44,7 @@ geometry_kernel(int N, int nA, const int32_t *__restrict__ parent,
       best = dist < best ? dist : best;
     }
     delta[i] = best;
-    pinned[i] = (onpath[i] || open[i]) ? 1 : 0;
+    pinned[i] = ((onpath[i] && k_protect == 0) || open[i]) ? 1 : 0;   // P:104, Q19
   }
 }
 
@@ -53,7 +53,8 @@ geometry_kernel(int N, int nA, const int32_t *__restrict__ parent,
 void launch_geometry(arbor_ctx *c, int N, int nA) {
   stage_begin(c, ARBOR_ST_GEOMETRY, c->ms);
   geometry_kernel<<<1, 1024, 0, c->ms>>>(N, nA, c->d.parent, c->d.active, c->d.open,
-                                          c->d.depth, c->d.delta, c->d.onpath, c->d.pinned);
+                                          c->d.depth, c->d.delta, c->d.onpath, c->d.pinned,
+                                          c->prm.k_protect);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_GEOMETRY, c->ms);
 }

@@ -43,7 +43,8 @@ def test_select_mode_two_stage_eviction(mode):
         kc = pr.orc.k_cur(j)
         kept = sorted(int(x) for x in pr.orc.kept[j][0, 0])
         tl = min(6, n[j])
-        sk = min(5, kc - tl) if mode == "sinks_tail" else 0
+        # global sinks live in the root only; elsewhere Sinks + Tail = Tail-only
+        sk = min(5, kc - tl) if (mode == "sinks_tail" and j == 0) else 0
         assert kept == sorted(set(range(sk)) | set(range(n[j] - (kc - sk), n[j])))
     pr.tree.active = [synth.leaves_of(pr.tree)[-1]]
     pr.decode_both()
@@ -62,3 +63,44 @@ def test_no_rehydrate_keeps_evicted_path_partial():
     pr.check_kv_state()
     assert pr.ctx.arbor_read_counters()[0] == 0
     pr.decode_both()       # attention over the partial Path* blocks
+
+
+@pytest.mark.parametrize("mode", ["heavy", "sinks_tail"])
+def test_k_protect_path_floor_and_global_sinks(mode):
+    """Invariant (i) with the high floor (params.k_protect): Path* blocks — the root
+    included — are allocated and evicted down to min(n, k_protect) instead of being pinned;
+    the global sinks (the root's first n_sinks positions) survive every
+    eviction of the root.  Bit-exact against the oracle (allocation on the GPU's s, selection
+    on the GPU's A); then the controller's protected Transition rehydrates only blocks below
+    their floor."""
+    pr = Pair(MID, seed=8, params_over=dict(select_mode=mode, n_sinks=4, l_tail=6, k_protect=20))
+    pr.warmup(steps_per_leaf=1)
+    pr.decode_both()
+    sc = pr.ctx.arbor_read_scores(pr.tree.num_nodes)
+    N = pr.tree.num_nodes
+    n = [int(x) for x in pr.tree.span_len]
+    B = int(0.2 * sum(n))
+    st, k_ref, _ = pr.discrete_allocate(sc["s"], B)
+    assert st == 0 and sum(k_ref) == B
+    k = torch.empty(N, dtype=torch.int32, device="cuda")
+    pr.ctx.arbor_allocate(pr.tree, torch.as_tensor(sc["s"], device="cuda"), B, k)
+    assert k.cpu().tolist() == k_ref
+    d, dist, on = pr.orc.geometry(pr.tree)
+    for j in range(N):
+        if on[j]:
+            assert k_ref[j] >= min(n[j], 20)
+    assert k_ref[0] < n[0], "the root must be evicted for the sinks to matter"
+    _evict_both(pr, k_ref)
+    root = set(int(x) for x in pr.orc.kept[0][0, 0])
+    assert set(range(4)) <= root, "global sinks evicted"
+    pr.decode_both()
+    # a protected Transition: rehydrate only Path* blocks below min(n, k_protect)
+    pr.tree.active = [synth.leaves_of(pr.tree)[-1]]
+    kd = torch.empty(N, dtype=torch.int32, device="cuda")
+    from oracle.controller import ControllerOracle
+    co = ControllerOracle(pr.orc, B, 0)
+    pr.ctx.arbor_policy_event(pr.tree, "transition", -1, B, kd)
+    s_now = pr.ctx.arbor_read_scores(N)["s"]       # the library's last scores (decode above)
+    co.transition(pr.tree, [float(x) for x in s_now], A_f32=pr.gpu_A())
+    pr.check_kv_state()
+    assert pr.ctx.arbor_read_counters()[0] == pr.orc.rehydrations

@@ -509,21 +509,30 @@ def test_state_hole_filling_layout():
 @pytest.mark.parametrize("n,k,l_tail,s", [(40, 13, 4, 3), (17, 9, 2, 4), (64, 20, 8, 0), (12, 5, 5, 2)])
 def test_select_variants_closed_forms(n, k, l_tail, s):
     """Tail-only and Sinks + Tail from full retention reduce to intervals:
-    Tail keeps the last k positions; Sinks+Tail keeps the block's first min(s, m) positions
-    and the most recent k − min(s, m) (m = k − |tail|).  Neither depends on A."""
+    Tail keeps the last k positions; Sinks + Tail keeps the global sinks — the first
+    min(s, m) positions of the ROOT block (the initial prompt; m = k − |tail|) —
+    and the most recent k − min(s, m); in any other block it is Tail-only.  HEAVY keeps the
+    root's sinks before any heavy hitter.  None of the recency rules depends on A."""
     rng = np.random.default_rng(n * 7 + k)
     A = rng.random(n).astype(np.float32)
     full = list(range(n))
     tl = min(l_tail, n)
-    assert select.retained_set(full, n, k, l_tail, A, select.TAIL) == list(range(n - k, n))
+    last = list(range(n - k, n))
+    assert select.retained_set(full, n, k, l_tail, A, select.TAIL) == last
+    assert select.retained_set(full, n, k, l_tail, A, select.TAIL, s, is_root=True) == last
+    assert select.retained_set(full, n, k, l_tail, A, select.SINKS_TAIL, s) == last
     m = max(k - tl, 0)
     sk = min(s, m) if k > tl else 0
     want = sorted(set(range(sk)) | set(range(n - (k - sk), n)))
-    assert select.retained_set(full, n, k, l_tail, A, select.SINKS_TAIL, s) == want
+    assert select.retained_set(full, n, k, l_tail, A, select.SINKS_TAIL, s, is_root=True) == want
+    # HEAVY in the root: the sinks, then the top-(m − sinks) of the rest by A, plus the tail
+    hv = select.retained_set(full, n, k, l_tail, A, select.HEAVY, s, is_root=True)
+    rest = sorted(range(sk, n - tl), key=lambda t: (A[t], t), reverse=True)[:m - sk]
+    assert hv == sorted(set(range(sk)) | set(rest) | set(range(n - tl, n)))
     A2 = rng.permutation(A)
     for mode in (select.TAIL, select.SINKS_TAIL):
-        assert (select.retained_set(full, n, k, l_tail, A, mode, s) ==
-                select.retained_set(full, n, k, l_tail, A2, mode, s))
+        assert (select.retained_set(full, n, k, l_tail, A, mode, s, is_root=True) ==
+                select.retained_set(full, n, k, l_tail, A2, mode, s, is_root=True))
 
 
 def test_select_variants_compose():
@@ -748,3 +757,37 @@ def test_hole_fill_worked_example():
     o.evict(tree2, [g["k_app"], 4], A_f32=A)
     assert sorted(o.kept[0][0, 0].tolist()) == g["retained"]
     assert o.kept[0][0, 0].tolist() == g["new_slots"]
+
+
+def test_k_protect_reduces_to_pinning_and_keeps_floors():
+    """P:104 "k_i = n_i or a high floor k_protect": a floor at least every n is the pinned
+    policy exactly (all modes); a lower floor keeps every Path* block at ≥ min(n, k_protect),
+    still meets the budget exactly (WATERFILL) and reports min_feasible with those floors."""
+    rng = np.random.default_rng(77)
+    for trial in range(200):
+        N = int(rng.integers(2, 25))
+        parent = [-1] + [int(rng.integers(0, i)) for i in range(1, N)]
+        n = [int(x) for x in rng.integers(1, 20, size=N)]
+        kids = set(parent[1:])
+        leaves = [i for i in range(N) if i not in kids]
+        act = sorted(set(int(x) for x in rng.choice(leaves, size=min(2, len(leaves)), replace=False)))
+        d = geometry.depths(parent)
+        dist = geometry.delta(parent, act)
+        on = [i in geometry.path_star(parent, act) for i in range(N)]
+        opn = [False] * N
+        s = [float(np.float32(x)) for x in rng.random(N)]
+        B = int(rng.integers(sum(n) // 4, sum(n)))
+        for mode in (0, 1, 2):
+            base = default_params(k_min=int(rng.integers(0, 4)), l_tail=int(rng.integers(0, 4)))
+            ref = tae.allocate(mode, s, d, dist, on, opn, n, base, B)
+            big = tae.allocate(mode, s, d, dist, on, opn, n, dict(base, k_protect=max(n)), B)
+            assert ref == big, (trial, mode)
+            prot = int(rng.integers(1, 10))
+            st, k, mf = tae.allocate(mode, s, d, dist, on, opn, n, dict(base, k_protect=prot), B)
+            if st != 0:
+                continue
+            for j in range(N):
+                if on[j]:
+                    assert k[j] >= min(n[j], prot)
+            if mode == 0 and sum(n) > B:
+                assert sum(k) == B
