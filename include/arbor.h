@@ -90,6 +90,15 @@ typedef struct {
                          * raised to min(n, k_protect), and may be evicted down to it; the
                          * global sinks (first n_sinks positions of the root) are then kept
                          * by arbor_evict explicitly (Q22).  Open blocks stay pinned.       */
+  /* Thin slice 𝓛 × 𝓗 ("aggregated over a thin slice of heads/layers"): the
+   * last slice_layers layers and the first slice_kv_heads KV heads of the model (global
+   * indices; 0 = all).  a_i then counts the slice rows' mass only, normalised by
+   * |𝓛|·|𝓗_q| (Q4, Q6).                                                                */
+  int32_t slice_layers, slice_kv_heads;
+  /* 1: the paper-literal shared selection (Q1): arbor_evict ranks every block
+   * once, by Â(t) = Σ_{(l,h) ∈ slice} A[l][h][t] (f32 values summed in fp64 in ascending
+   * row order, rounded to f32), and every row keeps the same positions.  world_size 1. */
+  int32_t select_shared;
 } arbor_params;
 
 /* Intra-block retention rule of arbor_evict (P:660-675 ablation).  The block tail

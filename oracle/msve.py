@@ -48,14 +48,35 @@ def row_node_mass(A_row, span_start: int, n: int) -> float:
     return s
 
 
-def node_mass(A, span_start: int, n: int) -> int:
-    """Mass_i = Σ_{rows (l,h)} Q(m_{l,h,i}) (exact integer sum, Q29)."""
+def node_mass(A, span_start: int, n: int, rows=None) -> int:
+    """Mass_i = Σ_{rows (l,h)} Q(m_{l,h,i}) (exact integer sum, Q29); `rows` restricts the
+    sum to a thin slice of (layer, KV head) rows (Q6), default all."""
     total = 0
     L, H = A.shape[0], A.shape[1]
     for l in range(L):
         for h in range(H):
+            if rows is not None and (l, h) not in rows:
+                continue
             total += quantize_mass(row_node_mass(A[l, h], span_start, n))
     return total
+
+
+def slice_rows(L: int, H: int, layer_begin: int, kv_head_begin: int, num_layers: int,
+               slice_layers: int, slice_kv_heads: int):
+    """Local (l, h) rows of the thin slice 𝓛 × 𝓗 ("aggregated over a thin slice of
+    heads/layers"): the last `slice_layers` layers of the model and its first
+    `slice_kv_heads` KV heads (global indices; 0 = all), as SPEC's default reads
+    it.  None when the slice is everything."""
+    if not slice_layers and not slice_kv_heads:
+        return None
+    lo = num_layers - slice_layers if slice_layers else 0
+    out = set()
+    for l in range(L):
+        for h in range(H):
+            gl, gh = layer_begin + l, kv_head_begin + h
+            if gl >= lo and (not slice_kv_heads or gh < slice_kv_heads):
+                out.add((l, h))
+    return out
 
 
 def attention_feature(mass: int, mclose: int, nq: int, num_layers: int,

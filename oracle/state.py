@@ -37,7 +37,8 @@ def default_params(**over) -> dict:
     """SURVEY Appendix B defaults (documented choices; the paper gives none)."""
     p = dict(alpha=1.0, gamma=2.0, lambda_d=0.0, lambda_delta=0.5, eta=0.8, r_min=0.05,
              k_min=4, l_tail=8, n_sinks=4, theta=(-1.0, 2.0, 1.0, 4.0),
-             alloc_mode=tae.MODE_WATERFILL, select_mode=0, no_rehydrate=False, k_protect=0)
+             alloc_mode=tae.MODE_WATERFILL, select_mode=0, no_rehydrate=False, k_protect=0,
+             slice_layers=0, slice_kv_heads=0, select_shared=0)
     p.update(over)
     return p
 
@@ -50,7 +51,8 @@ class ArborOracle:
     num_q_heads_global normalise a_i (Q4)."""
 
     def __init__(self, K_all, V_all, num_q_heads_local: int, page_size: int, num_pages: int,
-                 params: dict, num_layers_global=None, num_q_heads_global=None):
+                 params: dict, num_layers_global=None, num_q_heads_global=None, layer_begin=0,
+                 kv_head_begin=0, num_kv_heads_global=None):
         self.K = np.asarray(K_all, dtype=np.float64)
         self.V = np.asarray(V_all, dtype=np.float64)
         self.L, self.H, self.Tmax, self.d = self.K.shape
@@ -61,6 +63,14 @@ class ArborOracle:
         self.params = dict(params)
         self.Lg = num_layers_global or self.L
         self.Hqg = num_q_heads_global or self.Hq
+        Hg = num_kv_heads_global or (self.Hqg // self.G)
+        # thin slice 𝓛 × 𝓗 for a_i (and the shared selection): local rows, and the a_i
+        # normalisation |𝓛|·|𝓗_q| (global counts, Q4/Q6)
+        sl, sh = int(self.params.get("slice_layers", 0)), int(self.params.get("slice_kv_heads", 0))
+        self.slice = msve.slice_rows(self.L, self.H, layer_begin, kv_head_begin, self.Lg, sl, sh)
+        self.norm_layers = sl or self.Lg
+        self.norm_qheads = (sh * self.G) if sh else self.Hqg
+        del Hg
         self.span_start, self.n, self.open = [], [], []
         self.kept = []            # per node: int64 [L][H][k_cur] offset held by each slot
         self.pages = []           # per node: list of page ids
@@ -107,7 +117,7 @@ class ArborOracle:
                                           (self.L, self.H, new_n)).copy()
 
     def node_mass_partial(self, i: int) -> int:
-        return msve.node_mass(self.A, self.span_start[i], self.n[i])
+        return msve.node_mass(self.A, self.span_start[i], self.n[i], self.slice)
 
     def close_node(self, node: int):
         """Boundary: fix n_i, snapshot Mclose_i (Q5), reset Nq_i."""
@@ -197,7 +207,7 @@ class ArborOracle:
             if self.open[i]:
                 continue
             a[i] = msve.attention_feature(masses[i], self.Mclose[i], self.Nq[i],
-                                          self.Lg, self.Hqg)
+                                          self.norm_layers, self.norm_qheads)
             s[i] = float(np.float32(msve.msve_score(self.params["theta"], float(tree.v[i]),
                                                      float(tree.u[i]), a[i])))
         self.s_last = s
@@ -232,6 +242,17 @@ class ArborOracle:
         (P:171); the slot order is this build's paging choice."""
         if A_f32 is None:
             A_f32 = self.A.astype(np.float32)
+        A_f32 = np.asarray(A_f32, np.float32)
+        if self.params.get("select_shared", 0):
+            # paper-literal shared selection (P:187-189, Q1): one retained set per block, by
+            # Â(t) = Σ_{(l,h) ∈ slice} A[l][h][t] (f32 values summed in fp64, rows ascending,
+            # rounded to f32), applied to every row
+            rows = sorted(self.slice) if self.slice is not None else \
+                [(l, h) for l in range(self.L) for h in range(self.H)]
+            acc = np.zeros(A_f32.shape[-1], np.float64)
+            for (l, h) in rows:
+                acc = acc + A_f32[l, h].astype(np.float64)
+            A_f32 = np.broadcast_to(acc.astype(np.float32), A_f32.shape)
         _, _, on_path = self.geometry(tree)
         protect = self.params.get("k_protect", 0)
         evicted = 0

@@ -42,7 +42,8 @@ class ArborParams(C.Structure):
                 ("k_min", C.c_int32), ("l_tail", C.c_int32), ("n_sinks", C.c_int32),
                 ("alloc_mode", C.c_int32), ("theta", C.c_double * 4),
                 ("select_mode", C.c_int32), ("no_rehydrate", C.c_int32),
-                ("k_protect", C.c_int32)]
+                ("k_protect", C.c_int32), ("slice_layers", C.c_int32),
+                ("slice_kv_heads", C.c_int32), ("select_shared", C.c_int32)]
 
 
 class ArborConfig(C.Structure):
@@ -125,7 +126,7 @@ def load_library(path: str = LIB_PATH):
 def make_params(alpha=1.0, gamma=2.0, lambda_d=0.0, lambda_delta=0.5, eta=0.8, r_min=0.05,
                 k_min=4, l_tail=8, n_sinks=4, theta=(-1.0, 2.0, 1.0, 4.0),
                 alloc_mode="waterfill", select_mode="heavy", no_rehydrate=False,
-                k_protect=0) -> ArborParams:
+                k_protect=0, slice_layers=0, slice_kv_heads=0, select_shared=False) -> ArborParams:
     """Parameter bundle Π (Alg. 1 caption P:498); defaults are DESIGN.md's documented choices."""
     mode = ALLOC_MODES[alloc_mode] if isinstance(alloc_mode, str) else int(alloc_mode)
     sel = SELECT_MODES[select_mode] if isinstance(select_mode, str) else int(select_mode)
@@ -134,6 +135,9 @@ def make_params(alpha=1.0, gamma=2.0, lambda_d=0.0, lambda_delta=0.5, eta=0.8, r
     p.select_mode = sel
     p.no_rehydrate = 1 if no_rehydrate else 0
     p.k_protect = int(k_protect)
+    p.slice_layers = int(slice_layers)
+    p.slice_kv_heads = int(slice_kv_heads)
+    p.select_shared = 1 if select_shared else 0
     for i, t in enumerate(theta):
         p.theta[i] = float(t)
     return p

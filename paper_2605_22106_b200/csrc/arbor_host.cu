@@ -112,6 +112,8 @@ arbor_status validate_params(const arbor_params *p, std::string &msg) {
   if (p->select_mode < 0 || p->select_mode > 2) { msg = "bad select_mode"; return ARBOR_ERR_INVALID_ARG; }
   if (p->no_rehydrate != 0 && p->no_rehydrate != 1) { msg = "no_rehydrate must be 0 or 1"; return ARBOR_ERR_INVALID_ARG; }
   if (p->k_protect < 0) { msg = "k_protect must be >= 0"; return ARBOR_ERR_INVALID_ARG; }
+  if (p->slice_layers < 0 || p->slice_kv_heads < 0) { msg = "slice sizes must be >= 0"; return ARBOR_ERR_INVALID_ARG; }
+  if (p->select_shared != 0 && p->select_shared != 1) { msg = "select_shared must be 0 or 1"; return ARBOR_ERR_INVALID_ARG; }
   return ARBOR_OK;
 }
 
@@ -646,6 +648,9 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   if (k.world_size < 1 || k.rank < 0 || k.rank >= k.world_size) return ARBOR_ERR_INVALID_ARG;
   const bool ext_reduce = (k.flags & ARBOR_FLAG_EXTERNAL_REDUCE) != 0;
   if (k.world_size > 1 && !k.nccl_unique_id && !ext_reduce) return ARBOR_ERR_INVALID_ARG;
+  if (params->slice_layers > k.num_layers || params->slice_kv_heads > k.num_kv_heads)
+    return ARBOR_ERR_INVALID_ARG;
+  if (params->select_shared && k.world_size > 1) return ARBOR_ERR_INVALID_ARG;   // Â is rank-local
 
   arbor_ctx *c = new arbor_ctx();
   c->cfg = k;
@@ -714,6 +719,7 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
     if (rows_total >= (1ll << 31)) { c->err = "pool too large for int32 row ids"; return bail(ARBOR_ERR_INVALID_ARG); }
   }
   ALLOC(d.rehyd_nodes, MN + 1); ALLOC(d.rehyd_flag, MN + 2);
+  if (params->select_shared) ALLOC(d.ahat, static_cast<size_t>(k.max_tokens));
 #undef ALLOC
   init_free_kernel<<<(c->NP + 255) / 256, 256, 0, c->ms>>>(d.free_stack, c->NP, d.ctrl);
   fill_f32<<<(MN + 255) / 256, 256, 0, c->ms>>>(d.s, MN, 0.5f);
@@ -784,7 +790,7 @@ void arbor_destroy(arbor_ctx *c) {
                   d.a, d.s, d.ctrl, d.parent, d.onpath, d.pinned, d.depth, d.delta, d.Ed, d.ED,
                   d.work, d.rehyd_nodes, d.rehyd_flag, d.seg,
                   d.partials, d.lse_scratch, d.out_scratch, d.zbuf, d.mass_part, d.mass_scratch,
-                  d.mass_acc, d.ticket, d.row_done};
+                  d.mass_acc, d.ticket, d.row_done, d.ahat};
   for (void *p : ptrs) if (p) cudaFree(p);
   for (auto &sn : c->snap) {
     if (!sn.valid) continue;
@@ -1097,6 +1103,10 @@ arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_
     launch_geometry(c, tree->num_nodes, tree->num_active);
     CK_LAUNCH();
     c->geom_version = c->tree_version;
+  }
+  if (c->prm.select_shared) {   // one ranking per block on the slice-summed Â
+    launch_ahat(c);
+    CK_LAUNCH();
   }
   launch_evict(c, tree->num_nodes, k_target, max_n);
   CK_LAUNCH();

@@ -69,6 +69,7 @@ struct DevState {
   int64_t *mclose;           // this rank's Mclose partial
   int64_t *nq;               // Nq_i (uploaded)
   float *a, *s;              // last a_i, s_i
+  float *ahat = nullptr;     // select_shared: slice-summed Â[t] (f32, by absolute position)
   Ctrl *ctrl;
   // tree mirror
   int32_t *parent, *len, *active;
@@ -101,6 +102,13 @@ struct DevState {
 // once for all of them.  An attention item is a chunk with a subset of ≤ kLeavesPerItem of
 // its leaves.  bp_list holds, per leaf b, its pairs in root→leaf, chunk-ascending order
 // (the merge order).
+// Thin slice 𝓛 × 𝓗 (arbor_params.slice_layers / slice_kv_heads) in this
+// rank's local (layer, KV head) coordinates: rows l ≥ l_lo with h < h_hi.
+struct SliceView {
+  int l_lo, h_hi;
+  __host__ __device__ bool has(int l, int h) const { return l >= l_lo && h < h_hi; }
+};
+
 struct PlanView {
   const int32_t *ch_node, *ch_chunk, *ch_poff, *ch_pcnt;   // C chunks: (node, chunk) + pairs
   const int4 *it_rec;                                       // I items: {node, c0, pair base, cnt}
@@ -216,6 +224,18 @@ void launch_geometry(arbor_ctx *c, int N, int nA);
 void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64_t *out,
                       int out_stride);
 void launch_msve(arbor_ctx *c, int N, float *s_out);
+// the thin slice in local coordinates, and the a_i normalisation |𝓛|·|𝓗_q| (Q4, Q6)
+inline SliceView slice_view(const arbor_ctx *c) {
+  const int lo_g = c->prm.slice_layers ? c->Lg - c->prm.slice_layers : 0;
+  const int hi_g = c->prm.slice_kv_heads ? c->prm.slice_kv_heads : c->Hg;
+  return SliceView{lo_g - c->cfg.layer_begin, hi_g - c->cfg.kv_head_begin};
+}
+inline double msve_norm(const arbor_ctx *c) {
+  const double nl = c->prm.slice_layers ? c->prm.slice_layers : c->Lg;
+  const double nh = c->prm.slice_kv_heads ? static_cast<double>(c->prm.slice_kv_heads) * c->G
+                                          : static_cast<double>(c->Hqg);
+  return nl * nh;
+}
 // nparts (a power of two) CTAs per (layer, KV head) row; CTA (row, p) owns the nodes with
 // id & (nparts − 1) == p
 void launch_score_fused(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
@@ -238,6 +258,8 @@ void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget
 
 // evict.cu
 void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n);
+// select_shared: Â[t] = Σ_{slice rows, ascending} A[l][h][t] in fp64, rounded to f32
+void launch_ahat(arbor_ctx *c);
 
 // pages.cu
 void launch_append(arbor_ctx *c, int node, const void *k, const void *v, int n_old, int ntok);

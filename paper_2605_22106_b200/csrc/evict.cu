@@ -49,6 +49,7 @@ struct CompactArgs {
   const int64_t *span;
   int32_t *kcur, *npages, *free_stack;
   const float *A;
+  const float *Ahat;   // select_shared: the slice-summed Â[t] every row ranks by (else NULL)
   const Ctrl *ctrl_ro;
   Ctrl *ctrl;
   const int32_t *ptab;
@@ -369,7 +370,7 @@ select_move_ws_kernel(CompactArgs a) {
     const int tl = min(a.l_tail, e.n);
     if (e.ka > tl && a.select_mode == ARBOR_SELECT_HEAVY) {   // ranked by A: the non-tail span
       const int r = it - wring[k & 3] * a.R;
-      const float *Arow = a.A + static_cast<int64_t>(r) * a.max_tokens + e.span;
+      const float *Arow = a.Ahat ? a.Ahat + e.span : a.A + static_cast<int64_t>(r) * a.max_tokens + e.span;
       float *ab = Abuf + (k & 1) * cap;
       for (int p = lane; p < e.n - tl; p += 32) cp_async4(ab + p, Arow + p);
     }
@@ -592,8 +593,29 @@ select_move_ws_kernel(CompactArgs a) {
 
 }  // namespace
 
+// Â[t] = Σ_{(l,h) ∈ slice, ascending} A[l][h][t]: fp64 accumulation of the f32 values, one
+// f32 rounding (the oracle's definition, bit for bit); grid-stride over positions
+__global__ void ahat_kernel(const float *__restrict__ A, int L, int H, int64_t max_tokens,
+                            SliceView sv, float *__restrict__ out) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < max_tokens;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int l = 0; l < L; ++l)
+      for (int h = 0; h < H; ++h)
+        if (sv.has(l, h)) acc = __dadd_rn(acc, static_cast<double>(A[(static_cast<int64_t>(l) * H + h) * max_tokens + t]));
+    out[t] = __double2float_rn(acc);
+  }
+}
+
 long long *g_evict_trace = nullptr;
 size_t g_evict_trace_n = 0;
+
+void launch_ahat(arbor_ctx *c) {
+  const int grid = static_cast<int>(std::min<int64_t>((c->max_tokens + 255) / 256, 4 * c->num_sms));
+  ahat_kernel<<<grid, 256, 0, c->ms>>>(c->cfg.score, c->L, c->H, c->max_tokens, slice_view(c),
+                                       c->d.ahat);
+  ARBOR_LAUNCHED(c);
+}
 
 void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
   CompactArgs a{};
@@ -616,6 +638,7 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
   a.npages = c->d.npages;
   a.free_stack = c->d.free_stack;
   a.A = c->cfg.score;
+  a.Ahat = c->prm.select_shared ? c->d.ahat : nullptr;
   a.ctrl_ro = c->d.ctrl;
   a.ctrl = c->d.ctrl;
   a.ptab = c->d.ptab;

@@ -40,7 +40,7 @@ constexpr int kMassThreads = 256;
 __global__ void __launch_bounds__(kMassThreads)
 node_mass_kernel(const int32_t *__restrict__ nodes, const int32_t *__restrict__ nlen,
                  const int64_t *__restrict__ span, const float *__restrict__ A, int L, int H,
-                 int64_t max_tokens, int64_t *__restrict__ scratch) {
+                 int64_t max_tokens, int64_t *__restrict__ scratch, SliceView sv) {
   const int node = nodes[blockIdx.x];
   const int l = blockIdx.y;
   const int n = nlen[node];
@@ -50,6 +50,7 @@ node_mass_kernel(const int32_t *__restrict__ nodes, const int32_t *__restrict__ 
   __shared__ long long red[kW];
   long long qsum = 0;
   for (int h = warp; h < H; h += kW) {
+    if (!sv.has(l, h)) continue;                  // thin slice (Q6)
     const float *row = A + (static_cast<int64_t>(l) * H + h) * max_tokens + a0;
     double m = 0.0;
     for (int t = lane; t < n; t += 32) m += static_cast<double>(row[t]);
@@ -124,6 +125,7 @@ struct FusedArgs {
   ApplyArgs ap;
   const int32_t *mass_nodes;
   int n_mass, N, L, H;
+  SliceView sv;                // rows whose masses count (thin slice)
   int64_t max_tokens;
   const int32_t *nlen;
   unsigned long long *acc;     // [max_nodes] int64 accumulators (zero between calls)
@@ -319,13 +321,14 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   }
   __syncthreads();
   // (2) this row's partial node masses: warp per node, lanes strided, fixed xor tree (Q29);
-  // node metadata batched like the chunks'
+  // node metadata batched like the chunks'.  Rows outside the thin slice add nothing.
   const float *Arow = a.A + (static_cast<int64_t>(li) * f.H + h) * f.max_tokens;
-  for (int mb = warp; mb < f.n_mass; mb += NW * 32) {
+  const int mass_end = f.sv.has(li, h) ? f.n_mass : 0;
+  for (int mb = warp; mb < mass_end; mb += NW * 32) {
     const MassMeta mmeta = (mb == warp && pre_m) ? *pre_m : load_mass_meta(f, mb + NW * lane, part, nparts);
     const int m_node = mmeta.node, m_n = mmeta.n;
     const long long m_sp = mmeta.sp;
-    const int nb = min(32, (f.n_mass - mb + NW - 1) / NW);
+    const int nb = min(32, (mass_end - mb + NW - 1) / NW);
     for (int j = 0; j < nb; ++j) {
       const int n = __shfl_sync(0xffffffffu, m_n, j);
       if (n == 0) continue;
@@ -575,6 +578,7 @@ FusedArgs fused_args(arbor_ctx *c, const PlanView &pv, const float *lse, const i
   a.Lc = c->L;
   a.Hq = c->Hq;
   a.G = c->G;
+  f.sv = slice_view(c);
   f.mass_nodes = d_nodes;
   f.n_mass = num_nodes;
   f.N = N;
@@ -595,7 +599,7 @@ FusedArgs fused_args(arbor_ctx *c, const PlanView &pv, const float *lse, const i
   m.u = c->d.u;
   m.mass2 = c->d.mass2;
   m.nq = c->nq_dev ? c->nq_dev : c->d.nq;
-  m.norm = static_cast<double>(c->Lg) * static_cast<double>(c->Hqg);
+  m.norm = msve_norm(c);
   m.th0 = c->prm.theta[0];
   m.thv = c->prm.theta[1];
   m.thu = c->prm.theta[2];
@@ -649,7 +653,8 @@ void launch_node_mass(arbor_ctx *c, const int32_t *d_nodes, int num_nodes, int64
                       int out_stride) {
   if (num_nodes == 0) return;
   node_mass_kernel<<<dim3(num_nodes, c->L), kMassThreads, 0, c->ms>>>(
-      d_nodes, c->d.n, c->d.span, c->cfg.score, c->L, c->H, c->max_tokens, c->d.mass_scratch);
+      d_nodes, c->d.n, c->d.span, c->cfg.score, c->L, c->H, c->max_tokens, c->d.mass_scratch,
+      slice_view(c));
   node_mass_finalize<<<(num_nodes + 127) / 128, 128, 0, c->ms>>>(d_nodes, num_nodes, c->L,
                                                                  c->d.mass_scratch, out, out_stride);
   c->launches += 2;
@@ -663,7 +668,7 @@ void launch_msve(arbor_ctx *c, int N, float *s_out) {
   m.u = c->d.u;
   m.mass2 = c->d.mass2;
   m.nq = c->nq_dev ? c->nq_dev : c->d.nq;
-  m.norm = static_cast<double>(c->Lg) * static_cast<double>(c->Hqg);
+  m.norm = msve_norm(c);
   m.th0 = c->prm.theta[0];
   m.thv = c->prm.theta[1];
   m.thu = c->prm.theta[2];

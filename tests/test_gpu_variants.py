@@ -104,3 +104,38 @@ def test_k_protect_path_floor_and_global_sinks(mode):
     co.transition(pr.tree, [float(x) for x in s_now], A_f32=pr.gpu_A())
     pr.check_kv_state()
     assert pr.ctx.arbor_read_counters()[0] == pr.orc.rehydrations
+
+
+@pytest.mark.parametrize("shared", [0, 1])
+def test_thin_slice_a_i_and_shared_selection(shared):
+    """Thin slice 𝓛 × 𝓗 (params.slice_layers / slice_kv_heads): a_i counts
+    the slice rows' mass only, normalised by |𝓛|·|𝓗_q|; with select_shared (the
+    paper-literal shared selection, Q1) every block is ranked once by the
+    slice-summed Â and every row keeps the same positions.  Masses bit-exact (oracle node
+    mass on the GPU's A over the slice rows), s against the oracle's fp64 MSVE, k and kept
+    sets bit-exact (tier (i))."""
+    from oracle import msve as omsve
+    preset = dict(MID, L=3, H=4, Hq=16)
+    pr = Pair(preset, seed=12, params_over=dict(slice_layers=2, slice_kv_heads=2,
+                                                 select_shared=shared))
+    assert pr.orc.slice == {(l, h) for l in (1, 2) for h in (0, 1)}
+    pr.warmup(steps_per_leaf=1)
+    pr.decode_both()
+    N = pr.tree.num_nodes
+    sc = pr.ctx.arbor_read_scores(N)
+    A = pr.gpu_A()[:, :, :pr.orc.Tmax].astype(np.float64)
+    for i in range(N):
+        m = omsve.node_mass(A, int(pr.tree.span_start[i]), int(pr.tree.span_len[i]), pr.orc.slice)
+        assert int(sc["mass"][i]) == m, i
+    a_ref, s_ref = pr.orc.msve(pr.tree)
+    assert np.allclose(sc["a"], a_ref, rtol=1e-6, atol=1e-7)
+    assert np.allclose(sc["s"], s_ref, rtol=1e-5)
+    B = int(0.3 * pr.tree.total_tokens)
+    st, k_ref, _ = pr.discrete_allocate(sc["s"], B)
+    assert st == 0
+    _evict_both(pr, k_ref)
+    if shared:
+        for i in range(N):
+            rows = [sorted(int(x) for x in pr.orc.kept[i][l, h]) for l in range(3) for h in range(4)]
+            assert all(r == rows[0] for r in rows), f"node {i}: rows keep different positions"
+    pr.decode_both()

@@ -791,3 +791,24 @@ def test_k_protect_reduces_to_pinning_and_keeps_floors():
                     assert k[j] >= min(n[j], prot)
             if mode == 0 and sum(n) > B:
                 assert sum(k) == B
+
+
+def test_thin_slice_rows_and_shared_selection_reduce_to_per_row():
+    """Slice rows = the last slice_layers layers × first slice_kv_heads KV heads (global,
+    shards offset); the shared selection on Â reduces to the per-row selection when every
+    row carries the same A (Â is then |slice|·A, the same order)."""
+    assert msve.slice_rows(2, 4, 0, 0, 2, 0, 0) is None
+    assert msve.slice_rows(2, 4, 0, 0, 4, 1, 2) == set()                     # layers 0-1 of 4
+    assert msve.slice_rows(2, 4, 2, 4, 4, 1, 6) == {(1, 0), (1, 1)}          # shard: layers 2-3, heads 4-7
+    tree, o, E = _small_state(levels=3, width=2, t_node=14, L=2, H=2, seed=21,
+                              params=default_params(k_min=2, l_tail=3, r_min=0.0, select_shared=1))
+    tree2, o2, _ = _small_state(levels=3, width=2, t_node=14, L=2, H=2, seed=21)
+    rng = np.random.default_rng(5)
+    base = rng.random(o.Tmax).astype(np.float32)
+    A = np.broadcast_to(base, (2, 2, o.Tmax)).copy()
+    tree.active = tree2.active = [synth.leaves_of(tree)[0]]
+    k = [max(2, x // 3) for x in o.n]
+    o.evict(tree, k, A_f32=A)
+    o2.evict(tree2, k, A_f32=A)
+    for i in range(len(o.n)):
+        assert np.array_equal(o.kept[i], o2.kept[i])
