@@ -294,6 +294,17 @@ arbor_status arbor_policy_event(arbor_ctx *ctx, const arbor_tree *tree, int32_t 
 /* Alg. 2 l.31-33 waterline input: M = Σ_i k_i over every known node (open nodes count their
  * current length).  HOST out, syncs main_stream. */
 arbor_status arbor_retained_tokens(arbor_ctx *ctx, int64_t *total);
+/* f1 — the waterline on the device (Alg. 2 l.31-33; "M ≥ 𝓑 − δ"): enqueue, with no
+ * host sync, a check of M = Σ_i k_cur_i against budget − delta and a Pressure (allocation in
+ * the bundle's Pressure mode, as ARBOR_PUE_PRESSURE, then evict) that takes effect only if
+ * the check fires; the Pressure is handled in the same call, so at most one is pending
+ * (SPEC S:529).  k_out: DEVICE [num_nodes] scratch (k = k_cur when nothing fired).  A fired
+ * check on a budget below the minimum feasible latches ARBOR_ERR_INFEASIBLE_BUDGET (reported
+ * by the next synchronising call). */
+arbor_status arbor_policy_waterline(arbor_ctx *ctx, const arbor_tree *tree, int64_t budget,
+                                    int64_t delta, int32_t *k_out);
+/* HOST out (sync): Pressures raised by arbor_policy_waterline so far. */
+arbor_status arbor_pressure_events(arbor_ctx *ctx, int64_t *count);
 
 /* f3 — Eq. 1 on the device: the MSVE uncertainty feature at a block boundary,
  * u = 1 − H/log|𝒱| with H = −Σ_w p(w) log p(w), p = softmax(logits) over the full vocabulary
@@ -303,6 +314,18 @@ arbor_status arbor_retained_tokens(arbor_ctx *ctx, int64_t *total);
  * ARBOR_ERR_INVALID_ARG for vocab < 2, batch < 1, NULL pointers or an unknown dtype. */
 arbor_status arbor_boundary_uncertainty(arbor_ctx *ctx, const void *logits, int32_t dtype,
                                         int32_t batch, int32_t vocab, float *u_out);
+
+/* f3 — MSVE θ calibration on the device ("calibrated
+ * offline using hindsight interventions"; loss and optimiser from SPEC S:224-242): full-batch
+ * gradient descent of L(θ) = mean_i (σ(θ₀ + θ_v v_i + θ_u u_i + θ_a a_i) − y_i)² for `epochs`
+ * epochs from the given θ; a step that would raise the loss halves the rate and retries (at
+ * most 20 halvings, the reduced rate is kept), so the loss never increases.
+ *  phi:    DEVICE [n][3] f32 (v_i, u_i, a_i ∈ [0,1])     target: DEVICE [n] f32 y_i ∈ [0,1]
+ *  theta:  HOST [4] fp64, in: start, out: fitted          loss_out: HOST [2] (initial, final) or NULL
+ * Context-free and synchronous (legacy default stream).  ARBOR_ERR_INVALID_ARG for n < 1,
+ * epochs < 0, lr ≤ 0, non-finite θ or NULL pointers. */
+arbor_status arbor_fit_theta(const float *phi, const float *target, int32_t n, int32_t epochs,
+                             double lr, double *theta, double *loss_out);
 
 /* ---- inspection / plumbing ------------------------------------------------------------ */
 arbor_status arbor_sync(arbor_ctx *ctx);   /* wait for both streams; returns latched errors */

@@ -91,6 +91,8 @@ def load_library(path: str = LIB_PATH):
         "arbor_rehydrate": ([P, C.POINTER(ArborTree), P, I32], I32),
         "arbor_policy_event": ([P, C.POINTER(ArborTree), I32, I32, I64, P, C.POINTER(C.c_int64)], I32),
         "arbor_retained_tokens": ([P, C.POINTER(C.c_int64)], I32),
+        "arbor_policy_waterline": ([P, C.POINTER(ArborTree), I64, I64, P], I32),
+        "arbor_pressure_events": ([P, C.POINTER(C.c_int64)], I32),
         "arbor_boundary_uncertainty": ([P, P, I32, I32, I32, P], I32),
         "arbor_tree_decode_attn": ([P, C.POINTER(ArborTree), I32, I32, P, P, P], I32),
         "arbor_decode_step": ([P, C.POINTER(ArborTree), P, P, P, P], I32),
@@ -114,6 +116,7 @@ def load_library(path: str = LIB_PATH):
         "arbor_min_feasible_budget": ([C.POINTER(ArborParams), C.POINTER(ArborTree),
                                        C.POINTER(C.c_int64)], I32),
         "arbor_version": ([], C.c_char_p),
+        "arbor_fit_theta": ([P, P, I32, I32, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)], I32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -330,6 +333,18 @@ class ArborKV:
         self._check(st, "arbor_policy_event")
         return k_out
 
+    def arbor_policy_waterline(self, tree, budget: int, delta: int, k_out):
+        """f1: the waterline check + gated Pressure on the device (no host sync)."""
+        ta = _tree(tree)
+        self._check(self.lib.arbor_policy_waterline(self._ctx, C.byref(ta.struct), int(budget),
+                                                    int(delta), k_out.data_ptr()),
+                    "arbor_policy_waterline")
+
+    def arbor_pressure_events(self) -> int:
+        v = C.c_int64(0)
+        self._check(self.lib.arbor_pressure_events(self._ctx, C.byref(v)), "arbor_pressure_events")
+        return int(v.value)
+
     def arbor_boundary_uncertainty(self, logits, u_out):
         """f3: Eq. 1 uncertainty of each row of logits [batch][vocab] (f32 or bf16) → u_out."""
         import torch
@@ -462,3 +477,16 @@ class ArborKV:
     def slot_rows(self, node: int):
         """(k_cur, n, pages) of a node (sync)."""
         return self.arbor_read_node(node)
+
+
+def fit_theta(phi, target, theta0=(0.0, 0.0, 0.0, 0.0), epochs=200, lr=4.0):
+    """f3: MSVE θ calibration on the device (include/arbor.h arbor_fit_theta).
+    phi: DEVICE f32 tensor [n][3] (v, u, a); target: DEVICE f32 [n].  Returns (θ, (L0, L1))."""
+    lib = load_library()
+    th = (C.c_double * 4)(*[float(x) for x in theta0])
+    ls = (C.c_double * 2)()
+    st = lib.arbor_fit_theta(phi.data_ptr(), target.data_ptr(), int(target.numel()), int(epochs),
+                             float(lr), th, ls)
+    if st != ARBOR_OK:
+        raise ArborError(st, "arbor_fit_theta failed")
+    return [th[i] for i in range(4)], (ls[0], ls[1])

@@ -43,6 +43,8 @@ struct AllocArgs {
   const double *Ed, *ED;
   int32_t *k_out;
   int only_node;   // ≥ 0: only this node's target is computed; the others get n (no change)
+  const int32_t *gate;   // f1 device waterline: when *gate == 0, k_out = k_cur (no change)
+  const int32_t *kcur;
   Ctrl *ctrl;
   long long *trace; // ARBOR_ALLOC_TRACE builds only: clock64() at phase boundaries
 };
@@ -177,6 +179,10 @@ allocate_kernel(AllocArgs a) {
   }
   pdl_wait();
   pdl_trigger();
+  if (a.gate && *a.gate == 0) {   // the waterline did not fire: no Pressure (Alg. 2 l.31-33)
+    for (int i = threadIdx.x; i < N; i += blockDim.x) a.k_out[i] = a.kcur[i];
+    return;
+  }
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
     a.depth[i] = dep[i];
     a.delta[i] = dlt[i];
@@ -524,9 +530,35 @@ allocate_kernel(AllocArgs a) {
 
 }  // namespace
 
+__global__ void waterline_kernel(const int32_t *__restrict__ kcur, int N, long long thresh,
+                                 int infeasible, Ctrl *ctrl) {
+  __shared__ long long red[32];
+  long long m = 0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) m += kcur[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tot = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+    const int fire = tot >= thresh ? 1 : 0;     // M ≥ 𝓑 − δ (Alg. 2 l.31)
+    ctrl->gate = infeasible ? 0 : fire;
+    if (fire && infeasible) atomicOr(&ctrl->err, DERR_INFEASIBLE);
+    if (fire && !infeasible) ctrl->pressure_events += 1;
+  }
+}
+
+void launch_waterline(arbor_ctx *c, int N, int64_t thresh, bool infeasible) {
+  waterline_kernel<<<1, 256, 0, c->ms>>>(c->d.kcur, N, thresh, infeasible ? 1 : 0, c->d.ctrl);
+  ARBOR_LAUNCHED(c);
+}
+
 void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget, int32_t *k_out,
-                     int mode, int only_node) {
+                     int mode, int only_node, bool gated) {
   AllocArgs a{};
+  a.gate = gated ? &c->d.ctrl->gate : nullptr;
+  a.kcur = c->d.kcur;
   a.N = N;
   a.budget = budget;
   a.mode = mode < 0 ? c->prm.alloc_mode : mode;

@@ -513,6 +513,7 @@ arbor_status latched(arbor_ctx *c) {
     if (h.err & DERR_INVARIANT)
       return fail(c, ARBOR_ERR_INVARIANT, "device: invalid accumulated attention / weight (NaN, negative or out of range)");
     if (h.err & DERR_OUT_OF_PAGES) return fail(c, ARBOR_ERR_OUT_OF_PAGES, "device: page pool exhausted");
+    if (h.err & DERR_INFEASIBLE) return fail(c, ARBOR_ERR_INFEASIBLE_BUDGET, "device waterline: Pressure on an infeasible budget");
     return fail(c, ARBOR_ERR_STATE, "device: state error");
   }
   return ARBOR_OK;
@@ -546,6 +547,11 @@ __global__ void init_free_kernel(int32_t *free_stack, int num_pages, Ctrl *ctrl)
     ctrl->evicted = 0;
     ctrl->rehydrations = 0;
     ctrl->pages_in_use = 0;
+    ctrl->gate = 0;
+    ctrl->pressure_events = 0;
+    ctrl->item_next = 0;
+    ctrl->item_done = 0;
+    ctrl->plan_ticket = 0;
   }
 }
 
@@ -1048,7 +1054,7 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
 
 static arbor_status allocate_impl(arbor_ctx *c, const arbor_tree *tree, const float *s,
                                   int64_t budget, int32_t *k_out, int64_t *min_feasible_out,
-                                  int mode, int only_node) {
+                                  int mode, int only_node, bool gated = false) {
   std::vector<int32_t> depth;
   TRY(check_tree(c, tree, &depth));
   if (!k_out) return fail(c, ARBOR_ERR_INVALID_ARG, "k_out is NULL");
@@ -1068,7 +1074,7 @@ static arbor_status allocate_impl(arbor_ctx *c, const arbor_tree *tree, const fl
   }
   TRY(upload_tree(c, tree));
   launch_allocate(c, tree->num_nodes, tree->num_active, s ? s : c->d.s, budget, k_out, mode,
-                  only_node);
+                  only_node, gated);
   CK_LAUNCH();
   c->geom_version = c->tree_version;   // the allocate kernel wrote depth, Δ, Path*, pinned
   return ARBOR_OK;
@@ -1080,8 +1086,16 @@ arbor_status arbor_allocate(arbor_ctx *c, const arbor_tree *tree, const float *s
   return allocate_impl(c, tree, s, budget, k_out, min_feasible_out, c->prm.alloc_mode, -1);
 }
 
+static arbor_status evict_impl(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_target,
+                               int64_t *evicted_tokens_out, bool gated);
+
 arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_target,
                          int64_t *evicted_tokens_out) {
+  return evict_impl(c, tree, k_target, evicted_tokens_out, false);
+}
+
+static arbor_status evict_impl(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_target,
+                               int64_t *evicted_tokens_out, bool gated) {
   if (!c) return ARBOR_ERR_INVALID_ARG;
   TRY(check_tree(c, tree));
   if (!k_target) return fail(c, ARBOR_ERR_INVALID_ARG, "k_target is NULL");
@@ -1108,7 +1122,7 @@ arbor_status arbor_evict(arbor_ctx *c, const arbor_tree *tree, const int32_t *k_
     launch_ahat(c);
     CK_LAUNCH();
   }
-  launch_evict(c, tree->num_nodes, k_target, max_n);
+  launch_evict(c, tree->num_nodes, k_target, max_n, gated);
   CK_LAUNCH();
   if (evicted_tokens_out) {
     CK(cudaStreamSynchronize(c->ms));
@@ -1217,6 +1231,39 @@ arbor_status arbor_boundary_uncertainty(arbor_ctx *c, const void *logits, int32_
   const arbor_status s = launch_uncertainty(c, logits, dtype, batch, vocab, u_out);
   if (s != ARBOR_OK) return fail(c, s, "uncertainty launch failed");
   CK_LAUNCH();
+  return ARBOR_OK;
+}
+
+// f1: Alg. 2 l.31-33 on the device — no host sync per decode step.  The waterline kernel
+// compares M = Σ_i k_cur_i with 𝓑 − δ and gates a Pressure (allocation in the bundle's
+// Pressure mode + evict) that is enqueued unconditionally behind it; when the gate is 0 the
+// allocation writes k = k_cur and the eviction finds nothing to do.  The Pressure runs in the
+// same call, so at most one is ever pending.
+arbor_status arbor_policy_waterline(arbor_ctx *c, const arbor_tree *tree, int64_t budget,
+                                    int64_t delta, int32_t *k_out) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  TRY(check_tree(c, tree));
+  if (!k_out) return fail(c, ARBOR_ERR_INVALID_ARG, "k_out is NULL");
+  if (budget < 0 || delta < 0) return fail(c, ARBOR_ERR_INVALID_ARG, "negative budget / delta");
+  const int mode = c->prm.alloc_mode == ARBOR_ALLOC_WATERFILL ? ARBOR_ALLOC_WATERFILL
+                                                               : ARBOR_ALLOC_STATIC_DRAIN;
+  arbor_params pm = c->prm;
+  pm.alloc_mode = mode;
+  const bool infeasible = budget < min_feasible(&pm, tree);
+  TRY(upload_tree(c, tree));
+  launch_waterline(c, tree->num_nodes, budget - delta, infeasible);
+  CK_LAUNCH();
+  if (infeasible) return ARBOR_OK;   // a raised Pressure latches ARBOR_ERR_INFEASIBLE_BUDGET
+  TRY(allocate_impl(c, tree, nullptr, budget, k_out, nullptr, mode, -1, true));
+  return evict_impl(c, tree, k_out, nullptr, true);
+}
+
+arbor_status arbor_pressure_events(arbor_ctx *c, int64_t *count) {
+  if (!c || !count) return ARBOR_ERR_INVALID_ARG;
+  TRY(sync_all(c));
+  long long v = 0;
+  CK(cudaMemcpy(&v, &c->d.ctrl->pressure_events, sizeof(v), cudaMemcpyDeviceToHost));
+  *count = v;
   return ARBOR_OK;
 }
 

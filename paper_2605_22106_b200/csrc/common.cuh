@@ -31,6 +31,7 @@ enum : int32_t {
   DERR_INVARIANT = 1,      // NaN / negative A, overflow
   DERR_OUT_OF_PAGES = 2,   // pool exhausted during append / rehydrate
   DERR_STATE = 4,
+  DERR_INFEASIBLE = 8,     // device waterline raised Pressure on an infeasible budget
 };
 
 // Device-side control block (library-owned, one per context)
@@ -42,6 +43,9 @@ struct Ctrl {
   int32_t plan_ticket;     // last-CTA ticket of the fused evict kernel (zero at rest)
   int32_t item_next;       // evict: next (node, row) work item to hand out (zero at rest)
   int32_t item_done;       // evict: select warps past the last item (zero at rest)
+  int32_t gate;            // f1 device waterline: 1 when the last check raised Pressure
+  int32_t pad_;
+  long long pressure_events;   // Pressures raised by the device waterline
   long long evicted;       // tokens evicted by the last evict
   long long rehydrations;  // total rehydrations
   long long pages_in_use;  // pages held by nodes
@@ -254,10 +258,14 @@ arbor_status launch_uncertainty(arbor_ctx *c, const void *logits, int dtype, int
 // allocate.cu
 // mode < 0: params.alloc_mode; only_node ≥ 0: targets of the other nodes are n (unchanged)
 void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget, int32_t *k_out,
-                     int mode = -1, int only_node = -1);
+                     int mode = -1, int only_node = -1, bool gated = false);
+// f1 waterline (Alg. 2 l.31-33) on the device: ctrl->gate = (Σ_i k_cur_i ≥ thresh); a gated
+// allocate then writes k_out = k_cur (no change) when the gate is 0.  infeasible: the
+// budget cannot be met — a raised Pressure latches DERR_INFEASIBLE instead.
+void launch_waterline(arbor_ctx *c, int N, int64_t thresh, bool infeasible);
 
 // evict.cu
-void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n);
+void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n, bool gated = false);
 // select_shared: Â[t] = Σ_{slice rows, ascending} A[l][h][t] in fp64, rounded to f32
 void launch_ahat(arbor_ctx *c);
 

@@ -63,6 +63,7 @@ struct CompactArgs {
   int n_sinks;      // global sinks: the root's first n_sinks positions (HEAVY, SINKS_TAIL)
   long long *trace; // ARBOR_EVICT_TRACE=1 (diagnostics): [cta][warp][4] globaltimer ns
   int wl_smem;      // N when the work list also lives in shared memory (N ≤ kSmemWorkNodes), else 0
+  const int32_t *gate;   // f1 device waterline: nothing to do when *gate == 0 (else NULL)
 };
 constexpr int kSmemWorkNodes = 1024;   // 32 KB of work entries per CTA
 
@@ -161,6 +162,7 @@ select_move_ws_kernel(CompactArgs a) {
   __syncthreads();
   pdl_wait();
   pdl_trigger();
+  if (a.gate && *a.gate == 0) return;   // the waterline did not fire: k = k_cur everywhere
   EV_TRACE(0);
   // ---- plan (Alg. 2, Q17): k_app = min(k_cur, k_target) for every non-pinned node;
   // the changed ones, ascending id, are the work list.  Every CTA derives it from the same
@@ -617,8 +619,9 @@ void launch_ahat(arbor_ctx *c) {
   ARBOR_LAUNCHED(c);
 }
 
-void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n) {
+void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n, bool gated) {
   CompactArgs a{};
+  a.gate = gated ? &c->d.ctrl->gate : nullptr;
   a.R = c->L * c->H;
   a.H = c->H;
   a.P = c->P;

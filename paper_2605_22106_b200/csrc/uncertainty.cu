@@ -12,6 +12,7 @@
 // CTAs' triples in fp64 and writes u.
 // HBM-bound: one read of the logits (4 or 2 B per vocabulary entry).
 #include <algorithm>
+#include <cmath>
 
 #include "common.cuh"
 
@@ -171,4 +172,109 @@ arbor_status launch_uncertainty(arbor_ctx *c, const void *logits, int dtype, int
   return e == cudaSuccess ? ARBOR_OK : ARBOR_ERR_CUDA;
 }
 
+
+// ---------------------------------------------------------------- f3: MSVE θ calibration
+// Full-batch gradient descent of L(θ) = mean_i (σ(θᵀx_i) − y_i)², x_i = (1, v_i, u_i, a_i),
+// with loss-nonincrease backoff (a step that raises the loss halves the rate and retries, at
+// most 20 halvings, the reduced rate is kept) — oracle/calibrate.py.  One CTA
+// runs every epoch: thread t sums examples t, t + 256, … in fp64, then a fixed-order tree
+// reduction in shared memory (deterministic); z = θ₀ + θ_v v + θ_u u + θ_a a left to right.
+namespace {
+constexpr int kFitThreads = 256;
+
+__device__ __forceinline__ double fit_sigma(const double *th, float v, float u, float a) {
+  double z = __dadd_rn(th[0], __dmul_rn(th[1], static_cast<double>(v)));
+  z = __dadd_rn(z, __dmul_rn(th[2], static_cast<double>(u)));
+  z = __dadd_rn(z, __dmul_rn(th[3], static_cast<double>(a)));
+  return 1.0 / (1.0 + exp(-z));
+}
+
+// block sum of per-thread values (fixed tree order); every thread gets the result
+template <int W>
+__device__ __forceinline__ void block_sum_vec(double (&v)[W], double (*red)[kFitThreads]) {
+  for (int k = 0; k < W; ++k) red[k][threadIdx.x] = v[k];
+  __syncthreads();
+  for (int off = kFitThreads / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off)
+      for (int k = 0; k < W; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + off];
+    __syncthreads();
+  }
+  for (int k = 0; k < W; ++k) v[k] = red[k][0];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kFitThreads)
+fit_theta_kernel(const float *__restrict__ phi, const float *__restrict__ y, int n, int epochs,
+                 double lr, double *theta_io, double *loss_io) {
+  __shared__ double red[4][kFitThreads];
+  __shared__ double th[4], cand[4];
+  if (threadIdx.x < 4) th[threadIdx.x] = theta_io[threadIdx.x];
+  __syncthreads();
+  const double inv_n = 1.0 / static_cast<double>(n);
+  auto loss_of = [&](const double *t) {
+    double acc[1] = {0.0};
+    for (int i = threadIdx.x; i < n; i += kFitThreads) {
+      const double d = fit_sigma(t, phi[3 * i], phi[3 * i + 1], phi[3 * i + 2]) - static_cast<double>(y[i]);
+      acc[0] += d * d;
+    }
+    block_sum_vec<1>(acc, red);
+    return acc[0] * inv_n;
+  };
+  double cur = loss_of(th);
+  const double first = cur;
+  for (int ep = 0; ep < epochs; ++ep) {
+    double g[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = threadIdx.x; i < n; i += kFitThreads) {
+      const float v = phi[3 * i], u = phi[3 * i + 1], a = phi[3 * i + 2];
+      const double s = fit_sigma(th, v, u, a);
+      const double c = 2.0 * (s - static_cast<double>(y[i])) * s * (1.0 - s);
+      g[0] += c;
+      g[1] += c * v;
+      g[2] += c * u;
+      g[3] += c * a;
+    }
+    block_sum_vec<4>(g, red);
+    for (int k = 0; k < 4; ++k) g[k] *= inv_n;
+    double step = lr, lc = 0.0;
+    bool ok = false;
+    for (int tr = 0; tr < 21; ++tr) {
+      if (threadIdx.x < 4) cand[threadIdx.x] = th[threadIdx.x] - step * g[threadIdx.x];
+      __syncthreads();
+      lc = loss_of(cand);
+      if (lc <= cur) { ok = true; break; }
+      step *= 0.5;
+    }
+    if (!ok) break;
+    if (threadIdx.x < 4) th[threadIdx.x] = cand[threadIdx.x];
+    __syncthreads();
+    cur = lc;
+    lr = step;
+  }
+  if (threadIdx.x < 4) theta_io[threadIdx.x] = th[threadIdx.x];
+  if (threadIdx.x == 0) { loss_io[0] = first; loss_io[1] = cur; }
+}
+}  // namespace
+
 }  // namespace arbor
+
+extern "C" arbor_status arbor_fit_theta(const float *phi, const float *target, int32_t n,
+                                        int32_t epochs, double lr, double *theta,
+                                        double *loss_out) {
+  if (!phi || !target || !theta || n < 1 || epochs < 0 || !(lr > 0.0)) return ARBOR_ERR_INVALID_ARG;
+  for (int k = 0; k < 4; ++k) if (!std::isfinite(theta[k])) return ARBOR_ERR_INVALID_ARG;
+  double *d = nullptr;
+  if (cudaMalloc(&d, 6 * sizeof(double)) != cudaSuccess) return ARBOR_ERR_CUDA;
+  arbor_status st = ARBOR_OK;
+  double h[6] = {theta[0], theta[1], theta[2], theta[3], 0.0, 0.0};
+  if (cudaMemcpy(d, h, 4 * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) st = ARBOR_ERR_CUDA;
+  if (st == ARBOR_OK) {
+    arbor::fit_theta_kernel<<<1, arbor::kFitThreads>>>(phi, target, n, epochs, lr, d, d + 4);
+    if (cudaGetLastError() != cudaSuccess || cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
+      st = ARBOR_ERR_CUDA;
+  }
+  cudaFree(d);
+  if (st != ARBOR_OK) return st;
+  for (int k = 0; k < 4; ++k) theta[k] = h[k];
+  if (loss_out) { loss_out[0] = h[4]; loss_out[1] = h[5]; }
+  return ARBOR_OK;
+}

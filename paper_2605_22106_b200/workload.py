@@ -298,8 +298,8 @@ class DptsRun:
 class Controller:
     """Alg. 2 on the library: every policy update event is one
     ``arbor_policy_event`` call (rehydrate / allocate / evict kernels, no host sync); the
-    waterline (Alg. 2 l.31-33, Σ k ≥ 𝓑 − δ, at most one pending Pressure) reads the retained
-    total (``arbor_retained_tokens``)."""
+    waterline (Alg. 2 l.31-33, Σ k ≥ 𝓑 − δ, at most one pending Pressure) runs on the device
+    (``arbor_policy_waterline``: the check gates a Pressure enqueued behind it)."""
 
     def __init__(self, ctx: ArborKV, budget: int, delta: int):
         import torch
@@ -330,7 +330,15 @@ class Controller:
         return self.ctx.arbor_retained_tokens()
 
     def waterline(self) -> bool:
+        """Host-side waterline (syncs for Σ k): kept for diagnostics; the decode loop uses
+        waterline_device."""
         if not self.pending and self.total() >= self.budget - self.delta:
             self.pending = True
             return True
         return False
+
+    def waterline_device(self, tree):
+        """Alg. 2 l.31-33 on the device: check M ≥ 𝓑 − δ and, if it fires, Pressure — in one
+        call, no host sync (arbor_policy_waterline)."""
+        self.ctx.arbor_policy_waterline(tree, self.budget, self.delta, self.k_buf[:tree.num_nodes])
+        self.log.append(("waterline", -1))

@@ -75,8 +75,11 @@ def run(expansions, rho, t_node, seed, controlled, budget=None):
         sample(kind)
 
     def waterline():
-        if ctl is not None and ctl.waterline():
-            policy("pressure")
+        # Alg. 2 l.31-33 on the device: check + gated Pressure, no host sync (the device time
+        # of every check counts as policy time, fired or not)
+        if ctl is not None:
+            pol_ms.append(timed(lambda: ctl.waterline_device(tree)))
+            kinds.append("waterline")
 
     def decode():
         q = sc.queries(50_000 + step[0], 1)
@@ -123,10 +126,11 @@ def run(expansions, rho, t_node, seed, controlled, budget=None):
            "nodes": tree.num_nodes, "final_tokens": int(tree.total_tokens),
            "decode_steps": len(dms), "decode_ms_total": sum(dms),
            "decode_ms_p50": statistics.median(dms),
-           "policy_events": {k: kinds.count(k) for k in ("boundary", "transition", "pressure")},
+           "policy_events": dict({k: kinds.count(k) for k in ("boundary", "transition", "waterline")},
+                                 pressure_fired=ctx.arbor_pressure_events() if controlled else 0),
            "policy_ms_total": sum(pms), "policy_ms_p50_by_kind": {
                k: statistics.median([m for m, kk in zip(pms, kinds) if kk == k])
-               for k in ("boundary", "transition", "pressure") if k in kinds},
+               for k in ("boundary", "transition", "waterline") if k in kinds},
            "policy_overhead_frac": sum(pms) / (sum(pms) + sum(dms)) if pms else 0.0,
            "rehydrations": rehyd,
            "peak_tokens": max(x["tokens"] for x in series),

@@ -9,7 +9,7 @@ both sides of every parity test see byte-identical inputs.
 """
 from .trees import (SynthTree, full_tree, search_tree, leaves_of, highest_v_leaf,
                     dpts_initial_leaves, dpts_schedule, tot_expansion)
-from .tensors import bf16_round_np, make_kv, make_queries, heavy_positions
+from .tensors import bf16_round_np, make_kv, make_queries, heavy_positions, hindsight_labels
 
 __all__ = [
     "SynthTree", "full_tree", "search_tree", "leaves_of", "highest_v_leaf",

@@ -74,3 +74,15 @@ def make_queries(n_active: int, L: int, Hq: int, d: int, dtype: str, seed: int, 
     e = E.to(device).repeat_interleave(G, dim=1)          # [L][Hq][d]
     q = q + 2.0 * e[None]
     return q.to(_torch_dtype(dtype)).contiguous()
+
+
+def hindsight_labels(n: int, seed: int, noise: float = 0.05):
+    """Synthetic stand-ins for MSVE calibration labels (the paper's are leave-one-out
+    accuracy drops, which need models): features φ = (v, u, a) ~ U(0,1)³ and a
+    hidden utility y = clip(0.55 v + 0.15 u + 0.30 a + N(0, noise²), 0, 1).  Returns
+    (phi float32 [n][3], y float32 [n], utility without noise float64 [n])."""
+    rng = np.random.default_rng(seed)
+    phi = rng.random((n, 3))
+    util = 0.55 * phi[:, 0] + 0.15 * phi[:, 1] + 0.30 * phi[:, 2]
+    y = np.clip(util + rng.normal(0.0, noise, n), 0.0, 1.0)
+    return phi.astype(np.float32), y.astype(np.float32), util

@@ -60,10 +60,18 @@ def test_controller_trace_lockstep(mode, budget, delta):
         assert gctl.total() == octl.total(), f"{kind}: retained totals differ"
 
     def waterline():
-        g, o = gctl.waterline(), octl.waterline()
-        assert g == o, "waterline decisions differ"
-        if g:
-            both("pressure")
+        # the device waterline (no host sync): check + gated Pressure in one call; the
+        # oracle decides on the host, and the states must agree afterwards
+        s, A = scores(), pr.gpu_A()
+        p0 = ctx.arbor_pressure_events()
+        gctl.waterline_device(tree)
+        fired = octl.waterline()
+        if fired:
+            octl.pressure(tree, s, A_f32=A)
+            events["pressure"] += 1
+        assert ctx.arbor_pressure_events() - p0 == (1 if fired else 0), "waterline decisions differ"
+        pr.check_kv_state()
+        assert gctl.total() == octl.total()
 
     pr.decode_both()
     both("boundary", 0)

@@ -812,3 +812,36 @@ def test_thin_slice_rows_and_shared_selection_reduce_to_per_row():
     o2.evict(tree2, k, A_f32=A)
     for i in range(len(o.n)):
         assert np.array_equal(o.kept[i], o2.kept[i])
+
+
+# ---------------------------------------------------------------- f3 θ-fitter
+def test_theta_fitter_gradient_constant_fit_and_separable():
+    """The fitter's gradient equals a central finite difference of its loss (independent
+    of the analytic formula); constant targets c converge to σ(θ₀) ≈ c; separable data
+    (critical blocks v = 1) rank perfectly; the loss never increases."""
+    from oracle import calibrate as cal
+    rng = np.random.default_rng(4)
+    phi = [tuple(float(x) for x in rng.random(3)) for _ in range(40)]
+    y = [float(x) for x in rng.random(40)]
+    th = [0.3, -0.7, 1.1, 0.2]
+    g = cal.grad(th, phi, y)
+    for k in range(4):
+        e = [0.0] * 4
+        e[k] = 1e-6
+        fd = (cal.loss([a + b for a, b in zip(th, e)], phi, y) -
+              cal.loss([a - b for a, b in zip(th, e)], phi, y)) / 2e-6
+        assert abs(fd - g[k]) < 1e-8
+    th_c, (l0, l1) = cal.fit_theta(phi, [0.2] * 40, [0, 0, 0, 0], 3000, 4.0)
+    assert l1 <= l0 and l1 < 1e-6
+    assert abs(cal.sigmoid(th_c[0] + sum(th_c[k + 1] * np.mean([p[k] for p in phi]) for k in range(3))) - 0.2) < 1e-3
+    crit = [i % 3 == 0 for i in range(30)]
+    phi2 = [(1.0 if c else 0.0, float(rng.random()), float(rng.random())) for c in crit]
+    th_s, _ = cal.fit_theta(phi2, [1.0 if c else 0.0 for c in crit], [0, 0, 0, 0], 500, 4.0)
+    sc = [cal.sigmoid(th_s[0] + th_s[1] * v + th_s[2] * u + th_s[3] * a) for v, u, a in phi2]
+    assert min(s for s, c in zip(sc, crit) if c) > max(s for s, c in zip(sc, crit) if not c)
+    # loss trace never increases (one epoch at a time from the same start)
+    th, prev = [0, 0, 0, 0], cal.loss([0, 0, 0, 0], phi, y)
+    for _ in range(20):
+        th, (_, cur) = cal.fit_theta(phi, y, th, 1, 8.0)
+        assert cur <= prev
+        prev = cur
