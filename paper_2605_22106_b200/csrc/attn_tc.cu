@@ -43,8 +43,17 @@
 namespace arbor {
 namespace {
 
-constexpr int kTcThreads = 448;   // producer, MMA, 4 softmax warps (even tiles), 4 epilogue warps,
-                                  // 4 softmax warps (odd tiles)
+// softmax warpgroups, each with its own TMEM S/Oᵀ buffer and P tile, taking tiles k ≡ group
+// (mod kGroups).  Two by default: three (ARBOR_TC_GROUPS=3, 576 threads) measured the same
+// tile rate on C3 (137.7 vs 137.0 µs closed tree, 184 vs 180 µs DPTS) — each group's softmax
+// slowed from 2.3 to 3.3 µs per tile, so the SM, not the per-group chain, sets the rate
+#ifndef ARBOR_TC_GROUPS
+#define ARBOR_TC_GROUPS 2
+#endif
+constexpr int kGroups = ARBOR_TC_GROUPS;
+constexpr int kTcThreads = 32 * (6 + 4 * kGroups);   // producer, MMA, 4 epilogue warps (6..9),
+                                                     // softmax groups: warps 2..5, 10..13, 14..17
+constexpr int kHdrRing = 8;                           // epilogue header / column-reduction rings
 constexpr int kTileRows = 128;
 constexpr int kHalf = 64;                       // = kAttnChunk
 constexpr uint32_t kKVBytes = kTileRows * 256;  // one K (or V) tile: 128 rows × 128 bf16
@@ -307,13 +316,17 @@ __device__ __forceinline__ unsigned long long colmask(int cnt, int G, int qw) {
   return m;
 }
 
-// two buffers of [S: NQ cols | Oᵀ: NQ cols]
+constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+constexpr int lcm_c(int a, int b) { return a / gcd_c(a, b) * b; }
+
+// kGroups buffers of [S: NQ cols | Oᵀ: NQ cols]
 template <int NQ>
 constexpr int tmem_cols() {
-  return 4 * NQ <= 32 ? 32 : 4 * NQ <= 64 ? 64 : 4 * NQ <= 128 ? 128 : 4 * NQ <= 256 ? 256 : 512;
+  constexpr int c = 2 * kGroups * NQ;
+  return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
 }
 
-// Dynamic smem: NSK K stages [K | Q], NSV V stages, two P tiles (all 1024-B aligned).
+// Dynamic smem: NSK K stages [K | Q], NSV V stages, kGroups P tiles (all 1024-B aligned).
 template <int NQ, int NSK, int NSV>
 struct TcSmem {
   static constexpr uint32_t kQ = NQ * 256;                    // Q tile bytes
@@ -321,9 +334,13 @@ struct TcSmem {
   static constexpr uint32_t kVBase = NSK * kKS;               // first V stage
   static constexpr uint32_t kP = NQ * 256;                    // P tile bytes (NQ rows × 128 slots)
   static constexpr uint32_t kPBase = kVBase + NSV * kKVBytes;
-  static constexpr uint32_t kBytes = kPBase + 2 * kP;
+  static constexpr uint32_t kBytes = kPBase + kGroups * kP;
   static constexpr uint32_t kAlloc = kBytes + 1024;           // + alignment slack
-  static constexpr int kRing = 2 * (NSK > NSV ? NSK : NSV);  // per-tile header ring
+  // per-tile header ring: slot k is rewritten at K(k + kRing)'s issue, which needs
+  // MMA1(k + kRing − NSK) complete ← MMA2(k + kRing − NSK − kGroups) issued ← softmax of that
+  // tile done: kRing ≥ NSK + kGroups keeps it past softmax(k) (and the V issue of tile k)
+  static constexpr int kRing = 8;
+  static_assert(kRing >= NSK + kGroups && kRing >= NSV + kGroups, "header ring");
 };
 
 template <int NQ, int NSK, int NSV>
@@ -341,22 +358,33 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   auto Vst = [&](int s) { return sm + S::kVBase + s * kKVBytes; };  // V stage s
   // K (+ q rows) and V of a stage have their own barriers: K is free again once MMA1 has
   // read it, V only after MMA2, so the next K loads go out ~1.5 µs earlier
-  __shared__ __align__(8) uint64_t full_k[NSK], empty_k[NSK], full_v[NSV], empty_v[NSV];
-  // kcons[s]: the softmax group of tile k has passed its full_k[k % NSK] wait (128 arrivals).
-  // K(j) is issued only after kcons of tile j − NSK, so full_k[s] is never a phase ahead of a
+  // The full barriers the softmax groups wait on are split by (stage, group): tile k arms
+  // full_k[k % NSK][k % kGroups] (and full_v likewise), whose consecutive tiles are LK
+  // (LV) = lcm(stages, kGroups) apart, so each is waited by ONE group in tile order — with
+  // kGroups not dividing the stage count a shared full barrier could be waited two phases
+  // early (a fresh barrier reads its "previous" phase as complete: group 2's first tile,
+  // k = 2 on stage 0, passed before K(0) landed — the 3-group hang).
+  constexpr int LK = lcm_c(NSK, kGroups), LV = lcm_c(NSV, kGroups);
+  __shared__ __align__(8) uint64_t full_k[NSK][kGroups], empty_k[NSK], full_v[NSV][kGroups],
+      empty_v[NSV];
+  // kcons[s][g]: the softmax of tile k (stage s, group g) has passed its full_k wait (128
+  // arrivals).  K(j) is issued only after kcons of tile j − LK (the previous tile on its full
+  // barrier), so a full barrier is never a phase ahead of a
   // softmax wait on it (no parity aliasing, for any NSK)
-  __shared__ __align__(8) uint64_t kcons[NSK];
-  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], o_full[2], o_empty[2];
+  __shared__ __align__(8) uint64_t kcons[NSK][kGroups];
+  __shared__ __align__(8) uint64_t s_full[kGroups], s_empty[kGroups], p_full[kGroups],
+      o_full[kGroups], o_empty[kGroups];
   // per-tile header and page list, ring of RING = 2·max(NSK, NSV) tiles (written at K issue;
   // read by the V issue, the softmax and — via ohdr — the epilogue; slot k is rewritten by
   // tile k + RING, whose K issue needs MMA1(k + RING − NSK), i.e. MMA2(k) issued, i.e.
   // softmax(k) done; K issue runs < RING tiles ahead of V issue)
   __shared__ TcHdr hdr[RING];
   __shared__ int vpage[RING][kMaxTilePages];
-  __shared__ TcHdr ohdr[4];                             // tile k's header for the epilogue warps
-  // column max / sum of each warp quadrant, ring of 4 tiles (the epilogue warps read tile k's
-  // before releasing Oᵀ buffer k&1, which softmax(k+4) needs first)
-  __shared__ float red_m[4][4][NQ], red_l[4][4][NQ];
+  __shared__ TcHdr ohdr[kHdrRing];                      // tile k's header for the epilogue warps
+  // column max / sum of each warp quadrant, ring of kHdrRing tiles (the epilogue warps read
+  // tile k's before releasing Oᵀ buffer k % kGroups; softmax(k + 8) writes after o_full of
+  // k + 8 − kGroups, which needed epilogue(k + 8 − 2·kGroups) ≥ epilogue(k))
+  __shared__ float red_m[kHdrRing][4][NQ], red_l[kHdrRing][4][NQ];
   // column n of a tile = leaf slot j = n / qw, q head g = n % qw: col_j[n] = j and
   // col_js[n] = j·SP + g (SP = Lc·H·G: the pair stride of zbuf / partials in (l, h, g) units);
   // launch constants, so the per-column address math needs no division
@@ -427,7 +455,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     for (int s = 0; s < NSK; ++s)
       for (uint32_t i = (tid - 32) * 16; i < S::kQ; i += (kTcThreads - 32) * 16)
         *reinterpret_cast<uint4 *>(Kst(s) + kKVBytes + i) = make_uint4(0, 0, 0, 0);
-    for (uint32_t i = (tid - 32) * 16; i < 2 * S::kP; i += (kTcThreads - 32) * 16)
+    for (uint32_t i = (tid - 32) * 16; i < kGroups * S::kP; i += (kTcThreads - 32) * 16)
       *reinterpret_cast<uint4 *>(Pbuf + i) = make_uint4(0, 0, 0, 0);
     fence_proxy_async();
   }
@@ -438,15 +466,17 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   }
   if (tid == 32) {
     for (int s = 0; s < NSK; ++s) {
-      mbar_init(&full_k[s], 1);
+      for (int g = 0; g < kGroups; ++g) {
+        mbar_init(&full_k[s][g], 1);
+        mbar_init(&kcons[s][g], 128);   // the 4 warps of one softmax group
+      }
       mbar_init(&empty_k[s], 1);
-      mbar_init(&kcons[s], 128);    // the 4 warps of one softmax group
     }
     for (int s = 0; s < NSV; ++s) {
-      mbar_init(&full_v[s], 1);
+      for (int g = 0; g < kGroups; ++g) mbar_init(&full_v[s][g], 1);
       mbar_init(&empty_v[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kGroups; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 128);   // the 4 softmax warps
       mbar_init(&o_full[b], 1);
@@ -485,7 +515,27 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     const int ppH = kHalf >> lgP;
     int kk_k = 0, kk_v = 0;
     if (ntiles > 0) load_state(0);
+#ifdef ARBOR_MBAR_WATCHDOG
+    unsigned long long wd_t0 = 0;
+    int wd_k = -1, wd_v = -1;
+#endif
     while (kk_v < ntiles) {
+#ifdef ARBOR_MBAR_WATCHDOG
+      {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (kk_k != wd_k || kk_v != wd_v) { wd_k = kk_k; wd_v = kk_v; wd_t0 = t; }
+        else if (wd_t0 && t - wd_t0 > 5000000000ull) {
+          if (lane == 0)
+            printf("producer stuck: block %d ntiles %d kk_k %d kk_v %d empty_k %d kcons %d empty_v %d\n",
+                   blockIdx.x, ntiles, kk_k, kk_v,
+                   (int)mbar_test(&empty_k[kk_k % NSK], ((kk_k / NSK) & 1u) ^ 1u),
+                   (int)mbar_test(&kcons[kk_k % NSK][kk_k % kGroups], ((kk_k / LK) & 1u) ^ 1u),
+                   (int)mbar_test(&empty_v[kk_v % NSV], ((kk_v / NSV) & 1u) ^ 1u));
+          wd_t0 = 0;
+        }
+      }
+#endif
       bool go_k = false, go_v = false;
       if (kk_k < ntiles && kk_k < kk_v + RING) {
         // K(j) may land only after softmax(j − NSK) has passed its full_k wait (kcons):
@@ -500,7 +550,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 #ifdef ARBOR_TC_NOGATE   // diagnostics only: no kcons gate (can deadlock)
         const bool ok = mbar_test(&empty_k[sk], par);
 #else
-        const bool ok = mbar_test(&empty_k[sk], par) && mbar_test(&kcons[sk], par);
+        const bool ok = mbar_test(&empty_k[sk], par) &&
+                        mbar_test(&kcons[sk][kk_k % kGroups], ((kk_k / LK) & 1u) ^ 1u);
 #endif
         go_k = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
       }
@@ -532,14 +583,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         const int it = blockIdx.x + k * gridDim.x;
         const int li = (it / a.g.H) % a.Lc, h = it % a.g.H;
         const int pgA = (ntA + P - 1) >> lgP, pgB = (ntB + P - 1) >> lgP;
-        const int s = k % NSK, r = k % RING, fk = s;
+        const int s = k % NSK, r = k % RING;
+        uint64_t *fkb = &full_k[s][k % kGroups];
         if (lane == 0) { TC_TRACE(k, 0); TC_TRACE(k, 1); }
         unsigned char *Ks = Kst(s);
         unsigned char *Qs = Ks + kKVBytes;
         if (lane == 0) {
           hdr[r] = TcHdr{ntA, ntB, li, h, pbA, pbB, cnt,
                          (pbB >= 0 ? 1 : 0) | (cntB > 0 ? 2 : 0) | (cntA << 4)};
-          mbar_arrive_expect_tx(&full_k[fk], static_cast<uint32_t>(pgA + pgB) * P * 256u +
+          mbar_arrive_expect_tx(fkb, static_cast<uint32_t>(pgA + pgB) * P * 256u +
                                                 static_cast<uint32_t>(cnt * a.qw) * 256u);
         }
         if (lane < kMaxTilePages) vpage[r][lane] = page;
@@ -559,20 +611,20 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           if (pi == 0) {
             const int lp = l * a.g.NP + page;
             const uint32_t dst = static_cast<uint32_t>(half * kHalf) * 128u;
-            tma_load_5d(Ks + dst, &tmk4, 0, 0, 0, h, lp, &full_k[fk]);
-            tma_load_5d(Ks + 16384 + dst, &tmk4, 0, 1, 0, h, lp, &full_k[fk]);
+            tma_load_5d(Ks + dst, &tmk4, 0, 0, 0, h, lp, fkb);
+            tma_load_5d(Ks + 16384 + dst, &tmk4, 0, 1, 0, h, lp, fkb);
           }
         } else if (lane < 2 * ppH && pi < pgh) {
           const int row = static_cast<int>(pool_row(a.g, l, page, h, 0));
           const uint32_t dst = static_cast<uint32_t>(half * kHalf + pi * P) * 128u;
-          tma_load_2d(Ks + dst, &tmk, 0, row, &full_k[fk]);
-          tma_load_2d(Ks + 16384 + dst, &tmk, 64, row, &full_k[fk]);
+          tma_load_2d(Ks + dst, &tmk, 0, row, fkb);
+          tma_load_2d(Ks + 16384 + dst, &tmk, 64, row, fkb);
         }
         if (lane < cnt) {
           // leaf `lane`: its G q rows (a qw-row box) → Q rows [qw·lane, qw·lane + qw)
           const int row = (leaf * a.Lc + li) * a.Hq + h * a.G;
-          tma_load_2d(Qs + lane * a.qw * 128, &tmq, 0, row, &full_k[fk]);
-          tma_load_2d(Qs + NQ * 128 + lane * a.qw * 128, &tmq, 64, row, &full_k[fk]);
+          tma_load_2d(Qs + lane * a.qw * 128, &tmq, 0, row, fkb);
+          tma_load_2d(Qs + NQ * 128 + lane * a.qw * 128, &tmq, 64, row, fkb);
         }
         if (lane == 0) TC_TRACE(k, 2);
         ++kk_k;
@@ -588,7 +640,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         const int page = lane < kMaxTilePages ? vpage[r][lane] : 0;
         const int pgA = (hd.ntA + P - 1) >> lgP, pgB = (hd.ntB + P - 1) >> lgP;
         unsigned char *Vs = Vst(s);
-        if (lane == 0) mbar_arrive_expect_tx(&full_v[s], static_cast<uint32_t>(pgA + pgB) * P * 256u);
+        uint64_t *fvb = &full_v[s][k % kGroups];
+        if (lane == 0) mbar_arrive_expect_tx(fvb, static_cast<uint32_t>(pgA + pgB) * P * 256u);
         __syncwarp();
         const int l = a.layer_begin + hd.li;
         const int half = lane >= ppH, pi = lane - half * ppH;
@@ -602,14 +655,14 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           if (pi == 0) {
             const int lp = l * a.g.NP + page;
             const uint32_t dst = static_cast<uint32_t>(half * kHalf) * 128u;
-            tma_load_5d(Vs + dst, &tmv4, 0, 0, 0, hd.h, lp, &full_v[s]);
-            tma_load_5d(Vs + 16384 + dst, &tmv4, 0, 1, 0, hd.h, lp, &full_v[s]);
+            tma_load_5d(Vs + dst, &tmv4, 0, 0, 0, hd.h, lp, fvb);
+            tma_load_5d(Vs + 16384 + dst, &tmv4, 0, 1, 0, hd.h, lp, fvb);
           }
         } else if (lane < 2 * ppH && pi < pgh) {
           const int row = static_cast<int>(pool_row(a.g, l, page, hd.h, 0));
           const uint32_t dst = static_cast<uint32_t>(half * kHalf + pi * P) * 128u;
-          tma_load_2d(Vs + dst, &tmv, 0, row, &full_v[s]);
-          tma_load_2d(Vs + 16384 + dst, &tmv, 64, row, &full_v[s]);
+          tma_load_2d(Vs + dst, &tmv, 0, row, fvb);
+          tma_load_2d(Vs + 16384 + dst, &tmv, 64, row, fvb);
         }
         ++kk_v;
       }
@@ -620,13 +673,35 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       constexpr uint32_t id1 = bf16_idesc(128, NQ, 0, 0);       // S = K · Qᵀ
       constexpr uint32_t id2 = bf16_idesc(128, NQ, 1, 0);       // Oᵀ = Vᵀ · Pᵀ
       // Two independent streams of work, issued as soon as each is ready (non-blocking
-      // polls): MMA1(j) needs tile j's stage (full) and S buffer j&1 drained (s_empty of
-      // j−2); MMA2(j) needs P(j) (p_full) and Oᵀ buffer j&1 drained (o_empty of j−2).
+      // polls): MMA1(j) needs tile j's stage (full) and S buffer j % kGroups drained (s_empty
+      // of j − kGroups); MMA2(j) needs P(j) (p_full) and Oᵀ buffer j % kGroups drained
+      // (o_empty of j − kGroups).  MMA1 runs at most kGroups − 1 tiles ahead of MMA2.
       int js = 0, jo = 0;
+#ifdef ARBOR_MBAR_WATCHDOG
+      unsigned long long wd_t0 = 0;
+      int wd_s = -1, wd_o = -1;
+#endif
       while (jo < ntiles) {
-        if (js < ntiles && js <= jo + 1 && mbar_test(&full_k[js % NSK], (js / NSK) & 1u) &&
-            (js < 2 || mbar_test(&s_empty[js & 1], ((js - 2) >> 1) & 1u))) {
-          const int s = js % NSK, b = js & 1;
+#ifdef ARBOR_MBAR_WATCHDOG
+        {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          if (js != wd_s || jo != wd_o) { wd_s = js; wd_o = jo; wd_t0 = t; }
+          else if (wd_t0 && t - wd_t0 > 5000000000ull) {
+            printf("mma stuck: block %d ntiles %d js %d jo %d full_k %d s_empty %d p_full %d o_empty %d\n",
+                   blockIdx.x, ntiles, js, jo,
+                   js < ntiles ? (int)mbar_test(&full_k[js % NSK][js % kGroups], (js / LK) & 1u) : -1,
+                   js < kGroups ? 1 : (int)mbar_test(&s_empty[js % kGroups], ((js - kGroups) / kGroups) & 1u),
+                   (int)mbar_test(&p_full[jo % kGroups], (jo / kGroups) & 1u),
+                   jo < kGroups ? 1 : (int)mbar_test(&o_empty[jo % kGroups], ((jo - kGroups) / kGroups) & 1u));
+            wd_t0 = 0;
+          }
+        }
+#endif
+        if (js < ntiles && js <= jo + kGroups - 1 &&
+            mbar_test(&full_k[js % NSK][js % kGroups], (js / LK) & 1u) &&
+            (js < kGroups || mbar_test(&s_empty[js % kGroups], ((js - kGroups) / kGroups) & 1u))) {
+          const int s = js % NSK, b = js % kGroups;
           TC_TRACE(js, 3);
           tc_fence_after();
           const uint32_t ks = smem_u32(Kst(s));
@@ -639,12 +714,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           }
           tc_commit(&s_full[b]);
           tc_commit(&empty_k[s]);            // K (and q) of this stage may be reloaded
-          if (a.trace) { mbar_wait(&s_full[b], (js >> 1) & 1u); TC_TRACE(js, 12); }
+          if (a.trace) { mbar_wait(&s_full[b], (js / kGroups) & 1u); TC_TRACE(js, 12); }
           ++js;
         }
-        if (jo < js && mbar_test(&p_full[jo & 1], (jo >> 1) & 1u) &&
-            (jo < 2 || mbar_test(&o_empty[jo & 1], ((jo - 2) >> 1) & 1u))) {
-          const int s = jo % NSV, b = jo & 1;
+        if (jo < js && mbar_test(&p_full[jo % kGroups], (jo / kGroups) & 1u) &&
+            (jo < kGroups || mbar_test(&o_empty[jo % kGroups], ((jo - kGroups) / kGroups) & 1u))) {
+          const int s = jo % NSV, b = jo % kGroups;
           TC_TRACE(jo, 5);
           tc_fence_after();
           const uint32_t vs = smem_u32(Vst(s));
@@ -657,7 +732,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           }
           tc_commit(&o_full[b]);
           tc_commit(&empty_v[s]);
-          if (a.trace) { mbar_wait(&o_full[b], (jo >> 1) & 1u); TC_TRACE(jo, 13); }
+          if (a.trace) { mbar_wait(&o_full[b], (jo / kGroups) & 1u); TC_TRACE(jo, 13); }
           ++jo;
         }
       }
@@ -673,7 +748,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     // One column max / sum over the whole 128-slot tile (both chunks): the four warps of the
     // group combine their warp results through smem behind one 128-thread named barrier.
     constexpr int GW = kW<NQ>;
-    const int grp = warp >= 10 ? 1 : 0;
+    const int grp = warp < 6 ? 0 : (warp - 6) / 4;   // warps 2..5 → 0, 10..13 → 1, 14..17 → 2
+    static_assert(kGroups >= 2 && kGroups <= 3, "softmax groups");
     const int quad = warp & 3;                 // TMEM lane quadrant of this warp
     const int half = quad >> 1;                // slot half (chunk A or B) of this thread
     const int bar_id = 1 + grp;                // named barrier of this group (128 threads)
@@ -684,12 +760,12 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     const int SP = a.Lc * a.g.H * G;
     const int myc = colW<NQ>(lane);
     const uint32_t cb = static_cast<uint32_t>(tc * 2);
-    for (int k = grp; k < ntiles; k += 2) {
-      const int s = k % NSK, b = k & 1;
-      mbar_wait(&full_k[s], (k / NSK) & 1u);
+    for (int k = grp; k < ntiles; k += kGroups) {
+      const int s = k % NSK, b = k % kGroups, ph = (k / kGroups) & 1;
+      mbar_wait(&full_k[s][grp], (k / LK) & 1u);
       if (tid == 64) TC_TRACE(k, 7);
       const TcHdr hd = hdr[k % RING];
-      mbar_arrive(&kcons[s]);               // past the full_k wait: K(k + NSK) may land
+      mbar_arrive(&kcons[s][grp]);          // past the full_k wait: K(k + LK) may land
       const int cntA = hd.meta >> 4;
       const bool pack = (hd.meta & 2) != 0;
       // this half's query columns: a packed B half has its own, after A's
@@ -702,16 +778,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       const int pb = half ? hd.pbB : hd.pbA;
       const bool valid = present && tc < nt;
       const int ngrp = (min(NQ, qw * hd.cnt) + GW - 1) / GW;
-      mbar_wait(&s_full[b], (k >> 1) & 1u);
+      mbar_wait(&s_full[b], ph);
       if (tid == 64) TC_TRACE(k, 8);
       tc_fence_after();
-      // P buffer b was last read by MMA2(k−2)
-      if (k >= 2) mbar_wait(&o_full[b], ((k - 2) >> 1) & 1u);
-      // the header for the epilogue warps: ring slot k&3 was last read by epilogue(k − 4),
-      // which did so before its o_empty arrival, which MMA2(k − 2) — complete, o_full above —
-      // waited for (written earlier, right after the full_k wait, it could overtake
-      // epilogue(k − 4) once K runs ahead: tiles with another tile's header)
-      if (half == 0 && lane == 0 && quad == 0) ohdr[k & 3] = hd;
+      // P buffer b was last read by MMA2(k − kGroups)
+      if (k >= kGroups) mbar_wait(&o_full[b], ph ^ 1);
+      // the header for the epilogue warps: ring slot k % 8 was last read by epilogue(k − 8)
+      // before its o_empty arrival, which MMA2(k − kGroups) — complete, o_full above —
+      // waited for (kHdrRing ≥ 2·kGroups); written earlier, right after the full_k wait, it
+      // could overtake the epilogue once K runs ahead (tiles with another tile's header)
+      if (half == 0 && lane == 0 && quad == 0) ohdr[k % kHdrRing] = hd;
       // P (bf16) goes to row n of slot-half `half` of the Pᵀ tile; rows of columns past the
       // tile's own keep stale values: they only feed output columns that are never stored
       // (Oᵀ column n depends on Pᵀ row n alone)
@@ -728,16 +804,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         // column max and sum over the 128 slots: butterfly transpose-reduce in the warp, then
         // the group's four warps combine through smem (ring of 4 tiles)
         const float mw = warp_reduceW<GW, true>(z, lane);
-        if (!(lane & 1)) red_m[k & 3][quad][c + myc] = mw;
+        if (!(lane & 1)) red_m[k % kHdrRing][quad][c + myc] = mw;
         named_bar_sync(bar_id, 128);
 #pragma unroll
         for (int i = 0; i < GW; ++i) {
-          const float m = fmaxf(fmaxf(red_m[k & 3][0][c + i], red_m[k & 3][1][c + i]),
-                                fmaxf(red_m[k & 3][2][c + i], red_m[k & 3][3][c + i]));
+          const float m = fmaxf(fmaxf(red_m[k % kHdrRing][0][c + i], red_m[k % kHdrRing][1][c + i]),
+                                fmaxf(red_m[k % kHdrRing][2][c + i], red_m[k % kHdrRing][3][c + i]));
           p[i] = z[i] == -INFINITY ? 0.f : fast_exp2(z[i] - m);   // m = −inf only if all masked
         }
         const float lw = warp_reduceW<GW, false>(p, lane);
-        if (!(lane & 1)) red_l[k & 3][quad][c + myc] = lw;
+        if (!(lane & 1)) red_l[k % kHdrRing][quad][c + myc] = lw;
 #pragma unroll
         for (int i = 0; i < GW; ++i) {
           const int r = c + i;
@@ -759,7 +835,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       // 0 · v stays 0 in Oᵀ = Vᵀ·Pᵀ (the rows past the last page were zeroed before)
       // V of this stage has landed (MMA2 needs it anyway; P is only published after)
       const int sv = k % NSV;
-      mbar_wait(&full_v[sv], (k / NSV) & 1u);
+      mbar_wait(&full_v[sv][grp], (k / LV) & 1u);
       if (present && (nt & (P - 1))) {
         const int r0 = nt, r1 = (nt + P - 1) & ~(P - 1);
         unsigned char *Vs = Vst(sv);
@@ -787,18 +863,18 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     const int SP = a.Lc * a.g.H * G;
     const int etid = tid - 192;                // 0..127
     for (int k = 0; k < ntiles; ++k) {
-      const int b = k & 1;
-      mbar_wait(&o_full[b], (k >> 1) & 1u);
+      const int b = k % kGroups;
+      mbar_wait(&o_full[b], (k / kGroups) & 1u);
       if (tid == 192) TC_TRACE(k, 10);
       tc_fence_after();
-      const TcHdr hd = ohdr[k & 3];   // read before o_empty: softmax(k+4) rewrites this slot
-      // m (log2 domain) and l of column n = etid, from the softmax ring slot k&3
+      const TcHdr hd = ohdr[k % kHdrRing];   // read before o_empty (see the softmax)
+      // m (log2 domain) and l of column n = etid, from the softmax ring slot k % kHdrRing
       float mm = 0.f, ll = 0.f;
       if (etid < NQ) {
-        mm = fmaxf(fmaxf(red_m[k & 3][0][etid], red_m[k & 3][1][etid]),
-                   fmaxf(red_m[k & 3][2][etid], red_m[k & 3][3][etid]));
-        ll = (red_l[k & 3][0][etid] + red_l[k & 3][1][etid]) +
-             (red_l[k & 3][2][etid] + red_l[k & 3][3][etid]);
+        mm = fmaxf(fmaxf(red_m[k % kHdrRing][0][etid], red_m[k % kHdrRing][1][etid]),
+                   fmaxf(red_m[k % kHdrRing][2][etid], red_m[k % kHdrRing][3][etid]));
+        ll = (red_l[k % kHdrRing][0][etid] + red_l[k % kHdrRing][1][etid]) +
+             (red_l[k % kHdrRing][2][etid] + red_l[k % kHdrRing][3][etid]);
       }
       const int qw = a.qw;
       const int ngrp = (min(NQ, qw * hd.cnt) + GW - 1) / GW;
@@ -988,7 +1064,11 @@ bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_b
   // (K, V) ring depths; (4, 2) for NQ = 8 / 16 measured the same as (3, 3) on C2
   if (nq <= 8) launch_tc<8, 3, 3>(c, a);
   else if (nq <= 16) launch_tc<16, 3, 3>(c, a);
+#ifdef ARBOR_TC_NQ32_NSK3
+  else if (nq <= 32) launch_tc<32, 3, 2>(c, a);
+#else
   else if (nq <= 32) launch_tc<32, 2, 2>(c, a);
+#endif
   else if (nq <= 48) launch_tc<48, 2, 2>(c, a);
   else return false;
   return true;

@@ -105,12 +105,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef ARBOR_MBAR_WATCHDOG
+#define mbar_wait(bar, parity) mbar_wait_impl((bar), (parity), __LINE__)
+__device__ __forceinline__ void mbar_wait_impl(uint64_t *bar, uint32_t parity, int line) {
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#endif
 #ifdef ARBOR_MBAR_WATCHDOG
   // debug builds (ARBOR_NVCC_FLAGS=-DARBOR_MBAR_WATCHDOG): a wait still pending after 5 s
-  // prints the barrier and traps, so a pipeline deadlock surfaces as a CUDA error, not a hang
+  // prints its call site and barrier (lane 0 of the warp) and keeps waiting, so every stuck
+  // role reports; after 15 s it traps — a deadlock surfaces as a CUDA error, not a hang
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  bool reported = false;
   for (;;) {
     uint32_t ok;
     asm volatile(
@@ -122,11 +129,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (ok) return;
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    if (t1 - t0 > 5000000000ull) {
-      printf("mbarrier watchdog: block %d thread %d bar smem 0x%x parity %u\n", blockIdx.x,
-             threadIdx.x, smem_u32(bar), parity);
-      __trap();
+    if (!reported && t1 - t0 > 5000000000ull) {
+      if ((threadIdx.x & 31) == 0)
+        printf("mbarrier watchdog: line %d block %d thread %d bar smem 0x%x parity %u\n", line,
+               blockIdx.x, threadIdx.x, smem_u32(bar), parity);
+      reported = true;
     }
+    if (t1 - t0 > 15000000000ull) __trap();
   }
 #endif
   asm volatile(
