@@ -47,11 +47,11 @@ def main():
     del os.environ["ARBOR_EVICT_TRACE"]
     lib = pk.load_library()
     ctas = torch.cuda.get_device_properties(0).multi_processor_count * 2
-    n = ctas * 16 * 4
+    n = ctas * 16 * 8
     buf = (C.c_longlong * n)()
     lib.arbor_debug_evict_trace.argtypes = [C.POINTER(C.c_longlong), C.c_longlong]
     assert lib.arbor_debug_evict_trace(buf, n) == 0
-    tr = np.frombuffer(buf, dtype=np.int64).reshape(ctas, 16, 4).astype(np.float64)
+    tr = np.frombuffer(buf, dtype=np.int64).reshape(ctas, 16, 8).astype(np.float64)
     t0 = tr[:, :, 0][tr[:, :, 0] > 0].min()
     rel = (tr - t0) / 1e3
     valid = tr > 0
@@ -66,6 +66,8 @@ def main():
         "ctas": ctas,
         "pct": "min/p10/p50/p90/max µs after the first CTA start",
         "cta_start": pct(np.where(valid[:, 0, 0], rel[:, 0, 0], np.nan)),
+        "plan_loads_done": pct(np.where(valid[:, 0, 4], rel[:, 0, 4], np.nan)),
+        "plan_scans_done": pct(np.where(valid[:, 0, 5], rel[:, 0, 5], np.nan)),
         "plan_done": pct(np.where(valid[:, 0, 1], rel[:, 0, 1], np.nan)),
         "select_first_job": pct(np.where(valid[:, sel, 2], rel[:, sel, 2], np.nan).ravel()),
         "move_first_job": pct(np.where(valid[:, mov, 2], rel[:, mov, 2], np.nan).ravel()),
