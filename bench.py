@@ -728,6 +728,15 @@ def main():
         pg.destroy_process_group()
 
 
+def c3_traffic():
+    """DRAM bytes per launch of the C3 attention kernel from the committed ncu capture
+    (profiles/ncu_traffic.json, c3/attn), or None."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["c3"]["attn"]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def run_c3(args, dev, rank, ws, hc, nid, pg):
     """configs[2]: the DPTS frontier.  16 active leaves under distinct
     level-2 parents of the 8B-shaped depth-4 × width-5 tree, ρ = 0.5 (B = 9,984 fixed while
@@ -887,7 +896,7 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
             "roofline": {"kernel": "attn_tc (a9, 16 leaves, tree-shared tiles)", "bound": "hbm",
                          "achieved": kern_gbs, "peak": peak, "unit": "GB/s",
                          "frac": kern_gbs / peak, "frac_of_nominal_8TBps": kern_gbs / NOMINAL_HBM,
-                         "traffic": None, "peak_source": peak_src,
+                         "traffic": c3_traffic(), "peak_source": peak_src,
                          "alg_bytes_per_launch": attn_b, "ms_per_launch": kern_ms,
                          "decode_step_GBps": attn_gbs, "decode_step_ms": attn_ms,
                          "note": "achieved / ms_per_launch: the attention kernel's mean launch "
