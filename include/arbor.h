@@ -55,7 +55,14 @@ typedef enum { ARBOR_F32 = 0, ARBOR_BF16 = 1 } arbor_dtype;
 typedef enum {
   ARBOR_ALLOC_WATERFILL = 0,    /* budget-exact optimisation view with floors (default) */
   ARBOR_ALLOC_STATIC = 1,       /* Eqs. 2-3 directly, no budget guarantee                */
-  ARBOR_ALLOC_STATIC_DRAIN = 2  /* Eqs. 2-3, then Alg. 2's Pressure drain to the budget  */
+  ARBOR_ALLOC_STATIC_DRAIN = 2, /* Eqs. 2-3, then Alg. 2's Pressure drain to the budget  */
+  /* f4 — the sequence-flattened StreamingLLM analogue: the single
+   * active path root → ℓ is one token stream keeping its global sinks (the root's first
+   * n_sinks tokens) and its most recent 𝓑 − Σ_open n − |sinks| tokens; off-path blocks get
+   * k = 0; open blocks stay pinned.  Requires num_active = 1, l_tail = 0 and select_mode
+   * SINKS_TAIL (the per-block selection is then exactly "sinks + the most recent k");
+   * pair with no_rehydrate = 1 for the baseline's irreversible eviction. */
+  ARBOR_ALLOC_STREAM = 3
 } arbor_alloc_mode;
 
 /* config.flags */

@@ -222,7 +222,8 @@ class ArborOracle:
         d, dist, on_path = self.geometry(tree)
         mode = self.params["alloc_mode"] if mode is None else mode
         st, k, mf = tae.allocate(mode, s, d, dist, on_path, self.open, self.n, self.params,
-                                 budget)
+                                 budget, parent=[int(x) for x in tree.parent],
+                                 leaf=int(tree.active[0]))
         if st != tae.STATUS_OK:
             raise OracleError(ERR_INFEASIBLE, f"infeasible budget, min feasible {mf}")
         return k
@@ -254,10 +255,12 @@ class ArborOracle:
                 acc = acc + A_f32[l, h].astype(np.float64)
             A_f32 = np.broadcast_to(acc.astype(np.float32), A_f32.shape)
         _, _, on_path = self.geometry(tree)
-        protect = self.params.get("k_protect", 0)
+        # pinned: open blocks, and Path* unless k_protect or the flattened-stream
+        # analogue (its path is a stream, not a protected set) is in force
+        path_free = self.params.get("k_protect", 0) or self.params["alloc_mode"] == tae.MODE_STREAM
         evicted = 0
         for j in range(len(self.n)):
-            if self.open[j] or (on_path[j] and not protect):   # pinned (Q19; P:104 k_protect)
+            if self.open[j] or (on_path[j] and not path_free):
                 continue
             kc = self.k_cur(j)
             k_app = min(kc, max(0, int(k_target[j])))

@@ -27,7 +27,7 @@ WEIGHT_SCALE_LOG2 = 24          # Q29: W_j = round(w_j · 2^24)
 WEIGHT_SCALE = 1 << WEIGHT_SCALE_LOG2
 EPS_FLOOR = 1e-9                # Q10: ⌊x + 1e-9⌋
 
-MODE_WATERFILL, MODE_STATIC, MODE_STATIC_DRAIN = 0, 1, 2
+MODE_WATERFILL, MODE_STATIC, MODE_STATIC_DRAIN, MODE_STREAM = 0, 1, 2, 3
 
 STATUS_OK = 0
 STATUS_INFEASIBLE = 3
@@ -169,7 +169,35 @@ def proportional_slack(f, n, R, ids):
     return k
 
 
-def allocate(mode, s, depth, dist, on_path, is_open, n, params, budget):
+def stream_targets(parent, leaf: int, is_open, n, n_sinks: int, budget: int):
+    """The sequence-flattened StreamingLLM analogue (the baselines are adapted to
+    ToT "by treating the currently active search path as the streaming sequence"; SPEC
+    S:626 SeqFlat with no heavy hitters): the active path root → ℓ is one token stream that
+    keeps its global sinks (the root's first n_sinks tokens) and its most recent
+    W = 𝓑 − Σ_open n − |sinks| tokens; blocks off the path are outside the stream (k = 0).
+    Open blocks stay pinned.  Returns (status, k, min_feasible)."""
+    N = len(n)
+    k = [n[j] if is_open[j] else 0 for j in range(N)]
+    s0 = min(n_sinks, n[0]) if not is_open[0] else 0
+    need = sum(n[j] for j in range(N) if is_open[j]) + s0
+    if budget < need:
+        return STATUS_INFEASIBLE, None, need
+    rem = budget - need
+    path = []
+    x = leaf
+    while x >= 0:
+        path.append(x)
+        x = parent[x]
+    for x in path:                      # leaf first: the most recent tokens
+        if is_open[x]:
+            continue
+        w = min(n[x], rem)
+        rem -= w
+        k[x] = min(n[x], s0 + w) if x == 0 else w
+    return STATUS_OK, k, None
+
+
+def allocate(mode, s, depth, dist, on_path, is_open, n, params, budget, parent=None, leaf=None):
     """TAE allocation of k_i for every node.
 
     s: per-node MSVE score (float, fp32 value), depth/dist: geometry,
@@ -178,6 +206,8 @@ def allocate(mode, s, depth, dist, on_path, is_open, n, params, budget):
     Returns (status, k: list[int], min_feasible: int|None)."""
     N = len(n)
     n = [int(x) for x in n]
+    if mode == MODE_STREAM:
+        return stream_targets(parent, leaf, is_open, n, int(params["n_sinks"]), budget)
     # invariant (i) (P:104): Path* blocks keep k = n (Q19, default) — or, with k_protect > 0,
     # a high floor min(n, k_protect) instead; open blocks are always pinned
     protect = int(params.get("k_protect", 0))

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libarbor.so")
 ARBOR_OK = 0
 STATUS = {0: "OK", 2: "INVALID_ARG", 3: "INFEASIBLE_BUDGET", 4: "INVARIANT", 5: "IO",
           6: "OUT_OF_PAGES", 7: "STATE", 8: "CUDA", 9: "NCCL"}
-ALLOC_MODES = {"waterfill": 0, "static": 1, "static_drain": 2}
+ALLOC_MODES = {"waterfill": 0, "static": 1, "static_drain": 2, "stream": 3}
 SELECT_MODES = {"heavy": 0, "tail": 1, "sinks_tail": 2}
 FLAG_PROFILE = 1
 FLAG_EXTERNAL_REDUCE = 2

@@ -33,6 +33,7 @@ struct AllocArgs {
   double alpha, gamma, eta, r_min;
   int k_min, l_tail, gamma_int;   // gamma_int ≥ 0: integer exponent (repeated products)
   int k_protect;                  // 0 → Path* pinned at n; > 0 → Path* floor min(n, k_protect)
+  int n_sinks;                    // STREAM: the root's sink tokens
   const float *s;
   const int32_t *n;
   const int32_t *parent, *active;
@@ -187,7 +188,7 @@ allocate_kernel(AllocArgs a) {
     a.depth[i] = dep[i];
     a.delta[i] = dlt[i];
     a.onpath[i] = onp[i];
-    a.pinned[i] = ((onp[i] && a.k_protect == 0) || a.open[i]) ? 1 : 0;
+    a.pinned[i] = ((onp[i] && a.k_protect == 0 && a.mode != 3) || a.open[i]) ? 1 : 0;
   }
   __syncthreads();
 
@@ -195,7 +196,8 @@ allocate_kernel(AllocArgs a) {
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
     const int nj = a.n[j];
     nn[j] = nj;
-    const bool pin = (onp[j] && a.k_protect == 0) || a.open[j];
+    // mode 3 (STREAM, the flattened-stream analogue): the path is a stream, not pinned
+    const bool pin = (onp[j] && a.k_protect == 0 && a.mode != 3) || a.open[j];
     // protected Path* block: allocated like the others above min(n, k_protect)
     const int pf = (onp[j] && a.k_protect > 0) ? min(nj, a.k_protect) : 0;
     // w = s^γ · E_d[d] · E_Δ[Δ] · (η if off-path), strictly left to right
@@ -220,6 +222,9 @@ allocate_kernel(AllocArgs a) {
     if (pin) {
       k[j] = nj;
       cls[j] = 0;   // pinned
+    } else if (a.mode == 3) {
+      k[j] = 0;      // outside the stream until the path walk below
+      cls[j] = 1;
     } else if (a.mode != 0) {
       // Eq. 2-3 (STATIC): r = clip(α·w, r_min, 1)
       const double r = fmin(1.0, fmax(a.r_min, __dmul_rn(a.alpha, w)));
@@ -283,6 +288,23 @@ allocate_kernel(AllocArgs a) {
           dr = dr < 0 ? 0 : (dr > cap ? cap : dr);
           k[j] -= static_cast<int>(dr);
         }
+      }
+    }
+  } else if (a.mode == 3) {
+    // ---- STREAM: the sequence-flattened StreamingLLM analogue ----
+    // the single active path root → ℓ keeps the root's first n_sinks tokens and its most
+    // recent 𝓑 − Σ_open n − |sinks| tokens, walking from ℓ up (oracle/tae.stream_targets)
+    long long open_n = 0;
+    for (int j = threadIdx.x; j < N; j += blockDim.x) if (a.open[j]) open_n += nn[j];
+    open_n = block_sum(open_n, red64);
+    if (threadIdx.x == 0) {
+      const int s0 = a.open[0] ? 0 : min(a.n_sinks, nn[0]);
+      long long rem = a.budget - open_n - s0;   // ≥ 0: the host checked min_feasible
+      for (int x = act[0]; x >= 0; x = par[x]) {
+        if (a.open[x]) continue;
+        const int w = static_cast<int>(min(static_cast<long long>(nn[x]), rem));
+        rem -= w;
+        k[x] = x == 0 ? min(nn[x], s0 + w) : w;
       }
     }
   } else if (a.mode == 0) {
@@ -570,6 +592,7 @@ void launch_allocate(arbor_ctx *c, int N, int nA, const float *s, int64_t budget
   a.k_min = c->prm.k_min;
   a.l_tail = c->prm.l_tail;
   a.k_protect = c->prm.k_protect;
+  a.n_sinks = c->prm.n_sinks;
   const double g = c->prm.gamma;
   a.gamma_int = (g >= 0.0 && g <= 64.0 && g == static_cast<double>(static_cast<int>(g)))
                     ? static_cast<int>(g) : -1;

@@ -107,7 +107,10 @@ arbor_status validate_params(const arbor_params *p, std::string &msg) {
   if (!fin(p->eta) || p->eta <= 0 || p->eta > 1) { msg = "eta must be in (0,1]"; return ARBOR_ERR_INVALID_ARG; }
   if (!fin(p->r_min) || p->r_min < 0 || p->r_min > 1) { msg = "r_min must be in [0,1]"; return ARBOR_ERR_INVALID_ARG; }
   if (p->k_min < 0 || p->l_tail < 0 || p->n_sinks < 0) { msg = "k_min, l_tail, n_sinks must be >= 0"; return ARBOR_ERR_INVALID_ARG; }
-  if (p->alloc_mode < 0 || p->alloc_mode > 2) { msg = "bad alloc_mode"; return ARBOR_ERR_INVALID_ARG; }
+  if (p->alloc_mode < 0 || p->alloc_mode > 3) { msg = "bad alloc_mode"; return ARBOR_ERR_INVALID_ARG; }
+  if (p->alloc_mode == ARBOR_ALLOC_STREAM && (p->l_tail != 0 || p->select_mode != ARBOR_SELECT_SINKS_TAIL)) {
+    msg = "alloc_mode STREAM needs l_tail 0 and select_mode SINKS_TAIL"; return ARBOR_ERR_INVALID_ARG;
+  }
   for (double t : p->theta) if (!fin(t)) { msg = "theta must be finite"; return ARBOR_ERR_INVALID_ARG; }
   if (p->select_mode < 0 || p->select_mode > 2) { msg = "bad select_mode"; return ARBOR_ERR_INVALID_ARG; }
   if (p->no_rehydrate != 0 && p->no_rehydrate != 1) { msg = "no_rehydrate must be 0 or 1"; return ARBOR_ERR_INVALID_ARG; }
@@ -164,8 +167,10 @@ std::vector<uint8_t> host_path_star(const arbor_tree *t) {
 }
 
 // pinned (k = n, never evicted): open blocks, and Path* unless params.k_protect > 0
-std::vector<uint8_t> host_pinned(const arbor_tree *t, int k_protect) {
-  std::vector<uint8_t> pin = k_protect > 0 ? std::vector<uint8_t>(t->num_nodes, 0) : host_path_star(t);
+// or the flattened-stream analogue is the allocation (its path is a stream)
+std::vector<uint8_t> host_pinned(const arbor_tree *t, const arbor_params *p) {
+  const bool path_free = p->k_protect > 0 || p->alloc_mode == ARBOR_ALLOC_STREAM;
+  std::vector<uint8_t> pin = path_free ? std::vector<uint8_t>(t->num_nodes, 0) : host_path_star(t);
   for (int i = 0; i < t->num_nodes; ++i) if (t->is_open[i]) pin[i] = 1;
   return pin;
 }
@@ -178,7 +183,12 @@ int64_t floor_count_host(int n, const arbor_params *p) {
 
 int64_t min_feasible(const arbor_params *p, const arbor_tree *t) {
   if (p->alloc_mode == ARBOR_ALLOC_STATIC) return 0;
-  const auto pin = host_pinned(t, p->k_protect);
+  if (p->alloc_mode == ARBOR_ALLOC_STREAM) {   // open blocks + the root's sinks
+    int64_t tot = t->is_open[0] ? 0 : std::min(p->n_sinks, t->span_len[0]);
+    for (int i = 0; i < t->num_nodes; ++i) if (t->is_open[i]) tot += t->span_len[i];
+    return tot;
+  }
+  const auto pin = host_pinned(t, p);
   const auto on = host_path_star(t);
   int64_t tot = 0;
   for (int i = 0; i < t->num_nodes; ++i) {
@@ -1059,6 +1069,8 @@ static arbor_status allocate_impl(arbor_ctx *c, const arbor_tree *tree, const fl
   TRY(check_tree(c, tree, &depth));
   if (!k_out) return fail(c, ARBOR_ERR_INVALID_ARG, "k_out is NULL");
   if (budget < 0) return fail(c, ARBOR_ERR_INVALID_ARG, "negative budget");
+  if (mode == ARBOR_ALLOC_STREAM && tree->num_active != 1)
+    return fail(c, ARBOR_ERR_INVALID_ARG, "alloc_mode STREAM flattens one active path");
   // weights must stay ≤ 2^16 (Q29): bound e^{−λ_d d} e^{−λ_Δ Δ} over the tree's depths
   int maxd = 0;
   for (int x : depth) maxd = std::max(maxd, x);
@@ -1066,7 +1078,9 @@ static arbor_status allocate_impl(arbor_ctx *c, const arbor_tree *tree, const fl
   for (int x = 0; x <= maxd; ++x) bd = std::max(bd, std::exp(-c->prm.lambda_d * x));
   for (int x = 0; x <= 2 * maxd; ++x) bD = std::max(bD, std::exp(-c->prm.lambda_delta * x));
   if (!(bd * bD <= 65536.0)) return fail(c, ARBOR_ERR_INVALID_ARG, "lambda_d / lambda_delta make weights exceed 2^16");
-  const int64_t mf = min_feasible(&c->prm, tree);
+  arbor_params pm = c->prm;
+  pm.alloc_mode = mode;
+  const int64_t mf = min_feasible(&pm, tree);
   if (mode != ARBOR_ALLOC_STATIC && budget < mf) {
     if (min_feasible_out) *min_feasible_out = mf;
     return fail(c, ARBOR_ERR_INFEASIBLE_BUDGET, "budget " + std::to_string(budget) +
@@ -1100,7 +1114,7 @@ static arbor_status evict_impl(arbor_ctx *c, const arbor_tree *tree, const int32
   TRY(check_tree(c, tree));
   if (!k_target) return fail(c, ARBOR_ERR_INVALID_ARG, "k_target is NULL");
   TRY(upload_tree(c, tree));
-  const auto pin = host_pinned(tree, c->prm.k_protect);
+  const auto pin = host_pinned(tree, &c->prm);
   int max_n = 0;
   for (int i = 0; i < tree->num_nodes; ++i)
     if (!pin[i]) max_n = std::max(max_n, c->h_n[i]);

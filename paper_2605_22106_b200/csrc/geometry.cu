@@ -44,7 +44,7 @@ geometry_kernel(int N, int nA, const int32_t *__restrict__ parent,
       best = dist < best ? dist : best;
     }
     delta[i] = best;
-    pinned[i] = ((onpath[i] && k_protect == 0) || open[i]) ? 1 : 0;   // P:104, Q19
+    pinned[i] = ((onpath[i] && k_protect == 0) || open[i]) ? 1 : 0;   // P:104, Q19 (+STREAM)
   }
 }
 
@@ -54,7 +54,7 @@ void launch_geometry(arbor_ctx *c, int N, int nA) {
   stage_begin(c, ARBOR_ST_GEOMETRY, c->ms);
   geometry_kernel<<<1, 1024, 0, c->ms>>>(N, nA, c->d.parent, c->d.active, c->d.open,
                                           c->d.depth, c->d.delta, c->d.onpath, c->d.pinned,
-                                          c->prm.k_protect);
+                                          c->prm.alloc_mode == ARBOR_ALLOC_STREAM ? 1 : c->prm.k_protect);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_GEOMETRY, c->ms);
 }

@@ -17,7 +17,7 @@ def oracle_params(preset_params: dict) -> dict:
     p = default_params()
     p.update(preset_params)
     if isinstance(p.get("alloc_mode"), str):
-        p["alloc_mode"] = {"waterfill": 0, "static": 1, "static_drain": 2}[p["alloc_mode"]]
+        p["alloc_mode"] = {"waterfill": 0, "static": 1, "static_drain": 2, "stream": 3}[p["alloc_mode"]]
     if isinstance(p.get("select_mode"), str):
         p["select_mode"] = {"heavy": 0, "tail": 1, "sinks_tail": 2}[p["select_mode"]]
     return p
@@ -183,4 +183,5 @@ class Pair:
         d, dist, on_path = self.orc.geometry(self.tree)
         m = self.orc.params["alloc_mode"] if mode is None else mode
         return tae.allocate(m, [float(x) for x in s], d, dist, on_path, self.orc.open, self.orc.n,
-                            self.orc.params, budget)
+                            self.orc.params, budget, parent=[int(x) for x in self.tree.parent],
+                            leaf=int(self.tree.active[0]))

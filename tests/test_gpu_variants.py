@@ -139,3 +139,32 @@ def test_thin_slice_a_i_and_shared_selection(shared):
             rows = [sorted(int(x) for x in pr.orc.kept[i][l, h]) for l in range(3) for h in range(4)]
             assert all(r == rows[0] for r in rows), f"node {i}: rows keep different positions"
     pr.decode_both()
+
+
+def test_stream_analogue_irreversible():
+    """The flattened StreamingLLM analogue (alloc_mode STREAM) with irreversible
+    eviction (no_rehydrate): allocation and eviction bit-exact against the oracle on
+    one path, then after a backtrack to another leaf (the old path's blocks leave the stream
+    for good); decode over what is left."""
+    pr = Pair(MID, seed=14, params_over=dict(alloc_mode="stream", l_tail=0,
+                                              select_mode="sinks_tail", n_sinks=4,
+                                              no_rehydrate=True))
+    pr.warmup(steps_per_leaf=1)
+    leaves = synth.leaves_of(pr.tree)
+    N = pr.tree.num_nodes
+    for leaf, frac in ((leaves[0], 0.08), (leaves[-1], 0.06)):
+        pr.tree.active = [leaf]
+        pr.decode_both()
+        B = int(frac * pr.tree.total_tokens)
+        st, k_ref, _ = pr.discrete_allocate([0.5] * N, B)
+        assert st == 0 and sum(k_ref) <= B
+        k = torch.empty(N, dtype=torch.int32, device="cuda")
+        pr.ctx.arbor_allocate(pr.tree, None, B, k)
+        assert k.cpu().tolist() == k_ref
+        _evict_both(pr, k_ref)
+        path = [x for x in range(N) if pr.orc.k_cur(x) < int(pr.tree.span_len[x])]
+        pr.ctx.arbor_rehydrate(pr.tree, path)      # a no-op under no_rehydrate
+        assert pr.orc.rehydrate(path) == 0
+        pr.check_kv_state()
+    assert set(range(4)) <= set(int(x) for x in pr.orc.kept[0][0, 0])
+    pr.decode_both()

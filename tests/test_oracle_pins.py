@@ -845,3 +845,23 @@ def test_theta_fitter_gradient_constant_fit_and_separable():
         th, (_, cur) = cal.fit_theta(phi, y, th, 1, 8.0)
         assert cur <= prev
         prev = cur
+
+
+def test_stream_analogue_closed_forms():
+    """The sequence-flattened StreamingLLM analogue: on the active path
+    root → ℓ the most recent W = 𝓑 − |open| − |sinks| tokens are kept whole blocks first from
+    the leaf up, one block partially, plus the root's sinks; off-path blocks get 0."""
+    parent = [-1, 0, 0, 1, 1, 3]
+    n = [10, 20, 30, 40, 50, 60]
+    opn = [False] * 6
+    st, k, _ = tae.stream_targets(parent, 5, opn, n, 4, 4 + 60 + 40 + 7)
+    assert st == 0 and k == [4, 7, 0, 40, 0, 60]              # leaf, node 3 whole, node 1 partial
+    st, k, _ = tae.stream_targets(parent, 5, opn, n, 4, 10 ** 6)
+    assert k == [10, 20, 0, 40, 0, 60]                          # the whole path, nothing else
+    st, k, _ = tae.stream_targets(parent, 5, opn, n, 4, 4 + 60 + 40 + 20 + 3)
+    assert k == [7, 20, 0, 40, 0, 60]                           # sinks + the root's last 3
+    opn[5] = True
+    st, k, mf = tae.stream_targets(parent, 5, opn, n, 4, 50)
+    assert st == 3 and mf == 64                                 # open leaf + sinks > 𝓑
+    st, k, _ = tae.stream_targets(parent, 5, opn, n, 4, 64 + 5)
+    assert k == [4, 0, 0, 5, 0, 60]
