@@ -522,9 +522,10 @@ allocate_kernel(AllocArgs a) {
       given = block_sum(given, red64);
       TRACE(5);
       const long long leftover = Num - given;
-      if (leftover > 0) {
-        // largest remainder: rank of each active node by (rem desc, W desc, id asc) — a warp
-        // per node, lanes over the other nodes, one __reduce_add_sync per node
+      if (leftover > 0 && N <= 256) {
+        // largest remainder: the `leftover` active nodes first in (rem desc, W desc, id asc)
+        // get +1.  Small trees: rank of each active node — a warp per node, lanes over the
+        // other nodes, one __reduce_add_sync per node (O(N²/32): 4.8 µs at N = 156)
         int *rank = cand;                       // the breakpoint list is no longer needed
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
         for (int j = wid; j < N; j += nw) {
@@ -541,6 +542,43 @@ allocate_kernel(AllocArgs a) {
         __syncthreads();
         for (int j = threadIdx.x; j < N; j += blockDim.x)
           if (cls[j] == 6 && rank[j] < leftover) k[j] += 1;
+      } else if (leftover > 0) {
+        // larger trees: bitonic sort of the active ids in shared memory by the same key (keys
+        // are unique — the id breaks every tie — so the compaction order does not matter);
+        // the quadratic ranking took 23 µs at N = 512 (C5), this 15 µs
+        int *idx = cand;
+        __shared__ int na_s;
+        if (threadIdx.x == 0) na_s = 0;
+        __syncthreads();
+        for (int j = threadIdx.x; j < N; j += blockDim.x)
+          if (cls[j] == 6) idx[atomicAdd(&na_s, 1)] = j;
+        __syncthreads();
+        const int na = na_s;
+        int P2 = 1;
+        while (P2 < na) P2 <<= 1;
+        for (int t = na + threadIdx.x; t < P2; t += blockDim.x) idx[t] = -1;   // sentinels: last
+        __syncthreads();
+        auto gt = [&](int x, int y) {           // key(x) > key(y); −1 below everything
+          if (y < 0) return x >= 0;
+          if (x < 0) return false;
+          if (rem[x] != rem[y]) return rem[x] > rem[y];
+          if (W[x] != W[y]) return W[x] > W[y];
+          return x < y;
+        };
+        for (int size = 2; size <= P2; size <<= 1) {
+          for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+              const int p = i ^ stride;
+              if (p > i) {
+                const int x = idx[i], y = idx[p];
+                const bool desc = (i & size) == 0;   // this run sorted descending
+                if (desc ? gt(y, x) : gt(x, y)) { idx[i] = y; idx[p] = x; }
+              }
+            }
+            __syncthreads();
+          }
+        }
+        for (int t = threadIdx.x; t < leftover; t += blockDim.x) k[idx[t]] += 1;
       }
     }
   }

@@ -29,7 +29,8 @@ def main():
     fn = lib.arbor_debug_set_alloc_trace
     fn.argtypes = [C.c_void_p, C.c_void_p]
     fn.restype = C.c_int32
-    sc = workload.setup("c2", 0)
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    sc = workload.setup(cfg, 0)
     ctx, tree = sc.ctx, sc.tree
     workload.warmup_leaf_cycling(sc, 1)
     tr = torch.zeros(16, dtype=torch.int64, device="cuda")
@@ -55,7 +56,7 @@ def main():
         ok = t[:, j] > 0
         if ok.any():
             res[f"t{j}_us"] = float(np.median((t[ok, j] - t[ok, 0]) / 1965.0))
-    print(json.dumps({"config": "c2", "nodes": tree.num_nodes, "phase_end_us_from_start": res}))
+    print(json.dumps({"config": cfg, "nodes": tree.num_nodes, "phase_end_us_from_start": res}))
 
 
 if __name__ == "__main__":

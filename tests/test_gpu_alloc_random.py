@@ -88,3 +88,43 @@ def test_allocation_ten_thousand_random_instances():
             ctx.arbor_sync()
             del ctx
     print(f"a4 random parity: {done} instances on {trees} trees, {infeasible} infeasible")
+
+
+def test_allocation_large_trees_bitonic_path():
+    """Trees above 256 nodes take the allocate kernel's bitonic largest-remainder selection
+    (allocate.cu): bit-exact against the oracle on 24 instances of 257-700 nodes."""
+    rng = np.random.default_rng(77)
+    preset = dict(tree=None, L=1, H=1, Hq=1, d=64, dtype="f32", P=4, rho=0.5, params={},
+                  active=None)
+    done = 0
+    for trial in range(8):
+        N = int(rng.integers(257, 701))
+        tree = _tree(rng, N)
+        n = [int(x) for x in tree.span_len]
+        leaves = synth.leaves_of(tree)
+        d_ = geometry.depths([int(x) for x in tree.parent])
+        pd = dict(alloc_mode="waterfill", n_sinks=0, k_min=int(rng.integers(0, 5)),
+                  l_tail=int(rng.integers(0, 5)), r_min=float(rng.choice([0.0, 0.05])))
+        ctx = workload.make_context(preset, tree, params=make_params(**pd), page_margin=8)
+        K = torch.zeros((1, 1, tree.end_position() + 8, 64), device="cuda")
+        workload.load_tree(ctx, tree, K, K)
+        op = oracle_params(pd)
+        k = torch.full((N,), -1, dtype=torch.int32, device="cuda")
+        for rep in range(3):
+            act = sorted(set(int(x) for x in rng.choice(leaves, size=2)))
+            tree.active = act
+            s = rng.random(N).astype(np.float32)
+            parent = [int(x) for x in tree.parent]
+            dist = geometry.delta(parent, act)
+            ps = geometry.path_star(parent, act)
+            on = [i in ps for i in range(N)]
+            B = int(sum(n) * float(rng.choice([0.3, 0.5, 0.7])))
+            st, k_ref, mf = tae.allocate(0, [float(x) for x in s], d_, dist, on,
+                                         [bool(x) for x in tree.is_open], n, op, B)
+            if st != 0:
+                continue
+            ctx.arbor_allocate(tree, torch.as_tensor(s, device="cuda"), B, k)
+            assert k.cpu().tolist() == k_ref, (trial, rep, N, B)
+            done += 1
+        ctx.arbor_sync()
+    assert done >= 12
