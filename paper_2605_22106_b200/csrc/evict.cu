@@ -427,6 +427,7 @@ select_move_ws_kernel(CompactArgs a) {
     // ---- rank item k from shared memory
     const WorkEnt e = meta(k);
     const bool ident = e.kc == e.n;
+    if (k == 0) EV_TRACE(6);         // item 0's data landed: ranking starts
     const int kc = e.kc, ka = e.ka, n = e.n;
     const int tl = min(a.l_tail, n);
     const int32_t *pgs = Gbuf + (k % 3) * pcap;

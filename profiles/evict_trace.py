@@ -69,6 +69,7 @@ def main():
         "plan_loads_done": pct(np.where(valid[:, 0, 4], rel[:, 0, 4], np.nan)),
         "plan_scans_done": pct(np.where(valid[:, 0, 5], rel[:, 0, 5], np.nan)),
         "plan_done": pct(np.where(valid[:, 0, 1], rel[:, 0, 1], np.nan)),
+        "select_first_rank_start": pct(np.where(valid[:, sel, 6], rel[:, sel, 6], np.nan).ravel()),
         "select_first_job": pct(np.where(valid[:, sel, 2], rel[:, sel, 2], np.nan).ravel()),
         "move_first_job": pct(np.where(valid[:, mov, 2], rel[:, mov, 2], np.nan).ravel()),
         "select_done": pct(np.where(valid[:, sel, 3], rel[:, sel, 3], np.nan).ravel()),
