@@ -51,8 +51,11 @@ namespace {
 #define ARBOR_TC_GROUPS 2
 #endif
 constexpr int kGroups = ARBOR_TC_GROUPS;
-constexpr int kTcThreads = 32 * (6 + 4 * kGroups);   // producer, MMA, 4 epilogue warps (6..9),
-                                                     // softmax groups: warps 2..5, 10..13, 14..17
+// warps: 0 K producer, 1 MMA, 2..5 softmax group 0, 6..9 epilogue, 10.. further softmax
+// groups, last: the V producer (a second TMA-issuing warp: one warp issuing every K, Q and V
+// box of a tile was the C3 tile-rate limit, ~0.6-0.8 µs of issue per tile half)
+constexpr int kVWarp = 6 + 4 * kGroups;
+constexpr int kTcThreads = 32 * (kVWarp + 1);
 constexpr int kHdrRing = 8;                           // epilogue header / column-reduction rings
 constexpr int kTileRows = 128;
 constexpr int kHalf = 64;                       // = kAttnChunk
@@ -379,6 +382,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   // tile k + RING, whose K issue needs MMA1(k + RING − NSK), i.e. MMA2(k) issued, i.e.
   // softmax(k) done; K issue runs < RING tiles ahead of V issue)
   __shared__ TcHdr hdr[RING];
+  // producer progress between the two TMA warps: K issued for tiles < kk_k_pub (their hdr and
+  // vpage written first); V issued for tiles < kk_v_pub (the K producer's ring bound)
+  __shared__ volatile int kk_k_pub, kk_v_pub;
   __shared__ int vpage[RING][kMaxTilePages];
   __shared__ TcHdr ohdr[kHdrRing];                      // tile k's header for the epilogue warps
   // column max / sum of each warp quadrant, ring of kHdrRing tiles (the epilogue warps read
@@ -465,6 +471,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     col_js[n] = j * (a.Lc * a.g.H * a.G) + (n - j * a.qw);
   }
   if (tid == 32) {
+    kk_k_pub = 0;
+    kk_v_pub = 0;
     for (int s = 0; s < NSK; ++s) {
       for (int g = 0; g < kGroups; ++g) {
         mbar_init(&full_k[s][g], 1);
@@ -519,7 +527,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
     unsigned long long wd_t0 = 0;
     int wd_k = -1, wd_v = -1;
 #endif
-    while (kk_v < ntiles) {
+    while (kk_k < ntiles) {
+      kk_v = __shfl_sync(0xffffffffu, kk_v_pub, 0);
 #ifdef ARBOR_MBAR_WATCHDOG
       {
         unsigned long long t;
@@ -628,7 +637,19 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         }
         if (lane == 0) TC_TRACE(k, 2);
         ++kk_k;
+        __syncwarp();
+        __threadfence_block();               // hdr / vpage of tile k before the count
+        if (lane == 0) kk_k_pub = kk_k;
       }
+    }
+  } else if (warp == kVWarp) {
+    // ------------------------------------------------------------- V producer
+    const int ppH = kHalf >> lgP;
+    int kk_v = 0;
+    while (kk_v < ntiles) {
+      const int kk_k = __shfl_sync(0xffffffffu, kk_k_pub, 0);
+      __threadfence_block();                 // the count before the tile's hdr / vpage
+      bool go_v = false;
       if (kk_v < kk_k) {
         const int sv = kk_v % NSV;
         go_v = __shfl_sync(0xffffffffu, mbar_test(&empty_v[sv], ((kk_v / NSV) & 1u) ^ 1u) ? 1 : 0, 0) != 0;
@@ -665,6 +686,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           tma_load_2d(Vs + 16384 + dst, &tmv, 64, row, fvb);
         }
         ++kk_v;
+        __syncwarp();
+        if (lane == 0) kk_v_pub = kk_v;
       }
     }
   } else if (warp == 1) {
@@ -698,7 +721,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           }
         }
 #endif
+#ifdef ARBOR_TC_MMA1_LOCKSTEP   // round-1 behaviour: MMA1 at most kGroups − 1 tiles ahead of MMA2
         if (js < ntiles && js <= jo + kGroups - 1 &&
+#else
+        // MMA1(j) waits only for its data and its S buffer: with the lock step (j ≤ MMA2's
+        // index + 1) softmax(j) could not start before softmax(j − 1) had finished, which
+        // serialised the two groups (round-1 design; the deadlock it was blamed on was the
+        // full-barrier parity aliasing, fixed by the per-(stage, group) barriers)
+        if (js < ntiles &&
+#endif
             mbar_test(&full_k[js % NSK][js % kGroups], (js / LK) & 1u) &&
             (js < kGroups || mbar_test(&s_empty[js % kGroups], ((js - kGroups) / kGroups) & 1u))) {
           const int s = js % NSK, b = js % kGroups;
@@ -1064,8 +1095,10 @@ bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_b
   // (K, V) ring depths; (4, 2) for NQ = 8 / 16 measured the same as (3, 3) on C2
   if (nq <= 8) launch_tc<8, 3, 3>(c, a);
   else if (nq <= 16) launch_tc<16, 3, 3>(c, a);
-#ifdef ARBOR_TC_NQ32_NSK3
+#if defined(ARBOR_TC_NQ32_NSK3)
   else if (nq <= 32) launch_tc<32, 3, 2>(c, a);
+#elif defined(ARBOR_TC_NQ32_NSV3)
+  else if (nq <= 32) launch_tc<32, 2, 3>(c, a);
 #else
   else if (nq <= 32) launch_tc<32, 2, 2>(c, a);
 #endif
