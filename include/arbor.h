@@ -232,7 +232,7 @@ arbor_status arbor_allocate(arbor_ctx *ctx, const arbor_tree *tree, const float 
  * the prefix stay, the i-th dropped slot of the prefix (ascending) receives the i-th kept
  * row from beyond it (ascending); every slot carries its position tag.  The page list is
  * truncated to ⌈k_app/P⌉ and the freed pages pushed on the LIFO free list (nodes
- * ascending).  Pinned nodes are untouched.
+ * ascending, each node's run in descending list order).  Pinned nodes are untouched.
  *  k_target: DEVICE [num_nodes] int32 (e.g. arbor_allocate's k_out)
  *  evicted_tokens_out: HOST, optional (forces a sync): Σ_j (k_cur_j − k_app_j). */
 arbor_status arbor_evict(arbor_ctx *ctx, const arbor_tree *tree, const int32_t *k_target,

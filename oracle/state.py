@@ -240,7 +240,8 @@ class ArborOracle:
         already in slots [0, k_app) stay in place; the i-th hole there (a slot
         whose row was evicted, ascending) receives the i-th retained row from
         slots >= k_app (ascending).  The paper fixes only the retained set
-        (P:171); the slot order is this build's paging choice."""
+        (P:171); the slot order is this build's paging choice.  Freed pages go
+        on the free stack nodes ascending, each node's in descending list order."""
         if A_f32 is None:
             A_f32 = self.A.astype(np.float32)
         A_f32 = np.asarray(A_f32, np.float32)
@@ -285,7 +286,10 @@ class ArborOracle:
                     new[l, h] = row
             self.kept[j] = new
             keep_pages = -(-k_app // self.P)
-            for p in self.pages[j][keep_pages:]:
+            # freed pages pushed in DESCENDING list order (Q23'': the next pops —
+            # LIFO — then return a block's freed run in ascending order, so a rehydrated
+            # node gets consecutive pages: one TMA box per 64-slot half in the attention)
+            for p in reversed(self.pages[j][keep_pages:]):
                 self.free.append(p)
             self.pages[j] = self.pages[j][:keep_pages]
             evicted += kc - k_app

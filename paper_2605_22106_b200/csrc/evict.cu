@@ -11,7 +11,8 @@
 // B200 design:
 //  * evict_plan (1 CTA): decides k_app per node, builds the work list of changed non-pinned
 //    nodes in ascending id, truncates page lists to ⌈k_app/P⌉ and pushes the freed pages on
-//    the LIFO free list in ascending (node, list) order — all on the device, no host sync.
+//    the LIFO free list nodes ascending, each node's run in descending list order — all on
+//    the device, no host sync.
 //  * select (persistent grid, one WARP per (node, row) work item, no block barriers):
 //    pos tags + A keys of the kept slots, the m-th largest unique 48-bit key ⟨A bits, pos⟩
 //    by a warp radix select (8-bit digits, per-warp smem histogram, warp scan) — exact top-m
@@ -168,7 +169,7 @@ select_move_ws_kernel(CompactArgs a) {
   // the changed ones, ascending id, are the work list.  Every CTA derives it from the same
   // unmodified state into its own copy; the last CTA to get there (ticket) applies it —
   // k_cur, page-list truncation to ⌈k_app/P⌉, freed pages pushed on the LIFO free stack in
-  // ascending (node, list) order — after every CTA has read that state.
+  // ascending node order (each node's run descending) — after every CTA has read that state.
   WorkEnt *wl = a.work + static_cast<int64_t>(blockIdx.x) * a.MN;
   {
     // nodes j = i·blockDim + thread, one slice i at a time: the slice's loads in one round
@@ -249,7 +250,8 @@ select_move_ws_kernel(CompactArgs a) {
 #pragma unroll
           for (int t = 0; t < kB; ++t) v[t] = t0 + t < e.nfree ? __ldg(pl + t0 + t) : 0;
 #pragma unroll
-          for (int t = 0; t < kB; ++t) if (t0 + t < e.nfree) dst[t0 + t] = v[t];
+          // descending list order (Q23''): LIFO pops return the run ascending
+          for (int t = 0; t < kB; ++t) if (t0 + t < e.nfree) dst[e.nfree - 1 - (t0 + t)] = v[t];
         }
         a.npages[e.node] = newp;
         a.kcur[e.node] = e.ka;
