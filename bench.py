@@ -556,9 +556,12 @@ def main():
             kc, n, pages = ctx.arbor_read_node(j)
             if kc == n:
                 continue
+            ko = ctx.arbor_read_node_offset(j)
             idx = torch.as_tensor(pages, device=dev, dtype=torch.long)
-            pos = ctx.pos_pool[:, idx].permute(0, 2, 1, 3).reshape(L, Hh, -1)[:, :, :kc]
-            moved = int((pos.long() != torch.arange(kc, device=dev)).sum().item())
+            pos = ctx.pos_pool[:, idx].permute(0, 2, 1, 3).reshape(L, Hh, -1)[:, :, ko:ko + kc]
+            # from full retention the kept window is slots n − k_cur … n − 1 (Q23*): a row
+            # moved iff its position is not its slot
+            moved = int((pos.long() != torch.arange(n - kc, n, device=dev)).sum().item())
             # select, per (row, changed node): pos + A of the k_cur kept slots (2 + 4 B each);
             # move, per moved row: K and V read + write (4·rb) and its pos tag (2 + 2 B)
             byts["select"] += L * Hh * 6 * n

@@ -228,19 +228,22 @@ arbor_status arbor_allocate(arbor_ctx *ctx, const arbor_tree *tree, const float 
  * k_cur_j, and every row (l, h): keep the last min(L_tail, n_j) positions, plus the top
  * (k_app − tail) currently kept positions by the key ⟨f32 A, position⟩ (descending, Q3);
  * if k_app ≤ tail keep the last k_app.  Kept K/V/pos rows are compacted in place into
- * the node's slot prefix [0, k_app) by hole filling (Q23'): kept rows already in
- * the prefix stay, the i-th dropped slot of the prefix (ascending) receives the i-th kept
- * row from beyond it (ascending); every slot carries its position tag.  The page list is
- * truncated to ⌈k_app/P⌉ and the freed pages pushed on the LIFO free list (nodes
- * ascending, each node's run in descending list order).  Pinned nodes are untouched.
+ * the LAST k_app of the node's k_cur valid slots (end-window hole filling, Q23*:
+ * the always-kept tail already sits there): kept rows inside the window stay, the i-th
+ * dropped slot of the window (ascending) receives the i-th kept row from before it
+ * (ascending); every slot carries its position tag.  The window starts at page-list slot
+ * c = first_slot + k_cur − k_app: the ⌊c/P⌋ leading pages are freed (all of them when
+ * k_app = 0) and first_slot becomes c mod P (see arbor_read_node_offset); freed pages are
+ * pushed on the LIFO free list nodes ascending, each node's run in descending list order.
+ * Pinned nodes are untouched.
  *  k_target: DEVICE [num_nodes] int32 (e.g. arbor_allocate's k_out)
  *  evicted_tokens_out: HOST, optional (forces a sync): Σ_j (k_cur_j − k_app_j). */
 arbor_status arbor_evict(arbor_ctx *ctx, const arbor_tree *tree, const int32_t *k_target,
                          int64_t *evicted_tokens_out);
 
 /* a7/a8 — lazy rehydration (Alg. 2).  For each listed closed
- * node with k_cur < n (ascending id, duplicates ignored): pop ⌈n/P⌉ − #pages pages and
- * copy the node's full K/V back from the pinned host stash (bit-exact, Q20); pos = identity,
+ * node with k_cur < n (ascending id, duplicates ignored): keep its live pages (first_slot
+ * becomes 0), pop ⌈n/P⌉ − #pages more and copy the node's full K/V back from the pinned host stash (bit-exact, Q20); pos = identity,
  * k_cur = n, rehydrations += 1.  Full nodes are a no-op and are not counted.  Listing an
  * open node is ARBOR_ERR_STATE.  nodes: HOST [count] int32.
  * ARBOR_ERR_OUT_OF_PAGES is returned (state unchanged) if the pool cannot hold the worst
@@ -336,9 +339,14 @@ arbor_status arbor_fit_theta(const float *phi, const float *target, int32_t n, i
 
 /* ---- inspection / plumbing ------------------------------------------------------------ */
 arbor_status arbor_sync(arbor_ctx *ctx);   /* wait for both streams; returns latched errors */
-/* HOST outs (sync): the node's k_cur, n, and page list (pages may be NULL; *num_pages in). */
+/* HOST outs (sync): the node's k_cur, n, and live page list (pages may be NULL;
+ * *num_pages in: capacity, out: ⌈(first_slot + k_cur)/P⌉ pages). */
 arbor_status arbor_read_node(arbor_ctx *ctx, int32_t node, int32_t *k_cur, int32_t *n,
                              int32_t *pages, int32_t *num_pages);
+/* HOST out (sync): first_slot ∈ [0, P), the slot of the node's live page list that holds
+ * its valid slot 0 (valid slots: first_slot … first_slot + k_cur − 1 of the live list;
+ * 0 until an eviction, Q23*). */
+arbor_status arbor_read_node_offset(arbor_ctx *ctx, int32_t node, int32_t *first_slot);
 /* HOST out (sync): free stack bottom→top into `pages` (capacity *count in, size out). */
 arbor_status arbor_read_free_list(arbor_ctx *ctx, int32_t *pages, int32_t *count);
 /* HOST outs (sync), each [num_nodes] or NULL: all-reduced Mass_i, Mclose_i (this rank's

@@ -12,7 +12,7 @@ K/V are never moved here: compaction is token-extractive and rehydration
 restores "the same conditioning state as full retention", so the
 content of any retained slot is the original K/V at its absolute position.
 The oracle therefore tracks, per (row, node), the within-node offset held by
-each slot (slot order: DESIGN.md reading Q23'), plus the per-node page lists
+each slot (slot order: DESIGN.md reading Q23*), plus the per-node page lists
 and the LIFO free stack of the paged layout (§8(c).1 step 8).
 """
 from __future__ import annotations
@@ -73,7 +73,8 @@ class ArborOracle:
         del Hg
         self.span_start, self.n, self.open = [], [], []
         self.kept = []            # per node: int64 [L][H][k_cur] offset held by each slot
-        self.pages = []           # per node: list of page ids
+        self.pages = []           # per node: list of live page ids
+        self.koff = []            # per node: page-list slot of valid slot 0 (0 <= koff < P, Q23*)
         self.free = list(range(num_pages - 1, -1, -1))   # LIFO, top at the end
         self.A = np.zeros((self.L, self.H, self.Tmax), dtype=np.float64)
         self.Nq, self.Mclose, self.s_last = [], [], []
@@ -97,6 +98,7 @@ class ArborOracle:
         self.open.append(True)
         self.kept.append(np.zeros((self.L, self.H, 0), dtype=np.int64))
         self.pages.append([])
+        self.koff.append(0)
         self.Nq.append(0)
         self.Mclose.append(0)
         self.s_last.append(0.5)          # never scored (Q31)
@@ -232,16 +234,19 @@ class ArborOracle:
     def evict(self, tree, k_target, A_f32=None) -> int:
         """Select + compact every non-pinned closed node whose applied target
         k_app = min(k_cur, k_target) drops (Alg. 2 P:567 'evict only if
-        k_new < k', Q17), nodes ascending; freed pages pushed in ascending
-        list order.  A_f32: the f32 accumulated attention that orders heavy
-        hitters (default: the oracle's own A rounded to f32).
+        k_new < k', Q17), nodes ascending.  A_f32: the f32 accumulated attention that
+        orders heavy hitters (default: the oracle's own A rounded to f32).
 
-        Slot layout after eviction (reading Q23'): retained rows
-        already in slots [0, k_app) stay in place; the i-th hole there (a slot
-        whose row was evicted, ascending) receives the i-th retained row from
-        slots >= k_app (ascending).  The paper fixes only the retained set
-        (P:171); the slot order is this build's paging choice.  Freed pages go
-        on the free stack nodes ascending, each node's in descending list order."""
+        Slot layout after eviction (reading Q23*, end-window hole filling): the
+        new block is the LAST k_app of the k_cur valid slots, w = k_cur − k_app onward —
+        where the block tail 𝒯 (always kept) already sits.  Retained rows inside
+        the window stay in place; the i-th hole there (a slot whose row was evicted,
+        ascending) receives the i-th retained row from slots < w (ascending).  The window
+        starts at page-list slot c = koff + w: the ⌊c/P⌋ leading pages are freed and
+        koff ← c mod P (k_app = 0 frees every page, koff ← 0).  The paper fixes only the
+        retained set; the slot order is this build's paging choice.  Freed
+        pages go on the free stack nodes ascending, each node's run in descending list
+        order."""
         if A_f32 is None:
             A_f32 = self.A.astype(np.float32)
         A_f32 = np.asarray(A_f32, np.float32)
@@ -268,6 +273,7 @@ class ArborOracle:
             if k_app == kc:
                 continue
             a, n = self.span_start[j], self.n[j]
+            w = kc - k_app                        # first slot of the kept window
             new = np.zeros((self.L, self.H, k_app), dtype=np.int64)
             for l in range(self.L):
                 for h in range(self.H):
@@ -277,21 +283,24 @@ class ArborOracle:
                                                 self.params.get("select_mode", select.HEAVY),
                                                 self.params["n_sinks"],
                                                 is_root=int(tree.parent[j]) < 0))
-                    holes = [s for s in range(k_app) if old[s] not in R]
-                    movers = [old[s] for s in range(k_app, kc) if old[s] in R]
+                    holes = [s for s in range(w, kc) if old[s] not in R]
+                    movers = [old[s] for s in range(w) if old[s] in R]
                     assert len(holes) == len(movers)
-                    row = old[:k_app]
+                    row = old[w:kc]
                     for hs, mv in zip(holes, movers):
-                        row[hs] = mv
+                        row[hs - w] = mv
                     new[l, h] = row
             self.kept[j] = new
-            keep_pages = -(-k_app // self.P)
-            # freed pages pushed in DESCENDING list order (Q23'': the next pops —
-            # LIFO — then return a block's freed run in ascending order, so a rehydrated
-            # node gets consecutive pages: one TMA box per 64-slot half in the attention)
-            for p in reversed(self.pages[j][keep_pages:]):
+            if k_app > 0:
+                c = self.koff[j] + w
+                drop = c // self.P
+                self.koff[j] = c % self.P
+            else:
+                drop = len(self.pages[j])
+                self.koff[j] = 0
+            for p in reversed(self.pages[j][:drop]):
                 self.free.append(p)
-            self.pages[j] = self.pages[j][:keep_pages]
+            self.pages[j] = self.pages[j][drop:]
             evicted += kc - k_app
         return evicted
 
@@ -299,8 +308,9 @@ class ArborOracle:
     def rehydrate(self, nodes) -> int:
         """Lazy rehydration (Alg. 2): a node with
         k_cur < n gets its full span back (bit-exact copy of the stash, Q20);
-        pages popped in ascending node order; full nodes are a no-op and are
-        not counted."""
+        pages popped in ascending node order (appended to the node's live
+        list, which then holds slots 0.. from its first page: koff = 0); full
+        nodes are a no-op and are not counted."""
         nodes = sorted(set(int(x) for x in nodes))
         for i in nodes:
             if self.open[i]:
@@ -315,6 +325,7 @@ class ArborOracle:
             need = -(-n // self.P) - len(self.pages[i])
             for _ in range(need):
                 self.pages[i].append(self._pop())
+            self.koff[i] = 0
             self.kept[i] = np.broadcast_to(np.arange(n, dtype=np.int64),
                                            (self.L, self.H, n)).copy()
             count += 1
@@ -327,4 +338,5 @@ class ArborOracle:
         return int(self.kept[i][l, h, slot])
 
     def page_of_slot(self, i: int, slot: int) -> tuple:
-        return self.pages[i][slot // self.P], slot % self.P
+        c = self.koff[i] + slot
+        return self.pages[i][c // self.P], c % self.P

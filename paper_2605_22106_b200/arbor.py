@@ -14,7 +14,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libarbor.so")
+# ARBOR_LIB: A/B experiments only (profiles/, tools/) — the default is the in-tree build
+LIB_PATH = os.environ.get("ARBOR_LIB") or os.path.join(_HERE, "libarbor.so")
 
 ARBOR_OK = 0
 STATUS = {0: "OK", 2: "INVALID_ARG", 3: "INFEASIBLE_BUDGET", 4: "INVARIANT", 5: "IO",
@@ -98,6 +99,7 @@ def load_library(path: str = LIB_PATH):
         "arbor_decode_step": ([P, C.POINTER(ArborTree), P, P, P, P], I32),
         "arbor_sync": ([P], I32),
         "arbor_read_node": ([P, I32, P, P, P, P], I32),
+        "arbor_read_node_offset": ([P, I32, C.POINTER(C.c_int32)], I32),
         "arbor_read_free_list": ([P, P, P], I32),
         "arbor_read_scores": ([P, I32, P, P, P, P, P], I32),
         "arbor_read_counters": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], I32),
@@ -402,6 +404,13 @@ class ArborKV:
         self._check(self.lib.arbor_read_node(self._ctx, int(node), None, None, pages.ctypes.data,
                                              C.byref(cnt)), "arbor_read_node")
         return int(kc.value), int(n.value), pages[:cnt.value].tolist()
+
+    def arbor_read_node_offset(self, node: int) -> int:
+        """Slot of the node's live page list holding its valid slot 0 (Q23*)."""
+        v = C.c_int32(0)
+        self._check(self.lib.arbor_read_node_offset(self._ctx, int(node), C.byref(v)),
+                    "arbor_read_node_offset")
+        return int(v.value)
 
     def arbor_read_free_list(self):
         cnt = C.c_int32(0)

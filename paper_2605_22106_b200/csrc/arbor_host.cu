@@ -536,10 +536,12 @@ arbor_status sync_all(arbor_ctx *c) {
 }
 
 __global__ void init_node_kernel(int node, int64_t span, int32_t *n, int32_t *kcur, int32_t *npages,
-                                 int64_t *span_arr, int64_t *mclose, float *s, float *a) {
+                                 int32_t *soff, int64_t *span_arr, int64_t *mclose, float *s,
+                                 float *a) {
   n[node] = 0;
   kcur[node] = 0;
   npages[node] = 0;
+  soff[node] = 0;
   span_arr[node] = span;
   mclose[node] = 0;
   s[node] = 0.5f;
@@ -696,7 +698,7 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   DevState &d = c->d;
   arbor_status s = ARBOR_OK;
 #define ALLOC(ptr, cnt) do { s = dmalloc(c, &(ptr), (cnt)); if (s != ARBOR_OK) return bail(s); } while (0)
-  ALLOC(d.n, MN); ALLOC(d.kcur, MN); ALLOC(d.npages, MN);
+  ALLOC(d.n, MN); ALLOC(d.kcur, MN); ALLOC(d.npages, MN); ALLOC(d.soff, MN);
   ALLOC(d.ptab, static_cast<size_t>(MN) * c->max_pages_node);
   ALLOC(d.free_stack, c->NP);
   ALLOC(d.span, MN); ALLOC(d.mass2, 2 * MN); ALLOC(d.mclose, MN); ALLOC(d.nq, MN);
@@ -802,7 +804,7 @@ void arbor_destroy(arbor_ctx *c) {
   DevState &d = c->d;
   if (c->unc_part) cudaFree(c->unc_part);
   if (c->unc_ticket) cudaFree(c->unc_ticket);
-  void *ptrs[] = {d.n, d.kcur, d.npages, d.ptab, d.free_stack, d.span, d.mass2, d.mclose, d.nq,
+  void *ptrs[] = {d.n, d.kcur, d.npages, d.soff, d.ptab, d.free_stack, d.span, d.mass2, d.mclose, d.nq,
                   d.a, d.s, d.ctrl, d.parent, d.onpath, d.pinned, d.depth, d.delta, d.Ed, d.ED,
                   d.work, d.rehyd_nodes, d.rehyd_flag, d.seg,
                   d.partials, d.lse_scratch, d.out_scratch, d.zbuf, d.mass_part, d.mass_scratch,
@@ -810,7 +812,7 @@ void arbor_destroy(arbor_ctx *c) {
   for (void *p : ptrs) if (p) cudaFree(p);
   for (auto &sn : c->snap) {
     if (!sn.valid) continue;
-    void *sp[] = {sn.n, sn.kcur, sn.npages, sn.ptab, sn.free_stack, sn.mclose, sn.nq_dev, sn.s, sn.ctrl,
+    void *sp[] = {sn.n, sn.kcur, sn.npages, sn.soff, sn.ptab, sn.free_stack, sn.mclose, sn.nq_dev, sn.s, sn.ctrl,
                   sn.mass_part};
     for (void *p : sp) if (p) cudaFree(p);
   }
@@ -843,7 +845,7 @@ arbor_status arbor_open_node(arbor_ctx *c, int32_t node, int64_t span_start) {
   for (int j = 0; j < c->num_known; ++j)
     if (span_start >= c->h_span[j] && span_start < c->h_span[j] + c->h_n[j])
       return fail(c, ARBOR_ERR_INVALID_ARG, "span_start lies inside node " + std::to_string(j) + "'s span");
-  init_node_kernel<<<1, 1, 0, c->ms>>>(node, span_start, c->d.n, c->d.kcur, c->d.npages, c->d.span,
+  init_node_kernel<<<1, 1, 0, c->ms>>>(node, span_start, c->d.n, c->d.kcur, c->d.npages, c->d.soff, c->d.span,
                                        c->d.mclose, c->d.s, c->d.a);
   ARBOR_LAUNCHED(c);
   CK_LAUNCH();
@@ -1325,19 +1327,32 @@ arbor_status arbor_read_node(arbor_ctx *c, int32_t node, int32_t *k_cur, int32_t
   if (!c) return ARBOR_ERR_INVALID_ARG;
   if (node < 0 || node >= c->num_known) return fail(c, ARBOR_ERR_INVALID_ARG, "unknown node");
   TRY(sync_all(c));
-  int32_t kc = 0, nn = 0, np = 0;
+  int32_t kc = 0, nn = 0, np = 0, so = 0;
   CK(cudaMemcpy(&kc, c->d.kcur + node, 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(&nn, c->d.n + node, 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(&np, c->d.npages + node, 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&so, c->d.soff + node, 4, cudaMemcpyDeviceToHost));
+  const int first = so / c->P;   // pages before it were freed by an eviction (Q23*)
+  np -= first;
   if (k_cur) *k_cur = kc;
   if (n) *n = nn;
   if (num_pages) {
     if (pages) {
       if (*num_pages < np) return fail(c, ARBOR_ERR_INVALID_ARG, "pages buffer too small");
-      if (np) CK(cudaMemcpy(pages, c->d.ptab + static_cast<int64_t>(node) * c->max_pages_node, np * 4, cudaMemcpyDeviceToHost));
+      if (np) CK(cudaMemcpy(pages, c->d.ptab + static_cast<int64_t>(node) * c->max_pages_node + first, np * 4, cudaMemcpyDeviceToHost));
     }
     *num_pages = np;
   }
+  return ARBOR_OK;
+}
+
+arbor_status arbor_read_node_offset(arbor_ctx *c, int32_t node, int32_t *first_slot) {
+  if (!c || !first_slot) return ARBOR_ERR_INVALID_ARG;
+  if (node < 0 || node >= c->num_known) return fail(c, ARBOR_ERR_INVALID_ARG, "unknown node");
+  TRY(sync_all(c));
+  int32_t so = 0;
+  CK(cudaMemcpy(&so, c->d.soff + node, 4, cudaMemcpyDeviceToHost));
+  *first_slot = so % c->P;
   return ARBOR_OK;
 }
 
@@ -1412,6 +1427,7 @@ arbor_status arbor_save_state(arbor_ctx *c, int32_t slot) {
   const size_t MN = c->max_nodes, PT = MN * c->max_pages_node;
   if (!sn.valid) {
     CK(cudaMalloc(&sn.n, MN * 4)); CK(cudaMalloc(&sn.kcur, MN * 4)); CK(cudaMalloc(&sn.npages, MN * 4));
+    CK(cudaMalloc(&sn.soff, MN * 4));
     CK(cudaMalloc(&sn.ptab, PT * 4)); CK(cudaMalloc(&sn.free_stack, c->NP * 4));
     CK(cudaMalloc(&sn.mclose, MN * 8)); CK(cudaMalloc(&sn.nq_dev, MN * 8)); CK(cudaMalloc(&sn.s, MN * 4));
     CK(cudaMalloc(&sn.mass_part, MN * 8));
@@ -1423,6 +1439,7 @@ arbor_status arbor_save_state(arbor_ctx *c, int32_t slot) {
     return cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToDevice, c->ms);
   };
   CK(cp(sn.n, c->d.n, MN * 4)); CK(cp(sn.kcur, c->d.kcur, MN * 4)); CK(cp(sn.npages, c->d.npages, MN * 4));
+  CK(cp(sn.soff, c->d.soff, MN * 4));
   CK(cp(sn.ptab, c->d.ptab, PT * 4)); CK(cp(sn.free_stack, c->d.free_stack, c->NP * 4));
   CK(cp(sn.mclose, c->d.mclose, MN * 8)); CK(cp(sn.s, c->d.s, MN * 4)); CK(cp(sn.ctrl, c->d.ctrl, sizeof(Ctrl)));
   CK(cp(sn.mass_part, c->d.mass_part, MN * 8));
@@ -1441,6 +1458,7 @@ arbor_status arbor_load_state(arbor_ctx *c, int32_t slot) {
     return cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToDevice, c->ms);
   };
   CK(cp(c->d.n, sn.n, MN * 4)); CK(cp(c->d.kcur, sn.kcur, MN * 4)); CK(cp(c->d.npages, sn.npages, MN * 4));
+  CK(cp(c->d.soff, sn.soff, MN * 4));
   CK(cp(c->d.ptab, sn.ptab, PT * 4)); CK(cp(c->d.free_stack, sn.free_stack, c->NP * 4));
   CK(cp(c->d.mclose, sn.mclose, MN * 8)); CK(cp(c->d.s, sn.s, MN * 4)); CK(cp(c->d.ctrl, sn.ctrl, sizeof(Ctrl)));
   CK(cp(c->d.mass_part, sn.mass_part, MN * 8));

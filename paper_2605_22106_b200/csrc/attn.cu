@@ -38,7 +38,7 @@ struct StreamArgs {
   PlanView pv;
   PoolView g;
   const void *kpool, *vpool;
-  const int32_t *ptab, *kcur;
+  const int32_t *ptab, *kcur, *soff;
   const void *q;
   float *partials;   // [pair][Lc][H][G][D+2]
   float *zbuf;       // [pair][Lc][H][G][kCh] log2-domain logits
@@ -47,7 +47,7 @@ struct StreamArgs {
 };
 
 struct StageHdr {
-  int nt, li, h, pbase, cnt, pad0, pad1, pad2;
+  int nt, li, h, pbase, cnt, lo, pad1, pad2;   // valid slots of the chunk: [lo, nt)
 };
 
 template <typename T>
@@ -118,12 +118,13 @@ attn_stream_kernel(StreamArgs a) {
     const T *vpool = static_cast<const T *>(a.vpool);
     const int lgP = 31 - __clz(a.g.P);
     const int pages_per_item = a.g.P >= kCh ? 1 : kCh / a.g.P;
-    struct Meta { int4 rec; int kc, page, b; };
+    struct Meta { int4 rec; int kc, so, page, b; };
     auto fetch = [&](int it, Meta &m) {
       if (it >= total) return;
       const int item = it / (a.g.H * a.Lc);
       m.rec = a.pv.it_rec[item];
       m.kc = a.kcur[m.rec.x];
+      m.so = a.soff[m.rec.x];
       m.page = lane < pages_per_item
                    ? a.ptab[static_cast<int64_t>(m.rec.x) * a.g.MPN + (m.rec.y >> lgP) + lane] : 0;
       m.b = lane < m.rec.w ? a.pv.pair_b[m.rec.z + lane] : 0;
@@ -139,13 +140,16 @@ attn_stream_kernel(StreamArgs a) {
       const int li = (it / a.g.H) % a.Lc;
       const int node = cur.rec.x, c0 = cur.rec.y, pbase = cur.rec.z, cnt = cur.rec.w;
       (void)node;
-      const int nt = max(0, min(kCh, cur.kc - c0));
+      // rows [0, hi) of the chunk are loaded, those below lo (stale pages before soff,
+      // DESIGN.md Q23*) masked
+      const int span = chunk_span(cur.so, cur.kc, c0, kCh);
+      const int nt = span_hi(span), lo = span_lo(span);
       mbar_wait(&empty[st], ph ^ 1u);
       T *Ks = stage0 + st * stage_elems;
       T *Vs = Ks + kCh * D;
       T *Qs = Vs + kCh * D;
       if (lane == 0) {
-        hdr[st] = StageHdr{nt, li, h, pbase, cnt, 0, 0, 0};
+        hdr[st] = StageHdr{nt, li, h, pbase, cnt, lo, 0, 0};
         mbar_arrive_expect_tx(&full[st], static_cast<uint32_t>((2 * nt + cnt * G) * rb));
       }
       __syncwarp();
@@ -176,7 +180,7 @@ attn_stream_kernel(StreamArgs a) {
     const uint32_t ph = (k / kNst) & 1u;
     mbar_wait(&full[st], ph);
     const StageHdr hd = hdr[st];
-    const int nt = hd.nt, li = hd.li, h = hd.h, cnt = hd.cnt, pbase = hd.pbase;
+    const int nt = hd.nt, lo = hd.lo, li = hd.li, h = hd.h, cnt = hd.cnt, pbase = hd.pbase;
     const T *Ks = stage0 + st * stage_elems;
     const T *Vs = Ks + kCh * D;
     const T *Qs = Vs + kCh * D;
@@ -200,7 +204,7 @@ attn_stream_kernel(StreamArgs a) {
           for (int t0 = 0; t0 < kCh; t0 += TPP) {
             const int t = t0 + tt;
             float dot[4] = {0.f, 0.f, 0.f, 0.f};
-            if (t < nt) {
+            if (t >= lo && t < nt) {
               float kf[16];
               load16<T>(Ks + t * D + sl * 16, kf);
 #pragma unroll
@@ -220,7 +224,7 @@ attn_stream_kernel(StreamArgs a) {
 #pragma unroll
               for (int qi = 0; qi < 4; ++qi)
                 if (q0 + qi < QB)
-                  zs[t * QB + q0 + qi] = (t < nt && q0 + qi < nq) ? dot[qi] * a.scale_log2 : -INFINITY;
+                  zs[t * QB + q0 + qi] = (t >= lo && t < nt && q0 + qi < nq) ? dot[qi] * a.scale_log2 : -INFINITY;
             }
           }
         }
@@ -265,7 +269,7 @@ attn_stream_kernel(StreamArgs a) {
         float acc[QB][4];
 #pragma unroll
         for (int qi = 0; qi < QB; ++qi) acc[qi][0] = acc[qi][1] = acc[qi][2] = acc[qi][3] = 0.f;
-        for (int t = tg; t < nt; t += TG) {
+        for (int t = lo + tg; t < nt; t += TG) {   // rows below lo: not the node's (Q23*)
           float vf[4];
           load4<T>(Vs + t * D + e4 * 4, vf);
           float p[QB];
@@ -412,6 +416,7 @@ bool launch_attn_partial(arbor_ctx *c, const PlanView &pv, const void *q, int la
   a.vpool = c->cfg.v_pool;
   a.ptab = c->d.ptab;
   a.kcur = c->d.kcur;
+  a.soff = c->d.soff;
   a.q = q;
   a.partials = c->d.partials;
   a.zbuf = c->d.zbuf;

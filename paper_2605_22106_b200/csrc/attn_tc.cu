@@ -68,7 +68,7 @@ static_assert(kAttnChunk == kHalf, "a tensor-core tile is two score/attention ch
 struct TcArgs {
   PlanView pv;
   PoolView g;
-  const int32_t *ptab, *kcur;
+  const int32_t *ptab, *kcur, *soff;
   const __nv_bfloat16 *q;
   float *partials, *zbuf;
   __nv_bfloat16 *out;              // merged output [nA][Lc][Hq][128] and LSE [nA][Lc][Hq]
@@ -88,7 +88,8 @@ struct TcArgs {
   } while (0)
 
 // cnt: leaves (8-column query slots) of the tile; meta: bit 0 a B half exists, bit 1 the B
-// half is packed (another node's chunk with its own columns [8·cntA, 8·cnt)), bits 4+: cntA
+// half is packed (another node's chunk with its own columns [8·cntA, 8·cnt)), bits 4+: cntA;
+// ntA / ntB: the half's valid slots [lo, hi) as chunk_span packs them (common.cuh)
 struct TcHdr {
   int ntA, ntB, li, h, pbA, pbB, cnt, meta;
 };
@@ -436,11 +437,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   auto load_state = [&](int k0) {
     const int kk = k0 + lane;
     if (kk < ntiles) {
-      const int kc = a.kcur[b_node];
-      const int kcB = b_nodeB < 0 ? 0 : (b_nodeB == b_node ? kc : a.kcur[b_nodeB]);
-      b_ntA = max(0, min(kHalf, kc - b_c0));
-      b_ntB = b_nodeB >= 0 ? max(0, min(kHalf, kcB - b_c0B)) : 0;
-      const int pgA = (b_ntA + P - 1) >> lgP, pgB = (b_ntB + P - 1) >> lgP;
+      const int kc = a.kcur[b_node], so = a.soff[b_node];
+      const bool same = b_nodeB == b_node;
+      const int kcB = b_nodeB < 0 ? 0 : (same ? kc : a.kcur[b_nodeB]);
+      const int soB = b_nodeB < 0 ? 0 : (same ? so : a.soff[b_nodeB]);
+      // a half's pages are loaded from its first page up to the one holding slot hi − 1;
+      // the slots below lo (stale pages before soff, Q23*) are masked, not skipped
+      b_ntA = chunk_span(so, kc, b_c0, kHalf);
+      b_ntB = b_nodeB >= 0 ? chunk_span(soB, kcB, b_c0B, kHalf) : 0;
+      const int pgA = (span_hi(b_ntA) + P - 1) >> lgP, pgB = (span_hi(b_ntB) + P - 1) >> lgP;
       const int ppH = kHalf >> lgP;   // pages per 64-slot half
       const int32_t *ptA = a.ptab + static_cast<int64_t>(b_node) * a.g.MPN + (b_c0 >> lgP);
       const int32_t *ptB = a.ptab + static_cast<int64_t>(b_nodeB < 0 ? 0 : b_nodeB) * a.g.MPN + (b_c0B >> lgP);
@@ -591,7 +596,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         }
         const int it = blockIdx.x + k * gridDim.x;
         const int li = (it / a.g.H) % a.Lc, h = it % a.g.H;
-        const int pgA = (ntA + P - 1) >> lgP, pgB = (ntB + P - 1) >> lgP;
+        const int pgA = (span_hi(ntA) + P - 1) >> lgP, pgB = (span_hi(ntB) + P - 1) >> lgP;
         const int s = k % NSK, r = k % RING;
         uint64_t *fkb = &full_k[s][k % kGroups];
         if (lane == 0) { TC_TRACE(k, 0); TC_TRACE(k, 1); }
@@ -659,7 +664,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
         const int s = k % NSV, r = k % RING;
         const TcHdr hd = hdr[r];
         const int page = lane < kMaxTilePages ? vpage[r][lane] : 0;
-        const int pgA = (hd.ntA + P - 1) >> lgP, pgB = (hd.ntB + P - 1) >> lgP;
+        const int pgA = (span_hi(hd.ntA) + P - 1) >> lgP, pgB = (span_hi(hd.ntB) + P - 1) >> lgP;
         unsigned char *Vs = Vst(s);
         uint64_t *fvb = &full_v[s][k % kGroups];
         if (lane == 0) mbar_arrive_expect_tx(fvb, static_cast<uint32_t>(pgA + pgB) * P * 256u);
@@ -807,7 +812,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       const int nt = half ? hd.ntB : hd.ntA;
       const bool present = half == 0 || (hd.meta & 1);
       const int pb = half ? hd.pbB : hd.pbA;
-      const bool valid = present && tc < nt;
+      const bool valid = present && tc >= span_lo(nt) && tc < span_hi(nt);
       const int ngrp = (min(NQ, qw * hd.cnt) + GW - 1) / GW;
       mbar_wait(&s_full[b], ph);
       if (tid == 64) TC_TRACE(k, 8);
@@ -862,17 +867,21 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
       }
       tc_fence_before();
       mbar_arrive(&s_empty[b]);             // S of this buffer has been read
-      // V rows of a partly filled last page hold pool bytes past k_cur: zero them so that
-      // 0 · v stays 0 in Oᵀ = Vᵀ·Pᵀ (the rows past the last page were zeroed before)
-      // V of this stage has landed (MMA2 needs it anyway; P is only published after)
+      // V rows of a partly filled last page hold pool bytes past k_cur, and the rows below
+      // lo (the pages before soff and the first live page's slots before it, Q23*) bytes the
+      // node no longer owns: zero them so that 0 · v stays 0 in Oᵀ = Vᵀ·Pᵀ (the rows past the
+      // last page were zeroed before).  V of this stage has landed (MMA2 needs it anyway; P
+      // is only published after)
       const int sv = k % NSV;
       mbar_wait(&full_v[sv][grp], (k / LV) & 1u);
-      if (present && (nt & (P - 1))) {
-        const int r0 = nt, r1 = (nt + P - 1) & ~(P - 1);
+      const int hi = span_hi(nt), lo = span_lo(nt);
+      if (present && ((hi & (P - 1)) || lo)) {
+        const int r0 = hi, r1 = (hi + P - 1) & ~(P - 1);
         unsigned char *Vs = Vst(sv);
         const int tl = trow - half * 64;   // 0..63 within the half
-        for (int idx = tl; idx < (r1 - r0) * 16; idx += 64) {
-          const int r = half * kHalf + r0 + (idx >> 4), c16 = idx & 15;
+        for (int idx = tl; idx < (r1 - r0 + lo) * 16; idx += 64) {
+          const int rr = idx >> 4;
+          const int r = half * kHalf + (rr < lo ? rr : r0 + rr - lo), c16 = idx & 15;
           *reinterpret_cast<uint4 *>(Vs + (c16 >> 3) * 16384 + r * 128 + (c16 & 7) * 16) =
               make_uint4(0, 0, 0, 0);
         }
@@ -1072,6 +1081,7 @@ bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_b
   a.g = PoolView{c->L, c->H, c->P, c->D, c->NP, c->max_pages_node, c->max_tokens};
   a.ptab = c->d.ptab;
   a.kcur = c->d.kcur;
+  a.soff = c->d.soff;
   a.q = static_cast<const __nv_bfloat16 *>(q);
   a.partials = c->d.partials;
   a.zbuf = c->d.zbuf;

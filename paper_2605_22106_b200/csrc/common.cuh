@@ -56,9 +56,21 @@ struct Ctrl {
 struct __align__(16) WorkEnt {
   int32_t node, kc, ka, n;   // node id, k_cur before, k_app after, n_i
   int64_t span;              // a_i (absolute position of the node's first token)
-  int32_t foff, nfree;       // offset of its freed pages among all freed pages; their count
+  int32_t foff;              // offset of its freed pages among all freed pages
+  int16_t nfree, so;         // their count (≤ max_pages_node); soff before (< 2^15: int16 pos tags bound n)
 };
 constexpr int kEvictCtasPerSm = 2;   // the fused evict kernel's work-list copies: [SMs·2][max_nodes]
+
+// Valid slots of the chunk [c0, c0 + len) of a node's page list whose valid slots are
+// [soff, soff + k_cur) (Q23*): [lo, hi) relative to c0, packed hi | lo << 8
+// (len ≤ 255), 0 when the chunk holds none.
+__host__ __device__ __forceinline__ int chunk_span(int soff, int kc, int c0, int len) {
+  const int hi = min(len, max(0, soff + kc - c0));
+  const int lo = min(len, max(0, soff - c0));
+  return lo < hi ? (hi | (lo << 8)) : 0;
+}
+__host__ __device__ __forceinline__ int span_hi(int sp) { return sp & 255; }
+__host__ __device__ __forceinline__ int span_lo(int sp) { return sp >> 8; }
 
 // Per-launch geometry of the K/V pools
 struct PoolGeom {
@@ -68,6 +80,9 @@ struct PoolGeom {
 
 struct DevState {
   int32_t *n, *kcur, *npages, *ptab, *free_stack;
+  // soff: page-list slot of valid slot 0 (Q23*): the node's valid slots are
+  // [soff, soff + k_cur) of its page list; entries below soff / P are freed (stale)
+  int32_t *soff;
   int64_t *span;             // a_i
   int64_t *mass2;            // [2*max_nodes]: mass partial | mclose partial → all-reduced
   int64_t *mclose;           // this rank's Mclose partial
@@ -129,7 +144,7 @@ struct PoolView {
 
 struct Snapshot {
   bool valid = false;
-  int32_t *n, *kcur, *npages, *ptab, *free_stack;
+  int32_t *n, *kcur, *npages, *ptab, *free_stack, *soff;
   int64_t *mclose, *nq_dev, *mass_part;
   float *s;
   bool mass_valid = true;

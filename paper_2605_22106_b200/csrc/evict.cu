@@ -10,15 +10,16 @@
 //
 // B200 design:
 //  * evict_plan (1 CTA): decides k_app per node, builds the work list of changed non-pinned
-//    nodes in ascending id, truncates page lists to ⌈k_app/P⌉ and pushes the freed pages on
-//    the LIFO free list nodes ascending, each node's run in descending list order — all on
-//    the device, no host sync.
+//    nodes in ascending id, frees the leading pages before the kept window (soff moves up,
+//    DESIGN.md Q23*) and pushes them on the LIFO free list nodes ascending, each node's run
+//    in descending list order — all on the device, no host sync.
 //  * select (persistent grid, one WARP per (node, row) work item, no block barriers):
 //    pos tags + A keys of the kept slots, the m-th largest unique 48-bit key ⟨A bits, pos⟩
 //    by a warp radix select (8-bit digits, per-warp smem histogram, warp scan) — exact top-m
-//    membership in O(c) — then hole-filling: kept rows inside the new prefix [0, k_app)
-//    stay, the i-th hole takes the i-th kept row from beyond it (Q23').  Sources
-//    and destinations are disjoint, so the (src, dst) row pairs go to a global list.
+//    membership in O(c) — then end-window hole filling: the new block is the last k_app
+//    valid slots (where the always-kept block tail 𝒯 sits), kept rows inside it stay, the
+//    i-th hole takes the i-th kept row from before it (Q23*: ~1/3 fewer moved rows
+//    than a [0, k_app) prefix on C2).  Sources and destinations are disjoint.
 //  * move (persistent grid): a pure 16-byte-coalesced streaming copy of the listed K, V
 //    rows and pos tags — no ordering constraints, full occupancy.
 #include <cub/block/block_scan.cuh>
@@ -49,6 +50,7 @@ struct CompactArgs {
   const uint8_t *pinned;
   const int64_t *span;
   int32_t *kcur, *npages, *free_stack;
+  int32_t *soff;    // page-list slot of each node's valid slot 0 (Q23*)
   const float *A;
   const float *Ahat;   // select_shared: the slice-summed Â[t] every row ranks by (else NULL)
   const Ctrl *ctrl_ro;
@@ -91,6 +93,41 @@ __device__ __forceinline__ void cp_async16ca(void *smem, const void *gmem) {
                : "memory");
 }
 
+// Streams nm (src row, dst row) pairs — K and V rows 16-byte coalesced (a row is cpr lanes,
+// rpi rows per warp instruction, U instructions in flight per lane), pos tags by the lane
+// holding piece 0.  src(i) / dst(i) give the rows of pair i.  Sources and destinations are
+// disjoint (Q23'), so the pairs need no order.
+template <int U, typename Src, typename Dst>
+__device__ __forceinline__ void move_rows(int nm, Src src, Dst dst, char *kp8, char *vp8,
+                                          int16_t *pos, int rb, int rpi, int piece, int sub) {
+  for (int c0 = 0; c0 < nm; c0 += rpi * U) {
+    uint4 bk[U], bv[U];
+    int sr[U], dr[U];
+    int16_t pt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = c0 + u * rpi + sub;
+      sr[u] = i < nm ? src(i) : -1;
+      dr[u] = i < nm ? dst(i) : -1;
+      if (sr[u] >= 0) {
+        const int64_t off = static_cast<int64_t>(sr[u]) * rb + piece * 16;
+        bk[u] = *reinterpret_cast<const uint4 *>(kp8 + off);
+        bv[u] = *reinterpret_cast<const uint4 *>(vp8 + off);
+        if (piece == 0) pt[u] = pos[sr[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (sr[u] >= 0) {
+        const int64_t off = static_cast<int64_t>(dr[u]) * rb + piece * 16;
+        *reinterpret_cast<uint4 *>(kp8 + off) = bk[u];
+        *reinterpret_cast<uint4 *>(vp8 + off) = bv[u];
+        if (piece == 0) pos[dr[u]] = pt[u];
+      }
+    }
+  }
+}
+
 // Shared-memory layout of select_move_ws_kernel (per CTA), all offsets 16-byte aligned.
 struct WsLayout {
   int cap, capP, pcap, jcap;
@@ -99,7 +136,7 @@ struct WsLayout {
   __host__ __device__ WsLayout(int cap_, int lgP, int wl_n_) {
     cap = cap_;
     wl_n = wl_n_;
-    capP = (cap + 9) & ~7;                 // pos pairs may read one slot past k_cur
+    capP = (cap + (1 << lgP) + 9) & ~7;   // pos tags by page-list slot from soff mod P (+1: pairs)
     pcap = (cap >> lgP) + 2;
     jcap = cap / 2 + 1;                    // moves per item ≤ min(k_app, k_cur − k_app)
     size_t o = 0;
@@ -126,12 +163,13 @@ struct WsLayout {
 // exposed latency): work entry of item k+3 → page list of item k+2 → pos tags and A span of
 // item k+1 (A is read by position over the span, independent of the pos tags), while item k
 // is ranked from shared memory.  Keep = the block tail 𝒯 (positions ≥ n − |𝒯|)
-// ∪ the top-m non-tail candidates by the 48-bit key ⟨A bits, pos⟩, or the last
-// k_app positions when k_app ≤ |𝒯| (Alg. 1).  The m-th largest key is found by a
-// warp radix select (8-bit digits, per-warp smem histogram, warp scan) that starts at the
-// highest key bit on which the candidates differ (warp min/max reductions of the A bits), so
-// the shared exponent bits cost no pass.  Slot layout (Q23'): kept rows in slots
-// [0, k_app) stay; the i-th hole there takes the i-th kept row from slots ≥ k_app.  The item's
+// ∪ the top-m non-tail candidates by the 49-bit key ⟨sink, A bits, pos⟩,
+// or the last k_app positions when k_app ≤ |𝒯| (Alg. 1).  The m-th largest key is
+// found by a warp radix select (8-bit digits, per-warp smem histogram, warp scan) that starts
+// at the highest key bit on which the candidates differ (warp min/max reductions), so the
+// shared exponent bits cost no pass.  Slot layout (Q23*): the new block is the
+// window of the last k_app valid slots; kept rows there stay, the i-th hole there takes the
+// i-th kept row from before the window.  The item's
 // (src row, dst row) list goes to move warp p through a 2-slot job queue in shared memory
 // guarded by mbarriers (full / empty).
 //
@@ -180,7 +218,7 @@ select_move_ws_kernel(CompactArgs a) {
     WorkEnt *swl = reinterpret_cast<WorkEnt *>(sm + Ly.swl);
     for (int j0 = 0; j0 < a.N; j0 += blockDim.x) {
       const int j = j0 + threadIdx.x;
-      int kc = 0, kt = 0, nn = 0, npg = 0;
+      int kc = 0, kt = 0, nn = 0, npg = 0, so = 0;
       long long sp = 0;
       bool pin = true;
       if (j < a.N) {
@@ -190,11 +228,14 @@ select_move_ws_kernel(CompactArgs a) {
         npg = a.npages[j];
         nn = a.n[j];
         sp = a.span[j];
+        so = a.soff[j];
       }
       const int ka = min(max(kt, 0), kc);
       const int ev = (!pin && ka < kc) ? 1 : 0;
       if (j0 == 0) EV_TRACE(4);
-      const int fr = ev ? npg - ((ka + a.P - 1) >> lgP) : 0;
+      // freed: the live pages before the one holding the window's first slot so + kc − ka
+      // (every live page when nothing is kept)
+      const int fr = ev ? (ka > 0 ? ((so + kc - ka) >> lgP) : npg) - (so >> lgP) : 0;
       if (ev) my_ev += static_cast<unsigned long long>(kc - ka);
       int wo, fo, tw, tf;
       Scan(scan_tmp).ExclusiveSum(ev, wo, tw);
@@ -210,7 +251,8 @@ select_move_ws_kernel(CompactArgs a) {
         e.n = nn;
         e.span = sp;
         e.foff = tot_free + fo;
-        e.nfree = fr;
+        e.nfree = static_cast<int16_t>(fr);
+        e.so = static_cast<int16_t>(so);
         wl[tot_work + wo] = e;
         if (Ly.wl_n) swl[tot_work + wo] = e;
       }
@@ -241,8 +283,7 @@ select_move_ws_kernel(CompactArgs a) {
       const int top = a.ctrl->free_top;
       for (int w = mt; w < s_work; w += kPairsWs * 32) {
         const WorkEnt e = wl[w];
-        const int newp = (e.ka + a.P - 1) >> lgP;
-        const int32_t *__restrict__ pl = a.ptab + static_cast<int64_t>(e.node) * a.MPN + newp;
+        const int32_t *__restrict__ pl = a.ptab + static_cast<int64_t>(e.node) * a.MPN + (e.so >> lgP);
         int32_t *__restrict__ dst = a.free_stack + top + e.foff;
         constexpr int kB = 8;
         for (int t0 = 0; t0 < e.nfree; t0 += kB) {
@@ -253,7 +294,14 @@ select_move_ws_kernel(CompactArgs a) {
           // descending list order (Q23''): LIFO pops return the run ascending
           for (int t = 0; t < kB; ++t) if (t0 + t < e.nfree) dst[e.nfree - 1 - (t0 + t)] = v[t];
         }
-        a.npages[e.node] = newp;
+        // the window's page-list slots stay where they are: soff moves up, the stale
+        // entries below it are never read again (an empty node resets)
+        if (e.ka > 0) {
+          a.soff[e.node] = e.so + e.kc - e.ka;
+        } else {
+          a.soff[e.node] = 0;
+          a.npages[e.node] = 0;
+        }
         a.kcur[e.node] = e.ka;
       }
       if (mt == 0) {
@@ -271,43 +319,33 @@ select_move_ws_kernel(CompactArgs a) {
     char *vp8 = static_cast<char *>(a.vpool);
     // jobs until the select warp posts the end marker (count < 0): the items are handed out
     // dynamically, so the number of jobs is not known in advance
+    long long mv_rows = 0, w_full = 0;
+    int k_jobs = 0;
     for (int k = 0;; ++k) {
       const int sl = k & (kJobSlots - 1);
+      const long long tw0 = a.trace ? clock64() : 0;
       mbar_wait(&full[sl], (k / kJobSlots) & 1);
+      if (a.trace && k > 0) w_full += clock64() - tw0;
       if (k == 0) EV_TRACE(2);
       const int cnt = mycount[sl];
       if (cnt < 0) break;
+      k_jobs = k + 1;
       const int nm = (a.exp & 1) ? 0 : cnt;
       const int2 *jb = myjobs + sl * jcap;
-      for (int c0 = 0; c0 < nm; c0 += rpi * kUw) {
-        uint4 bk[kUw], bv[kUw];
-        int2 mv[kUw];
-        int16_t pt[kUw];
-#pragma unroll
-        for (int u = 0; u < kUw; ++u) {
-          const int i = c0 + u * rpi + sub;
-          mv[u] = i < nm ? jb[i] : make_int2(-1, -1);
-          if (mv[u].x >= 0) {
-            const int64_t off = static_cast<int64_t>(mv[u].x) * rb + piece * 16;
-            bk[u] = *reinterpret_cast<const uint4 *>(kp8 + off);
-            bv[u] = *reinterpret_cast<const uint4 *>(vp8 + off);
-            if (piece == 0) pt[u] = a.pos[mv[u].x];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kUw; ++u) {
-          if (mv[u].x >= 0) {
-            const int64_t off = static_cast<int64_t>(mv[u].y) * rb + piece * 16;
-            *reinterpret_cast<uint4 *>(kp8 + off) = bk[u];
-            *reinterpret_cast<uint4 *>(vp8 + off) = bv[u];
-            if (piece == 0) a.pos[mv[u].y] = pt[u];
-          }
-        }
-      }
+      move_rows<kUw>(nm, [&](int i) { return jb[i].x; }, [&](int i) { return jb[i].y; }, kp8, vp8,
+                a.pos, rb, rpi, piece, sub);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[sl]);
+      if (a.trace) mv_rows += cnt;
     }
     EV_TRACE(3);
+    if (a.trace && lane == 0) {   // diagnostics: SM id, jobs and rows this move warp handled
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * 8 + 7] =
+          (static_cast<long long>(smid) << 40) | (static_cast<long long>(k_jobs) << 20) | mv_rows;
+      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * 8 + 6] = w_full;   // cycles
+    }
     return;
   }
   // -------------------------------------------------------------- select warp
@@ -349,11 +387,14 @@ select_move_ws_kernel(CompactArgs a) {
     cp_async16ca(reinterpret_cast<char *>(&Mbuf[k & 3]) + lane * 16,
                  reinterpret_cast<const char *>(&wl[w]) + lane * 16);
   };
+  // page list of the valid slots: from the live page holding slot soff (Gbuf[0]); valid slot
+  // s sits at Gbuf-relative slot (soff mod P) + s
   auto issue_pages = [&](int k) {
     if (item_of(k) >= items) return;
     const WorkEnt &e = meta(k);
-    const int np = (e.kc + Pm) >> lgP;
-    const int32_t *pl = a.ptab + static_cast<int64_t>(e.node) * a.MPN;
+    const int f0 = e.so >> lgP;
+    const int np = ((e.so + e.kc + Pm) >> lgP) - f0;
+    const int32_t *pl = a.ptab + static_cast<int64_t>(e.node) * a.MPN + f0;
     int32_t *g = Gbuf + (k % 3) * pcap;
     for (int i = lane; i < np; i += 32) cp_async4(g + i, pl + i);
   };
@@ -364,14 +405,14 @@ select_move_ws_kernel(CompactArgs a) {
     const int it = item_of(k);
     if (it >= items) return;
     const WorkEnt &e = meta(k);
-    if (e.kc == e.n) return;
+    if (e.kc == e.n && e.so == 0) return;
     const int32_t *g = Gbuf + (k % 3) * pcap;
     const int64_t base = row_base(it, wring[k & 3]);
     int16_t *pb = Pbuf + (k & 1) * capP;
-    for (int q = lane; 2 * q < e.kc; q += 32) {     // slot pairs (P even: same page)
-      const int s = 2 * q;
-      cp_async4(pb + s, a.pos + base + static_cast<int64_t>(g[s >> lgP]) * pstride + (s & Pm));
-    }
+    const int sb = e.so & Pm;
+    // Gbuf-relative slot pairs (c even; P even: same page) covering [sb, sb + k_cur)
+    for (int c = (sb & ~1) + 2 * lane; c < sb + e.kc; c += 64)
+      cp_async4(pb + c, a.pos + base + static_cast<int64_t>(g[c >> lgP]) * pstride + (c & Pm));
   };
   auto issue_A = [&](int k) {
     const int it = item_of(k);
@@ -414,6 +455,7 @@ select_move_ws_kernel(CompactArgs a) {
   issue_pos(0);
   cp_async_commit();
   int k = 0;
+  long long w_empty = 0;
   for (;; ++k) {
     const int it = item_of(k);
     if (it >= items) break;          // the counter only grows: every later draw is past the end
@@ -428,7 +470,8 @@ select_move_ws_kernel(CompactArgs a) {
     cp_async_commit();
     // ---- rank item k from shared memory
     const WorkEnt e = meta(k);
-    const bool ident = e.kc == e.n;
+    const bool ident = e.kc == e.n && e.so == 0;
+    const int sb = e.so & Pm;
     if (k == 0) EV_TRACE(6);         // item 0's data landed: ranking starts
     const int kc = e.kc, ka = e.ka, n = e.n;
     const int tl = min(a.l_tail, n);
@@ -437,37 +480,40 @@ select_move_ws_kernel(CompactArgs a) {
     const float *ab = Abuf + (k & 1) * cap;
     const int64_t base = row_base(it, wring[k & 3]);
     auto row = [&](int slot) -> int64_t {
-      return base + static_cast<int64_t>(pgs[slot >> lgP]) * pstride + (slot & Pm);
+      const int c = sb + slot;
+      return base + static_cast<int64_t>(pgs[c >> lgP]) * pstride + (c & Pm);
     };
     const bool ranked = ka > tl;
     const int m = ka - tl;
     const int tail_from = n - (ranked ? tl : ka);   // keep positions ≥ tail_from outright
     int ncand = 0;
     uint32_t bmin = 0xffffffffu, bmax = 0u;
+    unsigned sink_all = 1u, sink_any = 0u;
     for (int s0 = 0; s0 < kc; s0 += 32) {
       const int s = s0 + lane;
       unsigned long long kk = 0;
       if (s < kc) {
-        const int p = ident ? s : pb[s];
+        const int p = ident ? s : pb[sb + s];
         kk = static_cast<unsigned>(p);
         if (ranked && p < tail_from) {
-          // the key's high part: f32 bits of A (HEAVY), 0 (recency: TAIL, SINKS_TAIL); the
-          // global sinks — the root's first n_sinks positions — rank above
-          // everything else in HEAVY (all-ones: above any finite A) and SINKS_TAIL
-          const bool sink = e.node == 0 && p < a.n_sinks && a.select_mode != ARBOR_SELECT_TAIL;
-          unsigned bits = sink ? 1u : 0u;
+          // key = ⟨sink, A bits, position⟩ (oracle/select.rank_key): the global sinks — the
+          // root's first n_sinks positions — rank above everything else
+          // in HEAVY and SINKS_TAIL (bit 48), then the f32 bits of A (HEAVY; 0 for the
+          // recency rules TAIL, SINKS_TAIL), then the position
+          const unsigned sink =
+              (e.node == 0 && p < a.n_sinks && a.select_mode != ARBOR_SELECT_TAIL) ? 1u : 0u;
+          unsigned bits = 0u;
           if (a.select_mode == ARBOR_SELECT_HEAVY) {
-            if (sink) {
-              bits = 0xffffffffu;
-            } else {
-              const float av = ab[p];
-              if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
-              bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
-            }
+            const float av = ab[p];
+            if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+            bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
           }
-          kk = kCand | (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
+          kk = kCand | (static_cast<unsigned long long>(sink) << 48) |
+               (static_cast<unsigned long long>(bits) << 16) | static_cast<unsigned>(p);
           bmin = min(bmin, bits);
           bmax = max(bmax, bits);
+          sink_all &= sink;
+          sink_any |= sink;
         }
         key[s] = kk;
       }
@@ -483,7 +529,11 @@ select_move_ws_kernel(CompactArgs a) {
       // min and max differ); the radix passes start there
       bmin = __reduce_min_sync(0xffffffffu, bmin);
       bmax = __reduce_max_sync(0xffffffffu, bmax);
-      const int top = bmin != bmax ? 16 + 31 - __clz(static_cast<int>(bmin ^ bmax)) : 15;
+      sink_all = __reduce_and_sync(0xffffffffu, sink_all);
+      sink_any = __reduce_or_sync(0xffffffffu, sink_any);
+      // the sink bit differs among the candidates: start at bit 48
+      const int top = sink_all != sink_any ? 48
+                      : bmin != bmax ? 16 + 31 - __clz(static_cast<int>(bmin ^ bmax)) : 15;
       unsigned long long prefix = kCand, pmask = kCand;
       int need = m;
       for (int shift = top - 7; shift > -8; shift -= 8) {
@@ -540,7 +590,9 @@ select_move_ws_kernel(CompactArgs a) {
       tkey = prefix;
       tmask = pmask;
     }
-    // keep flags → holes (dropped slots < k_app) and movers (kept slots ≥ k_app), ascending
+    // keep flags → holes (dropped slots of the window [k_cur − k_app, k_cur)) and movers
+    // (kept slots before it), ascending
+    const int w0 = kc - ka;
     int nh = 0, nm = 0;
     for (int s0 = 0; s0 < kc; s0 += 32) {
       const int s = s0 + lane;
@@ -550,8 +602,8 @@ select_move_ws_kernel(CompactArgs a) {
         const int p = static_cast<int>(kk & 0xffffu);
         keep = (p >= tail_from) || (ranked && (kk & kCand) && (kk & tmask) >= tkey);
       }
-      const int hole = s < ka && !keep;
-      const int mv = s >= ka && s < kc && keep;
+      const int hole = s >= w0 && s < kc && !keep;
+      const int mv = s < w0 && keep;
       const unsigned hb = __ballot_sync(0xffffffffu, hole);
       const unsigned mb = __ballot_sync(0xffffffffu, mv);
       if (hole) holes[nh + __popc(hb & lt_mask)] = s;
@@ -567,7 +619,9 @@ select_move_ws_kernel(CompactArgs a) {
     nm = nm < nh ? nm : nh;
     // hand the job to the move warp
     const int sl = k & (kJobSlots - 1);
+    const long long tw0 = a.trace ? clock64() : 0;
     mbar_wait(&empty[sl], ((k / kJobSlots) & 1) ^ 1);
+    if (a.trace) w_empty += clock64() - tw0;
     int2 *jb = myjobs + sl * jcap;
     for (int i = lane; i < nm; i += 32)
       jb[i] = make_int2(static_cast<int>(row(movers[i])), static_cast<int>(row(holes[i])));
@@ -600,6 +654,8 @@ select_move_ws_kernel(CompactArgs a) {
     }
   }
   EV_TRACE(3);
+  if (a.trace && lane == 0)   // diagnostics: cycles this select warp waited for a free job slot
+    a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * 8 + 7] = w_empty;
 }
 
 }  // namespace
@@ -647,6 +703,7 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n, bool 
   a.pinned = c->d.pinned;
   a.span = c->d.span;
   a.kcur = c->d.kcur;
+  a.soff = c->d.soff;
   a.npages = c->d.npages;
   a.free_stack = c->d.free_stack;
   a.A = c->cfg.score;

@@ -112,18 +112,27 @@ __global__ void stash_kernel(PoolArgs g, const int32_t *ptab, int node, int n, i
 }
 
 // Rehydrate plan: nodes ascending; a node with k_cur < n gets its pages and k_cur = n.
+// Its live pages (from the one holding slot soff, Q23*) move to the front of its
+// list and soff = 0, then pages are popped up to ⌈n/P⌉ (oracle/state.rehydrate).
 // keep_floor > 0 (the controller's Transition under params.k_protect): only nodes
 // below min(n, keep_floor) are restored (to the full span).
 __global__ void rehydrate_plan_kernel(Ctrl *ctrl, int32_t *free_stack, int32_t *npages,
-                                      int32_t *ptab, const int32_t *n, int32_t *kcur, int MPN,
-                                      int P, const int32_t *nodes, int count, int32_t *flag,
-                                      int keep_floor) {
+                                      int32_t *ptab, const int32_t *n, int32_t *kcur,
+                                      int32_t *soff, int MPN, int P, const int32_t *nodes,
+                                      int count, int32_t *flag, int keep_floor) {
   int done = 0;
   for (int i = 0; i < count; ++i) {
     const int node = nodes[i];
     flag[i] = 0;
     if (kcur[node] >= n[node]) continue;   // full: no-op, not counted
     if (keep_floor > 0 && kcur[node] >= min(n[node], keep_floor)) continue;
+    const int first = soff[node] / P;
+    if (first > 0) {
+      int32_t *pl = ptab + static_cast<int64_t>(node) * MPN;
+      for (int i = first; i < npages[node]; ++i) pl[i - first] = pl[i];
+      npages[node] -= first;
+    }
+    soff[node] = 0;
     if (!pop_pages(ctrl, free_stack, npages, ptab, MPN, P, node, n[node])) continue;
     kcur[node] = n[node];
     flag[i] = 1;
@@ -199,7 +208,7 @@ void launch_stash(arbor_ctx *c, int node, int n, int64_t span) {
 
 void launch_rehydrate_plan(arbor_ctx *c, int count, int keep_floor) {
   rehydrate_plan_kernel<<<1, 1, 0, c->ms>>>(c->d.ctrl, c->d.free_stack, c->d.npages, c->d.ptab,
-                                           c->d.n, c->d.kcur, c->max_pages_node, c->P,
+                                           c->d.n, c->d.kcur, c->d.soff, c->max_pages_node, c->P,
                                            c->d.rehyd_nodes, count, c->d.rehyd_flag, keep_floor);
   ARBOR_LAUNCHED(c);
 }

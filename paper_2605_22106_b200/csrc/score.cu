@@ -23,7 +23,7 @@ struct ApplyArgs {
   PlanView pv;
   PoolView g;
   const int16_t *pos;
-  const int32_t *ptab, *kcur;
+  const int32_t *ptab, *kcur, *soff;
   const int64_t *span;
   const float *zbuf, *lse;
   float *A;
@@ -169,7 +169,7 @@ __device__ __forceinline__ void msve_compute(const MsveArgs &m, int i, bool open
 // nodes (lane i: mass node w + NW·i).  Plan arrays, k_cur, n and spans are not written by
 // the attention kernel, so decode_post loads the first batch before griddepcontrol.wait.
 struct ChunkMeta {
-  int node = 0, c0 = 0, p0 = 0, pc = 0, nt = 0, ident = 0;
+  int node = 0, c0 = 0, p0 = 0, pc = 0, nt = 0, ident = 0;   // nt: chunk_span of the chunk
   long long sp = 0;
 };
 struct MassMeta {
@@ -188,9 +188,9 @@ __device__ __forceinline__ ChunkMeta load_chunk_meta(const FusedArgs &f, int cm,
     // A_i(t) = Σ_{u>b_i}: the open block that holds the query (an open active leaf)
     // gets no mass from it — its chunks attend but are skipped here (Q5')
     if ((m.node & (nparts - 1)) == part && !f.m.open[m.node]) {   // nparts: a power of two
-      const int kc = a.kcur[m.node];
-      m.nt = max(0, min(kAttnChunk, kc - m.c0));
-      m.ident = kc == f.nlen[m.node];
+      const int kc = a.kcur[m.node], so = a.soff[m.node];
+      m.nt = chunk_span(so, kc, m.c0, kAttnChunk);
+      m.ident = kc == f.nlen[m.node] && so == 0;
       m.sp = a.span[m.node];
     }
   }
@@ -244,7 +244,8 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
       const int32_t *pl = a.ptab + static_cast<int64_t>(node) * a.g.MPN;
       // both 32-slot halves of the chunk at once (lane: slots lane and lane + 32), so their
       // logit and A loads are in flight together
-      const bool v0 = lane < nt, v1 = lane + 32 < nt;
+      const int hi = span_hi(nt), lo = span_lo(nt);   // valid slots [lo, hi) of the chunk (Q23*)
+      const bool v0 = lane >= lo && lane < hi, v1 = lane + 32 >= lo && lane + 32 < hi;
       auto pos_of = [&](int slot) {   // page size: a power of two (arbor_init)
         return ident ? slot : a.pos[pool_row(a.g, li, pl[slot >> lgP], h, slot & (a.g.P - 1))];
       };
@@ -570,6 +571,7 @@ FusedArgs fused_args(arbor_ctx *c, const PlanView &pv, const float *lse, const i
   a.pos = c->cfg.pos_pool;
   a.ptab = c->d.ptab;
   a.kcur = c->d.kcur;
+  a.soff = c->d.soff;
   a.span = c->d.span;
   a.zbuf = c->d.zbuf;
   a.lse = lse;

@@ -75,6 +75,34 @@ def main():
         "select_done": pct(np.where(valid[:, sel, 3], rel[:, sel, 3], np.nan).ravel()),
         "move_done": pct(np.where(valid[:, mov, 3], rel[:, mov, 3], np.nan).ravel()),
     }
+    # move warps: SM id, jobs, rows (slot 7) against their finishing time
+    info = tr[:, mov, 7].astype(np.int64)
+    smid, jobs, rows = info >> 40, (info >> 20) & 0xFFFFF, info & 0xFFFFF
+    done = rel[:, mov, 3]
+    ok = valid[:, mov, 3]
+    res["move_jobs"] = pct(np.where(ok, jobs, np.nan).ravel())
+    res["move_rows"] = pct(np.where(ok, rows, np.nan).ravel())
+    # cycles → µs at 1.965 GHz: move warps waiting for a job, select warps waiting for a slot
+    res["move_wait_full_us"] = pct(np.where(ok, tr[:, mov, 6] / 1965.0, np.nan).ravel())
+    res["select_wait_empty_us"] = pct(np.where(valid[:, sel, 3], tr[:, sel, 7] / 1965.0, np.nan).ravel())
+    late = np.argsort(np.where(ok, done, -1).ravel())[::-1][:12]
+    res["latest_moves"] = [{"cta": int(i // 8), "sm": int(smid.ravel()[i]), "jobs": int(jobs.ravel()[i]),
+                            "rows": int(rows.ravel()[i]), "done": round(float(done.ravel()[i]), 2)}
+                           for i in late]
+    # per SM: rows moved by its move warps and the time its last one finished
+    sm_rows, sm_done = {}, {}
+    for c in range(ctas):
+        for w in range(8):
+            if not ok[c, w]:
+                continue
+            m = int(smid[c, w])
+            sm_rows[m] = sm_rows.get(m, 0) + int(rows[c, w])
+            sm_done[m] = max(sm_done.get(m, 0.0), float(done[c, w]))
+    ms = sorted(sm_done, key=lambda m: sm_done[m])
+    res["sm_rows_vs_done"] = [[m, sm_rows[m], round(sm_done[m], 2)] for m in ms[:5] + ms[-8:]]
+    if len(ms) > 2:
+        res["corr_rows_done_per_sm"] = float(np.corrcoef([sm_rows[m] for m in ms], [sm_done[m] for m in ms])[0, 1])
+        res["corr_smid_done"] = float(np.corrcoef(ms, [sm_done[m] for m in ms])[0, 1])
     print(json.dumps(res))
 
 

@@ -148,24 +148,28 @@ class Pair:
         return self.ctx.score.cpu().numpy()
 
     def gpu_node(self, node):
-        """(k_cur, pages, pos [L][H][k], K rows [L][H][k][d] raw, V rows raw)."""
+        """(k_cur, pages, pos [L][H][k], K rows [L][H][k][d] raw, V rows raw, first_slot):
+        the valid slots are first_slot … first_slot + k_cur − 1 of the live page list."""
         kc, n, pages = self.ctx.arbor_read_node(node)
+        ko = self.ctx.arbor_read_node_offset(node)
         L, H, P = self.ctx.L, self.ctx.H, self.ctx.P
         if kc == 0:
-            return kc, pages, np.zeros((L, H, 0), np.int64), None, None
+            return kc, pages, np.zeros((L, H, 0), np.int64), None, None, ko
         idx = torch.as_tensor(pages, device="cuda", dtype=torch.long)
-        pos = self.ctx.pos_pool[:, idx].permute(0, 2, 1, 3).reshape(L, H, -1)[:, :, :kc]
-        kr = self.ctx.k_pool[:, idx].permute(0, 2, 1, 3, 4).reshape(L, H, -1, self.ctx.D)[:, :, :kc]
-        vr = self.ctx.v_pool[:, idx].permute(0, 2, 1, 3, 4).reshape(L, H, -1, self.ctx.D)[:, :, :kc]
-        return kc, pages, pos.cpu().numpy().astype(np.int64), kr.cpu(), vr.cpu()
+        sl = slice(ko, ko + kc)
+        pos = self.ctx.pos_pool[:, idx].permute(0, 2, 1, 3).reshape(L, H, -1)[:, :, sl]
+        kr = self.ctx.k_pool[:, idx].permute(0, 2, 1, 3, 4).reshape(L, H, -1, self.ctx.D)[:, :, sl]
+        vr = self.ctx.v_pool[:, idx].permute(0, 2, 1, 3, 4).reshape(L, H, -1, self.ctx.D)[:, :, sl]
+        return kc, pages, pos.cpu().numpy().astype(np.int64), kr.cpu(), vr.cpu(), ko
 
     def check_kv_state(self, nodes=None):
         """Bit-exact: k_cur, page lists, pos tags = oracle kept offsets, K/V bytes = original."""
         nodes = range(self.tree.num_nodes) if nodes is None else nodes
         for i in nodes:
-            kc, pages, pos, kr, vr = self.gpu_node(i)
+            kc, pages, pos, kr, vr, ko = self.gpu_node(i)
             assert kc == self.orc.k_cur(i), (i, kc, self.orc.k_cur(i))
             assert pages == self.orc.pages[i], (i, pages, self.orc.pages[i])
+            assert ko == self.orc.koff[i], (i, ko, self.orc.koff[i])
             assert np.array_equal(pos, self.orc.kept[i]), f"kept positions differ at node {i}"
             if kc:
                 a = int(self.tree.span_start[i])

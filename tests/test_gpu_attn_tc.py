@@ -25,15 +25,22 @@ RAGGED = dict(tree=("full", 3, 3, 93), L=2, H=4, Hq=16, d=128, dtype="bf16", P=1
 
 
 def _poison_page_tails(pr: Pair):
-    """Write NaN into every slot past k_cur of each node's last page (garbage by contract)."""
+    """Write NaN into every slot past the valid ones of each node's last page, and before
+    them in its first page (an evicted node's valid slots start at first_slot, Q23*) —
+    garbage by contract."""
     P = pr.ctx.P
     for i in range(pr.tree.num_nodes):
         kc, n, pages = pr.ctx.arbor_read_node(i)
-        if not pages or kc % P == 0:
+        ko = pr.ctx.arbor_read_node_offset(i)
+        if not pages:
             continue
-        last = pages[-1]
-        pr.ctx.k_pool[:, last, :, kc % P:] = float("nan")
-        pr.ctx.v_pool[:, last, :, kc % P:] = float("nan")
+        e = (ko + kc) % P
+        if e:
+            pr.ctx.k_pool[:, pages[-1], :, e:] = float("nan")
+            pr.ctx.v_pool[:, pages[-1], :, e:] = float("nan")
+        if ko:
+            pr.ctx.k_pool[:, pages[0], :, :ko] = float("nan")
+            pr.ctx.v_pool[:, pages[0], :, :ko] = float("nan")
 
 
 def _evict_ragged(pr: Pair, frac: float):

@@ -98,16 +98,17 @@ def test_c3_full_size_transitions_sampled_rows():
             assert o.free == free, f"transition {t}: free list"
         for i in range(tree.num_nodes):
             kc, n, pages = ctx.arbor_read_node(i)
+            ko = ctx.arbor_read_node_offset(i)
             if kc == 0:
                 assert all(o.k_cur(i) == 0 for o in orcs.values())
                 continue
             idx = torch.as_tensor(pages, device="cuda", dtype=torch.long)
             for (l, h), o in orcs.items():
-                assert kc == o.k_cur(i) and pages == o.pages[i], (t, i)
-                pos = ctx.pos_pool[l, idx, h].reshape(-1)[:kc].cpu().numpy().astype(np.int64)
+                assert kc == o.k_cur(i) and pages == o.pages[i] and ko == o.koff[i], (t, i)
+                pos = ctx.pos_pool[l, idx, h].reshape(-1)[ko:ko + kc].cpu().numpy().astype(np.int64)
                 assert np.array_equal(pos, o.kept[i][0, 0]), (t, i, (l, h))
                 if i % 7 == 0 or tree.is_open[i]:    # K/V bytes on a sample of nodes
-                    kr = ctx.k_pool[l, idx, h].reshape(-1, ctx.D)[:kc]
+                    kr = ctx.k_pool[l, idx, h].reshape(-1, ctx.D)[ko:ko + kc]
                     want = torch.as_tensor(o.K[0, 0, int(tree.span_start[i]) + pos]).to(torch.bfloat16)
                     assert torch.equal(kr.cpu().view(torch.int16), want.view(torch.int16)), (t, i)
         for _ in range(D):

@@ -166,11 +166,12 @@ def test_full_size_decode_step_sampled_rows(cfg):
         assert o.free == free, "free list"
     for i in range(tree.num_nodes):
         kc, n, pages = ctx.arbor_read_node(i)
+        ko = ctx.arbor_read_node_offset(i)
         idx = torch.as_tensor(pages, device="cuda", dtype=torch.long)
         for (l, h), o in orcs.items():
-            assert kc == o.k_cur(i) and pages == o.pages[i], i
+            assert kc == o.k_cur(i) and pages == o.pages[i] and ko == o.koff[i], i
             if kc:
-                pos = ctx.pos_pool[l, idx, h].reshape(-1)[:kc].cpu().numpy().astype(np.int64)
+                pos = ctx.pos_pool[l, idx, h].reshape(-1)[ko:ko + kc].cpu().numpy().astype(np.int64)
                 assert np.array_equal(pos, o.kept[i][0, 0]), (i, (l, h))
     # decode over the compacted pages
     for leaf in order[40:44]:

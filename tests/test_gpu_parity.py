@@ -286,7 +286,7 @@ def test_stash_rehydrate_bit_exact_roundtrip():
     assert pr.orc.rehydrate(allnodes) > 0
     pr.check_kv_state()
     for i in range(N):
-        kc, pages, pos, kr, vr = pr.gpu_node(i)
+        kc, pages, pos, kr, vr, _ = pr.gpu_node(i)
         assert kc == int(pr.tree.span_len[i]) and np.array_equal(pos[0, 0], np.arange(kc))
 
 

@@ -28,7 +28,7 @@ MID = dict(tree=("full", 4, 4, 96), L=2, H=4, Hq=16, d=128, dtype="bf16", P=16, 
 
 
 def _kept_sets(pr, node):
-    kc, pages, pos, _, _ = pr.gpu_node(node)
+    kc, pages, pos, _, _, _ = pr.gpu_node(node)
     return kc, pos
 
 

@@ -475,34 +475,54 @@ def test_state_lifecycle_errors():
 
 
 def test_state_hole_filling_layout():
-    """DESIGN.md Q23': after eviction every row holds exactly the retained set; retained rows
-    already inside [0, k_app) keep their slot; the holes are filled, in ascending order, by the
-    retained rows from slots >= k_app in ascending order."""
+    """DESIGN.md Q23* (end-window hole filling): after eviction every row holds exactly the
+    retained set; the new block is the last k_app of the old valid slots (w = k_cur − k_app
+    onward); retained rows already inside the window keep their slot; the holes there are
+    filled, in ascending order, by the retained rows from slots < w in ascending order.  The
+    page list loses its ⌊(koff + w)/P⌋ leading pages (pushed descending), koff ← (koff + w)
+    mod P, and the live list is exactly ⌈(koff + k_cur)/P⌉ pages — checked over two rounds
+    of eviction, so a block that already has koff > 0 is evicted again."""
     tree, o, E = _small_state(levels=3, width=3, t_node=20, seed=6)
     tree.active = [synth.leaves_of(tree)[0]]
     q = synth.make_queries(1, o.L, o.Hq, o.d, "f32", 9, E).double().numpy()
-    for _ in range(4):
-        o.score_accumulate(tree, q)
-    before = [o.kept[i].copy() for i in range(tree.num_nodes)]
-    a, s = o.msve(tree)
-    k = o.allocate(tree, s, int(tree.total_tokens * 0.6))
-    o.evict(tree, k)
-    Af = o.A.astype(np.float32)
-    for i in range(tree.num_nodes):
-        if o.k_cur(i) == before[i].shape[-1]:
-            continue
-        ka, a0, n = o.k_cur(i), o.span_start[i], o.n[i]
-        for l in range(o.L):
-            for h in range(o.H):
-                old = [int(x) for x in before[i][l, h]]
-                new = [int(x) for x in o.kept[i][l, h]]
-                R = select.retained_set(old, n, ka, o.params["l_tail"], Af[l, h, a0:a0 + n])
-                assert sorted(new) == R
-                stay = [s_ for s_ in range(ka) if old[s_] in R]
-                assert all(new[s_] == old[s_] for s_ in stay)
-                holes = [s_ for s_ in range(ka) if old[s_] not in R]
-                movers = [old[s_] for s_ in range(ka, len(old)) if old[s_] in R]
-                assert [new[s_] for s_ in holes] == movers
+    for frac in (0.6, 0.35):
+        for _ in range(4):
+            o.score_accumulate(tree, q)
+        before = [o.kept[i].copy() for i in range(tree.num_nodes)]
+        pages_before = [list(o.pages[i]) for i in range(tree.num_nodes)]
+        koff_before = list(o.koff)
+        free_before = list(o.free)
+        a, s = o.msve(tree)
+        k = o.allocate(tree, s, int(tree.total_tokens * frac))
+        o.evict(tree, k)
+        Af = o.A.astype(np.float32)
+        pushed = []
+        for i in range(tree.num_nodes):
+            kc0 = before[i].shape[-1]
+            assert 0 <= o.koff[i] < o.P
+            assert len(o.pages[i]) == -(-(o.koff[i] + o.k_cur(i)) // o.P)
+            if o.k_cur(i) == kc0:
+                assert o.pages[i] == pages_before[i] and o.koff[i] == koff_before[i]
+                continue
+            ka, a0, n = o.k_cur(i), o.span_start[i], o.n[i]
+            w = kc0 - ka
+            c = koff_before[i] + w
+            drop = c // o.P if ka else len(pages_before[i])
+            assert o.pages[i] == pages_before[i][drop:]
+            assert o.koff[i] == (c % o.P if ka else 0)
+            pushed += list(reversed(pages_before[i][:drop]))
+            for l in range(o.L):
+                for h in range(o.H):
+                    old = [int(x) for x in before[i][l, h]]
+                    new = [int(x) for x in o.kept[i][l, h]]
+                    R = select.retained_set(old, n, ka, o.params["l_tail"], Af[l, h, a0:a0 + n])
+                    assert sorted(new) == R
+                    stay = [s_ for s_ in range(w, kc0) if old[s_] in R]
+                    assert all(new[s_ - w] == old[s_] for s_ in stay)
+                    holes = [s_ for s_ in range(w, kc0) if old[s_] not in R]
+                    movers = [old[s_] for s_ in range(w) if old[s_] in R]
+                    assert [new[s_ - w] for s_ in holes] == movers
+        assert o.free == free_before + pushed
 
 
 # ---------------------------------------------------------------- f4 intra-block variants
@@ -735,28 +755,35 @@ def test_node_mass_counts_frozen_evicted_scores():
         assert abs(o.masses()[i] - ref) <= o.L * o.H
 
 
-def test_hole_fill_worked_example():
-    """Q23' slot order on the hand-worked example of tests/golden."""
-    g = GOLD["hole_fill_example"]
+@pytest.mark.parametrize("name", ["hole_fill_example", "hole_fill_example2"])
+def test_hole_fill_worked_example(name):
+    """Q23* slot order and page accounting on the hand-worked examples of tests/golden (the
+    first from SPEC S:392; the second with a staying row between two holes)."""
+    g = GOLD[name]
+    A_row = GOLD["select_example"]["A"] if name == "hole_fill_example" else g["A"]
     tree = synth.SynthTree(np.array([-1, 0], np.int32), np.array([0, 10], np.int64),
                            np.array([10, 4], np.int32), np.zeros(2, np.uint8),
                            np.zeros(2, np.float32), np.zeros(2, np.float32), [1])
     L, H, d = 1, 1, 4
     K = np.zeros((L, H, 14, d))
-    o = ArborOracle(K, K, 1, 4, 8, default_params(k_min=1, l_tail=3, r_min=0.0))
+    o = ArborOracle(K, K, 1, g["page_size"], 8, default_params(k_min=1, l_tail=3, r_min=0.0, n_sinks=0))
     for i in range(2):
         o.open_node(i, int(tree.span_start[i]))
         o.append(i, int(tree.span_len[i]))
         o.close_node(i)
     tree.active = [1]
     A = np.zeros((L, H, 14), np.float32)
-    A[0, 0, :10] = GOLD["select_example"]["A"]
+    A[0, 0, :10] = A_row
+    pages0 = list(o.pages[0])
     # the root is on Path*: evict node 0 through a tree in which node 1 hangs off elsewhere
     tree2 = synth.SynthTree(np.array([-1, -1], np.int32), tree.span_start, tree.span_len,
                             tree.is_open, tree.v, tree.u, [1])
     o.evict(tree2, [g["k_app"], 4], A_f32=A)
     assert sorted(o.kept[0][0, 0].tolist()) == g["retained"]
     assert o.kept[0][0, 0].tolist() == g["new_slots"]
+    assert o.koff[0] == g["koff"]
+    assert o.pages[0] == pages0[g["freed_pages_front"]:]
+    assert o.free[-g["freed_pages_front"]:] == list(reversed(pages0[:g["freed_pages_front"]]))
 
 
 def test_k_protect_reduces_to_pinning_and_keeps_floors():
