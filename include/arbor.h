@@ -186,7 +186,12 @@ arbor_status arbor_nccl_unique_id(void *out128);
  * (concurrently decoded siblings need reserved position ranges). */
 arbor_status arbor_open_node(arbor_ctx *ctx, int32_t node, int64_t span_start);
 /* Append ntok decoded tokens to an open node.  k, v: DEVICE [layer_count][kv_head_count]
- * [ntok][head_dim] in kv_dtype.  Pages are popped from the free list in token order. */
+ * [ntok][head_dim] in kv_dtype.  Pages are popped from the free list in token order, on the
+ * device and asynchronously: when the pool runs out the append is skipped on the device and
+ * ARBOR_ERR_OUT_OF_PAGES latches there; it is returned by the next call that syncs
+ * (arbor_sync, the inspection calls, an evict with evicted_tokens_out).  Until then the
+ * host's view of n (used to plan attention) is ahead of the device's: call arbor_sync after
+ * appends when the pool can run dry. */
 arbor_status arbor_append_kv(arbor_ctx *ctx, int32_t node, const void *k, const void *v,
                              int32_t ntok);
 /* Boundary: close an open node (n_i ≥ 1), snapshot its post-close mass baseline

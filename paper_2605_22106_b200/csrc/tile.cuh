@@ -1,6 +1,8 @@
 // tile.cuh — paged K/V tile staging shared by the attention and score kernels.
 #pragma once
-#include <cstdio>
+#ifdef ARBOR_MBAR_WATCHDOG
+#include <cstdio>   // the debug watchdog's report (mbar_wait below)
+#endif
 #include "common.cuh"
 
 namespace arbor {

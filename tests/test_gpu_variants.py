@@ -106,6 +106,29 @@ def test_k_protect_path_floor_and_global_sinks(mode):
     assert pr.ctx.arbor_read_counters()[0] == pr.orc.rehydrations
 
 
+@pytest.mark.parametrize("mode", ["heavy", "sinks_tail"])
+def test_sinks_outnumber_heavy_slots(mode):
+    """The root's global sinks compete among themselves when fewer heavy-hitter slots than
+    sinks remain (m = k − |tail| < n_sinks): HEAVY keeps the sinks with the largest ⟨A, t⟩
+    (oracle/select.rank_key: sink first, then A, then position), SINKS_TAIL the most recent
+    sinks.  Two rounds (the second from a compacted root with first_slot > 0), bit-exact."""
+    pr = Pair(MID, seed=19, params_over=dict(select_mode=mode, n_sinks=12, l_tail=6,
+                                             k_protect=1))
+    pr.warmup(steps_per_leaf=1)
+    pr.decode_both()
+    N = pr.tree.num_nodes
+    n = [int(x) for x in pr.tree.span_len]
+    for m_heavy in (9, 3):
+        k = [max(1, int(0.5 * x)) for x in n]
+        k[0] = 6 + m_heavy                            # 9 then 3 heavy slots for 12 sinks
+        for j in range(N):
+            k[j] = min(k[j], pr.orc.k_cur(j))
+        _evict_both(pr, k)
+        root = [int(x) for x in pr.orc.kept[0][0, 0]]
+        assert len([p for p in root if p < 12]) == m_heavy
+        pr.decode_both()
+
+
 @pytest.mark.parametrize("shared", [0, 1])
 def test_thin_slice_a_i_and_shared_selection(shared):
     """Thin slice 𝓛 × 𝓗 (params.slice_layers / slice_kv_heads): a_i counts
