@@ -926,12 +926,16 @@ static void score_bookkeeping(arbor_ctx *c, const arbor_tree *tree, const HostPl
     if (!c->h_open[i] && (vis[i] || !c->mass_valid)) mass_nodes.push_back(i);
 }
 
-// node-wise split of each row over CTAs: about two recomputed nodes per CTA, ≤ 8 per row
-// (a power of two: CTA (row, p) owns the nodes with id & (parts − 1) == p)
-static int score_parts(size_t mass_nodes) {
-  const int want = std::max(1, std::min(8, static_cast<int>(mass_nodes) / 2));
+// split of each row's score pass over CTAs (score.cu score_row: part p takes the plan's
+// chunks p, p + parts, …; the row's last part computes its node masses): about 16 chunks per
+// part, ≤ 8 parts (a power of two), and never more CTAs than one resident wave (2 per SM) —
+// a second wave costs the whole per-CTA latency chain again (decode_post phase trace, C3:
+// 2 parts 83 µs vs 1 part 67 µs)
+static int score_parts(const arbor_ctx *c, size_t chunks) {
+  const int want = std::max(1, std::min(8, static_cast<int>(chunks) / 16));
   int p = 1;
   while (p * 2 <= want) p *= 2;
+  while (p > 1 && c->L * c->H * p > 2 * c->num_sms) p /= 2;
   return p;
 }
 
@@ -987,7 +991,7 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
   // single rank — the MSVE score; with several ranks the all-reduce sits before the MSVE
   const bool single = c->cfg.world_size == 1;
   launch_score_fused(c, pv, lse_use, d_mass_nodes, static_cast<int>(mass_nodes.size()), N, single,
-                     s_out, score_parts(mass_nodes.size()));
+                     s_out, score_parts(c, hp.ch_node.size()));
   CK_LAUNCH();
   c->lg_epoch = -1;   // A changed: the logits must not be applied twice
   c->mass_valid = true;
@@ -1040,9 +1044,7 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
   CK_LAUNCH();
   mark();
   const bool single = c->cfg.world_size == 1;
-  // parts per row: no more CTAs than one resident wave (2 per SM at the kernel's bounds)
-  int parts = score_parts(mass_nodes.size());
-  while (parts > 1 && c->L * c->H * parts > 2 * c->num_sms) parts /= 2;
+  int parts = score_parts(c, hp.ch_node.size());
   static const int parts_env = getenv("ARBOR_POST_PARTS") ? atoi(getenv("ARBOR_POST_PARTS")) : 0;
   if (parts_env > 0) parts = parts_env;   // diagnostics
   launch_decode_post(c, pv, out, lse_out, d_mass_nodes, static_cast<int>(mass_nodes.size()), N,

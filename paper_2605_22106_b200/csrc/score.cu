@@ -132,11 +132,26 @@ struct FusedArgs {
   int64_t *mass_part, *mass2;
   const int64_t *mclose;
   unsigned int *ticket;
+  unsigned int *row_done;      // [L·H] parts of each row past step (1) (zero at rest)
+  long long *trace;            // ARBOR_POST_TRACE=1 (diagnostics): [CTA][16] globaltimer ns
   int do_msve;
   MsveArgs m;
 };
 
-constexpr int kFusedThreads = 256;
+#ifndef ARBOR_POST_THREADS
+#define ARBOR_POST_THREADS 256
+#endif
+constexpr int kFusedThreads = ARBOR_POST_THREADS;
+
+#define POST_TRACE(f, e)                                                                    \
+  do {                                                                                      \
+    if ((f).trace && threadIdx.x == 0) {                                                    \
+      unsigned long long t_;                                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
+      (f).trace[(static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 16 + (e)] =   \
+          static_cast<long long>(t_);                                                       \
+    }                                                                                       \
+  } while (0)
 
 // MSVE of node i from its inputs (open flag, Nq, Mass, Mclose, v, u): a_i, s_i (fp64, no
 // contraction, same expression order as msve_kernel and the oracle)
@@ -176,10 +191,13 @@ struct MassMeta {
   int node = 0, n = 0;
   long long sp = 0;
 };
-__device__ __forceinline__ ChunkMeta load_chunk_meta(const FusedArgs &f, int cm, int part,
+// chunk v of part `part`: plan chunk part + nparts·v (round robin: the shared root chunks
+// spread over the parts)
+__device__ __forceinline__ ChunkMeta load_chunk_meta(const FusedArgs &f, int v, int part,
                                                      int nparts) {
   const ApplyArgs &a = f.ap;
   ChunkMeta m;
+  const int cm = part + nparts * v;
   if (cm < a.pv.C) {
     m.node = a.pv.ch_node[cm];
     m.c0 = a.pv.ch_chunk[cm] * kAttnChunk;
@@ -187,7 +205,7 @@ __device__ __forceinline__ ChunkMeta load_chunk_meta(const FusedArgs &f, int cm,
     m.pc = a.pv.ch_pcnt[cm];
     // A_i(t) = Σ_{u>b_i}: the open block that holds the query (an open active leaf)
     // gets no mass from it — its chunks attend but are skipped here (Q5')
-    if ((m.node & (nparts - 1)) == part && !f.m.open[m.node]) {   // nparts: a power of two
+    if (!f.m.open[m.node]) {
       const int kc = a.kcur[m.node], so = a.soff[m.node];
       m.nt = chunk_span(so, kc, m.c0, kAttnChunk);
       m.ident = kc == f.nlen[m.node] && so == 0;
@@ -196,15 +214,12 @@ __device__ __forceinline__ ChunkMeta load_chunk_meta(const FusedArgs &f, int cm,
   }
   return m;
 }
-__device__ __forceinline__ MassMeta load_mass_meta(const FusedArgs &f, int mm, int part,
-                                                   int nparts) {
+__device__ __forceinline__ MassMeta load_mass_meta(const FusedArgs &f, int mm) {
   MassMeta m;
   if (mm < f.n_mass) {
     m.node = f.mass_nodes[mm];
-    if ((m.node & (nparts - 1)) == part) {
-      m.n = f.nlen[m.node];
-      m.sp = f.ap.span[m.node];
-    }
+    m.n = f.nlen[m.node];
+    m.sp = f.ap.span[m.node];
   }
   return m;
 }
@@ -213,6 +228,8 @@ template <typename LseFn>
 __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int part, int nparts,
                                           LseFn lse2, const ChunkMeta *pre_c = nullptr,
                                           const MassMeta *pre_m = nullptr) {
+  // (row, part): the part's chunks (round robin over the row's plan chunks) in step (1); the
+  // row's last part to finish (1) computes every listed node's mass of the row in step (2)
   const ApplyArgs &a = f.ap;
   const int tid = threadIdx.x;
   // (1) A[li][h][a_j + pos] += Σ_pairs Σ_g exp2(z − LSE·log2 e)
@@ -226,12 +243,13 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   // Warp w takes chunks w, w + NW, …  Their metadata is loaded 32 chunks at a time, lane i
   // holding chunk w + NW·i (two round trips per batch instead of two per chunk), then
   // broadcast chunk by chunk.
-  for (int cb = warp; cb < a.pv.C; cb += NW * 32) {
+  const int Cp = a.pv.C > part ? (a.pv.C - part + nparts - 1) / nparts : 0;   // this part's chunks
+  for (int cb = warp; cb < Cp; cb += NW * 32) {
     const ChunkMeta cmeta = (cb == warp && pre_c) ? *pre_c : load_chunk_meta(f, cb + NW * lane, part, nparts);
     const int m_node = cmeta.node, m_c0 = cmeta.c0, m_p0 = cmeta.p0, m_pc = cmeta.pc,
               m_nt = cmeta.nt, m_ident = cmeta.ident;
     const long long m_sp = cmeta.sp;
-    const int nb = min(32, (a.pv.C - cb + NW - 1) / NW);
+    const int nb = min(32, (Cp - cb + NW - 1) / NW);
     for (int j = 0; j < nb; ++j) {
       const int nt = __shfl_sync(0xffffffffu, m_nt, j);
       if (nt == 0) continue;
@@ -320,13 +338,31 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
       }
     }
   }
-  __syncthreads();
+  POST_TRACE(f, 4);
+  // row ticket: the last part of the row to get here sees every part's A updates
+  __shared__ bool row_last;
+  if (nparts > 1) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const int row = li * f.H + h;
+      row_last = atomicAdd(&f.row_done[row], 1u) == static_cast<unsigned>(nparts - 1);
+      if (row_last) f.row_done[row] = 0u;
+    }
+    __syncthreads();
+    __threadfence();
+  } else {
+    __syncthreads();
+    if (tid == 0) row_last = true;
+    __syncthreads();
+  }
   // (2) this row's partial node masses: warp per node, lanes strided, fixed xor tree (Q29);
   // node metadata batched like the chunks'.  Rows outside the thin slice add nothing.
   const float *Arow = a.A + (static_cast<int64_t>(li) * f.H + h) * f.max_tokens;
-  const int mass_end = f.sv.has(li, h) ? f.n_mass : 0;
+  POST_TRACE(f, 5);
+  const int mass_end = (f.sv.has(li, h) && row_last) ? f.n_mass : 0;
   for (int mb = warp; mb < mass_end; mb += NW * 32) {
-    const MassMeta mmeta = (mb == warp && pre_m) ? *pre_m : load_mass_meta(f, mb + NW * lane, part, nparts);
+    const MassMeta mmeta = (mb == warp && pre_m) ? *pre_m : load_mass_meta(f, mb + NW * lane);
     const int m_node = mmeta.node, m_n = mmeta.n;
     const long long m_sp = mmeta.sp;
     const int nb = min(32, (mass_end - mb + NW - 1) / NW);
@@ -347,6 +383,7 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   // The inputs of each thread's first node and the listed-node bitmap are loaded before
   // the ticket (plan data and library state this kernel does not write), so the last CTA's
   // serial tail is one round trip (the accumulators) plus the MSVE arithmetic.
+  POST_TRACE(f, 6);
   constexpr int kMaxNodes = 3072;                      // arbor_init's max_nodes bound
   __shared__ unsigned listed[kMaxNodes / 32];
   __shared__ bool last;
@@ -372,6 +409,7 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
   __syncthreads();
   if (tid == 0) last = atomicAdd(f.ticket, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
+  POST_TRACE(f, 7);
   if (!last) return;
   __threadfence();
   if (tid == 0) *f.ticket = 0u;
@@ -391,6 +429,8 @@ __device__ __forceinline__ void score_row(const FusedArgs &f, int li, int h, int
       msve_compute(f.m, i, first ? p_open : f.m.open[i] != 0, first ? p_nq : f.m.nq[i], mass,
                    mclose, first ? p_v : f.m.v[i], first ? p_u : f.m.u[i]);
   }
+  __syncthreads();
+  POST_TRACE(f, 8);
 }
 
 __global__ void __launch_bounds__(kFusedThreads)
@@ -431,13 +471,14 @@ __global__ void __launch_bounds__(kFusedThreads, MINB)
 decode_post_kernel(PostArgs pa) {
   const FusedArgs &f = pa.f;
   const ApplyArgs &a = f.ap;
+  POST_TRACE(f, 0);
   const int row = blockIdx.x, part = blockIdx.y, nparts = gridDim.y;
   const int li = row / f.H, h = row - li * f.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = kFusedThreads / 32, EPL = D / 32;
   // first batch of score_row's metadata: overlaps the attention kernel's tail
   const ChunkMeta pre_c = load_chunk_meta(f, warp + NW * lane, part, nparts);
-  const MassMeta pre_m = load_mass_meta(f, warp + NW * lane, part, nparts);
+  const MassMeta pre_m = load_mass_meta(f, warp + NW * lane);
   // … and the first (leaf, q head) item's path bounds and this lane's first pair (plan arrays)
   int pre_p0 = 0, pre_p1 = 0, pre_pi = 0;
   {
@@ -451,6 +492,7 @@ decode_post_kernel(PostArgs pa) {
   }
   pdl_wait();
   pdl_trigger();
+  POST_TRACE(f, 1);
   const int G = a.G;
   __shared__ float lse2s[kPostItems], Ms[kPostItems], invL[kPostItems];
   auto part_ptr = [&](int p, int g) -> const float * {
@@ -500,6 +542,7 @@ decode_post_kernel(PostArgs pa) {
     }
   }
   __syncthreads();
+  POST_TRACE(f, 2);
   // (b) owned items, eight lanes per item (four items per warp at once): lane j of the group
   // holds pair p0 + j's index and weight 2^(m−M); then, pairs in path order, each lane
   // accumulates D/8 of o with float2 loads: o = Σ w o_p / L
@@ -555,11 +598,15 @@ decode_post_kernel(PostArgs pa) {
     }
   }
   __syncthreads();
+  POST_TRACE(f, 3);
   if (pa.exp & 2) return;
   score_row(f, li, h, part, nparts, [&](int b, int g) { return lse2s[b * G + g]; }, &pre_c, &pre_m);
 }
 
 }  // namespace
+
+long long *g_post_trace = nullptr;
+size_t g_post_trace_n = 0;
 
 namespace {
 FusedArgs fused_args(arbor_ctx *c, const PlanView &pv, const float *lse, const int32_t *d_nodes,
@@ -593,6 +640,18 @@ FusedArgs fused_args(arbor_ctx *c, const PlanView &pv, const float *lse, const i
   f.mass2 = c->d.mass2;
   f.mclose = c->d.mclose;
   f.ticket = c->d.ticket;
+  f.row_done = c->d.row_done;
+  f.trace = nullptr;
+  if (getenv("ARBOR_POST_TRACE")) {
+    const size_t need = static_cast<size_t>(c->L) * c->H * 64 * 16;
+    if (need > g_post_trace_n) {
+      if (g_post_trace) cudaFree(g_post_trace);
+      cudaMalloc(&g_post_trace, need * sizeof(long long));
+      g_post_trace_n = need;
+    }
+    cudaMemsetAsync(g_post_trace, 0, g_post_trace_n * sizeof(long long), c->ms);
+    f.trace = g_post_trace;
+  }
   f.do_msve = do_msve ? 1 : 0;
   MsveArgs &m = f.m;
   m.N = N;
@@ -685,3 +744,13 @@ void launch_msve(arbor_ctx *c, int N, float *s_out) {
 }
 
 }  // namespace arbor
+
+// debug only (not part of include/arbor.h): the last ARBOR_POST_TRACE timeline of
+// decode_post / score_fused ([CTA = part·rows + row][16] globaltimer ns: 0 start, 1 past
+// griddepcontrol.wait, 2 (a) merged LSE, 3 (b) outputs, 4 (1) A updates, 5 row ticket,
+// 6 (2) masses, 7 global ticket, 8 the last CTA's MSVE done)
+extern "C" int arbor_debug_post_trace(long long *host, long long count) {
+  if (!arbor::g_post_trace || count < 0 || static_cast<size_t>(count) > arbor::g_post_trace_n) return -1;
+  cudaDeviceSynchronize();
+  return cudaMemcpy(host, arbor::g_post_trace, sizeof(long long) * count, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
+}

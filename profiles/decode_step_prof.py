@@ -57,8 +57,38 @@ def main():
     st = ctx.arbor_stage_times()
     ctx.arbor_set_profiling(False)
     us = sorted(a.elapsed_time(b) * 1e3 for a, b in ts)
-    print(json.dumps({"config": cfg, "active_leaves": nA, "decode_step_us_p50": us[len(us) // 2],
-                      "stage_us": {k: round(v * 1e3, 2) for k, v in st.items() if v}}))
+    res = {"config": cfg, "active_leaves": nA, "decode_step_us_p50": us[len(us) // 2],
+           "stage_us": {k: round(v * 1e3, 2) for k, v in st.items() if v}}
+    if os.environ.get("POST_TRACE"):
+        # one more step with the decode_post phase trace (score.cu POST_TRACE): percentiles
+        # over CTAs of each phase end, µs after the earliest CTA start
+        import ctypes as C
+        import numpy as np
+        import paper_2605_22106_b200 as pk
+        os.environ["ARBOR_POST_TRACE"] = "1"
+        flush.zero_()
+        ctx.arbor_decode_step(tree, qs[0], out, lse, s)
+        torch.cuda.synchronize()
+        del os.environ["ARBOR_POST_TRACE"]
+        lib = pk.load_library()
+        n = ctx.L * ctx.H * 64 * 16
+        buf = (C.c_longlong * n)()
+        lib.arbor_debug_post_trace.argtypes = [C.POINTER(C.c_longlong), C.c_longlong]
+        assert lib.arbor_debug_post_trace(buf, n) == 0
+        tr = np.frombuffer(buf, dtype=np.int64).reshape(-1, 16).astype(np.float64)
+        tr = tr[tr[:, 0] > 0]
+        t0 = tr[:, 0].min()
+        names = ["start", "pdl_wait", "a_lse", "b_out", "score_A", "row_ticket", "masses",
+                 "ticket", "last_msve"]
+        ph = {}
+        for e, nm in enumerate(names):
+            x = tr[:, e]
+            x = (x[x > 0] - t0) / 1e3
+            if x.size:
+                ph[nm] = [round(float(v), 2) for v in np.percentile(x, [0, 50, 90, 100])]
+        res["post_trace_us_min_p50_p90_max"] = ph
+        res["post_ctas"] = int(tr.shape[0])
+    print(json.dumps(res))
 
 
 if __name__ == "__main__":
