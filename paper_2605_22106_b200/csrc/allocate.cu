@@ -153,7 +153,11 @@ allocate_kernel(AllocArgs a) {
   int *dlt = dep + N;                                            // [N]
   int *act = dlt + N;                                            // [nA]
   unsigned char *onp = reinterpret_cast<unsigned char *>(act + a.nA);   // [N]
-  for (int j = threadIdx.x; j < N; j += blockDim.x) { par[j] = a.parent[j]; onp[j] = 0; }
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    par[j] = a.parent[j];
+    onp[j] = 0;
+    dlt[j] = 0x7fffffff;
+  }
   for (int b = threadIdx.x; b < a.nA; b += blockDim.x) act[b] = a.active[b];
   __syncthreads();
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
@@ -164,22 +168,25 @@ allocate_kernel(AllocArgs a) {
   for (int b = threadIdx.x; b < a.nA; b += blockDim.x)
     for (int x = act[b]; x >= 0; x = par[x]) onp[x] = 1;
   __syncthreads();
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    int best = 0x7fffffff;
+  // one (node, active leaf) pair per thread — the LCA walks are dependent shared-memory
+  // chains, so spreading the pairs (not the nodes) over the threads shortens the longest
+  // chain nA-fold when nA is large (C3: 16 leaves); min over the leaves by shared atomics
+  for (int u = threadIdx.x; u < N * a.nA; u += blockDim.x) {
+    const int i = u / a.nA, b = u - i * a.nA;
     const int di = dep[i];
-    for (int b = 0; b < a.nA; ++b) {
-      int x = i, y = act[b];
-      int dx = di, dy = dep[y];
-      while (dx > dy) { x = par[x]; --dx; }
-      while (dy > dx) { y = par[y]; --dy; }
-      while (x != y) { x = par[x]; y = par[y]; --dx; }
-      const int dist = di + dep[act[b]] - 2 * dx;
-      best = dist < best ? dist : best;
-    }
-    dlt[i] = best;
+    int x = i, y = act[b];
+    int dx = di, dy = dep[y];
+    while (dx > dy) { x = par[x]; --dx; }
+    while (dy > dx) { y = par[y]; --dy; }
+    while (x != y) { x = par[x]; y = par[y]; --dx; }
+    const int dist = di + dep[act[b]] - 2 * dx;
+    if (a.nA == 1) dlt[i] = dist;     // one leaf: thread u owns node u (read back by it below)
+    else atomicMin(&dlt[i], dist);
   }
+  if (a.nA > 1) __syncthreads();
   pdl_wait();
   pdl_trigger();
+  TRACE(3);
   if (a.gate && *a.gate == 0) {   // the waterline did not fire: no Pressure (Alg. 2 l.31-33)
     for (int i = threadIdx.x; i < N; i += blockDim.x) a.k_out[i] = a.kcur[i];
     return;
@@ -406,7 +413,14 @@ allocate_kernel(AllocArgs a) {
       };
       int M = ncand;
       int stall = 0;
+#ifdef ARBOR_ALLOC_TRACE
+      int rounds = 0;
+      if (threadIdx.x == 0 && a.trace) a.trace[8] = ncand;
+#endif
       while (M > 0) {
+#ifdef ARBOR_ALLOC_TRACE
+        ++rounds;
+#endif
         const bool all = M <= nw || stall;   // test every remaining candidate this round
         const int P = all ? M : nw;
         // pivots: evenly spaced list entries (all entries when testing all)
@@ -488,6 +502,9 @@ allocate_kernel(AllocArgs a) {
       }
       __syncthreads();
       TRACE(4);
+#ifdef ARBOR_ALLOC_TRACE
+      if (threadIdx.x == 0 && a.trace) a.trace[7] = rounds;
+#endif
       const long long bnum = static_cast<long long>(best_num);
       const long long bden = static_cast<long long>(best_den);
       // classify the open interval just above β

@@ -30,21 +30,35 @@ def main():
     fn.argtypes = [C.c_void_p, C.c_void_p]
     fn.restype = C.c_int32
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-    sc = workload.setup(cfg, 0)
+    if cfg == "c3dpts":      # the DPTS loop's state (decode_step_prof.py c3dpts): 16 leaves
+        T, D = 6, 8
+        extra_nodes, extra_tokens, node_extra = workload.dpts_sizing(T, D)
+        sc = workload.setup("c3", 0, extra_tokens=extra_tokens, extra_nodes=extra_nodes,
+                            max_active=16, node_extra_tokens=node_extra)
+        workload.warmup_leaf_cycling(sc, 1)
+        run = workload.DptsRun(sc, n_active=16, transitions=T, swap=4, decode_steps=D, seed=0)
+        for leaves_t in [run.base_leaves] + run.schedule:
+            run.transition(leaves_t)
+            for _ in range(D):
+                run.decode()
+        sets = [list(sc.tree.active)] * 2
+    else:
+        sc = workload.setup(cfg, 0)
+        workload.warmup_leaf_cycling(sc, 1)
+        sets = [[x] for x in sorted(synth.leaves_of(sc.tree), key=lambda x: -float(sc.tree.v[x]))[:2]]
     ctx, tree = sc.ctx, sc.tree
-    workload.warmup_leaf_cycling(sc, 1)
     tr = torch.zeros(16, dtype=torch.int64, device="cuda")
     assert fn(ctx._ctx, C.c_void_p(tr.data_ptr())) == 0
-    leaves = sorted(synth.leaves_of(tree), key=lambda x: -float(tree.v[x]))[:2]
     s = torch.empty(tree.num_nodes, dtype=torch.float32, device="cuda")
     k = torch.empty(tree.num_nodes, dtype=torch.int32, device="cuda")
     B = sc.budget
     rows = []
     for i in range(20):
-        tree.active = [leaves[i % 2]]
-        q = sc.queries(10_000 + i, 1)
+        tree.active = sets[i % 2]
+        nA = len(tree.active)
+        q = sc.queries(10_000 + i, nA)
         out = torch.empty_like(q)
-        lse = torch.empty((1, ctx.L, ctx.Hq), dtype=torch.float32, device="cuda")
+        lse = torch.empty((nA, ctx.L, ctx.Hq), dtype=torch.float32, device="cuda")
         ctx.arbor_decode_step(tree, q, out, lse, s)
         tr.zero_()
         ctx.arbor_allocate(tree, s, B, k)
@@ -52,7 +66,9 @@ def main():
         rows.append(tr.cpu().numpy().copy())
     t = np.array(rows, dtype=np.float64)
     res = {}
-    for j in (1, 2, 4, 5, 6):
+    res["multisection_rounds"] = float(np.median(t[:, 7]))
+    res["breakpoints"] = float(np.median(t[:, 8]))
+    for j in (1, 2, 3, 4, 5, 6):
         ok = t[:, j] > 0
         if ok.any():
             res[f"t{j}_us"] = float(np.median((t[ok, j] - t[ok, 0]) / 1965.0))
