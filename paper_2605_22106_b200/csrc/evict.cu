@@ -37,6 +37,9 @@ constexpr int kUw = ARBOR_KUW;   // rows in flight per lane group of a move warp
 #ifndef ARBOR_JOB_SLOTS
 #define ARBOR_JOB_SLOTS 2
 #endif
+#ifndef ARBOR_EVICT_SLEEP_NS
+#define ARBOR_EVICT_SLEEP_NS 2000
+#endif
 constexpr int kJobSlots = ARBOR_JOB_SLOTS;   // job queue depth per pair (power of 2; 2, 4, 8 measured equal on C2)
 static_assert((kJobSlots & (kJobSlots - 1)) == 0, "job slots: a power of two");
 
@@ -68,19 +71,35 @@ struct CompactArgs {
   int wl_smem;      // N when the work list also lives in shared memory (N ≤ kSmemWorkNodes), else 0
   const int32_t *gate;   // f1 device waterline: nothing to do when *gate == 0 (else NULL)
 };
-constexpr int kSmemWorkNodes = 1024;   // 32 KB of work entries per CTA
+constexpr int kSmemWorkNodes = 1024;
+constexpr int kFinish = 32;   // radix passes stop once this few keys share the prefix (rank-count finish)   // 32 KB of work entries per CTA
 
 __device__ __forceinline__ long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return static_cast<long long>(t);
 }
+constexpr int kTraceSlots = 16;   // per warp: 8 events / counters + 8 select-phase cycle sums
+// select-phase cycle sums (debug builds with -DARBOR_EVICT_PHASES, trace slots 8-13): 0 data
+// wait + next issues, 1 key build, 2 threshold, 3 hole / mover lists, 4 job hand-off
+#ifdef ARBOR_EVICT_PHASES
+#define PH_MARK(i)                                      \
+  do {                                                  \
+    if (a.trace) {                                      \
+      const long long t_ = clock64();                   \
+      ph[i] += t_ - ph_t;                               \
+      ph_t = t_;                                        \
+    }                                                   \
+  } while (0)
+#else
+#define PH_MARK(i) do { } while (0)
+#endif
 // trace events per warp: 0 kernel start (after griddepcontrol.wait), 1 plan done,
 // 2 first job handed / started, 3 last job handed / done, 4 plan loads done, 5 plan scans done
 #define EV_TRACE(e)                                                                           \
   do {                                                                                        \
     if (a.trace && lane == 0)                                                                 \
-      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * 8 + (e)] = gtimer(); \
+      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + (e)] = gtimer(); \
   } while (0)
 
 
@@ -130,12 +149,13 @@ __device__ __forceinline__ void move_rows(int nm, Src src, Dst dst, char *kp8, c
 
 // Shared-memory layout of select_move_ws_kernel (per CTA), all offsets 16-byte aligned.
 struct WsLayout {
-  int cap, capP, pcap, jcap;
+  int cap, capA, capP, pcap, jcap;
   int wl_n;                                // nodes of the shared-memory work list (0: global)
   size_t keys, lists, abuf, pbuf, gbuf, mbuf, jobs, jcount, bars, iring, swl, total;
   __host__ __device__ WsLayout(int cap_, int lgP, int wl_n_) {
     cap = cap_;
     wl_n = wl_n_;
+    capA = (cap + 9) & ~3;                 // A span from its 16-byte-aligned start (≤ 3 floats before)
     capP = (cap + (1 << lgP) + 9) & ~7;   // pos tags by page-list slot from soff mod P (+1: pairs)
     pcap = (cap >> lgP) + 2;
     jcap = cap / 2 + 1;                    // moves per item ≤ min(k_app, k_cur − k_app)
@@ -143,7 +163,7 @@ struct WsLayout {
     auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 15) & ~size_t(15); return r; };
     keys = take(size_t(kPairsWs) * cap * 8);              // u64 keys
     lists = take(size_t(kPairsWs) * 2 * cap * 4);         // holes | movers
-    abuf = take(size_t(kPairsWs) * 2 * cap * 4);          // A span, 2 pipeline slots
+    abuf = take(size_t(kPairsWs) * 2 * capA * 4);         // A span, 2 pipeline slots
     pbuf = take(size_t(kPairsWs) * 2 * capP * 2);         // pos tags, 2 pipeline slots
     gbuf = take(size_t(kPairsWs) * 3 * pcap * 4);         // page lists, 3 pipeline slots
     mbuf = take(size_t(kPairsWs) * 4 * sizeof(WorkEnt));  // work entries, 4 pipeline slots
@@ -182,13 +202,13 @@ select_move_ws_kernel(CompactArgs a) {
   const bool mover = warp >= kPairsWs;
   const int pid = mover ? warp - kPairsWs : warp;
   const WsLayout Ly(a.cap, a.lgP, a.wl_smem);
-  const int cap = Ly.cap, capP = Ly.capP, pcap = Ly.pcap, jcap = Ly.jcap;
+  const int cap = Ly.cap, capA = Ly.capA, capP = Ly.capP, pcap = Ly.pcap, jcap = Ly.jcap;
   const int lgP = a.lgP, Pm = (1 << lgP) - 1;
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm + Ly.bars);
   uint64_t *full = bars + pid * 2 * kJobSlots, *empty = full + kJobSlots;
   int2 *myjobs = reinterpret_cast<int2 *>(sm + Ly.jobs) + pid * kJobSlots * jcap;
   int32_t *mycount = reinterpret_cast<int32_t *>(sm + Ly.jcount) + pid * kJobSlots;
-  __shared__ uint32_t hist_all[kPairsWs][256];
+  __shared__ __align__(16) uint32_t hist_all[kPairsWs][256];
   using Scan = cub::BlockScan<int, kPairsWs * 64>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ int s_work, s_free, s_apply;
@@ -324,7 +344,10 @@ select_move_ws_kernel(CompactArgs a) {
     for (int k = 0;; ++k) {
       const int sl = k & (kJobSlots - 1);
       const long long tw0 = a.trace ? clock64() : 0;
-      mbar_wait(&full[sl], (k / kJobSlots) & 1);
+      // a starved move warp sleeps in the try_wait instead of spinning: its spin loop took
+      // ~18% of the kernel's issued instructions from the select warps it waits for
+      if (ARBOR_EVICT_SLEEP_NS) mbar_wait_sleep(&full[sl], (k / kJobSlots) & 1, ARBOR_EVICT_SLEEP_NS);
+      else mbar_wait(&full[sl], (k / kJobSlots) & 1);
       if (a.trace && k > 0) w_full += clock64() - tw0;
       if (k == 0) EV_TRACE(2);
       const int cnt = mycount[sl];
@@ -342,9 +365,9 @@ select_move_ws_kernel(CompactArgs a) {
     if (a.trace && lane == 0) {   // diagnostics: SM id, jobs and rows this move warp handled
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * 8 + 7] =
+      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 7] =
           (static_cast<long long>(smid) << 40) | (static_cast<long long>(k_jobs) << 20) | mv_rows;
-      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * 8 + 6] = w_full;   // cycles
+      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 6] = w_full;   // cycles
     }
     return;
   }
@@ -352,7 +375,7 @@ select_move_ws_kernel(CompactArgs a) {
   unsigned long long *key = reinterpret_cast<unsigned long long *>(sm + Ly.keys) + pid * cap;
   int32_t *holes = reinterpret_cast<int32_t *>(sm + Ly.lists) + pid * 2 * cap;
   int32_t *movers = holes + cap;
-  float *Abuf = reinterpret_cast<float *>(sm + Ly.abuf) + pid * 2 * cap;
+  float *Abuf = reinterpret_cast<float *>(sm + Ly.abuf) + pid * 2 * capA;
   int16_t *Pbuf = reinterpret_cast<int16_t *>(sm + Ly.pbuf) + pid * 2 * capP;
   int32_t *Gbuf = reinterpret_cast<int32_t *>(sm + Ly.gbuf) + pid * 3 * pcap;
   WorkEnt *Mbuf = reinterpret_cast<WorkEnt *>(sm + Ly.mbuf) + pid * 4;
@@ -414,16 +437,25 @@ select_move_ws_kernel(CompactArgs a) {
     for (int c = (sb & ~1) + 2 * lane; c < sb + e.kc; c += 64)
       cp_async4(pb + c, a.pos + base + static_cast<int64_t>(g[c >> lgP]) * pstride + (c & Pm));
   };
+  // the A row of pipeline step k's item over its span (A is read by position)
+  auto a_row = [&](int k) -> const float * {
+    const WorkEnt &e = meta(k);
+    const int r = item_of(k) - wring[k & 3] * a.R;
+    return a.Ahat ? a.Ahat + e.span : a.A + static_cast<int64_t>(r) * a.max_tokens + e.span;
+  };
+  // 16-byte cp.async from the span's aligned start: float p of the span lands at ab[mis + p]
+  // (an aligned 16-byte chunk that overlaps the row never leaves its allocation)
   auto issue_A = [&](int k) {
     const int it = item_of(k);
     if (it >= items) return;
     const WorkEnt &e = meta(k);
     const int tl = min(a.l_tail, e.n);
     if (e.ka > tl && a.select_mode == ARBOR_SELECT_HEAVY) {   // ranked by A: the non-tail span
-      const int r = it - wring[k & 3] * a.R;
-      const float *Arow = a.Ahat ? a.Ahat + e.span : a.A + static_cast<int64_t>(r) * a.max_tokens + e.span;
-      float *ab = Abuf + (k & 1) * cap;
-      for (int p = lane; p < e.n - tl; p += 32) cp_async4(ab + p, Arow + p);
+      const uintptr_t ar = reinterpret_cast<uintptr_t>(a_row(k));
+      const char *a0 = reinterpret_cast<const char *>(ar & ~uintptr_t(15));
+      const int nch = (static_cast<int>((ar & 15) >> 2) + e.n - tl + 3) >> 2;
+      float *ab = Abuf + (k & 1) * capA;
+      for (int c = lane; c < nch; c += 32) cp_async16(ab + 4 * c, a0 + 16 * c);
     }
   };
   // the first four items of select warp w are 4w … 4w + 3 (no atomic storm at the start);
@@ -456,6 +488,10 @@ select_move_ws_kernel(CompactArgs a) {
   cp_async_commit();
   int k = 0;
   long long w_empty = 0;
+#ifdef ARBOR_EVICT_PHASES
+  long long ph[5] = {0, 0, 0, 0, 0};
+  long long ph_t = clock64();
+#endif
   for (;; ++k) {
     const int it = item_of(k);
     if (it >= items) break;          // the counter only grows: every later draw is past the end
@@ -468,6 +504,7 @@ select_move_ws_kernel(CompactArgs a) {
     issue_pages(k + 2);
     issue_meta(k + 3);
     cp_async_commit();
+    PH_MARK(0);
     // ---- rank item k from shared memory
     const WorkEnt e = meta(k);
     const bool ident = e.kc == e.n && e.so == 0;
@@ -477,7 +514,8 @@ select_move_ws_kernel(CompactArgs a) {
     const int tl = min(a.l_tail, n);
     const int32_t *pgs = Gbuf + (k % 3) * pcap;
     const int16_t *pb = Pbuf + (k & 1) * capP;
-    const float *ab = Abuf + (k & 1) * cap;
+    const float *ab = Abuf + (k & 1) * capA +
+                      ((reinterpret_cast<uintptr_t>(a_row(k)) & 15) >> 2);
     const int64_t base = row_base(it, wring[k & 3]);
     auto row = [&](int slot) -> int64_t {
       const int c = sb + slot;
@@ -520,6 +558,7 @@ select_move_ws_kernel(CompactArgs a) {
       ncand += __popc(__ballot_sync(0xffffffffu, (kk & kCand) != 0));
     }
     __syncwarp();
+    PH_MARK(1);
     // threshold: keep a candidate iff (key & tmask) >= tkey (the top m unique keys)
     unsigned long long tkey = kCand, tmask = kCand;     // m ≥ ncand: all candidates
     if (ranked && m <= 0) {
@@ -535,11 +574,12 @@ select_move_ws_kernel(CompactArgs a) {
       const int top = sink_all != sink_any ? 48
                       : bmin != bmax ? 16 + 31 - __clz(static_cast<int>(bmin ^ bmax)) : 15;
       unsigned long long prefix = kCand, pmask = kCand;
-      int need = m;
-      for (int shift = top - 7; shift > -8; shift -= 8) {
+      int need = m, inb = ncand;   // the need-th largest of the inb keys matching prefix
+      // 8-bit digit passes while more than kFinish keys share the prefix
+      for (int shift = top - 7; shift > -8 && inb > kFinish && need < inb; shift -= 8) {
         const unsigned long long dmask = shift >= 0 ? 255ull << shift : 255ull >> -shift;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) hist[lane * 8 + b] = 0;
+        reinterpret_cast<uint4 *>(hist)[2 * lane] = make_uint4(0u, 0u, 0u, 0u);
+        reinterpret_cast<uint4 *>(hist)[2 * lane + 1] = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
         for (int s = lane; s < kc; s += 32) {
           const unsigned long long kk = key[s];
@@ -550,10 +590,13 @@ select_move_ws_kernel(CompactArgs a) {
           }
         }
         __syncwarp();
-        uint32_t cnt8[8];
+        // lane j scans digits 255 − 8j … 248 − 8j (descending): bins 8(31 − j) … 8(31 − j) + 7
+        const uint4 h0 = reinterpret_cast<const uint4 *>(hist)[2 * (31 - lane)];
+        const uint4 h1 = reinterpret_cast<const uint4 *>(hist)[2 * (31 - lane) + 1];
+        const uint32_t cnt8[8] = {h1.w, h1.z, h1.y, h1.x, h0.w, h0.z, h0.y, h0.x};
         uint32_t loc = 0;
 #pragma unroll
-        for (int b = 0; b < 8; ++b) { cnt8[b] = hist[255 - lane * 8 - b]; loc += cnt8[b]; }
+        for (int b = 0; b < 8; ++b) loc += cnt8[b];
         uint32_t incl = loc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -585,11 +628,37 @@ select_move_ws_kernel(CompactArgs a) {
         prefix |= shift >= 0 ? static_cast<unsigned long long>(dsel) << shift
                              : static_cast<unsigned long long>(dsel) >> -shift;
         pmask |= dmask;
-        if (static_cast<uint32_t>(need) == inbin) break;   // the whole bin survives
+        inb = static_cast<int>(inbin);
       }
       tkey = prefix;
       tmask = pmask;
+      if (need < inb) {
+        // finish (≤ kFinish keys left in the prefix's bin): gather them, one per lane, and
+        // take the one with exactly need − 1 larger keys (keys are unique) — replaces the
+        // remaining digit passes; `holes` is scratch here (written only below)
+        unsigned long long *bin = reinterpret_cast<unsigned long long *>(holes);
+        int c = 0;
+        for (int s0 = 0; s0 < kc; s0 += 32) {
+          const int s = s0 + lane;
+          const unsigned long long kk = s < kc ? key[s] : 0ull;
+          const bool in = s < kc && (kk & pmask) == prefix;
+          const unsigned bb = __ballot_sync(0xffffffffu, in);
+          if (in) bin[c + __popc(bb & lt_mask)] = kk;
+          c += __popc(bb);
+        }
+        __syncwarp();
+        const unsigned long long mk = lane < inb ? bin[lane] : 0ull;
+        int gt = 0;
+        for (int j = 0; j < inb; ++j) gt += __shfl_sync(0xffffffffu, mk, j) > mk ? 1 : 0;
+        const unsigned hit = __ballot_sync(0xffffffffu, lane < inb && gt == need - 1);
+        if (hit) {                        // else non-unique keys (corrupted state): latched below
+          tkey = __shfl_sync(0xffffffffu, mk, __ffs(hit) - 1);
+          tmask = ~0ull;
+        }
+        __syncwarp();
+      }
     }
+    PH_MARK(2);
     // keep flags → holes (dropped slots of the window [k_cur − k_app, k_cur)) and movers
     // (kept slots before it), ascending
     const int w0 = kc - ka;
@@ -617,10 +686,12 @@ select_move_ws_kernel(CompactArgs a) {
     // pairs that exist, so a corrupted state can never produce out-of-range rows
     if (nh != nm && lane == 0 && !a.exp) atomicOr(&a.ctrl->err, DERR_STATE);
     nm = nm < nh ? nm : nh;
+    PH_MARK(3);
     // hand the job to the move warp
     const int sl = k & (kJobSlots - 1);
     const long long tw0 = a.trace ? clock64() : 0;
-    mbar_wait(&empty[sl], ((k / kJobSlots) & 1) ^ 1);
+    if (ARBOR_EVICT_SLEEP_NS) mbar_wait_sleep(&empty[sl], ((k / kJobSlots) & 1) ^ 1, ARBOR_EVICT_SLEEP_NS);
+    else mbar_wait(&empty[sl], ((k / kJobSlots) & 1) ^ 1);
     if (a.trace) w_empty += clock64() - tw0;
     int2 *jb = myjobs + sl * jcap;
     for (int i = lane; i < nm; i += 32)
@@ -633,7 +704,15 @@ select_move_ws_kernel(CompactArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&full[sl]);
     if (k == 0) EV_TRACE(2);
+    PH_MARK(4);
   }
+#ifdef ARBOR_EVICT_PHASES
+  if (a.trace && lane == 0)
+    for (int i = 0; i < 5; ++i)
+      a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 8 + i] = ph[i];
+  if (a.trace && lane == 0)
+    a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 13] = k;
+#endif
   cp_async_wait_all();               // prefetches past the end (none were issued, but be tidy)
   // end marker for the move warp
   {
@@ -655,7 +734,7 @@ select_move_ws_kernel(CompactArgs a) {
   }
   EV_TRACE(3);
   if (a.trace && lane == 0)   // diagnostics: cycles this select warp waited for a free job slot
-    a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * 8 + 7] = w_empty;
+    a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 7] = w_empty;
 }
 
 }  // namespace
@@ -729,7 +808,7 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n, bool 
   static long long *trace = nullptr;
   static size_t trace_n = 0;
   if (getenv("ARBOR_EVICT_TRACE")) {
-    const size_t need = static_cast<size_t>(c->num_sms) * kEvictCtasPerSm * 2 * kPairsWs * 8;
+    const size_t need = static_cast<size_t>(c->num_sms) * kEvictCtasPerSm * 2 * kPairsWs * kTraceSlots;
     if (need > trace_n) {
       if (trace) cudaFree(trace);
       cudaMalloc(&trace, need * sizeof(long long));

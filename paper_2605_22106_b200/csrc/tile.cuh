@@ -148,6 +148,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+// Blocking wait for a role that may wait long (e.g. a consumer starved by its producer): the
+// try_wait suspends the warp for up to `hint_ns` instead of returning at once, so the waiting
+// warp does not spin issue slots away from the warps it waits for.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t hint_ns) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity), "r"(hint_ns) : "memory");
+}
 // 1-D bulk copy global → shared (TMA engine), completing `bytes` on the mbarrier.
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(

@@ -47,11 +47,11 @@ def main():
     del os.environ["ARBOR_EVICT_TRACE"]
     lib = pk.load_library()
     ctas = torch.cuda.get_device_properties(0).multi_processor_count * 2
-    n = ctas * 16 * 8
+    n = ctas * 16 * 16
     buf = (C.c_longlong * n)()
     lib.arbor_debug_evict_trace.argtypes = [C.POINTER(C.c_longlong), C.c_longlong]
     assert lib.arbor_debug_evict_trace(buf, n) == 0
-    tr = np.frombuffer(buf, dtype=np.int64).reshape(ctas, 16, 8).astype(np.float64)
+    tr = np.frombuffer(buf, dtype=np.int64).reshape(ctas, 16, 16).astype(np.float64)
     t0 = tr[:, :, 0][tr[:, :, 0] > 0].min()
     rel = (tr - t0) / 1e3
     valid = tr > 0
@@ -85,6 +85,12 @@ def main():
     # cycles → µs at 1.965 GHz: move warps waiting for a job, select warps waiting for a slot
     res["move_wait_full_us"] = pct(np.where(ok, tr[:, mov, 6] / 1965.0, np.nan).ravel())
     res["select_wait_empty_us"] = pct(np.where(valid[:, sel, 3], tr[:, sel, 7] / 1965.0, np.nan).ravel())
+    if (tr[:, sel, 8:13] > 0).any():   # -DARBOR_EVICT_PHASES builds: select-phase µs per warp
+        names = ["wait_issue", "keys", "threshold", "lists", "handoff"]
+        okk = valid[:, sel, 3]
+        res["select_phase_us"] = {nm: pct(np.where(okk, tr[:, sel, 8 + i] / 1965.0, np.nan).ravel())
+                                  for i, nm in enumerate(names)}
+        res["select_items"] = pct(np.where(okk, tr[:, sel, 13], np.nan).ravel())
     late = np.argsort(np.where(ok, done, -1).ravel())[::-1][:12]
     res["latest_moves"] = [{"cta": int(i // 8), "sm": int(smid.ravel()[i]), "jobs": int(jobs.ravel()[i]),
                             "rows": int(rows.ravel()[i]), "done": round(float(done.ravel()[i]), 2)}
