@@ -72,7 +72,10 @@ struct CompactArgs {
   const int32_t *gate;   // f1 device waterline: nothing to do when *gate == 0 (else NULL)
 };
 constexpr int kSmemWorkNodes = 1024;
-constexpr int kFinish = 32;   // radix passes stop once this few keys share the prefix (rank-count finish)   // 32 KB of work entries per CTA
+constexpr int kFinish = 32;
+// slot loops of the select warp are kept rolled: unrolling them 2x / 4x measured slower (C5
+// select_compact 278 -> 294-296 us; C2 113 -> 114-115 us), as did the compiler's default
+constexpr int kSelUnroll = 1;   // radix passes stop once this few keys share the prefix (rank-count finish)   // 32 KB of work entries per CTA
 
 __device__ __forceinline__ long long gtimer() {
   unsigned long long t;
@@ -527,6 +530,7 @@ select_move_ws_kernel(CompactArgs a) {
     int ncand = 0;
     uint32_t bmin = 0xffffffffu, bmax = 0u;
     unsigned sink_all = 1u, sink_any = 0u;
+#pragma unroll kSelUnroll
     for (int s0 = 0; s0 < kc; s0 += 32) {
       const int s = s0 + lane;
       unsigned long long kk = 0;
@@ -581,6 +585,7 @@ select_move_ws_kernel(CompactArgs a) {
         reinterpret_cast<uint4 *>(hist)[2 * lane] = make_uint4(0u, 0u, 0u, 0u);
         reinterpret_cast<uint4 *>(hist)[2 * lane + 1] = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
+#pragma unroll kSelUnroll
         for (int s = lane; s < kc; s += 32) {
           const unsigned long long kk = key[s];
           if ((kk & pmask) == prefix) {
@@ -638,7 +643,8 @@ select_move_ws_kernel(CompactArgs a) {
         // remaining digit passes; `holes` is scratch here (written only below)
         unsigned long long *bin = reinterpret_cast<unsigned long long *>(holes);
         int c = 0;
-        for (int s0 = 0; s0 < kc; s0 += 32) {
+    #pragma unroll kSelUnroll
+    for (int s0 = 0; s0 < kc; s0 += 32) {
           const int s = s0 + lane;
           const unsigned long long kk = s < kc ? key[s] : 0ull;
           const bool in = s < kc && (kk & pmask) == prefix;
@@ -663,6 +669,7 @@ select_move_ws_kernel(CompactArgs a) {
     // (kept slots before it), ascending
     const int w0 = kc - ka;
     int nh = 0, nm = 0;
+#pragma unroll kSelUnroll
     for (int s0 = 0; s0 < kc; s0 += 32) {
       const int s = s0 + lane;
       int keep = 0;

@@ -47,6 +47,10 @@ def main():
                 pass
     tot = sum(samples.values()) or 1
     print(f"total samples {tot}, instructions {sum(insts.values())}")
+    agg = collections.Counter()
+    for c in why.values():
+        agg.update(c)
+    print("stall reasons (all lines):", ", ".join(f"{k[6:]} {v}" for k, v in agg.most_common(10)))
     for (f, ln), s in samples.most_common(top):
         top3 = ", ".join(f"{k[6:]} {v}" for k, v in why[(f, ln)].most_common(3))
         print(f"{f}:{ln:<5d} samples {s:6d} ({100 * s / tot:4.1f}%)  insts {insts[(f, ln)]:10d}  [{top3}]")

@@ -187,9 +187,14 @@ int main(int argc, char **argv) {
     printf("%-28s best %8.2f us  mean %8.2f us  %7.1f GB/s (best)\n", name, best * 1e3, sum / 10 * 1e3,
            bytes / (best * 1e-3) / 1e9);
   };
-  timeit("reg U=4 (2 CTA/SM x16w)", [&] { reg_move<4><<<sms * 2, 512>>>(jobs, M, kp, vp, pos, ctr); });
-  timeit("reg U=2", [&] { reg_move<2><<<sms * 2, 512>>>(jobs, M, kp, vp, pos, ctr); });
-  timeit("reg U=8", [&] { reg_move<8><<<sms * 2, 512>>>(jobs, M, kp, vp, pos, ctr); });
+  for (int wps : {32, 16, 12, 8, 6}) {   // moving warps per SM (2 CTAs)
+    char nm[64];
+    snprintf(nm, sizeof nm, "reg U=4 %d warps/SM", wps);
+    timeit(nm, [&] { reg_move<4><<<sms * 2, wps * 16>>>(jobs, M, kp, vp, pos, ctr); });
+    snprintf(nm, sizeof nm, "reg U=6 %d warps/SM", wps);
+    timeit(nm, [&] { reg_move<6><<<sms * 2, wps * 16>>>(jobs, M, kp, vp, pos, ctr); });
+  }
+  if (argc > 3) return 0;
   for (int W : {2, 3, 4}) {
     for (int S : {3, 4}) {
       const size_t smem = static_cast<size_t>(W) * 32 * S * 2 * RB + W * 32 * S * 8;
