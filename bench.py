@@ -670,10 +670,10 @@ def main():
         path = synth_path(tree.parent, tree.active[0])
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         r0 = ctx.arbor_read_counters()[0]
-        # PCIe bytes: the full spans of the path nodes that lost tokens (k_cur < n)
-        need = [x for x in path if ctx.arbor_read_node(x)[0] < int(tree.span_len[x])]
-        nbytes = sum(int(tree.span_len[x]) for x in need) * ctx.L * ctx.H * ctx.D * 2 * (
-            2 if preset["dtype"] == "bf16" else 4)
+        # PCIe bytes: the evicted rows (n − k_cur) of the path nodes (Q23r: the
+        # kept rows are restored within HBM)
+        miss = sum(int(tree.span_len[x]) - ctx.arbor_read_node(x)[0] for x in path)
+        nbytes = miss * ctx.L * ctx.H * ctx.D * 2 * (2 if preset["dtype"] == "bf16" else 4)
         torch.cuda.synchronize()
         a.record(stream)
         ctx.arbor_rehydrate(ta, path)
@@ -788,11 +788,10 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
         r0 = ctx.arbor_read_counters()[0]
         k = run.k_buf[:tree.num_nodes]
         path = [x for x in run.path_union() if not tree.is_open[x]]
-        rbytes = 0                                  # PCIe bytes: only nodes with k_cur < n
+        rbytes = 0                                  # PCIe bytes: the evicted rows only (Q23r)
         for x in path:
             kc_x, n_x, _ = ctx.arbor_read_node(x)
-            if kc_x < n_x:
-                rbytes += n_x * rows * 2 * rb
+            rbytes += (n_x - kc_x) * rows * 2 * rb
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         rs, rd = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()

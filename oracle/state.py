@@ -306,11 +306,18 @@ class ArborOracle:
 
     # ------------------------------------------------------------ rehydrate
     def rehydrate(self, nodes) -> int:
-        """Lazy rehydration (Alg. 2): a node with
-        k_cur < n gets its full span back (bit-exact copy of the stash, Q20);
-        pages popped in ascending node order (appended to the node's live
-        list, which then holds slots 0.. from its first page: koff = 0); full
-        nodes are a no-op and are not counted."""
+        """Lazy rehydration (Alg. 2): a node with k_cur < n gets its
+        full span back (bit-exact copy of the stash, Q20); full nodes are a no-op and are
+        not counted.
+
+        Slot layout (reading Q23r, a paging choice: the paper fixes only that the
+        full span is restored).  An evicted closed block's k_cur retained rows fill the last
+        k_cur of its n page-list slots (end-window compaction, Q23*, never moves the end);
+        its ⌊(n - k_cur)/P⌋ freed leading pages are popped again, nodes ascending, in list
+        order, koff ← 0, and every position p goes back to slot p (a full block holds its
+        positions in slot order).  Only the n - k_cur evicted rows cross PCIe; the retained
+        ones are moved within HBM.  A block evicted to 0 holds no pages: ⌈n/P⌉ are popped.
+        """
         nodes = sorted(set(int(x) for x in nodes))
         for i in nodes:
             if self.open[i]:
@@ -319,15 +326,18 @@ class ArborOracle:
             return 0
         count = 0
         for i in nodes:
-            n = self.n[i]
-            if self.k_cur(i) == n:
+            n, kc = self.n[i], self.k_cur(i)
+            if kc == n:
                 continue
-            need = -(-n // self.P) - len(self.pages[i])
-            for _ in range(need):
-                self.pages[i].append(self._pop())
+            if kc == 0:                           # no pages left: a fresh list
+                lead = -(-n // self.P)
+            else:                                 # the freed leading pages of the list
+                slots = n - kc - self.koff[i]
+                assert slots >= 0 and slots % self.P == 0, "closed block: window ends at slot n"
+                lead = slots // self.P
+            self.pages[i] = [self._pop() for _ in range(lead)] + self.pages[i]
+            self.kept[i] = np.broadcast_to(np.arange(n, dtype=np.int64), (self.L, self.H, n)).copy()
             self.koff[i] = 0
-            self.kept[i] = np.broadcast_to(np.arange(n, dtype=np.int64),
-                                           (self.L, self.H, n)).copy()
             count += 1
         self.rehydrations += count
         return count

@@ -829,6 +829,7 @@ void arbor_destroy(arbor_ctx *c) {
       for (int r = 0; r < kStageRing; ++r)
         for (int j = 0; j < 2; ++j) if (c->st_ev[i][r][j]) cudaEventDestroy(c->st_ev[i][r][j]);
   if (c->own_stash && c->stash_host) cudaFreeHost(c->stash_host);
+  if (c->rehyd_scratch) cudaFree(c->rehyd_scratch);
   if (c->own_ms) cudaStreamDestroy(c->ms);
   if (c->own_ss) cudaStreamDestroy(c->ss);
   delete c;

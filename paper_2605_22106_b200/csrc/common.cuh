@@ -188,6 +188,10 @@ struct arbor_ctx {
   void *stash_host = nullptr;   // host pointer
   void *stash_dev = nullptr;    // device-visible pointer to the same memory
   bool own_stash = false;
+  // rehydration: per-CTA staging of the retained rows that change slot (Q23r),
+  // grown on demand
+  void *rehyd_scratch = nullptr;
+  size_t rehyd_scratch_bytes = 0;
   cudaEvent_t ev_main_to_side = nullptr, ev_side_done = nullptr;
   // lazy rehydration ("before the next decoding step"): the main stream waits for the
   // side-stream copy only when a call next reads or moves pool rows (attention, evict)

@@ -111,9 +111,12 @@ __global__ void stash_kernel(PoolArgs g, const int32_t *ptab, int node, int n, i
   }
 }
 
-// Rehydrate plan: nodes ascending; a node with k_cur < n gets its pages and k_cur = n.
-// Its live pages (from the one holding slot soff, Q23*) move to the front of its
-// list and soff = 0, then pages are popped up to ⌈n/P⌉ (oracle/state.rehydrate).
+// Rehydrate plan: nodes ascending; a node with k_cur < n gets its pages and k_cur = n
+// (oracle/state.rehydrate, Q23r).  A closed block's kept window ends at slot n
+// (end-window compaction, Q23*: soff + k_cur = n), so the evicted positions go to the slots
+// 0 … soff − 1 before it: the ⌊soff/P⌋ stale leading list entries get freshly popped pages (list
+// order), the first live page's slots below soff are free already; soff ← 0.  A node evicted
+// to 0 (no pages) pops ⌈n/P⌉.  flag[i] = old k_cur + 1 for a restored node, 0 otherwise.
 // keep_floor > 0 (the controller's Transition under params.k_protect): only nodes
 // below min(n, keep_floor) are restored (to the full span).
 __global__ void rehydrate_plan_kernel(Ctrl *ctrl, int32_t *free_stack, int32_t *npages,
@@ -124,55 +127,104 @@ __global__ void rehydrate_plan_kernel(Ctrl *ctrl, int32_t *free_stack, int32_t *
   for (int i = 0; i < count; ++i) {
     const int node = nodes[i];
     flag[i] = 0;
-    if (kcur[node] >= n[node]) continue;   // full: no-op, not counted
-    if (keep_floor > 0 && kcur[node] >= min(n[node], keep_floor)) continue;
-    const int first = soff[node] / P;
-    if (first > 0) {
+    const int kc = kcur[node], nn = n[node];
+    if (kc >= nn) continue;   // full: no-op, not counted
+    if (keep_floor > 0 && kc >= min(nn, keep_floor)) continue;
+    if (kc == 0) {
+      soff[node] = 0;
+      if (!pop_pages(ctrl, free_stack, npages, ptab, MPN, P, node, nn)) continue;
+    } else {
+      const int lead = soff[node] / P;
+      if (soff[node] + kc != nn || lead > ctrl->free_top) {
+        ctrl->err |= soff[node] + kc != nn ? DERR_STATE : DERR_OUT_OF_PAGES;
+        continue;
+      }
       int32_t *pl = ptab + static_cast<int64_t>(node) * MPN;
-      for (int i = first; i < npages[node]; ++i) pl[i - first] = pl[i];
-      npages[node] -= first;
+      for (int e = 0; e < lead; ++e) pl[e] = free_stack[--ctrl->free_top];
+      ctrl->pages_in_use += lead;
+      soff[node] = 0;
     }
-    soff[node] = 0;
-    if (!pop_pages(ctrl, free_stack, npages, ptab, MPN, P, node, n[node])) continue;
-    kcur[node] = n[node];
-    flag[i] = 1;
+    flag[i] = kc + 1;
+    kcur[node] = nn;
     ++done;
   }
   ctrl->rehydrations += done;
   ctrl->rehyd_count = done;
 }
 
-// stash → pages, pos = slot; work unit = (listed node i, row r, token chunk of 64), grid-stride
+// stash → the evicted rows of each restored node (Q23r): work unit = (listed node,
+// row), grid-stride over a small persistent grid (PCIe, not the SMs, is the limit).  The
+// k_old kept rows sit in slots n − k_old … n − 1; position p must end in slot p.  Pass 1 reads
+// their pos tags into a shared-memory bitmap and stages every kept row that changes slot in
+// this CTA's scratch (HBM; its reads of the window all precede pass 2); pass 2 writes the
+// staged rows to their slots and copies each missing position from the stash.  Only the
+// n − k_old evicted rows cross PCIe (a node evicted to 0: all n).
 __global__ void rehydrate_copy_kernel(PoolArgs g, const int32_t *ptab, const int32_t *nodes,
-                                      const int32_t *flag, const int32_t *n, const int64_t *span,
-                                      const char *stash, char *kpool, char *vpool, int16_t *pos,
-                                      int count, int nch) {
+                                      const int32_t *flag, const int32_t *n,
+                                      const int64_t *span, const char *stash, char *kpool,
+                                      char *vpool, int16_t *pos, int count, char *scratch,
+                                      int max_n) {
+  extern __shared__ __align__(16) uint32_t rsm[];   // bitmap [nw] | kept positions [max_n] int16
   const int rb = g.D * g.esize, cpr = rb / 16;
-  const int lgP = 31 - __clz(g.P);
+  const int lgP = 31 - __clz(g.P), Pm = g.P - 1;
   const int64_t plane = static_cast<int64_t>(g.L) * g.H * g.max_tokens * rb;
   const int rows = g.L * g.H;
-  for (int u = blockIdx.x; u < count * rows * nch; u += gridDim.x) {
-    const int i = u / (rows * nch);
-    const int rem = u - i * rows * nch;
-    const int r = rem / nch, t0 = (rem - r * nch) * 64;
-    if (!flag[i]) continue;
+  char *stage = scratch + static_cast<int64_t>(blockIdx.x) * max_n * 2 * rb;   // [k][K|V]
+  for (int u = blockIdx.x; u < count * rows; u += gridDim.x) {
+    const int i = u / rows, r = u - i * rows;
+    const int fl = flag[i];
+    if (!fl) continue;                   // uniform over the CTA
+    const int kold = fl - 1;
     const int node = nodes[i];
-    const int nn = n[node];
-    if (t0 >= nn) continue;
-    const int nt = min(64, nn - t0);
+    const int nn = n[node], w0 = nn - kold;
     const int l = r / g.H, h = r - l * g.H;
     const int32_t *pl = ptab + static_cast<int64_t>(node) * g.MPN;
     const int64_t a0 = span[node];
-    for (int idx = threadIdx.x; idx < nt * cpr; idx += blockDim.x) {
-      const int tt = idx / cpr, cc = idx - tt * cpr;
-      const int slot = t0 + tt;
-      const int64_t row = prow(g, l, pl[slot >> lgP], h, slot & (g.P - 1));
-      const int64_t src = ((static_cast<int64_t>(r)) * g.max_tokens + a0 + slot) * rb + cc * 16;
+    const int nw = (nn + 31) >> 5;
+    uint32_t *bits = rsm;
+    int16_t *kp = reinterpret_cast<int16_t *>(rsm + nw);
+    auto row_of = [&](int slot) { return prow(g, l, pl[slot >> lgP], h, slot & Pm); };
+    for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0u;
+    __syncthreads();
+    if (kold > 0) {
+      for (int j = threadIdx.x; j < kold; j += blockDim.x) {
+        const int p = pos[row_of(w0 + j)];
+        kp[j] = static_cast<int16_t>(p);
+        if (p >= 0 && p < nn) atomicOr(&bits[p >> 5], 1u << (p & 31));
+      }
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < kold * cpr; idx += blockDim.x) {
+        const int j = idx / cpr, cc = idx - j * cpr;
+        if (kp[j] == w0 + j) continue;   // already in its slot
+        const int64_t src = row_of(w0 + j) * rb + cc * 16;
+        char *st = stage + static_cast<int64_t>(j) * 2 * rb + cc * 16;
+        *reinterpret_cast<uint4 *>(st) = *reinterpret_cast<const uint4 *>(kpool + src);
+        *reinterpret_cast<uint4 *>(st + rb) = *reinterpret_cast<const uint4 *>(vpool + src);
+      }
+      __syncthreads();                   // every window read is done before any slot is written
+      for (int idx = threadIdx.x; idx < kold * cpr; idx += blockDim.x) {
+        const int j = idx / cpr, cc = idx - j * cpr;
+        const int p = kp[j];
+        if (p == w0 + j || p < 0 || p >= nn) continue;
+        const int64_t dst = row_of(p);
+        const char *st = stage + static_cast<int64_t>(j) * 2 * rb + cc * 16;
+        *reinterpret_cast<uint4 *>(kpool + dst * rb + cc * 16) = *reinterpret_cast<const uint4 *>(st);
+        *reinterpret_cast<uint4 *>(vpool + dst * rb + cc * 16) = *reinterpret_cast<const uint4 *>(st + rb);
+        if (cc == 0) pos[dst] = static_cast<int16_t>(p);
+      }
+    }
+    // the missing positions, from the stash over PCIe (16-byte zero-copy reads)
+    for (int idx = threadIdx.x; idx < nn * cpr; idx += blockDim.x) {
+      const int p = idx / cpr, cc = idx - p * cpr;
+      if (bits[p >> 5] & (1u << (p & 31))) continue;
+      const int64_t row = row_of(p);
+      const int64_t src = ((static_cast<int64_t>(r)) * g.max_tokens + a0 + p) * rb + cc * 16;
       *reinterpret_cast<uint4 *>(kpool + row * rb + cc * 16) = *reinterpret_cast<const uint4 *>(stash + src);
       *reinterpret_cast<uint4 *>(vpool + row * rb + cc * 16) =
           *reinterpret_cast<const uint4 *>(stash + plane + src);
-      if (cc == 0) pos[row] = static_cast<int16_t>(slot);
+      if (cc == 0) pos[row] = static_cast<int16_t>(p);
     }
+    __syncthreads();                     // the next unit reuses the bitmap, list and staging
   }
 }
 
@@ -215,12 +267,28 @@ void launch_rehydrate_plan(arbor_ctx *c, int count, int keep_floor) {
 
 void launch_rehydrate_copy(arbor_ctx *c, int count, int max_n) {
   if (count == 0 || max_n == 0) return;
-  rehydrate_copy_kernel<<<kCopyCtas, 256, 0, c->ss>>>(pool_args(c), c->d.ptab, c->d.rehyd_nodes,
+  const size_t need = static_cast<size_t>(kCopyCtas) * max_n * 2 * c->D * c->esize;
+  if (need > c->rehyd_scratch_bytes) {   // grown on first use (a synchronising cudaMalloc)
+    if (c->rehyd_scratch) cudaFree(c->rehyd_scratch);
+    if (cudaMalloc(&c->rehyd_scratch, need) != cudaSuccess) {
+      c->rehyd_scratch = nullptr;
+      c->rehyd_scratch_bytes = 0;
+      return;                            // the caller's launch check reports the error
+    }
+    c->rehyd_scratch_bytes = need;
+  }
+  const int nw = (max_n + 31) / 32;
+  const size_t smem = static_cast<size_t>(nw) * 4 + ((static_cast<size_t>(max_n) * 2 + 15) & ~size_t(15));
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(rehydrate_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  rehydrate_copy_kernel<<<kCopyCtas, 256, smem, c->ss>>>(pool_args(c), c->d.ptab, c->d.rehyd_nodes,
                                                       c->d.rehyd_flag, c->d.n, c->d.span,
                                                       static_cast<const char *>(c->stash_dev),
                                                       static_cast<char *>(c->cfg.k_pool),
                                                       static_cast<char *>(c->cfg.v_pool),
-                                                      c->cfg.pos_pool, count, (max_n + 63) / 64);
+                                                      c->cfg.pos_pool, count,
+                                                      static_cast<char *>(c->rehyd_scratch), max_n);
   ARBOR_LAUNCHED(c);
 }
 

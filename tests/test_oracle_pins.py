@@ -441,6 +441,31 @@ def test_state_pages_conserved_and_evict_rehydrate_roundtrip():
     assert sum(len(pg) for pg in o.pages) + len(o.free) == o.num_pages
 
 
+def test_rehydrate_slot_layout_worked_example():
+    """DESIGN.md Q23r, worked by hand: P = 4, a 10-token block (pages p0 p1 p2 for slots
+    0-3, 4-7, 8-11) evicted to k = 3: its window is the last 3 slots 7, 8, 9 holding
+    positions [7, 2, 9] — page p0 freed, koff = 3 in the live list [p1, p2].  Rehydration
+    pops one page (the top of the LIFO free stack) for the freed slots 0-3 and puts every
+    position back in its slot."""
+    tree = synth.full_tree(1, 1, 10)
+    K = np.zeros((1, 1, tree.total_tokens, 2))
+    o = ArborOracle(K, K, 1, 4, 16, default_params())
+    o.open_node(0, 0)
+    o.append(0, 10)
+    o.close_node(0)
+    p0, p1, p2 = o.pages[0]
+    o.free.append(p0)                          # the evicted state by construction
+    o.pages[0] = [p1, p2]
+    o.koff[0] = 3
+    o.kept[0] = np.array([[[7, 2, 9]]], dtype=np.int64)
+    stack = list(o.free)
+    assert o.rehydrate([0]) == 1
+    assert o.kept[0].tolist() == [[list(range(10))]]
+    assert o.koff[0] == 0
+    assert o.pages[0] == [stack[-1], p1, p2] and stack[-1] == p0
+    assert o.free == stack[:-1]
+
+
 def test_state_unlimited_budget_is_full_retention():
     tree, o, E = _small_state(seed=3)
     tree.active = [synth.leaves_of(tree)[1]]
