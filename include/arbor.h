@@ -247,9 +247,11 @@ arbor_status arbor_evict(arbor_ctx *ctx, const arbor_tree *tree, const int32_t *
                          int64_t *evicted_tokens_out);
 
 /* a7/a8 — lazy rehydration (Alg. 2).  For each listed closed
- * node with k_cur < n (ascending id, duplicates ignored): keep its live pages (first_slot
- * becomes 0), pop ⌈n/P⌉ − #pages more and copy the node's full K/V back from the pinned host stash (bit-exact, Q20); pos = identity,
- * k_cur = n, rehydrations += 1.  Full nodes are a no-op and are not counted.  Listing an
+ * node with k_cur < n (ascending id, duplicates ignored): its kept rows are the last k_cur of
+ * its n list slots (Q23r); pop pages for the freed leading list entries (a node
+ * evicted to 0: ⌈n/P⌉), move the kept rows within HBM to slot = position and copy ONLY the
+ * n − k_cur evicted rows back from the pinned host stash (bit-exact, Q20); first_slot = 0,
+ * pos = identity, k_cur = n, rehydrations += 1.  Full nodes are a no-op and are not counted.  Listing an
  * open node is ARBOR_ERR_STATE.  nodes: HOST [count] int32.
  * ARBOR_ERR_OUT_OF_PAGES is returned (state unchanged) if the pool cannot hold the worst
  * case Σ ⌈n/P⌉ − #pages of the listed nodes. */
