@@ -29,7 +29,10 @@
 namespace arbor {
 namespace {
 
-constexpr int kPairsWs = 8;   // (select warp, move warp) pairs per CTA of select_move_ws_kernel
+#ifndef ARBOR_PAIRS
+#define ARBOR_PAIRS 8
+#endif
+constexpr int kPairsWs = ARBOR_PAIRS;   // (select warp, move warp) pairs per CTA of select_move_ws_kernel
 #ifndef ARBOR_KUW
 #define ARBOR_KUW 4
 #endif
