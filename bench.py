@@ -543,6 +543,56 @@ def main():
     ms_per_step = tot_ms / args.steps
     value = cached * args.steps / (tot_ms / 1e3)
 
+    # ---------------- CUDA-Graph pass (SURVEY §8(d) timing protocol: eager AND graph-captured
+    # steps): the step of each active leaf captured once (arbor_capture_begin/end), replayed
+    # K times from the restored state; the restores stay eager, outside the timed region.
+    graph_res = None
+    if os.environ.get("ARBOR_BENCH_GRAPH", "1") == "1" and not two_call:
+        graphs = []
+        try:
+            for i in range(2):
+                restore()
+                torch.cuda.synchronize()
+                ctx.arbor_capture_begin()
+                step(i)
+                graphs.append(ctx.arbor_capture_end())
+            # a replay must leave what the eager step leaves (k, s, the kept K/V)
+            restore()
+            step(0)
+            torch.cuda.synchronize()
+            k_e, s_e, kp_e = k_buf.clone(), s_buf.clone(), ctx.k_pool.view(torch.int16).sum(dtype=torch.int64)
+            restore()
+            ctx.arbor_graph_launch(graphs[0])
+            torch.cuda.synchronize()
+            same = bool(torch.equal(k_buf, k_e) and torch.equal(s_buf, s_e) and
+                        int(ctx.k_pool.view(torch.int16).sum(dtype=torch.int64)) == int(kp_e))
+            for i in range(max(3, args.warmup)):
+                restore()
+                ctx.arbor_graph_launch(graphs[i % 2])
+            gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            torch.cuda.synchronize()
+            for i in range(args.steps):
+                restore()
+                gev[i][0].record(stream)
+                ctx.arbor_graph_launch(graphs[i % 2])
+                gev[i][1].record(stream)
+            torch.cuda.synchronize()
+            g_tot = sum(a.elapsed_time(b) for a, b in gev)
+            if pg is not None:
+                t = torch.tensor([g_tot], dtype=torch.float64, device=dev)
+                pg.all_reduce(t, op=pg.ReduceOp.MAX)
+                g_tot = float(t.item())
+            graph_res = {"value": cached * args.steps / (g_tot / 1e3), "unit": "tokens/s",
+                         "ms_per_step": g_tot / args.steps, "replay_matches_eager": same,
+                         "note": "one CUDA graph per active leaf (arbor_capture_begin/end), "
+                                 "replayed after the same eager restore; device-timed like value"}
+        except Exception as e:  # noqa: BLE001
+            graph_res = {"error": str(e)}
+        finally:
+            for g in graphs:
+                ctx.arbor_graph_destroy(g)
+
     # ---------------- algorithmic bytes for the roofline, from the
     # device state after one step from full retention (per active leaf)
     def alg_bytes(i):
@@ -716,7 +766,7 @@ def main():
                 "config": dict(workload_config(args.config, ws), cached_tokens=cached, budget=B,
                                nodes=N, step="a9 attn + a2 score + a3 mass/MSVE + a1 geometry + "
                                             "a4 allocate + a5/a6 select+compact (+a10 all-reduce)"),
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "graph": graph_res,
                 "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
                 "clocks": clk, "kernels": kernels, "kernel_timing": "second pass of the same K steps with per-stage CUDA events on the launching stream (each event pair adds ~3 us of stream time; included, so per-kernel GB/s are conservative)",
                 "stage_ms_median": {k: statistics.median(v) for k, v in stage_ms.items() if v},

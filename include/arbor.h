@@ -407,6 +407,21 @@ arbor_status arbor_reset_stage_times(arbor_ctx *ctx);
  * flag. */
 arbor_status arbor_set_profiling(arbor_ctx *ctx, int32_t on);
 
+/* ---- CUDA Graph capture (SURVEY §8(d) timing protocol: eager and graph-captured steps) --
+ * arbor_capture_begin: synchronises both streams, then records (does not run) the device work
+ *   of the calls that follow on an internal stream in relaxed capture mode.  Only calls
+ *   without a host out-parameter and without side-stream work (no stash / rehydrate) may be
+ *   captured; host uploads go to pinned buffers owned by the graph.
+ * arbor_capture_end: ends the capture, instantiates it, *graph_out = opaque handle (HOST).
+ * arbor_graph_launch: replays it on main_stream.  A replay updates device state only (the
+ *   host mirrors stay as the captured calls left them): replay from the state the capture
+ *   started in, e.g. after arbor_load_state.
+ * arbor_graph_destroy: synchronises the device and frees the graph and its buffers. */
+arbor_status arbor_capture_begin(arbor_ctx *ctx);
+arbor_status arbor_capture_end(arbor_ctx *ctx, void **graph_out);
+arbor_status arbor_graph_launch(arbor_ctx *ctx, void *graph);
+arbor_status arbor_graph_destroy(void *graph);
+
 /* ---- host-only helpers (no device work; usable without a GPU) ------------------------ */
 /* Validate a tree snapshot: dense ids, parent < child, spans non-overlapping along
  * every root path, closed n ≥ 1, active ids valid, n_sinks ≤ n_root.  msg may be NULL. */

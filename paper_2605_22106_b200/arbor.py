@@ -114,6 +114,10 @@ def load_library(path: str = LIB_PATH):
         "arbor_stage_times": ([P, P], I32),
         "arbor_reset_stage_times": ([P], I32),
         "arbor_set_profiling": ([P, I32], I32),
+        "arbor_capture_begin": ([P], I32),
+        "arbor_capture_end": ([P, C.POINTER(C.c_void_p)], I32),
+        "arbor_graph_launch": ([P, P], I32),
+        "arbor_graph_destroy": ([P], I32),
         "arbor_validate_tree": ([C.POINTER(ArborTree), I32, C.c_char_p, C.c_size_t], I32),
         "arbor_min_feasible_budget": ([C.POINTER(ArborParams), C.POINTER(ArborTree),
                                        C.POINTER(C.c_int64)], I32),
@@ -476,6 +480,21 @@ class ArborKV:
 
     def arbor_set_profiling(self, on: bool):
         self._check(self.lib.arbor_set_profiling(self._ctx, 1 if on else 0), "arbor_set_profiling")
+
+    def arbor_capture_begin(self):
+        self._check(self.lib.arbor_capture_begin(self._ctx), "arbor_capture_begin")
+
+    def arbor_capture_end(self):
+        """Ends the capture; returns the graph handle (an int)."""
+        g = C.c_void_p()
+        self._check(self.lib.arbor_capture_end(self._ctx, C.byref(g)), "arbor_capture_end")
+        return g.value
+
+    def arbor_graph_launch(self, graph):
+        self._check(self.lib.arbor_graph_launch(self._ctx, C.c_void_p(graph)), "arbor_graph_launch")
+
+    def arbor_graph_destroy(self, graph):
+        self._check(self.lib.arbor_graph_destroy(C.c_void_p(graph)), "arbor_graph_destroy")
 
     def arbor_stage_times(self) -> dict:
         ms = (C.c_float * NUM_STAGES)()

@@ -79,6 +79,12 @@ arbor_status dmalloc(arbor_ctx *c, T **p, size_t count) {
 // Pinned staging ring for host→device uploads: a slot is reused only after the copy that
 // last read it has completed.
 arbor_status ring_acquire(arbor_ctx *c, size_t bytes, void **out) {
+  if (c->capturing) {
+    // a captured copy reads its source at every replay: a pinned buffer owned by the graph
+    CK(cudaHostAlloc(out, bytes > 0 ? bytes : 1, cudaHostAllocDefault));
+    c->cap_bufs.push_back(*out);
+    return ARBOR_OK;
+  }
   if (bytes > kRingBytes) return fail(c, ARBOR_ERR_INVALID_ARG, "upload larger than staging ring");
   const int i = c->ring_i;
   CK(cudaEventSynchronize(c->ring_ev[i]));
@@ -93,7 +99,7 @@ arbor_status ring_upload(arbor_ctx *c, void *dst, const void *host_src, size_t b
   TRY(ring_acquire(c, bytes, &buf));
   std::memcpy(buf, host_src, bytes);
   CK(cudaMemcpyAsync(dst, buf, bytes, cudaMemcpyHostToDevice, c->ms));
-  CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
+  if (!c->capturing) CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
   return ARBOR_OK;
 }
 
@@ -273,7 +279,7 @@ arbor_status upload_tree(arbor_ctx *c, const arbor_tree *t) {
   TRY(ring_acquire(c, bytes, &buf));
   pack_tree(c, t, static_cast<char *>(buf));
   CK(cudaMemcpyAsync(c->d.parent, buf, bytes, cudaMemcpyHostToDevice, c->ms));
-  CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
+  if (!c->capturing) CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
   // a1 runs inside arbor_allocate's kernel; arbor_evict launches it only if needed
   tree_commit(c, t);
   return ARBOR_OK;
@@ -424,7 +430,7 @@ arbor_status upload_plan(arbor_ctx *c, const HostPlan &p, int nA, bool with_nq,
       pack_tree(c, t, static_cast<char *>(buf));
       if (plan_bytes) std::memcpy(static_cast<char *>(buf) + off, packed.data(), plan_bytes);
       CK(cudaMemcpyAsync(c->d.parent, buf, off + plan_bytes, cudaMemcpyHostToDevice, c->ms));
-      CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
+      if (!c->capturing) CK(cudaEventRecord(c->ring_ev[c->ring_last], c->ms));
       tree_commit(c, t);
     } else if (!packed.empty()) {
       TRY(ring_upload(c, c->d.inline_seg, packed.data(), plan_bytes));
@@ -797,6 +803,19 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
 }
 
 void arbor_destroy(arbor_ctx *c) {
+  if (c && c->capturing) {   // abandon an unfinished capture
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c->ms, &g);
+    if (g) cudaGraphDestroy(g);
+    c->ms = c->saved_ms;
+    c->capturing = false;
+    for (void *b : c->cap_bufs) cudaFreeHost(b);
+    c->cap_bufs.clear();
+  }
+  if (c && c->cap_stream) {
+    cudaStreamDestroy(c->cap_stream);
+    c->cap_stream = nullptr;
+  }
   if (!c) return;
   if (c->ms) cudaStreamSynchronize(c->ms);
   if (c->ss) cudaStreamSynchronize(c->ss);
@@ -1475,6 +1494,81 @@ arbor_status arbor_load_state(arbor_ctx *c, int32_t slot) {
 
 int64_t arbor_launch_count(const arbor_ctx *c) { return c ? c->launches : 0; }
 int32_t arbor_attn_tensor_cores(const arbor_ctx *c) { return c ? (c->tc_ok ? 1 : 0) : -1; }
+// ---------------------------------------------------------------- CUDA Graph capture
+struct ArborGraph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<void *> bufs;   // pinned sources of the captured uploads
+};
+
+arbor_status arbor_capture_begin(arbor_ctx *c) {
+  if (!c) return ARBOR_ERR_INVALID_ARG;
+  if (c->capturing) return fail(c, ARBOR_ERR_STATE, "already capturing");
+  TRY(sync_all(c));
+  if (c->rehyd_pending || c->stash_pending || c->side_pending) {
+    c->rehyd_pending = c->stash_pending = c->side_pending = false;   // both streams are idle
+    c->rehyd_list.clear();
+  }
+  if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  c->saved_ms = c->ms;
+  c->ms = c->cap_stream;
+  c->cap_bufs.clear();
+  // the captured calls must not rely on device state the host believes current (the tree
+  // mirror, the geometry of this tree): a replay may follow any other work
+  c->tree_valid = false;
+  ++c->tree_version;
+  const cudaError_t e = cudaStreamBeginCapture(c->ms, cudaStreamCaptureModeRelaxed);
+  if (e != cudaSuccess) {
+    c->ms = c->saved_ms;
+    return fail(c, ARBOR_ERR_CUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e));
+  }
+  c->capturing = true;
+  return ARBOR_OK;
+}
+
+arbor_status arbor_capture_end(arbor_ctx *c, void **graph_out) {
+  if (!c || !graph_out) return ARBOR_ERR_INVALID_ARG;
+  if (!c->capturing) return fail(c, ARBOR_ERR_STATE, "not capturing");
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(c->ms, &g);
+  c->ms = c->saved_ms;
+  c->capturing = false;
+  // nothing captured has run: the host's view of the device goes back to "unknown"
+  c->tree_valid = false;
+  ++c->tree_version;
+  c->mass_valid = false;
+  auto *ag = new ArborGraph();
+  ag->bufs.swap(c->cap_bufs);
+  cudaError_t e2 = e;
+  if (e == cudaSuccess) {
+    e2 = cudaGraphInstantiate(&ag->exec, g, 0);
+    cudaGraphDestroy(g);
+  }
+  if (e2 != cudaSuccess) {
+    for (void *b : ag->bufs) cudaFreeHost(b);
+    delete ag;
+    cudaGetLastError();
+    return fail(c, ARBOR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e2));
+  }
+  *graph_out = ag;
+  return ARBOR_OK;
+}
+
+arbor_status arbor_graph_launch(arbor_ctx *c, void *graph) {
+  if (!c || !graph) return ARBOR_ERR_INVALID_ARG;
+  CK(cudaGraphLaunch(static_cast<ArborGraph *>(graph)->exec, c->ms));
+  return ARBOR_OK;
+}
+
+arbor_status arbor_graph_destroy(void *graph) {
+  if (!graph) return ARBOR_ERR_INVALID_ARG;
+  auto *ag = static_cast<ArborGraph *>(graph);
+  cudaDeviceSynchronize();
+  if (ag->exec) cudaGraphExecDestroy(ag->exec);
+  for (void *b : ag->bufs) cudaFreeHost(b);
+  delete ag;
+  return ARBOR_OK;
+}
+
 arbor_status arbor_set_profiling(arbor_ctx *c, int32_t on) {
   if (!c) return ARBOR_ERR_INVALID_ARG;
   if (!(c->cfg.flags & ARBOR_FLAG_PROFILE)) return fail(c, ARBOR_ERR_STATE, "context created without ARBOR_FLAG_PROFILE");

@@ -165,6 +165,11 @@ struct arbor_ctx {
   int max_nodes, max_pages_node, max_active;
   int64_t max_tokens;
   cudaStream_t ms, ss;
+  // CUDA Graph capture (arbor_capture_begin/end): main_stream is swapped for cap_stream while
+  // capturing; uploads then go to pinned buffers owned by the graph, not the staging ring
+  cudaStream_t cap_stream = nullptr, saved_ms = nullptr;
+  bool capturing = false;
+  std::vector<void *> cap_bufs;
   bool own_ms = false, own_ss = false;
   void *unc_part = nullptr, *unc_ticket = nullptr;   // f3 uncertainty scratch (grown on demand)
   size_t unc_cap = 0;
