@@ -86,8 +86,9 @@ __device__ __forceinline__ long long gtimer() {
   return static_cast<long long>(t);
 }
 constexpr int kTraceSlots = 16;   // per warp: 8 events / counters + 8 select-phase cycle sums
-// select-phase cycle sums (debug builds with -DARBOR_EVICT_PHASES, trace slots 8-13): 0 data
-// wait + next issues, 1 key build, 2 threshold, 3 hole / mover lists, 4 job hand-off
+// select-phase cycle sums (debug builds with -DARBOR_EVICT_PHASES, trace slots 8-13): 5 the
+// cp.async wait for the item's data, 0 the next items' issues, 1 key build, 2 threshold,
+// 3 hole / mover lists, 4 job hand-off; slot 14: items
 #ifdef ARBOR_EVICT_PHASES
 #define PH_MARK(i)                                      \
   do {                                                  \
@@ -495,7 +496,7 @@ select_move_ws_kernel(CompactArgs a) {
   int k = 0;
   long long w_empty = 0;
 #ifdef ARBOR_EVICT_PHASES
-  long long ph[5] = {0, 0, 0, 0, 0};
+  long long ph[6] = {0, 0, 0, 0, 0, 0};
   long long ph_t = clock64();
 #endif
   for (;; ++k) {
@@ -505,6 +506,7 @@ select_move_ws_kernel(CompactArgs a) {
     if (lane == 0) nxt = 4 * nsel + atomicAdd(&a.ctrl->item_next, 1);   // step k + 4's item
     cp_async_wait_all();
     __syncwarp();
+    PH_MARK(5);
     issue_pos(k + 1);
     issue_A(k + 1);
     issue_pages(k + 2);
@@ -718,10 +720,10 @@ select_move_ws_kernel(CompactArgs a) {
   }
 #ifdef ARBOR_EVICT_PHASES
   if (a.trace && lane == 0)
-    for (int i = 0; i < 5; ++i)
+    for (int i = 0; i < 6; ++i)
       a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 8 + i] = ph[i];
   if (a.trace && lane == 0)
-    a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 13] = k;
+    a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 14] = k;
 #endif
   cp_async_wait_all();               // prefetches past the end (none were issued, but be tidy)
   // end marker for the move warp

@@ -85,12 +85,12 @@ def main():
     # cycles → µs at 1.965 GHz: move warps waiting for a job, select warps waiting for a slot
     res["move_wait_full_us"] = pct(np.where(ok, tr[:, mov, 6] / 1965.0, np.nan).ravel())
     res["select_wait_empty_us"] = pct(np.where(valid[:, sel, 3], tr[:, sel, 7] / 1965.0, np.nan).ravel())
-    if (tr[:, sel, 8:13] > 0).any():   # -DARBOR_EVICT_PHASES builds: select-phase µs per warp
-        names = ["wait_issue", "keys", "threshold", "lists", "handoff"]
+    if (tr[:, sel, 8:14] > 0).any():   # -DARBOR_EVICT_PHASES builds: select-phase µs per warp
+        names = ["issue_next", "keys", "threshold", "lists", "handoff", "data_wait"]
         okk = valid[:, sel, 3]
         res["select_phase_us"] = {nm: pct(np.where(okk, tr[:, sel, 8 + i] / 1965.0, np.nan).ravel())
                                   for i, nm in enumerate(names)}
-        res["select_items"] = pct(np.where(okk, tr[:, sel, 13], np.nan).ravel())
+        res["select_items"] = pct(np.where(okk, tr[:, sel, 14], np.nan).ravel())
     late = np.argsort(np.where(ok, done, -1).ravel())[::-1][:12]
     res["latest_moves"] = [{"cta": int(i // 8), "sm": int(smid.ravel()[i]), "jobs": int(jobs.ravel()[i]),
                             "rows": int(rows.ravel()[i]), "done": round(float(done.ravel()[i]), 2)}
