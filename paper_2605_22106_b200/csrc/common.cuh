@@ -59,7 +59,10 @@ struct __align__(16) WorkEnt {
   int32_t foff;              // offset of its freed pages among all freed pages
   int16_t nfree, so;         // their count (≤ max_pages_node); soff before (< 2^15: int16 pos tags bound n)
 };
-constexpr int kEvictCtasPerSm = 2;   // the fused evict kernel's work-list copies: [SMs·2][max_nodes]
+constexpr int kEvictCtasPerSm = 2;
+// CTAs of the side-stream PCIe copy kernels (stash / rehydrate, pages.cu): a small persistent
+// grid — PCIe needs ~100 KB of reads in flight, not the whole GPU
+constexpr int kCopyCtas = 32;   // the fused evict kernel's work-list copies: [SMs·2][max_nodes]
 
 // Valid slots of the chunk [c0, c0 + len) of a node's page list whose valid slots are
 // [soff, soff + k_cur) (Q23*): [lo, hi) relative to c0, packed hi | lo << 8

@@ -84,7 +84,6 @@ __global__ void append_copy_kernel(PoolArgs g, const int32_t *ptab, const int32_
 // bandwidth (~50 GB/s) needs ~100 KB of reads in flight, not the whole GPU, and a full-GPU
 // grid of long-running zero-copy CTAs would starve the main stream's kernels (allocate, evict)
 // that run concurrently with a rehydration (Alg. 2 Transition order).
-constexpr int kCopyCtas = 32;
 
 // Stash: node slots 0..n-1 (pos = identity at close) → host [2][L][H][max_tokens][D];
 // work unit = (row r, token chunk of 64), grid-stride
