@@ -2,8 +2,9 @@
 intra-block retention Tail-only and Sinks + Tail (arbor_params.select_mode) through two
 successive evictions (the second acting on already-compacted blocks), and the no-rehydration
 ablation (arbor_params.no_rehydrate: Transition/rehydrate leave evicted blocks partial).
-MSVE-only (λ_Δ = 0) and TAE-only (constant s) are parameter settings of the method's path,
-covered by the allocation tests in test_gpu_parity.py."""
+MSVE-only (λ_d = λ_Δ = 0, η = 1) and TAE-only (constant s) are parameter settings of the
+method's path: their allocations and the evictions after them are checked bit-exact at the end
+(and pinned on the CPU in test_oracle_pins.test_ablation_variants_msve_only_and_tae_only)."""
 from __future__ import annotations
 
 import numpy as np
@@ -191,3 +192,25 @@ def test_stream_analogue_irreversible():
         pr.check_kv_state()
     assert set(range(4)) <= set(int(x) for x in pr.orc.kept[0][0, 0])
     pr.decode_both()
+
+
+@pytest.mark.parametrize("variant", ["msve_only", "tae_only"])
+def test_ablation_allocations_bit_exact(variant):
+    """P:408-414 ablations as parameter settings: MSVE-only (λ_d = λ_Δ = 0,
+    η = 1: the weight is s^γ alone) and TAE-only (s ≡ const: the tree alone).  The device
+    allocation equals the oracle's bit for bit, and the eviction that follows matches it."""
+    over = dict(lambda_d=0.0, lambda_delta=0.0, eta=1.0) if variant == "msve_only" else \
+        dict(lambda_d=0.0, lambda_delta=0.7, eta=1.0)
+    pr = Pair(MID, seed=21, params_over=over)
+    pr.warmup(steps_per_leaf=1, check=False, fused=True)
+    N = pr.tree.num_nodes
+    if variant == "msve_only":
+        s = np.asarray(pr.ctx.arbor_read_scores(N)["s"], np.float32)
+    else:
+        s = np.full(N, 0.5, np.float32)
+    B = int(0.3 * pr.tree.total_tokens)
+    k = torch.empty(N, dtype=torch.int32, device="cuda")
+    pr.ctx.arbor_allocate(pr.tree, torch.as_tensor(s, device="cuda"), B, k)
+    st, k_ref, _ = pr.discrete_allocate(s, B)
+    assert st == 0 and k.cpu().tolist() == k_ref and sum(k_ref) == B
+    _evict_both(pr, k_ref)

@@ -261,6 +261,47 @@ def test_allocate_invariants_random():
     assert k[2] == k[3] and sum(k) == 48
 
 
+def test_ablation_variants_msve_only_and_tae_only():
+    """P:408-414 ablations as parameter settings of the same allocation.
+    MSVE-only (λ_d = λ_Δ = 0, η = 1): the weight is s^γ alone, so on random trees two
+    non-pinned nodes with equal (s, n) get k within 1 of each other and a larger s never gets
+    a smaller k at equal n.  TAE-only (s ≡ const): k follows the tree alone — equal (Δ, n) off
+    the path (depth unused at λ_d = 0, η = 1) → k within 1, larger Δ → k no larger."""
+    rng = np.random.default_rng(41)
+    for trial in range(120):
+        N = int(rng.integers(6, 40))
+        parent = random_tree(N, rng)
+        leaves = [i for i in range(N) if i not in set(parent)]
+        active = [int(rng.choice(leaves))]
+        d = geometry.depths(parent)
+        dist = geometry.delta(parent, active)
+        ps = geometry.path_star(parent, active)
+        on = [i in ps for i in range(N)]
+        n = [int(x) for x in rng.choice([24, 48], size=N)]
+        free = [j for j in range(N) if not on[j]]
+        B = sum(n[j] for j in range(N) if on[j]) + sum(n[j] for j in free) // 3
+        if trial % 2 == 0:      # MSVE-only
+            p = default_params(lambda_d=0.0, lambda_delta=0.0, eta=1.0, r_min=0.0)
+            s = [float(np.float32(x)) for x in rng.choice([0.2, 0.5, 0.9], size=N)]
+            key = lambda j: (s[j], n[j])                       # noqa: E731
+            order = lambda j: s[j]                             # noqa: E731
+            sign = 1
+        else:                   # TAE-only
+            p = default_params(lambda_d=0.0, lambda_delta=0.7, eta=1.0, r_min=0.0)
+            s = [0.5] * N
+            key = lambda j: (dist[j], n[j])                    # noqa: E731
+            order = lambda j: dist[j]                          # noqa: E731
+            sign = -1
+        st, k, _ = tae.allocate(tae.MODE_WATERFILL, s, d, dist, on, [0] * N, n, p, B)
+        assert st == 0 and sum(k) == B
+        for a in free:
+            for b in free:
+                if key(a) == key(b):
+                    assert abs(k[a] - k[b]) <= 1, (trial, a, b, k[a], k[b])
+                elif n[a] == n[b] and sign * (order(a) - order(b)) > 0:
+                    assert k[a] >= k[b], (trial, a, b, k[a], k[b])
+
+
 def test_allocate_zero_weights_saturation():
     """W rounding to 0 (s ≈ 0): floor only unless positive-weight nodes saturate;
     then the remainder is spread over zero-weight nodes by slack (§8(c).1 step 10)."""
