@@ -73,6 +73,13 @@ typedef enum {
  * KV-head shards on one device — a plain device sum) and calls arbor_score_finish, which runs
  * the MSVE on the reduced masses.  nccl_unique_id is then ignored. */
 #define ARBOR_FLAG_EXTERNAL_REDUCE 2u
+/* The library's NCCL path (a10) at any world size, including 1 (a one-rank communicator):
+ * arbor_score / arbor_decode_step take the multi-rank finisher — partial node masses →
+ * ncclAllReduce(int64, sum) on main_stream → the MSVE kernel — instead of the single-rank
+ * fused MSVE.  Integer sums are order-free, so every result equals the single-rank path's bit
+ * for bit; it lets one GPU execute the collective path (dlopen, ncclCommInitRank,
+ * ncclAllReduce).  Needs nccl_unique_id; incompatible with ARBOR_FLAG_EXTERNAL_REDUCE. */
+#define ARBOR_FLAG_COLLECTIVE 4u
 
 /* Parameter bundle Π (Alg. 1 caption P:498, Alg. 2).  Host struct. */
 typedef struct {

@@ -24,6 +24,7 @@ ALLOC_MODES = {"waterfill": 0, "static": 1, "static_drain": 2, "stream": 3}
 SELECT_MODES = {"heavy": 0, "tail": 1, "sinks_tail": 2}
 FLAG_PROFILE = 1
 FLAG_EXTERNAL_REDUCE = 2
+FLAG_COLLECTIVE = 4
 NUM_STAGES = 13
 STAGES = ["geometry", "score_accum", "node_mass", "msve", "allocate", "evict_plan",
           "select_compact", "rehydrate", "attn", "attn_merge", "allreduce", "stash",
@@ -227,7 +228,7 @@ class ArborKV:
                  page_size=16, num_pages, max_nodes, max_node_tokens, max_active=16, max_tokens,
                  params: ArborParams, layer_begin=0, layer_count=None, kv_head_begin=0,
                  kv_head_count=None, rank=0, world_size=1, nccl_id: bytes = None,
-                 profile=False, device=None, external_reduce=False):
+                 profile=False, device=None, external_reduce=False, collective=False):
         import torch
         if not torch.cuda.is_available():
             raise ArborError(8, "no CUDA device: the ArborKV path has no CPU fallback")
@@ -262,7 +263,8 @@ class ArborKV:
                           C.cast(self._nccl, C.c_void_p) if self._nccl is not None else None,
                           self.stream.cuda_stream, self.side.cuda_stream,
                           (FLAG_PROFILE if profile else 0) |
-                          (FLAG_EXTERNAL_REDUCE if external_reduce else 0))
+                          (FLAG_EXTERNAL_REDUCE if external_reduce else 0) |
+                          (FLAG_COLLECTIVE if collective else 0))
         self.params = params
         self._ctx = C.c_void_p()
         st = self.lib.arbor_init(C.byref(cfg), C.byref(params), C.byref(self._ctx))

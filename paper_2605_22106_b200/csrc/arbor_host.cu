@@ -671,7 +671,9 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   if (!k.k_pool || !k.v_pool || !k.pos_pool || !k.score) return ARBOR_ERR_INVALID_ARG;
   if (k.world_size < 1 || k.rank < 0 || k.rank >= k.world_size) return ARBOR_ERR_INVALID_ARG;
   const bool ext_reduce = (k.flags & ARBOR_FLAG_EXTERNAL_REDUCE) != 0;
-  if (k.world_size > 1 && !k.nccl_unique_id && !ext_reduce) return ARBOR_ERR_INVALID_ARG;
+  const bool coll = (k.flags & ARBOR_FLAG_COLLECTIVE) != 0;
+  if ((k.world_size > 1 || coll) && !k.nccl_unique_id && !ext_reduce) return ARBOR_ERR_INVALID_ARG;
+  if (coll && ext_reduce) return ARBOR_ERR_INVALID_ARG;
   if (params->slice_layers > k.num_layers || params->slice_kv_heads > k.num_kv_heads)
     return ARBOR_ERR_INVALID_ARG;
   if (params->select_shared && k.world_size > 1) return ARBOR_ERR_INVALID_ARG;   // Â is rank-local
@@ -788,7 +790,7 @@ arbor_status arbor_init(const arbor_config *cfg, const arbor_params *params, arb
   }
   if (cudaHostGetDevicePointer(&c->stash_dev, c->stash_host, 0) != cudaSuccess) return bail(ARBOR_ERR_IO);
   // NCCL communicator for the mass all-reduce (a10)
-  if (k.world_size > 1 && !ext_reduce) {
+  if ((k.world_size > 1 || coll) && !ext_reduce) {
     if (!g_nccl.load()) return bail(ARBOR_ERR_NCCL);
     ncclUniqueId id;
     std::memcpy(&id, k.nccl_unique_id, sizeof(id));
@@ -959,6 +961,11 @@ static int score_parts(const arbor_ctx *c, size_t chunks) {
   return p;
 }
 
+// the fused single-rank finisher (MSVE inside the score / decode_post kernel) applies
+static bool single_rank(const arbor_ctx *c) {
+  return c->cfg.world_size == 1 && !(c->cfg.flags & ARBOR_FLAG_COLLECTIVE);
+}
+
 // a10 + MSVE on several ranks: the all-reduce sits between the partial masses and the score
 // (ARBOR_FLAG_EXTERNAL_REDUCE: the caller's collective, then arbor_score_finish)
 static arbor_status score_allreduce(arbor_ctx *c, int N, float *s_out) {
@@ -1009,7 +1016,7 @@ arbor_status arbor_score(arbor_ctx *c, const arbor_tree *tree, const void *q, co
   }
   // a2 + a3 in one launch (score.cu): score pass, partial masses, Mass/Mclose → mass2, and —
   // single rank — the MSVE score; with several ranks the all-reduce sits before the MSVE
-  const bool single = c->cfg.world_size == 1;
+  const bool single = single_rank(c);
   launch_score_fused(c, pv, lse_use, d_mass_nodes, static_cast<int>(mass_nodes.size()), N, single,
                      s_out, score_parts(c, hp.ch_node.size()));
   CK_LAUNCH();
@@ -1063,7 +1070,7 @@ arbor_status arbor_decode_step(arbor_ctx *c, const arbor_tree *tree, const void 
   launch_attn_partial(c, pv, q, 0, c->L, hp.max_cnt, out, lse_out);
   CK_LAUNCH();
   mark();
-  const bool single = c->cfg.world_size == 1;
+  const bool single = single_rank(c);
   int parts = score_parts(c, hp.ch_node.size());
   static const int parts_env = getenv("ARBOR_POST_PARTS") ? atoi(getenv("ARBOR_POST_PARTS")) : 0;
   if (parts_env > 0) parts = parts_env;   // diagnostics

@@ -58,7 +58,8 @@ def preset_params(preset: dict, **over):
 def make_context(preset: dict, tree, *, extra_tokens=0, extra_nodes=0, max_active=16,
                  params=None, layer_begin=0, layer_count=None, kv_head_begin=0,
                  kv_head_count=None, rank=0, world_size=1, nccl_id=None, profile=False,
-                 page_margin=64, node_extra_tokens=None, external_reduce=False) -> ArborKV:
+                 page_margin=64, node_extra_tokens=None, external_reduce=False,
+                 collective=False) -> ArborKV:
     """extra_tokens / extra_nodes: growth of the whole tree beyond the snapshot (pages, the
     position stream); node_extra_tokens: the most tokens any ONE node may grow to beyond
     the snapshot's largest node (int16 position tags per node; default extra_tokens)."""
@@ -76,7 +77,7 @@ def make_context(preset: dict, tree, *, extra_tokens=0, extra_nodes=0, max_activ
                    params=params if params is not None else preset_params(preset),
                    layer_begin=layer_begin, layer_count=layer_count, kv_head_begin=kv_head_begin,
                    kv_head_count=kv_head_count, rank=rank, world_size=world_size, nccl_id=nccl_id,
-                   profile=profile, external_reduce=external_reduce)
+                   profile=profile, external_reduce=external_reduce, collective=collective)
 
 
 def load_tree(ctx: ArborKV, tree, K, V):
@@ -146,7 +147,7 @@ class Scenario:
 def setup(preset_name: str, seed: int = 0, *, kv_head_begin=0, kv_head_count=None, rank=0,
           world_size=1, nccl_id=None, profile=False, extra_tokens=0, extra_nodes=0,
           params=None, max_active=16, device="cuda", node_extra_tokens=None,
-          external_reduce=False) -> Scenario:
+          external_reduce=False, collective=False) -> Scenario:
     """Build the preset's tree, its seeded K/V (on the device), a context, and prefill it."""
     preset = PRESETS[preset_name]
     tree = build_tree(preset, seed)
@@ -161,7 +162,7 @@ def setup(preset_name: str, seed: int = 0, *, kv_head_begin=0, kv_head_count=Non
                        max_active=max_active, params=params, kv_head_begin=kv_head_begin,
                        kv_head_count=hc, rank=rank, world_size=world_size, nccl_id=nccl_id,
                        profile=profile, node_extra_tokens=node_extra_tokens,
-                       external_reduce=external_reduce)
+                       external_reduce=external_reduce, collective=collective)
     load_tree(ctx, tree, K, V)
     return Scenario(preset, tree, ctx, K, V, E, seed, kv_head_begin)
 

@@ -159,3 +159,53 @@ def test_world_size_gt1_external_reduce_bit_identical(shards):
     # finishing without a pending score is a lifecycle error
     with pytest.raises(Exception):
         parts[0].ctx.arbor_score_finish(red)
+
+
+def test_collective_flag_one_rank_nccl_bit_identical():
+    """a10 on hardware with one GPU (ARBOR_FLAG_COLLECTIVE): a one-rank NCCL communicator
+    (arbor_nccl_unique_id → ncclCommInitRank) and the multi-rank finisher — partial masses →
+    ncclAllReduce(int64, sum) → msve_kernel — on the arbor_decode_step and arbor_score paths.
+    Scores, A, k, page tables and free list equal the fused single-rank context's bit for bit;
+    NCCL itself (dlopen of libnccl.so.2, init, the collective) runs on the device."""
+    from paper_2605_22106_b200.arbor import nccl_unique_id
+    preset = dict(tree=("full", 3, 4, 96), L=3, H=8, Hq=32, d=128, dtype="bf16", P=16, rho=0.5,
+                  params={}, active="highest_v")
+    workload.PRESETS["_coll_test"] = preset
+    try:
+        ref = workload.setup("_coll_test", 9)
+        col = workload.setup("_coll_test", 9, nccl_id=nccl_unique_id(), collective=True)
+    finally:
+        del workload.PRESETS["_coll_test"]
+    tree = ref.tree
+    N = tree.num_nodes
+    leaves = synth.leaves_of(tree)
+    B = int(math.floor(preset["rho"] * tree.total_tokens))
+    for step in range(6):
+        act = [leaves[(3 * step + j) % len(leaves)] for j in range(1 + step % 2)]
+        for sc in (ref, col):
+            sc.tree.active = act
+            q = sc.queries(step, len(act))
+            out = torch.empty_like(q)
+            lse = torch.empty((len(act), sc.ctx.L, sc.ctx.Hq), dtype=torch.float32, device="cuda")
+            if step % 3 == 2:        # the two-call path: a9, then a2 + a3 (+ a10) in arbor_score
+                sc.ctx.arbor_tree_decode_attn(sc.tree, q, out, lse)
+                sc.ctx.arbor_score(sc.tree, q, lse)
+            else:                    # f2: arbor_decode_step
+                sc.ctx.arbor_decode_step(sc.tree, q, out, lse)
+        fr, fc = ref.ctx.arbor_read_scores(N), col.ctx.arbor_read_scores(N)
+        for key in ("mass", "mclose", "nq"):
+            assert np.array_equal(fr[key], fc[key]), (key, step)
+        for key in ("a", "s"):
+            assert np.array_equal(fr[key].view(np.int32), fc[key].view(np.int32)), (key, step)
+        assert torch.equal(ref.ctx.score, col.ctx.score)
+        if step in (2, 5):
+            ks = []
+            for sc in (ref, col):
+                k = torch.empty(N, dtype=torch.int32, device="cuda")
+                sc.ctx.arbor_allocate(sc.tree, None, B, k)
+                sc.ctx.arbor_evict(sc.tree, k)
+                ks.append(k.cpu())
+            assert torch.equal(ks[0], ks[1]), f"k differs at step {step}"
+            assert [ref.ctx.arbor_read_node(i) for i in range(N)] == \
+                [col.ctx.arbor_read_node(i) for i in range(N)]
+            assert ref.ctx.arbor_read_free_list() == col.ctx.arbor_read_free_list()
