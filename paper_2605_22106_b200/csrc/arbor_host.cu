@@ -957,7 +957,7 @@ static int score_parts(const arbor_ctx *c, size_t chunks) {
   const int want = std::max(1, std::min(8, static_cast<int>(chunks) / 16));
   int p = 1;
   while (p * 2 <= want) p *= 2;
-  while (p > 1 && c->L * c->H * p > 2 * c->num_sms) p /= 2;
+  while (p > 1 && c->L * c->H * p > kPostCtasPerSm * c->num_sms) p /= 2;
   return p;
 }
 

@@ -62,7 +62,13 @@ struct __align__(16) WorkEnt {
 constexpr int kEvictCtasPerSm = 2;
 // CTAs of the side-stream PCIe copy kernels (stash / rehydrate, pages.cu): a small persistent
 // grid — PCIe needs ~100 KB of reads in flight, not the whole GPU
-constexpr int kCopyCtas = 32;   // the fused evict kernel's work-list copies: [SMs·2][max_nodes]
+constexpr int kCopyCtas = 32;
+// decode_post / score_fused CTAs resident per SM (__launch_bounds__ min blocks): the score
+// pass is split into parts only up to one resident wave
+#ifndef ARBOR_POST_MINB
+#define ARBOR_POST_MINB 2
+#endif
+constexpr int kPostCtasPerSm = ARBOR_POST_MINB;   // the fused evict kernel's work-list copies: [SMs·2][max_nodes]
 
 // Valid slots of the chunk [c0, c0 + len) of a node's page list whose valid slots are
 // [soff, soff + k_cur) (Q23*): [lo, hi) relative to c0, packed hi | lo << 8

@@ -700,11 +700,11 @@ void launch_decode_post(arbor_ctx *c, const PlanView &pv, void *out, float *lse_
   // was slower as a PDL launch than as a plain one, 269 vs 237 µs per C2 step; this one is
   // faster with PDL: 238.9 vs 243.7 µs, A/B on one box.)
   if (c->esize == 2) {
-    if (c->D == 128) launch_pdl(decode_post_kernel<__nv_bfloat16, 128, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
-    else launch_pdl(decode_post_kernel<__nv_bfloat16, 64, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    if (c->D == 128) launch_pdl(decode_post_kernel<__nv_bfloat16, 128, kPostCtasPerSm>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    else launch_pdl(decode_post_kernel<__nv_bfloat16, 64, kPostCtasPerSm>, grid, dim3(kFusedThreads), 0, c->ms, pa);
   } else {
-    if (c->D == 128) launch_pdl(decode_post_kernel<float, 128, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
-    else launch_pdl(decode_post_kernel<float, 64, 2>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    if (c->D == 128) launch_pdl(decode_post_kernel<float, 128, kPostCtasPerSm>, grid, dim3(kFusedThreads), 0, c->ms, pa);
+    else launch_pdl(decode_post_kernel<float, 64, kPostCtasPerSm>, grid, dim3(kFusedThreads), 0, c->ms, pa);
   }
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SCORE_ACCUM, c->ms);
