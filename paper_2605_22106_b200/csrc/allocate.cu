@@ -539,7 +539,10 @@ allocate_kernel(AllocArgs a) {
       given = block_sum(given, red64);
       TRACE(5);
       const long long leftover = Num - given;
-      if (leftover > 0 && N <= 256) {
+#ifndef ARBOR_ALLOC_LR_WARP_MAX
+#define ARBOR_ALLOC_LR_WARP_MAX 256   // trees up to this size rank by warp per node
+#endif
+      if (leftover > 0 && N <= ARBOR_ALLOC_LR_WARP_MAX) {
         // largest remainder: the `leftover` active nodes first in (rem desc, W desc, id asc)
         // get +1.  Small trees: rank of each active node — a warp per node, lanes over the
         // other nodes, one __reduce_add_sync per node (O(N²/32): 4.8 µs at N = 156)
@@ -582,6 +585,50 @@ allocate_kernel(AllocArgs a) {
           if (W[x] != W[y]) return W[x] > W[y];
           return x < y;
         };
+#ifndef ARBOR_ALLOC_LR_SHFL
+#define ARBOR_ALLOC_LR_SHFL 1
+#endif
+        if (ARBOR_ALLOC_LR_SHFL && P2 <= kThreads) {
+          // ≤ 512 keys: one per thread, the key (rem, W, id) in registers; a compare-exchange
+          // stage of stride < 32 is a warp shuffle, only strides ≥ 32 go through shared memory
+          // with a barrier (10 barrier stages at 512 keys instead of 45)
+          const int P = P2 < 64 ? 64 : P2;    // whole warps
+          for (int t = na + threadIdx.x; t < P; t += blockDim.x) idx[t] = -1;
+          __syncthreads();
+          const int t = threadIdx.x;
+          int x = t < P ? idx[t] : -1;
+          long long xr = x >= 0 ? rem[x] : 0, xw = x >= 0 ? W[x] : 0;
+          auto gtk = [](int a, long long ar, long long aw, int b, long long br, long long bw) {
+            if (b < 0) return a >= 0;
+            if (a < 0) return false;
+            if (ar != br) return ar > br;
+            if (aw != bw) return aw > bw;
+            return a < b;
+          };
+          for (int size = 2; size <= P; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+              int y;
+              long long yr, yw;
+              if (stride >= 32) {
+                __syncthreads();                 // the previous stage's reads are done
+                if (t < P) idx[t] = x;
+                __syncthreads();
+                y = t < P ? idx[t ^ stride] : -1;
+                yr = y >= 0 ? rem[y] : 0;
+                yw = y >= 0 ? W[y] : 0;
+              } else {
+                y = __shfl_xor_sync(0xffffffffu, x, stride);
+                yr = __shfl_xor_sync(0xffffffffu, xr, stride);
+                yw = __shfl_xor_sync(0xffffffffu, xw, stride);
+              }
+              const bool lower = (t & stride) == 0, desc = (t & size) == 0;
+              // a descending run keeps the larger key at the lower position
+              const bool take = (lower == desc) ? gtk(y, yr, yw, x, xr, xw) : gtk(x, xr, xw, y, yr, yw);
+              if (take) { x = y; xr = yr; xw = yw; }
+            }
+          }
+          if (t < leftover && x >= 0) k[x] += 1;
+        } else
         for (int size = 2; size <= P2; size <<= 1) {
           for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int i = threadIdx.x; i < P2; i += blockDim.x) {
@@ -595,7 +642,8 @@ allocate_kernel(AllocArgs a) {
             __syncthreads();
           }
         }
-        for (int t = threadIdx.x; t < leftover; t += blockDim.x) k[idx[t]] += 1;
+        if (!(ARBOR_ALLOC_LR_SHFL && P2 <= kThreads))
+          for (int t = threadIdx.x; t < leftover; t += blockDim.x) k[idx[t]] += 1;
       }
     }
   }
