@@ -74,11 +74,18 @@ struct CompactArgs {
   int wl_smem;      // N when the work list also lives in shared memory (N ≤ kSmemWorkNodes), else 0
   const int32_t *gate;   // f1 device waterline: nothing to do when *gate == 0 (else NULL)
 };
-constexpr int kSmemWorkNodes = 1024;
-constexpr int kFinish = 32;
+constexpr int kSmemWorkNodes = 1024;   // 32 KB of work entries per CTA
+constexpr int kFinish = 32;   // radix passes stop once this few keys share the prefix (rank-count finish)
 // slot loops of the select warp are kept rolled: unrolling them 2x / 4x measured slower (C5
 // select_compact 278 -> 294-296 us; C2 113 -> 114-115 us), as did the compiler's default
-constexpr int kSelUnroll = 1;   // radix passes stop once this few keys share the prefix (rank-count finish)   // 32 KB of work entries per CTA
+constexpr int kSelUnroll = 1;
+// … except the hole / mover list build: unrolled 4x it measured C2 113.4 -> 112.2 us, C5
+// 278.3 -> 276.7 us (the key build unrolled alone: C5 300 us; hoisting its uniform tests and
+// deferring its invariant check out of the loop: C5 287 us — register pressure at the cap)
+#ifndef ARBOR_UNROLL_LISTS
+#define ARBOR_UNROLL_LISTS 4
+#endif
+constexpr int kUnrollLists = ARBOR_UNROLL_LISTS;
 
 __device__ __forceinline__ long long gtimer() {
   unsigned long long t;
@@ -674,7 +681,7 @@ select_move_ws_kernel(CompactArgs a) {
     // (kept slots before it), ascending
     const int w0 = kc - ka;
     int nh = 0, nm = 0;
-#pragma unroll kSelUnroll
+#pragma unroll kUnrollLists
     for (int s0 = 0; s0 < kc; s0 += 32) {
       const int s = s0 + lane;
       int keep = 0;
