@@ -75,7 +75,10 @@ struct CompactArgs {
   const int32_t *gate;   // f1 device waterline: nothing to do when *gate == 0 (else NULL)
 };
 constexpr int kSmemWorkNodes = 1024;   // 32 KB of work entries per CTA
-constexpr int kFinish = 32;   // radix passes stop once this few keys share the prefix (rank-count finish)
+#ifndef ARBOR_FINISH
+#define ARBOR_FINISH 32
+#endif
+constexpr int kFinish = ARBOR_FINISH;   // ≤ 32; radix passes stop once this few keys share the prefix (rank-count finish)
 // slot loops of the select warp are kept rolled: unrolling them 2x / 4x measured slower (C5
 // select_compact 278 -> 294-296 us; C2 113 -> 114-115 us), as did the compiler's default
 constexpr int kSelUnroll = 1;
