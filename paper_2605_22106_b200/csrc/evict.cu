@@ -475,15 +475,23 @@ select_move_ws_kernel(CompactArgs a) {
       for (int c = lane; c < nch; c += 32) cp_async16(ab + 4 * c, a0 + 16 * c);
     }
   };
-  // the first four items of select warp w are 4w … 4w + 3 (no atomic storm at the start);
-  // the counter hands out the rest, from 4·(select warps) on
+  // items are drawn `draw` pipeline steps ahead: 4 with a global work list (its entries are
+  // fetched three steps ahead), 3 with the shared-memory list (page lists two steps ahead are
+  // the farthest look-ahead) — every item drawn but not yet ranked when the counter runs out
+  // is tail work for its warp alone.  The first `draw` items of select warp w are
+  // draw·w … draw·w + draw − 1 (no atomic storm at the start); the counter hands out the
+  // rest, from draw·(select warps) on
+#ifndef ARBOR_EVICT_DRAW_SMEM
+#define ARBOR_EVICT_DRAW_SMEM 3
+#endif
+  const int draw = Ly.wl_n ? ARBOR_EVICT_DRAW_SMEM : 4;
   const int nsel = static_cast<int>(gridDim.x) * kPairsWs;
   const int gw = static_cast<int>(blockIdx.x) * kPairsWs + pid;
   if (lane == 0) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      iring[i] = 4 * gw + i;
-      wring[i] = (4 * gw + i) / a.R;
+      iring[i] = i < draw ? draw * gw + i : items;
+      wring[i] = (draw * gw + i) / a.R;
     }
   }
   __syncwarp();
@@ -513,7 +521,7 @@ select_move_ws_kernel(CompactArgs a) {
     const int it = item_of(k);
     if (it >= items) break;          // the counter only grows: every later draw is past the end
     int nxt = 0;
-    if (lane == 0) nxt = 4 * nsel + atomicAdd(&a.ctrl->item_next, 1);   // step k + 4's item
+    if (lane == 0) nxt = draw * nsel + atomicAdd(&a.ctrl->item_next, 1);   // step k + draw's item
     cp_async_wait_all();
     __syncwarp();
     PH_MARK(5);
@@ -720,8 +728,8 @@ select_move_ws_kernel(CompactArgs a) {
       jb[i] = make_int2(static_cast<int>(row(movers[i])), static_cast<int>(row(holes[i])));
     if (lane == 0) {
       mycount[sl] = nm;
-      iring[k & 3] = nxt;            // step k + 4 (read after the next step's __syncwarp)
-      wring[k & 3] = nxt / a.R;
+      iring[(k + draw) & 3] = nxt;   // step k + draw (read after the next step's __syncwarp)
+      wring[(k + draw) & 3] = nxt / a.R;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&full[sl]);
