@@ -95,14 +95,22 @@ __device__ __forceinline__ long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return static_cast<long long>(t);
 }
-constexpr int kTraceSlots = 16;   // per warp: 8 events / counters + 8 select-phase cycle sums
+constexpr int kTraceSlots = 16;
+// the timeline (ARBOR_EVICT_TRACE=1 at run time) is compiled only into diagnostic builds
+// (-DARBOR_EVICT_TRACE_BUILD): its clock reads and counters cost the production kernel
+// registers at its 64-register cap
+#ifdef ARBOR_EVICT_TRACE_BUILD
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif   // per warp: 8 events / counters + 8 select-phase cycle sums
 // select-phase cycle sums (debug builds with -DARBOR_EVICT_PHASES, trace slots 8-13): 5 the
 // cp.async wait for the item's data, 0 the next items' issues, 1 key build, 2 threshold,
 // 3 hole / mover lists, 4 job hand-off; slot 14: items
 #ifdef ARBOR_EVICT_PHASES
 #define PH_MARK(i)                                      \
   do {                                                  \
-    if (a.trace) {                                      \
+    if (kTrace && a.trace) {                            \
       const long long t_ = clock64();                   \
       ph[i] += t_ - ph_t;                               \
       ph_t = t_;                                        \
@@ -115,7 +123,7 @@ constexpr int kTraceSlots = 16;   // per warp: 8 events / counters + 8 select-ph
 // 2 first job handed / started, 3 last job handed / done, 4 plan loads done, 5 plan scans done
 #define EV_TRACE(e)                                                                           \
   do {                                                                                        \
-    if (a.trace && lane == 0)                                                                 \
+    if (kTrace && a.trace && lane == 0)                                                                 \
       a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + (e)] = gtimer(); \
   } while (0)
 
@@ -360,12 +368,12 @@ select_move_ws_kernel(CompactArgs a) {
     int k_jobs = 0;
     for (int k = 0;; ++k) {
       const int sl = k & (kJobSlots - 1);
-      const long long tw0 = a.trace ? clock64() : 0;
+      const long long tw0 = (kTrace && a.trace) ? clock64() : 0;
       // a starved move warp sleeps in the try_wait instead of spinning: its spin loop took
       // ~18% of the kernel's issued instructions from the select warps it waits for
       if (ARBOR_EVICT_SLEEP_NS) mbar_wait_sleep(&full[sl], (k / kJobSlots) & 1, ARBOR_EVICT_SLEEP_NS);
       else mbar_wait(&full[sl], (k / kJobSlots) & 1);
-      if (a.trace && k > 0) w_full += clock64() - tw0;
+      if (kTrace && a.trace && k > 0) w_full += clock64() - tw0;
       if (k == 0) EV_TRACE(2);
       const int cnt = mycount[sl];
       if (cnt < 0) break;
@@ -376,10 +384,10 @@ select_move_ws_kernel(CompactArgs a) {
                 a.pos, rb, rpi, piece, sub);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[sl]);
-      if (a.trace) mv_rows += cnt;
+      if (kTrace && a.trace) mv_rows += cnt;
     }
     EV_TRACE(3);
-    if (a.trace && lane == 0) {   // diagnostics: SM id, jobs and rows this move warp handled
+    if (kTrace && a.trace && lane == 0) {   // diagnostics: SM id, jobs and rows this move warp handled
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 7] =
@@ -719,10 +727,10 @@ select_move_ws_kernel(CompactArgs a) {
     PH_MARK(3);
     // hand the job to the move warp
     const int sl = k & (kJobSlots - 1);
-    const long long tw0 = a.trace ? clock64() : 0;
+    const long long tw0 = (kTrace && a.trace) ? clock64() : 0;
     if (ARBOR_EVICT_SLEEP_NS) mbar_wait_sleep(&empty[sl], ((k / kJobSlots) & 1) ^ 1, ARBOR_EVICT_SLEEP_NS);
     else mbar_wait(&empty[sl], ((k / kJobSlots) & 1) ^ 1);
-    if (a.trace) w_empty += clock64() - tw0;
+    if (kTrace && a.trace) w_empty += clock64() - tw0;
     int2 *jb = myjobs + sl * jcap;
     for (int i = lane; i < nm; i += 32)
       jb[i] = make_int2(static_cast<int>(row(movers[i])), static_cast<int>(row(holes[i])));
@@ -737,10 +745,10 @@ select_move_ws_kernel(CompactArgs a) {
     PH_MARK(4);
   }
 #ifdef ARBOR_EVICT_PHASES
-  if (a.trace && lane == 0)
+  if (kTrace && a.trace && lane == 0)
     for (int i = 0; i < 6; ++i)
       a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 8 + i] = ph[i];
-  if (a.trace && lane == 0)
+  if (kTrace && a.trace && lane == 0)
     a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 14] = k;
 #endif
   cp_async_wait_all();               // prefetches past the end (none were issued, but be tidy)
@@ -763,7 +771,7 @@ select_move_ws_kernel(CompactArgs a) {
     }
   }
   EV_TRACE(3);
-  if (a.trace && lane == 0)   // diagnostics: cycles this select warp waited for a free job slot
+  if (kTrace && a.trace && lane == 0)   // diagnostics: cycles this select warp waited for a free job slot
     a.trace[(static_cast<int64_t>(blockIdx.x) * (2 * kPairsWs) + warp) * kTraceSlots + 7] = w_empty;
 }
 

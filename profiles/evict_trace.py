@@ -5,7 +5,11 @@ globaltimer trace each warp writes (evict.cu EV_TRACE: 0 start after griddepcont
 1 plan done, 2 first job handed (select) / started (move), 3 last job handed / done).  Prints
 percentiles in µs relative to the earliest CTA start.  A diagnostic, not a bench.
 
+    ARBOR_NVCC_FLAGS=-DARBOR_EVICT_TRACE_BUILD python -m paper_2605_22106_b200.build --force
     python profiles/evict_trace.py [c2|c4|c5] > gpurun_out/evict_trace_c2.json
+
+(the timeline is compiled only into that diagnostic build; add -DARBOR_EVICT_PHASES for the
+select-phase cycle sums)
 """
 from __future__ import annotations
 

@@ -20,7 +20,9 @@ python bench.py --config c3 --no-cpu-baseline > gpurun_out/${V}_bench_c3.json 2>
 python bench.py --config c4 --no-cpu-baseline > gpurun_out/${V}_bench_c4.json 2>>gpurun_out/bench_err.log
 python bench.py --config c5 --no-cpu-baseline > gpurun_out/${V}_bench_c5.json 2>>gpurun_out/bench_err.log
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${V}_bench_reference.json 2>>gpurun_out/bench_err.log
+ARBOR_NVCC_FLAGS="-DARBOR_EVICT_TRACE_BUILD" python -m paper_2605_22106_b200.build --force > /dev/null 2>&1
 python profiles/evict_trace.py c2 > gpurun_out/${V}_evict_trace_c2.json 2>&1
+python -m paper_2605_22106_b200.build --force > /dev/null 2>&1
 POST_TRACE=1 python profiles/decode_step_prof.py c3dpts 10 > gpurun_out/${V}_post_trace_c3dpts.json 2>&1
 POST_TRACE=1 python profiles/decode_step_prof.py c2 10 > gpurun_out/${V}_post_trace_c2.json 2>&1
 python profiles/attn_trace.py c3dpts > gpurun_out/${V}_attn_trace_c3dpts.json 2>&1
