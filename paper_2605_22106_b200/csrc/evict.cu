@@ -103,6 +103,13 @@ constexpr int kTraceSlots = 16;
 constexpr bool kTrace = true;
 #else
 constexpr bool kTrace = false;
+#endif
+// the isolation experiments (ARBOR_EVICT_EXP at run time: skip moves / the radix select) are
+// compiled only into -DARBOR_EVICT_EXP_BUILD builds, for the same reason
+#ifdef ARBOR_EVICT_EXP_BUILD
+constexpr bool kExp = true;
+#else
+constexpr bool kExp = false;
 #endif   // per warp: 8 events / counters + 8 select-phase cycle sums
 // select-phase cycle sums (debug builds with -DARBOR_EVICT_PHASES, trace slots 8-13): 5 the
 // cp.async wait for the item's data, 0 the next items' issues, 1 key build, 2 threshold,
@@ -378,7 +385,7 @@ select_move_ws_kernel(CompactArgs a) {
       const int cnt = mycount[sl];
       if (cnt < 0) break;
       k_jobs = k + 1;
-      const int nm = (a.exp & 1) ? 0 : cnt;
+      const int nm = (kExp && (a.exp & 1)) ? 0 : cnt;
       const int2 *jb = myjobs + sl * jcap;
       move_rows<kUw>(nm, [&](int i) { return jb[i].x; }, [&](int i) { return jb[i].y; }, kp8, vp8,
                 a.pos, rb, rpi, piece, sub);
@@ -598,7 +605,7 @@ select_move_ws_kernel(CompactArgs a) {
     unsigned long long tkey = kCand, tmask = kCand;     // m ≥ ncand: all candidates
     if (ranked && m <= 0) {
       tkey = ~0ull; tmask = ~0ull;                      // none survives
-    } else if (ranked && m < ncand && !(a.exp & 2)) {
+    } else if (ranked && m < ncand && !(kExp && (a.exp & 2))) {
       // candidates share every key bit above `top` (bits of A above the highest bit where
       // min and max differ); the radix passes start there
       bmin = __reduce_min_sync(0xffffffffu, bmin);
@@ -722,7 +729,7 @@ select_move_ws_kernel(CompactArgs a) {
     // holes and movers pair up exactly when the kept keys are unique (they are for a
     // consistent state: one pos tag per position); otherwise latch the error and move only the
     // pairs that exist, so a corrupted state can never produce out-of-range rows
-    if (nh != nm && lane == 0 && !a.exp) atomicOr(&a.ctrl->err, DERR_STATE);
+    if (nh != nm && lane == 0 && !(kExp && a.exp)) atomicOr(&a.ctrl->err, DERR_STATE);
     nm = nm < nh ? nm : nh;
     PH_MARK(3);
     // hand the job to the move warp
