@@ -81,9 +81,15 @@ struct TcArgs {
 };
 
 // debug timeline (ARBOR_TC_TRACE=1): trace[(cta·64 + tile)·16 + event] = clock64 − CTA start
+// compiled only into diagnostic builds (-DARBOR_TC_TRACE_BUILD)
+#ifdef ARBOR_TC_TRACE_BUILD
+constexpr bool kTcTrace = true;
+#else
+constexpr bool kTcTrace = false;
+#endif
 #define TC_TRACE(k, e)                                                                      \
   do {                                                                                      \
-    if (a.trace && (k) < 64)                                                                \
+    if (kTcTrace && a.trace && (k) < 64)                                                    \
       a.trace[(static_cast<int64_t>(blockIdx.x) * 64 + (k)) * 16 + (e)] = clock64() - t_start; \
   } while (0)
 
@@ -400,7 +406,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long t_start = clock64();
-  if (a.trace && threadIdx.x == 0) {
+  if (kTcTrace && a.trace && threadIdx.x == 0) {
     unsigned long long g0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
     a.trace[(static_cast<int64_t>(blockIdx.x) * 64 + 63) * 16 + 0] = static_cast<long long>(g0);
@@ -750,7 +756,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           }
           tc_commit(&s_full[b]);
           tc_commit(&empty_k[s]);            // K (and q) of this stage may be reloaded
-          if (a.trace) { mbar_wait(&s_full[b], (js / kGroups) & 1u); TC_TRACE(js, 12); }
+          if (kTcTrace && a.trace) { mbar_wait(&s_full[b], (js / kGroups) & 1u); TC_TRACE(js, 12); }
           ++js;
         }
         if (jo < js && mbar_test(&p_full[jo % kGroups], (jo / kGroups) & 1u) &&
@@ -768,7 +774,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
           }
           tc_commit(&o_full[b]);
           tc_commit(&empty_v[s]);
-          if (a.trace) { mbar_wait(&o_full[b], (jo / kGroups) & 1u); TC_TRACE(jo, 13); }
+          if (kTcTrace && a.trace) { mbar_wait(&o_full[b], (jo / kGroups) & 1u); TC_TRACE(jo, 13); }
           ++jo;
         }
       }
@@ -953,7 +959,7 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ 
   }
   tc_fence_before();
   __syncthreads();
-  if (a.trace && threadIdx.x == 0) {
+  if (kTcTrace && a.trace && threadIdx.x == 0) {
     unsigned long long g1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
     a.trace[(static_cast<int64_t>(blockIdx.x) * 64 + 63) * 16 + 1] = static_cast<long long>(g1);

@@ -143,9 +143,16 @@ struct FusedArgs {
 #endif
 constexpr int kFusedThreads = ARBOR_POST_THREADS;
 
+// the phase timeline (ARBOR_POST_TRACE=1 at run time) is compiled only into diagnostic builds
+// (-DARBOR_POST_TRACE_BUILD)
+#ifdef ARBOR_POST_TRACE_BUILD
+constexpr bool kPostTrace = true;
+#else
+constexpr bool kPostTrace = false;
+#endif
 #define POST_TRACE(f, e)                                                                    \
   do {                                                                                      \
-    if ((f).trace && threadIdx.x == 0) {                                                    \
+    if (kPostTrace && (f).trace && threadIdx.x == 0) {                                      \
       unsigned long long t_;                                                                \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
       (f).trace[(static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 16 + (e)] =   \

@@ -7,7 +7,10 @@ saw S, 9 P written, 10 epilogue saw O, 11 partials stored) and prints per-event 
 relative to the producer turn plus the CTA span.  Trace mode serialises the MMA issuer on
 its own commits, so absolute spans are upper bounds; it is a diagnostic, not a bench.
 
+    ARBOR_NVCC_FLAGS=-DARBOR_TC_TRACE_BUILD python -m paper_2605_22106_b200.build --force
     python profiles/attn_trace.py [c2|c3] > gpurun_out/attn_trace_c2.json
+
+(the trace is compiled only into that diagnostic build)
 """
 from __future__ import annotations
 

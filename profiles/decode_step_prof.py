@@ -2,6 +2,7 @@
 c3: 16 DPTS leaves on the same 8B-shaped tree), full retention, device-resident inputs.
 
     python profiles/decode_step_prof.py c3 [steps]        # prints per-call CUDA-event µs
+    POST_TRACE=1 … (decode_post phase timeline: a -DARBOR_POST_TRACE_BUILD build)
     ncu -k regex:"attn_tc|decode_post" ... python profiles/decode_step_prof.py c3 3
 """
 from __future__ import annotations

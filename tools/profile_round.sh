@@ -23,8 +23,11 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${V}_bench_re
 ARBOR_NVCC_FLAGS="-DARBOR_EVICT_TRACE_BUILD" python -m paper_2605_22106_b200.build --force > /dev/null 2>&1
 python profiles/evict_trace.py c2 > gpurun_out/${V}_evict_trace_c2.json 2>&1
 python -m paper_2605_22106_b200.build --force > /dev/null 2>&1
+# the timelines are compiled only into diagnostic builds
+ARBOR_NVCC_FLAGS="-DARBOR_TC_TRACE_BUILD -DARBOR_POST_TRACE_BUILD" python -m paper_2605_22106_b200.build --force > /dev/null 2>&1
 POST_TRACE=1 python profiles/decode_step_prof.py c3dpts 10 > gpurun_out/${V}_post_trace_c3dpts.json 2>&1
 POST_TRACE=1 python profiles/decode_step_prof.py c2 10 > gpurun_out/${V}_post_trace_c2.json 2>&1
 python profiles/attn_trace.py c3dpts > gpurun_out/${V}_attn_trace_c3dpts.json 2>&1
 python profiles/attn_trace.py c2 > gpurun_out/${V}_attn_trace_c2.json 2>&1
+python -m paper_2605_22106_b200.build --force > /dev/null 2>&1
 for f in gpurun_out/${V}_bench*.json; do python tools/summ.py $f; done
