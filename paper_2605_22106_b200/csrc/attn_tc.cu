@@ -1111,12 +1111,15 @@ bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_b
   // (K, V) ring depths; (4, 2) for NQ = 8 / 16 measured the same as (3, 3) on C2
   if (nq <= 8) launch_tc<8, 3, 3>(c, a);
   else if (nq <= 16) launch_tc<16, 3, 3>(c, a);
-#if defined(ARBOR_TC_NQ32_NSK3)
-  else if (nq <= 32) launch_tc<32, 3, 2>(c, a);
+  // NQ = 32 (the C3 frontier's 4-6-leaf tiles): three K stages, two V (round 2, late: C3
+  // DPTS decode attention 156.3 -> 154.5 us once the trace code left the production build;
+  // three V stages or 2 / 2 measured slower)
+#if defined(ARBOR_TC_NQ32_NSK2)
+  else if (nq <= 32) launch_tc<32, 2, 2>(c, a);
 #elif defined(ARBOR_TC_NQ32_NSV3)
   else if (nq <= 32) launch_tc<32, 2, 3>(c, a);
 #else
-  else if (nq <= 32) launch_tc<32, 2, 2>(c, a);
+  else if (nq <= 32) launch_tc<32, 3, 2>(c, a);
 #endif
   else if (nq <= 48) launch_tc<48, 2, 2>(c, a);
   else return false;
