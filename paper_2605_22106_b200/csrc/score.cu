@@ -483,9 +483,17 @@ decode_post_kernel(PostArgs pa) {
   const int li = row / f.H, h = row - li * f.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = kFusedThreads / 32, EPL = D / 32;
-  // first batch of score_row's metadata: overlaps the attention kernel's tail
+// Prefetching score_row's first chunk / mass metadata here, before griddepcontrol.wait, kept
+// ~11 registers live through phases (a) and (b) and spilled at the 128-register cap: without it
+// C3 DPTS decode_post 66.9 -> 63.6 us, C2 17.4 -> 16.7 us (round 2, late; -DARBOR_POST_PREFETCH=1
+// restores it)
+#ifndef ARBOR_POST_PREFETCH
+#define ARBOR_POST_PREFETCH 0
+#endif
+#if ARBOR_POST_PREFETCH
   const ChunkMeta pre_c = load_chunk_meta(f, warp + NW * lane, part, nparts);
   const MassMeta pre_m = load_mass_meta(f, warp + NW * lane);
+#endif
   // … and the first (leaf, q head) item's path bounds and this lane's first pair (plan arrays)
   int pre_p0 = 0, pre_p1 = 0, pre_pi = 0;
   {
@@ -607,7 +615,11 @@ decode_post_kernel(PostArgs pa) {
   __syncthreads();
   POST_TRACE(f, 3);
   if (pa.exp & 2) return;
+#if ARBOR_POST_PREFETCH
   score_row(f, li, h, part, nparts, [&](int b, int g) { return lse2s[b * G + g]; }, &pre_c, &pre_m);
+#else
+  score_row(f, li, h, part, nparts, [&](int b, int g) { return lse2s[b * G + g]; });
+#endif
 }
 
 }  // namespace
