@@ -211,8 +211,8 @@ struct WsLayout {
 // Warp-specialised select + move.  A CTA holds kPairsWs (select warp, move warp) pairs.
 //
 // Select warp p processes work items (item = (changed node, row)) drawn from a global counter.
-// Its global reads run three items ahead through a cp.async pipeline (no register cost, no
-// exposed latency): work entry of item k+3 → page list of item k+2 → pos tags and A span of
+// Its global reads run ahead through a cp.async pipeline (no register cost, no exposed
+// latency): work entry of item k+3 (global work list only) → page list of item k+2 → pos tags and A span of
 // item k+1 (A is read by position over the span, independent of the pos tags), while item k
 // is ranked from shared memory.  Keep = the block tail 𝒯 (positions ≥ n − |𝒯|)
 // ∪ the top-m non-tail candidates by the 49-bit key ⟨sink, A bits, pos⟩,
@@ -416,10 +416,10 @@ select_move_ws_kernel(CompactArgs a) {
   const int64_t pstride = static_cast<int64_t>(a.H) << lgP;
   constexpr unsigned long long kCand = 1ull << 63;
   // work items (changed node, row) are handed out dynamically — lane 0 draws the item of
-  // pipeline step k (three steps ahead of the one being ranked) from a global counter — so
+  // pipeline step k + draw (ahead of the one being ranked) from a global counter — so
   // every pair finishes within about one item of the others (a static round robin left a
   // ~40 µs spread of finishing times on C2, profiles/evict_trace.py)
-  // The draw for step k + 4 is issued at the top of step k and stored at its end (its latency
+  // The draw for step k + draw is issued at the top of step k and stored at its end (its latency
   // hides behind the ranking).
   int *iring = reinterpret_cast<int *>(sm + Ly.iring) + pid * 4;
   int *wring = iring + 4 * kPairsWs;     // work entry of each slot's item (item / R, once)
