@@ -227,15 +227,19 @@ struct WsLayout {
 //
 // Move warp p streams those rows (K, V: 16-byte coalesced, kUw rows in flight per lane group;
 // pos tags).  Sources and destinations are disjoint, so moves need no ordering.
+// CAPT > 0: a compile-time capacity (k_cur ≤ CAPT) and page size 2^LGPT — every shared-memory
+// offset of the layout is then a constant off one base address, which at the 64-register cap
+// saves the registers (and the rematerialisation) that runtime offsets cost; CAPT = 0: runtime
+template <int CAPT, int LGPT>
 __global__ void __launch_bounds__(kPairsWs * 64, 2)
 select_move_ws_kernel(CompactArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool mover = warp >= kPairsWs;
   const int pid = mover ? warp - kPairsWs : warp;
-  const WsLayout Ly(a.cap, a.lgP, a.wl_smem);
+  const WsLayout Ly(CAPT ? CAPT : a.cap, CAPT ? LGPT : a.lgP, a.wl_smem);
   const int cap = Ly.cap, capA = Ly.capA, capP = Ly.capP, pcap = Ly.pcap, jcap = Ly.jcap;
-  const int lgP = a.lgP, Pm = (1 << lgP) - 1;
+  const int lgP = CAPT ? LGPT : a.lgP, Pm = (1 << lgP) - 1;
   uint64_t *bars = reinterpret_cast<uint64_t *>(sm + Ly.bars);
   uint64_t *full = bars + pid * 2 * kJobSlots, *empty = full + kJobSlots;
   int2 *myjobs = reinterpret_cast<int2 *>(sm + Ly.jobs) + pid * kJobSlots * jcap;
@@ -864,26 +868,34 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n, bool 
     g_evict_trace = trace;
     g_evict_trace_n = trace_n;
   }
+  // the fixed-layout instantiation for the common shape: nodes of ≤ 128 slots, 16-slot pages
+#ifndef ARBOR_EVICT_FIXED
+#define ARBOR_EVICT_FIXED 1
+#endif
+  const bool fixed = ARBOR_EVICT_FIXED && a.cap <= 128 && a.lgP == 4;
+  if (fixed) a.cap = 128;
   const WsLayout ly(a.cap, a.lgP, a.wl_smem);
-  // occupancy / smem attribute cached per capacity (host-side cost stays off the launch path)
-  static size_t attr_smem = 0;
-  static size_t cached_total = 0;
-  static int cached_grid = 0;
-  if (ly.total > attr_smem) {
+  const int inst = fixed ? 1 : 0;
+  auto kfn = fixed ? select_move_ws_kernel<128, 4> : select_move_ws_kernel<0, 0>;
+  // occupancy / smem attribute cached per instantiation and layout (host-side cost stays off
+  // the launch path)
+  static size_t attr_smem[2] = {0, 0};
+  static size_t cached_total[2] = {0, 0};
+  static int cached_grid[2] = {0, 0};
+  if (ly.total > attr_smem[inst]) {
     const size_t want = ly.total < 48 * 1024 ? 48 * 1024 : ly.total;
-    cudaFuncSetAttribute(select_move_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(want));
-    attr_smem = want;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(want));
+    attr_smem[inst] = want;
   }
-  if (ly.total != cached_total) {
+  if (ly.total != cached_total[inst]) {
     int sms = 148, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, select_move_ws_kernel, kPairsWs * 64, ly.total);
-    cached_grid = sms * std::min(std::max(per, 1), kEvictCtasPerSm);
-    cached_total = ly.total;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, kPairsWs * 64, ly.total);
+    cached_grid[inst] = sms * std::min(std::max(per, 1), kEvictCtasPerSm);
+    cached_total[inst] = ly.total;
   }
   stage_begin(c, ARBOR_ST_SELECT_COMPACT, c->ms);
-  launch_pdl(select_move_ws_kernel, dim3(cached_grid), dim3(kPairsWs * 64), ly.total, c->ms, a);
+  launch_pdl(kfn, dim3(cached_grid[inst]), dim3(kPairsWs * 64), ly.total, c->ms, a);
   ARBOR_LAUNCHED(c);
   stage_end(c, ARBOR_ST_SELECT_COMPACT, c->ms);
 }
