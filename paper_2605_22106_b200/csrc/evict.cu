@@ -230,9 +230,10 @@ struct WsLayout {
 // CAPT > 0: a compile-time capacity (k_cur ≤ CAPT) and page size 2^LGPT — every shared-memory
 // offset of the layout is then a constant off one base address, which at the 64-register cap
 // saves the registers (and the rematerialisation) that runtime offsets cost; CAPT = 0: runtime
-template <int CAPT, int LGPT>
+template <int CAPT, int LGPT, int HT>
 __global__ void __launch_bounds__(kPairsWs * 64, 2)
 select_move_ws_kernel(CompactArgs a) {
+  const int H = HT ? HT : a.H;           // KV heads of a row index (a constant divisor when HT > 0)
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool mover = warp >= kPairsWs;
@@ -417,7 +418,7 @@ select_move_ws_kernel(CompactArgs a) {
   WorkEnt *Mbuf = reinterpret_cast<WorkEnt *>(sm + Ly.mbuf) + pid * 4;
   uint32_t *hist = hist_all[pid];
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int64_t pstride = static_cast<int64_t>(a.H) << lgP;
+  const int64_t pstride = static_cast<int64_t>(H) << lgP;
   constexpr unsigned long long kCand = 1ull << 63;
   // work items (changed node, row) are handed out dynamically — lane 0 draws the item of
   // pipeline step k + draw (ahead of the one being ranked) from a global counter — so
@@ -435,8 +436,8 @@ select_move_ws_kernel(CompactArgs a) {
   };
   auto row_base = [&](int it, int w) -> int64_t {
     const int r = it - w * a.R;
-    const int l = r / a.H, h = r - l * a.H;
-    return (static_cast<int64_t>(l) * a.NP * a.H + h) << lgP;
+    const int l = r / H, h = r - l * H;
+    return (static_cast<int64_t>(l) * a.NP * H + h) << lgP;
   };
   // pipeline stages (each lane issues its share; completion via cp.async.wait_all + __syncwarp)
   auto issue_meta = [&](int k) {
@@ -868,15 +869,16 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n, bool 
     g_evict_trace = trace;
     g_evict_trace_n = trace_n;
   }
-  // the fixed-layout instantiation for the common shape: nodes of ≤ 128 slots, 16-slot pages
+  // the fixed-layout instantiation for the common shape: nodes of ≤ 128 slots, 16-slot pages,
+  // 8 KV heads (the Llama-3.1-8B / Qwen2.5-32B shapes of C2-C5)
 #ifndef ARBOR_EVICT_FIXED
 #define ARBOR_EVICT_FIXED 1
 #endif
-  const bool fixed = ARBOR_EVICT_FIXED && a.cap <= 128 && a.lgP == 4;
+  const bool fixed = ARBOR_EVICT_FIXED && a.cap <= 128 && a.lgP == 4 && a.H == 8;
   if (fixed) a.cap = 128;
   const WsLayout ly(a.cap, a.lgP, a.wl_smem);
   const int inst = fixed ? 1 : 0;
-  auto kfn = fixed ? select_move_ws_kernel<128, 4> : select_move_ws_kernel<0, 0>;
+  auto kfn = fixed ? select_move_ws_kernel<128, 4, 8> : select_move_ws_kernel<0, 0, 0>;
   // occupancy / smem attribute cached per instantiation and layout (host-side cost stays off
   // the launch path)
   static size_t attr_smem[2] = {0, 0};
