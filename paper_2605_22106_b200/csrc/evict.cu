@@ -719,7 +719,10 @@ select_move_ws_kernel(CompactArgs a) {
       if (s < kc) {
         const unsigned long long kk = key[s];
         const int p = static_cast<int>(kk & 0xffffu);
-        keep = (p >= tail_from) || (ranked && (kk & kCand) && (kk & tmask) >= tkey);
+        // branch-free (the short-circuit form compiled to a divergent branch per slot)
+        keep = static_cast<int>(p >= tail_from) |
+               (static_cast<int>(ranked) & static_cast<int>(kk >> 63) &
+                static_cast<int>((kk & tmask) >= tkey));
       }
       const int hole = s >= w0 && s < kc && !keep;
       const int mv = s < w0 && keep;
