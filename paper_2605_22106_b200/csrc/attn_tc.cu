@@ -1109,7 +1109,14 @@ bool launch_attn_tc(arbor_ctx *c, const PlanView &pv, const void *q, int layer_b
     g_tc_trace = trace;
   }
   // (K, V) ring depths; (4, 2) for NQ = 8 / 16 measured the same as (3, 3) on C2
+  // NQ = 8 (single-leaf tiles: C2, C4, C5): two K / V stages — fewer bytes requested per SM at
+  // the kernel start, the first tile lands sooner (round 2, late: attention +3.5-4.5% GB/s on
+  // C2 / C4 / C5; -DARBOR_TC_NQ8_STAGES3 restores three)
+#if defined(ARBOR_TC_NQ8_STAGES3)
   if (nq <= 8) launch_tc<8, 3, 3>(c, a);
+#else
+  if (nq <= 8) launch_tc<8, 2, 2>(c, a);
+#endif
   else if (nq <= 16) launch_tc<16, 3, 3>(c, a);
   // NQ = 32 (the C3 frontier's 4-6-leaf tiles): three K stages, two V (round 2, late: C3
   // DPTS decode attention 156.3 -> 154.5 us once the trace code left the production build;
