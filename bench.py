@@ -989,7 +989,9 @@ def run_c3(args, dev, rank, ws, hc, nid, pg):
             "e2e": {"value": sum(r["cached"] for r in rec_e2e) / wall_tot, "unit": "tokens/s",
                     "h2d_bytes_per_step": int(nodes_n * 25 + 64), "d2h_bytes_per_step": 16,
                     "note": "host wall clock of the transition calls incl. tree upload and sync "
-                            "(the transitions without host run-ahead)"},
+                            "(the transitions without host run-ahead)",
+                    "wall_us_p50": statistics.median(r["wall"] * 1e6 for r in rec_e2e),
+                    "device_us_p50": statistics.median(r["trans"] * 1e3 for r in rec_e2e)},
             "timing_note": "value and the per-transition device times come from the transitions "
                            "queued behind a ~300 us device sleep (host run-ahead, as in the C2 "
                            "loop); e2e from the others (ARBOR_BENCH_RUN_AHEAD=0: no sleep)",

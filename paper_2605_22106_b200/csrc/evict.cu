@@ -882,6 +882,16 @@ void launch_evict(arbor_ctx *c, int N, const int32_t *k_target, int max_n, bool 
   const WsLayout ly(a.cap, a.lgP, a.wl_smem);
   const int inst = fixed ? 1 : 0;
   auto kfn = fixed ? select_move_ws_kernel<128, 4, 8> : select_move_ws_kernel<0, 0, 0>;
+  // both instantiations are loaded on the first call (lazy loading would otherwise load the
+  // runtime-layout one the first time a node above 128 slots is evicted: a millisecond-scale
+  // stall in the middle of a run, e.g. C3's e2e)
+  static const bool loaded = [] {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, select_move_ws_kernel<128, 4, 8>);
+    cudaFuncGetAttributes(&fa, select_move_ws_kernel<0, 0, 0>);
+    return true;
+  }();
+  (void)loaded;
   // occupancy / smem attribute cached per instantiation and layout (host-side cost stays off
   // the launch path)
   static size_t attr_smem[2] = {0, 0};
