@@ -41,7 +41,10 @@ def test_random_evict_rehydrate_rounds(trial):
         tree_spec = ("full", int(rng.integers(2, 4)), int(rng.integers(2, 4)), int(rng.choice([40, 64, 96])))
     else:
         tree_spec = ("search", int(rng.integers(10, 30)), 3, 4, int(rng.choice([32, 72])))
-    preset = dict(tree=tree_spec, L=2, H=2, Hq=8, d=128, dtype="bf16", P=16, rho=0.3,
+    # half the trials in the 8-KV-head shape (nodes ≤ 128 slots, 16-slot pages): the fixed-layout
+    # select_compact instantiation; the others take the runtime-layout kernel
+    L, H, Hq = (1, 8, 32) if trial % 4 >= 2 else (2, 2, 8)
+    preset = dict(tree=tree_spec, L=L, H=H, Hq=Hq, d=128, dtype="bf16", P=16, rho=0.3,
                   params=dict(l_tail=int(rng.choice([0, 2, 8])), k_min=int(rng.choice([0, 2]))),
                   active="highest_v")
     pr = Pair(preset, seed=trial)
