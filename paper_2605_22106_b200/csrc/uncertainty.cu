@@ -7,7 +7,7 @@
 //
 // With a reference m: S = Σ e^{z−m}, T = Σ e^{z−m}(z − m), and H = log S − T/S.  Changing the
 // reference to m' ≥ m rescales S' = e^{m−m'} S and T' = e^{m−m'} (T + (m − m') S), so each
-// thread streams its slice once (8 logits per load batch, (m, S, T) in fp32), the CTA
+// thread streams its slice once (16-byte vector loads, four in flight, (m, S, T) in fp32), the CTA
 // combines its threads' triples by shuffles, and the last CTA of a row (ticket) combines the
 // CTAs' triples in fp64 and writes u.
 // HBM-bound: one read of the logits (4 or 2 B per vocabulary entry).
@@ -20,8 +20,12 @@ namespace arbor {
 namespace {
 
 constexpr int kUncThreads = 256;
-constexpr int kUncPer = 8;           // logits per thread: loaded together, then absorbed
-constexpr int kUncMaxSplit = 256;    // CTAs per row: ⌈vocab / (256·8)⌉, at most this
+constexpr int kUncVecs = 4;          // 16-byte vectors per thread in flight per step
+constexpr int kUncMaxSplit = 256;    // CTAs per row (at most)
+#ifndef ARBOR_UNC_PER_CTA
+#define ARBOR_UNC_PER_CTA 16384
+#endif
+constexpr int kUncPerCta = ARBOR_UNC_PER_CTA;   // logits per CTA (about)
 
 struct Triple {
   double m, S, T;
@@ -58,38 +62,87 @@ __device__ __forceinline__ TripleF merge_f(TripleF a, TripleF b) {
   return TripleF{m, ra * a.S + rb * b.S, ra * (a.T + (a.m - m) * a.S) + rb * (b.T + (b.m - m) * b.S)};
 }
 
+// 16-byte vector of logits and its element count
+template <typename T> struct UncVec;
+template <> struct UncVec<float> {
+  static constexpr int N = 4;
+  __device__ __forceinline__ static void load(const float *p, float (&v)[4]) {
+    const float4 q = __ldg(reinterpret_cast<const float4 *>(p));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  }
+};
+template <> struct UncVec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ __forceinline__ static void load(const __nv_bfloat16 *p, float (&v)[8]) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4 *>(p));
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {   // bf16 → f32 is a 16-bit shift: exact
+      v[2 * k] = __uint_as_float(w[k] << 16);
+      v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+  }
+};
+
+// absorb n logits (−inf: masked, p = 0) into the running triple, one rescale per call
+template <int NV>
+__device__ __forceinline__ void absorb(TripleF &acc, const float (&v)[NV]) {
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) mx = fmaxf(mx, v[j]);
+  if (mx == -INFINITY) return;
+  TripleF t{mx, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const float d = v[j] - mx, e = v[j] == -INFINITY ? 0.f : expf(d);
+    t.S += e;
+    t.T = fmaf(e, v[j] == -INFINITY ? 0.f : d, t.T);
+  }
+  acc = merge_f(acc, t);
+}
+
+// Row `row`, split `split` of `nsplit`: the row's 16-byte-aligned body is cut into nsplit
+// ranges of whole vectors (kUncVecs vectors per thread in flight per step); the unaligned head
+// (< one vector) goes to split 0 and the tail to the last split, element by element.
 template <typename T>
 __global__ void __launch_bounds__(kUncThreads)
 uncertainty_kernel(const T *__restrict__ logits, int vocab, Triple *__restrict__ part,
                    unsigned *__restrict__ ticket, float *__restrict__ u_out) {
   pdl_wait();
   pdl_trigger();
+  constexpr int NV = UncVec<T>::N;
   const int row = blockIdx.y, split = blockIdx.x, nsplit = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const T *z = logits + static_cast<int64_t>(row) * vocab;
-  const int per = (vocab + nsplit - 1) / nsplit;
-  const int lo = split * per, hi = min(vocab, lo + per);
+  const int head = min(vocab, static_cast<int>(((16 - (reinterpret_cast<uintptr_t>(z) & 15)) & 15) / sizeof(T)));
+  const int nvec = (vocab - head) / NV;                  // whole vectors of the body
+  const int tail0 = head + nvec * NV;                    // first element of the tail
+  const int vper = (nvec + nsplit - 1) / nsplit;
+  const int v_lo = min(nvec, split * vper), v_hi = min(nvec, v_lo + vper);
+  const T *body = z + head;
   TripleF acc{-INFINITY, 0.f, 0.f};
-  for (int i0 = lo + threadIdx.x; i0 < hi; i0 += kUncThreads * kUncPer) {
-    float v[kUncPer];
-    float m8 = -INFINITY;
+  for (int v0 = v_lo + threadIdx.x; v0 < v_hi; v0 += kUncThreads * kUncVecs) {
+    float v[kUncVecs][NV];
 #pragma unroll
-    for (int j = 0; j < kUncPer; ++j) {       // all loads in flight before any use
-      const int i = i0 + j * kUncThreads;
-      v[j] = i < hi ? to_f(__ldg(z + i)) : -INFINITY;
+    for (int k = 0; k < kUncVecs; ++k) {      // every load in flight before any use
+      const int vi = v0 + k * kUncThreads;
+      if (vi < v_hi) {
+        UncVec<T>::load(body + static_cast<int64_t>(vi) * NV, v[k]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) v[k][j] = -INFINITY;
+      }
     }
 #pragma unroll
-    for (int j = 0; j < kUncPer; ++j) m8 = fmaxf(m8, v[j]);
-    if (m8 == -INFINITY) continue;            // all masked
-    TripleF t{m8, 0.f, 0.f};
-#pragma unroll
-    for (int j = 0; j < kUncPer; ++j) {
-      if (v[j] == -INFINITY) continue;        // a masked logit: p = 0
-      const float d = v[j] - m8, e = expf(d);
-      t.S += e;
-      t.T = fmaf(e, d, t.T);
-    }
-    acc = merge_f(acc, t);
+    for (int k = 0; k < kUncVecs; ++k) absorb<NV>(acc, v[k]);
+  }
+  // the unaligned head (split 0) and tail (last split): one element per thread
+  {
+    const bool first = split == 0, lastsplit = split == nsplit - 1;
+    float e1[1] = {-INFINITY};
+    if (first && static_cast<int>(threadIdx.x) < head) e1[0] = to_f(z[threadIdx.x]);
+    else if (lastsplit && static_cast<int>(threadIdx.x) < vocab - tail0) e1[0] = to_f(z[tail0 + threadIdx.x]);
+    absorb<1>(acc, e1);
   }
   // warp, then CTA combine (fixed shuffle / slot order: deterministic)
 #pragma unroll
@@ -143,8 +196,11 @@ uncertainty_kernel(const T *__restrict__ logits, int vocab, Triple *__restrict__
 
 arbor_status launch_uncertainty(arbor_ctx *c, const void *logits, int dtype, int batch, int vocab,
                                 float *u_out) {
-  const int nsplit = std::min(kUncMaxSplit, std::max(1, (vocab + kUncThreads * kUncPer - 1) /
-                                                            (kUncThreads * kUncPer)));
+  // logits per CTA: about half a wave of CTAs in total, within [4096, kUncPerCta] (measured:
+  // 4096 best for one row, 16384 for 64 rows of a 128k vocabulary)
+  const int64_t want = static_cast<int64_t>(vocab) * batch / 512;
+  const int per = static_cast<int>(std::min<int64_t>(kUncPerCta, std::max<int64_t>(4096, want)));
+  const int nsplit = std::min(kUncMaxSplit, std::max(1, (vocab + per - 1) / per));
   const size_t need = static_cast<size_t>(batch) * kUncMaxSplit;
   if (need > c->unc_cap) {
     if (c->unc_part) cudaFree(c->unc_part);
