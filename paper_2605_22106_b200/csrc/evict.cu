@@ -22,6 +22,7 @@
 //    than a [0, k_app) prefix on C2).  Sources and destinations are disjoint.
 //  * move (persistent grid): a pure 16-byte-coalesced streaming copy of the listed K, V
 //    rows and pos tags — no ordering constraints, full occupancy.
+#include <type_traits>
 #include <cub/block/block_scan.cuh>
 
 #include "tile.cuh"
@@ -418,7 +419,16 @@ select_move_ws_kernel(CompactArgs a) {
   WorkEnt *Mbuf = reinterpret_cast<WorkEnt *>(sm + Ly.mbuf) + pid * 4;
   uint32_t *hist = hist_all[pid];
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int64_t pstride = static_cast<int64_t>(H) << lgP;
+  // pool row ids fit int32 (arbor_init checks L·NP·H·P < 2^31): 32-bit row math in the select
+  // warp (one register and one add per use fewer than 64-bit offsets at the 64-register cap)
+#ifndef ARBOR_EVICT_HOIST
+#define ARBOR_EVICT_HOIST 1
+#endif
+#ifndef ARBOR_EVICT_ROW32
+#define ARBOR_EVICT_ROW32 1
+#endif
+  using RowT = std::conditional_t<ARBOR_EVICT_ROW32 != 0, int, int64_t>;
+  const RowT pstride = static_cast<RowT>(H) << lgP;
   constexpr unsigned long long kCand = 1ull << 63;
   // work items (changed node, row) are handed out dynamically — lane 0 draws the item of
   // pipeline step k + draw (ahead of the one being ranked) from a global counter — so
@@ -434,10 +444,10 @@ select_move_ws_kernel(CompactArgs a) {
   auto meta = [&](int k) -> const WorkEnt & {
     return Ly.wl_n ? swl[wring[k & 3]] : Mbuf[k & 3];
   };
-  auto row_base = [&](int it, int w) -> int64_t {
+  auto row_base = [&](int it, int w) -> RowT {
     const int r = it - w * a.R;
     const int l = r / H, h = r - l * H;
-    return (static_cast<int64_t>(l) * a.NP * H + h) << lgP;
+    return (static_cast<RowT>(l) * a.NP * H + h) << lgP;
   };
   // pipeline stages (each lane issues its share; completion via cp.async.wait_all + __syncwarp)
   auto issue_meta = [&](int k) {
@@ -467,12 +477,12 @@ select_move_ws_kernel(CompactArgs a) {
     const WorkEnt &e = meta(k);
     if (e.kc == e.n && e.so == 0) return;
     const int32_t *g = Gbuf + (k % 3) * pcap;
-    const int64_t base = row_base(it, wring[k & 3]);
+    const RowT base = row_base(it, wring[k & 3]);
     int16_t *pb = Pbuf + (k & 1) * capP;
     const int sb = e.so & Pm;
     // Gbuf-relative slot pairs (c even; P even: same page) covering [sb, sb + k_cur)
     for (int c = (sb & ~1) + 2 * lane; c < sb + e.kc; c += 64)
-      cp_async4(pb + c, a.pos + base + static_cast<int64_t>(g[c >> lgP]) * pstride + (c & Pm));
+      cp_async4(pb + c, a.pos + (base + static_cast<RowT>(g[c >> lgP]) * pstride + (c & Pm)));
   };
   // the A row of pipeline step k's item over its span (A is read by position)
   auto a_row = [&](int k) -> const float * {
@@ -562,10 +572,10 @@ select_move_ws_kernel(CompactArgs a) {
     const int16_t *pb = Pbuf + (k & 1) * capP;
     const float *ab = Abuf + (k & 1) * capA +
                       ((reinterpret_cast<uintptr_t>(a_row(k)) & 15) >> 2);
-    const int64_t base = row_base(it, wring[k & 3]);
-    auto row = [&](int slot) -> int64_t {
+    const RowT base = row_base(it, wring[k & 3]);
+    auto row = [&](int slot) -> RowT {
       const int c = sb + slot;
-      return base + static_cast<int64_t>(pgs[c >> lgP]) * pstride + (c & Pm);
+      return base + static_cast<RowT>(pgs[c >> lgP]) * pstride + (c & Pm);
     };
     const bool ranked = ka > tl;
     const int m = ka - tl;
@@ -573,6 +583,12 @@ select_move_ws_kernel(CompactArgs a) {
     int ncand = 0;
     uint32_t bmin = 0xffffffffu, bmax = 0u;
     unsigned sink_all = 1u, sink_any = 0u;
+#if ARBOR_EVICT_HOIST
+    // positions below nsk are global sinks (0 unless this is the root under HEAVY / SINKS_TAIL);
+    // an invalid A (NaN, negative, inf) is latched once per item, not branched on per slot
+    const int nsk = (e.node == 0 && a.select_mode != ARBOR_SELECT_TAIL) ? a.n_sinks : 0;
+    unsigned bad = 0u;
+#endif
 #pragma unroll kSelUnroll
     for (int s0 = 0; s0 < kc; s0 += 32) {
       const int s = s0 + lane;
@@ -585,12 +601,20 @@ select_move_ws_kernel(CompactArgs a) {
           // root's first n_sinks positions — rank above everything else
           // in HEAVY and SINKS_TAIL (bit 48), then the f32 bits of A (HEAVY; 0 for the
           // recency rules TAIL, SINKS_TAIL), then the position
+#if ARBOR_EVICT_HOIST
+          const unsigned sink = p < nsk ? 1u : 0u;
+#else
           const unsigned sink =
               (e.node == 0 && p < a.n_sinks && a.select_mode != ARBOR_SELECT_TAIL) ? 1u : 0u;
+#endif
           unsigned bits = 0u;
           if (a.select_mode == ARBOR_SELECT_HEAVY) {
             const float av = ab[p];
+#if ARBOR_EVICT_HOIST
+            bad |= static_cast<unsigned>(!(av >= 0.f) || isinf(av));
+#else
             if (!(av >= 0.f) || isinf(av)) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+#endif
             bits = (av == 0.f) ? 0u : __float_as_uint(av);   // −0 → +0 (Q3)
           }
           kk = kCand | (static_cast<unsigned long long>(sink) << 48) |
@@ -604,6 +628,9 @@ select_move_ws_kernel(CompactArgs a) {
       }
       ncand += __popc(__ballot_sync(0xffffffffu, (kk & kCand) != 0));
     }
+#if ARBOR_EVICT_HOIST
+    if (bad) atomicOr(&a.ctrl->err, DERR_INVARIANT);
+#endif
     __syncwarp();
     PH_MARK(1);
     // threshold: keep a candidate iff (key & tmask) >= tkey (the top m unique keys)
